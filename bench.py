@@ -1,0 +1,376 @@
+#!/usr/bin/env python
+"""Shared-LHS batch solve throughput on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--mode exact|fast]
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N     (N > 1)
+    python bench.py --impl reference                                            (CPU reference arm)
+
+A step is one in-place solve of one synthetic batch. Default workload is
+BASELINE.json configs[1]: pentadiagonal shared-LHS, fp64, N = 512 rows,
+65536 systems per GPU, hyperdiffusion LHS sigma_x = 1 (pde.cpp:67-71).
+Multi-GPU: every rank solves its own contiguous shard of the global batch
+(j0 = g*M), no data-path collective ("weak" scaling); NCCL carries only the
+barrier and the max-over-ranks of the device time.
+
+Prints one JSON line on rank 0. Fields: value (device-resident, CUDA-event
+timed), e2e (through the reference-facing C ABI with a pinned host batch,
+H2D + sweep + D2H inside the timed region), roofline of the sweep kernel
+against MEASURED_PEAKS.json, cpu_baseline (the reference CPU solver on this
+host), clocks sampled during the timed regions.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "batch·N rows solved/s (fp64) and % of HBM roofline at 1/2/4/8 B200 vs CPU ref"
+
+CONFIGS = {
+    # name: (kind, n, systems per GPU, description)
+    "c1": ("tri", 256, 4096, "configs[0]: tridiagonal shared-LHS, N=256, batch=4096, diffusion LHS sigma_x=1"),
+    "c2": ("pent", 512, 65536, "configs[1]: pentadiagonal shared-LHS, N=512, batch=65536, hyperdiffusion LHS sigma_x=1"),
+    "tri512": ("tri", 512, 1 << 20, "north-star target: tridiagonal N=512, batch=2^20, diffusion LHS sigma_x=1"),
+    "pent512": ("pent", 512, 1 << 20, "north-star target: pentadiagonal N=512, batch=2^20, hyperdiffusion sigma_x=1"),
+    "c5": ("pent", 1024, 1 << 21, "configs[4] shard: pentadiagonal N=1024, 2^21 systems per GPU (2^24 at 8 GPUs)"),
+}
+SEED = 42
+
+NVML_REASONS = {
+    0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+    0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+    0x100: "display_clock_setting",
+}
+
+
+def lhs_for(kind: str, n: int):
+    from paper_1909_04539_b200 import bandsolve as bs
+    return bs.diffusion_bands(1.0, n) if kind == "tri" else bs.hyper_bands(1.0, n)
+
+
+# ---- clocks -------------------------------------------------------------------------
+class ClockSampler:
+    """Samples SM clock and throttle reasons via NVML while marked windows are open."""
+
+    def __init__(self, device_index: int, period_s: float = 0.02):
+        self.samples: list[tuple[float, int, int]] = []
+        self.windows: list[tuple[float, float]] = []
+        self.ok = False
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            return
+        self.period = period_s
+        self.stop_evt = threading.Event()
+        self.th = threading.Thread(target=self._run, daemon=True)
+        self.th.start()
+
+    def _run(self):
+        while not self.stop_evt.is_set():
+            try:
+                clk = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
+                rs = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((time.perf_counter(), clk, rs))
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def window(self):
+        sampler = self
+
+        class _W:
+            def __enter__(self):
+                self.t0 = time.perf_counter()
+
+            def __exit__(self, *a):
+                sampler.windows.append((self.t0, time.perf_counter()))
+        return _W()
+
+    def summary(self) -> dict:
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        self.stop_evt.set()
+        self.th.join(timeout=1)
+        inside = [s for s in self.samples if any(a <= s[0] <= b for a, b in self.windows)]
+        use = inside or self.samples
+        reasons = set()
+        for _, _, rs in use:
+            for bit, name in NVML_REASONS.items():
+                if rs & bit and name != "gpu_idle":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(c for _, c, _ in use) if use else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(reasons),
+                "samples": len(use), "samples_in_timed_regions": len(inside)}
+
+
+# ---- CPU reference ------------------------------------------------------------------------
+def reference_library():
+    """(Library, kind): the reference compiled from its own sources
+    (oracle/_ref, built here and shipped with the repo snapshot), else None."""
+    from oracle.oracle import REF_LIB, build_ref
+    from paper_1909_04539_b200.bandsolve import Library
+    path = REF_LIB if os.path.exists(REF_LIB) else build_ref()
+    if path and os.path.exists(path):
+        return Library(path), "reference"
+    return None, "port"
+
+
+def cpu_solve_fn(kind: str, n: int, m: int):
+    """Return (solve() -> seconds, cores, kind, sample) for the CPU reference
+    on an n x m batch. The factor is created outside the timing, as in the
+    paper."""
+    from oracle.oracle import Oracle
+    orc = Oracle()
+    rhs = orc.rhs(SEED, n, m)
+    bands = lhs_for(kind, n)
+    lib, lkind = reference_library()
+    if lib is not None:
+        from paper_1909_04539_b200.bandsolve import Batch, PentFactor, TriFactor
+        cores = os.cpu_count() or 1
+        lib.set_threads(cores)
+        fac = TriFactor(lib, *bands) if kind == "tri" else PentFactor(lib, *bands)
+        batch = Batch.from_array(lib, rhs)
+
+        def solve():
+            batch.array[...] = rhs  # restore b (outside the timed call)
+            t0 = time.perf_counter()
+            fac.solve(batch)
+            return time.perf_counter() - t0
+        return solve, cores, lkind
+    f = orc.tri_prefactor(*bands) if kind == "tri" else orc.pent_prefactor(*bands)
+
+    def solve_port():
+        x = rhs.copy()
+        t0 = time.perf_counter()
+        (orc.tri_solve if kind == "tri" else orc.pent_solve)(f, x)
+        return time.perf_counter() - t0
+    return solve_port, 1, "port"
+
+
+def cpu_sample_columns(n: int, m: int, budget_rows: int = 1 << 26) -> int:
+    """Bounded CPU sample: whole batch when small, else a column subsample."""
+    return max(1, min(m, budget_rows // n))
+
+
+def cpu_baseline(kind: str, n: int, m: int, seconds: float = 4.0) -> dict:
+    ms = cpu_sample_columns(n, m)
+    solve, cores, lkind = cpu_solve_fn(kind, n, ms)
+    solve()  # warm-up (first-touch, thread team)
+    times = []
+    t_end = time.perf_counter() + seconds
+    while len(times) < 3 or (time.perf_counter() < t_end and len(times) < 200):
+        times.append(solve())
+    t = statistics.median(times)
+    return {"value": n * ms / t, "unit": "rows/s", "cores": cores, "kind": lkind,
+            "sample": f"{kind} N={n} x {ms} systems ({'full batch' if ms == m else 'column subsample'}), "
+                      f"median of {len(times)} solves, bandsolve_{kind}_solve_shared, "
+                      f"{cores} threads, {os.cpu_count()} host cores"}
+
+
+def run_reference_arm(args, rank: int) -> None:
+    if rank != 0:
+        return
+    kind, n, m, desc = CONFIGS[args.config]
+    ms = cpu_sample_columns(n, m)
+    solve, cores, lkind = cpu_solve_fn(kind, n, ms)
+    for _ in range(args.warmup):
+        solve()
+    times = [solve() for _ in range(args.steps)]
+    total = sum(times)
+    value = n * ms * len(times) / total
+    sample = (f"{kind} N={n} x {ms} systems ({'full batch' if ms == m else 'column subsample'}) per step, "
+              f"{cores} threads on {os.cpu_count()} host cores")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": desc, "kind": kind, "n": n, "batch": ms},
+            "cpu_baseline": {"value": value, "unit": "rows/s", "cores": cores, "kind": lkind, "sample": sample},
+            "e2e": {"value": value, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---- GPU arm --------------------------------------------------------------------------------
+def load_peak() -> tuple[float, str]:
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_traffic(config: str, mode: str) -> float | None:
+    """Per-launch DRAM bytes of the sweep kernel from the committed ncu capture."""
+    path = os.path.join(REPO, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)[f"{config}/{mode}"]["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
+def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
+    import torch
+    import torch.distributed as dist
+
+    from paper_1909_04539_b200 import bandsolve as bs
+
+    torch.cuda.set_device(local_rank)
+    lib = bs.load()
+    lib.set_mode(bs.MODE_FAST if args.mode == "fast" else bs.MODE_EXACT)
+    kind, n, m, desc = CONFIGS[args.config]
+    elem = 4 if args.f32 else 8
+    dt = torch.float32 if args.f32 else torch.float64
+    bands = lhs_for(kind, n)
+    fac = bs.TriFactor(lib, *bands) if kind == "tri" else bs.PentFactor(lib, *bands)
+    j_off = rank * m  # this rank's shard of the global batch
+
+    # Rotating in-place buffers so every timed step streams from HBM: the
+    # working set is >= 4x the 126 MB L2.
+    bytes_per = n * m * elem
+    nbuf = max(2, min(8, -(-4 * 132644864 // bytes_per)))
+    bufs = [torch.empty((n, m), dtype=dt, device="cuda") for _ in range(nbuf)]
+    for b in bufs:
+        lib.fill_rhs_dev(b.data_ptr(), n, m, m, SEED, j_off, torch.cuda.current_stream().cuda_stream, f32=args.f32)
+    stream = torch.cuda.current_stream()
+    sptr = stream.cuda_stream
+    clocks = ClockSampler(local_rank)
+
+    def step(k):
+        fac.solve_dev(bufs[k % nbuf].data_ptr(), n, m, ld=m, stream=sptr, f32=args.f32)
+
+    for k in range(args.warmup):
+        step(k)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = lib.kernel_launches()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with clocks.window():
+        e0.record(stream)
+        for k in range(args.steps):
+            step(k)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    launches = lib.kernel_launches() - launches0
+    if world > 1:
+        dist.barrier()
+    ms_local = e0.elapsed_time(e1)
+    t = torch.tensor([ms_local], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    rows_total = float(n) * m * world * args.steps
+    value = rows_total / (ms_max / 1e3)
+    ms_per_step = ms_max / args.steps
+
+    # roofline of the sweep kernel: algorithmic bytes (read b once, write x
+    # once) per launch / average launch duration on the launching stream
+    algo_bytes = 2.0 * elem * n * m
+    achieved = algo_bytes / (ms_local / args.steps / 1e3) / 1e9
+    peak, peak_src = load_peak()
+    traffic = load_traffic(args.config, args.mode)
+
+    # e2e through the reference-facing host API (pinned host batch; H2D,
+    # sweep, D2H inside bandsolve_*_solve_shared, synchronous)
+    e2e = None
+    if not args.f32:
+        host = bs.Batch.from_array(lib, bufs[0].cpu().numpy())
+        e2e_steps = max(1, min(args.steps, 50))
+        for _ in range(min(args.warmup, 3)):
+            fac.solve(host)
+        if world > 1:
+            dist.barrier()
+        with clocks.window():
+            t0 = time.perf_counter()
+            for _ in range(e2e_steps):
+                fac.solve(host)
+            t_e2e = time.perf_counter() - t0
+        te = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": float(n) * m * world * e2e_steps / float(te.item()), "unit": "rows/s",
+               "h2d_bytes_per_step": n * m * elem, "d2h_bytes_per_step": n * m * elem,
+               "steps": e2e_steps, "api": f"bandsolve_{kind}_solve_shared (pinned host batch)"}
+    clk = clocks.summary()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(kind, n, m)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32" if args.f32 else "f64",
+            "data": "synthetic: U(-1,1) RHS from SplitMix64(seed=42, i, global j), generated on device",
+            "config": {"workload": desc, "kind": kind, "n": n, "batch_per_gpu": m, "global_batch": m * world,
+                       "mode": args.mode, "plan": lib.describe_plan(0 if kind == "tri" else 1, n, m, m, args.f32),
+                       "parallelism": f"dp{world} (systems sharded, no data-path collective)",
+                       "l2": f"{nbuf} rotating in-place buffers of {bytes_per / 2**20:.0f} MiB "
+                             f"(working set {nbuf * bytes_per / 132644864:.1f}x L2)"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "algorithmic_bytes_per_launch": algo_bytes, "peak_source": peak_src,
+                         "kernel": f"sweep_smem<{'float' if args.f32 else 'double'},{kind}>"},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main() -> int:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    ap.add_argument("--mode", choices=["exact", "fast"], default=os.environ.get("BANDSOLVE_BENCH_MODE", "exact"))
+    ap.add_argument("--f32", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference_arm(args, rank)
+        return 0
+
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_gpu_arm(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,247 @@
+/*
+ * bandsolve (B200) — shared-LHS interleaved batch tridiagonal / pentadiagonal
+ * solvers for NVIDIA B200 (sm_100a), drop-in for the reference C ABI.
+ *
+ * Every declaration in the first part carries the same name, arguments,
+ * ownership and status semantics as the reference header
+ * /root/reference/proj/include/bandsolve.h (cited per entry point as
+ * "ref bandsolve.h:<line>", with the implementing reference source). A
+ * caller linked against libbandsolve.so.1 can relink against
+ * libbandsolve_b200.so for these entry points unchanged. The reference's
+ * periodic, per-system, IBAT, footprint and benchmark-driver entry points
+ * are outside this library's scope.
+ *
+ * The second part ("B200 extensions") adds device-resident entry points for
+ * callers that keep their batch in HBM: they take a device pointer, a row
+ * pitch and a CUDA stream, enqueue the solve and return without
+ * synchronising.
+ *
+ * Layout contract (ref batch.hpp:13-16): element (row i, system j) of an
+ * n x m batch lives at data[i*m + j] (device variants: data[i*ld + j]).
+ *
+ * Solves run on the GPU only. Without a usable CUDA device every solve
+ * returns BANDSOLVE_ERR_INTERNAL and bandsolve_last_error() says why; there
+ * is no CPU fallback.
+ */
+#ifndef BANDSOLVE_H
+#define BANDSOLVE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ref bandsolve.h:22-33 — identical values. */
+typedef enum bandsolve_status {
+  BANDSOLVE_OK = 0,
+  BANDSOLVE_ERR_BAD_ARG = 1,
+  BANDSOLVE_ERR_SHAPE_MISMATCH = 2,
+  BANDSOLVE_ERR_FACTORIZATION_BREAKDOWN = 3,
+  BANDSOLVE_ERR_DIVISION_BY_ZERO = 4,
+  BANDSOLVE_ERR_SINGULAR_CORRECTION = 5,
+  BANDSOLVE_ERR_SINGULAR_MATRIX = 6,
+  BANDSOLVE_ERR_BAD_FORMAT = 7,
+  BANDSOLVE_ERR_IO = 8,
+  BANDSOLVE_ERR_INTERNAL = 9
+} bandsolve_status;
+
+/* ref bandsolve.h:35 (capi.cpp:82-97) — same strings. */
+const char* bandsolve_status_string(bandsolve_status status);
+/* ref bandsolve.h:36 (capi.cpp:99) — the ABI version, "1.0.0". */
+const char* bandsolve_version(void);
+
+/* ref bandsolve.h:41-42 (parallel.cpp:30-37). The count is recorded and
+ * reported with the reference's resolution order (set value >
+ * BANDSOLVE_THREADS > hardware concurrency); it does not change the GPU
+ * solve, whose results are bitwise independent of it, as in the reference. */
+int bandsolve_get_threads(void);
+void bandsolve_set_threads(int threads);
+
+/* ---- Interleaved batch (ref bandsolve.h:47-55, capi.cpp:105-128) ---------
+ * Host storage, zero-filled, page-locked when a CUDA driver is present so
+ * the staged solves copy at full PCIe rate. n == 0 or m == 0 -> BAD_ARG. */
+typedef struct bandsolve_batch bandsolve_batch;
+
+bandsolve_status bandsolve_batch_create(size_t n, size_t m,
+                                        bandsolve_batch** out);
+void bandsolve_batch_destroy(bandsolve_batch* batch);
+size_t bandsolve_batch_rows(const bandsolve_batch* batch);
+size_t bandsolve_batch_systems(const bandsolve_batch* batch);
+double* bandsolve_batch_data(bandsolve_batch* batch);
+const double* bandsolve_batch_data_const(const bandsolve_batch* batch);
+
+/* ---- Tridiagonal (ref bandsolve.h:67-78) ---------------------------------
+ * sub/diag/sup of length n >= 2, finite, sub[0] = sup[n-1] = 0
+ * (banded.cpp:40-57). The factor (banded.cpp:67-86) is computed on the host
+ * in the reference's operation order and uploaded to each device on first
+ * use; the handle is immutable and may be shared across threads. */
+typedef struct bandsolve_tri_factor bandsolve_tri_factor;
+
+bandsolve_status bandsolve_tri_factor_create(const double* sub,
+                                             const double* diag,
+                                             const double* sup, size_t n,
+                                             bandsolve_tri_factor** out);
+void bandsolve_tri_factor_destroy(bandsolve_tri_factor* factor);
+
+/* ref bandsolve.h:77-78 (capi.cpp:159-163 -> tri_solver.cpp:11-49).
+ * Overwrites every system of the host batch with its solution: pinned
+ * host -> device copies, sweep kernel, device -> host copies, pipelined over
+ * column chunks, synchronous on return. rows != n -> SHAPE_MISMATCH. */
+bandsolve_status bandsolve_tri_solve_shared(const bandsolve_tri_factor* factor,
+                                            bandsolve_batch* batch);
+
+/* ---- Pentadiagonal (ref bandsolve.h:91-113) ------------------------------
+ * Bands a..e of length n >= 5, main diagonal c, structural zeros
+ * a[0] = a[1] = b[0] = d[n-1] = e[n-1] = e[n-2] = 0 (banded.cpp:88-116). */
+typedef struct bandsolve_pent_factor bandsolve_pent_factor;
+typedef struct bandsolve_uniform_pent_factor bandsolve_uniform_pent_factor;
+
+bandsolve_status bandsolve_pent_factor_create(const double* a, const double* b,
+                                              const double* c, const double* d,
+                                              const double* e, size_t n,
+                                              bandsolve_pent_factor** out);
+void bandsolve_pent_factor_destroy(bandsolve_pent_factor* factor);
+/* ref bandsolve.h:99-100 (capi.cpp:191-195 -> pent_solver.cpp:67-81). */
+bandsolve_status bandsolve_pent_solve_shared(
+    const bandsolve_pent_factor* factor, bandsolve_batch* batch);
+
+/* ref bandsolve.h:107-113 (capi.cpp:207-227 -> pent_solver.cpp:83-111):
+ * constant bands, epsilon kept as one scalar; bitwise equal to the shared
+ * solve of the expanded matrix. */
+bandsolve_status bandsolve_uniform_pent_factor_create(
+    double a, double b, double c, double d, double e, size_t n,
+    bandsolve_uniform_pent_factor** out);
+void bandsolve_uniform_pent_factor_destroy(
+    bandsolve_uniform_pent_factor* factor);
+bandsolve_status bandsolve_pent_solve_uniform(
+    const bandsolve_uniform_pent_factor* factor, bandsolve_batch* batch);
+
+/* ---- Residuals (ref bandsolve.h:165-179, tri_solver.cpp:116-156,
+ * pent_solver.cpp:223-273) — max over systems of ||A x - rhs||_inf /
+ * ||rhs||_inf, evaluated on the GPU in the reference's operation order.
+ * cyclic != 0 reads the wrap corners from the interior band entries. */
+bandsolve_status bandsolve_tri_residual(const double* sub, const double* diag,
+                                        const double* sup, size_t n,
+                                        int cyclic,
+                                        const bandsolve_batch* x,
+                                        const bandsolve_batch* rhs,
+                                        double* out);
+bandsolve_status bandsolve_pent_residual(const double* a, const double* b,
+                                         const double* c, const double* d,
+                                         const double* e, size_t n, int cyclic,
+                                         const bandsolve_batch* x,
+                                         const bandsolve_batch* rhs,
+                                         double* out);
+
+/* ======================================================================== */
+/* B200 extensions                                                          */
+/* ======================================================================== */
+
+/* Arithmetic mode of the sweep kernels.
+ *   EXACT (default): the reference's operation order with every product and
+ *     difference rounded separately (no FMA contraction): fp64 results are
+ *     bitwise identical to the reference CPU solver.
+ *   FAST: fused multiply-adds over host-prescaled factors (tri: p_i = a_i m_i;
+ *     pent: beta_i/alpha_i, eps_i/alpha_i) — one dependent DFMA per row and
+ *     sweep. Differs from the reference by rounding only (per-system
+ *     max-norm relative gap <= 1e-12 on the conditioned systems tested).
+ * Process-global; the environment variable BANDSOLVE_MODE=exact|fast sets
+ * the initial value. */
+typedef enum bandsolve_mode {
+  BANDSOLVE_MODE_EXACT = 0,
+  BANDSOLVE_MODE_FAST = 1
+} bandsolve_mode;
+bandsolve_status bandsolve_set_mode(int mode);
+int bandsolve_get_mode(void);
+
+/* Device-resident solves. x points to an n x m interleaved array in device
+ * memory of the current CUDA device, row pitch ld >= m elements; stream is a
+ * cudaStream_t (NULL = legacy default stream). The call validates, enqueues
+ * and returns; it does not synchronise. n must equal the factor's order.
+ * The f32 variants round the fp64 factor once and sweep in binary32. */
+bandsolve_status bandsolve_tri_solve_shared_dev(
+    const bandsolve_tri_factor* factor, double* x, size_t n, size_t m,
+    size_t ld, void* stream);
+bandsolve_status bandsolve_tri_solve_shared_dev_f32(
+    const bandsolve_tri_factor* factor, float* x, size_t n, size_t m,
+    size_t ld, void* stream);
+bandsolve_status bandsolve_pent_solve_shared_dev(
+    const bandsolve_pent_factor* factor, double* x, size_t n, size_t m,
+    size_t ld, void* stream);
+bandsolve_status bandsolve_pent_solve_shared_dev_f32(
+    const bandsolve_pent_factor* factor, float* x, size_t n, size_t m,
+    size_t ld, void* stream);
+bandsolve_status bandsolve_pent_solve_uniform_dev(
+    const bandsolve_uniform_pent_factor* factor, double* x, size_t n,
+    size_t m, size_t ld, void* stream);
+bandsolve_status bandsolve_pent_solve_uniform_dev_f32(
+    const bandsolve_uniform_pent_factor* factor, float* x, size_t n, size_t m,
+    size_t ld, void* stream);
+
+/* Device residual of a device-resident solution against a device-resident
+ * right-hand side (both n x m, pitch ld), bands on the host. Synchronous:
+ * writes the max relative residual to *out. */
+bandsolve_status bandsolve_tri_residual_dev(const double* sub,
+                                            const double* diag,
+                                            const double* sup, size_t n,
+                                            int cyclic, const double* x,
+                                            const double* rhs, size_t m,
+                                            size_t ld, void* stream,
+                                            double* out);
+bandsolve_status bandsolve_pent_residual_dev(
+    const double* a, const double* b, const double* c, const double* d,
+    const double* e, size_t n, int cyclic, const double* x, const double* rhs,
+    size_t m, size_t ld, void* stream, double* out);
+
+/* Synthetic right-hand side on the device: x[i*ld + j] = U(-1, 1) drawn
+ * from SplitMix64 of (seed, i, j_offset + j), identical bit for bit to the
+ * host generator in oracle/ (so shards of one global batch agree). */
+bandsolve_status bandsolve_fill_rhs_dev(double* x, size_t n, size_t m,
+                                        size_t ld, uint64_t seed,
+                                        uint64_t j_offset, void* stream);
+bandsolve_status bandsolve_fill_rhs_dev_f32(float* x, size_t n, size_t m,
+                                            size_t ld, uint64_t seed,
+                                            uint64_t j_offset, void* stream);
+
+/* Factor introspection: copies the host factor arrays (the reference's
+ * tri_factor / pent_factor / uniform_pent_factor fields, banded.hpp:48-53,
+ * :88-95, pent_solver.hpp:31-38). Any pointer may be NULL. */
+size_t bandsolve_tri_factor_order(const bandsolve_tri_factor* factor);
+bandsolve_status bandsolve_tri_factor_arrays(const bandsolve_tri_factor* f,
+                                             double* chat, double* inv_denom,
+                                             double* sub);
+size_t bandsolve_pent_factor_order(const bandsolve_pent_factor* factor);
+bandsolve_status bandsolve_pent_factor_arrays(const bandsolve_pent_factor* f,
+                                              double* inv_alpha, double* beta,
+                                              double* gamma, double* delta,
+                                              double* epsilon);
+size_t bandsolve_uniform_pent_factor_order(
+    const bandsolve_uniform_pent_factor* factor);
+bandsolve_status bandsolve_uniform_pent_factor_arrays(
+    const bandsolve_uniform_pent_factor* f, double* inv_alpha, double* beta,
+    double* gamma, double* delta, double* eps_scalar);
+
+/* Kernel plan the sweep would use for (kind, n, m, dtype) on the current
+ * device: writes a short human-readable description ("smem-tma W=16 ..."). */
+typedef enum bandsolve_kind {
+  BANDSOLVE_KIND_TRI = 0,
+  BANDSOLVE_KIND_PENT = 1,
+  BANDSOLVE_KIND_UNIFORM = 2
+} bandsolve_kind;
+bandsolve_status bandsolve_describe_plan(int kind, size_t n, size_t m,
+                                         size_t ld, int f32, char* buf,
+                                         size_t buflen);
+
+/* Number of this library's kernels launched since load (all threads). */
+uint64_t bandsolve_kernel_launches(void);
+
+/* Thread-local description of the last non-OK status on this thread. */
+const char* bandsolve_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BANDSOLVE_H */

@@ -1,0 +1,400 @@
+/*
+ * TEST INFRASTRUCTURE ONLY — see bandsolve_oracle.h. Plain-C restatement of
+ * the reference hot path, pinned bit-for-bit against the reference build in
+ * oracle/_ref/ by tests/test_oracle.py. Compile with -ffp-contract=off.
+ */
+#include "bandsolve_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+enum {
+  ST_OK = 0,
+  ST_BAD_ARG = 1,
+  ST_SHAPE = 2,
+  ST_BREAKDOWN = 3,
+  ST_SINGULAR_MATRIX = 6,
+  ST_INTERNAL = 9
+};
+
+/* common.hpp:17 */
+static const double k_breakdown_eps = 1e-300;
+
+/* banded.cpp:32-36 — the negated >= also rejects NaN pivots */
+static int denom_ok(double denom) { return fabs(denom) >= k_breakdown_eps; }
+
+static int all_finite(const double* v, size_t n) {
+  for (size_t i = 0; i < n; ++i)
+    if (!isfinite(v[i])) return 0;
+  return 1;
+}
+
+int oracle_tri_prefactor(const double* sub, const double* diag,
+                         const double* sup, size_t n, double* chat,
+                         double* inv_denom, double* sub_out) {
+  /* tri_lhs validation, banded.cpp:40-57 */
+  if (!sub || !diag || !sup || !chat || !inv_denom || !sub_out) return ST_BAD_ARG;
+  if (n < 2) return ST_BAD_ARG;
+  if (!all_finite(sub, n) || !all_finite(diag, n) || !all_finite(sup, n))
+    return ST_BAD_ARG;
+  if (sub[0] != 0.0 || sup[n - 1] != 0.0) return ST_BAD_ARG;
+
+  /* banded.cpp:75-84; chat divides by denom (not sup * inv) */
+  memcpy(sub_out, sub, n * sizeof(double));
+  double denom = diag[0];
+  if (!denom_ok(denom)) return ST_BREAKDOWN;
+  inv_denom[0] = 1.0 / denom;
+  chat[0] = sup[0] / denom;
+  for (size_t i = 1; i < n; ++i) {
+    denom = diag[i] - sub[i] * chat[i - 1];
+    if (!denom_ok(denom)) return ST_BREAKDOWN;
+    inv_denom[i] = 1.0 / denom;
+    chat[i] = (i + 1 < n) ? sup[i] / denom : 0.0;
+  }
+  return ST_OK;
+}
+
+void oracle_tri_solve_shared(const double* chat, const double* inv_denom,
+                             const double* sub, size_t n, size_t m, size_t ld,
+                             double* x) {
+  /* forward, tri_solver.cpp:24-38 */
+  for (size_t j = 0; j < m; ++j) x[j] *= inv_denom[0];
+  for (size_t i = 1; i < n; ++i) {
+    const double ai = sub[i], mi = inv_denom[i];
+    double* row = x + i * ld;
+    const double* prev = row - ld;
+    for (size_t j = 0; j < m; ++j) row[j] = (row[j] - ai * prev[j]) * mi;
+  }
+  /* backward, tri_solver.cpp:39-47 */
+  for (size_t i = n - 1; i-- > 0;) {
+    const double ci = chat[i];
+    double* row = x + i * ld;
+    const double* next = row + ld;
+    for (size_t j = 0; j < m; ++j) row[j] -= ci * next[j];
+  }
+}
+
+int oracle_pent_prefactor(const double* a, const double* b, const double* c,
+                          const double* d, const double* e, size_t n,
+                          double* inv_alpha, double* beta, double* gamma,
+                          double* delta, double* epsilon) {
+  /* pent_lhs validation, banded.cpp:88-116 */
+  if (!a || !b || !c || !d || !e || !inv_alpha || !beta || !gamma || !delta ||
+      !epsilon)
+    return ST_BAD_ARG;
+  if (n < 5) return ST_BAD_ARG;
+  if (!all_finite(a, n) || !all_finite(b, n) || !all_finite(c, n) ||
+      !all_finite(d, n) || !all_finite(e, n))
+    return ST_BAD_ARG;
+  if (a[0] != 0.0 || a[1] != 0.0 || b[0] != 0.0 || d[n - 1] != 0.0 ||
+      e[n - 1] != 0.0 || e[n - 2] != 0.0)
+    return ST_BAD_ARG;
+
+  double* alpha = (double*)malloc(n * sizeof(double));
+  if (!alpha) return ST_INTERNAL;
+  int st = ST_OK;
+  memset(beta, 0, n * sizeof(double));
+  memset(gamma, 0, n * sizeof(double));
+  memset(delta, 0, n * sizeof(double));
+  memcpy(epsilon, a, n * sizeof(double));
+
+  /* banded.cpp:141-150 */
+  alpha[0] = c[0];
+  if (!denom_ok(alpha[0])) { st = ST_BREAKDOWN; goto done; }
+  gamma[0] = d[0] / alpha[0];
+  delta[0] = e[0] / alpha[0];
+  beta[1] = b[1];
+  alpha[1] = c[1] - beta[1] * gamma[0];
+  if (!denom_ok(alpha[1])) { st = ST_BREAKDOWN; goto done; }
+  gamma[1] = (d[1] - beta[1] * delta[0]) / alpha[1];
+  delta[1] = e[1] / alpha[1];
+  /* banded.cpp:152-158; alpha is (c - a*delta) - beta*gamma, left to right */
+  for (size_t i = 2; i + 2 < n; ++i) {
+    beta[i] = b[i] - a[i] * gamma[i - 2];
+    alpha[i] = c[i] - a[i] * delta[i - 2] - beta[i] * gamma[i - 1];
+    if (!denom_ok(alpha[i])) { st = ST_BREAKDOWN; goto done; }
+    gamma[i] = (d[i] - beta[i] * delta[i - 1]) / alpha[i];
+    delta[i] = e[i] / alpha[i];
+  }
+  /* banded.cpp:160-172 */
+  {
+    const size_t i = n - 2;
+    beta[i] = b[i] - a[i] * gamma[i - 2];
+    alpha[i] = c[i] - a[i] * delta[i - 2] - beta[i] * gamma[i - 1];
+    if (!denom_ok(alpha[i])) { st = ST_BREAKDOWN; goto done; }
+    gamma[i] = (d[i] - beta[i] * delta[i - 1]) / alpha[i];
+  }
+  {
+    const size_t i = n - 1;
+    beta[i] = b[i] - a[i] * gamma[i - 2];
+    alpha[i] = c[i] - a[i] * delta[i - 2] - beta[i] * gamma[i - 1];
+    if (!denom_ok(alpha[i])) { st = ST_BREAKDOWN; goto done; }
+  }
+  /* banded.cpp:174 */
+  for (size_t i = 0; i < n; ++i) inv_alpha[i] = 1.0 / alpha[i];
+done:
+  free(alpha);
+  return st;
+}
+
+void oracle_pent_solve(const double* inv_alpha, const double* beta,
+                       const double* gamma, const double* delta,
+                       const double* eps, double eps_scalar, size_t n,
+                       size_t m, size_t ld, double* x) {
+  /* g over f, pent_solver.cpp:19-43 */
+  for (size_t j = 0; j < m; ++j) x[j] *= inv_alpha[0];
+  {
+    const double b1 = beta[1], ia1 = inv_alpha[1];
+    double* row = x + ld;
+    for (size_t j = 0; j < m; ++j) row[j] = (row[j] - b1 * x[j]) * ia1;
+  }
+  for (size_t i = 2; i < n; ++i) {
+    const double ei = eps ? eps[i] : eps_scalar;
+    const double bi = beta[i], iai = inv_alpha[i];
+    double* row = x + i * ld;
+    const double* p1 = row - ld;
+    const double* p2 = row - 2 * ld;
+    for (size_t j = 0; j < m; ++j)
+      row[j] = (row[j] - ei * p2[j] - bi * p1[j]) * iai;
+  }
+  /* x over g, pent_solver.cpp:44-62 */
+  {
+    const double gn2 = gamma[n - 2];
+    double* row = x + (n - 2) * ld;
+    const double* next = row + ld;
+    for (size_t j = 0; j < m; ++j) row[j] -= gn2 * next[j];
+  }
+  for (size_t i = n - 2; i-- > 0;) {
+    const double gi = gamma[i], di = delta[i];
+    double* row = x + i * ld;
+    const double* n1 = row + ld;
+    const double* n2 = row + 2 * ld;
+    for (size_t j = 0; j < m; ++j) row[j] -= gi * n1[j] + di * n2[j];
+  }
+}
+
+int oracle_uniform_pent_prefactor(double a, double b, double c, double d,
+                                  double e, size_t n, double* inv_alpha,
+                                  double* beta, double* gamma, double* delta,
+                                  double* eps_scalar) {
+  if (n < 5) return ST_BAD_ARG; /* banded.cpp:120 */
+  double* bands = (double*)malloc(6 * n * sizeof(double));
+  if (!bands) return ST_INTERNAL;
+  double *av = bands, *bv = bands + n, *cv = bands + 2 * n, *dv = bands + 3 * n,
+         *ev = bands + 4 * n, *eps = bands + 5 * n;
+  for (size_t i = 0; i < n; ++i) {
+    av[i] = a; bv[i] = b; cv[i] = c; dv[i] = d; ev[i] = e;
+  }
+  av[0] = av[1] = bv[0] = 0.0; /* banded.cpp:122-123 */
+  dv[n - 1] = ev[n - 1] = ev[n - 2] = 0.0;
+  int st = oracle_pent_prefactor(av, bv, cv, dv, ev, n, inv_alpha, beta, gamma,
+                                 delta, eps);
+  if (st == ST_OK && eps_scalar) *eps_scalar = a; /* pent_solver.cpp:109 */
+  free(bands);
+  return st;
+}
+
+static double residual_pass_tri(size_t n, size_t m, const double* x,
+                                const double* rhs, const double* sub,
+                                const double* diag, const double* sup,
+                                double corner_tr, double corner_bl) {
+  /* tri_solver.cpp:116-136 */
+  double worst = 0.0;
+  for (size_t j = 0; j < m; ++j) {
+    double rmax = 0.0, dmax = 0.0;
+    for (size_t i = 0; i < n; ++i) {
+      double acc = diag[i] * x[i * m + j];
+      if (i > 0) acc += sub[i] * x[(i - 1) * m + j];
+      if (i + 1 < n) acc += sup[i] * x[(i + 1) * m + j];
+      if (i == 0) acc += corner_tr * x[(n - 1) * m + j];
+      if (i == n - 1) acc += corner_bl * x[j];
+      double r = fabs(acc - rhs[i * m + j]);
+      if (r > rmax) rmax = r;
+      double dv = fabs(rhs[i * m + j]);
+      if (dv > dmax) dmax = dv;
+    }
+    double w = dmax > 0.0 ? rmax / dmax : rmax;
+    if (w > worst) worst = w;
+  }
+  return worst;
+}
+
+int oracle_tri_residual(const double* sub, const double* diag,
+                        const double* sup, size_t n, int cyclic, size_t m,
+                        const double* x, const double* rhs, double* out) {
+  if (!sub || !diag || !sup || !x || !rhs || !out) return ST_BAD_ARG;
+  if (cyclic) {
+    /* capi.cpp:336-339, tri_solver.cpp:149-156 */
+    if (n < 3) return ST_BAD_ARG;
+    const double a = sub[1], b = diag[0], c = sup[0];
+    double* bands = (double*)malloc(3 * n * sizeof(double));
+    if (!bands) return ST_INTERNAL;
+    double *sv = bands, *dv = bands + n, *uv = bands + 2 * n;
+    for (size_t i = 0; i < n; ++i) { sv[i] = a; dv[i] = b; uv[i] = c; }
+    sv[0] = 0.0;
+    uv[n - 1] = 0.0;
+    if (!all_finite(bands, 3 * n)) { free(bands); return ST_BAD_ARG; }
+    *out = residual_pass_tri(n, m, x, rhs, sv, dv, uv, a, c);
+    free(bands);
+    return ST_OK;
+  }
+  if (n < 2 || !all_finite(sub, n) || !all_finite(diag, n) ||
+      !all_finite(sup, n) || sub[0] != 0.0 || sup[n - 1] != 0.0)
+    return ST_BAD_ARG;
+  *out = residual_pass_tri(n, m, x, rhs, sub, diag, sup, 0.0, 0.0);
+  return ST_OK;
+}
+
+static double residual_pass_pent(size_t n, size_t m, const double* x,
+                                 const double* rhs, const double* a,
+                                 const double* b, const double* c,
+                                 const double* d, const double* e, int cyclic,
+                                 double ca, double cb, double cd, double ce) {
+  /* pent_solver.cpp:223-251 */
+  double worst = 0.0;
+  for (size_t j = 0; j < m; ++j) {
+    double rmax = 0.0, dmax = 0.0;
+#define X(r) x[(r) * m + j]
+    for (size_t i = 0; i < n; ++i) {
+      double acc = c[i] * X(i);
+      if (i >= 2) acc += a[i] * X(i - 2);
+      if (i >= 1) acc += b[i] * X(i - 1);
+      if (i + 1 < n) acc += d[i] * X(i + 1);
+      if (i + 2 < n) acc += e[i] * X(i + 2);
+      if (cyclic) {
+        if (i == 0) acc += ca * X(n - 2) + cb * X(n - 1);
+        if (i == 1) acc += ca * X(n - 1);
+        if (i == n - 2) acc += ce * X(0);
+        if (i == n - 1) acc += cd * X(0) + ce * X(1);
+      }
+      double r = fabs(acc - rhs[i * m + j]);
+      if (r > rmax) rmax = r;
+      double dv = fabs(rhs[i * m + j]);
+      if (dv > dmax) dmax = dv;
+    }
+#undef X
+    double w = dmax > 0.0 ? rmax / dmax : rmax;
+    if (w > worst) worst = w;
+  }
+  return worst;
+}
+
+int oracle_pent_residual(const double* a, const double* b, const double* c,
+                         const double* d, const double* e, size_t n,
+                         int cyclic, size_t m, const double* x,
+                         const double* rhs, double* out) {
+  if (!a || !b || !c || !d || !e || !x || !rhs || !out) return ST_BAD_ARG;
+  if (cyclic) {
+    /* capi.cpp:357-360, pent_solver.cpp:265-273 */
+    if (n < 6) return ST_BAD_ARG;
+    const double ca = a[2], cb = b[1], cc = c[0], cd = d[0], ce = e[0];
+    double* bands = (double*)malloc(5 * n * sizeof(double));
+    if (!bands) return ST_INTERNAL;
+    double *av = bands, *bv = bands + n, *cv = bands + 2 * n, *dv = bands + 3 * n,
+           *ev = bands + 4 * n;
+    for (size_t i = 0; i < n; ++i) {
+      av[i] = ca; bv[i] = cb; cv[i] = cc; dv[i] = cd; ev[i] = ce;
+    }
+    av[0] = av[1] = bv[0] = 0.0;
+    dv[n - 1] = ev[n - 1] = ev[n - 2] = 0.0;
+    if (!all_finite(bands, 5 * n)) { free(bands); return ST_BAD_ARG; }
+    *out = residual_pass_pent(n, m, x, rhs, av, bv, cv, dv, ev, 1, ca, cb, cd,
+                              ce);
+    free(bands);
+    return ST_OK;
+  }
+  if (n < 5 || !all_finite(a, n) || !all_finite(b, n) || !all_finite(c, n) ||
+      !all_finite(d, n) || !all_finite(e, n) || a[0] != 0.0 || a[1] != 0.0 ||
+      b[0] != 0.0 || d[n - 1] != 0.0 || e[n - 1] != 0.0 || e[n - 2] != 0.0)
+    return ST_BAD_ARG;
+  *out = residual_pass_pent(n, m, x, rhs, a, b, c, d, e, 0, 0, 0, 0, 0);
+  return ST_OK;
+}
+
+int oracle_max_error_vs_dense(const double* a, size_t n, size_t m,
+                              const double* x, const double* rhs,
+                              double* out) {
+  /* dense.cpp:15-48 (partial-pivot LU with row permutation), :50-71
+   * (solve_in_place), oracles.cpp:104-122 (metric). */
+  if (!a || !x || !rhs || !out || n == 0) return ST_BAD_ARG;
+  double* lu = (double*)malloc(n * n * sizeof(double));
+  size_t* perm = (size_t*)malloc(n * sizeof(size_t));
+  double* col = (double*)malloc(n * sizeof(double));
+  double* y = (double*)malloc(n * sizeof(double));
+  int st = ST_OK;
+  if (!lu || !perm || !col || !y) { st = ST_INTERNAL; goto done; }
+  memcpy(lu, a, n * n * sizeof(double));
+  for (size_t i = 0; i < n; ++i) perm[i] = i;
+  for (size_t k = 0; k < n; ++k) {
+    size_t piv = k;
+    double best = fabs(lu[perm[k] * n + k]);
+    for (size_t i = k + 1; i < n; ++i) {
+      double mag = fabs(lu[perm[i] * n + k]);
+      if (mag > best) { best = mag; piv = i; }
+    }
+    if (!(best > 1e-14)) { st = ST_SINGULAR_MATRIX; goto done; }
+    size_t t = perm[k]; perm[k] = perm[piv]; perm[piv] = t;
+    const double* prow = lu + perm[k] * n;
+    const double inv_piv = 1.0 / prow[k];
+    for (size_t i = k + 1; i < n; ++i) {
+      double* row = lu + perm[i] * n;
+      const double l = row[k] * inv_piv;
+      row[k] = l;
+      if (l != 0.0)
+        for (size_t jj = k + 1; jj < n; ++jj) row[jj] -= l * prow[jj];
+    }
+  }
+  double worst = 0.0;
+  for (size_t j = 0; j < m; ++j) {
+    for (size_t i = 0; i < n; ++i) col[i] = rhs[i * m + j];
+    for (size_t i = 0; i < n; ++i) {
+      double s = col[perm[i]];
+      const double* row = lu + perm[i] * n;
+      for (size_t q = 0; q < i; ++q) s -= row[q] * y[q];
+      y[i] = s;
+    }
+    for (size_t ii = n; ii-- > 0;) {
+      double s = y[ii];
+      const double* row = lu + perm[ii] * n;
+      for (size_t q = ii + 1; q < n; ++q) s -= row[q] * y[q];
+      y[ii] = s / row[ii];
+    }
+    double err = 0.0, scale = 0.0;
+    for (size_t i = 0; i < n; ++i) {
+      double e = fabs(x[i * m + j] - y[i]);
+      if (e > err) err = e;
+      double s = fabs(y[i]);
+      if (s > scale) scale = s;
+    }
+    double w = scale > 0.0 ? err / scale : err;
+    if (w > worst) worst = w;
+  }
+  *out = worst;
+done:
+  free(lu); free(perm); free(col); free(y);
+  return st;
+}
+
+static uint64_t splitmix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+double oracle_rhs_value(uint64_t seed, uint64_t i, uint64_t j) {
+  uint64_t h = splitmix64(seed);
+  h = splitmix64(h ^ i);
+  h = splitmix64(h ^ j);
+  /* (k - 2^52) / 2^52 with k < 2^53: exact in binary64, range [-1, 1) */
+  return (double)(h >> 11) * 0x1.0p-52 - 1.0;
+}
+
+void oracle_fill_rhs(uint64_t seed, size_t n, size_t m, size_t j_offset,
+                     size_t m_total, double* x) {
+  (void)m_total;
+  for (size_t i = 0; i < n; ++i)
+    for (size_t j = 0; j < m; ++j)
+      x[i * m + j] = oracle_rhs_value(seed, i, j_offset + j);
+}

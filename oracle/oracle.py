@@ -1,0 +1,214 @@
+"""TEST INFRASTRUCTURE ONLY — numpy/ctypes front end of the CPU oracle.
+
+Wraps oracle/liboracle.so (the plain-C restatement in bandsolve_oracle.c) and
+locates the reference build oracle/_ref/libbandsolve_ref.so. Only tests/,
+__graft_entry__.smoke() and bench.py's CPU legs may import this module; the
+product path never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+ORACLE_DIR = os.path.dirname(os.path.abspath(__file__))
+PORT_LIB = os.path.join(ORACLE_DIR, "liboracle.so")
+REF_LIB = os.path.join(ORACLE_DIR, "_ref", "libbandsolve_ref.so")
+REFERENCE_SRC = "/root/reference/proj"
+
+_dp = C.POINTER(C.c_double)
+_sz = C.c_size_t
+
+
+def build_port() -> str:
+    """Build liboracle.so if needed (gcc is in the image on both sides)."""
+    src = os.path.join(ORACLE_DIR, "bandsolve_oracle.c")
+    if not os.path.exists(PORT_LIB) or os.path.getmtime(PORT_LIB) < os.path.getmtime(src):
+        subprocess.check_call(["make", "-s", "-C", ORACLE_DIR, "port"])
+    return PORT_LIB
+
+
+def build_ref() -> str | None:
+    """Build the reference library from /root/reference when that tree exists."""
+    if os.path.exists(REF_LIB):
+        return REF_LIB
+    if not os.path.isdir(REFERENCE_SRC):
+        return None
+    subprocess.check_call(["make", "-s", "-C", ORACLE_DIR, "-j8", "ref"])
+    return REF_LIB
+
+
+def _d(a: np.ndarray):
+    return a.ctypes.data_as(_dp)
+
+
+def _arr(v, n=None) -> np.ndarray:
+    a = np.ascontiguousarray(np.asarray(v, dtype=np.float64))
+    if n is not None:
+        assert a.shape == (n,), (a.shape, n)
+    return a
+
+
+class OracleError(RuntimeError):
+    def __init__(self, status: int):
+        super().__init__(f"oracle status {status}")
+        self.status = status
+
+
+class Oracle:
+    def __init__(self, path: str | None = None):
+        self.lib = C.CDLL(path or build_port())
+        L = self.lib
+        L.oracle_tri_prefactor.argtypes = [_dp, _dp, _dp, _sz, _dp, _dp, _dp]
+        L.oracle_tri_solve_shared.argtypes = [_dp, _dp, _dp, _sz, _sz, _sz, _dp]
+        L.oracle_tri_solve_shared.restype = None
+        L.oracle_pent_prefactor.argtypes = [_dp] * 5 + [_sz] + [_dp] * 5
+        L.oracle_pent_solve.argtypes = [_dp] * 5 + [C.c_double, _sz, _sz, _sz, _dp]
+        L.oracle_pent_solve.restype = None
+        L.oracle_uniform_pent_prefactor.argtypes = [C.c_double] * 5 + [_sz] + [_dp] * 5
+        L.oracle_tri_residual.argtypes = [_dp, _dp, _dp, _sz, C.c_int, _sz, _dp, _dp, _dp]
+        L.oracle_pent_residual.argtypes = [_dp] * 5 + [_sz, C.c_int, _sz, _dp, _dp, _dp]
+        L.oracle_max_error_vs_dense.argtypes = [_dp, _sz, _sz, _dp, _dp, _dp]
+        L.oracle_rhs_value.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64]
+        L.oracle_rhs_value.restype = C.c_double
+        L.oracle_fill_rhs.argtypes = [C.c_uint64, _sz, _sz, _sz, _sz, _dp]
+        L.oracle_fill_rhs.restype = None
+
+    # -- factors ------------------------------------------------------------
+    def tri_prefactor(self, sub, diag, sup) -> dict:
+        n = len(diag)
+        s, d, u = _arr(sub, n), _arr(diag, n), _arr(sup, n)
+        out = {k: np.zeros(n) for k in ("chat", "inv_denom", "sub")}
+        st = self.lib.oracle_tri_prefactor(_d(s), _d(d), _d(u), n, _d(out["chat"]), _d(out["inv_denom"]),
+                                           _d(out["sub"]))
+        if st:
+            raise OracleError(st)
+        return out
+
+    def pent_prefactor(self, a, b, c, d, e) -> dict:
+        n = len(c)
+        bands = [_arr(v, n) for v in (a, b, c, d, e)]
+        keys = ("inv_alpha", "beta", "gamma", "delta", "epsilon")
+        out = {k: np.zeros(n) for k in keys}
+        st = self.lib.oracle_pent_prefactor(*[_d(v) for v in bands], n, *[_d(out[k]) for k in keys])
+        if st:
+            raise OracleError(st)
+        return out
+
+    def uniform_prefactor(self, a, b, c, d, e, n) -> dict:
+        keys = ("inv_alpha", "beta", "gamma", "delta")
+        out = {k: np.zeros(n) for k in keys}
+        eps = np.zeros(1)
+        st = self.lib.oracle_uniform_pent_prefactor(a, b, c, d, e, n, *[_d(out[k]) for k in keys], _d(eps))
+        if st:
+            raise OracleError(st)
+        out["eps_scalar"] = float(eps[0])
+        return out
+
+    # -- sweeps (in place on a C-contiguous (n, m) float64 array) -------------
+    def tri_solve(self, f: dict, x: np.ndarray) -> np.ndarray:
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        n, m = x.shape
+        self.lib.oracle_tri_solve_shared(_d(f["chat"]), _d(f["inv_denom"]), _d(f["sub"]), n, m, m, _d(x))
+        return x
+
+    def pent_solve(self, f: dict, x: np.ndarray) -> np.ndarray:
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        n, m = x.shape
+        eps = f.get("epsilon")
+        self.lib.oracle_pent_solve(_d(f["inv_alpha"]), _d(f["beta"]), _d(f["gamma"]), _d(f["delta"]),
+                                   _d(eps) if eps is not None else None, f.get("eps_scalar", 0.0),
+                                   n, m, m, _d(x))
+        return x
+
+    # -- checks ---------------------------------------------------------------
+    def tri_residual(self, sub, diag, sup, x, rhs, cyclic=False) -> float:
+        n = len(diag)
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        rhs = np.ascontiguousarray(rhs, dtype=np.float64)
+        out = np.zeros(1)
+        st = self.lib.oracle_tri_residual(_d(_arr(sub, n)), _d(_arr(diag, n)), _d(_arr(sup, n)), n,
+                                          int(cyclic), x.shape[1], _d(x), _d(rhs), _d(out))
+        if st:
+            raise OracleError(st)
+        return float(out[0])
+
+    def pent_residual(self, a, b, c, d, e, x, rhs, cyclic=False) -> float:
+        n = len(c)
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        rhs = np.ascontiguousarray(rhs, dtype=np.float64)
+        out = np.zeros(1)
+        st = self.lib.oracle_pent_residual(*[_d(_arr(v, n)) for v in (a, b, c, d, e)], n, int(cyclic),
+                                           x.shape[1], _d(x), _d(rhs), _d(out))
+        if st:
+            raise OracleError(st)
+        return float(out[0])
+
+    def max_error_vs_dense(self, dense: np.ndarray, x, rhs) -> float:
+        dense = np.ascontiguousarray(dense, dtype=np.float64)
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        rhs = np.ascontiguousarray(rhs, dtype=np.float64)
+        n = dense.shape[0]
+        out = np.zeros(1)
+        st = self.lib.oracle_max_error_vs_dense(_d(dense), n, x.shape[1], _d(x), _d(rhs), _d(out))
+        if st:
+            raise OracleError(st)
+        return float(out[0])
+
+    def rhs(self, seed: int, n: int, m: int, j_offset: int = 0) -> np.ndarray:
+        x = np.empty((n, m))
+        self.lib.oracle_fill_rhs(seed, n, m, j_offset, m, _d(x))
+        return x
+
+
+def dense_from_tri(sub, diag, sup) -> np.ndarray:
+    """tests/support/oracles.cpp:59-67 (banded -> dense)."""
+    n = len(diag)
+    a = np.zeros((n, n))
+    for i in range(n):
+        a[i, i] = diag[i]
+        if i > 0:
+            a[i, i - 1] = sub[i]
+        if i + 1 < n:
+            a[i, i + 1] = sup[i]
+    return a
+
+
+def dense_from_pent(a_, b_, c_, d_, e_) -> np.ndarray:
+    """tests/support/oracles.cpp:69-79."""
+    n = len(c_)
+    a = np.zeros((n, n))
+    for i in range(n):
+        a[i, i] = c_[i]
+        if i >= 2:
+            a[i, i - 2] = a_[i]
+        if i >= 1:
+            a[i, i - 1] = b_[i]
+        if i + 1 < n:
+            a[i, i + 1] = d_[i]
+        if i + 2 < n:
+            a[i, i + 2] = e_[i]
+    return a
+
+
+def per_system_max_rel(x: np.ndarray, ref: np.ndarray) -> float:
+    """max_j ||x_j - ref_j||_inf / ||ref_j||_inf (oracles.cpp:104-122 metric)."""
+    x = np.asarray(x, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    err = np.abs(x - ref).max(axis=0)
+    scale = np.abs(ref).max(axis=0)
+    rel = np.where(scale > 0, err / np.where(scale > 0, scale, 1.0), err)
+    return float(rel.max()) if rel.size else 0.0
+
+
+def bitwise_equal(x: np.ndarray, y: np.ndarray) -> bool:
+    """Bit-for-bit equality, treating any NaN as equal to any NaN."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    if x.shape != y.shape:
+        return False
+    same = x.view(np.uint64) == y.view(np.uint64)
+    both_nan = np.isnan(x) & np.isnan(y)
+    return bool(np.all(same | both_nan))

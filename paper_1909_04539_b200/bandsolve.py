@@ -1,0 +1,389 @@
+"""ctypes binding of the bandsolve C ABI (include/bandsolve.h).
+
+The same classes drive either the B200 library (libbandsolve_b200.so, the
+default) or any other library exporting the reference ABI
+(/root/reference/proj/include/bandsolve.h) — tests and the bench's reference
+arm point it at the reference build. Names follow the C entry points; every
+non-OK status raises BandsolveError carrying the status and the library's
+last-error text, the Python rendering of the reference's status returns
+(capi.cpp:38-72).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+PKG_DIR = os.path.dirname(os.path.abspath(__file__))
+DEFAULT_LIB = os.path.join(PKG_DIR, "libbandsolve_b200.so")
+
+OK = 0
+ERR_BAD_ARG = 1
+ERR_SHAPE_MISMATCH = 2
+ERR_FACTORIZATION_BREAKDOWN = 3
+ERR_DIVISION_BY_ZERO = 4
+ERR_SINGULAR_CORRECTION = 5
+ERR_SINGULAR_MATRIX = 6
+ERR_BAD_FORMAT = 7
+ERR_IO = 8
+ERR_INTERNAL = 9
+
+MODE_EXACT = 0
+MODE_FAST = 1
+
+KIND_TRI = 0
+KIND_PENT = 1
+KIND_UNIFORM = 2
+
+_dp = C.POINTER(C.c_double)
+_fp = C.POINTER(C.c_float)
+_vp = C.c_void_p
+_sz = C.c_size_t
+_st = C.c_int
+
+# (name, restype, argtypes) of the reference ABI subset (ref bandsolve.h)
+_REFERENCE_SIGS = [
+    ("bandsolve_status_string", C.c_char_p, [_st]),
+    ("bandsolve_version", C.c_char_p, []),
+    ("bandsolve_get_threads", C.c_int, []),
+    ("bandsolve_set_threads", None, [C.c_int]),
+    ("bandsolve_batch_create", _st, [_sz, _sz, C.POINTER(_vp)]),
+    ("bandsolve_batch_destroy", None, [_vp]),
+    ("bandsolve_batch_rows", _sz, [_vp]),
+    ("bandsolve_batch_systems", _sz, [_vp]),
+    ("bandsolve_batch_data", _dp, [_vp]),
+    ("bandsolve_batch_data_const", _dp, [_vp]),
+    ("bandsolve_tri_factor_create", _st, [_dp, _dp, _dp, _sz, C.POINTER(_vp)]),
+    ("bandsolve_tri_factor_destroy", None, [_vp]),
+    ("bandsolve_tri_solve_shared", _st, [_vp, _vp]),
+    ("bandsolve_pent_factor_create", _st, [_dp, _dp, _dp, _dp, _dp, _sz, C.POINTER(_vp)]),
+    ("bandsolve_pent_factor_destroy", None, [_vp]),
+    ("bandsolve_pent_solve_shared", _st, [_vp, _vp]),
+    ("bandsolve_uniform_pent_factor_create", _st,
+     [C.c_double] * 5 + [_sz, C.POINTER(_vp)]),
+    ("bandsolve_uniform_pent_factor_destroy", None, [_vp]),
+    ("bandsolve_pent_solve_uniform", _st, [_vp, _vp]),
+    ("bandsolve_tri_residual", _st, [_dp, _dp, _dp, _sz, C.c_int, _vp, _vp, _dp]),
+    ("bandsolve_pent_residual", _st, [_dp] * 5 + [_sz, C.c_int, _vp, _vp, _dp]),
+]
+
+# B200 extensions (include/bandsolve.h, second part)
+_EXTENSION_SIGS = [
+    ("bandsolve_set_mode", _st, [C.c_int]),
+    ("bandsolve_get_mode", C.c_int, []),
+    ("bandsolve_tri_solve_shared_dev", _st, [_vp, _vp, _sz, _sz, _sz, _vp]),
+    ("bandsolve_tri_solve_shared_dev_f32", _st, [_vp, _vp, _sz, _sz, _sz, _vp]),
+    ("bandsolve_pent_solve_shared_dev", _st, [_vp, _vp, _sz, _sz, _sz, _vp]),
+    ("bandsolve_pent_solve_shared_dev_f32", _st, [_vp, _vp, _sz, _sz, _sz, _vp]),
+    ("bandsolve_pent_solve_uniform_dev", _st, [_vp, _vp, _sz, _sz, _sz, _vp]),
+    ("bandsolve_pent_solve_uniform_dev_f32", _st, [_vp, _vp, _sz, _sz, _sz, _vp]),
+    ("bandsolve_tri_residual_dev", _st,
+     [_dp, _dp, _dp, _sz, C.c_int, _vp, _vp, _sz, _sz, _vp, _dp]),
+    ("bandsolve_pent_residual_dev", _st,
+     [_dp] * 5 + [_sz, C.c_int, _vp, _vp, _sz, _sz, _vp, _dp]),
+    ("bandsolve_fill_rhs_dev", _st, [_vp, _sz, _sz, _sz, C.c_uint64, C.c_uint64, _vp]),
+    ("bandsolve_fill_rhs_dev_f32", _st, [_vp, _sz, _sz, _sz, C.c_uint64, C.c_uint64, _vp]),
+    ("bandsolve_tri_factor_order", _sz, [_vp]),
+    ("bandsolve_tri_factor_arrays", _st, [_vp, _dp, _dp, _dp]),
+    ("bandsolve_pent_factor_order", _sz, [_vp]),
+    ("bandsolve_pent_factor_arrays", _st, [_vp, _dp, _dp, _dp, _dp, _dp]),
+    ("bandsolve_uniform_pent_factor_order", _sz, [_vp]),
+    ("bandsolve_uniform_pent_factor_arrays", _st, [_vp, _dp, _dp, _dp, _dp, _dp]),
+    ("bandsolve_describe_plan", _st, [C.c_int, _sz, _sz, _sz, C.c_int, C.c_char_p, _sz]),
+    ("bandsolve_kernel_launches", C.c_uint64, []),
+    ("bandsolve_last_error", C.c_char_p, []),
+]
+
+REFERENCE_SYMBOLS = [s[0] for s in _REFERENCE_SIGS]
+EXTENSION_SYMBOLS = [s[0] for s in _EXTENSION_SIGS]
+
+
+class BandsolveError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"{message} (status {status})")
+        self.status = status
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(_dp)
+
+
+def _f64(v, n: Optional[int] = None) -> np.ndarray:
+    a = np.ascontiguousarray(np.asarray(v, dtype=np.float64))
+    if n is not None and a.shape != (n,):
+        raise ValueError(f"band must have length {n}")
+    return a
+
+
+class Library:
+    """One loaded bandsolve-ABI shared library."""
+
+    def __init__(self, path: str = DEFAULT_LIB, mode: int = C.RTLD_LOCAL):
+        if not os.path.exists(path):
+            raise FileNotFoundError(
+                f"{path} is missing: build it first (python -c 'import __graft_entry__ as g; g.build()')")
+        self.path = path
+        self.lib = C.CDLL(path, mode=mode)
+        for name, res, args in _REFERENCE_SIGS:
+            fn = getattr(self.lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        self.has_extensions = hasattr(self.lib, "bandsolve_set_mode")
+        if self.has_extensions:
+            for name, res, args in _EXTENSION_SIGS:
+                fn = getattr(self.lib, name)
+                fn.restype = res
+                fn.argtypes = args
+
+    # -- status plumbing ----------------------------------------------------
+    def check(self, status: int, what: str = "") -> None:
+        if status != OK:
+            msg = self.lib.bandsolve_status_string(status).decode()
+            if self.has_extensions:
+                detail = self.lib.bandsolve_last_error().decode()
+                if detail:
+                    msg = f"{msg}: {detail}"
+            raise BandsolveError(status, f"{what}: {msg}" if what else msg)
+
+    def status_string(self, status: int) -> str:
+        return self.lib.bandsolve_status_string(status).decode()
+
+    def version(self) -> str:
+        return self.lib.bandsolve_version().decode()
+
+    def get_threads(self) -> int:
+        return self.lib.bandsolve_get_threads()
+
+    def set_threads(self, n: int) -> None:
+        self.lib.bandsolve_set_threads(n)
+
+    # -- extensions ---------------------------------------------------------
+    def set_mode(self, mode: int) -> None:
+        self.check(self.lib.bandsolve_set_mode(mode), "set_mode")
+
+    def get_mode(self) -> int:
+        return self.lib.bandsolve_get_mode()
+
+    def kernel_launches(self) -> int:
+        return int(self.lib.bandsolve_kernel_launches())
+
+    def describe_plan(self, kind: int, n: int, m: int, ld: Optional[int] = None, f32: bool = False) -> str:
+        buf = C.create_string_buffer(256)
+        self.check(self.lib.bandsolve_describe_plan(kind, n, m, ld if ld is not None else m,
+                                                    int(f32), buf, 256), "describe_plan")
+        return buf.value.decode()
+
+    def fill_rhs_dev(self, ptr: int, n: int, m: int, ld: int, seed: int, j_offset: int = 0,
+                     stream: int = 0, f32: bool = False) -> None:
+        fn = self.lib.bandsolve_fill_rhs_dev_f32 if f32 else self.lib.bandsolve_fill_rhs_dev
+        self.check(fn(ptr, n, m, ld, seed, j_offset, stream), "fill_rhs_dev")
+
+    # -- residuals ----------------------------------------------------------
+    def tri_residual(self, sub, diag, sup, x: "Batch", rhs: "Batch", cyclic: bool = False) -> float:
+        n = len(diag)
+        s, d, u = _f64(sub, n), _f64(diag, n), _f64(sup, n)
+        out = C.c_double(-1.0)
+        self.check(self.lib.bandsolve_tri_residual(_dptr(s), _dptr(d), _dptr(u), n, int(cyclic),
+                                                   x.handle, rhs.handle, C.byref(out)), "tri_residual")
+        return out.value
+
+    def pent_residual(self, a, b, c, d, e, x: "Batch", rhs: "Batch", cyclic: bool = False) -> float:
+        n = len(c)
+        bands = [_f64(v, n) for v in (a, b, c, d, e)]
+        out = C.c_double(-1.0)
+        self.check(self.lib.bandsolve_pent_residual(*[_dptr(v) for v in bands], n, int(cyclic),
+                                                    x.handle, rhs.handle, C.byref(out)), "pent_residual")
+        return out.value
+
+    def tri_residual_dev(self, sub, diag, sup, x_ptr: int, rhs_ptr: int, m: int, ld: int,
+                         cyclic: bool = False, stream: int = 0) -> float:
+        n = len(diag)
+        s, d, u = _f64(sub, n), _f64(diag, n), _f64(sup, n)
+        out = C.c_double(-1.0)
+        self.check(self.lib.bandsolve_tri_residual_dev(_dptr(s), _dptr(d), _dptr(u), n, int(cyclic),
+                                                       x_ptr, rhs_ptr, m, ld, stream, C.byref(out)),
+                   "tri_residual_dev")
+        return out.value
+
+    def pent_residual_dev(self, a, b, c, d, e, x_ptr: int, rhs_ptr: int, m: int, ld: int,
+                          cyclic: bool = False, stream: int = 0) -> float:
+        n = len(c)
+        bands = [_f64(v, n) for v in (a, b, c, d, e)]
+        out = C.c_double(-1.0)
+        self.check(self.lib.bandsolve_pent_residual_dev(*[_dptr(v) for v in bands], n, int(cyclic),
+                                                        x_ptr, rhs_ptr, m, ld, stream, C.byref(out)),
+                   "pent_residual_dev")
+        return out.value
+
+
+class Batch:
+    """Owning bandsolve_batch handle with a numpy (n, m) view of its data."""
+
+    def __init__(self, lib: Library, n: int, m: int):
+        self.lib = lib
+        h = _vp()
+        lib.check(lib.lib.bandsolve_batch_create(n, m, C.byref(h)), "batch_create")
+        self.handle = h
+        self.n, self.m = n, m
+        ptr = lib.lib.bandsolve_batch_data(h)
+        self.array = np.ctypeslib.as_array(ptr, shape=(n, m))
+
+    @classmethod
+    def from_array(cls, lib: Library, arr) -> "Batch":
+        a = np.asarray(arr, dtype=np.float64)
+        if a.ndim == 1:
+            a = a.reshape(-1, 1)
+        b = cls(lib, a.shape[0], a.shape[1])
+        b.array[...] = a
+        return b
+
+    def rows(self) -> int:
+        return self.lib.lib.bandsolve_batch_rows(self.handle)
+
+    def systems(self) -> int:
+        return self.lib.lib.bandsolve_batch_systems(self.handle)
+
+    def close(self) -> None:
+        if self.handle:
+            self.lib.lib.bandsolve_batch_destroy(self.handle)
+            self.handle = None
+            self.array = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class _Factor:
+    _destroy = ""
+    _solve = ""
+    _solve_dev = ""
+    _order = ""
+
+    def __init__(self, lib: Library, handle: _vp, n: int):
+        self.lib, self.handle, self.n = lib, handle, n
+
+    def solve(self, batch: Batch) -> None:
+        self.lib.check(getattr(self.lib.lib, self._solve)(self.handle, batch.handle), self._solve)
+
+    def solve_dev(self, ptr: int, n: int, m: int, ld: Optional[int] = None, stream: int = 0,
+                  f32: bool = False) -> None:
+        name = self._solve_dev + ("_f32" if f32 else "")
+        self.lib.check(getattr(self.lib.lib, name)(self.handle, ptr, n, m, m if ld is None else ld, stream),
+                       name)
+
+    def close(self) -> None:
+        if self.handle:
+            getattr(self.lib.lib, self._destroy)(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class TriFactor(_Factor):
+    """bandsolve_tri_factor (ref bandsolve.h:67-78)."""
+    _destroy = "bandsolve_tri_factor_destroy"
+    _solve = "bandsolve_tri_solve_shared"
+    _solve_dev = "bandsolve_tri_solve_shared_dev"
+
+    def __init__(self, lib: Library, sub, diag, sup):
+        n = len(diag)
+        s, d, u = _f64(sub, n), _f64(diag, n), _f64(sup, n)
+        h = _vp()
+        lib.check(lib.lib.bandsolve_tri_factor_create(_dptr(s), _dptr(d), _dptr(u), n, C.byref(h)),
+                  "tri_factor_create")
+        super().__init__(lib, h, n)
+
+    def arrays(self) -> dict:
+        out = {k: np.empty(self.n) for k in ("chat", "inv_denom", "sub")}
+        self.lib.check(self.lib.lib.bandsolve_tri_factor_arrays(
+            self.handle, _dptr(out["chat"]), _dptr(out["inv_denom"]), _dptr(out["sub"])), "tri_factor_arrays")
+        return out
+
+
+class PentFactor(_Factor):
+    """bandsolve_pent_factor (ref bandsolve.h:91-100)."""
+    _destroy = "bandsolve_pent_factor_destroy"
+    _solve = "bandsolve_pent_solve_shared"
+    _solve_dev = "bandsolve_pent_solve_shared_dev"
+
+    def __init__(self, lib: Library, a, b, c, d, e):
+        n = len(c)
+        bands = [_f64(v, n) for v in (a, b, c, d, e)]
+        h = _vp()
+        lib.check(lib.lib.bandsolve_pent_factor_create(*[_dptr(v) for v in bands], n, C.byref(h)),
+                  "pent_factor_create")
+        super().__init__(lib, h, n)
+
+    def arrays(self) -> dict:
+        keys = ("inv_alpha", "beta", "gamma", "delta", "epsilon")
+        out = {k: np.empty(self.n) for k in keys}
+        self.lib.check(self.lib.lib.bandsolve_pent_factor_arrays(self.handle, *[_dptr(out[k]) for k in keys]),
+                       "pent_factor_arrays")
+        return out
+
+
+class UniformPentFactor(_Factor):
+    """bandsolve_uniform_pent_factor (ref bandsolve.h:105-113)."""
+    _destroy = "bandsolve_uniform_pent_factor_destroy"
+    _solve = "bandsolve_pent_solve_uniform"
+    _solve_dev = "bandsolve_pent_solve_uniform_dev"
+
+    def __init__(self, lib: Library, a: float, b: float, c: float, d: float, e: float, n: int):
+        h = _vp()
+        lib.check(lib.lib.bandsolve_uniform_pent_factor_create(a, b, c, d, e, n, C.byref(h)),
+                  "uniform_pent_factor_create")
+        super().__init__(lib, h, n)
+
+    def arrays(self) -> dict:
+        keys = ("inv_alpha", "beta", "gamma", "delta")
+        out = {k: np.empty(self.n) for k in keys}
+        eps = C.c_double()
+        self.lib.check(self.lib.lib.bandsolve_uniform_pent_factor_arrays(
+            self.handle, *[_dptr(out[k]) for k in keys], C.byref(eps)), "uniform_pent_factor_arrays")
+        out["eps_scalar"] = eps.value
+        return out
+
+
+# ---- LHS definitions used by the configs (ref pde.cpp:62-71) ---------------
+def diffusion_bands(sigma: float, n: int):
+    """Crank-Nicolson diffusion LHS (-s, 1+2s, -s), structural zeros applied."""
+    sub = np.full(n, -sigma)
+    diag = np.full(n, 1.0 + 2.0 * sigma)
+    sup = np.full(n, -sigma)
+    sub[0] = 0.0
+    sup[-1] = 0.0
+    return sub, diag, sup
+
+
+def hyper_bands(sigma: float, n: int):
+    """Crank-Nicolson hyperdiffusion LHS (s, -4s, 1+6s, -4s, s)."""
+    a = np.full(n, sigma)
+    b = np.full(n, -4.0 * sigma)
+    c = np.full(n, 1.0 + 6.0 * sigma)
+    d = np.full(n, -4.0 * sigma)
+    e = np.full(n, sigma)
+    a[0] = a[1] = b[0] = 0.0
+    d[-1] = e[-1] = e[-2] = 0.0
+    return a, b, c, d, e
+
+
+_default: Optional[Library] = None
+
+
+def load(path: Optional[str] = None) -> Library:
+    """The B200 library (cached). Raises if the .so has not been built."""
+    global _default
+    if path is not None:
+        return Library(path)
+    if _default is None:
+        _default = Library(DEFAULT_LIB)
+    return _default

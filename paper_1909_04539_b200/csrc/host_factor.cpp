@@ -1,0 +1,168 @@
+// Host-side LHS validation and one-time prefactorisation.
+//
+// This is the "factorise once on the host" half of the hot path
+// (SURVEY.md §8a rows a1/a2/a4/a5/a7). It must reproduce the reference's
+// factor arrays bit for bit, so it follows the reference's evaluation order
+// exactly and this translation unit is compiled with -ffp-contract=off and
+// without -march (no FMA contraction): every expression below is one
+// IEEE-754 binary64 rounding per operator, left to right.
+#include <cmath>
+#include <cstring>
+
+#include "internal.hpp"
+
+namespace bsb {
+
+namespace {
+
+bool all_finite(const double* v, std::size_t n) {
+  for (std::size_t i = 0; i < n; ++i)
+    if (!std::isfinite(v[i])) return false;
+  return true;
+}
+
+// banded.cpp:32-36: the negated comparison also rejects NaN pivots.
+bool pivot_ok(double denom) { return std::abs(denom) >= kBreakdownEps; }
+
+}  // namespace
+
+bandsolve_status validate_tri_bands(const double* sub, const double* diag,
+                                    const double* sup, std::size_t n) {
+  // tri_lhs::tri_lhs, banded.cpp:40-57
+  if (n < 2) return fail(BANDSOLVE_ERR_BAD_ARG, "tridiagonal system needs n >= 2");
+  if (!all_finite(sub, n) || !all_finite(diag, n) || !all_finite(sup, n))
+    return fail(BANDSOLVE_ERR_BAD_ARG, "non-finite entry in a tridiagonal band");
+  if (sub[0] != 0.0 || sup[n - 1] != 0.0)
+    return fail(BANDSOLVE_ERR_BAD_ARG, "structural band slot must be zero: sub[0] / sup[n-1]");
+  return BANDSOLVE_OK;
+}
+
+bandsolve_status validate_pent_bands(const double* a, const double* b,
+                                     const double* c, const double* d,
+                                     const double* e, std::size_t n) {
+  // pent_lhs::pent_lhs, banded.cpp:88-116
+  if (n < 5) return fail(BANDSOLVE_ERR_BAD_ARG, "pentadiagonal system needs n >= 5");
+  if (!all_finite(a, n) || !all_finite(b, n) || !all_finite(c, n) ||
+      !all_finite(d, n) || !all_finite(e, n))
+    return fail(BANDSOLVE_ERR_BAD_ARG, "non-finite entry in a pentadiagonal band");
+  if (a[0] != 0.0 || a[1] != 0.0 || b[0] != 0.0 || d[n - 1] != 0.0 ||
+      e[n - 1] != 0.0 || e[n - 2] != 0.0)
+    return fail(BANDSOLVE_ERR_BAD_ARG,
+                "structural band slot must be zero: a[0], a[1], b[0], d[n-1], e[n-1], e[n-2]");
+  return BANDSOLVE_OK;
+}
+
+bandsolve_status make_tri_factor(const double* sub, const double* diag,
+                                 const double* sup, std::size_t n,
+                                 std::unique_ptr<Factor>& out) {
+  bandsolve_status st = validate_tri_bands(sub, diag, sup, n);
+  if (st != BANDSOLVE_OK) return st;
+  auto f = std::make_unique<Factor>();
+  f->kind = Kind::Tri;
+  f->n = n;
+  f->chat.assign(n, 0.0);
+  f->inv_denom.assign(n, 0.0);
+  f->sub.assign(sub, sub + n);  // banded.cpp:73: the factor keeps a copy of a_i
+
+  // banded.cpp:75-84. chat is sup / denom (a division, not sup * inv), and
+  // the last chat slot stays zero.
+  double denom = diag[0];
+  if (!pivot_ok(denom))
+    return fail(BANDSOLVE_ERR_FACTORIZATION_BREAKDOWN, "zero pivot at row 0");
+  f->inv_denom[0] = 1.0 / denom;
+  f->chat[0] = sup[0] / denom;
+  for (std::size_t i = 1; i < n; ++i) {
+    denom = diag[i] - sub[i] * f->chat[i - 1];
+    if (!pivot_ok(denom))
+      return fail(BANDSOLVE_ERR_FACTORIZATION_BREAKDOWN,
+                  "zero pivot at row " + std::to_string(i));
+    f->inv_denom[i] = 1.0 / denom;
+    if (i + 1 < n) f->chat[i] = sup[i] / denom;
+  }
+  out = std::move(f);
+  return BANDSOLVE_OK;
+}
+
+bandsolve_status make_pent_factor(const double* a, const double* b,
+                                  const double* c, const double* d,
+                                  const double* e, std::size_t n,
+                                  std::unique_ptr<Factor>& out) {
+  bandsolve_status st = validate_pent_bands(a, b, c, d, e, n);
+  if (st != BANDSOLVE_OK) return st;
+  auto f = std::make_unique<Factor>();
+  f->kind = Kind::Pent;
+  f->n = n;
+  f->inv_alpha.assign(n, 0.0);
+  f->beta.assign(n, 0.0);
+  f->gamma.assign(n, 0.0);
+  f->delta.assign(n, 0.0);
+  f->epsilon.assign(a, a + n);  // banded.cpp:137: epsilon is a verbatim copy of a
+  std::vector<double> alpha(n, 0.0);
+  auto& be = f->beta;
+  auto& ga = f->gamma;
+  auto& de = f->delta;
+
+  auto breakdown = [](std::size_t row) {
+    return fail(BANDSOLVE_ERR_FACTORIZATION_BREAKDOWN,
+                "zero alpha at row " + std::to_string(row));
+  };
+
+  // The fourteen steps of PAPER.md:461-482 as banded.cpp:141-172 orders them.
+  alpha[0] = c[0];
+  if (!pivot_ok(alpha[0])) return breakdown(0);
+  ga[0] = d[0] / alpha[0];
+  de[0] = e[0] / alpha[0];
+
+  be[1] = b[1];
+  alpha[1] = c[1] - be[1] * ga[0];
+  if (!pivot_ok(alpha[1])) return breakdown(1);
+  ga[1] = (d[1] - be[1] * de[0]) / alpha[1];
+  de[1] = e[1] / alpha[1];
+
+  for (std::size_t i = 2; i + 2 < n; ++i) {
+    be[i] = b[i] - a[i] * ga[i - 2];
+    alpha[i] = c[i] - a[i] * de[i - 2] - be[i] * ga[i - 1];
+    if (!pivot_ok(alpha[i])) return breakdown(i);
+    ga[i] = (d[i] - be[i] * de[i - 1]) / alpha[i];
+    de[i] = e[i] / alpha[i];
+  }
+  {
+    const std::size_t i = n - 2;  // no delta in the second-to-last row
+    be[i] = b[i] - a[i] * ga[i - 2];
+    alpha[i] = c[i] - a[i] * de[i - 2] - be[i] * ga[i - 1];
+    if (!pivot_ok(alpha[i])) return breakdown(i);
+    ga[i] = (d[i] - be[i] * de[i - 1]) / alpha[i];
+  }
+  {
+    const std::size_t i = n - 1;  // neither gamma nor delta in the last row
+    be[i] = b[i] - a[i] * ga[i - 2];
+    alpha[i] = c[i] - a[i] * de[i - 2] - be[i] * ga[i - 1];
+    if (!pivot_ok(alpha[i])) return breakdown(i);
+  }
+  // banded.cpp:174: only the reciprocal of alpha is stored.
+  for (std::size_t i = 0; i < n; ++i) f->inv_alpha[i] = 1.0 / alpha[i];
+  out = std::move(f);
+  return BANDSOLVE_OK;
+}
+
+bandsolve_status make_uniform_factor(double a, double b, double c, double d,
+                                     double e, std::size_t n,
+                                     std::unique_ptr<Factor>& out) {
+  // pent_solver.cpp:99-111: expand to constant bands with the structural
+  // zeros of constant_pent_lhs (banded.cpp:118-125), factor, keep a scalar.
+  if (n < 5) return fail(BANDSOLVE_ERR_BAD_ARG, "pentadiagonal system needs n >= 5");
+  std::vector<double> av(n, a), bv(n, b), cv(n, c), dv(n, d), ev(n, e);
+  av[0] = av[1] = bv[0] = 0.0;
+  dv[n - 1] = ev[n - 1] = ev[n - 2] = 0.0;
+  std::unique_ptr<Factor> f;
+  bandsolve_status st =
+      make_pent_factor(av.data(), bv.data(), cv.data(), dv.data(), ev.data(), n, f);
+  if (st != BANDSOLVE_OK) return st;
+  f->kind = Kind::Uniform;
+  f->eps_scalar = a;
+  f->epsilon.clear();  // 4N + 1 stored reals (pent_solver.hpp:29-38)
+  out = std::move(f);
+  return BANDSOLVE_OK;
+}
+
+}  // namespace bsb

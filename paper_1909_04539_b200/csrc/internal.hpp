@@ -1,0 +1,104 @@
+// Internal interfaces of libbandsolve_b200: host factor objects, the device
+// launch layer and the thread-local error channel. Nothing here is exported;
+// the C ABI lives in capi.cpp.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/bandsolve.h"
+
+namespace bsb {
+
+// common.hpp:17 — pivots with |denom| < 1e-300 are a breakdown.
+inline constexpr double kBreakdownEps = 1e-300;
+
+enum class Kind { Tri = 0, Pent = 1, Uniform = 2 };
+
+// Device copies of one factor on one device (see solve.cu for the packed
+// record layouts). One allocation holds all four variants
+// {exact, fast} x {f64, f32}.
+struct DeviceFactor {
+  int device = -1;
+  void* base = nullptr;
+  const void* fwd[2][2] = {};  // [f32][fast]
+  const void* bwd[2][2] = {};
+};
+
+// Host factor: the reference's factor arrays, computed once on the host in
+// the reference's operation order (banded.cpp:67-86, :127-176,
+// pent_solver.cpp:99-111), plus a lazily filled per-device cache.
+struct Factor {
+  Kind kind = Kind::Tri;
+  std::size_t n = 0;
+  // tri_factor fields (banded.hpp:48-53)
+  std::vector<double> chat, inv_denom, sub;
+  // pent_factor / uniform_pent_factor fields (banded.hpp:88-95)
+  std::vector<double> inv_alpha, beta, gamma, delta, epsilon;
+  double eps_scalar = 0.0;
+
+  mutable std::mutex mu;
+  mutable std::vector<DeviceFactor> devices;  // one entry per touched device
+  ~Factor();
+};
+
+// ---- host prefactor (host_factor.cpp) ------------------------------------
+bandsolve_status make_tri_factor(const double* sub, const double* diag,
+                                 const double* sup, std::size_t n,
+                                 std::unique_ptr<Factor>& out);
+bandsolve_status make_pent_factor(const double* a, const double* b,
+                                  const double* c, const double* d,
+                                  const double* e, std::size_t n,
+                                  std::unique_ptr<Factor>& out);
+bandsolve_status make_uniform_factor(double a, double b, double c, double d,
+                                     double e, std::size_t n,
+                                     std::unique_ptr<Factor>& out);
+// Band validation shared with the residual entry points
+// (banded.cpp:40-57, :88-116).
+bandsolve_status validate_tri_bands(const double* sub, const double* diag,
+                                    const double* sup, std::size_t n);
+bandsolve_status validate_pent_bands(const double* a, const double* b,
+                                     const double* c, const double* d,
+                                     const double* e, std::size_t n);
+
+// ---- device layer (solve.cu) ---------------------------------------------
+int current_mode();
+void set_mode(int mode);
+
+// Enqueue an in-place solve of the n x m (pitch ld) device array x.
+bandsolve_status solve_device(const Factor& f, void* x, bool f32,
+                              std::size_t n, std::size_t m, std::size_t ld,
+                              void* stream);
+// Host batch: staged through the device, synchronous.
+bandsolve_status solve_host(const Factor& f, double* x, std::size_t n,
+                            std::size_t m);
+// Residual kernels; bands are host arrays of length n (5 for pent).
+bandsolve_status residual_device(Kind kind, const double* const* bands,
+                                 std::size_t n, int cyclic, const double* x,
+                                 const double* rhs, std::size_t m,
+                                 std::size_t ld, void* stream, double* out);
+bandsolve_status residual_host(Kind kind, const double* const* bands,
+                               std::size_t n, int cyclic, const double* x,
+                               const double* rhs, std::size_t m, double* out);
+bandsolve_status fill_rhs_device(void* x, bool f32, std::size_t n,
+                                 std::size_t m, std::size_t ld, uint64_t seed,
+                                 uint64_t j_offset, void* stream);
+bandsolve_status describe_plan(Kind kind, std::size_t n, std::size_t m,
+                               std::size_t ld, bool f32, std::string& out);
+void release_device_factor(DeviceFactor& d);
+uint64_t kernel_launches();
+
+// Page-locked host allocation when a driver is present, else calloc.
+double* host_alloc_zeroed(std::size_t count, bool* pinned);
+void host_free(double* p, bool pinned);
+
+// ---- errors ----------------------------------------------------------------
+bandsolve_status fail(bandsolve_status st, const std::string& msg);
+const char* last_error();
+void clear_error();
+
+}  // namespace bsb

@@ -1,0 +1,685 @@
+// Device layer of libbandsolve_b200: factor upload, kernel plans, launches,
+// the staged host-batch pipeline, residual and synthetic-RHS kernels.
+#include <cudaTypedefs.h>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <climits>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.hpp"
+#include "sweep_kernels.cuh"
+
+namespace bsb {
+
+namespace {
+
+std::atomic<uint64_t> g_launches{0};
+std::atomic<int> g_mode{-1};
+
+int mode_from_env() {
+  const char* e = std::getenv("BANDSOLVE_MODE");
+  if (e && (std::strcmp(e, "fast") == 0 || std::strcmp(e, "FAST") == 0 || std::strcmp(e, "1") == 0))
+    return BANDSOLVE_MODE_FAST;
+  return BANDSOLVE_MODE_EXACT;
+}
+
+bandsolve_status cuda_fail(cudaError_t err, const char* what) {
+  return fail(BANDSOLVE_ERR_INTERNAL,
+              std::string(what) + ": " + cudaGetErrorName(err) + " (" + cudaGetErrorString(err) + ")");
+}
+
+#define BSB_CUDA(call)                                  \
+  do {                                                  \
+    cudaError_t err_ = (call);                          \
+    if (err_ != cudaSuccess) return cuda_fail(err_, #call); \
+  } while (0)
+
+int device_count_cached() {
+  static int count = [] {
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) {
+      cudaGetLastError();
+      return 0;
+    }
+    return c;
+  }();
+  return count;
+}
+
+// ---- packed factor records --------------------------------------------------
+// The signed zeros below make the generic row formulas of sweep_kernels.cuh
+// reproduce the reference's peeled boundary rows exactly:
+//   tri fwd row 0   (tri_solver.cpp:27)  : a_0 = +0        -> (d - (+0)) * m0 = d * m0
+//   tri bwd row n-1 (tri_solver.cpp:39)  : chat_{n-1} = +0 -> dhat - (+0) = dhat
+//   pent fwd rows 0,1 (pent_solver.cpp:19-31): eps_0 = eps_1 = beta_0 = +0
+//   pent bwd row n-1: gamma = delta = +0; row n-2 (pent_solver.cpp:44-50):
+//     exact mode delta_{n-2} = -0 so gamma*x1 + (-0) == gamma*x1 bit for bit.
+template <typename T>
+void pack_tri(const Factor& f, bool fast, std::vector<unsigned char>& fwd, std::vector<unsigned char>& bwd) {
+  const std::size_t n = f.n;
+  fwd.assign(n * sizeof(dev::TriFwd<T>), 0);
+  bwd.assign(n * sizeof(T), 0);
+  auto* rf = reinterpret_cast<dev::TriFwd<T>*>(fwd.data());
+  auto* rb = reinterpret_cast<T*>(bwd.data());
+  for (std::size_t i = 0; i < n; ++i) {
+    const double a = (i == 0) ? 0.0 : f.sub[i];
+    const double m = f.inv_denom[i];
+    rf[i].a = static_cast<T>(fast ? a * m : a);
+    rf[i].m = static_cast<T>(m);
+    rb[i] = static_cast<T>(i + 1 < n ? f.chat[i] : 0.0);
+  }
+}
+
+template <typename T>
+void pack_pent(const Factor& f, bool fast, std::vector<unsigned char>& fwd, std::vector<unsigned char>& bwd) {
+  const std::size_t n = f.n;
+  fwd.assign(n * sizeof(dev::PentFwd<T>), 0);
+  bwd.assign(n * sizeof(dev::PentBwd<T>), 0);
+  auto* rf = reinterpret_cast<dev::PentFwd<T>*>(fwd.data());
+  auto* rb = reinterpret_cast<dev::PentBwd<T>*>(bwd.data());
+  const bool uniform = f.kind == Kind::Uniform;
+  for (std::size_t i = 0; i < n; ++i) {
+    const double ia = f.inv_alpha[i];
+    // pent_solver.cpp:33: eps_i is read only for i >= 2 (scalar for uniform, :115)
+    const double e = (i < 2) ? 0.0 : (uniform ? f.eps_scalar : f.epsilon[i]);
+    const double b = (i == 0) ? 0.0 : f.beta[i];
+    rf[i].e = static_cast<T>(fast ? e * ia : e);
+    rf[i].b = static_cast<T>(fast ? b * ia : b);
+    rf[i].ia = static_cast<T>(ia);
+    rf[i].pad = T(0);
+    const double g = (i + 1 < n) ? f.gamma[i] : 0.0;
+    double d;
+    if (i + 2 < n) d = f.delta[i];
+    else if (i + 2 == n) d = fast ? 0.0 : -0.0;
+    else d = 0.0;
+    rb[i].g = static_cast<T>(g);
+    rb[i].d = static_cast<T>(d);
+  }
+}
+
+bandsolve_status ensure_device_factor(const Factor& f, int device, const DeviceFactor** out) {
+  std::lock_guard<std::mutex> lock(f.mu);
+  for (const DeviceFactor& d : f.devices) {
+    if (d.device == device) {
+      *out = &d;
+      return BANDSOLVE_OK;
+    }
+  }
+  // four variants {f64, f32} x {exact, fast}, each a fwd and a bwd array
+  std::vector<unsigned char> fw[2][2], bw[2][2];
+  for (int fast = 0; fast < 2; ++fast) {
+    if (f.kind == Kind::Tri) {
+      pack_tri<double>(f, fast, fw[0][fast], bw[0][fast]);
+      pack_tri<float>(f, fast, fw[1][fast], bw[1][fast]);
+    } else {
+      pack_pent<double>(f, fast, fw[0][fast], bw[0][fast]);
+      pack_pent<float>(f, fast, fw[1][fast], bw[1][fast]);
+    }
+  }
+  std::size_t total = 0;
+  std::size_t off_f[2][2], off_b[2][2];
+  auto align256 = [](std::size_t v) { return (v + 255) & ~std::size_t(255); };
+  for (int p = 0; p < 2; ++p)
+    for (int q = 0; q < 2; ++q) {
+      off_f[p][q] = total;
+      total = align256(total + fw[p][q].size());
+      off_b[p][q] = total;
+      total = align256(total + bw[p][q].size());
+    }
+  std::vector<unsigned char> blob(total, 0);
+  for (int p = 0; p < 2; ++p)
+    for (int q = 0; q < 2; ++q) {
+      std::memcpy(blob.data() + off_f[p][q], fw[p][q].data(), fw[p][q].size());
+      std::memcpy(blob.data() + off_b[p][q], bw[p][q].data(), bw[p][q].size());
+    }
+  DeviceFactor d;
+  d.device = device;
+  BSB_CUDA(cudaMalloc(&d.base, total));
+  cudaError_t err = cudaMemcpy(d.base, blob.data(), total, cudaMemcpyHostToDevice);
+  if (err != cudaSuccess) {
+    cudaFree(d.base);
+    return cuda_fail(err, "factor upload");
+  }
+  auto* base = static_cast<unsigned char*>(d.base);
+  for (int p = 0; p < 2; ++p)
+    for (int q = 0; q < 2; ++q) {
+      d.fwd[p][q] = base + off_f[p][q];
+      d.bwd[p][q] = base + off_b[p][q];
+    }
+  f.devices.push_back(d);
+  *out = &f.devices.back();
+  return BANDSOLVE_OK;
+}
+
+// ---- tensor maps --------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      return static_cast<PFN_cuTensorMapEncodeTiled_v12000>(nullptr);
+    }
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+// ---- plans ----------------------------------------------------------------------
+constexpr int kChunkRows = 32;
+constexpr std::size_t kSmemPerSm = 233472;     // 228 KB on sm_100 (measured via cudaGetDeviceProperties)
+constexpr std::size_t kSmemPerBlockMax = 232448;  // 227 KB opt-in
+constexpr std::size_t kSmemReservedPerCta = 1024;
+
+struct Plan {
+  bool smem = false;
+  int W = 0;
+  std::size_t smem_bytes = 0;
+  int ctas_per_sm = 0;
+  std::string why;
+};
+
+std::size_t smem_bytes_for(std::size_t n, int W, std::size_t elem) {
+  const std::size_t chunks = (n + kChunkRows - 1) / kChunkRows;
+  return chunks * kChunkRows * W * elem + chunks * sizeof(uint64_t);
+}
+
+Plan choose_plan(std::size_t n, std::size_t m, std::size_t ld, std::size_t elem, const void* x) {
+  Plan p;
+  const char* force = std::getenv("BANDSOLVE_PLAN");  // "global" | "smem" | "smemW8" | "smemW16" | "smemW32"
+  int forced_w = 0;
+  if (force) {
+    if (std::strcmp(force, "global") == 0) {
+      p.why = "forced global";
+      return p;
+    }
+    if (std::strncmp(force, "smemW", 5) == 0) forced_w = std::atoi(force + 5);
+  }
+  const bool aligned = (reinterpret_cast<uintptr_t>(x) % 16 == 0) && ((ld * elem) % 16 == 0);
+  if (!aligned) {
+    p.why = "row pitch or base not 16-byte aligned (TMA rule)";
+    return p;
+  }
+  if (n > static_cast<std::size_t>(INT_MAX) || m > static_cast<std::size_t>(INT_MAX)) {
+    p.why = "shape beyond 32-bit TMA coordinates";
+    return p;
+  }
+  int best_sys = 0;
+  for (int W : {8, 16, 32}) {
+    if (forced_w && W != forced_w) continue;
+    const std::size_t bytes = smem_bytes_for(n, W, elem);
+    if (bytes > kSmemPerBlockMax) continue;
+    int k = static_cast<int>(kSmemPerSm / (bytes + kSmemReservedPerCta));
+    k = std::min(k, 32);
+    const int sys = k * W;
+    // prefer more systems in flight; on ties the wider (more coalesced) box
+    if (sys > best_sys || (sys == best_sys && W > p.W)) {
+      best_sys = sys;
+      p.smem = true;
+      p.W = W;
+      p.smem_bytes = bytes;
+      p.ctas_per_sm = k;
+    }
+  }
+  if (!p.smem) p.why = "tile does not fit shared memory";
+  return p;
+}
+
+template <typename T, int W, bool PENT, bool FAST>
+cudaError_t launch_smem(const Plan& plan, T* x, int n, long long m, long long ld, const void* fwd,
+                        const void* bwd, cudaStream_t s) {
+  auto kern = dev::sweep_smem<T, W, kChunkRows, PENT, FAST>;
+  static std::atomic<std::size_t> configured{0};
+  if (configured.load(std::memory_order_relaxed) < plan.smem_bytes) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kSmemPerBlockMax));
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared);
+    if (e != cudaSuccess) return e;
+    configured.store(kSmemPerBlockMax, std::memory_order_relaxed);
+  }
+  auto encode = tensor_map_encoder();
+  if (!encode) return cudaErrorNotSupported;
+  CUtensorMap map;
+  const cuuint64_t gdim[2] = {static_cast<cuuint64_t>(m), static_cast<cuuint64_t>(n)};
+  const cuuint64_t gstride[1] = {static_cast<cuuint64_t>(ld) * sizeof(T)};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(W), static_cast<cuuint32_t>(kChunkRows)};
+  const cuuint32_t estride[2] = {1, 1};
+  CUresult r = encode(&map, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                      2, x, gdim, gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  const long long grid = (m + W - 1) / W;
+  kern<<<static_cast<unsigned>(grid), W, plan.smem_bytes, s>>>(map, x, n, m, ld, fwd, bwd);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
+template <typename T, bool PENT, bool FAST>
+cudaError_t launch_global(T* x, int n, long long m, long long ld, const void* fwd, const void* bwd,
+                          cudaStream_t s) {
+  const int threads = 128;
+  const long long grid = (m + threads - 1) / threads;
+  dev::sweep_global<T, PENT, FAST><<<static_cast<unsigned>(grid), threads, 0, s>>>(x, n, m, ld, fwd, bwd);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
+template <typename T, bool PENT, bool FAST>
+cudaError_t dispatch(const Plan& plan, T* x, int n, long long m, long long ld, const void* fwd,
+                     const void* bwd, cudaStream_t s) {
+  if (plan.smem) {
+    switch (plan.W) {
+      case 8: return launch_smem<T, 8, PENT, FAST>(plan, x, n, m, ld, fwd, bwd, s);
+      case 16: return launch_smem<T, 16, PENT, FAST>(plan, x, n, m, ld, fwd, bwd, s);
+      case 32: return launch_smem<T, 32, PENT, FAST>(plan, x, n, m, ld, fwd, bwd, s);
+      default: return cudaErrorInvalidValue;
+    }
+  }
+  return launch_global<T, PENT, FAST>(x, n, m, ld, fwd, bwd, s);
+}
+
+template <typename T>
+cudaError_t dispatch_kind(const Plan& plan, bool pent, bool fast, T* x, int n, long long m, long long ld,
+                          const void* fwd, const void* bwd, cudaStream_t s) {
+  if (pent)
+    return fast ? dispatch<T, true, true>(plan, x, n, m, ld, fwd, bwd, s)
+                : dispatch<T, true, false>(plan, x, n, m, ld, fwd, bwd, s);
+  return fast ? dispatch<T, false, true>(plan, x, n, m, ld, fwd, bwd, s)
+              : dispatch<T, false, false>(plan, x, n, m, ld, fwd, bwd, s);
+}
+
+// ---- residual ---------------------------------------------------------------
+// One thread per system, the reference's accumulation order
+// (tri_solver.cpp:116-136, pent_solver.cpp:223-251) with separately rounded
+// operations, then a max over systems. The per-system value is >= 0 and
+// NaN-free (std::max drops NaNs), so the max can be taken on the bit pattern.
+__device__ __forceinline__ double ref_max(double a, double b) { return (a < b) ? b : a; }
+
+__global__ void residual_tri_kernel(const double* __restrict__ x, const double* __restrict__ rhs, int n,
+                                    long long m, long long ld, const double* __restrict__ sub,
+                                    const double* __restrict__ diag, const double* __restrict__ sup,
+                                    double corner_tr, double corner_bl, unsigned long long* out) {
+  using namespace dev;
+  const long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  double w = 0.0;
+  if (j < m) {
+    auto X = [&](int i) { return x[static_cast<long long>(i) * ld + j]; };
+    double rmax = 0.0, dmax = 0.0;
+    for (int i = 0; i < n; ++i) {
+      double acc = mul_rn(diag[i], X(i));
+      if (i > 0) acc = add_rn(acc, mul_rn(sub[i], X(i - 1)));
+      if (i + 1 < n) acc = add_rn(acc, mul_rn(sup[i], X(i + 1)));
+      if (i == 0) acc = add_rn(acc, mul_rn(corner_tr, X(n - 1)));
+      if (i == n - 1) acc = add_rn(acc, mul_rn(corner_bl, X(0)));
+      const double b = rhs[static_cast<long long>(i) * ld + j];
+      rmax = ref_max(rmax, fabs(sub_rn(acc, b)));
+      dmax = ref_max(dmax, fabs(b));
+    }
+    w = dmax > 0.0 ? __ddiv_rn(rmax, dmax) : rmax;
+  }
+  for (int o = 16; o > 0; o >>= 1) w = ref_max(w, __shfl_xor_sync(0xffffffffu, w, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, static_cast<unsigned long long>(__double_as_longlong(w)));
+}
+
+__global__ void residual_pent_kernel(const double* __restrict__ x, const double* __restrict__ rhs, int n,
+                                     long long m, long long ld, const double* __restrict__ bands, int cyclic,
+                                     double ca, double cb, double cd, double ce, unsigned long long* out) {
+  using namespace dev;
+  const long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const double* a = bands;
+  const double* b = bands + n;
+  const double* c = bands + 2 * n;
+  const double* d = bands + 3 * n;
+  const double* e = bands + 4 * n;
+  double w = 0.0;
+  if (j < m) {
+    auto X = [&](int i) { return x[static_cast<long long>(i) * ld + j]; };
+    double rmax = 0.0, dmax = 0.0;
+    for (int i = 0; i < n; ++i) {
+      double acc = mul_rn(c[i], X(i));
+      if (i >= 2) acc = add_rn(acc, mul_rn(a[i], X(i - 2)));
+      if (i >= 1) acc = add_rn(acc, mul_rn(b[i], X(i - 1)));
+      if (i + 1 < n) acc = add_rn(acc, mul_rn(d[i], X(i + 1)));
+      if (i + 2 < n) acc = add_rn(acc, mul_rn(e[i], X(i + 2)));
+      if (cyclic) {
+        if (i == 0) acc = add_rn(acc, add_rn(mul_rn(ca, X(n - 2)), mul_rn(cb, X(n - 1))));
+        if (i == 1) acc = add_rn(acc, mul_rn(ca, X(n - 1)));
+        if (i == n - 2) acc = add_rn(acc, mul_rn(ce, X(0)));
+        if (i == n - 1) acc = add_rn(acc, add_rn(mul_rn(cd, X(0)), mul_rn(ce, X(1))));
+      }
+      const double r = rhs[static_cast<long long>(i) * ld + j];
+      rmax = ref_max(rmax, fabs(sub_rn(acc, r)));
+      dmax = ref_max(dmax, fabs(r));
+    }
+    w = dmax > 0.0 ? __ddiv_rn(rmax, dmax) : rmax;
+  }
+  for (int o = 16; o > 0; o >>= 1) w = ref_max(w, __shfl_xor_sync(0xffffffffu, w, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, static_cast<unsigned long long>(__double_as_longlong(w)));
+}
+
+// ---- synthetic RHS (bit-identical to oracle_rhs_value) ------------------------------
+__device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+template <typename T>
+__global__ void fill_rhs_kernel(T* __restrict__ x, int n, long long m, long long ld, uint64_t seed_hash,
+                                uint64_t j_offset) {
+  const long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  for (int i = blockIdx.y; i < n; i += gridDim.y) {
+    uint64_t h = splitmix64(seed_hash ^ static_cast<uint64_t>(i));
+    h = splitmix64(h ^ (j_offset + static_cast<uint64_t>(j)));
+    const double v = __dsub_rn(__dmul_rn(static_cast<double>(h >> 11), 0x1.0p-52), 1.0);
+    x[static_cast<long long>(i) * ld + j] = static_cast<T>(v);
+  }
+}
+
+uint64_t host_splitmix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// ---- per-thread staging context for host batches --------------------------------
+constexpr int kStages = 3;
+struct StageContext {
+  int device = -1;
+  cudaStream_t streams[kStages] = {};
+  void* buf[kStages] = {};
+  std::size_t cap[kStages] = {};
+};
+// Intentionally never destroyed: CUDA may already be torn down at thread exit.
+thread_local std::vector<StageContext*> t_contexts;
+
+bandsolve_status stage_context(int device, StageContext** out) {
+  for (StageContext* c : t_contexts)
+    if (c->device == device) {
+      *out = c;
+      return BANDSOLVE_OK;
+    }
+  auto* c = new StageContext;
+  c->device = device;
+  for (int s = 0; s < kStages; ++s) BSB_CUDA(cudaStreamCreateWithFlags(&c->streams[s], cudaStreamNonBlocking));
+  t_contexts.push_back(c);
+  *out = c;
+  return BANDSOLVE_OK;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------
+int current_mode() {
+  int m = g_mode.load(std::memory_order_relaxed);
+  if (m < 0) {
+    m = mode_from_env();
+    g_mode.store(m, std::memory_order_relaxed);
+  }
+  return m;
+}
+void set_mode(int mode) { g_mode.store(mode, std::memory_order_relaxed); }
+uint64_t kernel_launches() { return g_launches.load(std::memory_order_relaxed); }
+
+void release_device_factor(DeviceFactor& d) {
+  if (!d.base) return;
+  int prev = -1;
+  if (cudaGetDevice(&prev) == cudaSuccess && prev != d.device) cudaSetDevice(d.device);
+  cudaFree(d.base);
+  if (prev >= 0 && prev != d.device) cudaSetDevice(prev);
+  cudaGetLastError();
+  d.base = nullptr;
+}
+
+Factor::~Factor() {
+  for (DeviceFactor& d : devices) release_device_factor(d);
+}
+
+double* host_alloc_zeroed(std::size_t count, bool* pinned) {
+  *pinned = false;
+  const std::size_t bytes = count * sizeof(double);
+  if (device_count_cached() > 0) {
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, bytes, cudaHostAllocPortable) == cudaSuccess) {
+      std::memset(p, 0, bytes);
+      *pinned = true;
+      return static_cast<double*>(p);
+    }
+    cudaGetLastError();
+  }
+  return static_cast<double*>(std::calloc(count, sizeof(double)));
+}
+
+void host_free(double* p, bool pinned) {
+  if (!p) return;
+  if (pinned) cudaFreeHost(p);
+  else std::free(p);
+}
+
+bandsolve_status describe_plan(Kind kind, std::size_t n, std::size_t m, std::size_t ld, bool f32,
+                               std::string& out) {
+  (void)kind;
+  alignas(16) static const double kProbe[2] = {0.0, 0.0};  // 16-byte aligned stand-in base
+  const Plan p = choose_plan(n, m, ld, f32 ? 4 : 8, kProbe);
+  char buf[256];
+  if (p.smem)
+    std::snprintf(buf, sizeof buf, "smem-tma W=%d R=%d smem=%zu B ctas/sm=%d systems/sm=%d", p.W, kChunkRows,
+                  p.smem_bytes, p.ctas_per_sm, p.ctas_per_sm * p.W);
+  else
+    std::snprintf(buf, sizeof buf, "global-inplace (%s)", p.why.c_str());
+  out = buf;
+  return BANDSOLVE_OK;
+}
+
+bandsolve_status solve_device(const Factor& f, void* x, bool f32, std::size_t n, std::size_t m,
+                              std::size_t ld, void* stream) {
+  if (!x) return fail(BANDSOLVE_ERR_BAD_ARG, "null device pointer");
+  if (n != f.n) return fail(BANDSOLVE_ERR_SHAPE_MISMATCH, "factor order != batch rows");
+  if (ld < m) return fail(BANDSOLVE_ERR_BAD_ARG, "row pitch ld < m");
+  if (m == 0) return BANDSOLVE_OK;
+  if (n > static_cast<std::size_t>(INT_MAX)) return fail(BANDSOLVE_ERR_BAD_ARG, "n too large");
+  if (device_count_cached() == 0) return fail(BANDSOLVE_ERR_INTERNAL, "no CUDA device available (no CPU fallback)");
+  int device = 0;
+  BSB_CUDA(cudaGetDevice(&device));
+  const DeviceFactor* df = nullptr;
+  bandsolve_status st = ensure_device_factor(f, device, &df);
+  if (st != BANDSOLVE_OK) return st;
+  const bool fast = current_mode() == BANDSOLVE_MODE_FAST;
+  const bool pent = f.kind != Kind::Tri;
+  const int p = f32 ? 1 : 0;
+  const int q = fast ? 1 : 0;
+  auto s = static_cast<cudaStream_t>(stream);
+  const Plan plan = choose_plan(n, m, ld, f32 ? 4 : 8, x);
+  cudaError_t err;
+  if (f32)
+    err = dispatch_kind<float>(plan, pent, fast, static_cast<float*>(x), static_cast<int>(n),
+                               static_cast<long long>(m), static_cast<long long>(ld), df->fwd[p][q],
+                               df->bwd[p][q], s);
+  else
+    err = dispatch_kind<double>(plan, pent, fast, static_cast<double*>(x), static_cast<int>(n),
+                                static_cast<long long>(m), static_cast<long long>(ld), df->fwd[p][q],
+                                df->bwd[p][q], s);
+  if (err != cudaSuccess) return cuda_fail(err, "sweep launch");
+  return BANDSOLVE_OK;
+}
+
+bandsolve_status solve_host(const Factor& f, double* x, std::size_t n, std::size_t m) {
+  if (n != f.n) return fail(BANDSOLVE_ERR_SHAPE_MISMATCH, "factor order != batch rows");
+  if (m == 0) return BANDSOLVE_OK;
+  if (device_count_cached() == 0) return fail(BANDSOLVE_ERR_INTERNAL, "no CUDA device available (no CPU fallback)");
+  int device = 0;
+  BSB_CUDA(cudaGetDevice(&device));
+  StageContext* ctx = nullptr;
+  bandsolve_status st = stage_context(device, &ctx);
+  if (st != BANDSOLVE_OK) return st;
+
+  // Column chunks of ~16 MiB (multiple of 32 systems) pipelined over three
+  // streams: chunk k's H2D overlaps chunk k-1's sweep and chunk k-2's D2H.
+  const std::size_t row_bytes = n * sizeof(double);
+  std::size_t w = (16u << 20) / row_bytes;
+  w = std::max<std::size_t>(32, (w / 32) * 32);
+  if (w >= m) w = m;
+  const std::size_t chunks = (m + w - 1) / w;
+  const std::size_t need = n * ((w + 1) & ~std::size_t(1)) * sizeof(double);
+  const int stages = static_cast<int>(std::min<std::size_t>(kStages, chunks));
+  for (int s = 0; s < stages; ++s) {
+    if (ctx->cap[s] < need) {
+      if (ctx->buf[s]) {
+        BSB_CUDA(cudaStreamSynchronize(ctx->streams[s]));
+        BSB_CUDA(cudaFree(ctx->buf[s]));
+        ctx->buf[s] = nullptr;
+        ctx->cap[s] = 0;
+      }
+      BSB_CUDA(cudaMalloc(&ctx->buf[s], need));
+      ctx->cap[s] = need;
+    }
+  }
+  for (std::size_t k = 0; k < chunks; ++k) {
+    const int s = static_cast<int>(k % stages);
+    cudaStream_t strm = ctx->streams[s];
+    const std::size_t j0 = k * w;
+    const std::size_t wk = std::min(w, m - j0);
+    const std::size_t ldk = (wk + 1) & ~std::size_t(1);  // even pitch keeps the TMA path
+    double* d = static_cast<double*>(ctx->buf[s]);
+    BSB_CUDA(cudaMemcpy2DAsync(d, ldk * sizeof(double), x + j0, m * sizeof(double), wk * sizeof(double), n,
+                               cudaMemcpyHostToDevice, strm));
+    st = solve_device(f, d, false, n, wk, ldk, strm);
+    if (st != BANDSOLVE_OK) {
+      for (int q = 0; q < stages; ++q) cudaStreamSynchronize(ctx->streams[q]);
+      return st;
+    }
+    BSB_CUDA(cudaMemcpy2DAsync(x + j0, m * sizeof(double), d, ldk * sizeof(double), wk * sizeof(double), n,
+                               cudaMemcpyDeviceToHost, strm));
+  }
+  for (int s = 0; s < stages; ++s) BSB_CUDA(cudaStreamSynchronize(ctx->streams[s]));
+  return BANDSOLVE_OK;
+}
+
+bandsolve_status residual_device(Kind kind, const double* const* bands, std::size_t n, int cyclic,
+                                 const double* x, const double* rhs, std::size_t m, std::size_t ld,
+                                 void* stream, double* out) {
+  if (device_count_cached() == 0) return fail(BANDSOLVE_ERR_INTERNAL, "no CUDA device available (no CPU fallback)");
+  if (ld < m) return fail(BANDSOLVE_ERR_BAD_ARG, "row pitch ld < m");
+  if (n > static_cast<std::size_t>(INT_MAX)) return fail(BANDSOLVE_ERR_BAD_ARG, "n too large");
+  auto s = static_cast<cudaStream_t>(stream);
+  const bool pent = kind != Kind::Tri;
+  const int nb = pent ? 5 : 3;
+  // bands as the residual reads them: constant bands + corners when cyclic
+  // (tri_solver.cpp:149-156 via constant_tri_lhs; pent_solver.cpp:265-273)
+  std::vector<double> host(nb * n + 1, 0.0);
+  double corners[4] = {0, 0, 0, 0};
+  if (cyclic) {
+    if (!pent) {
+      const double a = bands[0][1], b = bands[1][0], c = bands[2][0];
+      for (std::size_t i = 0; i < n; ++i) {
+        host[i] = a;
+        host[n + i] = b;
+        host[2 * n + i] = c;
+      }
+      host[0] = 0.0;
+      host[2 * n + n - 1] = 0.0;
+      corners[0] = a;
+      corners[1] = c;
+    } else {
+      const double v[5] = {bands[0][2], bands[1][1], bands[2][0], bands[3][0], bands[4][0]};
+      for (int k = 0; k < 5; ++k)
+        for (std::size_t i = 0; i < n; ++i) host[k * n + i] = v[k];
+      host[0] = host[1] = host[n] = 0.0;
+      host[3 * n + n - 1] = host[4 * n + n - 1] = host[4 * n + n - 2] = 0.0;
+      corners[0] = v[0];
+      corners[1] = v[1];
+      corners[2] = v[3];
+      corners[3] = v[4];
+    }
+  } else {
+    for (int k = 0; k < nb; ++k) std::memcpy(host.data() + k * n, bands[k], n * sizeof(double));
+  }
+  double* dbands = nullptr;
+  unsigned long long* dout = nullptr;
+  BSB_CUDA(cudaMallocAsync(&dbands, host.size() * sizeof(double), s));
+  BSB_CUDA(cudaMallocAsync(&dout, sizeof(unsigned long long), s));
+  BSB_CUDA(cudaMemcpyAsync(dbands, host.data(), host.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+  BSB_CUDA(cudaMemsetAsync(dout, 0, sizeof(unsigned long long), s));
+  const int threads = 128;
+  const unsigned grid = static_cast<unsigned>((m + threads - 1) / threads);
+  if (grid > 0) {
+    if (pent)
+      residual_pent_kernel<<<grid, threads, 0, s>>>(x, rhs, static_cast<int>(n), static_cast<long long>(m),
+                                                    static_cast<long long>(ld), dbands, cyclic, corners[0],
+                                                    corners[1], corners[2], corners[3], dout);
+    else
+      residual_tri_kernel<<<grid, threads, 0, s>>>(x, rhs, static_cast<int>(n), static_cast<long long>(m),
+                                                   static_cast<long long>(ld), dbands, dbands + n, dbands + 2 * n,
+                                                   corners[0], corners[1], dout);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    BSB_CUDA(cudaGetLastError());
+  }
+  unsigned long long bits = 0;
+  BSB_CUDA(cudaMemcpyAsync(&bits, dout, sizeof bits, cudaMemcpyDeviceToHost, s));
+  BSB_CUDA(cudaFreeAsync(dbands, s));
+  BSB_CUDA(cudaFreeAsync(dout, s));
+  BSB_CUDA(cudaStreamSynchronize(s));
+  double w;
+  std::memcpy(&w, &bits, sizeof w);
+  *out = w;
+  return BANDSOLVE_OK;
+}
+
+bandsolve_status residual_host(Kind kind, const double* const* bands, std::size_t n, int cyclic, const double* x,
+                               const double* rhs, std::size_t m, double* out) {
+  if (device_count_cached() == 0) return fail(BANDSOLVE_ERR_INTERNAL, "no CUDA device available (no CPU fallback)");
+  int device = 0;
+  BSB_CUDA(cudaGetDevice(&device));
+  StageContext* ctx = nullptr;
+  bandsolve_status st = stage_context(device, &ctx);
+  if (st != BANDSOLVE_OK) return st;
+  cudaStream_t s = ctx->streams[0];
+  const std::size_t bytes = n * m * sizeof(double);
+  double *dx = nullptr, *dr = nullptr;
+  BSB_CUDA(cudaMallocAsync(&dx, bytes, s));
+  BSB_CUDA(cudaMallocAsync(&dr, bytes, s));
+  BSB_CUDA(cudaMemcpyAsync(dx, x, bytes, cudaMemcpyHostToDevice, s));
+  BSB_CUDA(cudaMemcpyAsync(dr, rhs, bytes, cudaMemcpyHostToDevice, s));
+  st = residual_device(kind, bands, n, cyclic, dx, dr, m, m, s, out);
+  cudaFreeAsync(dx, s);
+  cudaFreeAsync(dr, s);
+  cudaStreamSynchronize(s);
+  return st;
+}
+
+bandsolve_status fill_rhs_device(void* x, bool f32, std::size_t n, std::size_t m, std::size_t ld, uint64_t seed,
+                                 uint64_t j_offset, void* stream) {
+  if (!x) return fail(BANDSOLVE_ERR_BAD_ARG, "null device pointer");
+  if (ld < m) return fail(BANDSOLVE_ERR_BAD_ARG, "row pitch ld < m");
+  if (n == 0 || m == 0) return BANDSOLVE_OK;
+  if (device_count_cached() == 0) return fail(BANDSOLVE_ERR_INTERNAL, "no CUDA device available (no CPU fallback)");
+  auto s = static_cast<cudaStream_t>(stream);
+  const int threads = 256;
+  dim3 grid(static_cast<unsigned>((m + threads - 1) / threads), static_cast<unsigned>(std::min<std::size_t>(n, 64)));
+  const uint64_t sh = host_splitmix64(seed);
+  if (f32)
+    fill_rhs_kernel<float><<<grid, threads, 0, s>>>(static_cast<float*>(x), static_cast<int>(n),
+                                                    static_cast<long long>(m), static_cast<long long>(ld), sh, j_offset);
+  else
+    fill_rhs_kernel<double><<<grid, threads, 0, s>>>(static_cast<double*>(x), static_cast<int>(n),
+                                                     static_cast<long long>(m), static_cast<long long>(ld), sh, j_offset);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  BSB_CUDA(cudaGetLastError());
+  return BANDSOLVE_OK;
+}
+
+}  // namespace bsb
