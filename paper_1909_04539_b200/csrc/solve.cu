@@ -15,6 +15,7 @@
 
 #include "internal.hpp"
 #include "sweep_kernels.cuh"
+#include "sweep_persist.cuh"
 
 namespace bsb {
 
@@ -175,43 +176,145 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 
 // ---- plans ----------------------------------------------------------------------
 constexpr int kChunkRows = 32;
-constexpr std::size_t kSmemPerSm = 233472;     // 228 KB on sm_100 (measured via cudaGetDeviceProperties)
-constexpr std::size_t kSmemPerBlockMax = 232448;  // 227 KB opt-in
+constexpr std::size_t kSmemPerSm = 233472;        // 228 KB per SM on sm_100 (cudaGetDeviceProperties)
+constexpr std::size_t kSmemPerBlockMax = 232448;  // 227 KB opt-in per CTA
 constexpr std::size_t kSmemReservedPerCta = 1024;
+constexpr double kSpillBudget = 64.0 * (1 << 20);  // bytes of spilled d-hat kept L2-resident (of 126 MB)
+
+enum class PlanKind { Global, Smem, Persist };
 
 struct Plan {
-  bool smem = false;
-  int W = 0;
+  PlanKind kind = PlanKind::Global;
+  int W = 0;                 // smem: systems per CTA
+  int ctas_per_sm = 0;       // smem
+  int warps = 0;             // persist: warps per CTA (32 systems each)
+  int H = 0, TC = 0;         // persist: spilled head rows, tail chunks
   std::size_t smem_bytes = 0;
-  int ctas_per_sm = 0;
   std::string why;
 };
+
+int num_sms(int device) {
+  static std::atomic<int> cached[64];
+  if (device < 0 || device >= 64) return 148;
+  int v = cached[device].load(std::memory_order_relaxed);
+  if (v <= 0) {
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || v <= 0) {
+      cudaGetLastError();
+      v = 148;
+    }
+    cached[device].store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
 
 std::size_t smem_bytes_for(std::size_t n, int W, std::size_t elem) {
   const std::size_t chunks = (n + kChunkRows - 1) / kChunkRows;
   return chunks * kChunkRows * W * elem + chunks * sizeof(uint64_t);
 }
 
-Plan choose_plan(std::size_t n, std::size_t m, std::size_t ld, std::size_t elem, const void* x) {
+std::size_t fwd_rec_bytes(bool pent, std::size_t elem) { return (pent ? 4 : 2) * elem; }
+std::size_t bwd_rec_bytes(bool pent, std::size_t elem) { return (pent ? 2 : 1) * elem; }
+
+// Dependent-latency cycles per row (forward + backward) on B200: fp64
+// DADD/DMUL/DFMA 8 cycles, fp32 4 (tools/microbench/dplat.cu).
+int chain_cycles(bool pent, bool fast, std::size_t elem) {
+  const int lat = elem == 8 ? 8 : 4;
+  if (fast) return 2 * lat;
+  return (pent ? 6 : 5) * lat;
+}
+
+// Persistent plan: as many systems per SM as the chain needs (2x margin over
+// 1.125 rows/cycle/SM), all rows in smem when they fit, otherwise the head
+// rows spill to L2 within kSpillBudget.
+bool plan_persist(std::size_t n, std::size_t elem, bool pent, bool fast, int sms, Plan& p) {
+  const std::size_t fr = fwd_rec_bytes(pent, elem), br = bwd_rec_bytes(pent, elem);
+  const std::size_t fac = dev::align128(n * fr) + dev::align128(n * br);
+  if (fac > kSmemPerBlockMax / 2) return false;
+  const int tail_full_chunks = static_cast<int>((n + dev::kRT - 1) / dev::kRT);
+  const int need_sys = static_cast<int>(2.0 * 1.125 * chain_cycles(pent, fast, elem));
+  int target = std::max(2, std::min(16, (need_sys + dev::kPW - 1) / dev::kPW));
+  if (const char* e = std::getenv("BANDSOLVE_PWARPS")) target = std::max(1, std::min(16, std::atoi(e)));
+  const int forced_tail = std::getenv("BANDSOLVE_PTAIL") ? std::atoi(std::getenv("BANDSOLVE_PTAIL")) : -1;
+
+  auto fit = [&](int warps, int H, int TC) {
+    return dev::PersistLayout::make(static_cast<int>(n), H, TC, warps, elem, fr, br).total <= kSmemPerBlockMax;
+  };
+  // 1) everything resident: the most warps that fit (at least `target`)
+  if (forced_tail < 0) {
+    int w = 0;
+    for (int k = 16; k >= 1; --k)
+      if (fit(k, 0, tail_full_chunks)) {
+        w = k;
+        break;
+      }
+    if (w >= target) {
+      p.kind = PlanKind::Persist;
+      p.warps = w;
+      p.H = 0;
+      p.TC = tail_full_chunks;
+      p.smem_bytes = dev::PersistLayout::make(static_cast<int>(n), 0, p.TC, w, elem, fr, br).total;
+      return true;
+    }
+  }
+  // 2) spill the head: the largest tail that fits for `warps`, head in L2
+  for (int warps = target; warps >= 1; --warps) {
+    int best_tc = -1;
+    for (int tc = tail_full_chunks; tc >= 0; --tc) {
+      int tail_rows = std::min<int>(static_cast<int>(n), tc * dev::kRT);
+      if (forced_tail >= 0) tail_rows = std::min<int>(static_cast<int>(n), forced_tail);
+      int H = static_cast<int>(n) - tail_rows;
+      H = (H + dev::kRH - 1) / dev::kRH * dev::kRH;  // head rows: whole ring chunks
+      if (H > static_cast<int>(n)) H = static_cast<int>(n) / dev::kRH * dev::kRH;
+      const int TC = (static_cast<int>(n) - H + dev::kRT - 1) / dev::kRT;
+      if (static_cast<int>(n) - H > 0 && H % dev::kRH != 0) continue;
+      if (H + TC * dev::kRT < static_cast<int>(n)) continue;
+      if (fit(warps, H, TC)) {
+        best_tc = TC;
+        p.H = H;
+        break;
+      }
+      if (forced_tail >= 0) break;
+    }
+    if (best_tc < 0) continue;
+    const double spill = static_cast<double>(warps) * dev::kPW * sms * p.H * elem;
+    if (spill <= kSpillBudget || warps == 1 || forced_tail >= 0 || std::getenv("BANDSOLVE_PWARPS")) {
+      p.kind = PlanKind::Persist;
+      p.warps = warps;
+      p.TC = best_tc;
+      p.smem_bytes = dev::PersistLayout::make(static_cast<int>(n), p.H, p.TC, warps, elem, fr, br).total;
+      return true;
+    }
+  }
+  return false;
+}
+
+Plan choose_plan(std::size_t n, std::size_t m, std::size_t ld, std::size_t elem, const void* x, bool pent,
+                 bool fast, int sms) {
   Plan p;
-  const char* force = std::getenv("BANDSOLVE_PLAN");  // "global" | "smem" | "smemW8" | "smemW16" | "smemW32"
+  // BANDSOLVE_PLAN = global | persist | smem | smemW8 | smemW16 | smemW32 (tuning / tests)
+  const char* force = std::getenv("BANDSOLVE_PLAN");
   int forced_w = 0;
+  bool force_smem = false;
   if (force) {
     if (std::strcmp(force, "global") == 0) {
       p.why = "forced global";
       return p;
     }
-    if (std::strncmp(force, "smemW", 5) == 0) forced_w = std::atoi(force + 5);
+    if (std::strncmp(force, "smem", 4) == 0) {
+      force_smem = true;
+      if (std::strncmp(force, "smemW", 5) == 0) forced_w = std::atoi(force + 5);
+    }
   }
   const bool aligned = (reinterpret_cast<uintptr_t>(x) % 16 == 0) && ((ld * elem) % 16 == 0);
   if (!aligned) {
     p.why = "row pitch or base not 16-byte aligned (TMA rule)";
     return p;
   }
-  if (n > static_cast<std::size_t>(INT_MAX) || m > static_cast<std::size_t>(INT_MAX)) {
+  if (n > static_cast<std::size_t>(INT_MAX) || m > static_cast<std::size_t>(INT_MAX) / 2) {
     p.why = "shape beyond 32-bit TMA coordinates";
     return p;
   }
+  if (!force_smem && plan_persist(n, elem, pent, fast, sms, p)) return p;
   int best_sys = 0;
   for (int W : {8, 16, 32}) {
     if (forced_w && W != forced_w) continue;
@@ -223,44 +326,81 @@ Plan choose_plan(std::size_t n, std::size_t m, std::size_t ld, std::size_t elem,
     // prefer more systems in flight; on ties the wider (more coalesced) box
     if (sys > best_sys || (sys == best_sys && W > p.W)) {
       best_sys = sys;
-      p.smem = true;
+      p.kind = PlanKind::Smem;
       p.W = W;
       p.smem_bytes = bytes;
       p.ctas_per_sm = k;
     }
   }
-  if (!p.smem) p.why = "tile does not fit shared memory";
+  if (p.kind != PlanKind::Smem) p.why = "tile does not fit shared memory";
   return p;
+}
+
+bool encode_map(CUtensorMap* map, void* x, std::size_t elem, long long n, long long m, long long ld, int box_w,
+                int box_r) {
+  auto encode = tensor_map_encoder();
+  if (!encode) return false;
+  const cuuint64_t gdim[2] = {static_cast<cuuint64_t>(m), static_cast<cuuint64_t>(n)};
+  const cuuint64_t gstride[1] = {static_cast<cuuint64_t>(ld) * elem};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(box_w), static_cast<cuuint32_t>(box_r)};
+  const cuuint32_t estride[2] = {1, 1};
+  CUresult r = encode(map, elem == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, x,
+                      gdim, gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <typename K>
+cudaError_t allow_big_smem(K kern) {
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(kSmemPerBlockMax));
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
 }
 
 template <typename T, int W, bool PENT, bool FAST>
 cudaError_t launch_smem(const Plan& plan, T* x, int n, long long m, long long ld, const void* fwd,
                         const void* bwd, cudaStream_t s) {
   auto kern = dev::sweep_smem<T, W, kChunkRows, PENT, FAST>;
-  static std::atomic<std::size_t> configured{0};
-  if (configured.load(std::memory_order_relaxed) < plan.smem_bytes) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kSmemPerBlockMax));
+  static std::atomic<bool> configured{false};
+  if (!configured.load(std::memory_order_relaxed)) {
+    cudaError_t e = allow_big_smem(kern);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-                             cudaSharedmemCarveoutMaxShared);
-    if (e != cudaSuccess) return e;
-    configured.store(kSmemPerBlockMax, std::memory_order_relaxed);
+    configured.store(true, std::memory_order_relaxed);
   }
-  auto encode = tensor_map_encoder();
-  if (!encode) return cudaErrorNotSupported;
   CUtensorMap map;
-  const cuuint64_t gdim[2] = {static_cast<cuuint64_t>(m), static_cast<cuuint64_t>(n)};
-  const cuuint64_t gstride[1] = {static_cast<cuuint64_t>(ld) * sizeof(T)};
-  const cuuint32_t box[2] = {static_cast<cuuint32_t>(W), static_cast<cuuint32_t>(kChunkRows)};
-  const cuuint32_t estride[2] = {1, 1};
-  CUresult r = encode(&map, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
-                      2, x, gdim, gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  if (!encode_map(&map, x, sizeof(T), n, m, ld, W, kChunkRows)) return cudaErrorInvalidValue;
   const long long grid = (m + W - 1) / W;
   kern<<<static_cast<unsigned>(grid), W, plan.smem_bytes, s>>>(map, x, n, m, ld, fwd, bwd);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
+template <typename T, bool PENT, bool FAST>
+cudaError_t launch_persist(const Plan& plan, T* x, int n, long long m, long long ld, const void* fwd,
+                           const void* bwd, cudaStream_t s, int sms) {
+  auto kern = dev::sweep_persist<T, PENT, FAST>;
+  static std::atomic<bool> configured{false};
+  if (!configured.load(std::memory_order_relaxed)) {
+    cudaError_t e = allow_big_smem(kern);
+    if (e != cudaSuccess) return e;
+    configured.store(true, std::memory_order_relaxed);
+  }
+  CUtensorMap map_ring, map_tail;
+  if (!encode_map(&map_ring, x, sizeof(T), n, m, ld, dev::kPW, dev::kRH) ||
+      !encode_map(&map_tail, x, sizeof(T), n, m, ld, dev::kPW, dev::kRT))
+    return cudaErrorInvalidValue;
+  const long long tiles = (m + dev::kPW - 1) / dev::kPW;
+  // spread small batches over all SMs before stacking warps per CTA
+  int warps = plan.warps;
+  if (tiles < static_cast<long long>(sms) * warps)
+    warps = static_cast<int>(std::max<long long>(1, (tiles + sms - 1) / sms));
+  const long long grid = std::min<long long>(sms, (tiles + warps - 1) / warps);
+  const std::size_t smem = dev::PersistLayout::make(n, plan.H, plan.TC, warps, sizeof(T),
+                                                    sizeof(typename dev::Recs<T, PENT>::Fwd),
+                                                    sizeof(typename dev::Recs<T, PENT>::Bwd)).total;
+  kern<<<static_cast<unsigned>(grid), warps * 32, smem, s>>>(map_ring, map_tail, x, n, m, ld, plan.H, plan.TC,
+                                                            tiles, fwd, bwd);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }
@@ -277,8 +417,9 @@ cudaError_t launch_global(T* x, int n, long long m, long long ld, const void* fw
 
 template <typename T, bool PENT, bool FAST>
 cudaError_t dispatch(const Plan& plan, T* x, int n, long long m, long long ld, const void* fwd,
-                     const void* bwd, cudaStream_t s) {
-  if (plan.smem) {
+                     const void* bwd, cudaStream_t s, int sms) {
+  if (plan.kind == PlanKind::Persist) return launch_persist<T, PENT, FAST>(plan, x, n, m, ld, fwd, bwd, s, sms);
+  if (plan.kind == PlanKind::Smem) {
     switch (plan.W) {
       case 8: return launch_smem<T, 8, PENT, FAST>(plan, x, n, m, ld, fwd, bwd, s);
       case 16: return launch_smem<T, 16, PENT, FAST>(plan, x, n, m, ld, fwd, bwd, s);
@@ -291,12 +432,12 @@ cudaError_t dispatch(const Plan& plan, T* x, int n, long long m, long long ld, c
 
 template <typename T>
 cudaError_t dispatch_kind(const Plan& plan, bool pent, bool fast, T* x, int n, long long m, long long ld,
-                          const void* fwd, const void* bwd, cudaStream_t s) {
+                          const void* fwd, const void* bwd, cudaStream_t s, int sms) {
   if (pent)
-    return fast ? dispatch<T, true, true>(plan, x, n, m, ld, fwd, bwd, s)
-                : dispatch<T, true, false>(plan, x, n, m, ld, fwd, bwd, s);
-  return fast ? dispatch<T, false, true>(plan, x, n, m, ld, fwd, bwd, s)
-              : dispatch<T, false, false>(plan, x, n, m, ld, fwd, bwd, s);
+    return fast ? dispatch<T, true, true>(plan, x, n, m, ld, fwd, bwd, s, sms)
+                : dispatch<T, true, false>(plan, x, n, m, ld, fwd, bwd, s, sms);
+  return fast ? dispatch<T, false, true>(plan, x, n, m, ld, fwd, bwd, s, sms)
+              : dispatch<T, false, false>(plan, x, n, m, ld, fwd, bwd, s, sms);
 }
 
 // ---- residual ---------------------------------------------------------------
@@ -472,11 +613,19 @@ void host_free(double* p, bool pinned) {
 
 bandsolve_status describe_plan(Kind kind, std::size_t n, std::size_t m, std::size_t ld, bool f32,
                                std::string& out) {
-  (void)kind;
   alignas(16) static const double kProbe[2] = {0.0, 0.0};  // 16-byte aligned stand-in base
-  const Plan p = choose_plan(n, m, ld, f32 ? 4 : 8, kProbe);
+  int device = 0;
+  int sms = 148;
+  if (device_count_cached() > 0 && cudaGetDevice(&device) == cudaSuccess) sms = num_sms(device);
+  cudaGetLastError();
+  const bool pent = kind != Kind::Tri;
+  const bool fast = current_mode() == BANDSOLVE_MODE_FAST;
+  const Plan p = choose_plan(n, m, ld, f32 ? 4 : 8, kProbe, pent, fast, sms);
   char buf[256];
-  if (p.smem)
+  if (p.kind == PlanKind::Persist)
+    std::snprintf(buf, sizeof buf, "persist warps=%d systems/sm=%d head(L2)=%d tail(smem)=%d smem=%zu B", p.warps,
+                  p.warps * dev::kPW, p.H, static_cast<int>(n) - p.H, p.smem_bytes);
+  else if (p.kind == PlanKind::Smem)
     std::snprintf(buf, sizeof buf, "smem-tma W=%d R=%d smem=%zu B ctas/sm=%d systems/sm=%d", p.W, kChunkRows,
                   p.smem_bytes, p.ctas_per_sm, p.ctas_per_sm * p.W);
   else
@@ -503,16 +652,17 @@ bandsolve_status solve_device(const Factor& f, void* x, bool f32, std::size_t n,
   const int p = f32 ? 1 : 0;
   const int q = fast ? 1 : 0;
   auto s = static_cast<cudaStream_t>(stream);
-  const Plan plan = choose_plan(n, m, ld, f32 ? 4 : 8, x);
+  const int sms = num_sms(device);
+  const Plan plan = choose_plan(n, m, ld, f32 ? 4 : 8, x, pent, fast, sms);
   cudaError_t err;
   if (f32)
     err = dispatch_kind<float>(plan, pent, fast, static_cast<float*>(x), static_cast<int>(n),
                                static_cast<long long>(m), static_cast<long long>(ld), df->fwd[p][q],
-                               df->bwd[p][q], s);
+                               df->bwd[p][q], s, sms);
   else
     err = dispatch_kind<double>(plan, pent, fast, static_cast<double*>(x), static_cast<int>(n),
                                 static_cast<long long>(m), static_cast<long long>(ld), df->fwd[p][q],
-                                df->bwd[p][q], s);
+                                df->bwd[p][q], s, sms);
   if (err != cudaSuccess) return cuda_fail(err, "sweep launch");
   return BANDSOLVE_OK;
 }

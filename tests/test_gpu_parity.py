@@ -27,7 +27,7 @@ def _exact_mode(lib):
     lib.set_mode(bs.MODE_EXACT)
     yield
     lib.set_mode(bs.MODE_EXACT)
-    os.environ.pop("BANDSOLVE_PLAN", None)
+    set_plan(None)
 
 
 # ---- helpers -------------------------------------------------------------------
@@ -137,15 +137,24 @@ def test_cyclic_residual_matches_oracle(lib, oracle, cuda_device):
 # ---- device entry points over every plan and edge shape -----------------------------
 SHAPES = [(2, 1), (3, 2), (5, 3), (31, 7), (32, 16), (33, 17), (64, 8), (65, 40), (100, 33), (257, 130),
           (512, 64), (1024, 48)]
-PLANS = [None, "global", "smemW8", "smemW16", "smemW32"]
+# plan overrides: (BANDSOLVE_PLAN, BANDSOLVE_PWARPS, BANDSOLVE_PTAIL)
+PLANS = [None, ("global",), ("smemW8",), ("smemW16",), ("smemW32",), ("persist", "1", "0"),
+         ("persist", "2", "48"), ("persist", "3", "100000")]
+
+
+def set_plan(plan):
+    for k in ("BANDSOLVE_PLAN", "BANDSOLVE_PWARPS", "BANDSOLVE_PTAIL"):
+        os.environ.pop(k, None)
+    if plan:
+        for k, v in zip(("BANDSOLVE_PLAN", "BANDSOLVE_PWARPS", "BANDSOLVE_PTAIL"), plan):
+            os.environ[k] = v
 
 
 @pytest.mark.parametrize("plan", PLANS)
 def test_tri_device_plans_bitwise(lib, oracle, cuda_device, plan):
     torch = cuda_device
     rng = np.random.default_rng(100)
-    if plan:
-        os.environ["BANDSOLVE_PLAN"] = plan
+    set_plan(plan)
     for n, m in SHAPES:
         bands = random_tri(rng, n)
         f = bs.TriFactor(lib, *bands)
@@ -161,8 +170,7 @@ def test_tri_device_plans_bitwise(lib, oracle, cuda_device, plan):
 def test_pent_device_plans_bitwise(lib, oracle, cuda_device, plan):
     torch = cuda_device
     rng = np.random.default_rng(200)
-    if plan:
-        os.environ["BANDSOLVE_PLAN"] = plan
+    set_plan(plan)
     for n, m in SHAPES:
         if n < 5:
             continue
@@ -178,12 +186,11 @@ def test_pent_device_plans_bitwise(lib, oracle, cuda_device, plan):
         assert bitwise_equal(dev_solve(torch, u, rhs), want_u), (plan, n, m)
 
 
-@pytest.mark.parametrize("plan", [None, "global"])
+@pytest.mark.parametrize("plan", [None, ("global",), ("persist", "2", "0")])
 def test_fast_mode_within_tolerance(lib, oracle, cuda_device, plan):
     torch = cuda_device
     rng = np.random.default_rng(300)
-    if plan:
-        os.environ["BANDSOLVE_PLAN"] = plan
+    set_plan(plan)
     lib.set_mode(bs.MODE_FAST)
     for n, m in [(2, 3), (33, 17), (256, 64), (512, 96), (2048, 32)]:
         tb = random_tri(rng, n)
