@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -207,6 +208,46 @@ int num_sms(int device) {
   return v;
 }
 
+// Stream-ordered allocations (spill scratch, residual buffers) come from the
+// device's default pool; keep freed blocks cached so steady-state solves
+// never go back to the driver.
+void keep_pool_memory(int device) {
+  static std::atomic<uint64_t> done{0};
+  const uint64_t bit = device < 64 ? (1ull << device) : 0;
+  if (!bit || (done.load(std::memory_order_relaxed) & bit)) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t threshold = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
+  }
+  cudaGetLastError();
+  done.fetch_or(bit, std::memory_order_relaxed);
+}
+
+// The spill scratch is written and re-read within one tile; its evict_last
+// lines are only protected from the evict-first b/x streams inside the L2
+// persisting set-aside, which is 0 by default. Grow the set-aside (never
+// shrink it) to cover the scratch, up to the device maximum.
+// BANDSOLVE_L2_SETASIDE=0 disables this (the solve stays correct, only the
+// spilled rows may then round-trip through HBM).
+void ensure_l2_setaside(int device, std::size_t bytes) {
+  const char* env = std::getenv("BANDSOLVE_L2_SETASIDE");
+  if (env && std::strcmp(env, "0") == 0) return;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  int max_persist = 0;
+  if (cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, device) != cudaSuccess ||
+      max_persist <= 0) {
+    cudaGetLastError();
+    return;
+  }
+  const std::size_t want = std::min<std::size_t>(bytes + bytes / 8, static_cast<std::size_t>(max_persist));
+  std::size_t cur = 0;
+  if (cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize) == cudaSuccess && cur < want)
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+  cudaGetLastError();
+}
+
 std::size_t smem_bytes_for(std::size_t n, int W, std::size_t elem) {
   const std::size_t chunks = (n + kChunkRows - 1) / kChunkRows;
   return chunks * kChunkRows * W * elem + chunks * sizeof(uint64_t);
@@ -232,8 +273,8 @@ bool plan_persist(std::size_t n, std::size_t elem, bool pent, bool fast, int sms
   if (fac > kSmemPerBlockMax / 2) return false;
   const int tail_full_chunks = static_cast<int>((n + dev::kRT - 1) / dev::kRT);
   const int need_sys = static_cast<int>(2.0 * 1.125 * chain_cycles(pent, fast, elem));
-  int target = std::max(2, std::min(16, (need_sys + dev::kPW - 1) / dev::kPW));
-  if (const char* e = std::getenv("BANDSOLVE_PWARPS")) target = std::max(1, std::min(16, std::atoi(e)));
+  int target = std::max(2, std::min(dev::kMaxWarps, (need_sys + dev::kPW - 1) / dev::kPW));
+  if (const char* e = std::getenv("BANDSOLVE_PWARPS")) target = std::max(1, std::min(dev::kMaxWarps, std::atoi(e)));
   const int forced_tail = std::getenv("BANDSOLVE_PTAIL") ? std::atoi(std::getenv("BANDSOLVE_PTAIL")) : -1;
 
   auto fit = [&](int warps, int H, int TC) {
@@ -242,7 +283,7 @@ bool plan_persist(std::size_t n, std::size_t elem, bool pent, bool fast, int sms
   // 1) everything resident: the most warps that fit (at least `target`)
   if (forced_tail < 0) {
     int w = 0;
-    for (int k = 16; k >= 1; --k)
+    for (int k = dev::kMaxWarps; k >= 1; --k)
       if (fit(k, 0, tail_full_chunks)) {
         w = k;
         break;
@@ -263,10 +304,9 @@ bool plan_persist(std::size_t n, std::size_t elem, bool pent, bool fast, int sms
       int tail_rows = std::min<int>(static_cast<int>(n), tc * dev::kRT);
       if (forced_tail >= 0) tail_rows = std::min<int>(static_cast<int>(n), forced_tail);
       int H = static_cast<int>(n) - tail_rows;
-      H = (H + dev::kRH - 1) / dev::kRH * dev::kRH;  // head rows: whole ring chunks
-      if (H > static_cast<int>(n)) H = static_cast<int>(n) / dev::kRH * dev::kRH;
+      H = (H + dev::kHAlign - 1) / dev::kHAlign * dev::kHAlign;  // head rows: whole ring chunks / reload blocks
+      if (H > static_cast<int>(n)) H = static_cast<int>(n) / dev::kHAlign * dev::kHAlign;
       const int TC = (static_cast<int>(n) - H + dev::kRT - 1) / dev::kRT;
-      if (static_cast<int>(n) - H > 0 && H % dev::kRH != 0) continue;
       if (H + TC * dev::kRT < static_cast<int>(n)) continue;
       if (fit(warps, H, TC)) {
         best_tc = TC;
@@ -399,10 +439,25 @@ cudaError_t launch_persist(const Plan& plan, T* x, int n, long long m, long long
   const std::size_t smem = dev::PersistLayout::make(n, plan.H, plan.TC, warps, sizeof(T),
                                                     sizeof(typename dev::Recs<T, PENT>::Fwd),
                                                     sizeof(typename dev::Recs<T, PENT>::Bwd)).total;
+  // head-row spill scratch, one H x 32 block per warp, stream-ordered so
+  // concurrent launches on other streams never share it
+  T* scratch = nullptr;
+  if (plan.H > 0) {
+    const std::size_t bytes = static_cast<std::size_t>(grid) * warps * plan.H * dev::kPW * sizeof(T);
+    int device = 0;
+    if (cudaGetDevice(&device) == cudaSuccess) ensure_l2_setaside(device, bytes);
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch), bytes, s);
+    if (e != cudaSuccess) return e;
+  }
   kern<<<static_cast<unsigned>(grid), warps * 32, smem, s>>>(map_ring, map_tail, x, n, m, ld, plan.H, plan.TC,
-                                                            tiles, fwd, bwd);
+                                                            tiles, fwd, bwd, scratch);
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  return cudaGetLastError();
+  cudaError_t e = cudaGetLastError();
+  if (scratch) {
+    cudaError_t f = cudaFreeAsync(scratch, s);
+    if (e == cudaSuccess) e = f;
+  }
+  return e;
 }
 
 template <typename T, bool PENT, bool FAST>
@@ -653,6 +708,7 @@ bandsolve_status solve_device(const Factor& f, void* x, bool f32, std::size_t n,
   const int q = fast ? 1 : 0;
   auto s = static_cast<cudaStream_t>(stream);
   const int sms = num_sms(device);
+  keep_pool_memory(device);
   const Plan plan = choose_plan(n, m, ld, f32 ? 4 : 8, x, pent, fast, sms);
   cudaError_t err;
   if (f32)
