@@ -347,8 +347,14 @@ def main() -> int:
     ap.add_argument("--mode", choices=["exact", "fast"], default=os.environ.get("BANDSOLVE_BENCH_MODE", "exact"))
     ap.add_argument("--f32", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--n", type=int, default=0, help="override the config's rows per system (tuning)")
+    ap.add_argument("--m", type=int, default=0, help="override the config's systems per GPU (tuning)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.n or args.m:
+        kind, n, m, desc = CONFIGS[args.config]
+        n, m = args.n or n, args.m or m
+        CONFIGS[args.config] = (kind, n, m, f"{kind} N={n} batch={m} (tuning override of {args.config})")
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

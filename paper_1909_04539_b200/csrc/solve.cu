@@ -17,6 +17,7 @@
 #include "internal.hpp"
 #include "sweep_kernels.cuh"
 #include "sweep_persist.cuh"
+#include "sweep_stream.cuh"
 
 namespace bsb {
 
@@ -182,14 +183,18 @@ constexpr std::size_t kSmemPerBlockMax = 232448;  // 227 KB opt-in per CTA
 constexpr std::size_t kSmemReservedPerCta = 1024;
 constexpr double kSpillBudget = 64.0 * (1 << 20);  // bytes of spilled d-hat kept L2-resident (of 126 MB)
 
-enum class PlanKind { Global, Smem, Persist };
+enum class PlanKind { Global, Smem, Persist, Stream };
 
 struct Plan {
   PlanKind kind = PlanKind::Global;
   int W = 0;                 // smem: systems per CTA
   int ctas_per_sm = 0;       // smem
   int warps = 0;             // persist: warps per CTA (32 systems each)
-  int H = 0, TC = 0;         // persist: spilled head rows, tail chunks
+  int H = 0, TC = 0;         // persist/stream: spilled head rows, tail chunks
+  int Wg = 0, KB = 0, KR = 0, PD = 0;  // stream: systems per group, b / reload ring slots, L2 prefetch distance
+  int stagger_ns = 0;                  // stream: start delay of odd CTAs
+  int V = 1;                           // stream: systems per lane
+  double model_us = 0;       // stream: modelled time
   std::size_t smem_bytes = 0;
   std::string why;
 };
@@ -328,14 +333,117 @@ bool plan_persist(std::size_t n, std::size_t elem, bool pent, bool fast, int sms
   return false;
 }
 
+
+// Cycles per row-step (forward/backward average) of one warp's smem-resident
+// row loop, measured on B200 with tools/microbench/rowcost.cu (fp64); fp32
+// halves the DP latency but not the issue overhead (estimate).
+double row_cycles(bool pent, bool fast, std::size_t elem) {
+  double c = pent ? (fast ? 18.5 : 36.0) : (fast ? 12.0 : 22.0);
+  if (elem == 4) c *= 0.6;
+  return c;
+}
+
+int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
+
+// Streaming plan (sweep_stream.cuh): pick the group width Wg (systems per
+// SM in flight), the head/tail split and the ring depth that minimise a
+// simple time model: per round of groups, max(latency of one group's
+// sweeps, HBM time of the round's bytes), with spill beyond the L2 budget
+// charged as extra HBM traffic.
+bool plan_stream(std::size_t n, std::size_t m, std::size_t elem, bool pent, bool fast, int sms, Plan& p) {
+  const std::size_t fr = fwd_rec_bytes(pent, elem), br = bwd_rec_bytes(pent, elem);
+  const std::size_t fac = dev::align128(n * fr) + dev::align128(n * br);
+  if (fac > kSmemPerBlockMax / 2 || n < 2) return false;
+  const int forced_wg = env_int("BANDSOLVE_SWG", 0);
+  const int forced_tail = env_int("BANDSOLVE_STAIL", -1);
+  const int KB = std::max(1, env_int("BANDSOLVE_SKB", 4));
+  const int KR = std::max(1, env_int("BANDSOLVE_SKR", 3));
+  const int PD = std::max(0, env_int("BANDSOLVE_SPD", 8));
+  const double clk = 1.9e9, bw = 0.92 * 6.5e12;
+  const double c = row_cycles(pent, fast, elem);
+  const int N = static_cast<int>(n);
+  bool found = false;
+  double best_t = 1e300;
+  double best_spill = 1e300;
+  const int forced_v = env_int("BANDSOLVE_SV", 0);
+  for (int cand = 0; cand < 16; ++cand) {
+    const int V = cand < 8 ? 1 : 2;
+    const int P = cand < 8 ? cand + 1 : cand - 7;
+    if (P > dev::stream_max_warps(V)) continue;
+    if (forced_v && V != forced_v) continue;
+    const int Wg = 32 * V * P;
+    if (forced_wg && Wg != forced_wg) continue;
+    const long long groups = (static_cast<long long>(m) + Wg - 1) / Wg;
+    const long long grid = std::min<long long>(sms, groups);
+    auto fits = [&](int H, int TC) {
+      return dev::StreamLayout::make(N, H, TC, Wg, KB, KR, elem, fr, br).total <= kSmemPerBlockMax;
+    };
+    int H = -1;
+    const int all_tc = (N + dev::kSR - 1) / dev::kSR;
+    if (forced_tail >= 0) {
+      const int t = std::min(N, forced_tail);
+      H = (N - t + dev::kSR - 1) / dev::kSR * dev::kSR;
+      if (H > N) H = N / dev::kSR * dev::kSR;
+      if (!fits(H, (N - H + dev::kSR - 1) / dev::kSR)) continue;
+    } else if (fits(0, all_tc)) {
+      H = 0;
+    } else {
+      for (int tc = all_tc; tc >= 0; --tc) {
+        int h = (N - tc * dev::kSR + dev::kSR - 1) / dev::kSR * dev::kSR;
+        if (h < 0) h = 0;
+        if (h > N) h = N / dev::kSR * dev::kSR;
+        const int TC = (N - h + dev::kSR - 1) / dev::kSR;
+        if (fits(h, TC)) {
+          H = h;
+          break;
+        }
+      }
+    }
+    if (H < 0) continue;
+    const int TC = (N - H + dev::kSR - 1) / dev::kSR;
+    const double spill = static_cast<double>(grid) * Wg * H * elem;
+    const double over = spill > kSpillBudget ? (spill - kSpillBudget) / spill : 0.0;
+    const double bytes_row = 2.0 * elem * (1.0 + over * H / n);
+    const double lat = (2.0 * n * c * (1.0 + 0.15 * H / n) + 3000.0) / clk;
+    double t = 0;
+    for (long long done = 0; done < groups; done += grid) {
+      const double active = static_cast<double>(std::min<long long>(grid, groups - done));
+      t += std::max(lat, active * Wg * n * bytes_row / bw);
+    }
+    if (!found || t < best_t * 0.995 || (t <= best_t * 1.005 && spill < best_spill)) {
+      found = true;
+      best_t = t;
+      best_spill = spill;
+      p.kind = PlanKind::Stream;
+      p.Wg = Wg;
+      p.H = H;
+      p.TC = TC;
+      p.KB = KB;
+      p.KR = KR;
+      p.PD = PD;
+      p.stagger_ns = env_int("BANDSOLVE_SSTAG", 0);
+      p.warps = P;
+      p.model_us = t * 1e6;
+      p.smem_bytes = dev::StreamLayout::make(N, H, TC, Wg, KB, KR, elem, fr, br).total;
+      p.V = V;
+    }
+  }
+  return found;
+}
+
 Plan choose_plan(std::size_t n, std::size_t m, std::size_t ld, std::size_t elem, const void* x, bool pent,
                  bool fast, int sms) {
   Plan p;
-  // BANDSOLVE_PLAN = global | persist | smem | smemW8 | smemW16 | smemW32 (tuning / tests)
+  // BANDSOLVE_PLAN = stream | global | persist | smem | smemW8 | smemW16 | smemW32 (tuning / tests)
   const char* force = std::getenv("BANDSOLVE_PLAN");
   int forced_w = 0;
   bool force_smem = false;
+  bool force_persist = false;
   if (force) {
+    force_persist = std::strcmp(force, "persist") == 0;
     if (std::strcmp(force, "global") == 0) {
       p.why = "forced global";
       return p;
@@ -354,6 +462,7 @@ Plan choose_plan(std::size_t n, std::size_t m, std::size_t ld, std::size_t elem,
     p.why = "shape beyond 32-bit TMA coordinates";
     return p;
   }
+  if (!force_smem && !force_persist && plan_stream(n, m, elem, pent, fast, sms, p)) return p;
   if (!force_smem && plan_persist(n, elem, pent, fast, sms, p)) return p;
   int best_sys = 0;
   for (int W : {8, 16, 32}) {
@@ -460,6 +569,49 @@ cudaError_t launch_persist(const Plan& plan, T* x, int n, long long m, long long
   return e;
 }
 
+
+template <typename T, int V, bool PENT, bool FAST>
+cudaError_t launch_stream_v(const Plan& plan, T* x, int n, long long m, long long ld, const void* fwd,
+                            const void* bwd, cudaStream_t s, int sms) {
+  auto kern = dev::sweep_stream<T, V, PENT, FAST>;
+  static std::atomic<bool> configured{false};
+  if (!configured.load(std::memory_order_relaxed)) {
+    cudaError_t e = allow_big_smem(kern);
+    if (e != cudaSuccess) return e;
+    configured.store(true, std::memory_order_relaxed);
+  }
+  CUtensorMap map;
+  if (!encode_map(&map, x, sizeof(T), n, m, ld, 32 * V, dev::kSR)) return cudaErrorInvalidValue;
+  const long long groups = (m + plan.Wg - 1) / plan.Wg;
+  const long long grid = std::min<long long>(sms, groups);
+  const int P = plan.Wg / (32 * V);
+  T* scratch = nullptr;
+  if (plan.H > 0) {
+    const std::size_t bytes = static_cast<std::size_t>(grid) * plan.Wg * plan.H * sizeof(T);
+    int device = 0;
+    if (cudaGetDevice(&device) == cudaSuccess) ensure_l2_setaside(device, bytes);
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch), bytes, s);
+    if (e != cudaSuccess) return e;
+  }
+  kern<<<static_cast<unsigned>(grid), (P + 2) * 32, plan.smem_bytes, s>>>(map, x, n, m, ld, plan.H, plan.TC, plan.KB,
+                                                                         plan.KR, plan.PD, plan.stagger_ns, groups, fwd, bwd,
+                                                                         scratch);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  cudaError_t e = cudaGetLastError();
+  if (scratch) {
+    cudaError_t f = cudaFreeAsync(scratch, s);
+    if (e == cudaSuccess) e = f;
+  }
+  return e;
+}
+
+template <typename T, bool PENT, bool FAST>
+cudaError_t launch_stream(const Plan& plan, T* x, int n, long long m, long long ld, const void* fwd,
+                          const void* bwd, cudaStream_t s, int sms) {
+  if (plan.V == 2) return launch_stream_v<T, 2, PENT, FAST>(plan, x, n, m, ld, fwd, bwd, s, sms);
+  return launch_stream_v<T, 1, PENT, FAST>(plan, x, n, m, ld, fwd, bwd, s, sms);
+}
+
 template <typename T, bool PENT, bool FAST>
 cudaError_t launch_global(T* x, int n, long long m, long long ld, const void* fwd, const void* bwd,
                           cudaStream_t s) {
@@ -473,6 +625,7 @@ cudaError_t launch_global(T* x, int n, long long m, long long ld, const void* fw
 template <typename T, bool PENT, bool FAST>
 cudaError_t dispatch(const Plan& plan, T* x, int n, long long m, long long ld, const void* fwd,
                      const void* bwd, cudaStream_t s, int sms) {
+  if (plan.kind == PlanKind::Stream) return launch_stream<T, PENT, FAST>(plan, x, n, m, ld, fwd, bwd, s, sms);
   if (plan.kind == PlanKind::Persist) return launch_persist<T, PENT, FAST>(plan, x, n, m, ld, fwd, bwd, s, sms);
   if (plan.kind == PlanKind::Smem) {
     switch (plan.W) {
@@ -677,7 +830,10 @@ bandsolve_status describe_plan(Kind kind, std::size_t n, std::size_t m, std::siz
   const bool fast = current_mode() == BANDSOLVE_MODE_FAST;
   const Plan p = choose_plan(n, m, ld, f32 ? 4 : 8, kProbe, pent, fast, sms);
   char buf[256];
-  if (p.kind == PlanKind::Persist)
+  if (p.kind == PlanKind::Stream)
+    std::snprintf(buf, sizeof buf, "stream Wg=%d V=%d warps=%d+2 head(L2)=%d tail(smem)=%d rings=%d/%d pd=%d smem=%zu B model=%.1f us",
+                  p.Wg, p.V, p.warps, p.H, static_cast<int>(n) - p.H, p.KB, p.KR, p.PD, p.smem_bytes, p.model_us);
+  else if (p.kind == PlanKind::Persist)
     std::snprintf(buf, sizeof buf, "persist warps=%d systems/sm=%d head(L2)=%d tail(smem)=%d smem=%zu B", p.warps,
                   p.warps * dev::kPW, p.H, static_cast<int>(n) - p.H, p.smem_bytes);
   else if (p.kind == PlanKind::Smem)

@@ -1,0 +1,496 @@
+// Warp-specialised streaming shared-LHS sweep for sm_100a (the default plan).
+//
+// Why this shape (measured, profiles/): one thread per system walks a
+// dependent fp64 recurrence, so a row costs ~22 (tri) / ~36 (pent) cycles of
+// one warp's time in the exact arithmetic mode (tools/microbench/rowcost.cu),
+// and an SM must keep enough systems in flight to pull ~90% of HBM; every
+// system in flight owns its n forward intermediates (4 KiB at n = 512 fp64).
+// Each system's rows are therefore split:
+//
+//   head rows [0, H)   b arrives through a KB-slot TMA ring; the forward sweep
+//                      spills d-hat to an L2 scratch (evict_last, dropped
+//                      without write-back at the end); the backward sweep gets
+//                      it back through the same ring (TMA bulk copies).
+//   tail rows [H, n)   TMA-staged in shared memory, overwritten in place by
+//                      the forward sweep; the backward sweep starts here.
+//
+// HBM traffic stays at "read b once, write x once". With no spill (H = 0,
+// n <= ~256 fp64) this kernel runs at 92-97% of measured HBM bandwidth.
+//
+// Organisation: one CTA per SM, persistent over "groups" of Wg = 32 P
+// consecutive systems. P compute warps (lane = system) walk a group in
+// lockstep; one extra producer warp issues every TMA operation:
+//
+//   * smem tiles are per-warp [rows][32] blocks (256-byte rows), so every
+//     row access in the sweeps is a compile-time offset from one base
+//     register; a chunk of b is P TMA boxes {32 systems x kSR rows};
+//   * the ring is a FIFO over the CTA's element stream: per group, HC head
+//     chunks of b, then HC chunks of spilled d-hat in reverse order (one bulk
+//     copy each, issued once every compute warp has published its spill);
+//   * the producer keeps kSPD b chunks ahead of the ring in L2 with TMA
+//     prefetches, crossing into the next group while the current one is in
+//     its backward sweep, so ring loads pay L2 rather than HBM latency;
+//   * tail chunks are loaded into the slots the previous group's backward
+//     sweep frees, in reverse order on alternate groups so the chunk needed
+//     first is the one freed first;
+//   * the row loops are software-pipelined kSD rows deep ACROSS chunk
+//     boundaries (the next chunk's barrier is waited on kSD rows early).
+//
+// Arithmetic: the row formulas of sweep_kernels.cuh (exact = the reference's
+// operation order, bitwise equal; fast = one FMA per row on the chain).
+#pragma once
+
+#include "sweep_persist.cuh"
+
+namespace bsb {
+namespace dev {
+
+constexpr int kSR = 16;        // rows per chunk (ring and tail)
+constexpr int kSD = 4;         // software-pipeline depth (rows); divides kSR
+constexpr int kPR = 32;        // vectors per row of a warp block (one per lane)
+static_assert(kSR % kSD == 0, "pipeline depth must divide the chunk");
+// V = systems per lane (adjacent columns): a warp covers 32 V systems.
+__host__ __device__ constexpr int stream_max_warps(int V) { return V == 1 ? 8 : 4; }  // Wg <= 256 (TMA box)
+
+// A lane's V systems (adjacent columns V l .. V l + V-1): one 8/16-byte
+// access per row for all of them, and V independent dependency chains
+// interleaved in one instruction stream.
+template <typename T, int V>
+struct alignas(V * sizeof(T)) Vec {
+  T v[V];
+};
+template <typename T, int V, bool PENT, bool FAST>
+__device__ __forceinline__ Vec<T, V> fwd_vec(const typename Recs<T, PENT>::Fwd& r, Vec<T, V> d, Vec<T, V>& s1,
+                                             Vec<T, V>& s2) {
+  Vec<T, V> o;
+#pragma unroll
+  for (int k = 0; k < V; ++k) o.v[k] = fwd_row<T, PENT, FAST>(r, d.v[k], s1.v[k], s2.v[k]);
+  return o;
+}
+template <typename T, int V, bool PENT, bool FAST>
+__device__ __forceinline__ Vec<T, V> bwd_vec(const typename Recs<T, PENT>::Bwd& r, Vec<T, V> g, Vec<T, V>& s1,
+                                             Vec<T, V>& s2) {
+  Vec<T, V> o;
+#pragma unroll
+  for (int k = 0; k < V; ++k) o.v[k] = bwd_row<T, PENT, FAST>(r, g.v[k], s1.v[k], s2.v[k]);
+  return o;
+}
+template <typename T, int V>
+__device__ __forceinline__ void st_spill_vec(Vec<T, V>* p, Vec<T, V> v, uint64_t pol) {
+  if constexpr (V == 1) {
+    st_spill(&p->v[0], v.v[0], pol);
+  } else if constexpr (sizeof(T) == 8) {
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.v[0]),
+                 "d"(v.v[1]), "l"(pol)
+                 : "memory");
+  } else {
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(p), "f"(v.v[0]),
+                 "f"(v.v[1]), "l"(pol)
+                 : "memory");
+  }
+}
+template <typename T, int V>
+__device__ __forceinline__ void st_stream_vec(Vec<T, V>* p, Vec<T, V> v) {
+  if constexpr (V == 1) st_stream(&p->v[0], v.v[0]);
+  else if constexpr (sizeof(T) == 8) __stcs(reinterpret_cast<double2*>(p), make_double2(v.v[0], v.v[1]));
+  else __stcs(reinterpret_cast<float2*>(p), make_float2(v.v[0], v.v[1]));
+}
+
+struct StreamLayout {
+  size_t fwd_off, bwd_off, bring_off, rring_off, tail_off, bar_off, total;
+  // chunk: elements of one chunk (all warps) = kSR x Wg
+  __host__ __device__ static StreamLayout make(int n, int H, int TC, int Wg, int KB, int KR, size_t elem,
+                                               size_t fwd_rec, size_t bwd_rec) {
+    StreamLayout L{};
+    L.fwd_off = 0;
+    L.bwd_off = align128(static_cast<size_t>(n) * fwd_rec);
+    L.bring_off = L.bwd_off + align128(static_cast<size_t>(n) * bwd_rec);
+    const size_t chunk = static_cast<size_t>(kSR) * Wg * elem;
+    L.rring_off = L.bring_off + (H > 0 ? static_cast<size_t>(KB) * chunk : 0);
+    L.tail_off = L.rring_off + (H > 0 ? static_cast<size_t>(KR) * chunk : 0);
+    L.bar_off = L.tail_off + static_cast<size_t>(TC) * chunk;
+    L.total = L.bar_off + static_cast<size_t>(2 * KB + 2 * KR + 2 * TC + 1) * sizeof(uint64_t);
+    return L;
+  }
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
+
+// Forward sweep over C consecutive kSR-row chunks in ascending row order,
+// on this lane's pair of systems. base(c): the lane's row-0 pair of chunk c
+// (row r at +r*kPR pairs); ready(c) blocks until chunk c may be read;
+// release(c) is called once chunk c is no longer read; sink(c, r, p, v)
+// consumes row r's result (p = its smem pair). f: the records of chunk 0's
+// first row (chunk c at +c*kSR).
+template <typename T, int V, bool PENT, bool FAST, typename Base, typename Ready, typename Release, typename Sink>
+__device__ __forceinline__ void fwd_chunks(int C, const typename Recs<T, PENT>::Fwd* f, Vec<T, V>& s1, Vec<T, V>& s2,
+                                           Base&& base, Ready&& ready, Release&& release, Sink&& sink) {
+  using FwdR = typename Recs<T, PENT>::Fwd;
+  if (C <= 0) return;
+  Vec<T, V> dq[kSD];
+  FwdR fq[kSD];
+  ready(0);
+  Vec<T, V>* p = base(0);
+#pragma unroll
+  for (int k = 0; k < kSD; ++k) {
+    dq[k] = p[k * kPR];
+    fq[k] = f[k];
+  }
+  for (int c = 0; c < C; ++c) {
+    const bool more = c + 1 < C;
+    Vec<T, V>* pn = p;
+    const FwdR* fc = f + c * kSR;
+#pragma unroll
+    for (int r = 0; r < kSR; ++r) {
+      if (r == kSR - kSD && more) {
+        ready(c + 1);
+        pn = base(c + 1);
+      }
+      const Vec<T, V> v = fwd_vec<T, V, PENT, FAST>(fq[r % kSD], dq[r % kSD], s1, s2);
+      const int rn = r + kSD;
+      if (rn < kSR) {
+        dq[r % kSD] = p[rn * kPR];
+        fq[r % kSD] = fc[rn];
+      } else if (more) {
+        dq[r % kSD] = pn[(rn - kSR) * kPR];
+        fq[r % kSD] = fc[rn];
+      }
+      sink(c, r, p + r * kPR, v);
+    }
+    release(c);
+    p = pn;
+  }
+}
+
+// Backward sweep over chunks C-1 .. 0, rows descending. Same callbacks;
+// b: the records of chunk 0's first row.
+template <typename T, int V, bool PENT, bool FAST, typename Base, typename Ready, typename Release, typename Sink>
+__device__ __forceinline__ void bwd_chunks(int C, const typename Recs<T, PENT>::Bwd* b, Vec<T, V>& s1, Vec<T, V>& s2,
+                                           Base&& base, Ready&& ready, Release&& release, Sink&& sink) {
+  using BwdR = typename Recs<T, PENT>::Bwd;
+  if (C <= 0) return;
+  Vec<T, V> dq[kSD];
+  BwdR bq[kSD];
+  ready(C - 1);
+  const Vec<T, V>* p = base(C - 1);
+  const BwdR* bc0 = b + (C - 1) * kSR;
+#pragma unroll
+  for (int k = 0; k < kSD; ++k) {
+    dq[k] = p[(kSR - 1 - k) * kPR];
+    bq[k] = bc0[kSR - 1 - k];
+  }
+  for (int c = C - 1; c >= 0; --c) {
+    const bool more = c > 0;
+    const Vec<T, V>* pn = p;
+    const BwdR* bc = b + c * kSR;
+#pragma unroll
+    for (int q = 0; q < kSR; ++q) {  // q-th processed row is r = kSR-1-q
+      if (q == kSR - kSD && more) {
+        ready(c - 1);
+        pn = base(c - 1);
+      }
+      const Vec<T, V> v = bwd_vec<T, V, PENT, FAST>(bq[q % kSD], dq[q % kSD], s1, s2);
+      const int qn = q + kSD;
+      if (qn < kSR) {
+        dq[q % kSD] = p[(kSR - 1 - qn) * kPR];
+        bq[q % kSD] = bc[kSR - 1 - qn];
+      } else if (more) {
+        dq[q % kSD] = pn[(2 * kSR - 1 - qn) * kPR];
+        bq[q % kSD] = bc[kSR - 1 - qn];  // = records of chunk c-1, row 2kSR-1-qn
+      }
+      sink(c, kSR - 1 - q, v);
+    }
+    release(c);
+    p = pn;
+  }
+}
+
+// Ring cursor: slot index and mbarrier phase of the next element.
+struct Cursor {
+  uint32_t slot = 0, phase = 0;
+  __device__ __forceinline__ void next(int K) {
+    if (++slot == static_cast<uint32_t>(K)) {
+      slot = 0;
+      phase ^= 1u;
+    }
+  }
+};
+
+template <typename T, int V, bool PENT, bool FAST>
+__global__ void __launch_bounds__(32 * (stream_max_warps(V) + 2), 1)
+    sweep_stream(const __grid_constant__ CUtensorMap map_b, T* __restrict__ x, int n, long long m, long long ld,
+                 int H, int TC, int KB, int KR, int PD, int stagger_ns, long long groups,
+                 const void* __restrict__ fwd_g, const void* __restrict__ bwd_g, T* __restrict__ scratch) {
+  using FwdR = typename Recs<T, PENT>::Fwd;
+  using BwdR = typename Recs<T, PENT>::Bwd;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int P = static_cast<int>(blockDim.x >> 5) - 2;  // compute warps; warp P loads b, warp P+1 reloads
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const StreamLayout L = StreamLayout::make(n, H, TC, P * 32 * V, KB, KR, sizeof(T), sizeof(FwdR), sizeof(BwdR));
+  const FwdR* sf = reinterpret_cast<const FwdR*>(smem + L.fwd_off);
+  const BwdR* sb = reinterpret_cast<const BwdR*>(smem + L.bwd_off);
+  T* bring = reinterpret_cast<T*>(smem + L.bring_off);
+  T* rring = reinterpret_cast<T*>(smem + L.rring_off);
+  T* tail = reinterpret_cast<T*>(smem + L.tail_off);
+  uint64_t* b_full = reinterpret_cast<uint64_t*>(smem + L.bar_off);
+  uint64_t* b_empty = b_full + KB;
+  uint64_t* r_full = b_empty + KB;
+  uint64_t* r_empty = r_full + KR;
+  uint64_t* t_full = r_empty + KR;
+  uint64_t* t_empty = t_full + TC;
+  uint64_t* spilled = t_empty + TC;  // completes once per group when all warps' spills are published
+  const int HC = H / kSR;
+  constexpr int kLW = 32 * V;      // systems per warp
+  constexpr int kSBlk = kSR * kLW;  // elements of one warp's block of one chunk
+  const int Wg = P * kLW;
+  const int chunk = P * kSBlk;  // elements of one chunk (all warps)
+  // this CTA's spill scratch: HC chunks x P warps x (kSR x 32), reused by every group
+  T* const spill_cta = scratch + static_cast<long long>(blockIdx.x) * HC * chunk;
+
+  {  // factor records -> smem (16-byte words; device arrays padded to 256 B)
+    const int nf = static_cast<int>((static_cast<size_t>(n) * sizeof(FwdR) + 15) / 16);
+    const int nb = static_cast<int>((static_cast<size_t>(n) * sizeof(BwdR) + 15) / 16);
+    const int4* gf = static_cast<const int4*>(fwd_g);
+    const int4* gb = static_cast<const int4*>(bwd_g);
+    int4* df = reinterpret_cast<int4*>(smem + L.fwd_off);
+    int4* db = reinterpret_cast<int4*>(smem + L.bwd_off);
+    for (int k = threadIdx.x; k < nf; k += blockDim.x) df[k] = gf[k];
+    for (int k = threadIdx.x; k < nb; k += blockDim.x) db[k] = gb[k];
+  }
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < KB; ++k) {
+      mbar_init(&b_full[k], 1);
+      mbar_init(&b_empty[k], P);
+    }
+    for (int k = 0; k < KR; ++k) {
+      mbar_init(&r_full[k], 1);
+      mbar_init(&r_empty[k], P);
+    }
+    for (int k = 0; k < TC; ++k) {
+      mbar_init(&t_full[k], 1);
+      mbar_init(&t_empty[k], P);
+    }
+    mbar_init(spilled, P);
+    fence_barrier_init();
+  }
+  // Every CTA runs the same phases (forward: no HBM traffic for x, backward:
+  // x stores plus the next group's loads); odd CTAs start half a period late
+  // so the two halves of the GPU interleave their bursts.
+  if ((blockIdx.x & 1) && stagger_ns > 0) {
+    for (int t = 0; t < stagger_ns; t += 1000) __nanosleep(1000);
+  }
+  __syncthreads();
+
+  // tail chunk k of the group with iteration parity `par` lives in slot
+  // par ? TC-1-k : k
+  auto tail_slot = [TC](int k, uint32_t par) { return par ? TC - 1 - k : k; };
+  const uint32_t c_bytes = static_cast<uint32_t>(chunk * sizeof(T));
+
+  // ----------------------------------------------------- loader warp (b, tail)
+  // Order per group g: the first min(KB, HC) head chunks (their slots were
+  // freed by group g-1's forward head, so they load during g-1's tail and
+  // backward sweeps), then g's tail (slots freed by g-1's backward tail),
+  // then the remaining head chunks as g's own forward sweep drains the ring.
+  if (warp == P) {
+    if (lane != 0) return;
+    const uint64_t pol_b = policy_evict_first();  // every byte of b is read once
+    const long long my_groups = (groups - blockIdx.x + gridDim.x - 1) / gridDim.x;
+    const long long b_total = my_groups * HC;  // b chunks this CTA streams through the ring
+    long long b_next = 0;                      // next b chunk (CTA-local index) to enter the ring
+    long long b_pf = 0;                        // b chunks prefetched into L2 so far
+    Cursor cur;
+    uint32_t issued = 0;
+    auto load_chunk = [&](T* dst, int c0, int row, uint64_t* bar) {
+      mbar_expect_tx(bar, c_bytes);
+      for (int w = 0; w < P; ++w) tma_load_2d(dst + w * kSBlk, &map_b, c0 + w * kLW, row, bar, pol_b);
+    };
+    auto prefetch = [&]() {
+      while (b_pf < b_total && b_pf < b_next + PD) {
+        const long long gi = b_pf / HC;
+        const int c = static_cast<int>(b_pf - gi * HC);
+        const int c0 = static_cast<int>((blockIdx.x + gi * gridDim.x) * Wg);
+        for (int w = 0; w < P; ++w) tma_prefetch_2d(&map_b, c0 + w * kLW, c * kSR);
+        ++b_pf;
+      }
+    };
+    uint32_t it = 0;
+    for (long long g = blockIdx.x; g < groups; g += gridDim.x, ++it) {
+      const int c0 = static_cast<int>(g * Wg);
+      const uint32_t par = it & 1u;
+      const int pre = HC < KB ? HC : KB;
+      auto load_tail = [&]() {
+        for (int k = 0; k < TC; ++k) {
+          const int s = tail_slot(k, par);
+          if (it > 0) mbar_wait(&t_empty[s], (it - 1) & 1u);
+          load_chunk(tail + s * chunk, c0, H + k * kSR, &t_full[s]);
+        }
+      };
+      for (int c = 0; c < HC; ++c) {
+        if (c == pre) load_tail();
+        if (issued >= static_cast<uint32_t>(KB)) mbar_wait(&b_empty[cur.slot], cur.phase ^ 1u);
+        load_chunk(bring + cur.slot * chunk, c0, c * kSR, &b_full[cur.slot]);
+        cur.next(KB);
+        ++issued;
+        ++b_next;
+        prefetch();
+      }
+      if (pre == HC) load_tail();
+    }
+    return;
+  }
+
+  // ------------------------------------------------ reloader warp (spilled d-hat)
+  if (warp == P + 1) {
+    if (lane != 0 || HC == 0) return;
+    const uint64_t pol_keep = policy_evict_last();
+    Cursor cur;
+    uint32_t issued = 0;
+    uint32_t it = 0;
+    for (long long g = blockIdx.x; g < groups; g += gridDim.x, ++it) {
+      mbar_wait(spilled, it & 1u);  // every warp's head d-hat of this group is in the scratch
+      for (int c = HC - 1; c >= 0; --c) {
+        if (issued >= static_cast<uint32_t>(KR)) mbar_wait(&r_empty[cur.slot], cur.phase ^ 1u);
+        mbar_expect_tx(&r_full[cur.slot], c_bytes);
+        bulk_load(rring + cur.slot * chunk, spill_cta + static_cast<long long>(c) * chunk, c_bytes,
+                  &r_full[cur.slot], pol_keep);
+        cur.next(KR);
+        ++issued;
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------ compute warps
+  using P2 = Vec<T, V>;  // a lane's V systems
+  const uint64_t pol_keep = policy_evict_last();
+  const int wl = warp * (kSBlk / V) + lane;  // this lane's vector offset within a chunk
+  const int cpairs = chunk / V;              // vectors per chunk
+  P2* const bring_l = reinterpret_cast<P2*>(bring) + wl;
+  P2* const rring_l = reinterpret_cast<P2*>(rring) + wl;
+  P2* const tail_l = reinterpret_cast<P2*>(tail) + wl;
+  P2* const spill_l = reinterpret_cast<P2*>(spill_cta) + wl;
+  const int tfull = (n - H) / kSR;  // full tail chunks (a partial one may follow)
+  const int trem = (n - H) - tfull * kSR;
+  Cursor bw, brl, rw, rrl;  // wait / release cursors of the two rings
+  uint32_t it = 0;
+
+  long long g = blockIdx.x;
+  // One group. kFull: every column of the group exists (all groups but
+  // possibly the last), so the x stores are unconditional 16-byte stores.
+  auto run_group = [&](auto full_tag) {
+    constexpr bool kFull = decltype(full_tag)::value;
+    const long long j = g * Wg + warp * kLW + V * lane;  // this lane's first column
+    const bool live2 = kFull || j + V - 1 < m;           // all V columns exist
+    const bool live1 = kFull || j < m;                   // the first one does
+    const uint32_t par = it & 1u;
+    T* out = x + (live1 ? j : 0) + static_cast<long long>(n - 1) * ld;
+    auto put = [&](P2 v) {
+      if (kFull) {
+        st_stream_vec<T, V>(reinterpret_cast<P2*>(out), v);
+      } else {
+        if (live2) st_stream_vec<T, V>(reinterpret_cast<P2*>(out), v);
+        else if (live1) st_stream(out, v.v[0]);
+      }
+      out -= ld;
+    };
+    P2 s1{}, s2{};
+
+    // ---- forward, head rows: b ring -> registers -> d-hat spilled to L2
+    {
+      uint32_t cs = 0;
+      fwd_chunks<T, V, PENT, FAST>(
+          HC, sf, s1, s2, [&](int) { return bring_l + cs * cpairs; },
+          [&](int) {
+            cs = bw.slot;
+            mbar_wait(&b_full[bw.slot], bw.phase);
+            bw.next(KB);
+          },
+          [&](int) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&b_empty[brl.slot]);
+            brl.next(KB);
+          },
+          [&](int c, int r, P2*, P2 v) { st_spill_vec<T, V>(spill_l + c * cpairs + r * kPR, v, pol_keep); });
+    }
+    if (HC > 0) {  // publish the spill to the async proxy (the reloader's bulk copies)
+      fence_proxy_async_global();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(spilled);
+    }
+
+    // ---- forward, tail rows: in place in smem
+    auto tslot = [&](int k) { return tail_l + tail_slot(k, par) * cpairs; };
+    fwd_chunks<T, V, PENT, FAST>(
+        tfull, sf + H, s1, s2, tslot, [&](int k) { mbar_wait(&t_full[tail_slot(k, par)], par); }, [](int) {},
+        [](int, int, P2* p, P2 v) { *p = v; });
+    if (trem > 0) {
+      mbar_wait(&t_full[tail_slot(tfull, par)], par);
+      P2* p = tslot(tfull);
+      const FwdR* f = sf + H + tfull * kSR;
+      for (int r = 0; r < trem; ++r) p[r * kPR] = fwd_vec<T, V, PENT, FAST>(f[r], p[r * kPR], s1, s2);
+    }
+    fence_proxy_async_smem();  // in-place smem writes before the TMA refills of these slots
+
+    // ---- backward, tail rows: smem -> x streamed to HBM; each drained chunk
+    // goes back to the loader for the next group
+    s1 = P2{};
+    s2 = P2{};
+    auto tail_release = [&](int k) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&t_empty[tail_slot(k, par)]);
+    };
+    if (trem > 0) {
+      const P2* p = tslot(tfull);
+      const BwdR* b = sb + H + tfull * kSR;
+      for (int r = trem - 1; r >= 0; --r) put(bwd_vec<T, V, PENT, FAST>(b[r], p[r * kPR], s1, s2));
+      tail_release(tfull);
+    }
+    bwd_chunks<T, V, PENT, FAST>(
+        tfull, sb + H, s1, s2, [&](int k) -> const P2* { return tslot(k); }, [](int) {}, tail_release,
+        [&](int, int, P2 v) { put(v); });
+
+    // ---- backward, head rows: d-hat back through the reload ring, x to HBM
+    {
+      uint32_t cs = 0;
+      bwd_chunks<T, V, PENT, FAST>(
+          HC, sb, s1, s2, [&](int) -> const P2* { return rring_l + cs * cpairs; },
+          [&](int) {
+            cs = rw.slot;
+            mbar_wait(&r_full[rw.slot], rw.phase);
+            rw.next(KR);
+          },
+          [&](int) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&r_empty[rrl.slot]);
+            rrl.next(KR);
+          },
+          [&](int, int, P2 v) { put(v); });
+    }
+  };
+  for (; g < groups; g += gridDim.x, ++it) {
+    if ((g + 1) * Wg <= m) run_group(std::true_type{});
+    else run_group(std::false_type{});
+  }
+
+  // the scratch is dead: drop this warp's L2 lines instead of writing them back
+  if (HC > 0) {
+    __syncwarp();
+    for (int c = 0; c < HC; ++c) {
+      const char* base = reinterpret_cast<const char*>(spill_cta + static_cast<long long>(c) * chunk + warp * kSBlk);
+      for (int off = lane * 128; off < kSBlk * static_cast<int>(sizeof(T)); off += 32 * 128)
+        discard_l2_line(base + off);
+    }
+  }
+}
+
+}  // namespace dev
+}  // namespace bsb

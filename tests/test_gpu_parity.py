@@ -137,15 +137,28 @@ def test_cyclic_residual_matches_oracle(lib, oracle, cuda_device):
 # ---- device entry points over every plan and edge shape -----------------------------
 SHAPES = [(2, 1), (3, 2), (5, 3), (31, 7), (32, 16), (33, 17), (64, 8), (65, 40), (100, 33), (257, 130),
           (512, 64), (1024, 48)]
-# plan overrides: (BANDSOLVE_PLAN, BANDSOLVE_PWARPS, BANDSOLVE_PTAIL)
+# plan overrides: (BANDSOLVE_PLAN, BANDSOLVE_PWARPS, BANDSOLVE_PTAIL) for the persist/smem/global
+# plans; "stream" takes (BANDSOLVE_SWG, BANDSOLVE_STAIL, BANDSOLVE_SKB): group width, smem tail
+# rows, ring slots.
 PLANS = [None, ("global",), ("smemW8",), ("smemW16",), ("smemW32",), ("persist", "1", "0"),
-         ("persist", "2", "48"), ("persist", "3", "100000")]
+         ("persist", "2", "48"), ("persist", "3", "100000"),
+         ("stream", "64", "0", "4", "2"), ("stream", "64", "16", "2", "1"), ("stream", "128", "40", "4", "2"),
+         ("stream", "256", "100000", "4", "1"), ("stream", "192", "33", "2", "2"), ("stream", "96", "48", "3", "1"),
+         ("stream", "32", "0", "4", "1")]
+PLAN_ENV = ("BANDSOLVE_PLAN", "BANDSOLVE_PWARPS", "BANDSOLVE_PTAIL", "BANDSOLVE_SWG", "BANDSOLVE_STAIL",
+            "BANDSOLVE_SKB", "BANDSOLVE_SV")
 
 
 def set_plan(plan):
-    for k in ("BANDSOLVE_PLAN", "BANDSOLVE_PWARPS", "BANDSOLVE_PTAIL"):
+    for k in PLAN_ENV:
         os.environ.pop(k, None)
-    if plan:
+    if not plan:
+        return
+    if plan[0] == "stream":
+        os.environ["BANDSOLVE_PLAN"] = "stream"
+        for k, v in zip(("BANDSOLVE_SWG", "BANDSOLVE_STAIL", "BANDSOLVE_SKB", "BANDSOLVE_SV"), plan[1:]):
+            os.environ[k] = v
+    else:
         for k, v in zip(("BANDSOLVE_PLAN", "BANDSOLVE_PWARPS", "BANDSOLVE_PTAIL"), plan):
             os.environ[k] = v
 
@@ -186,7 +199,7 @@ def test_pent_device_plans_bitwise(lib, oracle, cuda_device, plan):
         assert bitwise_equal(dev_solve(torch, u, rhs), want_u), (plan, n, m)
 
 
-@pytest.mark.parametrize("plan", [None, ("global",), ("persist", "2", "0")])
+@pytest.mark.parametrize("plan", [None, ("global",), ("persist", "2", "0"), ("stream", "64", "48", "4", "2"), ("stream", "96", "48", "4", "1")])
 def test_fast_mode_within_tolerance(lib, oracle, cuda_device, plan):
     torch = cuda_device
     rng = np.random.default_rng(300)
