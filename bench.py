@@ -224,6 +224,14 @@ def load_traffic(config: str, mode: str) -> float | None:
         return None
 
 
+def kernel_name(plan: str, f32: bool, kind: str, mode: str) -> str:
+    """Name of the sweep kernel the plan launches (what ncu lists)."""
+    k = plan.split()[0] if plan else "?"
+    name = {"stream": "sweep_stream", "regs": "sweep_regs", "persist": "sweep_persist",
+            "smem-tma": "sweep_smem", "global-inplace": "sweep_global"}.get(k, k)
+    return f"{name}<{'float' if f32 else 'double'},{kind},{mode}>"
+
+
 def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
     import torch
     import torch.distributed as dist
@@ -286,6 +294,7 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
     achieved = algo_bytes / (ms_local / args.steps / 1e3) / 1e9
     peak, peak_src = load_peak()
     traffic = load_traffic(args.config, args.mode)
+    plan = lib.describe_plan(0 if kind == "tri" else 1, n, m, m, args.f32)
 
     # e2e through the reference-facing host API (pinned host batch; H2D,
     # sweep, D2H inside bandsolve_*_solve_shared, synchronous)
@@ -321,14 +330,14 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
             "vs_baseline": None, "dtype": "f32" if args.f32 else "f64",
             "data": "synthetic: U(-1,1) RHS from SplitMix64(seed=42, i, global j), generated on device",
             "config": {"workload": desc, "kind": kind, "n": n, "batch_per_gpu": m, "global_batch": m * world,
-                       "mode": args.mode, "plan": lib.describe_plan(0 if kind == "tri" else 1, n, m, m, args.f32),
+                       "mode": args.mode, "plan": plan,
                        "parallelism": f"dp{world} (systems sharded, no data-path collective)",
                        "l2": f"{nbuf} rotating in-place buffers of {bytes_per / 2**20:.0f} MiB "
                              f"(working set {nbuf * bytes_per / 132644864:.1f}x L2)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_bytes_per_launch": algo_bytes, "peak_source": peak_src,
-                         "kernel": f"sweep_smem<{'float' if args.f32 else 'double'},{kind}>"},
+                         "kernel": kernel_name(plan, args.f32, kind, args.mode)},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,

@@ -18,6 +18,7 @@
 #include "sweep_kernels.cuh"
 #include "sweep_persist.cuh"
 #include "sweep_stream.cuh"
+#include "sweep_regs.cuh"
 
 namespace bsb {
 
@@ -183,7 +184,7 @@ constexpr std::size_t kSmemPerBlockMax = 232448;  // 227 KB opt-in per CTA
 constexpr std::size_t kSmemReservedPerCta = 1024;
 constexpr double kSpillBudget = 64.0 * (1 << 20);  // bytes of spilled d-hat kept L2-resident (of 126 MB)
 
-enum class PlanKind { Global, Smem, Persist, Stream };
+enum class PlanKind { Global, Smem, Persist, Stream, Regs };
 
 struct Plan {
   PlanKind kind = PlanKind::Global;
@@ -334,13 +335,32 @@ bool plan_persist(std::size_t n, std::size_t elem, bool pent, bool fast, int sms
 }
 
 
-// Cycles per row-step (forward/backward average) of one warp's smem-resident
-// row loop, measured on B200 with tools/microbench/rowcost.cu (fp64); fp32
-// halves the DP latency but not the issue overhead (estimate).
-double row_cycles(bool pent, bool fast, std::size_t elem) {
-  double c = pent ? (fast ? 18.5 : 36.0) : (fast ? 12.0 : 22.0);
-  if (elem == 4) c *= 0.6;
-  return c;
+// Measured fraction of HBM bandwidth the streaming kernel reaches with S
+// systems per SM and no spill (B200, n = 256, 2^21 systems, V = 1, KR = 4;
+// tools/gpu_calib.sh). Below S = 64 a warp's recurrence latency, not HBM,
+// bounds the SM, so the fraction scales with S.
+double stream_compute_frac(int S, bool pent, bool fast) {
+  const double f64 = pent ? (fast ? 0.80 : 0.60) : (fast ? 0.93 : 0.72);
+  const double f96 = pent ? (fast ? 0.82 : 0.87) : (fast ? 0.82 : 0.84);
+  if (S <= 64) return f64 * S / 64.0;
+  if (S <= 96) return f64 + (f96 - f64) * (S - 64) / 32.0;
+  return f96 * (1.0 - 0.04 * (S - 96) / 32.0);
+}
+
+// Measured slowdown from the d-hat spill (total MB over all SMs): any spill
+// costs ~20% (ring waits on L2 round trips); beyond ~45 MB the spill no
+// longer stays L2-resident alongside the b/x streams and it falls off
+// quickly (n = 512 / 1024 sweeps, tools/gpu_calib.sh).
+double stream_spill_factor(double spill_mb) {
+  static const double pts[][2] = {{0, 1.0}, {1, 0.82}, {45, 0.80}, {57, 0.74}, {65, 0.60}, {98, 0.43}, {200, 0.25}};
+  const int np = sizeof(pts) / sizeof(pts[0]);
+  if (spill_mb >= pts[np - 1][0]) return pts[np - 1][1];
+  for (int k = 1; k < np; ++k)
+    if (spill_mb <= pts[k][0]) {
+      const double t = (spill_mb - pts[k - 1][0]) / (pts[k][0] - pts[k - 1][0]);
+      return pts[k - 1][1] + t * (pts[k][1] - pts[k - 1][1]);
+    }
+  return pts[np - 1][1];
 }
 
 int env_int(const char* name, int dflt) {
@@ -348,11 +368,11 @@ int env_int(const char* name, int dflt) {
   return e ? std::atoi(e) : dflt;
 }
 
-// Streaming plan (sweep_stream.cuh): pick the group width Wg (systems per
-// SM in flight), the head/tail split and the ring depth that minimise a
-// simple time model: per round of groups, max(latency of one group's
-// sweeps, HBM time of the round's bytes), with spill beyond the L2 budget
-// charged as extra HBM traffic.
+// Streaming plan (sweep_stream.cuh): pick the systems per lane V, the group
+// width Wg (systems per SM in flight), the head/tail split and the ring
+// depths that maximise the calibrated throughput estimate
+//   frac = compute(S) x spill_factor(spill) x (round utilisation),
+// preferring the smaller spill on ties.
 bool plan_stream(std::size_t n, std::size_t m, std::size_t elem, bool pent, bool fast, int sms, Plan& p) {
   const std::size_t fr = fwd_rec_bytes(pent, elem), br = bwd_rec_bytes(pent, elem);
   const std::size_t fac = dev::align128(n * fr) + dev::align128(n * br);
@@ -360,10 +380,8 @@ bool plan_stream(std::size_t n, std::size_t m, std::size_t elem, bool pent, bool
   const int forced_wg = env_int("BANDSOLVE_SWG", 0);
   const int forced_tail = env_int("BANDSOLVE_STAIL", -1);
   const int KB = std::max(1, env_int("BANDSOLVE_SKB", 4));
-  const int KR = std::max(1, env_int("BANDSOLVE_SKR", 3));
+  const int KR = std::max(1, env_int("BANDSOLVE_SKR", 4));
   const int PD = std::max(0, env_int("BANDSOLVE_SPD", 8));
-  const double clk = 1.9e9, bw = 0.92 * 6.5e12;
-  const double c = row_cycles(pent, fast, elem);
   const int N = static_cast<int>(n);
   bool found = false;
   double best_t = 1e300;
@@ -405,14 +423,11 @@ bool plan_stream(std::size_t n, std::size_t m, std::size_t elem, bool pent, bool
     if (H < 0) continue;
     const int TC = (N - H + dev::kSR - 1) / dev::kSR;
     const double spill = static_cast<double>(grid) * Wg * H * elem;
-    const double over = spill > kSpillBudget ? (spill - kSpillBudget) / spill : 0.0;
-    const double bytes_row = 2.0 * elem * (1.0 + over * H / n);
-    const double lat = (2.0 * n * c * (1.0 + 0.15 * H / n) + 3000.0) / clk;
-    double t = 0;
-    for (long long done = 0; done < groups; done += grid) {
-      const double active = static_cast<double>(std::min<long long>(grid, groups - done));
-      t += std::max(lat, active * Wg * n * bytes_row / bw);
-    }
+    const double rounds = static_cast<double>(m) / (static_cast<double>(Wg) * sms);
+    const double util = rounds / std::ceil(rounds);
+    const double frac = stream_compute_frac(Wg, pent, fast) * (V == 2 ? 0.95 : 1.0) *
+                        stream_spill_factor(spill / (1 << 20)) * util;
+    const double t = static_cast<double>(n) * m * 2.0 * elem / (frac * 6.5e12);
     if (!found || t < best_t * 0.995 || (t <= best_t * 1.005 && spill < best_spill)) {
       found = true;
       best_t = t;
@@ -432,6 +447,42 @@ bool plan_stream(std::size_t n, std::size_t m, std::size_t elem, bool pent, bool
     }
   }
   return found;
+}
+
+
+// Register-streamed plan (sweep_regs.cuh): Wg = 32 P systems per SM, the
+// longest smem tail that fits, the rest of the rows (a multiple of 16) in
+// the L2 scratch.
+bool plan_regs(std::size_t n, std::size_t m, std::size_t elem, bool pent, int sms, int P, Plan& p) {
+  const std::size_t fr = fwd_rec_bytes(pent, elem), br = bwd_rec_bytes(pent, elem);
+  const std::size_t fac = dev::align128(n * fr) + dev::align128(n * br);
+  if (fac > kSmemPerBlockMax / 2 || n < 2 || P < 1 || P > dev::kRMaxWarps) return false;
+  const int N = static_cast<int>(n);
+  const int Wg = 32 * P;
+  const int forced_tail = env_int("BANDSOLVE_STAIL", -1);
+  for (int tc = (N + dev::kSR - 1) / dev::kSR; tc >= 0; --tc) {
+    int h = std::max(0, N - tc * dev::kSR);
+    h = (h + dev::kSR - 1) / dev::kSR * dev::kSR;
+    if (forced_tail >= 0) h = (std::max(0, N - forced_tail) + dev::kSR - 1) / dev::kSR * dev::kSR;
+    if (h > N) h = N / dev::kSR * dev::kSR;
+    const int TC = (N - h + dev::kSR - 1) / dev::kSR;
+    const std::size_t bytes = dev::RegsLayout::make(N, TC, Wg, elem, fr, br).total;
+    if (bytes <= kSmemPerBlockMax) {
+      p.kind = PlanKind::Regs;
+      p.Wg = Wg;
+      p.warps = P;
+      p.H = h;
+      p.TC = TC;
+      p.V = 1;
+      p.KB = std::max(4, std::min(6, env_int("BANDSOLVE_SNB", pent ? 4 : 6)));  // register pipeline blocks
+      p.smem_bytes = bytes;
+      const long long groups = (static_cast<long long>(m) + Wg - 1) / Wg;
+      p.model_us = static_cast<double>(std::min<long long>(sms, groups)) * Wg * h * elem / 1e6;  // spill MB
+      return true;
+    }
+    if (forced_tail >= 0) return false;
+  }
+  return false;
 }
 
 Plan choose_plan(std::size_t n, std::size_t m, std::size_t ld, std::size_t elem, const void* x, bool pent,
@@ -462,6 +513,9 @@ Plan choose_plan(std::size_t n, std::size_t m, std::size_t ld, std::size_t elem,
     p.why = "shape beyond 32-bit TMA coordinates";
     return p;
   }
+  if (force && std::strcmp(force, "regs") == 0 &&
+      plan_regs(n, m, elem, pent, sms, std::max(1, env_int("BANDSOLVE_SWG", 96) / 32), p))
+    return p;
   if (!force_smem && !force_persist && plan_stream(n, m, elem, pent, fast, sms, p)) return p;
   if (!force_smem && plan_persist(n, elem, pent, fast, sms, p)) return p;
   int best_sys = 0;
@@ -612,6 +666,51 @@ cudaError_t launch_stream(const Plan& plan, T* x, int n, long long m, long long 
   return launch_stream_v<T, 1, PENT, FAST>(plan, x, n, m, ld, fwd, bwd, s, sms);
 }
 
+
+template <typename T, bool PENT, bool FAST, int NB>
+cudaError_t launch_regs_nb(const Plan& plan, T* x, int n, long long m, long long ld, const void* fwd,
+                           const void* bwd, cudaStream_t s, int sms);
+template <typename T, bool PENT, bool FAST>
+cudaError_t launch_regs(const Plan& plan, T* x, int n, long long m, long long ld, const void* fwd,
+                        const void* bwd, cudaStream_t s, int sms) {
+  if (plan.KB == 6) return launch_regs_nb<T, PENT, FAST, 6>(plan, x, n, m, ld, fwd, bwd, s, sms);
+  if (plan.KB == 5) return launch_regs_nb<T, PENT, FAST, 5>(plan, x, n, m, ld, fwd, bwd, s, sms);
+  return launch_regs_nb<T, PENT, FAST, 4>(plan, x, n, m, ld, fwd, bwd, s, sms);
+}
+
+template <typename T, bool PENT, bool FAST, int NB>
+cudaError_t launch_regs_nb(const Plan& plan, T* x, int n, long long m, long long ld, const void* fwd,
+                           const void* bwd, cudaStream_t s, int sms) {
+  auto kern = dev::sweep_regs<T, PENT, FAST, NB>;
+  static std::atomic<bool> configured{false};
+  if (!configured.load(std::memory_order_relaxed)) {
+    cudaError_t e = allow_big_smem(kern);
+    if (e != cudaSuccess) return e;
+    configured.store(true, std::memory_order_relaxed);
+  }
+  CUtensorMap map;
+  if (!encode_map(&map, x, sizeof(T), n, m, ld, 32, dev::kSR)) return cudaErrorInvalidValue;
+  const long long groups = (m + plan.Wg - 1) / plan.Wg;
+  const long long grid = std::min<long long>(sms, groups);
+  T* scratch = nullptr;
+  if (plan.H > 0) {
+    const std::size_t bytes = static_cast<std::size_t>(grid) * plan.Wg * plan.H * sizeof(T);
+    int device = 0;
+    if (cudaGetDevice(&device) == cudaSuccess) ensure_l2_setaside(device, bytes);
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch), bytes, s);
+    if (e != cudaSuccess) return e;
+  }
+  kern<<<static_cast<unsigned>(grid), (plan.warps + 1) * 32, plan.smem_bytes, s>>>(map, x, n, m, ld, plan.H, plan.TC,
+                                                                                  groups, fwd, bwd, scratch);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  cudaError_t e = cudaGetLastError();
+  if (scratch) {
+    cudaError_t f = cudaFreeAsync(scratch, s);
+    if (e == cudaSuccess) e = f;
+  }
+  return e;
+}
+
 template <typename T, bool PENT, bool FAST>
 cudaError_t launch_global(T* x, int n, long long m, long long ld, const void* fwd, const void* bwd,
                           cudaStream_t s) {
@@ -626,6 +725,7 @@ template <typename T, bool PENT, bool FAST>
 cudaError_t dispatch(const Plan& plan, T* x, int n, long long m, long long ld, const void* fwd,
                      const void* bwd, cudaStream_t s, int sms) {
   if (plan.kind == PlanKind::Stream) return launch_stream<T, PENT, FAST>(plan, x, n, m, ld, fwd, bwd, s, sms);
+  if (plan.kind == PlanKind::Regs) return launch_regs<T, PENT, FAST>(plan, x, n, m, ld, fwd, bwd, s, sms);
   if (plan.kind == PlanKind::Persist) return launch_persist<T, PENT, FAST>(plan, x, n, m, ld, fwd, bwd, s, sms);
   if (plan.kind == PlanKind::Smem) {
     switch (plan.W) {
@@ -830,7 +930,10 @@ bandsolve_status describe_plan(Kind kind, std::size_t n, std::size_t m, std::siz
   const bool fast = current_mode() == BANDSOLVE_MODE_FAST;
   const Plan p = choose_plan(n, m, ld, f32 ? 4 : 8, kProbe, pent, fast, sms);
   char buf[256];
-  if (p.kind == PlanKind::Stream)
+  if (p.kind == PlanKind::Regs)
+    std::snprintf(buf, sizeof buf, "regs Wg=%d warps=%d+1 nb=%d head(L2)=%d tail(smem)=%d smem=%zu B spill=%.1f MB",
+                  p.Wg, p.warps, p.KB, p.H, static_cast<int>(n) - p.H, p.smem_bytes, p.model_us);
+  else if (p.kind == PlanKind::Stream)
     std::snprintf(buf, sizeof buf, "stream Wg=%d V=%d warps=%d+2 head(L2)=%d tail(smem)=%d rings=%d/%d pd=%d smem=%zu B model=%.1f us",
                   p.Wg, p.V, p.warps, p.H, static_cast<int>(n) - p.H, p.KB, p.KR, p.PD, p.smem_bytes, p.model_us);
   else if (p.kind == PlanKind::Persist)

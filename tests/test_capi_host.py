@@ -208,7 +208,8 @@ def test_modes(lib):
 
 def test_plan_description(lib):
     s = lib.describe_plan(bs.KIND_PENT, 512, 65536)
-    assert s.startswith("persist"), s
+    assert s.startswith("stream"), s  # configs[1]: warp-specialised streaming kernel, head spilled to L2
+    assert "head(L2)=0" not in s
     assert "head(L2)=0" in lib.describe_plan(bs.KIND_TRI, 256, 4096)  # config 1 fits smem entirely
     assert "global" in lib.describe_plan(bs.KIND_TRI, 64, 3)  # odd pitch: no TMA
     assert "global" in lib.describe_plan(bs.KIND_TRI, 100000, 1 << 20)  # tile > smem

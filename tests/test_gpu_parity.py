@@ -144,7 +144,7 @@ PLANS = [None, ("global",), ("smemW8",), ("smemW16",), ("smemW32",), ("persist",
          ("persist", "2", "48"), ("persist", "3", "100000"),
          ("stream", "64", "0", "4", "2"), ("stream", "64", "16", "2", "1"), ("stream", "128", "40", "4", "2"),
          ("stream", "256", "100000", "4", "1"), ("stream", "192", "33", "2", "2"), ("stream", "96", "48", "3", "1"),
-         ("stream", "32", "0", "4", "1")]
+         ("stream", "32", "0", "4", "1"), ("regs", "96"), ("regs", "32", "16"), ("regs", "224", "40")]
 PLAN_ENV = ("BANDSOLVE_PLAN", "BANDSOLVE_PWARPS", "BANDSOLVE_PTAIL", "BANDSOLVE_SWG", "BANDSOLVE_STAIL",
             "BANDSOLVE_SKB", "BANDSOLVE_SV")
 
@@ -154,7 +154,11 @@ def set_plan(plan):
         os.environ.pop(k, None)
     if not plan:
         return
-    if plan[0] == "stream":
+    if plan[0] == "regs":
+        os.environ["BANDSOLVE_PLAN"] = "regs"
+        for k, v in zip(("BANDSOLVE_SWG", "BANDSOLVE_STAIL"), plan[1:]):
+            os.environ[k] = v
+    elif plan[0] == "stream":
         os.environ["BANDSOLVE_PLAN"] = "stream"
         for k, v in zip(("BANDSOLVE_SWG", "BANDSOLVE_STAIL", "BANDSOLVE_SKB", "BANDSOLVE_SV"), plan[1:]):
             os.environ[k] = v
