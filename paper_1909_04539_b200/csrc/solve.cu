@@ -379,9 +379,11 @@ bool plan_stream(std::size_t n, std::size_t m, std::size_t elem, bool pent, bool
   if (fac > kSmemPerBlockMax / 2 || n < 2) return false;
   const int forced_wg = env_int("BANDSOLVE_SWG", 0);
   const int forced_tail = env_int("BANDSOLVE_STAIL", -1);
+  // KR = 0: one FIFO ring of KB slots carries both the b chunks and the
+  // spill reloads (every slot serves whichever head phase is running)
   const int KB = std::max(1, env_int("BANDSOLVE_SKB", 4));
-  const int KR = std::max(1, env_int("BANDSOLVE_SKR", 4));
-  const int PD = std::max(0, env_int("BANDSOLVE_SPD", 8));
+  const int KR = std::max(0, env_int("BANDSOLVE_SKR", 4));
+  const int PD = std::max(0, env_int("BANDSOLVE_SPD", 4));
   const int N = static_cast<int>(n);
   bool found = false;
   double best_t = 1e300;
@@ -846,7 +848,7 @@ uint64_t host_splitmix64(uint64_t z) {
 }
 
 // ---- per-thread staging context for host batches --------------------------------
-constexpr int kStages = 3;
+constexpr int kStages = 4;
 struct StageContext {
   int device = -1;
   cudaStream_t streams[kStages] = {};
@@ -995,7 +997,8 @@ bandsolve_status solve_host(const Factor& f, double* x, std::size_t n, std::size
   // Column chunks of ~16 MiB (multiple of 32 systems) pipelined over three
   // streams: chunk k's H2D overlaps chunk k-1's sweep and chunk k-2's D2H.
   const std::size_t row_bytes = n * sizeof(double);
-  std::size_t w = (16u << 20) / row_bytes;
+  const std::size_t chunk_mib = static_cast<std::size_t>(std::max(1, env_int("BANDSOLVE_HOST_CHUNK_MIB", 16)));
+  std::size_t w = (chunk_mib << 20) / row_bytes;
   w = std::max<std::size_t>(32, (w / 32) * 32);
   if (w >= m) w = m;
   const std::size_t chunks = (m + w - 1) / w;

@@ -303,6 +303,7 @@ __global__ void __launch_bounds__(32 * (stream_max_warps(V) + 2), 1)
   if (warp == P) {
     if (lane != 0) return;
     const uint64_t pol_b = policy_evict_first();  // every byte of b is read once
+    const uint64_t pol_keep = policy_evict_last();
     const long long my_groups = (groups - blockIdx.x + gridDim.x - 1) / gridDim.x;
     const long long b_total = my_groups * HC;  // b chunks this CTA streams through the ring
     long long b_next = 0;                      // next b chunk (CTA-local index) to enter the ring
@@ -344,13 +345,24 @@ __global__ void __launch_bounds__(32 * (stream_max_warps(V) + 2), 1)
         prefetch();
       }
       if (pre == HC) load_tail();
+      if (KR == 0 && HC > 0) {  // unified ring: the spill comes back through the same FIFO
+        mbar_wait(spilled, par);
+        for (int c = HC - 1; c >= 0; --c) {
+          if (issued >= static_cast<uint32_t>(KB)) mbar_wait(&b_empty[cur.slot], cur.phase ^ 1u);
+          mbar_expect_tx(&b_full[cur.slot], c_bytes);
+          bulk_load(bring + cur.slot * chunk, spill_cta + static_cast<long long>(c) * chunk, c_bytes,
+                    &b_full[cur.slot], pol_keep);
+          cur.next(KB);
+          ++issued;
+        }
+      }
     }
     return;
   }
 
   // ------------------------------------------------ reloader warp (spilled d-hat)
   if (warp == P + 1) {
-    if (lane != 0 || HC == 0) return;
+    if (lane != 0 || HC == 0 || KR == 0) return;
     const uint64_t pol_keep = policy_evict_last();
     Cursor cur;
     uint32_t issued = 0;
@@ -458,20 +470,28 @@ __global__ void __launch_bounds__(32 * (stream_max_warps(V) + 2), 1)
         tfull, sb + H, s1, s2, [&](int k) -> const P2* { return tslot(k); }, [](int) {}, tail_release,
         [&](int, int, P2 v) { put(v); });
 
-    // ---- backward, head rows: d-hat back through the reload ring, x to HBM
+    // ---- backward, head rows: d-hat back through the reload ring (or, with
+    // KR == 0, through the b ring: one FIFO), x to HBM
     {
+      const bool uni = KR == 0;
+      Cursor& cw = uni ? bw : rw;
+      Cursor& cr = uni ? brl : rrl;
+      P2* const ring_l = uni ? bring_l : rring_l;
+      uint64_t* const full = uni ? b_full : r_full;
+      uint64_t* const empty = uni ? b_empty : r_empty;
+      const int K = uni ? KB : KR;
       uint32_t cs = 0;
       bwd_chunks<T, V, PENT, FAST>(
-          HC, sb, s1, s2, [&](int) -> const P2* { return rring_l + cs * cpairs; },
+          HC, sb, s1, s2, [&](int) -> const P2* { return ring_l + cs * cpairs; },
           [&](int) {
-            cs = rw.slot;
-            mbar_wait(&r_full[rw.slot], rw.phase);
-            rw.next(KR);
+            cs = cw.slot;
+            mbar_wait(&full[cw.slot], cw.phase);
+            cw.next(K);
           },
           [&](int) {
             __syncwarp();
-            if (lane == 0) mbar_arrive(&r_empty[rrl.slot]);
-            rrl.next(KR);
+            if (lane == 0) mbar_arrive(&empty[cr.slot]);
+            cr.next(K);
           },
           [&](int, int, P2 v) { put(v); });
     }

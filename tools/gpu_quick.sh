@@ -3,7 +3,7 @@
 set -u
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+[ -z "${SKIP_TESTS:-}" ] && timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 tail -3 gpurun_out/pytest_gpu.log
 rm -f gpurun_out/quick.jsonl
 while IFS='|' read -r envs args; do
@@ -15,5 +15,6 @@ python - <<'PY'
 import json
 for l in open('gpurun_out/quick.jsonl'):
     d=json.loads(l); c=d['config']
-    print(f"{c['kind']:5s} {c['n']:5d} {c['batch_per_gpu']:8d} {c['mode']:6s} {d['env'][:40]:40s} {d['value']:.3e} frac={d['roofline']['frac']:.3f} {c['plan'][:72]}")
+    e=d.get('e2e') or {}
+    print(f"{c['kind']:5s} {c['n']:5d} {c['batch_per_gpu']:8d} {c['mode']:6s} {d['env'][:40]:40s} {d['value']:.3e} frac={d['roofline']['frac']:.3f} e2e={e.get('value',0):.3e} {c['plan'][:60]}")
 PY
