@@ -245,7 +245,13 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
     elem = 4 if args.f32 else 8
     dt = torch.float32 if args.f32 else torch.float64
     bands = lhs_for(kind, n)
-    fac = bs.TriFactor(lib, *bands) if kind == "tri" else bs.PentFactor(lib, *bands)
+    if args.periodic:  # cyclic constant-band system: shared sweep of A' + wrap correction
+        consts = (-1.0, 3.0, -1.0) if kind == "tri" else (1.0, -4.0, 7.0, -4.0, 1.0)
+        fac = bs.PeriodicTri(lib, *consts, n) if kind == "tri" else bs.PeriodicPent(lib, *consts, n)
+        if args.f32:
+            raise SystemExit("--periodic is fp64 only")
+    else:
+        fac = bs.TriFactor(lib, *bands) if kind == "tri" else bs.PentFactor(lib, *bands)
     j_off = rank * m  # this rank's shard of the global batch
 
     # Rotating in-place buffers so every timed step streams from HBM: the
@@ -330,7 +336,7 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
             "vs_baseline": None, "dtype": "f32" if args.f32 else "f64",
             "data": "synthetic: U(-1,1) RHS from SplitMix64(seed=42, i, global j), generated on device",
             "config": {"workload": desc, "kind": kind, "n": n, "batch_per_gpu": m, "global_batch": m * world,
-                       "mode": args.mode, "plan": plan,
+                       "mode": args.mode, "plan": plan, "periodic": bool(args.periodic),
                        "parallelism": f"dp{world} (systems sharded, no data-path collective)",
                        "l2": f"{nbuf} rotating in-place buffers of {bytes_per / 2**20:.0f} MiB "
                              f"(working set {nbuf * bytes_per / 132644864:.1f}x L2)"},
@@ -356,6 +362,7 @@ def main() -> int:
     ap.add_argument("--mode", choices=["exact", "fast"], default=os.environ.get("BANDSOLVE_BENCH_MODE", "exact"))
     ap.add_argument("--f32", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--periodic", action="store_true", help="cyclic (periodic) variant of the config's LHS")
     ap.add_argument("--n", type=int, default=0, help="override the config's rows per system (tuning)")
     ap.add_argument("--m", type=int, default=0, help="override the config's systems per GPU (tuning)")
     args = ap.parse_args()

@@ -8,8 +8,8 @@
  * "ref bandsolve.h:<line>", with the implementing reference source). A
  * caller linked against libbandsolve.so.1 can relink against
  * libbandsolve_b200.so for these entry points unchanged. The reference's
- * periodic, per-system, IBAT, footprint and benchmark-driver entry points
- * are outside this library's scope.
+ * per-system, IBAT, footprint and benchmark-driver entry points are outside
+ * this library's scope.
  *
  * The second part ("B200 extensions") adds device-resident entry points for
  * callers that keep their batch in HBM: they take a device pointer, a row
@@ -118,6 +118,41 @@ void bandsolve_uniform_pent_factor_destroy(
 bandsolve_status bandsolve_pent_solve_uniform(
     const bandsolve_uniform_pent_factor* factor, bandsolve_batch* batch);
 
+/* ---- Periodic (cyclic) systems with constant bands (ref bandsolve.h:115-146,
+ * periodic.cpp, capi.cpp:229-298, :414-446). The cyclic matrix is split into
+ * a strictly banded A' (factorised once on the host, reference order) plus
+ * a rank-1 (tri) / rank-2 (pent, Woodbury) wrap; a solve is the shared A'
+ * sweep followed by the correction x = y - Z t(y), both on the GPU.
+ * create: BAD_ARG for n < 3 (tri) / n < 6 (pent) or non-finite bands,
+ * DIVISION_BY_ZERO for b == 0 (tri), SINGULAR_CORRECTION when the cyclic
+ * matrix is singular; *out is NULL on failure. */
+typedef struct bandsolve_periodic_tri bandsolve_periodic_tri;
+typedef struct bandsolve_periodic_pent bandsolve_periodic_pent;
+
+bandsolve_status bandsolve_periodic_tri_create(double a, double b, double c,
+                                               size_t n,
+                                               bandsolve_periodic_tri** out);
+void bandsolve_periodic_tri_destroy(bandsolve_periodic_tri* corr);
+bandsolve_status bandsolve_periodic_tri_solve(
+    const bandsolve_periodic_tri* corr, bandsolve_batch* batch);
+bandsolve_status bandsolve_periodic_tri_modified_bands(
+    const bandsolve_periodic_tri* corr, double* sub, double* diag,
+    double* sup);
+bandsolve_status bandsolve_periodic_tri_correct(
+    const bandsolve_periodic_tri* corr, bandsolve_batch* batch);
+
+bandsolve_status bandsolve_periodic_pent_create(double a, double b, double c,
+                                                double d, double e, size_t n,
+                                                bandsolve_periodic_pent** out);
+void bandsolve_periodic_pent_destroy(bandsolve_periodic_pent* corr);
+bandsolve_status bandsolve_periodic_pent_solve(
+    const bandsolve_periodic_pent* corr, bandsolve_batch* batch);
+bandsolve_status bandsolve_periodic_pent_modified_bands(
+    const bandsolve_periodic_pent* corr, double* a, double* b, double* c,
+    double* d, double* e);
+bandsolve_status bandsolve_periodic_pent_correct(
+    const bandsolve_periodic_pent* corr, bandsolve_batch* batch);
+
 /* ---- Residuals (ref bandsolve.h:165-179, tri_solver.cpp:116-156,
  * pent_solver.cpp:223-273) — max over systems of ||A x - rhs||_inf /
  * ||rhs||_inf, evaluated on the GPU in the reference's operation order.
@@ -178,6 +213,22 @@ bandsolve_status bandsolve_pent_solve_uniform_dev(
     size_t m, size_t ld, void* stream);
 bandsolve_status bandsolve_pent_solve_uniform_dev_f32(
     const bandsolve_uniform_pent_factor* factor, float* x, size_t n, size_t m,
+    size_t ld, void* stream);
+
+/* Periodic solves / corrections of a device-resident batch (same contract
+ * as the *_dev solves above; correct_only = the wrap correction alone, for
+ * callers that solved A' y = d themselves). */
+bandsolve_status bandsolve_periodic_tri_solve_dev(
+    const bandsolve_periodic_tri* corr, double* x, size_t n, size_t m,
+    size_t ld, void* stream);
+bandsolve_status bandsolve_periodic_tri_correct_dev(
+    const bandsolve_periodic_tri* corr, double* x, size_t n, size_t m,
+    size_t ld, void* stream);
+bandsolve_status bandsolve_periodic_pent_solve_dev(
+    const bandsolve_periodic_pent* corr, double* x, size_t n, size_t m,
+    size_t ld, void* stream);
+bandsolve_status bandsolve_periodic_pent_correct_dev(
+    const bandsolve_periodic_pent* corr, double* x, size_t n, size_t m,
     size_t ld, void* stream);
 
 /* Device residual of a device-resident solution against a device-resident

@@ -14,6 +14,8 @@ enum {
   ST_BAD_ARG = 1,
   ST_SHAPE = 2,
   ST_BREAKDOWN = 3,
+  ST_DIV_ZERO = 4,
+  ST_SINGULAR_CORRECTION = 5,
   ST_SINGULAR_MATRIX = 6,
   ST_INTERNAL = 9
 };
@@ -397,4 +399,122 @@ void oracle_fill_rhs(uint64_t seed, size_t n, size_t m, size_t j_offset,
   for (size_t i = 0; i < n; ++i)
     for (size_t j = 0; j < m; ++j)
       x[i * m + j] = oracle_rhs_value(seed, i, j_offset + j);
+}
+
+/* ---- periodic wrap correction (reference periodic.cpp) ------------------ */
+
+int oracle_periodic_tri_prepare(double a, double b, double c, size_t n,
+                                double* chat, double* inv_denom,
+                                double* sub, double* z, double* v_last,
+                                double* scale) {
+  /* periodic_tri_splitting, periodic.cpp:11-31 */
+  if (n < 3) return ST_BAD_ARG;
+  if (!(isfinite(a) && isfinite(b) && isfinite(c))) return ST_BAD_ARG;
+  if (b == 0.0) return ST_DIV_ZERO;
+  double* sb = malloc(3 * n * sizeof(double));
+  if (!sb) return ST_INTERNAL;
+  double *s_sub = sb, *s_diag = sb + n, *s_sup = sb + 2 * n;
+  for (size_t i = 0; i < n; ++i) {
+    s_sub[i] = a;
+    s_diag[i] = b;
+    s_sup[i] = c;
+  }
+  s_sub[0] = 0.0;
+  s_sup[n - 1] = 0.0;
+  s_diag[0] = 2.0 * b;
+  s_diag[n - 1] = b + a * c / b;
+  /* u = (-b, 0, ..., 0, c); v = (1, 0, ..., 0, -a/b) */
+  const double vl = -a / b;
+  /* periodic_tri_prepare, periodic.cpp:33-55 */
+  int st = oracle_tri_prefactor(s_sub, s_diag, s_sup, n, chat, inv_denom, sub);
+  free(sb);
+  if (st) return st;
+  for (size_t i = 0; i < n; ++i) z[i] = 0.0;
+  z[0] = -b;
+  z[n - 1] = c;
+  oracle_tri_solve_shared(chat, inv_denom, sub, n, 1, 1, z);
+  const double vdotz = z[0] + vl * z[n - 1];
+  const double denom = 1.0 + vdotz;
+  if (!(fabs(denom) > 1e-300)) return ST_SINGULAR_CORRECTION;
+  *v_last = vl;
+  *scale = 1.0 / denom; /* periodic.cpp:67 inv_denom_scale */
+  return ST_OK;
+}
+
+void oracle_periodic_tri_apply(const double* z, double v_last, double scale,
+                               size_t n, size_t m, double* x) {
+  /* periodic.cpp:57-89: w = (y_0 + v_last y_{n-1}) * scale; y_i -= w z_i */
+  for (size_t j = 0; j < m; ++j) {
+    const double w = (x[j] + v_last * x[(n - 1) * m + j]) * scale;
+    for (size_t i = 0; i < n; ++i) x[i * m + j] -= w * z[i];
+  }
+}
+
+int oracle_periodic_pent_prepare(double a, double b, double c, double d,
+                                 double e, size_t n, double* inv_alpha,
+                                 double* beta, double* gamma, double* delta,
+                                 double* epsilon, double* z1, double* z2,
+                                 double* cap_inv) {
+  /* periodic_pent_splitting, periodic.cpp:97-129 */
+  if (n < 6) return ST_BAD_ARG;
+  if (!(isfinite(a) && isfinite(b) && isfinite(c) && isfinite(d) && isfinite(e))) return ST_BAD_ARG;
+  double* bb = malloc(5 * n * sizeof(double));
+  if (!bb) return ST_INTERNAL;
+  double *av = bb, *bv = bb + n, *cv = bb + 2 * n, *dv = bb + 3 * n, *ev = bb + 4 * n;
+  for (size_t i = 0; i < n; ++i) {
+    av[i] = a;
+    bv[i] = b;
+    cv[i] = c;
+    dv[i] = d;
+    ev[i] = e;
+  }
+  av[0] = av[1] = bv[0] = 0.0;
+  dv[n - 1] = ev[n - 1] = ev[n - 2] = 0.0;
+  cv[0] = c + b;
+  dv[0] = d + a;
+  bv[1] = b + a;
+  dv[n - 2] = d + e;
+  bv[n - 1] = b + e;
+  cv[n - 1] = c + d;
+  /* periodic_pent_prepare, periodic.cpp:131-170 */
+  int st = oracle_pent_prefactor(av, bv, cv, dv, ev, n, inv_alpha, beta, gamma, delta, epsilon);
+  free(bb);
+  if (st) return st;
+  /* u1 = (-b, -a, 0, ..., 0, e, d), u2 = (-a, 0, ..., 0, e); solved as the two
+   * columns of one interleaved batch (identical per-column arithmetic) */
+  for (size_t i = 0; i < n; ++i) z1[i] = z2[i] = 0.0;
+  z1[0] = -b;
+  z1[1] = -a;
+  z1[n - 2] = e;
+  z1[n - 1] = d;
+  z2[0] = -a;
+  z2[n - 1] = e;
+  oracle_pent_solve(inv_alpha, beta, gamma, delta, epsilon, 0.0, n, 1, 1, z1);
+  oracle_pent_solve(inv_alpha, beta, gamma, delta, epsilon, 0.0, n, 1, 1, z2);
+  double cap[2][2];
+  cap[0][0] = 1.0 + z1[0] - z1[n - 1];
+  cap[0][1] = z2[0] - z2[n - 1];
+  cap[1][0] = z1[1] - z1[n - 2];
+  cap[1][1] = 1.0 + z2[1] - z2[n - 2];
+  const double det = cap[0][0] * cap[1][1] - cap[0][1] * cap[1][0];
+  if (!(fabs(det) > 1e-300)) return ST_SINGULAR_CORRECTION;
+  const double inv_det = 1.0 / det;
+  cap_inv[0] = cap[1][1] * inv_det;
+  cap_inv[1] = -cap[0][1] * inv_det;
+  cap_inv[2] = -cap[1][0] * inv_det;
+  cap_inv[3] = cap[0][0] * inv_det;
+  return ST_OK;
+}
+
+void oracle_periodic_pent_apply(const double* z1, const double* z2,
+                                const double* cap_inv, size_t n, size_t m,
+                                double* x) {
+  /* periodic.cpp:172-208 */
+  for (size_t j = 0; j < m; ++j) {
+    const double w1 = x[j] - x[(n - 1) * m + j];
+    const double w2 = x[m + j] - x[(n - 2) * m + j];
+    const double t1 = cap_inv[0] * w1 + cap_inv[1] * w2;
+    const double t2 = cap_inv[2] * w1 + cap_inv[3] * w2;
+    for (size_t i = 0; i < n; ++i) x[i * m + j] -= z1[i] * t1 + z2[i] * t2;
+  }
 }

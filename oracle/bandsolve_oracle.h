@@ -80,6 +80,27 @@ int oracle_max_error_vs_dense(const double* a, size_t n, size_t m,
                               const double* x, const double* rhs,
                               double* out);
 
+/* Periodic (cyclic, constant bands) wrap correction, reference
+ * periodic.cpp. tri: splitting :11-31, prepare :33-55 (factor of A' into
+ * chat/inv_denom/sub, z = A'^-1 u, v_last = -a/b, scale = 1/(1 + v.z));
+ * apply :57-89 (x = y - ((y_0 + v_last y_{n-1}) * scale) z). */
+int oracle_periodic_tri_prepare(double a, double b, double c, size_t n,
+                                double* chat, double* inv_denom,
+                                double* sub, double* z, double* v_last,
+                                double* scale);
+void oracle_periodic_tri_apply(const double* z, double v_last, double scale,
+                               size_t n, size_t m, double* x);
+/* pent: splitting :97-129, prepare :131-170 (Woodbury: z1, z2, the 2x2
+ * capacitance inverse cap_inv[4] row-major); apply :172-208. */
+int oracle_periodic_pent_prepare(double a, double b, double c, double d,
+                                 double e, size_t n, double* inv_alpha,
+                                 double* beta, double* gamma, double* delta,
+                                 double* epsilon, double* z1, double* z2,
+                                 double* cap_inv);
+void oracle_periodic_pent_apply(const double* z1, const double* z2,
+                                const double* cap_inv, size_t n, size_t m,
+                                double* x);
+
 /* Counter-based synthetic RHS shared with the device generator:
  * U(-1, 1) from SplitMix64 of (seed, i, j), 53-bit mantissa. */
 double oracle_rhs_value(uint64_t seed, uint64_t i, uint64_t j);

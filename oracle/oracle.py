@@ -75,6 +75,12 @@ class Oracle:
         L.oracle_rhs_value.restype = C.c_double
         L.oracle_fill_rhs.argtypes = [C.c_uint64, _sz, _sz, _sz, _sz, _dp]
         L.oracle_fill_rhs.restype = None
+        L.oracle_periodic_tri_prepare.argtypes = [C.c_double] * 3 + [_sz] + [_dp] * 6
+        L.oracle_periodic_tri_apply.argtypes = [_dp, C.c_double, C.c_double, _sz, _sz, _dp]
+        L.oracle_periodic_tri_apply.restype = None
+        L.oracle_periodic_pent_prepare.argtypes = [C.c_double] * 5 + [_sz] + [_dp] * 8
+        L.oracle_periodic_pent_apply.argtypes = [_dp, _dp, _dp, _sz, _sz, _dp]
+        L.oracle_periodic_pent_apply.restype = None
 
     # -- factors ------------------------------------------------------------
     def tri_prefactor(self, sub, diag, sup) -> dict:
@@ -121,6 +127,42 @@ class Oracle:
         self.lib.oracle_pent_solve(_d(f["inv_alpha"]), _d(f["beta"]), _d(f["gamma"]), _d(f["delta"]),
                                    _d(eps) if eps is not None else None, f.get("eps_scalar", 0.0),
                                    n, m, m, _d(x))
+        return x
+
+    # -- periodic wrap correction (reference periodic.cpp) -----------------------
+    def periodic_tri_prepare(self, a, b, c, n) -> dict:
+        f = {k: np.zeros(n) for k in ("chat", "inv_denom", "sub", "z")}
+        vl, sc = np.zeros(1), np.zeros(1)
+        st = self.lib.oracle_periodic_tri_prepare(a, b, c, n, _d(f["chat"]), _d(f["inv_denom"]), _d(f["sub"]),
+                                                  _d(f["z"]), _d(vl), _d(sc))
+        if st:
+            raise OracleError(st)
+        f["v_last"], f["scale"] = float(vl[0]), float(sc[0])
+        return f
+
+    def periodic_tri_solve(self, f: dict, x: np.ndarray, correct_only: bool = False) -> np.ndarray:
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        n, m = x.shape
+        if not correct_only:
+            self.tri_solve(f, x)
+        self.lib.oracle_periodic_tri_apply(_d(f["z"]), f["v_last"], f["scale"], n, m, _d(x))
+        return x
+
+    def periodic_pent_prepare(self, a, b, c, d, e, n) -> dict:
+        keys = ("inv_alpha", "beta", "gamma", "delta", "epsilon", "z1", "z2")
+        f = {k: np.zeros(n) for k in keys}
+        f["cap_inv"] = np.zeros(4)
+        st = self.lib.oracle_periodic_pent_prepare(a, b, c, d, e, n, *[_d(f[k]) for k in keys], _d(f["cap_inv"]))
+        if st:
+            raise OracleError(st)
+        return f
+
+    def periodic_pent_solve(self, f: dict, x: np.ndarray, correct_only: bool = False) -> np.ndarray:
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        n, m = x.shape
+        if not correct_only:
+            self.pent_solve(f, x)
+        self.lib.oracle_periodic_pent_apply(_d(f["z1"]), _d(f["z2"]), _d(f["cap_inv"]), n, m, _d(x))
         return x
 
     # -- checks ---------------------------------------------------------------

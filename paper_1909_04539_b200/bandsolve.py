@@ -67,6 +67,16 @@ _REFERENCE_SIGS = [
     ("bandsolve_pent_solve_uniform", _st, [_vp, _vp]),
     ("bandsolve_tri_residual", _st, [_dp, _dp, _dp, _sz, C.c_int, _vp, _vp, _dp]),
     ("bandsolve_pent_residual", _st, [_dp] * 5 + [_sz, C.c_int, _vp, _vp, _dp]),
+    ("bandsolve_periodic_tri_create", _st, [C.c_double] * 3 + [_sz, C.POINTER(_vp)]),
+    ("bandsolve_periodic_tri_destroy", None, [_vp]),
+    ("bandsolve_periodic_tri_solve", _st, [_vp, _vp]),
+    ("bandsolve_periodic_tri_modified_bands", _st, [_vp, _dp, _dp, _dp]),
+    ("bandsolve_periodic_tri_correct", _st, [_vp, _vp]),
+    ("bandsolve_periodic_pent_create", _st, [C.c_double] * 5 + [_sz, C.POINTER(_vp)]),
+    ("bandsolve_periodic_pent_destroy", None, [_vp]),
+    ("bandsolve_periodic_pent_solve", _st, [_vp, _vp]),
+    ("bandsolve_periodic_pent_modified_bands", _st, [_vp] + [_dp] * 5),
+    ("bandsolve_periodic_pent_correct", _st, [_vp, _vp]),
 ]
 
 # B200 extensions (include/bandsolve.h, second part)
@@ -91,6 +101,10 @@ _EXTENSION_SIGS = [
     ("bandsolve_pent_factor_arrays", _st, [_vp, _dp, _dp, _dp, _dp, _dp]),
     ("bandsolve_uniform_pent_factor_order", _sz, [_vp]),
     ("bandsolve_uniform_pent_factor_arrays", _st, [_vp, _dp, _dp, _dp, _dp, _dp]),
+    ("bandsolve_periodic_tri_solve_dev", _st, [_vp, _vp, _sz, _sz, _sz, _vp]),
+    ("bandsolve_periodic_tri_correct_dev", _st, [_vp, _vp, _sz, _sz, _sz, _vp]),
+    ("bandsolve_periodic_pent_solve_dev", _st, [_vp, _vp, _sz, _sz, _sz, _vp]),
+    ("bandsolve_periodic_pent_correct_dev", _st, [_vp, _vp, _sz, _sz, _sz, _vp]),
     ("bandsolve_describe_plan", _st, [C.c_int, _sz, _sz, _sz, C.c_int, C.c_char_p, _sz]),
     ("bandsolve_kernel_launches", C.c_uint64, []),
     ("bandsolve_last_error", C.c_char_p, []),
@@ -354,6 +368,61 @@ class UniformPentFactor(_Factor):
 
 
 # ---- LHS definitions used by the configs (ref pde.cpp:62-71) ---------------
+class _Periodic(_Factor):
+    _correct = ""
+    _correct_dev = ""
+
+    def correct(self, batch: Batch) -> None:
+        """The wrap correction alone (caller already solved A' y = d)."""
+        self.lib.check(getattr(self.lib.lib, self._correct)(self.handle, batch.handle), self._correct)
+
+    def correct_dev(self, ptr: int, n: int, m: int, ld: Optional[int] = None, stream: int = 0) -> None:
+        self.lib.check(getattr(self.lib.lib, self._correct_dev)(self.handle, ptr, n, m, m if ld is None else ld,
+                                                                  stream), self._correct_dev)
+
+
+class PeriodicTri(_Periodic):
+    """bandsolve_periodic_tri (ref bandsolve.h:118-131): cyclic constant-band
+    tridiagonal system, rank-1 wrap correction."""
+    _destroy = "bandsolve_periodic_tri_destroy"
+    _solve = "bandsolve_periodic_tri_solve"
+    _solve_dev = "bandsolve_periodic_tri_solve_dev"
+    _correct = "bandsolve_periodic_tri_correct"
+    _correct_dev = "bandsolve_periodic_tri_correct_dev"
+
+    def __init__(self, lib: Library, a: float, b: float, c: float, n: int):
+        h = _vp()
+        lib.check(lib.lib.bandsolve_periodic_tri_create(a, b, c, n, C.byref(h)), "periodic_tri_create")
+        super().__init__(lib, h, n)
+
+    def modified_bands(self):
+        out = [np.empty(self.n) for _ in range(3)]
+        self.lib.check(self.lib.lib.bandsolve_periodic_tri_modified_bands(self.handle, *[_dptr(v) for v in out]),
+                       "periodic_tri_modified_bands")
+        return out
+
+
+class PeriodicPent(_Periodic):
+    """bandsolve_periodic_pent (ref bandsolve.h:133-146): cyclic constant-band
+    pentadiagonal system, rank-2 (Woodbury) wrap correction."""
+    _destroy = "bandsolve_periodic_pent_destroy"
+    _solve = "bandsolve_periodic_pent_solve"
+    _solve_dev = "bandsolve_periodic_pent_solve_dev"
+    _correct = "bandsolve_periodic_pent_correct"
+    _correct_dev = "bandsolve_periodic_pent_correct_dev"
+
+    def __init__(self, lib: Library, a: float, b: float, c: float, d: float, e: float, n: int):
+        h = _vp()
+        lib.check(lib.lib.bandsolve_periodic_pent_create(a, b, c, d, e, n, C.byref(h)), "periodic_pent_create")
+        super().__init__(lib, h, n)
+
+    def modified_bands(self):
+        out = [np.empty(self.n) for _ in range(5)]
+        self.lib.check(self.lib.lib.bandsolve_periodic_pent_modified_bands(self.handle, *[_dptr(v) for v in out]),
+                       "periodic_pent_modified_bands")
+        return out
+
+
 def diffusion_bands(sigma: float, n: int):
     """Crank-Nicolson diffusion LHS (-s, 1+2s, -s), structural zeros applied."""
     sub = np.full(n, -sigma)

@@ -32,6 +32,12 @@ struct bandsolve_pent_factor {
 struct bandsolve_uniform_pent_factor {
   std::unique_ptr<bsb::Factor> impl;
 };
+struct bandsolve_periodic_tri {
+  std::unique_ptr<bsb::Periodic> impl;
+};
+struct bandsolve_periodic_pent {
+  std::unique_ptr<bsb::Periodic> impl;
+};
 
 namespace bsb {
 
@@ -194,6 +200,104 @@ BSB_API bandsolve_status bandsolve_pent_solve_uniform(const bandsolve_uniform_pe
                                                       bandsolve_batch* batch) {
   if (!factor || !batch) return null_arg();
   return guarded([&] { return bsb::solve_host(*factor->impl, batch->data, batch->n, batch->m); });
+}
+
+// ---- periodic (capi.cpp:229-298, :414-446) -----------------------------------
+BSB_API bandsolve_status bandsolve_periodic_tri_create(double a, double b, double c, size_t n,
+                                                       bandsolve_periodic_tri** out) {
+  if (!out) return null_arg();
+  *out = nullptr;
+  return guarded([&] {
+    std::unique_ptr<bsb::Periodic> p;
+    bandsolve_status st = bsb::make_periodic_tri(a, b, c, n, p);
+    if (st != BANDSOLVE_OK) return st;
+    *out = new bandsolve_periodic_tri{std::move(p)};
+    return BANDSOLVE_OK;
+  });
+}
+
+BSB_API void bandsolve_periodic_tri_destroy(bandsolve_periodic_tri* corr) { delete corr; }
+
+BSB_API bandsolve_status bandsolve_periodic_tri_solve(const bandsolve_periodic_tri* corr, bandsolve_batch* batch) {
+  if (!corr || !batch) return null_arg();
+  return guarded([&] {
+    return bsb::solve_host(*corr->impl->factor, batch->data, batch->n, batch->m, corr->impl.get(), false);
+  });
+}
+
+BSB_API bandsolve_status bandsolve_periodic_tri_correct(const bandsolve_periodic_tri* corr, bandsolve_batch* batch) {
+  if (!corr || !batch) return null_arg();
+  return guarded([&] {
+    return bsb::solve_host(*corr->impl->factor, batch->data, batch->n, batch->m, corr->impl.get(), true);
+  });
+}
+
+BSB_API bandsolve_status bandsolve_periodic_tri_modified_bands(const bandsolve_periodic_tri* corr, double* sub,
+                                                               double* diag, double* sup) {
+  if (!corr) return null_arg();
+  return guarded([&] {
+    bsb::periodic_tri_modified_bands(*corr->impl, sub, diag, sup);
+    return BANDSOLVE_OK;
+  });
+}
+
+BSB_API bandsolve_status bandsolve_periodic_pent_create(double a, double b, double c, double d, double e, size_t n,
+                                                        bandsolve_periodic_pent** out) {
+  if (!out) return null_arg();
+  *out = nullptr;
+  return guarded([&] {
+    std::unique_ptr<bsb::Periodic> p;
+    bandsolve_status st = bsb::make_periodic_pent(a, b, c, d, e, n, p);
+    if (st != BANDSOLVE_OK) return st;
+    *out = new bandsolve_periodic_pent{std::move(p)};
+    return BANDSOLVE_OK;
+  });
+}
+
+BSB_API void bandsolve_periodic_pent_destroy(bandsolve_periodic_pent* corr) { delete corr; }
+
+BSB_API bandsolve_status bandsolve_periodic_pent_solve(const bandsolve_periodic_pent* corr, bandsolve_batch* batch) {
+  if (!corr || !batch) return null_arg();
+  return guarded([&] {
+    return bsb::solve_host(*corr->impl->factor, batch->data, batch->n, batch->m, corr->impl.get(), false);
+  });
+}
+
+BSB_API bandsolve_status bandsolve_periodic_pent_correct(const bandsolve_periodic_pent* corr, bandsolve_batch* batch) {
+  if (!corr || !batch) return null_arg();
+  return guarded([&] {
+    return bsb::solve_host(*corr->impl->factor, batch->data, batch->n, batch->m, corr->impl.get(), true);
+  });
+}
+
+BSB_API bandsolve_status bandsolve_periodic_pent_modified_bands(const bandsolve_periodic_pent* corr, double* a,
+                                                                double* b, double* c, double* d, double* e) {
+  if (!corr) return null_arg();
+  return guarded([&] {
+    bsb::periodic_pent_modified_bands(*corr->impl, a, b, c, d, e);
+    return BANDSOLVE_OK;
+  });
+}
+
+BSB_API bandsolve_status bandsolve_periodic_tri_solve_dev(const bandsolve_periodic_tri* corr, double* x, size_t n,
+                                                          size_t m, size_t ld, void* stream) {
+  if (!corr) return null_arg();
+  return guarded([&] { return bsb::periodic_device(*corr->impl, x, n, m, ld, stream, false); });
+}
+BSB_API bandsolve_status bandsolve_periodic_tri_correct_dev(const bandsolve_periodic_tri* corr, double* x, size_t n,
+                                                            size_t m, size_t ld, void* stream) {
+  if (!corr) return null_arg();
+  return guarded([&] { return bsb::periodic_device(*corr->impl, x, n, m, ld, stream, true); });
+}
+BSB_API bandsolve_status bandsolve_periodic_pent_solve_dev(const bandsolve_periodic_pent* corr, double* x, size_t n,
+                                                           size_t m, size_t ld, void* stream) {
+  if (!corr) return null_arg();
+  return guarded([&] { return bsb::periodic_device(*corr->impl, x, n, m, ld, stream, false); });
+}
+BSB_API bandsolve_status bandsolve_periodic_pent_correct_dev(const bandsolve_periodic_pent* corr, double* x,
+                                                             size_t n, size_t m, size_t ld, void* stream) {
+  if (!corr) return null_arg();
+  return guarded([&] { return bsb::periodic_device(*corr->impl, x, n, m, ld, stream, true); });
 }
 
 // ---- residuals (capi.cpp:327-367) ----------------------------------------------

@@ -165,4 +165,156 @@ bandsolve_status make_uniform_factor(double a, double b, double c, double d,
   return BANDSOLVE_OK;
 }
 
+// ---- periodic wrap correction (reference periodic.cpp) -------------------
+namespace {
+
+// One column of the shared sweeps in the reference order
+// (tri_solver.cpp:25-47, pent_solver.cpp:19-62); used once per periodic
+// preparation for A' z = u, exactly as periodic.cpp:41-44 / :139-142 do.
+void tri_sweep_column(const Factor& f, double* x) {
+  const std::size_t n = f.n;
+  x[0] = x[0] * f.inv_denom[0];
+  for (std::size_t i = 1; i < n; ++i) x[i] = (x[i] - f.sub[i] * x[i - 1]) * f.inv_denom[i];
+  for (std::size_t i = n - 1; i-- > 0;) x[i] = x[i] - f.chat[i] * x[i + 1];
+}
+
+void pent_sweep_column(const Factor& f, double* x) {
+  const std::size_t n = f.n;
+  const double* ia = f.inv_alpha.data();
+  const double* be = f.beta.data();
+  const double* ga = f.gamma.data();
+  const double* de = f.delta.data();
+  const double* ep = f.epsilon.data();
+  x[0] = x[0] * ia[0];
+  x[1] = (x[1] - be[1] * x[0]) * ia[1];
+  for (std::size_t i = 2; i < n; ++i) x[i] = ((x[i] - ep[i] * x[i - 2]) - be[i] * x[i - 1]) * ia[i];
+  x[n - 2] = x[n - 2] - ga[n - 2] * x[n - 1];
+  for (std::size_t i = n - 2; i-- > 0;) x[i] = x[i] - (ga[i] * x[i + 1] + de[i] * x[i + 2]);
+}
+
+}  // namespace
+
+bandsolve_status make_periodic_tri(double a, double b, double c, std::size_t n,
+                                   std::unique_ptr<Periodic>& out) {
+  // periodic_tri_splitting, periodic.cpp:11-31
+  if (n < 3) return fail(BANDSOLVE_ERR_BAD_ARG, "periodic tridiagonal wrap needs n >= 3");
+  if (!(std::isfinite(a) && std::isfinite(b) && std::isfinite(c)))
+    return fail(BANDSOLVE_ERR_BAD_ARG, "non-finite band value");
+  if (b == 0.0) return fail(BANDSOLVE_ERR_DIVISION_BY_ZERO, "zero diagonal in periodic splitting");
+  std::vector<double> sub(n, a), diag(n, b), sup(n, c);
+  sub[0] = 0.0;
+  sup[n - 1] = 0.0;
+  diag[0] = 2.0 * b;
+  diag[n - 1] = b + a * c / b;
+  auto p = std::make_unique<Periodic>();
+  p->kind = Kind::Tri;
+  p->n = n;
+  // periodic_tri_prepare, periodic.cpp:33-55
+  bandsolve_status st = make_tri_factor(sub.data(), diag.data(), sup.data(), n, p->factor);
+  if (st != BANDSOLVE_OK) return st;
+  p->z1.assign(n, 0.0);
+  p->z1[0] = -b;  // u = (-b, 0, ..., 0, c)
+  p->z1[n - 1] = c;
+  tri_sweep_column(*p->factor, p->z1.data());
+  p->v_last = -a / b;  // v = (1, 0, ..., 0, -a/b)
+  const double vdotz = p->z1[0] + p->v_last * p->z1[n - 1];
+  const double denom = 1.0 + vdotz;
+  if (!(std::abs(denom) > kBreakdownEps))
+    return fail(BANDSOLVE_ERR_SINGULAR_CORRECTION, "cyclic system is singular: 1 + v.z vanishes");
+  p->scale = 1.0 / denom;  // periodic.cpp:67 inv_denom_scale
+  out = std::move(p);
+  return BANDSOLVE_OK;
+}
+
+bandsolve_status make_periodic_pent(double a, double b, double c, double d,
+                                    double e, std::size_t n,
+                                    std::unique_ptr<Periodic>& out) {
+  // periodic_pent_splitting, periodic.cpp:97-129
+  if (n < 6) return fail(BANDSOLVE_ERR_BAD_ARG, "periodic pentadiagonal wrap needs n >= 6");
+  if (!(std::isfinite(a) && std::isfinite(b) && std::isfinite(c) && std::isfinite(d) && std::isfinite(e)))
+    return fail(BANDSOLVE_ERR_BAD_ARG, "non-finite band value");
+  std::vector<double> av(n, a), bv(n, b), cv(n, c), dv(n, d), ev(n, e);
+  av[0] = av[1] = bv[0] = 0.0;
+  dv[n - 1] = ev[n - 1] = ev[n - 2] = 0.0;
+  cv[0] = c + b;
+  dv[0] = d + a;
+  bv[1] = b + a;
+  dv[n - 2] = d + e;
+  bv[n - 1] = b + e;
+  cv[n - 1] = c + d;
+  auto p = std::make_unique<Periodic>();
+  p->kind = Kind::Pent;
+  p->n = n;
+  // periodic_pent_prepare, periodic.cpp:131-170
+  bandsolve_status st = make_pent_factor(av.data(), bv.data(), cv.data(), dv.data(), ev.data(), n, p->factor);
+  if (st != BANDSOLVE_OK) return st;
+  p->z1.assign(n, 0.0);
+  p->z2.assign(n, 0.0);
+  p->z1[0] = -b;  // u1 = (-b, -a, 0, ..., 0, e, d)
+  p->z1[1] = -a;
+  p->z1[n - 2] = e;
+  p->z1[n - 1] = d;
+  p->z2[0] = -a;  // u2 = (-a, 0, ..., 0, e)
+  p->z2[n - 1] = e;
+  pent_sweep_column(*p->factor, p->z1.data());
+  pent_sweep_column(*p->factor, p->z2.data());
+  const std::vector<double>& z1 = p->z1;
+  const std::vector<double>& z2 = p->z2;
+  double cap[2][2];  // I + V^T Z, v1 = e_1 - e_N, v2 = e_2 - e_{N-1}
+  cap[0][0] = 1.0 + z1[0] - z1[n - 1];
+  cap[0][1] = z2[0] - z2[n - 1];
+  cap[1][0] = z1[1] - z1[n - 2];
+  cap[1][1] = 1.0 + z2[1] - z2[n - 2];
+  const double det = cap[0][0] * cap[1][1] - cap[0][1] * cap[1][0];
+  if (!(std::abs(det) > kBreakdownEps))
+    return fail(BANDSOLVE_ERR_SINGULAR_CORRECTION, "cyclic system is singular: capacitance");
+  const double inv_det = 1.0 / det;
+  p->cap_inv[0] = cap[1][1] * inv_det;
+  p->cap_inv[1] = -cap[0][1] * inv_det;
+  p->cap_inv[2] = -cap[1][0] * inv_det;
+  p->cap_inv[3] = cap[0][0] * inv_det;
+  out = std::move(p);
+  return BANDSOLVE_OK;
+}
+
+void periodic_tri_modified_bands(const Periodic& p, double* sub, double* diag, double* sup) {
+  // capi.cpp:249-262
+  const Factor& f = *p.factor;
+  const std::size_t n = f.n;
+  for (std::size_t i = 0; i < n; ++i) {
+    const double denom = 1.0 / f.inv_denom[i];
+    if (sub) sub[i] = f.sub[i];
+    if (diag) diag[i] = i == 0 ? denom : denom + f.sub[i] * f.chat[i - 1];
+    if (sup) sup[i] = i + 1 < n ? f.chat[i] * denom : 0.0;
+  }
+}
+
+void periodic_pent_modified_bands(const Periodic& p, double* a, double* b, double* c, double* d, double* e) {
+  // capi.cpp:414-446: A' = L R reassembled band by band
+  const Factor& f = *p.factor;
+  const std::size_t n = f.n;
+  std::vector<double> alpha(n), gamma(n, 0.0), delta(n, 0.0);
+  for (std::size_t i = 0; i < n; ++i) alpha[i] = 1.0 / f.inv_alpha[i];
+  for (std::size_t i = 0; i + 1 < n; ++i) gamma[i] = f.gamma[i];
+  for (std::size_t i = 0; i + 2 < n; ++i) delta[i] = f.delta[i];
+  for (std::size_t i = 0; i < n; ++i) {
+    const double eps = f.epsilon[i];
+    const double beta = f.beta[i];
+    if (a) a[i] = i >= 2 ? eps : 0.0;
+    if (b) b[i] = i >= 1 ? beta + (i >= 2 ? eps * gamma[i - 2] : 0.0) : 0.0;
+    if (c) {
+      double v = alpha[i];
+      if (i >= 1) v += beta * gamma[i - 1];
+      if (i >= 2) v += eps * delta[i - 2];
+      c[i] = v;
+    }
+    if (d) {
+      double v = i + 1 < n ? alpha[i] * gamma[i] : 0.0;
+      if (i >= 1 && i + 1 < n) v += beta * delta[i - 1];
+      d[i] = v;
+    }
+    if (e) e[i] = i + 2 < n ? alpha[i] * delta[i] : 0.0;
+  }
+}
+
 }  // namespace bsb

@@ -65,6 +65,36 @@ bandsolve_status validate_pent_bands(const double* a, const double* b,
                                      const double* c, const double* d,
                                      const double* e, std::size_t n);
 
+// Periodic (cyclic, constant bands) systems: the strictly banded A' that
+// backs them plus the low-rank wrap correction (reference periodic.hpp,
+// periodic.cpp). kind Tri: rank 1, z1 = A'^-1 u, v_last = -a/b,
+// scale = 1 / (1 + v.z). kind Pent: rank 2 (Woodbury), z1, z2 and the 2x2
+// capacitance inverse, row-major.
+struct Periodic {
+  Kind kind = Kind::Tri;
+  std::size_t n = 0;
+  std::unique_ptr<Factor> factor;
+  std::vector<double> z1, z2;
+  double v_last = 0.0, scale = 0.0;
+  double cap_inv[4] = {0.0, 0.0, 0.0, 0.0};
+
+  mutable std::mutex mu;
+  mutable std::vector<std::pair<int, double*>> devices;  // z1 | z2 per device
+  ~Periodic();
+};
+
+// periodic.cpp:11-55 / :97-170, in the reference's evaluation order.
+bandsolve_status make_periodic_tri(double a, double b, double c, std::size_t n,
+                                   std::unique_ptr<Periodic>& out);
+bandsolve_status make_periodic_pent(double a, double b, double c, double d,
+                                    double e, std::size_t n,
+                                    std::unique_ptr<Periodic>& out);
+// capi.cpp:249-262 / :414-446: A' reassembled from its factor.
+void periodic_tri_modified_bands(const Periodic& p, double* sub, double* diag,
+                                 double* sup);
+void periodic_pent_modified_bands(const Periodic& p, double* a, double* b,
+                                  double* c, double* d, double* e);
+
 // ---- device layer (solve.cu) ---------------------------------------------
 int current_mode();
 void set_mode(int mode);
@@ -73,9 +103,16 @@ void set_mode(int mode);
 bandsolve_status solve_device(const Factor& f, void* x, bool f32,
                               std::size_t n, std::size_t m, std::size_t ld,
                               void* stream);
-// Host batch: staged through the device, synchronous.
+// Host batch: staged through the device, synchronous. With `per`, the
+// periodic correction follows the sweep on each staged chunk; with
+// `correct_only`, only the correction runs.
 bandsolve_status solve_host(const Factor& f, double* x, std::size_t n,
-                            std::size_t m);
+                            std::size_t m, const Periodic* per = nullptr,
+                            bool correct_only = false);
+// Periodic solve / correction of a device array (pitch ld), stream-ordered.
+bandsolve_status periodic_device(const Periodic& p, double* x, std::size_t n,
+                                 std::size_t m, std::size_t ld, void* stream,
+                                 bool correct_only);
 // Residual kernels; bands are host arrays of length n (5 for pent).
 bandsolve_status residual_device(Kind kind, const double* const* bands,
                                  std::size_t n, int cyclic, const double* x,

@@ -840,6 +840,54 @@ __global__ void fill_rhs_kernel(T* __restrict__ x, int n, long long m, long long
   }
 }
 
+// ---- periodic wrap correction (reference periodic.cpp:57-89, :172-208) -----
+// One thread per system (coalesced rows), the reference's operation order
+// with separately rounded products/sums; z is read as warp-uniform
+// broadcasts. Rows are processed 8 at a time with the loads issued first.
+__global__ void periodic_tri_correct_kernel(double* __restrict__ x, int n, long long m, long long ld,
+                                            const double* __restrict__ z, double v_last, double scale) {
+  using namespace dev;
+  const long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  double* col = x + j;
+  // w = (y_0 + v_last * y_{n-1}) * scale                      periodic.cpp:80
+  const double w = mul_rn(add_rn(col[0], mul_rn(v_last, col[static_cast<long long>(n - 1) * ld])), scale);
+  int i = 0;
+  for (; i + 8 <= n; i += 8) {
+    double y[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) y[u] = col[static_cast<long long>(i + u) * ld];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) col[static_cast<long long>(i + u) * ld] = sub_rn(y[u], mul_rn(w, __ldg(z + i + u)));
+  }
+  for (; i < n; ++i) col[static_cast<long long>(i) * ld] = sub_rn(col[static_cast<long long>(i) * ld], mul_rn(w, __ldg(z + i)));
+}
+
+__global__ void periodic_pent_correct_kernel(double* __restrict__ x, int n, long long m, long long ld,
+                                             const double* __restrict__ z1, const double* __restrict__ z2,
+                                             double i00, double i01, double i10, double i11) {
+  using namespace dev;
+  const long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  double* col = x + j;
+  auto Y = [&](int i) -> double& { return col[static_cast<long long>(i) * ld]; };
+  // periodic.cpp:189-194
+  const double w1 = sub_rn(Y(0), Y(n - 1));
+  const double w2 = sub_rn(Y(1), Y(n - 2));
+  const double t1 = add_rn(mul_rn(i00, w1), mul_rn(i01, w2));
+  const double t2 = add_rn(mul_rn(i10, w1), mul_rn(i11, w2));
+  int i = 0;
+  for (; i + 8 <= n; i += 8) {
+    double y[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) y[u] = Y(i + u);
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      Y(i + u) = sub_rn(y[u], add_rn(mul_rn(__ldg(z1 + i + u), t1), mul_rn(__ldg(z2 + i + u), t2)));
+  }
+  for (; i < n; ++i) Y(i) = sub_rn(Y(i), add_rn(mul_rn(__ldg(z1 + i), t1), mul_rn(__ldg(z2 + i), t2)));
+}
+
 uint64_t host_splitmix64(uint64_t z) {
   z += 0x9E3779B97F4A7C15ull;
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -984,7 +1032,79 @@ bandsolve_status solve_device(const Factor& f, void* x, bool f32, std::size_t n,
   return BANDSOLVE_OK;
 }
 
-bandsolve_status solve_host(const Factor& f, double* x, std::size_t n, std::size_t m) {
+Periodic::~Periodic() {
+  for (auto& d : devices) {
+    int prev = -1;
+    if (cudaGetDevice(&prev) == cudaSuccess && prev != d.first) cudaSetDevice(d.first);
+    cudaFree(d.second);
+    if (prev >= 0 && prev != d.first) cudaSetDevice(prev);
+  }
+  cudaGetLastError();
+}
+
+namespace {
+bandsolve_status periodic_device_z(const Periodic& p, int device, const double** out) {
+  std::lock_guard<std::mutex> lock(p.mu);
+  for (const auto& d : p.devices)
+    if (d.first == device) {
+      *out = d.second;
+      return BANDSOLVE_OK;
+    }
+  const std::size_t n = p.n;
+  std::vector<double> host(2 * n, 0.0);
+  std::memcpy(host.data(), p.z1.data(), n * sizeof(double));
+  if (!p.z2.empty()) std::memcpy(host.data() + n, p.z2.data(), n * sizeof(double));
+  double* d = nullptr;
+  BSB_CUDA(cudaMalloc(&d, 2 * n * sizeof(double)));
+  cudaError_t err = cudaMemcpy(d, host.data(), 2 * n * sizeof(double), cudaMemcpyHostToDevice);
+  if (err != cudaSuccess) {
+    cudaFree(d);
+    return cuda_fail(err, "periodic z upload");
+  }
+  p.devices.emplace_back(device, d);
+  *out = d;
+  return BANDSOLVE_OK;
+}
+
+bandsolve_status launch_periodic_correct(const Periodic& p, double* x, std::size_t n, std::size_t m,
+                                         std::size_t ld, cudaStream_t s) {
+  int device = 0;
+  BSB_CUDA(cudaGetDevice(&device));
+  const double* z = nullptr;
+  bandsolve_status st = periodic_device_z(p, device, &z);
+  if (st != BANDSOLVE_OK) return st;
+  const int threads = 128;
+  const unsigned grid = static_cast<unsigned>((m + threads - 1) / threads);
+  if (p.kind == Kind::Tri)
+    periodic_tri_correct_kernel<<<grid, threads, 0, s>>>(x, static_cast<int>(n), static_cast<long long>(m),
+                                                         static_cast<long long>(ld), z, p.v_last, p.scale);
+  else
+    periodic_pent_correct_kernel<<<grid, threads, 0, s>>>(x, static_cast<int>(n), static_cast<long long>(m),
+                                                          static_cast<long long>(ld), z, z + n, p.cap_inv[0],
+                                                          p.cap_inv[1], p.cap_inv[2], p.cap_inv[3]);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  BSB_CUDA(cudaGetLastError());
+  return BANDSOLVE_OK;
+}
+}  // namespace
+
+bandsolve_status periodic_device(const Periodic& p, double* x, std::size_t n, std::size_t m, std::size_t ld,
+                                 void* stream, bool correct_only) {
+  if (!x) return fail(BANDSOLVE_ERR_BAD_ARG, "null device pointer");
+  if (n != p.n) return fail(BANDSOLVE_ERR_SHAPE_MISMATCH, "correction order != batch rows");
+  if (ld < m) return fail(BANDSOLVE_ERR_BAD_ARG, "row pitch ld < m");
+  if (m == 0) return BANDSOLVE_OK;
+  if (device_count_cached() == 0) return fail(BANDSOLVE_ERR_INTERNAL, "no CUDA device available (no CPU fallback)");
+  auto s = static_cast<cudaStream_t>(stream);
+  if (!correct_only) {
+    bandsolve_status st = solve_device(*p.factor, x, false, n, m, ld, stream);
+    if (st != BANDSOLVE_OK) return st;
+  }
+  return launch_periodic_correct(p, x, n, m, ld, s);
+}
+
+bandsolve_status solve_host(const Factor& f, double* x, std::size_t n, std::size_t m, const Periodic* per,
+                            bool correct_only) {
   if (n != f.n) return fail(BANDSOLVE_ERR_SHAPE_MISMATCH, "factor order != batch rows");
   if (m == 0) return BANDSOLVE_OK;
   if (device_count_cached() == 0) return fail(BANDSOLVE_ERR_INTERNAL, "no CUDA device available (no CPU fallback)");
@@ -1025,7 +1145,8 @@ bandsolve_status solve_host(const Factor& f, double* x, std::size_t n, std::size
     double* d = static_cast<double*>(ctx->buf[s]);
     BSB_CUDA(cudaMemcpy2DAsync(d, ldk * sizeof(double), x + j0, m * sizeof(double), wk * sizeof(double), n,
                                cudaMemcpyHostToDevice, strm));
-    st = solve_device(f, d, false, n, wk, ldk, strm);
+    if (per) st = periodic_device(*per, d, n, wk, ldk, strm, correct_only);
+    else st = solve_device(f, d, false, n, wk, ldk, strm);
     if (st != BANDSOLVE_OK) {
       for (int q = 0; q < stages; ++q) cudaStreamSynchronize(ctx->streams[q]);
       return st;
