@@ -222,6 +222,12 @@ bandsolve_status make_periodic_tri(double a, double b, double c, std::size_t n,
   if (!(std::abs(denom) > kBreakdownEps))
     return fail(BANDSOLVE_ERR_SINGULAR_CORRECTION, "cyclic system is singular: 1 + v.z vanishes");
   p->scale = 1.0 / denom;  // periodic.cpp:67 inv_denom_scale
+  // fused fast path: y_0 = sum_k r0_k dhat_k with U^T r0 = e_0 (U = I + chat superdiagonal)
+  p->fused.assign(2 * n, 0.0);
+  double* r0 = p->fused.data();
+  r0[0] = 1.0;
+  for (std::size_t k = 1; k < n; ++k) r0[k] = -p->factor->chat[k - 1] * r0[k - 1];
+  std::memcpy(p->fused.data() + n, p->z1.data(), n * sizeof(double));
   out = std::move(p);
   return BANDSOLVE_OK;
 }
@@ -273,6 +279,22 @@ bandsolve_status make_periodic_pent(double a, double b, double c, double d,
   p->cap_inv[1] = -cap[0][1] * inv_det;
   p->cap_inv[2] = -cap[1][0] * inv_det;
   p->cap_inv[3] = cap[0][0] * inv_det;
+  // fused fast path: y_0, y_1 = r0.g, r1.g with U^T r = e_0, e_1
+  // (U = I + gamma superdiagonal + delta second superdiagonal)
+  p->fused.assign(4 * n, 0.0);
+  double* r0 = p->fused.data();
+  double* r1 = r0 + n;
+  const Factor& f = *p->factor;
+  r0[0] = 1.0;
+  r0[1] = -f.gamma[0] * r0[0];
+  r1[0] = 0.0;
+  r1[1] = 1.0;
+  for (std::size_t k = 2; k < n; ++k) {
+    r0[k] = -f.gamma[k - 1] * r0[k - 1] - f.delta[k - 2] * r0[k - 2];
+    r1[k] = -f.gamma[k - 1] * r1[k - 1] - f.delta[k - 2] * r1[k - 2];
+  }
+  std::memcpy(r1 + n, p->z1.data(), n * sizeof(double));
+  std::memcpy(r1 + 2 * n, p->z2.data(), n * sizeof(double));
   out = std::move(p);
   return BANDSOLVE_OK;
 }

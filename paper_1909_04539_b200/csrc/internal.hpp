@@ -77,6 +77,9 @@ struct Periodic {
   std::vector<double> z1, z2;
   double v_last = 0.0, scale = 0.0;
   double cap_inv[4] = {0.0, 0.0, 0.0, 0.0};
+  // fused fast-mode sweep: rows 0 (and 1) of U^-1 of A' = L U, then z1 (z2):
+  // r0 | z1 (tri) or r0 | r1 | z1 | z2 (pent), n each
+  std::vector<double> fused;
 
   mutable std::mutex mu;
   mutable std::vector<std::pair<int, double*>> devices;  // z1 | z2 per device

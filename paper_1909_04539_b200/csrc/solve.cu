@@ -373,7 +373,8 @@ int env_int(const char* name, int dflt) {
 // depths that maximise the calibrated throughput estimate
 //   frac = compute(S) x spill_factor(spill) x (round utilisation),
 // preferring the smaller spill on ties.
-bool plan_stream(std::size_t n, std::size_t m, std::size_t elem, bool pent, bool fast, int sms, Plan& p) {
+bool plan_stream(std::size_t n, std::size_t m, std::size_t elem, bool pent, bool fast, int sms, Plan& p,
+                 int per_arrays = 0) {
   const std::size_t fr = fwd_rec_bytes(pent, elem), br = bwd_rec_bytes(pent, elem);
   const std::size_t fac = dev::align128(n * fr) + dev::align128(n * br);
   if (fac > kSmemPerBlockMax / 2 || n < 2) return false;
@@ -399,7 +400,7 @@ bool plan_stream(std::size_t n, std::size_t m, std::size_t elem, bool pent, bool
     const long long groups = (static_cast<long long>(m) + Wg - 1) / Wg;
     const long long grid = std::min<long long>(sms, groups);
     auto fits = [&](int H, int TC) {
-      return dev::StreamLayout::make(N, H, TC, Wg, KB, KR, elem, fr, br).total <= kSmemPerBlockMax;
+      return dev::StreamLayout::make(N, H, TC, Wg, KB, KR, elem, fr, br, per_arrays).total <= kSmemPerBlockMax;
     };
     int H = -1;
     const int all_tc = (N + dev::kSR - 1) / dev::kSR;
@@ -444,7 +445,7 @@ bool plan_stream(std::size_t n, std::size_t m, std::size_t elem, bool pent, bool
       p.stagger_ns = env_int("BANDSOLVE_SSTAG", 0);
       p.warps = P;
       p.model_us = t * 1e6;
-      p.smem_bytes = dev::StreamLayout::make(N, H, TC, Wg, KB, KR, elem, fr, br).total;
+      p.smem_bytes = dev::StreamLayout::make(N, H, TC, Wg, KB, KR, elem, fr, br, per_arrays).total;
       p.V = V;
     }
   }
@@ -626,10 +627,10 @@ cudaError_t launch_persist(const Plan& plan, T* x, int n, long long m, long long
 }
 
 
-template <typename T, int V, bool PENT, bool FAST>
+template <typename T, int V, bool PENT, bool FAST, int PER = 0>
 cudaError_t launch_stream_v(const Plan& plan, T* x, int n, long long m, long long ld, const void* fwd,
-                            const void* bwd, cudaStream_t s, int sms) {
-  auto kern = dev::sweep_stream<T, V, PENT, FAST>;
+                            const void* bwd, cudaStream_t s, int sms, const dev::PerArgs& per = dev::PerArgs{}) {
+  auto kern = dev::sweep_stream<T, V, PENT, FAST, PER>;
   static std::atomic<bool> configured{false};
   if (!configured.load(std::memory_order_relaxed)) {
     cudaError_t e = allow_big_smem(kern);
@@ -651,7 +652,7 @@ cudaError_t launch_stream_v(const Plan& plan, T* x, int n, long long m, long lon
   }
   kern<<<static_cast<unsigned>(grid), (P + 2) * 32, plan.smem_bytes, s>>>(map, x, n, m, ld, plan.H, plan.TC, plan.KB,
                                                                          plan.KR, plan.PD, plan.stagger_ns, groups, fwd, bwd,
-                                                                         scratch);
+                                                                         scratch, per);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();
   if (scratch) {
@@ -1051,12 +1052,14 @@ bandsolve_status periodic_device_z(const Periodic& p, int device, const double**
       return BANDSOLVE_OK;
     }
   const std::size_t n = p.n;
-  std::vector<double> host(2 * n, 0.0);
+  // z1 | z2 (correction kernel) followed by the fused-sweep arrays
+  std::vector<double> host(2 * n + p.fused.size(), 0.0);
   std::memcpy(host.data(), p.z1.data(), n * sizeof(double));
   if (!p.z2.empty()) std::memcpy(host.data() + n, p.z2.data(), n * sizeof(double));
+  std::memcpy(host.data() + 2 * n, p.fused.data(), p.fused.size() * sizeof(double));
   double* d = nullptr;
-  BSB_CUDA(cudaMalloc(&d, 2 * n * sizeof(double)));
-  cudaError_t err = cudaMemcpy(d, host.data(), 2 * n * sizeof(double), cudaMemcpyHostToDevice);
+  BSB_CUDA(cudaMalloc(&d, host.size() * sizeof(double)));
+  cudaError_t err = cudaMemcpy(d, host.data(), host.size() * sizeof(double), cudaMemcpyHostToDevice);
   if (err != cudaSuccess) {
     cudaFree(d);
     return cuda_fail(err, "periodic z upload");
@@ -1096,6 +1099,44 @@ bandsolve_status periodic_device(const Periodic& p, double* x, std::size_t n, st
   if (m == 0) return BANDSOLVE_OK;
   if (device_count_cached() == 0) return fail(BANDSOLVE_ERR_INTERNAL, "no CUDA device available (no CPU fallback)");
   auto s = static_cast<cudaStream_t>(stream);
+  if (!correct_only && current_mode() == BANDSOLVE_MODE_FAST && std::getenv("BANDSOLVE_PERIODIC_UNFUSED") == nullptr) {
+    // fast mode: one fused pass (sweep_stream PER), when a streaming plan fits
+    int device = 0;
+    BSB_CUDA(cudaGetDevice(&device));
+    const int sms = num_sms(device);
+    const bool pent = p.kind != Kind::Tri;
+    const bool aligned = (reinterpret_cast<uintptr_t>(x) % 16 == 0) && ((ld * sizeof(double)) % 16 == 0);
+    Plan plan;
+    if (aligned && n <= static_cast<std::size_t>(INT_MAX) && m <= static_cast<std::size_t>(INT_MAX) / 2 &&
+        plan_stream(n, m, sizeof(double), pent, true, sms, plan, pent ? 4 : 2)) {
+      const DeviceFactor* df = nullptr;
+      bandsolve_status st = ensure_device_factor(*p.factor, device, &df);
+      if (st != BANDSOLVE_OK) return st;
+      const double* blob = nullptr;
+      st = periodic_device_z(p, device, &blob);
+      if (st != BANDSOLVE_OK) return st;
+      keep_pool_memory(device);
+      dev::PerArgs per;
+      per.arrays = blob + 2 * n;
+      if (pent) {
+        for (int k = 0; k < 4; ++k) per.pc[k] = p.cap_inv[k];
+      } else {
+        per.pc[0] = p.v_last;
+        per.pc[1] = p.scale;
+      }
+      const int N = static_cast<int>(n);
+      const long long M = static_cast<long long>(m), LD = static_cast<long long>(ld);
+      cudaError_t err;
+      if (pent)
+        err = plan.V == 2 ? launch_stream_v<double, 2, true, true, 2>(plan, x, N, M, LD, df->fwd[0][1], df->bwd[0][1], s, sms, per)
+                          : launch_stream_v<double, 1, true, true, 2>(plan, x, N, M, LD, df->fwd[0][1], df->bwd[0][1], s, sms, per);
+      else
+        err = plan.V == 2 ? launch_stream_v<double, 2, false, true, 1>(plan, x, N, M, LD, df->fwd[0][1], df->bwd[0][1], s, sms, per)
+                          : launch_stream_v<double, 1, false, true, 1>(plan, x, N, M, LD, df->fwd[0][1], df->bwd[0][1], s, sms, per);
+      if (err != cudaSuccess) return cuda_fail(err, "fused periodic sweep launch");
+      return BANDSOLVE_OK;
+    }
+  }
   if (!correct_only) {
     bandsolve_status st = solve_device(*p.factor, x, false, n, m, ld, stream);
     if (st != BANDSOLVE_OK) return st;

@@ -97,14 +97,16 @@ __device__ __forceinline__ void st_stream_vec(Vec<T, V>* p, Vec<T, V> v) {
 }
 
 struct StreamLayout {
-  size_t fwd_off, bwd_off, bring_off, rring_off, tail_off, bar_off, total;
-  // chunk: elements of one chunk (all warps) = kSR x Wg
+  size_t fwd_off, bwd_off, per_off, bring_off, rring_off, tail_off, bar_off, total;
+  // chunk: elements of one chunk (all warps) = kSR x Wg; per_arrays: fp64
+  // arrays of n for the fused periodic correction (0, 2 tri, 4 pent)
   __host__ __device__ static StreamLayout make(int n, int H, int TC, int Wg, int KB, int KR, size_t elem,
-                                               size_t fwd_rec, size_t bwd_rec) {
+                                               size_t fwd_rec, size_t bwd_rec, int per_arrays = 0) {
     StreamLayout L{};
     L.fwd_off = 0;
     L.bwd_off = align128(static_cast<size_t>(n) * fwd_rec);
-    L.bring_off = L.bwd_off + align128(static_cast<size_t>(n) * bwd_rec);
+    L.per_off = L.bwd_off + align128(static_cast<size_t>(n) * bwd_rec);
+    L.bring_off = L.per_off + align128(static_cast<size_t>(per_arrays) * n * sizeof(double));
     const size_t chunk = static_cast<size_t>(kSR) * Wg * elem;
     L.rring_off = L.bring_off + (H > 0 ? static_cast<size_t>(KB) * chunk : 0);
     L.tail_off = L.rring_off + (H > 0 ? static_cast<size_t>(KR) * chunk : 0);
@@ -224,18 +226,37 @@ struct Cursor {
   }
 };
 
-template <typename T, int V, bool PENT, bool FAST>
+// Fused periodic (cyclic) correction, PER = 1 (tri, rank 1) / 2 (pent,
+// rank 2), fast mode: the correction needs y_0 (y_1), which the backward
+// sweep produces last; but y = U^-1 d-hat, so y_0 = sum_k r0_k d-hat_k with
+// r0 = U^-T e_0 (and r1 = U^-T e_1) fixed by the factor. The forward sweep
+// accumulates these dot products, the correction coefficients are known
+// when the backward sweep starts, and it emits x_i = y_i - w z_i directly:
+// one pass, HBM traffic stays at read b once, write x once.
+// per_g: r0 | z1 (tri) or r0 | r1 | z1 | z2 (pent), n each; pc: v_last,
+// scale (tri) or the capacitance inverse (pent).
+struct PerArgs {
+  const double* arrays = nullptr;
+  double pc[4] = {0.0, 0.0, 0.0, 0.0};
+};
+
+template <typename T, int V, bool PENT, bool FAST, int PER = 0>
 __global__ void __launch_bounds__(32 * (stream_max_warps(V) + 2), 1)
     sweep_stream(const __grid_constant__ CUtensorMap map_b, T* __restrict__ x, int n, long long m, long long ld,
                  int H, int TC, int KB, int KR, int PD, int stagger_ns, long long groups,
-                 const void* __restrict__ fwd_g, const void* __restrict__ bwd_g, T* __restrict__ scratch) {
+                 const void* __restrict__ fwd_g, const void* __restrict__ bwd_g, T* __restrict__ scratch,
+                 const PerArgs per) {
+  static_assert(PER == 0 || (FAST && sizeof(T) == 8 && (PER == 2) == PENT), "fused periodic: fast fp64 only");
+  constexpr int kPerArrays = PER == 0 ? 0 : (PER == 1 ? 2 : 4);
   using FwdR = typename Recs<T, PENT>::Fwd;
   using BwdR = typename Recs<T, PENT>::Bwd;
   extern __shared__ __align__(128) unsigned char smem[];
   const int P = static_cast<int>(blockDim.x >> 5) - 2;  // compute warps; warp P loads b, warp P+1 reloads
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const StreamLayout L = StreamLayout::make(n, H, TC, P * 32 * V, KB, KR, sizeof(T), sizeof(FwdR), sizeof(BwdR));
+  const StreamLayout L =
+      StreamLayout::make(n, H, TC, P * 32 * V, KB, KR, sizeof(T), sizeof(FwdR), sizeof(BwdR), kPerArrays);
+  const double* const spc = reinterpret_cast<const double*>(smem + L.per_off);  // staged per arrays
   const FwdR* sf = reinterpret_cast<const FwdR*>(smem + L.fwd_off);
   const BwdR* sb = reinterpret_cast<const BwdR*>(smem + L.bwd_off);
   T* bring = reinterpret_cast<T*>(smem + L.bring_off);
@@ -265,6 +286,10 @@ __global__ void __launch_bounds__(32 * (stream_max_warps(V) + 2), 1)
     int4* db = reinterpret_cast<int4*>(smem + L.bwd_off);
     for (int k = threadIdx.x; k < nf; k += blockDim.x) df[k] = gf[k];
     for (int k = threadIdx.x; k < nb; k += blockDim.x) db[k] = gb[k];
+    if constexpr (PER != 0) {
+      double* dp = reinterpret_cast<double*>(smem + L.per_off);
+      for (int k = threadIdx.x; k < kPerArrays * n; k += blockDim.x) dp[k] = per.arrays[k];
+    }
   }
   if (threadIdx.x == 0) {
     for (int k = 0; k < KB; ++k) {
@@ -415,6 +440,29 @@ __global__ void __launch_bounds__(32 * (stream_max_warps(V) + 2), 1)
       out -= ld;
     };
     P2 s1{}, s2{};
+    // fused periodic: y_0 (y_1) accumulated as dot products of the forward
+    // outputs; correction coefficients w (tri) / t1, t2 (pent) per system
+    P2 acc0{}, acc1{}, c1{}, c2{};
+    auto accum = [&](int row, P2 v) {
+      if constexpr (PER != 0) {
+#pragma unroll
+        for (int q = 0; q < V; ++q) {
+          acc0.v[q] = fma_rn(T(spc[row]), v.v[q], acc0.v[q]);
+          if constexpr (PER == 2) acc1.v[q] = fma_rn(T(spc[n + row]), v.v[q], acc1.v[q]);
+        }
+      }
+    };
+    auto emit = [&](int row, P2 y) {  // x_i = y_i - w z_i  (pent: - (z1_i t1 + z2_i t2))
+      if constexpr (PER == 1) {
+#pragma unroll
+        for (int q = 0; q < V; ++q) y.v[q] = fma_rn(-c1.v[q], T(spc[n + row]), y.v[q]);
+      } else if constexpr (PER == 2) {
+#pragma unroll
+        for (int q = 0; q < V; ++q)
+          y.v[q] = fma_rn(-c1.v[q], T(spc[2 * n + row]), fma_rn(-c2.v[q], T(spc[3 * n + row]), y.v[q]));
+      }
+      put(y);
+    };
 
     // ---- forward, head rows: b ring -> registers -> d-hat spilled to L2
     {
@@ -431,7 +479,10 @@ __global__ void __launch_bounds__(32 * (stream_max_warps(V) + 2), 1)
             if (lane == 0) mbar_arrive(&b_empty[brl.slot]);
             brl.next(KB);
           },
-          [&](int c, int r, P2*, P2 v) { st_spill_vec<T, V>(spill_l + c * cpairs + r * kPR, v, pol_keep); });
+          [&](int c, int r, P2*, P2 v) {
+            st_spill_vec<T, V>(spill_l + c * cpairs + r * kPR, v, pol_keep);
+            accum(c * kSR + r, v);
+          });
     }
     if (HC > 0) {  // publish the spill to the async proxy (the reloader's bulk copies)
       fence_proxy_async_global();
@@ -443,14 +494,33 @@ __global__ void __launch_bounds__(32 * (stream_max_warps(V) + 2), 1)
     auto tslot = [&](int k) { return tail_l + tail_slot(k, par) * cpairs; };
     fwd_chunks<T, V, PENT, FAST>(
         tfull, sf + H, s1, s2, tslot, [&](int k) { mbar_wait(&t_full[tail_slot(k, par)], par); }, [](int) {},
-        [](int, int, P2* p, P2 v) { *p = v; });
+        [&](int c, int r, P2* p, P2 v) {
+          *p = v;
+          accum(H + c * kSR + r, v);
+        });
     if (trem > 0) {
       mbar_wait(&t_full[tail_slot(tfull, par)], par);
       P2* p = tslot(tfull);
       const FwdR* f = sf + H + tfull * kSR;
-      for (int r = 0; r < trem; ++r) p[r * kPR] = fwd_vec<T, V, PENT, FAST>(f[r], p[r * kPR], s1, s2);
+      for (int r = 0; r < trem; ++r) {
+        p[r * kPR] = fwd_vec<T, V, PENT, FAST>(f[r], p[r * kPR], s1, s2);
+        accum(H + tfull * kSR + r, p[r * kPR]);
+      }
     }
     fence_proxy_async_smem();  // in-place smem writes before the TMA refills of these slots
+    if constexpr (PER == 1) {  // w = (y_0 + v_last y_{n-1}) * scale, y_{n-1} = d-hat_{n-1}
+#pragma unroll
+      for (int q = 0; q < V; ++q) c1.v[q] = T(per.pc[1]) * fma_rn(T(per.pc[0]), s1.v[q], acc0.v[q]);
+    } else if constexpr (PER == 2) {  // y_{n-1} = g_{n-1}, y_{n-2} = g_{n-2} - gamma_{n-2} g_{n-1}
+#pragma unroll
+      for (int q = 0; q < V; ++q) {
+        const T yl = s1.v[q];
+        const T yl2 = fma_rn(-T(sb[n - 2].g), s1.v[q], s2.v[q]);
+        const T w1 = acc0.v[q] - yl, w2 = acc1.v[q] - yl2;
+        c1.v[q] = fma_rn(T(per.pc[0]), w1, T(per.pc[1]) * w2);
+        c2.v[q] = fma_rn(T(per.pc[2]), w1, T(per.pc[3]) * w2);
+      }
+    }
 
     // ---- backward, tail rows: smem -> x streamed to HBM; each drained chunk
     // goes back to the loader for the next group
@@ -463,12 +533,13 @@ __global__ void __launch_bounds__(32 * (stream_max_warps(V) + 2), 1)
     if (trem > 0) {
       const P2* p = tslot(tfull);
       const BwdR* b = sb + H + tfull * kSR;
-      for (int r = trem - 1; r >= 0; --r) put(bwd_vec<T, V, PENT, FAST>(b[r], p[r * kPR], s1, s2));
+      for (int r = trem - 1; r >= 0; --r)
+        emit(H + tfull * kSR + r, bwd_vec<T, V, PENT, FAST>(b[r], p[r * kPR], s1, s2));
       tail_release(tfull);
     }
     bwd_chunks<T, V, PENT, FAST>(
         tfull, sb + H, s1, s2, [&](int k) -> const P2* { return tslot(k); }, [](int) {}, tail_release,
-        [&](int, int, P2 v) { put(v); });
+        [&](int c, int r, P2 v) { emit(H + c * kSR + r, v); });
 
     // ---- backward, head rows: d-hat back through the reload ring (or, with
     // KR == 0, through the b ring: one FIFO), x to HBM
@@ -493,7 +564,7 @@ __global__ void __launch_bounds__(32 * (stream_max_warps(V) + 2), 1)
             if (lane == 0) mbar_arrive(&empty[cr.slot]);
             cr.next(K);
           },
-          [&](int, int, P2 v) { put(v); });
+          [&](int c, int r, P2 v) { emit(c * kSR + r, v); });
     }
   };
   for (; g < groups; g += gridDim.x, ++it) {

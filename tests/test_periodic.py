@@ -205,3 +205,31 @@ def test_gpu_periodic_shape_mismatch(lib, cuda_device):
     with pytest.raises(bs.BandsolveError) as e:
         p.solve(b)
     assert e.value.status == bs.ERR_SHAPE_MISMATCH
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("wg", [None, "64", "96", "128"])
+def test_gpu_periodic_fused_fast_within_tolerance(lib, oracle, cuda_device, wg):
+    """Fast mode fuses the correction into the sweep (y_0, y_1 from dot products
+    of the forward outputs): within the 1e-12 fp64 tolerance of the reference."""
+    torch = cuda_device
+    set_plan(("stream", wg) if wg else None)
+    lib.set_mode(bs.MODE_FAST)
+    rng = np.random.default_rng(21)
+    try:
+        for n, m in [(6, 5), (33, 70), (256, 300), (512, 1000), (1024, 130)]:
+            x = rng.uniform(-1, 1, (n, m))
+            for bands in [(-1.0, 3.0, -1.0), (-0.3, 1.9, -0.5), (1.0, -4.0, 7.0, -4.0, 1.0),
+                          (0.2, -0.8, 3.1, -0.7, 0.1)]:
+                p = make(lib, bands, n)
+                for ld in (m, m + (m % 2) + 2):
+                    buf = torch.zeros((n, ld), dtype=torch.float64, device="cuda")
+                    buf[:, :m] = torch.from_numpy(x).cuda()
+                    p.solve_dev(buf.data_ptr(), n, m, ld=ld, stream=torch.cuda.current_stream().cuda_stream)
+                    torch.cuda.synchronize()
+                    got = buf[:, :m].cpu().numpy()
+                    want = oracle_solve(oracle, bands, x)
+                    assert per_system_max_rel(got, want) <= 1e-12, (wg, n, m, ld, bands)
+    finally:
+        lib.set_mode(bs.MODE_EXACT)
+        set_plan(None)
