@@ -245,6 +245,7 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
     elem = 4 if args.f32 else 8
     dt = torch.float32 if args.f32 else torch.float64
     bands = lhs_for(kind, n)
+    args.periodic = args.periodic or args.cn
     if args.periodic:  # cyclic constant-band system: shared sweep of A' + wrap correction
         consts = (-1.0, 3.0, -1.0) if kind == "tri" else (1.0, -4.0, 7.0, -4.0, 1.0)
         fac = bs.PeriodicTri(lib, *consts, n) if kind == "tri" else bs.PeriodicPent(lib, *consts, n)
@@ -265,8 +266,14 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
     sptr = stream.cuda_stream
     clocks = ClockSampler(local_rank)
 
+    cn_sigma = 1.0  # pde.cpp default dt: sigma_x = 1
+
     def step(k):
-        fac.solve_dev(bufs[k % nbuf].data_ptr(), n, m, ld=m, stream=sptr, f32=args.f32)
+        if args.cn:  # one Crank-Nicolson step: u_{k+1} = A^-1 B u_k, ping-pong buffers
+            fac.cn_step_dev(cn_sigma, bufs[k % nbuf].data_ptr(), bufs[(k + 1) % nbuf].data_ptr(), n, m, ld=m,
+                            stream=sptr)
+        else:
+            fac.solve_dev(bufs[k % nbuf].data_ptr(), n, m, ld=m, stream=sptr, f32=args.f32)
 
     for k in range(args.warmup):
         step(k)
@@ -305,7 +312,7 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
     # e2e through the reference-facing host API (pinned host batch; H2D,
     # sweep, D2H inside bandsolve_*_solve_shared, synchronous)
     e2e = None
-    if not args.f32:
+    if not args.f32 and not args.cn:
         host = bs.Batch.from_array(lib, bufs[0].cpu().numpy())
         e2e_steps = max(1, min(args.steps, 50))
         for _ in range(min(args.warmup, 3)):
@@ -336,7 +343,7 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
             "vs_baseline": None, "dtype": "f32" if args.f32 else "f64",
             "data": "synthetic: U(-1,1) RHS from SplitMix64(seed=42, i, global j), generated on device",
             "config": {"workload": desc, "kind": kind, "n": n, "batch_per_gpu": m, "global_batch": m * world,
-                       "mode": args.mode, "plan": plan, "periodic": bool(args.periodic),
+                       "mode": args.mode, "plan": plan, "periodic": bool(args.periodic), "cn_step": bool(args.cn),
                        "parallelism": f"dp{world} (systems sharded, no data-path collective)",
                        "l2": f"{nbuf} rotating in-place buffers of {bytes_per / 2**20:.0f} MiB "
                              f"(working set {nbuf * bytes_per / 132644864:.1f}x L2)"},
@@ -363,6 +370,8 @@ def main() -> int:
     ap.add_argument("--f32", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--periodic", action="store_true", help="cyclic (periodic) variant of the config's LHS")
+    ap.add_argument("--cn", action="store_true",
+                    help="Crank-Nicolson step (periodic stencil RHS + cyclic solve, sigma_x = 1) per step")
     ap.add_argument("--n", type=int, default=0, help="override the config's rows per system (tuning)")
     ap.add_argument("--m", type=int, default=0, help="override the config's systems per GPU (tuning)")
     args = ap.parse_args()

@@ -153,6 +153,61 @@ bandsolve_status bandsolve_periodic_pent_modified_bands(
 bandsolve_status bandsolve_periodic_pent_correct(
     const bandsolve_periodic_pent* corr, bandsolve_batch* batch);
 
+/* ---- Storage accounting (ref bandsolve.h:148-163, batch.cpp:72-105) -------- */
+typedef enum bandsolve_storage_variant {
+  BANDSOLVE_STORAGE_TRI_PER_SYSTEM = 0,
+  BANDSOLVE_STORAGE_TRI_SHARED = 1,
+  BANDSOLVE_STORAGE_PENT_PER_SYSTEM = 2,
+  BANDSOLVE_STORAGE_PENT_SHARED = 3,
+  BANDSOLVE_STORAGE_PENT_UNIFORM = 4
+} bandsolve_storage_variant;
+
+bandsolve_status bandsolve_footprint(bandsolve_storage_variant variant,
+                                     size_t n, size_t m, uint64_t* elements,
+                                     double* reduction_vs_baseline);
+
+/* ---- Crank-Nicolson driver (ref bandsolve.h:182-220, capi.cpp:369-411,
+ * pde.cpp run_benchmark). Periodic diffusion through the tridiagonal path,
+ * periodic hyperdiffusion through the pentadiagonal path, from the
+ * reference's default initial field. Same parameters, checks, statuses and
+ * IBAT dumps; the stepping loop (RHS assembly + cyclic solve per step) runs
+ * on the GPU and each step is timed with CUDA events. The uniform variant
+ * is the shared one (bitwise identical, pent_solver.cpp:83-97); the
+ * per-system variant is outside this library (BANDSOLVE_ERR_BAD_ARG). */
+typedef enum bandsolve_problem {
+  BANDSOLVE_PROBLEM_DIFFUSION = 0,
+  BANDSOLVE_PROBLEM_HYPERDIFFUSION = 1
+} bandsolve_problem;
+
+typedef enum bandsolve_variant {
+  BANDSOLVE_VARIANT_SHARED = 0,
+  BANDSOLVE_VARIANT_PER_SYSTEM = 1,
+  BANDSOLVE_VARIANT_UNIFORM = 2 /* hyperdiffusion only */
+} bandsolve_variant;
+
+typedef struct bandsolve_bench_params {
+  size_t n;
+  size_t m;
+  long steps;
+  double dt; /* <= 0 selects the default with sigma_x = 1 */
+  int problem; /* bandsolve_problem */
+  int variant; /* bandsolve_variant */
+  long dump_every; /* 0 disables IBAT field dumps */
+  const char* dump_prefix; /* may be NULL when dump_every is 0 */
+} bandsolve_bench_params;
+
+typedef struct bandsolve_bench_result {
+  double wall_s;
+  double per_step_mean_s;
+  double per_step_std_s;
+  uint64_t elements; /* storage footprint of the variant */
+  int threads;
+  long steps;
+} bandsolve_bench_result;
+
+bandsolve_status bandsolve_bench_run(const bandsolve_bench_params* params,
+                                     bandsolve_bench_result* result);
+
 /* ---- Residuals (ref bandsolve.h:165-179, tri_solver.cpp:116-156,
  * pent_solver.cpp:223-273) — max over systems of ||A x - rhs||_inf /
  * ||rhs||_inf, evaluated on the GPU in the reference's operation order.
@@ -230,6 +285,18 @@ bandsolve_status bandsolve_periodic_pent_solve_dev(
 bandsolve_status bandsolve_periodic_pent_correct_dev(
     const bandsolve_periodic_pent* corr, double* x, size_t n, size_t m,
     size_t ld, void* stream);
+
+/* One Crank-Nicolson step on device arrays: out = A^-1 (B u) with B the
+ * explicit periodic stencil of pde.cpp:73-114 for sigma_x (diffusion:
+ * s (u[i-1] + u[i+1]) + (1 - 2s) u[i]; hyperdiffusion: -s (u[i-2] + u[i+2])
+ * + 4s (u[i-1] + u[i+1]) + (1 - 6s) u[i], indices mod n) and A the cyclic
+ * LHS held by the handle. u and out must not alias (pitch ld, stream-ordered). */
+bandsolve_status bandsolve_periodic_tri_cn_step_dev(
+    const bandsolve_periodic_tri* lhs, double sigma_x, const double* u,
+    double* out, size_t n, size_t m, size_t ld, void* stream);
+bandsolve_status bandsolve_periodic_pent_cn_step_dev(
+    const bandsolve_periodic_pent* lhs, double sigma_x, const double* u,
+    double* out, size_t n, size_t m, size_t ld, void* stream);
 
 /* Device residual of a device-resident solution against a device-resident
  * right-hand side (both n x m, pitch ld), bands on the host. Synchronous:

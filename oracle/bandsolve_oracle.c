@@ -518,3 +518,45 @@ void oracle_periodic_pent_apply(const double* z1, const double* z2,
     for (size_t i = 0; i < n; ++i) x[i * m + j] -= z1[i] * t1 + z2[i] * t2;
   }
 }
+
+/* ---- Crank-Nicolson pieces (reference pde.cpp) ------------------------------ */
+
+void oracle_default_mode_initial(size_t n, size_t m, double* out) {
+  /* pde.cpp:48-58 */
+  const size_t mode_span = n / 4 > 0 ? n / 4 : 1;
+  const double pi = 3.141592653589793238462643383279502884; /* std::numbers::pi */
+  for (size_t j = 0; j < m; ++j) {
+    const double k = (double)(1 + (j % mode_span));
+    for (size_t i = 0; i < n; ++i) {
+      const double x = (double)(i + 1) / (double)n;
+      out[i * m + j] = sin(2.0 * pi * k * x);
+    }
+  }
+}
+
+void oracle_cn_rhs(int problem, double sigma_x, size_t n, size_t m,
+                   const double* u, double* out) {
+  if (problem == 0) { /* diffusion_rhs_into, pde.cpp:73-91 */
+    const double s = sigma_x;
+    const double mid = 1.0 - 2.0 * sigma_x;
+    for (size_t i = 0; i < n; ++i) {
+      const double* up = u + (i == 0 ? n - 1 : i - 1) * m;
+      const double* mi = u + i * m;
+      const double* dn = u + (i + 1 == n ? 0 : i + 1) * m;
+      for (size_t j = 0; j < m; ++j) out[i * m + j] = s * (up[j] + dn[j]) + mid * mi[j];
+    }
+  } else { /* hyper_rhs_into, pde.cpp:93-114 */
+    const double s = sigma_x;
+    const double s4 = 4.0 * sigma_x;
+    const double mid = 1.0 - 6.0 * sigma_x;
+    for (size_t i = 0; i < n; ++i) {
+      const double* u2 = u + ((i + n - 2) % n) * m;
+      const double* u1 = u + (i == 0 ? n - 1 : i - 1) * m;
+      const double* mi = u + i * m;
+      const double* d1 = u + (i + 1 == n ? 0 : i + 1) * m;
+      const double* d2 = u + ((i + 2) % n) * m;
+      for (size_t j = 0; j < m; ++j)
+        out[i * m + j] = -s * (u2[j] + d2[j]) + s4 * (u1[j] + d1[j]) + mid * mi[j];
+    }
+  }
+}

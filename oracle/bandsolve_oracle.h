@@ -101,6 +101,13 @@ void oracle_periodic_pent_apply(const double* z1, const double* z2,
                                 const double* cap_inv, size_t n, size_t m,
                                 double* x);
 
+/* Crank-Nicolson pieces of reference pde.cpp: default_mode_initial
+ * (:48-58) and the periodic explicit stencils diffusion_rhs_into (:73-91,
+ * problem 0) / hyper_rhs_into (:93-114, problem 1), out = B u. */
+void oracle_default_mode_initial(size_t n, size_t m, double* out);
+void oracle_cn_rhs(int problem, double sigma_x, size_t n, size_t m,
+                   const double* u, double* out);
+
 /* Counter-based synthetic RHS shared with the device generator:
  * U(-1, 1) from SplitMix64 of (seed, i, j), 53-bit mantissa. */
 double oracle_rhs_value(uint64_t seed, uint64_t i, uint64_t j);

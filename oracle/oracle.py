@@ -81,6 +81,10 @@ class Oracle:
         L.oracle_periodic_pent_prepare.argtypes = [C.c_double] * 5 + [_sz] + [_dp] * 8
         L.oracle_periodic_pent_apply.argtypes = [_dp, _dp, _dp, _sz, _sz, _dp]
         L.oracle_periodic_pent_apply.restype = None
+        L.oracle_default_mode_initial.argtypes = [_sz, _sz, _dp]
+        L.oracle_default_mode_initial.restype = None
+        L.oracle_cn_rhs.argtypes = [C.c_int, C.c_double, _sz, _sz, _dp, _dp]
+        L.oracle_cn_rhs.restype = None
 
     # -- factors ------------------------------------------------------------
     def tri_prefactor(self, sub, diag, sup) -> dict:
@@ -164,6 +168,43 @@ class Oracle:
             self.pent_solve(f, x)
         self.lib.oracle_periodic_pent_apply(_d(f["z1"]), _d(f["z2"]), _d(f["cap_inv"]), n, m, _d(x))
         return x
+
+    # -- Crank-Nicolson (reference pde.cpp) ---------------------------------------
+    def default_mode_initial(self, n: int, m: int) -> np.ndarray:
+        out = np.empty((n, m))
+        self.lib.oracle_default_mode_initial(n, m, _d(out))
+        return out
+
+    def cn_rhs(self, problem: int, sigma_x: float, u: np.ndarray) -> np.ndarray:
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        n, m = u.shape
+        out = np.empty_like(u)
+        self.lib.oracle_cn_rhs(problem, sigma_x, n, m, _d(u), _d(out))
+        return out
+
+    @staticmethod
+    def cn_sigma(problem: int, n: int, dt: float = 0.0) -> float:
+        """bench_config::sigma_x (pde.cpp:29-46)."""
+        dx = 1.0 / n
+        pow_dx = dx * dx if problem == 0 else dx * dx * dx * dx
+        dtv = dt if dt > 0.0 else 1.0 * 2.0 * pow_dx
+        return dtv / (2.0 * pow_dx)
+
+    def cn_trajectory(self, problem: int, n: int, m: int, steps: int, dt: float = 0.0) -> list:
+        """Fields after each step of run_benchmark (pde.cpp:279-343), shared variant."""
+        s = self.cn_sigma(problem, n, dt)
+        if problem == 0:
+            f = self.periodic_tri_prepare(-s, 1.0 + 2.0 * s, -s, n)
+            solve = self.periodic_tri_solve
+        else:
+            f = self.periodic_pent_prepare(s, -4.0 * s, 1.0 + 6.0 * s, -4.0 * s, s, n)
+            solve = self.periodic_pent_solve
+        u = self.default_mode_initial(n, m)
+        out = []
+        for _ in range(steps):
+            u = solve(f, self.cn_rhs(problem, s, u))
+            out.append(u.copy())
+        return out
 
     # -- checks ---------------------------------------------------------------
     def tri_residual(self, sub, diag, sup, x, rhs, cyclic=False) -> float:

@@ -43,6 +43,22 @@ _vp = C.c_void_p
 _sz = C.c_size_t
 _st = C.c_int
 
+class BenchParams(C.Structure):
+    """bandsolve_bench_params (ref bandsolve.h:199-208)."""
+    _fields_ = [("n", C.c_size_t), ("m", C.c_size_t), ("steps", C.c_long), ("dt", C.c_double),
+                ("problem", C.c_int), ("variant", C.c_int), ("dump_every", C.c_long),
+                ("dump_prefix", C.c_char_p)]
+
+
+class BenchResult(C.Structure):
+    """bandsolve_bench_result (ref bandsolve.h:210-217)."""
+    _fields_ = [("wall_s", C.c_double), ("per_step_mean_s", C.c_double), ("per_step_std_s", C.c_double),
+                ("elements", C.c_uint64), ("threads", C.c_int), ("steps", C.c_long)]
+
+
+PROBLEM_DIFFUSION, PROBLEM_HYPERDIFFUSION = 0, 1
+VARIANT_SHARED, VARIANT_PER_SYSTEM, VARIANT_UNIFORM = 0, 1, 2
+
 # (name, restype, argtypes) of the reference ABI subset (ref bandsolve.h)
 _REFERENCE_SIGS = [
     ("bandsolve_status_string", C.c_char_p, [_st]),
@@ -77,6 +93,8 @@ _REFERENCE_SIGS = [
     ("bandsolve_periodic_pent_solve", _st, [_vp, _vp]),
     ("bandsolve_periodic_pent_modified_bands", _st, [_vp] + [_dp] * 5),
     ("bandsolve_periodic_pent_correct", _st, [_vp, _vp]),
+    ("bandsolve_footprint", _st, [C.c_int, _sz, _sz, C.POINTER(C.c_uint64), _dp]),
+    ("bandsolve_bench_run", _st, [C.POINTER(BenchParams), C.POINTER(BenchResult)]),
 ]
 
 # B200 extensions (include/bandsolve.h, second part)
@@ -105,6 +123,8 @@ _EXTENSION_SIGS = [
     ("bandsolve_periodic_tri_correct_dev", _st, [_vp, _vp, _sz, _sz, _sz, _vp]),
     ("bandsolve_periodic_pent_solve_dev", _st, [_vp, _vp, _sz, _sz, _sz, _vp]),
     ("bandsolve_periodic_pent_correct_dev", _st, [_vp, _vp, _sz, _sz, _sz, _vp]),
+    ("bandsolve_periodic_tri_cn_step_dev", _st, [_vp, C.c_double, _vp, _vp, _sz, _sz, _sz, _vp]),
+    ("bandsolve_periodic_pent_cn_step_dev", _st, [_vp, C.c_double, _vp, _vp, _sz, _sz, _sz, _vp]),
     ("bandsolve_describe_plan", _st, [C.c_int, _sz, _sz, _sz, C.c_int, C.c_char_p, _sz]),
     ("bandsolve_kernel_launches", C.c_uint64, []),
     ("bandsolve_last_error", C.c_char_p, []),
@@ -195,6 +215,21 @@ class Library:
         self.check(fn(ptr, n, m, ld, seed, j_offset, stream), "fill_rhs_dev")
 
     # -- residuals ----------------------------------------------------------
+    def footprint(self, variant: int, n: int, m: int) -> tuple[int, float]:
+        el, red = C.c_uint64(), C.c_double()
+        self.check(self.lib.bandsolve_footprint(variant, n, m, C.byref(el), C.byref(red)), "footprint")
+        return int(el.value), float(red.value)
+
+    def bench_run(self, n: int, m: int, steps: int, problem: int = PROBLEM_DIFFUSION,
+                  variant: int = VARIANT_SHARED, dt: float = 0.0, dump_every: int = 0,
+                  dump_prefix: Optional[str] = None) -> BenchResult:
+        """bandsolve_bench_run (ref bandsolve.h:219-220): Crank-Nicolson stepping."""
+        p = BenchParams(n, m, steps, dt, problem, variant, dump_every,
+                        dump_prefix.encode() if dump_prefix else None)
+        r = BenchResult()
+        self.check(self.lib.bandsolve_bench_run(C.byref(p), C.byref(r)), "bench_run")
+        return r
+
     def tri_residual(self, sub, diag, sup, x: "Batch", rhs: "Batch", cyclic: bool = False) -> float:
         n = len(diag)
         s, d, u = _f64(sub, n), _f64(diag, n), _f64(sup, n)
@@ -381,6 +416,16 @@ class _Periodic(_Factor):
                                                                   stream), self._correct_dev)
 
 
+def read_ibat(path: str) -> np.ndarray:
+    """IBAT file (batch.cpp:146-218): 'IBAT', u32 version 1, u64 n, u64 m, n*m LE binary64."""
+    with open(path, "rb") as f:
+        blob = f.read()
+    if blob[:4] != b"IBAT" or int.from_bytes(blob[4:8], "little") != 1:
+        raise ValueError(f"not an IBAT v1 file: {path}")
+    n, m = int.from_bytes(blob[8:16], "little"), int.from_bytes(blob[16:24], "little")
+    return np.frombuffer(blob, dtype="<f8", count=n * m, offset=24).reshape(n, m).astype(np.float64)
+
+
 class PeriodicTri(_Periodic):
     """bandsolve_periodic_tri (ref bandsolve.h:118-131): cyclic constant-band
     tridiagonal system, rank-1 wrap correction."""
@@ -394,6 +439,12 @@ class PeriodicTri(_Periodic):
         h = _vp()
         lib.check(lib.lib.bandsolve_periodic_tri_create(a, b, c, n, C.byref(h)), "periodic_tri_create")
         super().__init__(lib, h, n)
+
+    def cn_step_dev(self, sigma_x: float, u_ptr: int, out_ptr: int, n: int, m: int, ld: Optional[int] = None,
+                    stream: int = 0) -> None:
+        self.lib.check(self.lib.lib.bandsolve_periodic_tri_cn_step_dev(self.handle, sigma_x, u_ptr, out_ptr, n, m,
+                                                                        m if ld is None else ld, stream),
+                       "periodic_tri_cn_step_dev")
 
     def modified_bands(self):
         out = [np.empty(self.n) for _ in range(3)]
@@ -415,6 +466,12 @@ class PeriodicPent(_Periodic):
         h = _vp()
         lib.check(lib.lib.bandsolve_periodic_pent_create(a, b, c, d, e, n, C.byref(h)), "periodic_pent_create")
         super().__init__(lib, h, n)
+
+    def cn_step_dev(self, sigma_x: float, u_ptr: int, out_ptr: int, n: int, m: int, ld: Optional[int] = None,
+                    stream: int = 0) -> None:
+        self.lib.check(self.lib.lib.bandsolve_periodic_pent_cn_step_dev(self.handle, sigma_x, u_ptr, out_ptr, n, m,
+                                                                         m if ld is None else ld, stream),
+                       "periodic_pent_cn_step_dev")
 
     def modified_bands(self):
         out = [np.empty(self.n) for _ in range(5)]

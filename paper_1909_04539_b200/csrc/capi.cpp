@@ -300,6 +300,55 @@ BSB_API bandsolve_status bandsolve_periodic_pent_correct_dev(const bandsolve_per
   return guarded([&] { return bsb::periodic_device(*corr->impl, x, n, m, ld, stream, true); });
 }
 
+// ---- Crank-Nicolson (capi.cpp:300-411) ------------------------------------------
+BSB_API bandsolve_status bandsolve_footprint(bandsolve_storage_variant variant, size_t n, size_t m,
+                                             uint64_t* elements, double* reduction_vs_baseline) {
+  // batch.cpp:72-105
+  if (!elements) return null_arg();
+  if (n < 2 || m < 1) return bsb::fail(BANDSOLVE_ERR_BAD_ARG, "footprint needs n >= 2, m >= 1");
+  const uint64_t un = n, um = m;
+  uint64_t count = 0, baseline = 0;
+  switch (variant) {
+    case BANDSOLVE_STORAGE_TRI_PER_SYSTEM: count = baseline = 4 * um * un; break;
+    case BANDSOLVE_STORAGE_TRI_SHARED: count = 3 * un + un * um; baseline = 4 * um * un; break;
+    case BANDSOLVE_STORAGE_PENT_PER_SYSTEM: count = baseline = 6 * um * un; break;
+    case BANDSOLVE_STORAGE_PENT_SHARED: count = 5 * un + un * um; baseline = 6 * um * un; break;
+    case BANDSOLVE_STORAGE_PENT_UNIFORM: count = 4 * un + un * um; baseline = 6 * um * un; break;
+    default: return bsb::fail(BANDSOLVE_ERR_BAD_ARG, "unknown storage variant");
+  }
+  *elements = count;
+  if (reduction_vs_baseline)
+    *reduction_vs_baseline = 1.0 - static_cast<double>(count) / static_cast<double>(baseline);
+  return BANDSOLVE_OK;
+}
+
+BSB_API bandsolve_status bandsolve_bench_run(const bandsolve_bench_params* params, bandsolve_bench_result* result) {
+  if (!params || !result) return null_arg();
+  return guarded([&] { return bsb::bench_run_device(*params, result, bandsolve_get_threads()); });
+}
+
+BSB_API bandsolve_status bandsolve_periodic_tri_cn_step_dev(const bandsolve_periodic_tri* lhs, double sigma_x,
+                                                            const double* u, double* out, size_t n, size_t m,
+                                                            size_t ld, void* stream) {
+  if (!lhs) return null_arg();
+  return guarded([&] {
+    bandsolve_status st = bsb::cn_rhs_device(false, sigma_x, u, out, n, m, ld, stream);
+    if (st != BANDSOLVE_OK) return st;
+    return bsb::periodic_device(*lhs->impl, out, n, m, ld, stream, false);
+  });
+}
+
+BSB_API bandsolve_status bandsolve_periodic_pent_cn_step_dev(const bandsolve_periodic_pent* lhs, double sigma_x,
+                                                             const double* u, double* out, size_t n, size_t m,
+                                                             size_t ld, void* stream) {
+  if (!lhs) return null_arg();
+  return guarded([&] {
+    bandsolve_status st = bsb::cn_rhs_device(true, sigma_x, u, out, n, m, ld, stream);
+    if (st != BANDSOLVE_OK) return st;
+    return bsb::periodic_device(*lhs->impl, out, n, m, ld, stream, false);
+  });
+}
+
 // ---- residuals (capi.cpp:327-367) ----------------------------------------------
 namespace {
 

@@ -112,6 +112,16 @@ bandsolve_status solve_device(const Factor& f, void* x, bool f32,
 bandsolve_status solve_host(const Factor& f, double* x, std::size_t n,
                             std::size_t m, const Periodic* per = nullptr,
                             bool correct_only = false);
+// Crank-Nicolson explicit half B u with the periodic stencil of
+// pde.cpp:73-114 (out must not alias u), stream-ordered.
+bandsolve_status cn_rhs_device(bool pent, double sigma_x, const double* u,
+                               double* out, std::size_t n, std::size_t m,
+                               std::size_t ld, void* stream);
+// bandsolve_bench_run: the reference's Crank-Nicolson driver (capi.cpp:369,
+// pde.cpp run_benchmark) with the stepping loop on the GPU.
+bandsolve_status bench_run_device(const bandsolve_bench_params& prm,
+                                  bandsolve_bench_result* res,
+                                  int threads_report);
 // Periodic solve / correction of a device array (pitch ld), stream-ordered.
 bandsolve_status periodic_device(const Periodic& p, double* x, std::size_t n,
                                  std::size_t m, std::size_t ld, void* stream,

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <atomic>
 #include <climits>
 #include <cstdio>
@@ -889,6 +890,45 @@ __global__ void periodic_pent_correct_kernel(double* __restrict__ x, int n, long
   for (; i < n; ++i) Y(i) = sub_rn(Y(i), add_rn(mul_rn(__ldg(z1 + i), t1), mul_rn(__ldg(z2 + i), t2)));
 }
 
+// ---- Crank-Nicolson explicit half, periodic stencil (reference pde.cpp:73-114) --
+// One thread per system walks its column with a register window of the
+// stencil's neighbours (wrap-around rows preloaded), so each row of u is
+// read once and each row of out written once; the reference's operation
+// order with separately rounded operations:
+//   diffusion  o = s*(u[i-1] + u[i+1]) + mid*u[i]                    (:85)
+//   hyper      o = -s*(u[i-2] + u[i+2]) + s4*(u[i-1] + u[i+1]) + mid*u[i]   (:108)
+template <bool PENT>
+__global__ void cn_rhs_kernel(const double* __restrict__ u, double* __restrict__ out, int n, long long m,
+                              long long ld, double s, double s4, double mid) {
+  using namespace dev;
+  const long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  auto U = [&](int i) { return u[static_cast<long long>(i) * ld + j]; };
+  double* o = out + j;
+  if constexpr (!PENT) {
+    const double first = U(0);
+    double um = U(n - 1), ui = first;
+    for (int i = 0; i < n; ++i) {
+      const double up = i + 1 < n ? U(i + 1) : first;
+      o[static_cast<long long>(i) * ld] = add_rn(mul_rn(s, add_rn(um, up)), mul_rn(mid, ui));
+      um = ui;
+      ui = up;
+    }
+  } else {
+    const double u0 = U(0), u1 = U(1);
+    double a2 = U(n - 2), a1 = U(n - 1), c = u0, b1 = u1;  // u[i-2], u[i-1], u[i], u[i+1]
+    for (int i = 0; i < n; ++i) {
+      const double b2 = i + 2 < n ? U(i + 2) : (i + 2 == n ? u0 : u1);
+      const double t = add_rn(mul_rn(-s, add_rn(a2, b2)), mul_rn(s4, add_rn(a1, b1)));
+      o[static_cast<long long>(i) * ld] = add_rn(t, mul_rn(mid, c));
+      a2 = a1;
+      a1 = c;
+      c = b1;
+      b1 = b2;
+    }
+  }
+}
+
 uint64_t host_splitmix64(uint64_t z) {
   z += 0x9E3779B97F4A7C15ull;
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -1199,6 +1239,31 @@ bandsolve_status solve_host(const Factor& f, double* x, std::size_t n, std::size
   return BANDSOLVE_OK;
 }
 
+bandsolve_status cn_rhs_device(bool pent, double sigma_x, const double* u, double* out, std::size_t n,
+                               std::size_t m, std::size_t ld, void* stream) {
+  if (!u || !out) return fail(BANDSOLVE_ERR_BAD_ARG, "null device pointer");
+  if (u == out) return fail(BANDSOLVE_ERR_BAD_ARG, "the stencil needs distinct input and output arrays");
+  if (ld < m) return fail(BANDSOLVE_ERR_BAD_ARG, "row pitch ld < m");
+  if (n < (pent ? 6u : 3u)) return fail(BANDSOLVE_ERR_BAD_ARG, "periodic stencil needs n >= 3 (tri) / 6 (pent)");
+  if (n > static_cast<std::size_t>(INT_MAX)) return fail(BANDSOLVE_ERR_BAD_ARG, "n too large");
+  if (m == 0) return BANDSOLVE_OK;
+  if (device_count_cached() == 0) return fail(BANDSOLVE_ERR_INTERNAL, "no CUDA device available (no CPU fallback)");
+  auto s = static_cast<cudaStream_t>(stream);
+  const int threads = 128;
+  const unsigned grid = static_cast<unsigned>((m + threads - 1) / threads);
+  // pde.cpp:80-81 / :101-103: the coefficients are formed once on the host
+  if (pent)
+    cn_rhs_kernel<true><<<grid, threads, 0, s>>>(u, out, static_cast<int>(n), static_cast<long long>(m),
+                                                 static_cast<long long>(ld), sigma_x, 4.0 * sigma_x,
+                                                 1.0 - 6.0 * sigma_x);
+  else
+    cn_rhs_kernel<false><<<grid, threads, 0, s>>>(u, out, static_cast<int>(n), static_cast<long long>(m),
+                                                  static_cast<long long>(ld), sigma_x, 0.0, 1.0 - 2.0 * sigma_x);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  BSB_CUDA(cudaGetLastError());
+  return BANDSOLVE_OK;
+}
+
 bandsolve_status residual_device(Kind kind, const double* const* bands, std::size_t n, int cyclic,
                                  const double* x, const double* rhs, std::size_t m, std::size_t ld,
                                  void* stream, double* out) {
@@ -1266,6 +1331,164 @@ bandsolve_status residual_device(Kind kind, const double* const* bands, std::siz
   double w;
   std::memcpy(&w, &bits, sizeof w);
   *out = w;
+  return BANDSOLVE_OK;
+}
+
+// ---- Crank-Nicolson driver: bandsolve_bench_run (reference capi.cpp:369-411,
+// pde.cpp run_benchmark :258-371) with the stepping loop on the GPU.
+namespace {
+void put_u32_le(unsigned char* p, uint32_t v) {
+  for (int k = 0; k < 4; ++k) p[k] = static_cast<unsigned char>(v >> (8 * k));
+}
+void put_u64_le(unsigned char* p, uint64_t v) {
+  for (int k = 0; k < 8; ++k) p[k] = static_cast<unsigned char>(v >> (8 * k));
+}
+// batch.cpp:146-171 (write_ibat): "IBAT", u32 version 1, u64 n, u64 m, then
+// the n x m payload as little-endian binary64.
+bandsolve_status write_ibat(const std::string& path, const double* data, std::size_t n, std::size_t m) {
+  FILE* f = std::fopen(path.c_str(), "wb");
+  if (!f) return fail(BANDSOLVE_ERR_IO, "cannot open for writing: " + path);
+  unsigned char header[24];
+  std::memcpy(header, "IBAT", 4);
+  put_u32_le(header + 4, 1);
+  put_u64_le(header + 8, n);
+  put_u64_le(header + 16, m);
+  bool ok = std::fwrite(header, 1, sizeof header, f) == sizeof header;
+  std::vector<unsigned char> payload(n * m * 8);
+  for (std::size_t k = 0; k < n * m; ++k) {
+    uint64_t bits;
+    std::memcpy(&bits, data + k, 8);
+    put_u64_le(payload.data() + 8 * k, bits);
+  }
+  ok = ok && std::fwrite(payload.data(), 1, payload.size(), f) == payload.size();
+  ok = (std::fflush(f) == 0) && ok;
+  std::fclose(f);
+  return ok ? BANDSOLVE_OK : fail(BANDSOLVE_ERR_IO, "short write: " + path);
+}
+}  // namespace
+
+bandsolve_status bench_run_device(const bandsolve_bench_params& prm, bandsolve_bench_result* res,
+                                  int threads_report) {
+  // capi.cpp:374-401 and pde.cpp:258-277: the reference's checks, in order
+  const bool diffusion = prm.problem == BANDSOLVE_PROBLEM_DIFFUSION;
+  if (prm.problem != BANDSOLVE_PROBLEM_DIFFUSION && prm.problem != BANDSOLVE_PROBLEM_HYPERDIFFUSION)
+    return fail(BANDSOLVE_ERR_BAD_ARG, "unknown problem");
+  if (prm.variant != BANDSOLVE_VARIANT_SHARED && prm.variant != BANDSOLVE_VARIANT_PER_SYSTEM &&
+      prm.variant != BANDSOLVE_VARIANT_UNIFORM)
+    return fail(BANDSOLVE_ERR_BAD_ARG, "unknown variant");
+  const std::string prefix = prm.dump_prefix ? prm.dump_prefix : "";
+  if (prm.dump_every > 0 && prefix.empty()) return fail(BANDSOLVE_ERR_BAD_ARG, "dump_every needs dump_prefix");
+  const std::size_t n = prm.n, m = prm.m;
+  if (n < 2 || m < 1) return fail(BANDSOLVE_ERR_BAD_ARG, "field shape must be at least 2 x 1");
+  if (prm.steps < 1) return fail(BANDSOLVE_ERR_BAD_ARG, "steps must be >= 1");
+  if (diffusion) {
+    if (n < 3) return fail(BANDSOLVE_ERR_BAD_ARG, "diffusion benchmark needs n >= 3");
+    if (prm.variant == BANDSOLVE_VARIANT_UNIFORM)
+      return fail(BANDSOLVE_ERR_BAD_ARG, "uniform variant applies to hyperdiffusion only");
+  } else if (n < 6) {
+    return fail(BANDSOLVE_ERR_BAD_ARG, "hyperdiffusion benchmark needs n >= 6");
+  }
+  if (prm.variant == BANDSOLVE_VARIANT_PER_SYSTEM)
+    return fail(BANDSOLVE_ERR_BAD_ARG,
+                "per-system variant is not provided by the B200 library (shared-LHS path only)");
+  // pde.cpp:29-46: sigma_x = dt / (2 dx^p), default dt gives sigma_x = 1
+  const double dx = 1.0 / static_cast<double>(n);
+  const double pow_dx = diffusion ? dx * dx : dx * dx * dx * dx;
+  const double dt = prm.dt > 0.0 ? prm.dt : 1.0 * 2.0 * pow_dx;
+  const double sigma = dt / (2.0 * pow_dx);
+  if (!(sigma > 0.0)) return fail(BANDSOLVE_ERR_BAD_ARG, "sigma_x must be positive");
+  // preparation (outside the timed loop): periodic LHS of pde.cpp:59-71;
+  // the uniform variant is bitwise the shared one (pent_solver.cpp:83-97)
+  std::unique_ptr<Periodic> per;
+  bandsolve_status st = diffusion ? make_periodic_tri(-sigma, 1.0 + 2.0 * sigma, -sigma, n, per)
+                                  : make_periodic_pent(sigma, -4.0 * sigma, 1.0 + 6.0 * sigma, -4.0 * sigma,
+                                                       sigma, n, per);
+  if (st != BANDSOLVE_OK) return st;
+  if (device_count_cached() == 0) return fail(BANDSOLVE_ERR_INTERNAL, "no CUDA device available (no CPU fallback)");
+  // default_mode_initial, pde.cpp:48-58
+  std::vector<double> field(n * m);
+  const std::size_t mode_span = n / 4 > 0 ? n / 4 : 1;
+  for (std::size_t j = 0; j < m; ++j) {
+    const double k = static_cast<double>(1 + (j % mode_span));
+    for (std::size_t i = 0; i < n; ++i) {
+      const double xv = static_cast<double>(i + 1) / static_cast<double>(n);
+      field[i * m + j] = std::sin(2.0 * 3.141592653589793238462643383279502884 * k * xv);  // std::numbers::pi
+    }
+  }
+  const std::size_t ld = (m + 1) & ~std::size_t(1);  // even pitch keeps the TMA plans
+  const std::size_t bytes = n * ld * sizeof(double);
+  double *du = nullptr, *ds = nullptr;
+  cudaStream_t s = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  auto cleanup = [&]() {
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    if (du) cudaFree(du);
+    if (ds) cudaFree(ds);
+    if (s) cudaStreamDestroy(s);
+    cudaGetLastError();
+  };
+  auto step = [&](const double* from, double* to) {
+    bandsolve_status r = cn_rhs_device(!diffusion, sigma, from, to, n, m, ld, s);
+    if (r != BANDSOLVE_OK) return r;
+    return periodic_device(*per, to, n, m, ld, s, false);
+  };
+  cudaError_t err = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  if (err == cudaSuccess) err = cudaMalloc(&du, bytes);
+  if (err == cudaSuccess) err = cudaMalloc(&ds, bytes);
+  if (err == cudaSuccess) err = cudaEventCreate(&e0);
+  if (err == cudaSuccess) err = cudaEventCreate(&e1);
+  if (err == cudaSuccess)
+    err = cudaMemcpy2DAsync(du, ld * sizeof(double), field.data(), m * sizeof(double), m * sizeof(double), n,
+                            cudaMemcpyHostToDevice, s);
+  if (err != cudaSuccess) {
+    cleanup();
+    return cuda_fail(err, "bench setup");
+  }
+  // one untimed warm-up step into the scratch buffer; the field is untouched
+  st = step(du, ds);
+  std::vector<double> per_step;
+  per_step.reserve(static_cast<std::size_t>(prm.steps));
+  for (long k = 0; st == BANDSOLVE_OK && k < prm.steps; ++k) {
+    cudaEventRecord(e0, s);
+    st = step(du, ds);
+    cudaEventRecord(e1, s);
+    if (st != BANDSOLVE_OK) break;
+    err = cudaEventSynchronize(e1);
+    if (err != cudaSuccess) {
+      st = cuda_fail(err, "bench step");
+      break;
+    }
+    float ms = 0.0f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    per_step.push_back(static_cast<double>(ms) * 1e-3);
+    std::swap(du, ds);
+    if (prm.dump_every > 0 && (k + 1) % prm.dump_every == 0) {
+      err = cudaMemcpy2D(field.data(), m * sizeof(double), du, ld * sizeof(double), m * sizeof(double), n,
+                         cudaMemcpyDeviceToHost);
+      if (err != cudaSuccess) {
+        st = cuda_fail(err, "bench dump");
+        break;
+      }
+      st = write_ibat(prefix + "_step" + std::to_string(k + 1) + ".ibat", field.data(), n, m);
+    }
+  }
+  cleanup();
+  if (st != BANDSOLVE_OK) return st;
+  // pde.cpp:351-370 timing report; batch.cpp:72-111 storage footprint
+  double total = 0.0;
+  for (double t : per_step) total += t;
+  const double mean = total / static_cast<double>(per_step.size());
+  double var = 0.0;
+  for (double t : per_step) var += (t - mean) * (t - mean);
+  res->wall_s = total;
+  res->per_step_mean_s = mean;
+  res->per_step_std_s = per_step.size() > 1 ? std::sqrt(var / static_cast<double>(per_step.size() - 1)) : 0.0;
+  const uint64_t un = n, um = m;
+  res->elements = diffusion ? 3 * un + un * um
+                            : (prm.variant == BANDSOLVE_VARIANT_UNIFORM ? 4 * un + un * um : 5 * un + un * um);
+  res->threads = threads_report;
+  res->steps = prm.steps;
   return BANDSOLVE_OK;
 }
 
