@@ -331,22 +331,14 @@ BSB_API bandsolve_status bandsolve_periodic_tri_cn_step_dev(const bandsolve_peri
                                                             const double* u, double* out, size_t n, size_t m,
                                                             size_t ld, void* stream) {
   if (!lhs) return null_arg();
-  return guarded([&] {
-    bandsolve_status st = bsb::cn_rhs_device(false, sigma_x, u, out, n, m, ld, stream);
-    if (st != BANDSOLVE_OK) return st;
-    return bsb::periodic_device(*lhs->impl, out, n, m, ld, stream, false);
-  });
+  return guarded([&] { return bsb::cn_step_device(*lhs->impl, sigma_x, u, out, n, m, ld, stream); });
 }
 
 BSB_API bandsolve_status bandsolve_periodic_pent_cn_step_dev(const bandsolve_periodic_pent* lhs, double sigma_x,
                                                              const double* u, double* out, size_t n, size_t m,
                                                              size_t ld, void* stream) {
   if (!lhs) return null_arg();
-  return guarded([&] {
-    bandsolve_status st = bsb::cn_rhs_device(true, sigma_x, u, out, n, m, ld, stream);
-    if (st != BANDSOLVE_OK) return st;
-    return bsb::periodic_device(*lhs->impl, out, n, m, ld, stream, false);
-  });
+  return guarded([&] { return bsb::cn_step_device(*lhs->impl, sigma_x, u, out, n, m, ld, stream); });
 }
 
 // ---- residuals (capi.cpp:327-367) ----------------------------------------------

@@ -117,6 +117,10 @@ bandsolve_status solve_host(const Factor& f, double* x, std::size_t n,
 bandsolve_status cn_rhs_device(bool pent, double sigma_x, const double* u,
                                double* out, std::size_t n, std::size_t m,
                                std::size_t ld, void* stream);
+// One Crank-Nicolson step out = A^-1 (B u), stencil fused into the sweep.
+bandsolve_status cn_step_device(const Periodic& p, double sigma_x,
+                                const double* u, double* out, std::size_t n,
+                                std::size_t m, std::size_t ld, void* stream);
 // bandsolve_bench_run: the reference's Crank-Nicolson driver (capi.cpp:369,
 // pde.cpp run_benchmark) with the stepping loop on the GPU.
 bandsolve_status bench_run_device(const bandsolve_bench_params& prm,

@@ -628,10 +628,10 @@ cudaError_t launch_persist(const Plan& plan, T* x, int n, long long m, long long
 }
 
 
-template <typename T, int V, bool PENT, bool FAST, int PER = 0>
+template <typename T, int V, bool PENT, bool FAST, int PER = 0, bool CN = false>
 cudaError_t launch_stream_v(const Plan& plan, T* x, int n, long long m, long long ld, const void* fwd,
                             const void* bwd, cudaStream_t s, int sms, const dev::PerArgs& per = dev::PerArgs{}) {
-  auto kern = dev::sweep_stream<T, V, PENT, FAST, PER>;
+  auto kern = dev::sweep_stream<T, V, PENT, FAST, PER, CN>;
   static std::atomic<bool> configured{false};
   if (!configured.load(std::memory_order_relaxed)) {
     cudaError_t e = allow_big_smem(kern);
@@ -1131,6 +1131,82 @@ bandsolve_status launch_periodic_correct(const Periodic& p, double* x, std::size
 }
 }  // namespace
 
+// One Crank-Nicolson step out = A^-1 (B u) in one streaming pass: the
+// stencil is fused into the forward sweep (sweep_stream CN), and in fast
+// mode the periodic correction as well (PER); exact mode follows with the
+// bitwise correction kernel on `out`. Falls back to stencil kernel + solve
+// when no streaming plan fits.
+bandsolve_status cn_step_device(const Periodic& p, double sigma_x, const double* u, double* out, std::size_t n,
+                                std::size_t m, std::size_t ld, void* stream) {
+  if (!u || !out) return fail(BANDSOLVE_ERR_BAD_ARG, "null device pointer");
+  if (u == out) return fail(BANDSOLVE_ERR_BAD_ARG, "the stencil needs distinct input and output arrays");
+  if (n != p.n) return fail(BANDSOLVE_ERR_SHAPE_MISMATCH, "correction order != batch rows");
+  if (ld < m) return fail(BANDSOLVE_ERR_BAD_ARG, "row pitch ld < m");
+  if (m == 0) return BANDSOLVE_OK;
+  if (device_count_cached() == 0) return fail(BANDSOLVE_ERR_INTERNAL, "no CUDA device available (no CPU fallback)");
+  auto s = static_cast<cudaStream_t>(stream);
+  const bool pent = p.kind != Kind::Tri;
+  const bool fast = current_mode() == BANDSOLVE_MODE_FAST;
+  int device = 0;
+  BSB_CUDA(cudaGetDevice(&device));
+  const int sms = num_sms(device);
+  const bool aligned = (reinterpret_cast<uintptr_t>(u) % 16 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0) &&
+                       ((ld * sizeof(double)) % 16 == 0);
+  Plan plan;
+  if (std::getenv("BANDSOLVE_CN_UNFUSED") == nullptr && aligned && n <= static_cast<std::size_t>(INT_MAX) &&
+      m <= static_cast<std::size_t>(INT_MAX) / 2 &&
+      plan_stream(n, m, sizeof(double), pent, fast, sms, plan, fast ? (pent ? 4 : 2) : 0)) {
+    const DeviceFactor* df = nullptr;
+    bandsolve_status st = ensure_device_factor(*p.factor, device, &df);
+    if (st != BANDSOLVE_OK) return st;
+    const double* blob = nullptr;
+    st = periodic_device_z(p, device, &blob);
+    if (st != BANDSOLVE_OK) return st;
+    keep_pool_memory(device);
+    dev::PerArgs per;
+    per.arrays = blob + 2 * n;
+    if (pent) {
+      for (int k = 0; k < 4; ++k) per.pc[k] = p.cap_inv[k];
+    } else {
+      per.pc[0] = p.v_last;
+      per.pc[1] = p.scale;
+    }
+    per.out = out;
+    // pde.cpp:80-81 / :101-103
+    per.cn[0] = sigma_x;
+    per.cn[1] = pent ? 4.0 * sigma_x : 0.0;
+    per.cn[2] = pent ? 1.0 - 6.0 * sigma_x : 1.0 - 2.0 * sigma_x;
+    const int N = static_cast<int>(n);
+    const long long M = static_cast<long long>(m), LD = static_cast<long long>(ld);
+    double* x = const_cast<double*>(u);  // read only (tensor map source); results go to per.out
+    const int q = fast ? 1 : 0;
+    const void* fw = df->fwd[0][q];
+    const void* bw = df->bwd[0][q];
+    cudaError_t err;
+    if (fast) {
+      if (pent)
+        err = plan.V == 2 ? launch_stream_v<double, 2, true, true, 2, true>(plan, x, N, M, LD, fw, bw, s, sms, per)
+                          : launch_stream_v<double, 1, true, true, 2, true>(plan, x, N, M, LD, fw, bw, s, sms, per);
+      else
+        err = plan.V == 2 ? launch_stream_v<double, 2, false, true, 1, true>(plan, x, N, M, LD, fw, bw, s, sms, per)
+                          : launch_stream_v<double, 1, false, true, 1, true>(plan, x, N, M, LD, fw, bw, s, sms, per);
+    } else {
+      if (pent)
+        err = plan.V == 2 ? launch_stream_v<double, 2, true, false, 0, true>(plan, x, N, M, LD, fw, bw, s, sms, per)
+                          : launch_stream_v<double, 1, true, false, 0, true>(plan, x, N, M, LD, fw, bw, s, sms, per);
+      else
+        err = plan.V == 2 ? launch_stream_v<double, 2, false, false, 0, true>(plan, x, N, M, LD, fw, bw, s, sms, per)
+                          : launch_stream_v<double, 1, false, false, 0, true>(plan, x, N, M, LD, fw, bw, s, sms, per);
+    }
+    if (err != cudaSuccess) return cuda_fail(err, "fused Crank-Nicolson sweep launch");
+    if (fast) return BANDSOLVE_OK;
+    return launch_periodic_correct(p, out, n, m, ld, s);
+  }
+  bandsolve_status st = cn_rhs_device(pent, sigma_x, u, out, n, m, ld, stream);
+  if (st != BANDSOLVE_OK) return st;
+  return periodic_device(p, out, n, m, ld, stream, false);
+}
+
 bandsolve_status periodic_device(const Periodic& p, double* x, std::size_t n, std::size_t m, std::size_t ld,
                                  void* stream, bool correct_only) {
   if (!x) return fail(BANDSOLVE_ERR_BAD_ARG, "null device pointer");
@@ -1428,11 +1504,7 @@ bandsolve_status bench_run_device(const bandsolve_bench_params& prm, bandsolve_b
     if (s) cudaStreamDestroy(s);
     cudaGetLastError();
   };
-  auto step = [&](const double* from, double* to) {
-    bandsolve_status r = cn_rhs_device(!diffusion, sigma, from, to, n, m, ld, s);
-    if (r != BANDSOLVE_OK) return r;
-    return periodic_device(*per, to, n, m, ld, s, false);
-  };
+  auto step = [&](const double* from, double* to) { return cn_step_device(*per, sigma, from, to, n, m, ld, s); };
   cudaError_t err = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
   if (err == cudaSuccess) err = cudaMalloc(&du, bytes);
   if (err == cudaSuccess) err = cudaMalloc(&ds, bytes);

@@ -132,10 +132,19 @@ __device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, 
 // release(c) is called once chunk c is no longer read; sink(c, r, p, v)
 // consumes row r's result (p = its smem pair). f: the records of chunk 0's
 // first row (chunk c at +c*kSR).
-template <typename T, int V, bool PENT, bool FAST, typename Base, typename Ready, typename Release, typename Sink>
+struct NoXf {};  // no input transform: the sweep consumes the staged rows as they are
+
+// xf (optional): input transform xf(c, r, u, look) -> value fed to the
+// recurrence for row r of chunk c, where look(k) (k = 1, 2) yields the raw
+// row r+k of the stream (from the software pipeline, or extra(k') for the
+// k'-th row past the stream's end). Used by the fused Crank-Nicolson step.
+template <typename T, int V, bool PENT, bool FAST, typename Base, typename Ready, typename Release, typename Sink,
+          typename Xf = NoXf, typename Extra = NoXf>
 __device__ __forceinline__ void fwd_chunks(int C, const typename Recs<T, PENT>::Fwd* f, Vec<T, V>& s1, Vec<T, V>& s2,
-                                           Base&& base, Ready&& ready, Release&& release, Sink&& sink) {
+                                           Base&& base, Ready&& ready, Release&& release, Sink&& sink,
+                                           Xf&& xf = NoXf{}, Extra&& extra = NoXf{}) {
   using FwdR = typename Recs<T, PENT>::Fwd;
+  constexpr bool kXf = !std::is_same<std::decay_t<Xf>, NoXf>::value;
   if (C <= 0) return;
   Vec<T, V> dq[kSD];
   FwdR fq[kSD];
@@ -156,7 +165,15 @@ __device__ __forceinline__ void fwd_chunks(int C, const typename Recs<T, PENT>::
         ready(c + 1);
         pn = base(c + 1);
       }
-      const Vec<T, V> v = fwd_vec<T, V, PENT, FAST>(fq[r % kSD], dq[r % kSD], s1, s2);
+      Vec<T, V> in = dq[r % kSD];
+      if constexpr (kXf) {
+        auto look = [&](int k) -> Vec<T, V> {
+          if (r + k < kSR || more) return dq[(r + k) % kSD];
+          return extra(r + k - kSR);
+        };
+        in = xf(c, r, in, look);
+      }
+      const Vec<T, V> v = fwd_vec<T, V, PENT, FAST>(fq[r % kSD], in, s1, s2);
       const int rn = r + kSD;
       if (rn < kSR) {
         dq[r % kSD] = p[rn * kPR];
@@ -238,15 +255,20 @@ struct Cursor {
 struct PerArgs {
   const double* arrays = nullptr;
   double pc[4] = {0.0, 0.0, 0.0, 0.0};
+  // fused Crank-Nicolson (CN): x is the old field u (read through the tensor
+  // map), out receives u_new; stencil coefficients s, 4s, 1-2s / 1-6s
+  void* out = nullptr;
+  double cn[3] = {0.0, 0.0, 0.0};
 };
 
-template <typename T, int V, bool PENT, bool FAST, int PER = 0>
+template <typename T, int V, bool PENT, bool FAST, int PER = 0, bool CN = false>
 __global__ void __launch_bounds__(32 * (stream_max_warps(V) + 2), 1)
     sweep_stream(const __grid_constant__ CUtensorMap map_b, T* __restrict__ x, int n, long long m, long long ld,
                  int H, int TC, int KB, int KR, int PD, int stagger_ns, long long groups,
                  const void* __restrict__ fwd_g, const void* __restrict__ bwd_g, T* __restrict__ scratch,
                  const PerArgs per) {
   static_assert(PER == 0 || (FAST && sizeof(T) == 8 && (PER == 2) == PENT), "fused periodic: fast fp64 only");
+  static_assert(!CN || sizeof(T) == 8, "fused Crank-Nicolson: fp64 only");
   constexpr int kPerArrays = PER == 0 ? 0 : (PER == 1 ? 2 : 4);
   using FwdR = typename Recs<T, PENT>::Fwd;
   using BwdR = typename Recs<T, PENT>::Bwd;
@@ -421,6 +443,24 @@ __global__ void __launch_bounds__(32 * (stream_max_warps(V) + 2), 1)
   uint32_t it = 0;
 
   long long g = blockIdx.x;
+  // Fused Crank-Nicolson: the forward sweep consumes f_i = (B u)_i, formed
+  // from a register window of raw rows (u_{i-2}, u_{i-1} kept, u_{i+1},
+  // u_{i+2} from the software pipeline). The wrap rows u_{n-2}, u_{n-1} that
+  // row 0 needs are loaded from global one group ahead; u_0, u_1 (for the
+  // last rows) are kept when they stream past.
+  T* const xout = CN ? static_cast<T*>(per.out) : x;
+  const uint64_t pol_wrap = policy_evict_first();
+  auto load_wrap = [&](long long grp, P2& w1, P2& w2) {  // rows n-1, n-2 of this lane's columns
+    const long long jj = grp * Wg + warp * kLW + V * lane;
+#pragma unroll
+    for (int q = 0; q < V; ++q) {
+      const bool ok = grp < groups && jj + q < m;
+      w1.v[q] = ok ? ld_spill(x + static_cast<long long>(n - 1) * ld + jj + q, pol_wrap) : T(0);
+      w2.v[q] = ok ? ld_spill(x + static_cast<long long>(n - 2) * ld + jj + q, pol_wrap) : T(0);
+    }
+  };
+  P2 nw1{}, nw2{};  // next group's wrap rows
+  if constexpr (CN) load_wrap(g, nw1, nw2);
   // One group. kFull: every column of the group exists (all groups but
   // possibly the last), so the x stores are unconditional 16-byte stores.
   auto run_group = [&](auto full_tag) {
@@ -429,7 +469,7 @@ __global__ void __launch_bounds__(32 * (stream_max_warps(V) + 2), 1)
     const bool live2 = kFull || j + V - 1 < m;           // all V columns exist
     const bool live1 = kFull || j < m;                   // the first one does
     const uint32_t par = it & 1u;
-    T* out = x + (live1 ? j : 0) + static_cast<long long>(n - 1) * ld;
+    T* out = xout + (live1 ? j : 0) + static_cast<long long>(n - 1) * ld;
     auto put = [&](P2 v) {
       if (kFull) {
         st_stream_vec<T, V>(reinterpret_cast<P2*>(out), v);
@@ -440,6 +480,40 @@ __global__ void __launch_bounds__(32 * (stream_max_warps(V) + 2), 1)
       out -= ld;
     };
     P2 s1{}, s2{};
+    // CN window: w1 = u_{i-1}, w2 = u_{i-2}; u0s/u1s = u_0, u_1 for the wrap
+    P2 w1 = nw1, w2 = nw2, u0s{}, u1s{};
+    auto stencil = [&](int row, P2 u, auto&& look) -> P2 {
+      if constexpr (!CN) {
+        return u;
+      } else {
+        const T cs = T(per.cn[0]), cs4 = T(per.cn[1]), cmid = T(per.cn[2]);
+        const P2 d1 = look(1);
+        P2 f;
+        if constexpr (!PENT) {  // pde.cpp:85  o = s*(up + dn) + mid*mi
+#pragma unroll
+          for (int q = 0; q < V; ++q) f.v[q] = add_rn(mul_rn(cs, add_rn(w1.v[q], d1.v[q])), mul_rn(cmid, u.v[q]));
+        } else {  // pde.cpp:108  o = -s*(u2 + d2) + s4*(u1 + d1) + mid*mi
+          const P2 d2 = look(2);
+#pragma unroll
+          for (int q = 0; q < V; ++q)
+            f.v[q] = add_rn(add_rn(mul_rn(-cs, add_rn(w2.v[q], d2.v[q])), mul_rn(cs4, add_rn(w1.v[q], d1.v[q]))),
+                            mul_rn(cmid, u.v[q]));
+        }
+        if (row == 0) u0s = u;
+        if (row == 1) u1s = u;
+        w2 = w1;
+        w1 = u;
+        return f;
+      }
+    };
+    // raw row `row` >= H of the old field (tail smem, or the wrap past n)
+    auto tslot0 = [&](int k) { return tail_l + tail_slot(k, par) * cpairs; };
+    auto raw_tail = [&](int row) -> P2 {
+      if (row >= n) return row == n ? u0s : u1s;
+      const int k = (row - H) / kSR;
+      mbar_wait(&t_full[tail_slot(k, par)], par);
+      return tslot0(k)[((row - H) - k * kSR) * kPR];
+    };
     // fused periodic: y_0 (y_1) accumulated as dot products of the forward
     // outputs; correction coefficients w (tri) / t1, t2 (pent) per system
     P2 acc0{}, acc1{}, c1{}, c2{};
@@ -482,7 +556,9 @@ __global__ void __launch_bounds__(32 * (stream_max_warps(V) + 2), 1)
           [&](int c, int r, P2*, P2 v) {
             st_spill_vec<T, V>(spill_l + c * cpairs + r * kPR, v, pol_keep);
             accum(c * kSR + r, v);
-          });
+          },
+          [&](int c, int r, P2 u, auto&& look) { return stencil(c * kSR + r, u, look); },
+          [&](int k) { return raw_tail(H + k); });
     }
     if (HC > 0) {  // publish the spill to the async proxy (the reloader's bulk copies)
       fence_proxy_async_global();
@@ -497,16 +573,21 @@ __global__ void __launch_bounds__(32 * (stream_max_warps(V) + 2), 1)
         [&](int c, int r, P2* p, P2 v) {
           *p = v;
           accum(H + c * kSR + r, v);
-        });
+        },
+        [&](int c, int r, P2 u, auto&& look) { return stencil(H + c * kSR + r, u, look); },
+        [&](int k) { return raw_tail(H + tfull * kSR + k); });
     if (trem > 0) {
       mbar_wait(&t_full[tail_slot(tfull, par)], par);
       P2* p = tslot(tfull);
       const FwdR* f = sf + H + tfull * kSR;
       for (int r = 0; r < trem; ++r) {
-        p[r * kPR] = fwd_vec<T, V, PENT, FAST>(f[r], p[r * kPR], s1, s2);
-        accum(H + tfull * kSR + r, p[r * kPR]);
+        const int row = H + tfull * kSR + r;
+        const P2 in = stencil(row, p[r * kPR], [&](int k) { return raw_tail(row + k); });
+        p[r * kPR] = fwd_vec<T, V, PENT, FAST>(f[r], in, s1, s2);
+        accum(row, p[r * kPR]);
       }
     }
+    if constexpr (CN) load_wrap(g + gridDim.x, nw1, nw2);  // the next group's wrap rows, a group ahead
     fence_proxy_async_smem();  // in-place smem writes before the TMA refills of these slots
     if constexpr (PER == 1) {  // w = (y_0 + v_last y_{n-1}) * scale, y_{n-1} = d-hat_{n-1}
 #pragma unroll

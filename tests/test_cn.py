@@ -117,3 +117,53 @@ def test_gpu_cn_step_dev(lib, oracle, cuda_device):
     du = torch.zeros((8, 4), dtype=torch.float64, device="cuda")
     with pytest.raises(bs.BandsolveError):
         h.cn_step_dev(0.5, du.data_ptr(), du.data_ptr(), 8, 4)
+
+
+PLAN_ENV = ("BANDSOLVE_PLAN", "BANDSOLVE_SWG", "BANDSOLVE_STAIL", "BANDSOLVE_SKB", "BANDSOLVE_SV", "BANDSOLVE_SKR")
+
+
+def set_stream_plan(plan):
+    for k in PLAN_ENV:
+        os.environ.pop(k, None)
+    if plan:
+        os.environ["BANDSOLVE_PLAN"] = "stream"
+        for k, v in zip(PLAN_ENV[1:], plan):
+            os.environ[k] = v
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("plan", [None, ("64", "0"), ("64", "16", "4", "2"), ("96", "40", "3", "1"),
+                                  ("32", "100000"), ("128", "33", "2", "2", "0"), ("64", "0", "4", "1", "0")])
+def test_gpu_cn_fused_over_plans(lib, oracle, cuda_device, plan):
+    """The stencil window crosses ring chunks, the head/tail boundary, partial
+    tail chunks and the wrap rows: every split must give the reference's
+    bits (exact) / stay within 1e-12 (fast, fused correction)."""
+    torch = cuda_device
+    set_stream_plan(plan)
+    rng = np.random.default_rng(31)
+    try:
+        for prob, n, m in [(0, 3, 70), (0, 37, 130), (0, 512, 200), (1, 6, 65), (1, 50, 129), (1, 512, 300)]:
+            s = 0.61
+            u = rng.uniform(-1, 1, (n, m))
+            if prob == 0:
+                h = bs.PeriodicTri(lib, -s, 1 + 2 * s, -s, n)
+                want = oracle.periodic_tri_solve(oracle.periodic_tri_prepare(-s, 1 + 2 * s, -s, n),
+                                                 oracle.cn_rhs(0, s, u))
+            else:
+                h = bs.PeriodicPent(lib, s, -4 * s, 1 + 6 * s, -4 * s, s, n)
+                want = oracle.periodic_pent_solve(
+                    oracle.periodic_pent_prepare(s, -4 * s, 1 + 6 * s, -4 * s, s, n), oracle.cn_rhs(1, s, u))
+            for mode in (bs.MODE_EXACT, bs.MODE_FAST):
+                lib.set_mode(mode)
+                du = torch.from_numpy(u).cuda()
+                do = torch.zeros_like(du)
+                h.cn_step_dev(s, du.data_ptr(), do.data_ptr(), n, m, stream=torch.cuda.current_stream().cuda_stream)
+                torch.cuda.synchronize()
+                got = do.cpu().numpy()
+                if mode == bs.MODE_EXACT:
+                    assert bitwise_equal(got, want), (plan, prob, n, m)
+                else:
+                    assert per_system_max_rel(got, want) <= 1e-12, (plan, prob, n, m)
+    finally:
+        lib.set_mode(bs.MODE_EXACT)
+        set_stream_plan(None)
