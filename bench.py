@@ -42,6 +42,10 @@ CONFIGS = {
     "tri512": ("tri", 512, 1 << 20, "north-star target: tridiagonal N=512, batch=2^20, diffusion LHS sigma_x=1"),
     "pent512": ("pent", 512, 1 << 20, "north-star target: pentadiagonal N=512, batch=2^20, hyperdiffusion sigma_x=1"),
     "c5": ("pent", 1024, 1 << 21, "configs[4] shard: pentadiagonal N=1024, 2^21 systems per GPU (2^24 at 8 GPUs)"),
+    "c4tri": ("tri", 4096, 4096, "configs[3]: 2D ADI step (Peaceman-Rachford, periodic diffusion) on a 4096x4096 "
+                                 "grid, tridiagonal solves along both axes"),
+    "c4pent": ("pent", 4096, 4096, "configs[3]: 2D ADI step (periodic hyperdiffusion) on a 4096x4096 grid, "
+                                   "pentadiagonal solves along both axes"),
 }
 SEED = 42
 
@@ -245,8 +249,11 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
     elem = 4 if args.f32 else 8
     dt = torch.float32 if args.f32 else torch.float64
     bands = lhs_for(kind, n)
+    adi = args.config.startswith("c4")
     args.periodic = args.periodic or args.cn
-    if args.periodic:  # cyclic constant-band system: shared sweep of A' + wrap correction
+    if adi:  # field C[y][x] = n x m; one step = an x-sweep and a y-sweep
+        fac = bs.ADI(lib, 0 if kind == "tri" else 1, 1.0, m, n)
+    elif args.periodic:  # cyclic constant-band system: shared sweep of A' + wrap correction
         consts = (-1.0, 3.0, -1.0) if kind == "tri" else (1.0, -4.0, 7.0, -4.0, 1.0)
         fac = bs.PeriodicTri(lib, *consts, n) if kind == "tri" else bs.PeriodicPent(lib, *consts, n)
         if args.f32:
@@ -269,7 +276,9 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
     cn_sigma = 1.0  # pde.cpp default dt: sigma_x = 1
 
     def step(k):
-        if args.cn:  # one Crank-Nicolson step: u_{k+1} = A^-1 B u_k, ping-pong buffers
+        if adi:
+            fac.step_dev(bufs[k % nbuf].data_ptr(), bufs[(k + 1) % nbuf].data_ptr(), ld=m, stream=sptr)
+        elif args.cn:  # one Crank-Nicolson step: u_{k+1} = A^-1 B u_k, ping-pong buffers
             fac.cn_step_dev(cn_sigma, bufs[k % nbuf].data_ptr(), bufs[(k + 1) % nbuf].data_ptr(), n, m, ld=m,
                             stream=sptr)
         else:
@@ -297,13 +306,14 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
-    rows_total = float(n) * m * world * args.steps
+    axes = 2 if adi else 1  # an ADI step solves every grid point along both axes
+    rows_total = float(n) * m * world * args.steps * axes
     value = rows_total / (ms_max / 1e3)
     ms_per_step = ms_max / args.steps
 
     # roofline of the sweep kernel: algorithmic bytes (read b once, write x
     # once) per launch / average launch duration on the launching stream
-    algo_bytes = 2.0 * elem * n * m
+    algo_bytes = 2.0 * elem * n * m * axes  # 16 B per point per axis solve
     achieved = algo_bytes / (ms_local / args.steps / 1e3) / 1e9
     peak, peak_src = load_peak()
     traffic = load_traffic(args.config, args.mode)
@@ -312,7 +322,7 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
     # e2e through the reference-facing host API (pinned host batch; H2D,
     # sweep, D2H inside bandsolve_*_solve_shared, synchronous)
     e2e = None
-    if not args.f32 and not args.cn:
+    if not args.f32 and not args.cn and not adi:
         host = bs.Batch.from_array(lib, bufs[0].cpu().numpy())
         e2e_steps = max(1, min(args.steps, 50))
         for _ in range(min(args.warmup, 3)):

@@ -298,6 +298,22 @@ bandsolve_status bandsolve_periodic_pent_cn_step_dev(
     const bandsolve_periodic_pent* lhs, double sigma_x, const double* u,
     double* out, size_t n, size_t m, size_t ld, void* stream);
 
+/* Two-dimensional ADI (BASELINE configs[3]; no reference counterpart). One
+ * Peaceman-Rachford step of the periodic diffusion / hyperdiffusion problem
+ * on an ny x nx field C[y*ld + x] (device, fp64):
+ *   (I - s Lx) u* = (I + s Ly) u,   (I - s Ly) u' = (I + s Lx) u*
+ * with the Crank-Nicolson bands and stencils of the 1D driver along each
+ * axis. y-solves run on the interleaved layout directly (systems = x), x-solves
+ * on a transposed copy (systems = y). work: an ny x ld scratch array; the
+ * call is stream-ordered. */
+typedef struct bandsolve_adi bandsolve_adi;
+bandsolve_status bandsolve_adi_create(int problem, double sigma_x, size_t nx,
+                                      size_t ny, bandsolve_adi** out);
+void bandsolve_adi_destroy(bandsolve_adi* adi);
+bandsolve_status bandsolve_adi_step_dev(const bandsolve_adi* adi,
+                                        double* field, double* work,
+                                        size_t ld, void* stream);
+
 /* Device residual of a device-resident solution against a device-resident
  * right-hand side (both n x m, pitch ld), bands on the host. Synchronous:
  * writes the max relative residual to *out. */

@@ -206,6 +206,24 @@ class Oracle:
             out.append(u.copy())
         return out
 
+    def adi_step(self, problem: int, s: float, field: np.ndarray) -> np.ndarray:
+        """One periodic Peaceman-Rachford step on an (ny, nx) field: explicit
+        along y + implicit along x, then explicit along x + implicit along y,
+        each half with the 1D Crank-Nicolson bands / stencil (pde.cpp)."""
+        ny, nx = field.shape
+        if problem == 0:
+            fx = self.periodic_tri_prepare(-s, 1 + 2 * s, -s, nx)
+            fy = self.periodic_tri_prepare(-s, 1 + 2 * s, -s, ny)
+            solve = self.periodic_tri_solve
+        else:
+            fx = self.periodic_pent_prepare(s, -4 * s, 1 + 6 * s, -4 * s, s, nx)
+            fy = self.periodic_pent_prepare(s, -4 * s, 1 + 6 * s, -4 * s, s, ny)
+            solve = self.periodic_pent_solve
+        t1 = np.ascontiguousarray(self.cn_rhs(problem, s, field).T)     # rows = x
+        t1 = solve(fx, t1)
+        t2 = np.ascontiguousarray(self.cn_rhs(problem, s, t1).T)        # rows = y
+        return solve(fy, t2)
+
     # -- checks ---------------------------------------------------------------
     def tri_residual(self, sub, diag, sup, x, rhs, cyclic=False) -> float:
         n = len(diag)

@@ -125,6 +125,9 @@ _EXTENSION_SIGS = [
     ("bandsolve_periodic_pent_correct_dev", _st, [_vp, _vp, _sz, _sz, _sz, _vp]),
     ("bandsolve_periodic_tri_cn_step_dev", _st, [_vp, C.c_double, _vp, _vp, _sz, _sz, _sz, _vp]),
     ("bandsolve_periodic_pent_cn_step_dev", _st, [_vp, C.c_double, _vp, _vp, _sz, _sz, _sz, _vp]),
+    ("bandsolve_adi_create", _st, [C.c_int, C.c_double, _sz, _sz, C.POINTER(_vp)]),
+    ("bandsolve_adi_destroy", None, [_vp]),
+    ("bandsolve_adi_step_dev", _st, [_vp, _vp, _vp, _sz, _vp]),
     ("bandsolve_describe_plan", _st, [C.c_int, _sz, _sz, _sz, C.c_int, C.c_char_p, _sz]),
     ("bandsolve_kernel_launches", C.c_uint64, []),
     ("bandsolve_last_error", C.c_char_p, []),
@@ -478,6 +481,31 @@ class PeriodicPent(_Periodic):
         self.lib.check(self.lib.lib.bandsolve_periodic_pent_modified_bands(self.handle, *[_dptr(v) for v in out]),
                        "periodic_pent_modified_bands")
         return out
+
+
+class ADI:
+    """bandsolve_adi (B200 extension): periodic 2D Peaceman-Rachford ADI step."""
+
+    def __init__(self, lib: Library, problem: int, sigma_x: float, nx: int, ny: int):
+        self.lib, self.nx, self.ny = lib, nx, ny
+        h = _vp()
+        lib.check(lib.lib.bandsolve_adi_create(problem, sigma_x, nx, ny, C.byref(h)), "adi_create")
+        self.handle = h
+
+    def step_dev(self, field_ptr: int, work_ptr: int, ld: Optional[int] = None, stream: int = 0) -> None:
+        self.lib.check(self.lib.lib.bandsolve_adi_step_dev(self.handle, field_ptr, work_ptr,
+                                                           self.nx if ld is None else ld, stream), "adi_step_dev")
+
+    def close(self) -> None:
+        if self.handle:
+            self.lib.lib.bandsolve_adi_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def diffusion_bands(sigma: float, n: int):

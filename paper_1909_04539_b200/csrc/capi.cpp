@@ -38,6 +38,12 @@ struct bandsolve_periodic_tri {
 struct bandsolve_periodic_pent {
   std::unique_ptr<bsb::Periodic> impl;
 };
+struct bandsolve_adi {
+  int problem = 0;
+  double sigma = 0.0;
+  std::size_t nx = 0, ny = 0;
+  std::unique_ptr<bsb::Periodic> px, py;
+};
 
 namespace bsb {
 
@@ -339,6 +345,44 @@ BSB_API bandsolve_status bandsolve_periodic_pent_cn_step_dev(const bandsolve_per
                                                              size_t ld, void* stream) {
   if (!lhs) return null_arg();
   return guarded([&] { return bsb::cn_step_device(*lhs->impl, sigma_x, u, out, n, m, ld, stream); });
+}
+
+// ---- 2D ADI (B200 extension; BASELINE configs[3]) -----------------------------
+BSB_API bandsolve_status bandsolve_adi_create(int problem, double sigma_x, size_t nx, size_t ny, bandsolve_adi** out) {
+  if (!out) return null_arg();
+  *out = nullptr;
+  if (problem != BANDSOLVE_PROBLEM_DIFFUSION && problem != BANDSOLVE_PROBLEM_HYPERDIFFUSION)
+    return bsb::fail(BANDSOLVE_ERR_BAD_ARG, "unknown problem");
+  if (!(sigma_x > 0.0)) return bsb::fail(BANDSOLVE_ERR_BAD_ARG, "sigma_x must be positive");
+  return guarded([&] {
+    auto h = std::make_unique<bandsolve_adi>();
+    h->problem = problem;
+    h->sigma = sigma_x;
+    h->nx = nx;
+    h->ny = ny;
+    const double s = sigma_x;
+    for (int axis = 0; axis < 2; ++axis) {
+      const std::size_t n = axis == 0 ? nx : ny;
+      std::unique_ptr<bsb::Periodic>& p = axis == 0 ? h->px : h->py;
+      // pde.cpp:59-71: diffusion (-s, 1+2s, -s), hyperdiffusion (s, -4s, 1+6s, -4s, s)
+      bandsolve_status st = problem == BANDSOLVE_PROBLEM_DIFFUSION
+                                ? bsb::make_periodic_tri(-s, 1.0 + 2.0 * s, -s, n, p)
+                                : bsb::make_periodic_pent(s, -4.0 * s, 1.0 + 6.0 * s, -4.0 * s, s, n, p);
+      if (st != BANDSOLVE_OK) return st;
+    }
+    *out = h.release();
+    return BANDSOLVE_OK;
+  });
+}
+
+BSB_API void bandsolve_adi_destroy(bandsolve_adi* adi) { delete adi; }
+
+BSB_API bandsolve_status bandsolve_adi_step_dev(const bandsolve_adi* adi, double* field, double* work, size_t ld,
+                                                void* stream) {
+  if (!adi) return null_arg();
+  return guarded([&] {
+    return bsb::adi_step_device(*adi->px, *adi->py, adi->sigma, field, work, adi->nx, adi->ny, ld, stream);
+  });
 }
 
 // ---- residuals (capi.cpp:327-367) ----------------------------------------------

@@ -117,6 +117,11 @@ bandsolve_status solve_host(const Factor& f, double* x, std::size_t n,
 bandsolve_status cn_rhs_device(bool pent, double sigma_x, const double* u,
                                double* out, std::size_t n, std::size_t m,
                                std::size_t ld, void* stream);
+// One Peaceman-Rachford ADI step of a periodic ny x nx field (pitch ld).
+bandsolve_status adi_step_device(const Periodic& px, const Periodic& py,
+                                 double sigma, double* field, double* work,
+                                 std::size_t nx, std::size_t ny,
+                                 std::size_t ld, void* stream);
 // One Crank-Nicolson step out = A^-1 (B u), stencil fused into the sweep.
 bandsolve_status cn_step_device(const Periodic& p, double sigma_x,
                                 const double* u, double* out, std::size_t n,

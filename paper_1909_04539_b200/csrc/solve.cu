@@ -717,8 +717,10 @@ cudaError_t launch_regs_nb(const Plan& plan, T* x, int n, long long m, long long
 
 template <typename T, bool PENT, bool FAST>
 cudaError_t launch_global(T* x, int n, long long m, long long ld, const void* fwd, const void* bwd,
-                          cudaStream_t s) {
-  const int threads = 128;
+                          cudaStream_t s, int sms = 148) {
+  // thread per system: spread few systems over every SM (latency-bound regime)
+  int threads = 128;
+  while (threads > 32 && (m + threads - 1) / threads < sms) threads >>= 1;
   const long long grid = (m + threads - 1) / threads;
   dev::sweep_global<T, PENT, FAST><<<static_cast<unsigned>(grid), threads, 0, s>>>(x, n, m, ld, fwd, bwd);
   g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -739,7 +741,7 @@ cudaError_t dispatch(const Plan& plan, T* x, int n, long long m, long long ld, c
       default: return cudaErrorInvalidValue;
     }
   }
-  return launch_global<T, PENT, FAST>(x, n, m, ld, fwd, bwd, s);
+  return launch_global<T, PENT, FAST>(x, n, m, ld, fwd, bwd, s, sms);
 }
 
 template <typename T>
@@ -926,6 +928,24 @@ __global__ void cn_rhs_kernel(const double* __restrict__ u, double* __restrict__
       c = b1;
       b1 = b2;
     }
+  }
+}
+
+// ---- tiled transpose for the ADI x-sweeps -------------------------------------
+// out[c * ldo + r] = in[r * ldi + c], 32 x 32 tiles through padded smem so
+// both the reads and the writes are coalesced.
+__global__ void transpose_kernel(const double* __restrict__ in, double* __restrict__ out, int rows, int cols,
+                                 long long ldi, long long ldo) {
+  __shared__ double tile[32][33];
+  const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int r = r0 + k, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) tile[k][threadIdx.x] = in[static_cast<long long>(r) * ldi + c];
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int c = c0 + k, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) out[static_cast<long long>(c) * ldo + r] = tile[threadIdx.x][k];
   }
 }
 
@@ -1408,6 +1428,55 @@ bandsolve_status residual_device(Kind kind, const double* const* bands, std::siz
   std::memcpy(&w, &bits, sizeof w);
   *out = w;
   return BANDSOLVE_OK;
+}
+
+// ---- 2D ADI step (configs[3]) -------------------------
+// Peaceman-Rachford on a periodic ny x nx field C[y*ld + x]:
+//   (I - s Lx) u* = (I + s Ly) u,   (I - s Ly) u' = (I + s Lx) u*
+// with L the periodic second-difference (diffusion) or minus the fourth
+// difference (hyperdiffusion) and the CN bands of pde.cpp:59-71. y-sweeps
+// run on the field's own interleaved layout (rows = y, systems = x); the
+// x-sweeps on its transpose (rows = x, systems = y).
+bandsolve_status adi_step_device(const Periodic& px, const Periodic& py, double sigma, double* field, double* work,
+                                 std::size_t nx, std::size_t ny, std::size_t ld, void* stream) {
+  if (!field || !work) return fail(BANDSOLVE_ERR_BAD_ARG, "null device pointer");
+  if (field == work) return fail(BANDSOLVE_ERR_BAD_ARG, "field and work must not alias");
+  if (px.n != nx || py.n != ny) return fail(BANDSOLVE_ERR_SHAPE_MISMATCH, "ADI handle order != field shape");
+  if (ld < nx) return fail(BANDSOLVE_ERR_BAD_ARG, "row pitch ld < nx");
+  if (device_count_cached() == 0) return fail(BANDSOLVE_ERR_INTERNAL, "no CUDA device available (no CPU fallback)");
+  auto s = static_cast<cudaStream_t>(stream);
+  const bool pent = px.kind != Kind::Tri;
+  const std::size_t ldt = (ny + 1) & ~std::size_t(1);  // transposed pitch (even: TMA plans)
+  double *t1 = nullptr, *t2 = nullptr;
+  BSB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&t1), nx * ldt * sizeof(double), s));
+  cudaError_t err = cudaMallocAsync(reinterpret_cast<void**>(&t2), nx * ldt * sizeof(double), s);
+  if (err != cudaSuccess) {
+    cudaFreeAsync(t1, s);
+    return cuda_fail(err, "ADI scratch");
+  }
+  auto transpose = [&](const double* in, double* out, std::size_t rows, std::size_t cols, std::size_t ldi,
+                       std::size_t ldo) {
+    dim3 block(32, 8), grid(static_cast<unsigned>((cols + 31) / 32), static_cast<unsigned>((rows + 31) / 32));
+    transpose_kernel<<<grid, block, 0, s>>>(in, out, static_cast<int>(rows), static_cast<int>(cols),
+                                            static_cast<long long>(ldi), static_cast<long long>(ldo));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return cudaGetLastError();
+  };
+  bandsolve_status st = BANDSOLVE_OK;
+  do {
+    // half step 1: explicit along y, implicit along x
+    if ((st = cn_rhs_device(pent, sigma, field, work, ny, nx, ld, stream)) != BANDSOLVE_OK) break;
+    if ((err = transpose(work, t1, ny, nx, ld, ldt)) != cudaSuccess) { st = cuda_fail(err, "ADI transpose"); break; }
+    if ((st = periodic_device(px, t1, nx, ny, ldt, stream, false)) != BANDSOLVE_OK) break;
+    // half step 2: explicit along x, implicit along y
+    if ((st = cn_rhs_device(pent, sigma, t1, t2, nx, ny, ldt, stream)) != BANDSOLVE_OK) break;
+    if ((err = transpose(t2, field, nx, ny, ldt, ld)) != cudaSuccess) { st = cuda_fail(err, "ADI transpose"); break; }
+    st = periodic_device(py, field, ny, nx, ld, stream, false);
+  } while (false);
+  cudaFreeAsync(t1, s);
+  cudaFreeAsync(t2, s);
+  cudaGetLastError();
+  return st;
 }
 
 // ---- Crank-Nicolson driver: bandsolve_bench_run (reference capi.cpp:369-411,
