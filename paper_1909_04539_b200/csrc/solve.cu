@@ -196,6 +196,7 @@ struct Plan {
   int Wg = 0, KB = 0, KR = 0, PD = 0;  // stream: systems per group, b / reload ring slots, L2 prefetch distance
   int stagger_ns = 0;                  // stream: start delay of odd CTAs
   int V = 1;                           // stream: systems per lane
+  int tmem_chunks = 0;                 // stream: head chunks kept in Tensor Memory
   double model_us = 0;       // stream: modelled time
   std::size_t smem_bytes = 0;
   std::string why;
@@ -375,7 +376,7 @@ int env_int(const char* name, int dflt) {
 //   frac = compute(S) x spill_factor(spill) x (round utilisation),
 // preferring the smaller spill on ties.
 bool plan_stream(std::size_t n, std::size_t m, std::size_t elem, bool pent, bool fast, int sms, Plan& p,
-                 int per_arrays = 0) {
+                 int per_arrays = 0, bool allow_tmem = true) {
   const std::size_t fr = fwd_rec_bytes(pent, elem), br = bwd_rec_bytes(pent, elem);
   const std::size_t fac = dev::align128(n * fr) + dev::align128(n * br);
   if (fac > kSmemPerBlockMax / 2 || n < 2) return false;
@@ -426,7 +427,11 @@ bool plan_stream(std::size_t n, std::size_t m, std::size_t elem, bool pent, bool
     }
     if (H < 0) continue;
     const int TC = (N - H + dev::kSR - 1) / dev::kSR;
-    const double spill = static_cast<double>(grid) * Wg * H * elem;
+    // TMEM tier (V = 1, one warp per TMEM lane quadrant): up to 2 KB per system
+    int rtc = 0;
+    if (allow_tmem && V == 1 && P <= 4 && env_int("BANDSOLVE_TMEM", 1) != 0)
+      rtc = std::min(H / dev::kSR, static_cast<int>(2048 / (dev::kSR * elem)));
+    const double spill = static_cast<double>(grid) * Wg * (H - rtc * dev::kSR) * elem;
     const double rounds = static_cast<double>(m) / (static_cast<double>(Wg) * sms);
     const double util = rounds / std::ceil(rounds);
     const double frac = stream_compute_frac(Wg, pent, fast) * (V == 2 ? 0.95 : 1.0) *
@@ -448,6 +453,7 @@ bool plan_stream(std::size_t n, std::size_t m, std::size_t elem, bool pent, bool
       p.model_us = t * 1e6;
       p.smem_bytes = dev::StreamLayout::make(N, H, TC, Wg, KB, KR, elem, fr, br, per_arrays).total;
       p.V = V;
+      p.tmem_chunks = rtc;
     }
   }
   return found;
@@ -628,10 +634,12 @@ cudaError_t launch_persist(const Plan& plan, T* x, int n, long long m, long long
 }
 
 
-template <typename T, int V, bool PENT, bool FAST, int PER = 0, bool CN = false>
+template <typename T, int V, bool PENT, bool FAST, int PER = 0, bool CN = false, bool TM = false>
 cudaError_t launch_stream_v(const Plan& plan, T* x, int n, long long m, long long ld, const void* fwd,
-                            const void* bwd, cudaStream_t s, int sms, const dev::PerArgs& per = dev::PerArgs{}) {
-  auto kern = dev::sweep_stream<T, V, PENT, FAST, PER, CN>;
+                            const void* bwd, cudaStream_t s, int sms, const dev::PerArgs& per_in = dev::PerArgs{}) {
+  auto kern = dev::sweep_stream<T, V, PENT, FAST, PER, CN, TM>;
+  dev::PerArgs per = per_in;
+  per.tmem_chunks = TM ? plan.tmem_chunks : 0;
   static std::atomic<bool> configured{false};
   if (!configured.load(std::memory_order_relaxed)) {
     cudaError_t e = allow_big_smem(kern);
@@ -644,8 +652,9 @@ cudaError_t launch_stream_v(const Plan& plan, T* x, int n, long long m, long lon
   const long long grid = std::min<long long>(sms, groups);
   const int P = plan.Wg / (32 * V);
   T* scratch = nullptr;
-  if (plan.H > 0) {
-    const std::size_t bytes = static_cast<std::size_t>(grid) * plan.Wg * plan.H * sizeof(T);
+  const int spilled_rows = plan.H - per.tmem_chunks * dev::kSR;
+  if (spilled_rows > 0) {
+    const std::size_t bytes = static_cast<std::size_t>(grid) * plan.Wg * spilled_rows * sizeof(T);
     int device = 0;
     if (cudaGetDevice(&device) == cudaSuccess) ensure_l2_setaside(device, bytes);
     cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch), bytes, s);
@@ -666,6 +675,8 @@ cudaError_t launch_stream_v(const Plan& plan, T* x, int n, long long m, long lon
 template <typename T, bool PENT, bool FAST>
 cudaError_t launch_stream(const Plan& plan, T* x, int n, long long m, long long ld, const void* fwd,
                           const void* bwd, cudaStream_t s, int sms) {
+  if (plan.V == 1 && plan.tmem_chunks > 0)
+    return launch_stream_v<T, 1, PENT, FAST, 0, false, true>(plan, x, n, m, ld, fwd, bwd, s, sms);
   if (plan.V == 2) return launch_stream_v<T, 2, PENT, FAST>(plan, x, n, m, ld, fwd, bwd, s, sms);
   return launch_stream_v<T, 1, PENT, FAST>(plan, x, n, m, ld, fwd, bwd, s, sms);
 }
@@ -1045,8 +1056,9 @@ bandsolve_status describe_plan(Kind kind, std::size_t n, std::size_t m, std::siz
     std::snprintf(buf, sizeof buf, "regs Wg=%d warps=%d+1 nb=%d head(L2)=%d tail(smem)=%d smem=%zu B spill=%.1f MB",
                   p.Wg, p.warps, p.KB, p.H, static_cast<int>(n) - p.H, p.smem_bytes, p.model_us);
   else if (p.kind == PlanKind::Stream)
-    std::snprintf(buf, sizeof buf, "stream Wg=%d V=%d warps=%d+2 head(L2)=%d tail(smem)=%d rings=%d/%d pd=%d smem=%zu B model=%.1f us",
-                  p.Wg, p.V, p.warps, p.H, static_cast<int>(n) - p.H, p.KB, p.KR, p.PD, p.smem_bytes, p.model_us);
+    std::snprintf(buf, sizeof buf, "stream Wg=%d V=%d warps=%d+2 tmem=%d head(L2)=%d tail(smem)=%d rings=%d/%d pd=%d smem=%zu B model=%.1f us",
+                  p.Wg, p.V, p.warps, p.tmem_chunks * dev::kSR, p.H - p.tmem_chunks * dev::kSR, static_cast<int>(n) - p.H,
+                  p.KB, p.KR, p.PD, p.smem_bytes, p.model_us);
   else if (p.kind == PlanKind::Persist)
     std::snprintf(buf, sizeof buf, "persist warps=%d systems/sm=%d head(L2)=%d tail(smem)=%d smem=%zu B", p.warps,
                   p.warps * dev::kPW, p.H, static_cast<int>(n) - p.H, p.smem_bytes);
@@ -1175,7 +1187,7 @@ bandsolve_status cn_step_device(const Periodic& p, double sigma_x, const double*
   Plan plan;
   if (std::getenv("BANDSOLVE_CN_UNFUSED") == nullptr && aligned && n <= static_cast<std::size_t>(INT_MAX) &&
       m <= static_cast<std::size_t>(INT_MAX) / 2 &&
-      plan_stream(n, m, sizeof(double), pent, fast, sms, plan, fast ? (pent ? 4 : 2) : 0)) {
+      plan_stream(n, m, sizeof(double), pent, fast, sms, plan, fast ? (pent ? 4 : 2) : 0, false)) {
     const DeviceFactor* df = nullptr;
     bandsolve_status st = ensure_device_factor(*p.factor, device, &df);
     if (st != BANDSOLVE_OK) return st;
@@ -1244,7 +1256,7 @@ bandsolve_status periodic_device(const Periodic& p, double* x, std::size_t n, st
     const bool aligned = (reinterpret_cast<uintptr_t>(x) % 16 == 0) && ((ld * sizeof(double)) % 16 == 0);
     Plan plan;
     if (aligned && n <= static_cast<std::size_t>(INT_MAX) && m <= static_cast<std::size_t>(INT_MAX) / 2 &&
-        plan_stream(n, m, sizeof(double), pent, true, sms, plan, pent ? 4 : 2)) {
+        plan_stream(n, m, sizeof(double), pent, true, sms, plan, pent ? 4 : 2, false)) {
       const DeviceFactor* df = nullptr;
       bandsolve_status st = ensure_device_factor(*p.factor, device, &df);
       if (st != BANDSOLVE_OK) return st;

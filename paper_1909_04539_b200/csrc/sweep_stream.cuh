@@ -111,7 +111,8 @@ struct StreamLayout {
     L.rring_off = L.bring_off + (H > 0 ? static_cast<size_t>(KB) * chunk : 0);
     L.tail_off = L.rring_off + (H > 0 ? static_cast<size_t>(KR) * chunk : 0);
     L.bar_off = L.tail_off + static_cast<size_t>(TC) * chunk;
-    L.total = L.bar_off + static_cast<size_t>(2 * KB + 2 * KR + 2 * TC + 1) * sizeof(uint64_t);
+    // barriers, then one word for the TMEM base address
+    L.total = L.bar_off + static_cast<size_t>(2 * KB + 2 * KR + 2 * TC + 2) * sizeof(uint64_t);
     return L;
   }
 };
@@ -125,6 +126,72 @@ __device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, 
                "r"(c0), "r"(c1)
                : "memory");
 }
+
+
+// ---- Tensor Memory as a per-lane store for forward intermediates -----------------
+// TMEM is 128 lanes x 512 columns x 32 bit per SM; with the .32x32b shape
+// thread t of warp w (w < 4) reads/writes its own lane 32w + t, so each
+// system owns up to 2 KB (256 fp64 rows) next to its registers: a third
+// on-chip tier between shared memory and the L2 spill.
+__device__ __forceinline__ void tmem_alloc_512(uint32_t* dst) {  // whole warp
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(dst)) : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc_512(uint32_t taddr) {  // the allocating warp
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(taddr) : "memory");
+}
+__device__ __forceinline__ void tmem_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+// 32 (fp64: 16 rows) / 16 (fp32: 16 rows) consecutive columns of this lane
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]) : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16};" ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]) : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];" : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]) : "r"(taddr) : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];" : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]) : "r"(taddr) : "memory");
+}
+// wait for this thread's TMEM loads; the registers are in/out operands so no
+// consumer can be scheduled above the wait
+__device__ __forceinline__ void tmem_wait_ld(uint32_t (&r)[32]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]), "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]), "+r"(r[29]), "+r"(r[30]), "+r"(r[31]) :: "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld(uint32_t (&r)[16]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15]) :: "memory");
+}
+// a 16-row chunk of one lane's values <-> raw 32-bit TMEM words
+template <typename T>
+struct TChunk {
+  static constexpr int kWords = kSR * static_cast<int>(sizeof(T)) / 4;
+  uint32_t w[kWords];
+  __device__ __forceinline__ void put(int r, T v) {
+    if constexpr (sizeof(T) == 8) {
+      w[2 * r] = static_cast<uint32_t>(__double2loint(v));
+      w[2 * r + 1] = static_cast<uint32_t>(__double2hiint(v));
+    } else {
+      w[r] = __float_as_uint(v);
+    }
+  }
+  __device__ __forceinline__ T get(int r) const {
+    if constexpr (sizeof(T) == 8) return __hiloint2double(static_cast<int>(w[2 * r + 1]), static_cast<int>(w[2 * r]));
+    else return __uint_as_float(w[r]);
+  }
+  __device__ __forceinline__ void store(uint32_t taddr) const {
+    if constexpr (kWords == 32) tmem_st32(taddr, w);
+    else tmem_st16(taddr, w);
+  }
+  __device__ __forceinline__ void load(uint32_t taddr) {
+    if constexpr (kWords == 32) tmem_ld32(taddr, w);
+    else tmem_ld16(taddr, w);
+  }
+  __device__ __forceinline__ void wait() { tmem_wait_ld(w); }
+};
 
 // Forward sweep over C consecutive kSR-row chunks in ascending row order,
 // on this lane's pair of systems. base(c): the lane's row-0 pair of chunk c
@@ -259,16 +326,22 @@ struct PerArgs {
   // map), out receives u_new; stencil coefficients s, 4s, 1-2s / 1-6s
   void* out = nullptr;
   double cn[3] = {0.0, 0.0, 0.0};
+  // TMEM tier (kernel template TM): head chunks [0, tmem_chunks) of each
+  // system live in Tensor Memory instead of the L2 spill
+  int tmem_chunks = 0;
 };
 
-template <typename T, int V, bool PENT, bool FAST, int PER = 0, bool CN = false>
-__global__ void __launch_bounds__(32 * (stream_max_warps(V) + 2), 1)
+__host__ __device__ constexpr int stream_threads(int V, bool TM) { return 32 * ((TM ? 4 : stream_max_warps(V)) + 2); }
+
+template <typename T, int V, bool PENT, bool FAST, int PER = 0, bool CN = false, bool TM = false>
+__global__ void __launch_bounds__(stream_threads(V, TM), 1)
     sweep_stream(const __grid_constant__ CUtensorMap map_b, T* __restrict__ x, int n, long long m, long long ld,
                  int H, int TC, int KB, int KR, int PD, int stagger_ns, long long groups,
                  const void* __restrict__ fwd_g, const void* __restrict__ bwd_g, T* __restrict__ scratch,
                  const PerArgs per) {
   static_assert(PER == 0 || (FAST && sizeof(T) == 8 && (PER == 2) == PENT), "fused periodic: fast fp64 only");
   static_assert(!CN || sizeof(T) == 8, "fused Crank-Nicolson: fp64 only");
+  static_assert(!TM || V == 1, "TMEM tier: one system per lane");
   constexpr int kPerArrays = PER == 0 ? 0 : (PER == 1 ? 2 : 4);
   using FwdR = typename Recs<T, PENT>::Fwd;
   using BwdR = typename Recs<T, PENT>::Bwd;
@@ -292,12 +365,16 @@ __global__ void __launch_bounds__(32 * (stream_max_warps(V) + 2), 1)
   uint64_t* t_empty = t_full + TC;
   uint64_t* spilled = t_empty + TC;  // completes once per group when all warps' spills are published
   const int HC = H / kSR;
+  const int RTc = TM ? per.tmem_chunks : 0;  // head chunks held in TMEM
+  const int HS = HC - RTc;                   // head chunks spilled to L2
   constexpr int kLW = 32 * V;      // systems per warp
   constexpr int kSBlk = kSR * kLW;  // elements of one warp's block of one chunk
   const int Wg = P * kLW;
   const int chunk = P * kSBlk;  // elements of one chunk (all warps)
-  // this CTA's spill scratch: HC chunks x P warps x (kSR x 32), reused by every group
-  T* const spill_cta = scratch + static_cast<long long>(blockIdx.x) * HC * chunk;
+  // this CTA's spill scratch: head chunks [RTc, HC) x P warps x (kSR x 32V),
+  // reused by every group; spill chunk c lives at (c - RTc)
+  T* const spill_cta = scratch + static_cast<long long>(blockIdx.x) * HS * chunk - static_cast<long long>(RTc) * chunk;
+  uint32_t& tmem_base_s = *reinterpret_cast<uint32_t*>(spilled + 1);  // written by tcgen05.alloc
 
   {  // factor records -> smem (16-byte words; device arrays padded to 256 B)
     const int nf = static_cast<int>((static_cast<size_t>(n) * sizeof(FwdR) + 15) / 16);
@@ -335,7 +412,16 @@ __global__ void __launch_bounds__(32 * (stream_max_warps(V) + 2), 1)
   if ((blockIdx.x & 1) && stagger_ns > 0) {
     for (int t = 0; t < stagger_ns; t += 1000) __nanosleep(1000);
   }
+  if constexpr (TM) {
+    if (warp == 0 && RTc > 0) tmem_alloc_512(&tmem_base_s);
+    tmem_fence_before();
+  }
   __syncthreads();
+  uint32_t tmem_lane_base = 0;  // this warp's TMEM lane quadrant, column 0
+  if constexpr (TM) {
+    tmem_fence_after();
+    tmem_lane_base = (RTc > 0 ? tmem_base_s : 0u) + (static_cast<uint32_t>(32 * (warp & 3)) << 16);
+  }
 
   // tail chunk k of the group with iteration parity `par` lives in slot
   // par ? TC-1-k : k
@@ -392,9 +478,9 @@ __global__ void __launch_bounds__(32 * (stream_max_warps(V) + 2), 1)
         prefetch();
       }
       if (pre == HC) load_tail();
-      if (KR == 0 && HC > 0) {  // unified ring: the spill comes back through the same FIFO
+      if (KR == 0 && HS > 0) {  // unified ring: the spill comes back through the same FIFO
         mbar_wait(spilled, par);
-        for (int c = HC - 1; c >= 0; --c) {
+        for (int c = HC - 1; c >= RTc; --c) {
           if (issued >= static_cast<uint32_t>(KB)) mbar_wait(&b_empty[cur.slot], cur.phase ^ 1u);
           mbar_expect_tx(&b_full[cur.slot], c_bytes);
           bulk_load(bring + cur.slot * chunk, spill_cta + static_cast<long long>(c) * chunk, c_bytes,
@@ -409,14 +495,14 @@ __global__ void __launch_bounds__(32 * (stream_max_warps(V) + 2), 1)
 
   // ------------------------------------------------ reloader warp (spilled d-hat)
   if (warp == P + 1) {
-    if (lane != 0 || HC == 0 || KR == 0) return;
+    if (lane != 0 || HS <= 0 || KR == 0) return;
     const uint64_t pol_keep = policy_evict_last();
     Cursor cur;
     uint32_t issued = 0;
     uint32_t it = 0;
     for (long long g = blockIdx.x; g < groups; g += gridDim.x, ++it) {
       mbar_wait(spilled, it & 1u);  // every warp's head d-hat of this group is in the scratch
-      for (int c = HC - 1; c >= 0; --c) {
+      for (int c = HC - 1; c >= RTc; --c) {
         if (issued >= static_cast<uint32_t>(KR)) mbar_wait(&r_empty[cur.slot], cur.phase ^ 1u);
         mbar_expect_tx(&r_full[cur.slot], c_bytes);
         bulk_load(rring + cur.slot * chunk, spill_cta + static_cast<long long>(c) * chunk, c_bytes,
@@ -480,6 +566,7 @@ __global__ void __launch_bounds__(32 * (stream_max_warps(V) + 2), 1)
       out -= ld;
     };
     P2 s1{}, s2{};
+    TChunk<T> tbuf;  // TMEM tier staging (one 16-row chunk)
     // CN window: w1 = u_{i-1}, w2 = u_{i-2}; u0s/u1s = u_0, u_1 for the wrap
     P2 w1 = nw1, w2 = nw2, u0s{}, u1s{};
     auto stencil = [&](int row, P2 u, auto&& look) -> P2 {
@@ -554,13 +641,20 @@ __global__ void __launch_bounds__(32 * (stream_max_warps(V) + 2), 1)
             brl.next(KB);
           },
           [&](int c, int r, P2*, P2 v) {
-            st_spill_vec<T, V>(spill_l + c * cpairs + r * kPR, v, pol_keep);
+            if (TM && c < RTc) {  // TMEM tier: gather the chunk, one tcgen05.st per 16 rows
+              if constexpr (TM) {
+                tbuf.put(r, v.v[0]);
+                if (r == kSR - 1) tbuf.store(tmem_lane_base + static_cast<uint32_t>(c * TChunk<T>::kWords));
+              }
+            } else {
+              st_spill_vec<T, V>(spill_l + c * cpairs + r * kPR, v, pol_keep);
+            }
             accum(c * kSR + r, v);
           },
           [&](int c, int r, P2 u, auto&& look) { return stencil(c * kSR + r, u, look); },
           [&](int k) { return raw_tail(H + k); });
     }
-    if (HC > 0) {  // publish the spill to the async proxy (the reloader's bulk copies)
+    if (HS > 0) {  // publish the spill to the async proxy (the reloader's bulk copies)
       fence_proxy_async_global();
       __syncwarp();
       if (lane == 0) mbar_arrive(spilled);
@@ -634,7 +728,7 @@ __global__ void __launch_bounds__(32 * (stream_max_warps(V) + 2), 1)
       const int K = uni ? KB : KR;
       uint32_t cs = 0;
       bwd_chunks<T, V, PENT, FAST>(
-          HC, sb, s1, s2, [&](int) -> const P2* { return ring_l + cs * cpairs; },
+          HS, sb + RTc * kSR, s1, s2, [&](int) -> const P2* { return ring_l + cs * cpairs; },
           [&](int) {
             cs = cw.slot;
             mbar_wait(&full[cw.slot], cw.phase);
@@ -645,7 +739,30 @@ __global__ void __launch_bounds__(32 * (stream_max_warps(V) + 2), 1)
             if (lane == 0) mbar_arrive(&empty[cr.slot]);
             cr.next(K);
           },
-          [&](int c, int r, P2 v) { emit(c * kSR + r, v); });
+          [&](int c, int r, P2 v) { emit((RTc + c) * kSR + r, v); });
+    }
+    // ---- backward, TMEM rows: one tcgen05.ld per 16 rows, a chunk ahead
+    if constexpr (TM) {
+      if (RTc > 0) {
+        TChunk<T> cur, nxt;
+        cur.load(tmem_lane_base + static_cast<uint32_t>((RTc - 1) * TChunk<T>::kWords));
+        cur.wait();
+        for (int c = RTc - 1; c >= 0; --c) {
+          if (c > 0) nxt.load(tmem_lane_base + static_cast<uint32_t>((c - 1) * TChunk<T>::kWords));
+          const BwdR* b = sb + c * kSR;
+#pragma unroll
+          for (int q = 0; q < kSR; ++q) {
+            const int r = kSR - 1 - q;
+            P2 y;
+            y.v[0] = bwd_row<T, PENT, FAST>(b[r], cur.get(r), s1.v[0], s2.v[0]);
+            emit(c * kSR + r, y);
+          }
+          if (c > 0) {
+            nxt.wait();
+            cur = nxt;
+          }
+        }
+      }
     }
   };
   for (; g < groups; g += gridDim.x, ++it) {
@@ -654,12 +771,20 @@ __global__ void __launch_bounds__(32 * (stream_max_warps(V) + 2), 1)
   }
 
   // the scratch is dead: drop this warp's L2 lines instead of writing them back
-  if (HC > 0) {
+  if (HS > 0) {
     __syncwarp();
-    for (int c = 0; c < HC; ++c) {
+    for (int c = RTc; c < HC; ++c) {
       const char* base = reinterpret_cast<const char*>(spill_cta + static_cast<long long>(c) * chunk + warp * kSBlk);
       for (int off = lane * 128; off < kSBlk * static_cast<int>(sizeof(T)); off += 32 * 128)
         discard_l2_line(base + off);
+    }
+  }
+  if constexpr (TM) {  // every compute warp is done with TMEM: warp 0 frees it
+    if (RTc > 0) {
+      tmem_fence_before();
+      asm volatile("bar.sync 1, %0;" ::"r"(P * 32) : "memory");
+      tmem_fence_after();
+      if (warp == 0) tmem_dealloc_512(tmem_base_s);
     }
   }
 }

@@ -145,7 +145,8 @@ PLANS = [None, ("global",), ("smemW8",), ("smemW16",), ("smemW32",), ("persist",
          ("stream", "64", "0", "4", "2"), ("stream", "64", "16", "2", "1"), ("stream", "128", "40", "4", "2"),
          ("stream", "256", "100000", "4", "1"), ("stream", "192", "33", "2", "2"), ("stream", "96", "48", "3", "1"),
          ("stream", "32", "0", "4", "1"), ("stream", "96", "48", "4", "1", "4"),
-         ("stream", "64", "8", "3", "2", "2"), ("regs", "96"), ("regs", "32", "16"), ("regs", "224", "40")]
+         ("stream", "64", "8", "3", "2", "2"), ("stream", "96", "16", "4", "1", "4"), ("stream", "128", "40", "4", "1", "4"),
+         ("stream", "32", "0", "2", "1", "2"), ("regs", "96"), ("regs", "32", "16"), ("regs", "224", "40")]
 PLAN_ENV = ("BANDSOLVE_PLAN", "BANDSOLVE_PWARPS", "BANDSOLVE_PTAIL", "BANDSOLVE_SWG", "BANDSOLVE_STAIL",
             "BANDSOLVE_SKB", "BANDSOLVE_SV", "BANDSOLVE_SKR")
 

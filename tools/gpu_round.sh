@@ -19,6 +19,9 @@ for mode in exact fast; do
   done
 done
 timeout 300 python bench.py --config tri512 --f32 --no-cpu --steps 50 --warmup 5 >> gpurun_out/bench_sweep.jsonl 2>> gpurun_out/bench_err.log
+for extra in "--config pent512 --periodic" "--config pent512 --periodic --mode fast" "--config pent512 --cn" "--config pent512 --cn --mode fast" "--config tri512 --cn --mode fast" "--config c4tri" "--config c4pent --mode fast"; do
+  timeout 300 python bench.py $extra --no-cpu --steps 20 --warmup 3 >> gpurun_out/bench_sweep.jsonl 2>> gpurun_out/bench_err.log
+done
 timeout 300 python bench.py --config pent512 --f32 --no-cpu --steps 50 --warmup 5 >> gpurun_out/bench_sweep.jsonl 2>> gpurun_out/bench_err.log
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
    --log-file gpurun_out/launches_c2.csv python bench.py --steps 5 --warmup 3 --no-cpu > gpurun_out/ncu_launch.log 2>&1
