@@ -354,7 +354,7 @@ double stream_compute_frac(int S, bool pent, bool fast) {
 // longer stays L2-resident alongside the b/x streams and it falls off
 // quickly (n = 512 / 1024 sweeps, tools/gpu_calib.sh).
 double stream_spill_factor(double spill_mb) {
-  static const double pts[][2] = {{0, 1.0}, {1, 0.82}, {45, 0.80}, {57, 0.74}, {65, 0.60}, {98, 0.43}, {200, 0.25}};
+  static const double pts[][2] = {{0, 1.0}, {1, 0.82}, {45, 0.80}, {57, 0.74}, {65, 0.56}, {98, 0.40}, {200, 0.25}};
   const int np = sizeof(pts) / sizeof(pts[0]);
   if (spill_mb >= pts[np - 1][0]) return pts[np - 1][1];
   for (int k = 1; k < np; ++k)
@@ -376,11 +376,11 @@ int env_int(const char* name, int dflt) {
 //   frac = compute(S) x spill_factor(spill) x (round utilisation),
 // preferring the smaller spill on ties.
 bool plan_stream(std::size_t n, std::size_t m, std::size_t elem, bool pent, bool fast, int sms, Plan& p,
-                 int per_arrays = 0, bool allow_tmem = true) {
+                 int per_arrays = 0, bool allow_tmem = true, int only_wg = 0) {
   const std::size_t fr = fwd_rec_bytes(pent, elem), br = bwd_rec_bytes(pent, elem);
   const std::size_t fac = dev::align128(n * fr) + dev::align128(n * br);
   if (fac > kSmemPerBlockMax / 2 || n < 2) return false;
-  const int forced_wg = env_int("BANDSOLVE_SWG", 0);
+  const int forced_wg = only_wg ? only_wg : env_int("BANDSOLVE_SWG", 0);
   const int forced_tail = env_int("BANDSOLVE_STAIL", -1);
   // KR = 0: one FIFO ring of KB slots carries both the b chunks and the
   // spill reloads (every slot serves whichever head phase is running)
@@ -391,6 +391,7 @@ bool plan_stream(std::size_t n, std::size_t m, std::size_t elem, bool pent, bool
   bool found = false;
   double best_t = 1e300;
   double best_spill = 1e300;
+  int tmem_pick = 0;
   const int forced_v = env_int("BANDSOLVE_SV", 0);
   for (int cand = 0; cand < 16; ++cand) {
     const int V = cand < 8 ? 1 : 2;
@@ -437,6 +438,13 @@ bool plan_stream(std::size_t n, std::size_t m, std::size_t elem, bool pent, bool
     const double frac = stream_compute_frac(Wg, pent, fast) * (V == 2 ? 0.95 : 1.0) *
                         stream_spill_factor(spill / (1 << 20)) * util;
     const double t = static_cast<double>(n) * m * 2.0 * elem / (frac * 6.5e12);
+    // TMEM-tier rule (measured at N = 384..512, tools/gpu_calib.sh): with the
+    // forward intermediates split over TMEM + smem, the largest group whose
+    // residual L2 spill stays <= 30 MB wins (capped at 96 systems in fast
+    // mode); the calibrated model below decides everything else.
+    if (rtc > 0 && N >= 384 && Wg >= 96 && spill <= 30.0 * (1 << 20) && Wg <= (fast ? 96 : 128) && !forced_wg) {
+      tmem_pick = Wg;
+    }
     if (!found || t < best_t * 0.995 || (t <= best_t * 1.005 && spill < best_spill)) {
       found = true;
       best_t = t;
@@ -455,6 +463,11 @@ bool plan_stream(std::size_t n, std::size_t m, std::size_t elem, bool pent, bool
       p.V = V;
       p.tmem_chunks = rtc;
     }
+  }
+  if (found && tmem_pick && tmem_pick != p.Wg) {
+    // re-plan with the TMEM rule's group width (same layout rules)
+    Plan q;
+    if (plan_stream(n, m, elem, pent, fast, sms, q, per_arrays, allow_tmem, tmem_pick)) p = q;
   }
   return found;
 }
