@@ -442,7 +442,8 @@ bool plan_stream(std::size_t n, std::size_t m, std::size_t elem, bool pent, bool
     // forward intermediates split over TMEM + smem, the largest group whose
     // residual L2 spill stays <= 30 MB wins (capped at 96 systems in fast
     // mode); the calibrated model below decides everything else.
-    if (rtc > 0 && N >= 384 && Wg >= 96 && spill <= 30.0 * (1 << 20) && Wg <= (fast ? 96 : 128) && !forced_wg) {
+    if (rtc > 0 && elem == 8 && N >= 384 && Wg >= 96 && spill <= 30.0 * (1 << 20) && Wg <= (fast ? 96 : 128) &&
+        !forced_wg) {
       tmem_pick = Wg;
     }
     if (!found || t < best_t * 0.995 || (t <= best_t * 1.005 && spill < best_spill)) {
@@ -1200,7 +1201,7 @@ bandsolve_status cn_step_device(const Periodic& p, double sigma_x, const double*
   Plan plan;
   if (std::getenv("BANDSOLVE_CN_UNFUSED") == nullptr && aligned && n <= static_cast<std::size_t>(INT_MAX) &&
       m <= static_cast<std::size_t>(INT_MAX) / 2 &&
-      plan_stream(n, m, sizeof(double), pent, fast, sms, plan, fast ? (pent ? 4 : 2) : 0, false)) {
+      plan_stream(n, m, sizeof(double), pent, fast, sms, plan, fast ? (pent ? 4 : 2) : 0)) {
     const DeviceFactor* df = nullptr;
     bandsolve_status st = ensure_device_factor(*p.factor, device, &df);
     if (st != BANDSOLVE_OK) return st;
@@ -1228,20 +1229,25 @@ bandsolve_status cn_step_device(const Periodic& p, double sigma_x, const double*
     const void* fw = df->fwd[0][q];
     const void* bw = df->bwd[0][q];
     cudaError_t err;
+    const bool tm = plan.V == 1 && plan.tmem_chunks > 0;
     if (fast) {
       if (pent)
-        err = plan.V == 2 ? launch_stream_v<double, 2, true, true, 2, true>(plan, x, N, M, LD, fw, bw, s, sms, per)
-                          : launch_stream_v<double, 1, true, true, 2, true>(plan, x, N, M, LD, fw, bw, s, sms, per);
+        err = tm ? launch_stream_v<double, 1, true, true, 2, true, true>(plan, x, N, M, LD, fw, bw, s, sms, per)
+              : plan.V == 2 ? launch_stream_v<double, 2, true, true, 2, true>(plan, x, N, M, LD, fw, bw, s, sms, per)
+                            : launch_stream_v<double, 1, true, true, 2, true>(plan, x, N, M, LD, fw, bw, s, sms, per);
       else
-        err = plan.V == 2 ? launch_stream_v<double, 2, false, true, 1, true>(plan, x, N, M, LD, fw, bw, s, sms, per)
-                          : launch_stream_v<double, 1, false, true, 1, true>(plan, x, N, M, LD, fw, bw, s, sms, per);
+        err = tm ? launch_stream_v<double, 1, false, true, 1, true, true>(plan, x, N, M, LD, fw, bw, s, sms, per)
+              : plan.V == 2 ? launch_stream_v<double, 2, false, true, 1, true>(plan, x, N, M, LD, fw, bw, s, sms, per)
+                            : launch_stream_v<double, 1, false, true, 1, true>(plan, x, N, M, LD, fw, bw, s, sms, per);
     } else {
       if (pent)
-        err = plan.V == 2 ? launch_stream_v<double, 2, true, false, 0, true>(plan, x, N, M, LD, fw, bw, s, sms, per)
-                          : launch_stream_v<double, 1, true, false, 0, true>(plan, x, N, M, LD, fw, bw, s, sms, per);
+        err = tm ? launch_stream_v<double, 1, true, false, 0, true, true>(plan, x, N, M, LD, fw, bw, s, sms, per)
+              : plan.V == 2 ? launch_stream_v<double, 2, true, false, 0, true>(plan, x, N, M, LD, fw, bw, s, sms, per)
+                            : launch_stream_v<double, 1, true, false, 0, true>(plan, x, N, M, LD, fw, bw, s, sms, per);
       else
-        err = plan.V == 2 ? launch_stream_v<double, 2, false, false, 0, true>(plan, x, N, M, LD, fw, bw, s, sms, per)
-                          : launch_stream_v<double, 1, false, false, 0, true>(plan, x, N, M, LD, fw, bw, s, sms, per);
+        err = tm ? launch_stream_v<double, 1, false, false, 0, true, true>(plan, x, N, M, LD, fw, bw, s, sms, per)
+              : plan.V == 2 ? launch_stream_v<double, 2, false, false, 0, true>(plan, x, N, M, LD, fw, bw, s, sms, per)
+                            : launch_stream_v<double, 1, false, false, 0, true>(plan, x, N, M, LD, fw, bw, s, sms, per);
     }
     if (err != cudaSuccess) return cuda_fail(err, "fused Crank-Nicolson sweep launch");
     if (fast) return BANDSOLVE_OK;
@@ -1269,7 +1275,7 @@ bandsolve_status periodic_device(const Periodic& p, double* x, std::size_t n, st
     const bool aligned = (reinterpret_cast<uintptr_t>(x) % 16 == 0) && ((ld * sizeof(double)) % 16 == 0);
     Plan plan;
     if (aligned && n <= static_cast<std::size_t>(INT_MAX) && m <= static_cast<std::size_t>(INT_MAX) / 2 &&
-        plan_stream(n, m, sizeof(double), pent, true, sms, plan, pent ? 4 : 2, false)) {
+        plan_stream(n, m, sizeof(double), pent, true, sms, plan, pent ? 4 : 2)) {
       const DeviceFactor* df = nullptr;
       bandsolve_status st = ensure_device_factor(*p.factor, device, &df);
       if (st != BANDSOLVE_OK) return st;
@@ -1288,12 +1294,17 @@ bandsolve_status periodic_device(const Periodic& p, double* x, std::size_t n, st
       const int N = static_cast<int>(n);
       const long long M = static_cast<long long>(m), LD = static_cast<long long>(ld);
       cudaError_t err;
+      const void* fw = df->fwd[0][1];
+      const void* bw = df->bwd[0][1];
+      const bool tm = plan.V == 1 && plan.tmem_chunks > 0;
       if (pent)
-        err = plan.V == 2 ? launch_stream_v<double, 2, true, true, 2>(plan, x, N, M, LD, df->fwd[0][1], df->bwd[0][1], s, sms, per)
-                          : launch_stream_v<double, 1, true, true, 2>(plan, x, N, M, LD, df->fwd[0][1], df->bwd[0][1], s, sms, per);
+        err = tm ? launch_stream_v<double, 1, true, true, 2, false, true>(plan, x, N, M, LD, fw, bw, s, sms, per)
+              : plan.V == 2 ? launch_stream_v<double, 2, true, true, 2>(plan, x, N, M, LD, fw, bw, s, sms, per)
+                            : launch_stream_v<double, 1, true, true, 2>(plan, x, N, M, LD, fw, bw, s, sms, per);
       else
-        err = plan.V == 2 ? launch_stream_v<double, 2, false, true, 1>(plan, x, N, M, LD, df->fwd[0][1], df->bwd[0][1], s, sms, per)
-                          : launch_stream_v<double, 1, false, true, 1>(plan, x, N, M, LD, df->fwd[0][1], df->bwd[0][1], s, sms, per);
+        err = tm ? launch_stream_v<double, 1, false, true, 1, false, true>(plan, x, N, M, LD, fw, bw, s, sms, per)
+              : plan.V == 2 ? launch_stream_v<double, 2, false, true, 1>(plan, x, N, M, LD, fw, bw, s, sms, per)
+                            : launch_stream_v<double, 1, false, true, 1>(plan, x, N, M, LD, fw, bw, s, sms, per);
       if (err != cudaSuccess) return cuda_fail(err, "fused periodic sweep launch");
       return BANDSOLVE_OK;
     }
