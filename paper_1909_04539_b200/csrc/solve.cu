@@ -540,6 +540,13 @@ Plan choose_plan(std::size_t n, std::size_t m, std::size_t ld, std::size_t elem,
   if (force && std::strcmp(force, "regs") == 0 &&
       plan_regs(n, m, elem, pent, sms, std::max(1, env_int("BANDSOLVE_SWG", 96) / 32), p))
     return p;
+  // few long systems (< ~1 warp per SM, n >= 1024): the group machinery cannot
+  // fill the SMs and the spill would not fit L2 -> thread per system in
+  // global memory with a deep register prefetch (measured on the ADI axes)
+  if (!force && m <= static_cast<std::size_t>(sms) * 32 && n >= 1024) {
+    p.why = "few long systems: deep-prefetch thread-per-system";
+    return p;
+  }
   if (!force_smem && !force_persist && plan_stream(n, m, elem, pent, fast, sms, p)) return p;
   if (!force_smem && plan_persist(n, elem, pent, fast, sms, p)) return p;
   int best_sys = 0;
@@ -747,7 +754,11 @@ cudaError_t launch_global(T* x, int n, long long m, long long ld, const void* fw
   int threads = 128;
   while (threads > 32 && (m + threads - 1) / threads < sms) threads >>= 1;
   const long long grid = (m + threads - 1) / threads;
-  dev::sweep_global<T, PENT, FAST><<<static_cast<unsigned>(grid), threads, 0, s>>>(x, n, m, ld, fwd, bwd);
+  const bool deep = m <= static_cast<long long>(sms) * 64 && n >= 256;  // few long systems
+  if (deep)
+    dev::sweep_global<T, PENT, FAST, 32><<<static_cast<unsigned>(grid), threads, 0, s>>>(x, n, m, ld, fwd, bwd);
+  else
+    dev::sweep_global<T, PENT, FAST><<<static_cast<unsigned>(grid), threads, 0, s>>>(x, n, m, ld, fwd, bwd);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }
@@ -870,51 +881,51 @@ __global__ void fill_rhs_kernel(T* __restrict__ x, int n, long long m, long long
 }
 
 // ---- periodic wrap correction (reference periodic.cpp:57-89, :172-208) -----
-// One thread per system (coalesced rows), the reference's operation order
-// with separately rounded products/sums; z is read as warp-uniform
-// broadcasts. Rows are processed 8 at a time with the loads issued first.
-__global__ void periodic_tri_correct_kernel(double* __restrict__ x, int n, long long m, long long ld,
-                                            const double* __restrict__ z, double v_last, double scale) {
+// Two phases so rows can be corrected in parallel without racing on the
+// rows the coefficients read: (1) one thread per system forms its
+// coefficient(s) from y_0 (y_1) and y_{n-1} (y_{n-2}) into coef[]; (2) a 2D
+// grid applies x_i = y_i - w z_i (pent: - (z1_i t1 + z2_i t2)) to every row,
+// the reference's operation order with separately rounded operations.
+__global__ void periodic_coef_kernel(const double* __restrict__ x, int n, long long m, long long ld, bool pent,
+                                     double c0, double c1, double c2, double c3, double* __restrict__ coef) {
   using namespace dev;
   const long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= m) return;
-  double* col = x + j;
-  // w = (y_0 + v_last * y_{n-1}) * scale                      periodic.cpp:80
-  const double w = mul_rn(add_rn(col[0], mul_rn(v_last, col[static_cast<long long>(n - 1) * ld])), scale);
-  int i = 0;
-  for (; i + 8 <= n; i += 8) {
-    double y[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) y[u] = col[static_cast<long long>(i + u) * ld];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) col[static_cast<long long>(i + u) * ld] = sub_rn(y[u], mul_rn(w, __ldg(z + i + u)));
+  auto Y = [&](int i) { return x[static_cast<long long>(i) * ld + j]; };
+  if (!pent) {
+    // w = (y_0 + v_last * y_{n-1}) * scale                          periodic.cpp:80
+    coef[j] = mul_rn(add_rn(Y(0), mul_rn(c0, Y(n - 1))), c1);
+  } else {
+    // periodic.cpp:189-194
+    const double w1 = sub_rn(Y(0), Y(n - 1));
+    const double w2 = sub_rn(Y(1), Y(n - 2));
+    coef[j] = add_rn(mul_rn(c0, w1), mul_rn(c1, w2));
+    coef[m + j] = add_rn(mul_rn(c2, w1), mul_rn(c3, w2));
   }
-  for (; i < n; ++i) col[static_cast<long long>(i) * ld] = sub_rn(col[static_cast<long long>(i) * ld], mul_rn(w, __ldg(z + i)));
 }
 
-__global__ void periodic_pent_correct_kernel(double* __restrict__ x, int n, long long m, long long ld,
-                                             const double* __restrict__ z1, const double* __restrict__ z2,
-                                             double i00, double i01, double i10, double i11) {
+constexpr int kCorrRows = 16;  // rows per thread of the apply kernel
+
+template <bool PENT>
+__global__ void periodic_apply_kernel(double* __restrict__ x, int n, long long m, long long ld,
+                                      const double* __restrict__ z1, const double* __restrict__ z2,
+                                      const double* __restrict__ coef) {
   using namespace dev;
   const long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= m) return;
+  const int i0 = blockIdx.y * kCorrRows;
+  const int i1 = min(n, i0 + kCorrRows);
   double* col = x + j;
-  auto Y = [&](int i) -> double& { return col[static_cast<long long>(i) * ld]; };
-  // periodic.cpp:189-194
-  const double w1 = sub_rn(Y(0), Y(n - 1));
-  const double w2 = sub_rn(Y(1), Y(n - 2));
-  const double t1 = add_rn(mul_rn(i00, w1), mul_rn(i01, w2));
-  const double t2 = add_rn(mul_rn(i10, w1), mul_rn(i11, w2));
-  int i = 0;
-  for (; i + 8 <= n; i += 8) {
-    double y[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) y[u] = Y(i + u);
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-      Y(i + u) = sub_rn(y[u], add_rn(mul_rn(__ldg(z1 + i + u), t1), mul_rn(__ldg(z2 + i + u), t2)));
+  if constexpr (!PENT) {
+    const double w = coef[j];
+    for (int i = i0; i < i1; ++i)  // periodic.cpp:85: row -= w * z_i
+      col[static_cast<long long>(i) * ld] = sub_rn(col[static_cast<long long>(i) * ld], mul_rn(w, __ldg(z1 + i)));
+  } else {
+    const double t1 = coef[j], t2 = coef[m + j];
+    for (int i = i0; i < i1; ++i)  // periodic.cpp:203: row -= z1_i t1 + z2_i t2
+      col[static_cast<long long>(i) * ld] = sub_rn(
+          col[static_cast<long long>(i) * ld], add_rn(mul_rn(__ldg(z1 + i), t1), mul_rn(__ldg(z2 + i), t2)));
   }
-  for (; i < n; ++i) Y(i) = sub_rn(Y(i), add_rn(mul_rn(__ldg(z1 + i), t1), mul_rn(__ldg(z2 + i), t2)));
 }
 
 // ---- Crank-Nicolson explicit half, periodic stencil (reference pde.cpp:73-114) --
@@ -924,28 +935,33 @@ __global__ void periodic_pent_correct_kernel(double* __restrict__ x, int n, long
 // order with separately rounded operations:
 //   diffusion  o = s*(u[i-1] + u[i+1]) + mid*u[i]                    (:85)
 //   hyper      o = -s*(u[i-2] + u[i+2]) + s4*(u[i-1] + u[i+1]) + mid*u[i]   (:108)
+constexpr int kStencilRows = 16;  // rows per thread of the stencil kernel
+
 template <bool PENT>
 __global__ void cn_rhs_kernel(const double* __restrict__ u, double* __restrict__ out, int n, long long m,
                               long long ld, double s, double s4, double mid) {
   using namespace dev;
   const long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= m) return;
-  auto U = [&](int i) { return u[static_cast<long long>(i) * ld + j]; };
+  const int i0 = blockIdx.y * kStencilRows;
+  const int i1 = min(n, i0 + kStencilRows);
+  auto U = [&](int i) {  // periodic row index (|offset| <= 2 < n)
+    i = i < 0 ? i + n : (i >= n ? i - n : i);
+    return u[static_cast<long long>(i) * ld + j];
+  };
   double* o = out + j;
   if constexpr (!PENT) {
-    const double first = U(0);
-    double um = U(n - 1), ui = first;
-    for (int i = 0; i < n; ++i) {
-      const double up = i + 1 < n ? U(i + 1) : first;
+    double um = U(i0 - 1), ui = U(i0);
+    for (int i = i0; i < i1; ++i) {
+      const double up = U(i + 1);
       o[static_cast<long long>(i) * ld] = add_rn(mul_rn(s, add_rn(um, up)), mul_rn(mid, ui));
       um = ui;
       ui = up;
     }
   } else {
-    const double u0 = U(0), u1 = U(1);
-    double a2 = U(n - 2), a1 = U(n - 1), c = u0, b1 = u1;  // u[i-2], u[i-1], u[i], u[i+1]
-    for (int i = 0; i < n; ++i) {
-      const double b2 = i + 2 < n ? U(i + 2) : (i + 2 == n ? u0 : u1);
+    double a2 = U(i0 - 2), a1 = U(i0 - 1), c = U(i0), b1 = U(i0 + 1);  // u[i-2], u[i-1], u[i], u[i+1]
+    for (int i = i0; i < i1; ++i) {
+      const double b2 = U(i + 2);
       const double t = add_rn(mul_rn(-s, add_rn(a2, b2)), mul_rn(s4, add_rn(a1, b1)));
       o[static_cast<long long>(i) * ld] = add_rn(t, mul_rn(mid, c));
       a2 = a1;
@@ -1162,16 +1178,27 @@ bandsolve_status launch_periodic_correct(const Periodic& p, double* x, std::size
   const double* z = nullptr;
   bandsolve_status st = periodic_device_z(p, device, &z);
   if (st != BANDSOLVE_OK) return st;
+  const bool pent = p.kind != Kind::Tri;
+  double* coef = nullptr;
+  BSB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&coef), (pent ? 2 : 1) * m * sizeof(double), s));
   const int threads = 128;
-  const unsigned grid = static_cast<unsigned>((m + threads - 1) / threads);
-  if (p.kind == Kind::Tri)
-    periodic_tri_correct_kernel<<<grid, threads, 0, s>>>(x, static_cast<int>(n), static_cast<long long>(m),
-                                                         static_cast<long long>(ld), z, p.v_last, p.scale);
+  const unsigned gx = static_cast<unsigned>((m + threads - 1) / threads);
+  if (pent)
+    periodic_coef_kernel<<<gx, threads, 0, s>>>(x, static_cast<int>(n), static_cast<long long>(m),
+                                                static_cast<long long>(ld), true, p.cap_inv[0], p.cap_inv[1],
+                                                p.cap_inv[2], p.cap_inv[3], coef);
   else
-    periodic_pent_correct_kernel<<<grid, threads, 0, s>>>(x, static_cast<int>(n), static_cast<long long>(m),
-                                                          static_cast<long long>(ld), z, z + n, p.cap_inv[0],
-                                                          p.cap_inv[1], p.cap_inv[2], p.cap_inv[3]);
-  g_launches.fetch_add(1, std::memory_order_relaxed);
+    periodic_coef_kernel<<<gx, threads, 0, s>>>(x, static_cast<int>(n), static_cast<long long>(m),
+                                                static_cast<long long>(ld), false, p.v_last, p.scale, 0.0, 0.0, coef);
+  const dim3 grid(gx, static_cast<unsigned>((n + kCorrRows - 1) / kCorrRows));
+  if (pent)
+    periodic_apply_kernel<true><<<grid, threads, 0, s>>>(x, static_cast<int>(n), static_cast<long long>(m),
+                                                         static_cast<long long>(ld), z, z + n, coef);
+  else
+    periodic_apply_kernel<false><<<grid, threads, 0, s>>>(x, static_cast<int>(n), static_cast<long long>(m),
+                                                          static_cast<long long>(ld), z, nullptr, coef);
+  g_launches.fetch_add(2, std::memory_order_relaxed);
+  cudaFreeAsync(coef, s);
   BSB_CUDA(cudaGetLastError());
   return BANDSOLVE_OK;
 }
@@ -1382,7 +1409,8 @@ bandsolve_status cn_rhs_device(bool pent, double sigma_x, const double* u, doubl
   if (device_count_cached() == 0) return fail(BANDSOLVE_ERR_INTERNAL, "no CUDA device available (no CPU fallback)");
   auto s = static_cast<cudaStream_t>(stream);
   const int threads = 128;
-  const unsigned grid = static_cast<unsigned>((m + threads - 1) / threads);
+  const dim3 grid(static_cast<unsigned>((m + threads - 1) / threads),
+                  static_cast<unsigned>((n + kStencilRows - 1) / kStencilRows));
   // pde.cpp:80-81 / :101-103: the coefficients are formed once on the host
   if (pent)
     cn_rhs_kernel<true><<<grid, threads, 0, s>>>(u, out, static_cast<int>(n), static_cast<long long>(m),

@@ -245,11 +245,13 @@ __global__ void __launch_bounds__(W) sweep_smem(const __grid_constant__ CUtensor
 // ---- global (L2) regime ----------------------------------------------------
 // One thread per system, in place; U-row blocks double-buffered in registers
 // so the next block's loads are in flight while the current block computes.
-template <typename T, bool PENT, bool FAST>
+// U: rows per register block (two blocks in flight). U = 8 when many systems
+// share an SM; U = 32 for the few-long-systems regime (e.g. ADI axes), where
+// each thread alone must cover HBM latency with its own prefetch.
+template <typename T, bool PENT, bool FAST, int U = 8>
 __global__ void __launch_bounds__(128) sweep_global(T* __restrict__ x, int n, long long m,
                                                     long long ld, const void* __restrict__ fwd,
                                                     const void* __restrict__ bwd) {
-  constexpr int U = 8;
   const long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= m) return;
   T* col = x + j;
