@@ -1,5 +1,5 @@
 #!/bin/bash
-# GPU tests + a few targeted bench lines given as "ENV|ARGS" entries in $RUNS (one per line).
+# GPU tests + targeted bench lines listed as "ENV|ARGS" entries (one per line) in tools/quick_runs.txt.
 set -u
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 mkdir -p gpurun_out
