@@ -585,6 +585,20 @@ bool encode_map(CUtensorMap* map, void* x, std::size_t elem, long long n, long l
 }
 
 template <typename K>
+cudaError_t allow_big_smem(K kern);
+// Set the large-smem attributes of `kern` once per device.
+template <typename K>
+cudaError_t allow_big_smem_once(K kern, std::atomic<uint64_t>& done) {
+  int device = 0;
+  if (cudaError_t e = cudaGetDevice(&device); e != cudaSuccess) return e;
+  const uint64_t bit = device < 64 ? (1ull << device) : 0;
+  if (bit && (done.load(std::memory_order_relaxed) & bit)) return cudaSuccess;
+  cudaError_t e = allow_big_smem(kern);
+  if (e == cudaSuccess && bit) done.fetch_or(bit, std::memory_order_relaxed);
+  return e;
+}
+
+template <typename K>
 cudaError_t allow_big_smem(K kern) {
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(kSmemPerBlockMax));
@@ -596,12 +610,8 @@ template <typename T, int W, bool PENT, bool FAST>
 cudaError_t launch_smem(const Plan& plan, T* x, int n, long long m, long long ld, const void* fwd,
                         const void* bwd, cudaStream_t s) {
   auto kern = dev::sweep_smem<T, W, kChunkRows, PENT, FAST>;
-  static std::atomic<bool> configured{false};
-  if (!configured.load(std::memory_order_relaxed)) {
-    cudaError_t e = allow_big_smem(kern);
-    if (e != cudaSuccess) return e;
-    configured.store(true, std::memory_order_relaxed);
-  }
+  static std::atomic<uint64_t> configured{0};  // one bit per device: attributes are per context
+  if (cudaError_t e = allow_big_smem_once(kern, configured); e != cudaSuccess) return e;
   CUtensorMap map;
   if (!encode_map(&map, x, sizeof(T), n, m, ld, W, kChunkRows)) return cudaErrorInvalidValue;
   const long long grid = (m + W - 1) / W;
@@ -614,12 +624,8 @@ template <typename T, bool PENT, bool FAST>
 cudaError_t launch_persist(const Plan& plan, T* x, int n, long long m, long long ld, const void* fwd,
                            const void* bwd, cudaStream_t s, int sms) {
   auto kern = dev::sweep_persist<T, PENT, FAST>;
-  static std::atomic<bool> configured{false};
-  if (!configured.load(std::memory_order_relaxed)) {
-    cudaError_t e = allow_big_smem(kern);
-    if (e != cudaSuccess) return e;
-    configured.store(true, std::memory_order_relaxed);
-  }
+  static std::atomic<uint64_t> configured{0};  // one bit per device: attributes are per context
+  if (cudaError_t e = allow_big_smem_once(kern, configured); e != cudaSuccess) return e;
   CUtensorMap map_ring, map_tail;
   if (!encode_map(&map_ring, x, sizeof(T), n, m, ld, dev::kPW, dev::kRH) ||
       !encode_map(&map_tail, x, sizeof(T), n, m, ld, dev::kPW, dev::kRT))
@@ -661,12 +667,8 @@ cudaError_t launch_stream_v(const Plan& plan, T* x, int n, long long m, long lon
   auto kern = dev::sweep_stream<T, V, PENT, FAST, PER, CN, TM>;
   dev::PerArgs per = per_in;
   per.tmem_chunks = TM ? plan.tmem_chunks : 0;
-  static std::atomic<bool> configured{false};
-  if (!configured.load(std::memory_order_relaxed)) {
-    cudaError_t e = allow_big_smem(kern);
-    if (e != cudaSuccess) return e;
-    configured.store(true, std::memory_order_relaxed);
-  }
+  static std::atomic<uint64_t> configured{0};  // one bit per device: attributes are per context
+  if (cudaError_t e = allow_big_smem_once(kern, configured); e != cudaSuccess) return e;
   CUtensorMap map;
   if (!encode_map(&map, x, sizeof(T), n, m, ld, 32 * V, dev::kSR)) return cudaErrorInvalidValue;
   const long long groups = (m + plan.Wg - 1) / plan.Wg;
@@ -718,12 +720,8 @@ template <typename T, bool PENT, bool FAST, int NB>
 cudaError_t launch_regs_nb(const Plan& plan, T* x, int n, long long m, long long ld, const void* fwd,
                            const void* bwd, cudaStream_t s, int sms) {
   auto kern = dev::sweep_regs<T, PENT, FAST, NB>;
-  static std::atomic<bool> configured{false};
-  if (!configured.load(std::memory_order_relaxed)) {
-    cudaError_t e = allow_big_smem(kern);
-    if (e != cudaSuccess) return e;
-    configured.store(true, std::memory_order_relaxed);
-  }
+  static std::atomic<uint64_t> configured{0};  // one bit per device: attributes are per context
+  if (cudaError_t e = allow_big_smem_once(kern, configured); e != cudaSuccess) return e;
   CUtensorMap map;
   if (!encode_map(&map, x, sizeof(T), n, m, ld, 32, dev::kSR)) return cudaErrorInvalidValue;
   const long long groups = (m + plan.Wg - 1) / plan.Wg;
