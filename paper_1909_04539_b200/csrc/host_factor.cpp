@@ -63,6 +63,8 @@ bandsolve_status make_tri_factor(const double* sub, const double* diag,
   f->chat.assign(n, 0.0);
   f->inv_denom.assign(n, 0.0);
   f->sub.assign(sub, sub + n);  // banded.cpp:73: the factor keeps a copy of a_i
+  f->bands.reserve(3 * n);
+  for (const double* v : {sub, diag, sup}) f->bands.insert(f->bands.end(), v, v + n);
 
   // banded.cpp:75-84. chat is sup / denom (a division, not sup * inv), and
   // the last chat slot stays zero.
@@ -97,6 +99,8 @@ bandsolve_status make_pent_factor(const double* a, const double* b,
   f->gamma.assign(n, 0.0);
   f->delta.assign(n, 0.0);
   f->epsilon.assign(a, a + n);  // banded.cpp:137: epsilon is a verbatim copy of a
+  f->bands.reserve(5 * n);
+  for (const double* v : {a, b, c, d, e}) f->bands.insert(f->bands.end(), v, v + n);
   std::vector<double> alpha(n, 0.0);
   auto& be = f->beta;
   auto& ga = f->gamma;

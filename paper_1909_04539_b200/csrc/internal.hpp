@@ -29,6 +29,13 @@ struct DeviceFactor {
   const void* bwd[2][2] = {};
 };
 
+// Partitioned (SPIKE) solve plan for few long systems, cached per factor and
+// block count (partition.cu).
+struct PartPlan;
+struct PartPlanDeleter {
+  void operator()(PartPlan* p) const;
+};
+
 // Host factor: the reference's factor arrays, computed once on the host in
 // the reference's operation order (banded.cpp:67-86, :127-176,
 // pent_solver.cpp:99-111), plus a lazily filled per-device cache.
@@ -40,9 +47,13 @@ struct Factor {
   // pent_factor / uniform_pent_factor fields (banded.hpp:88-95)
   std::vector<double> inv_alpha, beta, gamma, delta, epsilon;
   double eps_scalar = 0.0;
+  // the bands the factor was built from (tri: sub|diag|sup, pent: a|b|c|d|e),
+  // for the partitioned path's block factors
+  std::vector<double> bands;
 
   mutable std::mutex mu;
   mutable std::vector<DeviceFactor> devices;  // one entry per touched device
+  mutable std::vector<std::unique_ptr<PartPlan, PartPlanDeleter>> parts;
   ~Factor();
 };
 
@@ -106,6 +117,12 @@ void set_mode(int mode);
 bandsolve_status solve_device(const Factor& f, void* x, bool f32,
                               std::size_t n, std::size_t m, std::size_t ld,
                               void* stream);
+// Partitioned fast-mode solve (partition.cu) for the few-long-systems regime;
+// BANDSOLVE_OK and *done = false when it does not apply (caller falls back).
+int partition_blocks(std::size_t n, std::size_t m, int sms, bool pent);  // 0 = not used
+bandsolve_status partition_solve_device(const Factor& f, double* x, std::size_t n,
+                                        std::size_t m, std::size_t ld,
+                                        void* stream, int sms, bool* done);
 // Host batch: staged through the device, synchronous. With `per`, the
 // periodic correction follows the sweep on each staged chunk; with
 // `correct_only`, only the correction runs.
@@ -150,6 +167,7 @@ bandsolve_status describe_plan(Kind kind, std::size_t n, std::size_t m,
                                std::size_t ld, bool f32, std::string& out);
 void release_device_factor(DeviceFactor& d);
 uint64_t kernel_launches();
+void note_launches(int k);
 
 // Page-locked host allocation when a driver is present, else calloc.
 double* host_alloc_zeroed(std::size_t count, bool* pinned);

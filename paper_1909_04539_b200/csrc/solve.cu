@@ -1033,6 +1033,7 @@ int current_mode() {
 }
 void set_mode(int mode) { g_mode.store(mode, std::memory_order_relaxed); }
 uint64_t kernel_launches() { return g_launches.load(std::memory_order_relaxed); }
+void note_launches(int k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 
 void release_device_factor(DeviceFactor& d) {
   if (!d.base) return;
@@ -1080,7 +1081,11 @@ bandsolve_status describe_plan(Kind kind, std::size_t n, std::size_t m, std::siz
   const bool fast = current_mode() == BANDSOLVE_MODE_FAST;
   const Plan p = choose_plan(n, m, ld, f32 ? 4 : 8, kProbe, pent, fast, sms);
   char buf[256];
-  if (p.kind == PlanKind::Regs)
+  const int K = f32 ? 0 : partition_blocks(n, m, sms, pent);
+  if (K > 0)
+    std::snprintf(buf, sizeof buf, "partition K=%d blocks of %zu rows, interface system %d (dense LU), 3 launches", K,
+                  n / K, (pent ? 4 : 2) * K);
+  else if (p.kind == PlanKind::Regs)
     std::snprintf(buf, sizeof buf, "regs Wg=%d warps=%d+1 nb=%d head(L2)=%d tail(smem)=%d smem=%zu B spill=%.1f MB",
                   p.Wg, p.warps, p.KB, p.H, static_cast<int>(n) - p.H, p.smem_bytes, p.model_us);
   else if (p.kind == PlanKind::Stream)
@@ -1119,6 +1124,11 @@ bandsolve_status solve_device(const Factor& f, void* x, bool f32, std::size_t n,
   auto s = static_cast<cudaStream_t>(stream);
   const int sms = num_sms(device);
   keep_pool_memory(device);
+  if (fast && !f32) {
+    bool done = false;
+    st = partition_solve_device(f, static_cast<double*>(x), n, m, ld, stream, sms, &done);
+    if (st != BANDSOLVE_OK || done) return st;
+  }
   const Plan plan = choose_plan(n, m, ld, f32 ? 4 : 8, x, pent, fast, sms);
   cudaError_t err;
   if (f32)
@@ -1291,12 +1301,14 @@ bandsolve_status periodic_device(const Periodic& p, double* x, std::size_t n, st
   if (m == 0) return BANDSOLVE_OK;
   if (device_count_cached() == 0) return fail(BANDSOLVE_ERR_INTERNAL, "no CUDA device available (no CPU fallback)");
   auto s = static_cast<cudaStream_t>(stream);
-  if (!correct_only && current_mode() == BANDSOLVE_MODE_FAST && std::getenv("BANDSOLVE_PERIODIC_UNFUSED") == nullptr) {
+  int device = 0;
+  BSB_CUDA(cudaGetDevice(&device));
+  const int sms = num_sms(device);
+  const bool pent = p.kind != Kind::Tri;
+  if (!correct_only && current_mode() == BANDSOLVE_MODE_FAST && std::getenv("BANDSOLVE_PERIODIC_UNFUSED") == nullptr &&
+      partition_blocks(n, m, sms, pent) == 0) {
     // fast mode: one fused pass (sweep_stream PER), when a streaming plan fits
-    int device = 0;
-    BSB_CUDA(cudaGetDevice(&device));
-    const int sms = num_sms(device);
-    const bool pent = p.kind != Kind::Tri;
+    // (few long systems take the partitioned sweep + correction instead)
     const bool aligned = (reinterpret_cast<uintptr_t>(x) % 16 == 0) && ((ld * sizeof(double)) % 16 == 0);
     Plan plan;
     if (aligned && n <= static_cast<std::size_t>(INT_MAX) && m <= static_cast<std::size_t>(INT_MAX) / 2 &&

@@ -248,17 +248,19 @@ __global__ void __launch_bounds__(W) sweep_smem(const __grid_constant__ CUtensor
 // U: rows per register block (two blocks in flight). U = 8 when many systems
 // share an SM; U = 32 for the few-long-systems regime (e.g. ADI axes), where
 // each thread alone must cover HBM latency with its own prefetch.
-template <typename T, bool PENT, bool FAST, int U = 8>
-__global__ void __launch_bounds__(128) sweep_global(T* __restrict__ x, int n, long long m,
-                                                    long long ld, const void* __restrict__ fwd,
-                                                    const void* __restrict__ bwd) {
-  const long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (j >= m) return;
-  T* col = x + j;
-  const Rows<T, PENT, FAST> rows{fwd, bwd};
+// One system's column in place: rows [0, n) at col[i*ld], factor records of
+// those rows at rows.fwd/rows.bwd index 0..n-1. The forward and backward
+// halves are separate so the partitioned path (partition.cu) can hook them:
+// `post(i, v)` sees each forward value; `pre(i, g)` adjusts each backward
+// input; s1/s2 carry the recurrence state in and out.
+struct NoHook {
+  template <typename T>
+  __device__ __forceinline__ T operator()(int, T v) const { return v; }
+};
 
-  // forward
-  T s1 = T(0), s2 = T(0);
+template <typename T, bool PENT, bool FAST, int U, typename Post = NoHook>
+__device__ __forceinline__ void column_forward(T* col, int n, long long ld, const Rows<T, PENT, FAST>& rows,
+                                               T& s1, T& s2, const Post& post = Post{}) {
   T cur[U], nxt[U];
   const int full = n / U;  // number of complete U-row blocks
   if (full > 0) {
@@ -274,6 +276,7 @@ __global__ void __launch_bounds__(128) sweep_global(T* __restrict__ x, int n, lo
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       cur[u] = rows.forward(i0 + u, cur[u], s1, s2);
+      post(i0 + u, cur[u]);
       col[static_cast<long long>(i0 + u) * ld] = cur[u];
     }
 #pragma unroll
@@ -281,15 +284,21 @@ __global__ void __launch_bounds__(128) sweep_global(T* __restrict__ x, int n, lo
   }
   for (int i = full * U; i < n; ++i) {
     T* p = col + static_cast<long long>(i) * ld;
-    *p = rows.forward(i, *p, s1, s2);
+    const T v = rows.forward(i, *p, s1, s2);
+    post(i, v);
+    *p = v;
   }
+}
 
-  // backward: the tail rows first (descending), then whole blocks
-  s1 = T(0);
-  s2 = T(0);
+// backward over rows [0, n): the tail rows first (descending), then whole blocks
+template <typename T, bool PENT, bool FAST, int U, typename Pre = NoHook>
+__device__ __forceinline__ void column_backward(T* col, int n, long long ld, const Rows<T, PENT, FAST>& rows,
+                                                T& s1, T& s2, const Pre& pre = Pre{}) {
+  T cur[U], nxt[U];
+  const int full = n / U;
   for (int i = n - 1; i >= full * U; --i) {
     T* p = col + static_cast<long long>(i) * ld;
-    *p = rows.backward(i, *p, s1, s2);
+    *p = rows.backward(i, pre(i, *p), s1, s2);
   }
   if (full > 0) {
     const int top = (full - 1) * U;
@@ -304,12 +313,30 @@ __global__ void __launch_bounds__(128) sweep_global(T* __restrict__ x, int n, lo
     }
 #pragma unroll
     for (int u = U - 1; u >= 0; --u) {
-      cur[u] = rows.backward(i0 + u, cur[u], s1, s2);
+      cur[u] = rows.backward(i0 + u, pre(i0 + u, cur[u]), s1, s2);
       col[static_cast<long long>(i0 + u) * ld] = cur[u];
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) cur[u] = nxt[u];
   }
+}
+
+template <typename T, bool PENT, bool FAST, int U>
+__device__ __forceinline__ void column_sweep(T* col, int n, long long ld, const Rows<T, PENT, FAST>& rows) {
+  T s1 = T(0), s2 = T(0);
+  column_forward<T, PENT, FAST, U>(col, n, ld, rows, s1, s2);
+  s1 = T(0);
+  s2 = T(0);
+  column_backward<T, PENT, FAST, U>(col, n, ld, rows, s1, s2);
+}
+
+template <typename T, bool PENT, bool FAST, int U = 8>
+__global__ void __launch_bounds__(128) sweep_global(T* __restrict__ x, int n, long long m,
+                                                    long long ld, const void* __restrict__ fwd,
+                                                    const void* __restrict__ bwd) {
+  const long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  column_sweep<T, PENT, FAST, U>(x + j, n, ld, Rows<T, PENT, FAST>{fwd, bwd});
 }
 
 }  // namespace dev

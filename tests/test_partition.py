@@ -1,0 +1,128 @@
+"""Partitioned (SPIKE) fast-mode path for few long systems (csrc/partition.cu).
+
+Fast mode promises the reference's answer within a per-system max-norm
+relative error of 1e-12; the partitioned path reorders the
+arithmetic (block sweeps + a dense interface solve + spike update), so it is
+held to that same bound against the oracle, over ragged block splits, padded
+pitches and every band structure. BANDSOLVE_PARTITION=1 forces the path even
+where the planner would not pick it; =0 disables it.
+"""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+from oracle.oracle import per_system_max_rel
+from paper_1909_04539_b200 import bandsolve as bs
+
+pytestmark = pytest.mark.gpu
+
+TOL_F64 = 1e-12
+
+
+def _random_tri(rng, n):
+    sub = rng.uniform(-1, 1, n); sub[0] = 0
+    sup = rng.uniform(-1, 1, n); sup[-1] = 0
+    diag = np.abs(sub) + np.abs(sup) + rng.uniform(0.5, 1.5, n)
+    return sub, diag, sup
+
+
+def _random_pent(rng, n):
+    a = rng.uniform(-1, 1, n); a[:2] = 0
+    b = rng.uniform(-1, 1, n); b[0] = 0
+    d = rng.uniform(-1, 1, n); d[-1] = 0
+    e = rng.uniform(-1, 1, n); e[-2:] = 0
+    c = np.abs(a) + np.abs(b) + np.abs(d) + np.abs(e) + rng.uniform(0.5, 1.5, n)
+    return a, b, c, d, e
+
+
+@pytest.fixture(autouse=True)
+def _fast_mode(lib):
+    lib.set_mode(bs.MODE_FAST)
+    os.environ.pop("BANDSOLVE_PLAN", None)
+    yield
+    lib.set_mode(bs.MODE_EXACT)
+    os.environ.pop("BANDSOLVE_PARTITION", None)
+
+
+def _dev_solve(torch, factor, rhs, ld=None):
+    n, m = rhs.shape
+    ld = m if ld is None else ld
+    buf = torch.full((n, ld), float("nan"), dtype=torch.float64, device="cuda")
+    buf[:, :m] = torch.from_numpy(rhs).cuda()
+    factor.solve_dev(buf.data_ptr(), n, m, ld=ld, stream=torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    out = buf.cpu().numpy()
+    if ld > m:
+        assert np.all(np.isnan(out[:, m:]))
+    return out[:, :m]
+
+
+@pytest.mark.parametrize("forced", ["1", None])
+def test_partition_within_tolerance(lib, oracle, cuda_device, forced):
+    torch = cuda_device
+    if forced:
+        os.environ["BANDSOLVE_PARTITION"] = forced
+    rng = np.random.default_rng(77)
+    for n, m in [(128, 5), (200, 33), (1000, 64), (1023, 257), (4096, 128), (4099, 96)]:
+        rhs = rng.uniform(-1, 1, (n, m))
+        tb = _random_tri(rng, n)
+        want = oracle.tri_solve(oracle.tri_prefactor(*tb), rhs.copy())
+        for ld in (m, m + 3):
+            got = _dev_solve(torch, bs.TriFactor(lib, *tb), rhs, ld)
+            assert per_system_max_rel(got, want) <= TOL_F64, ("tri", n, m, ld)
+        db = bs.diffusion_bands(1.0, n)
+        want = oracle.tri_solve(oracle.tri_prefactor(*db), rhs.copy())
+        assert per_system_max_rel(_dev_solve(torch, bs.TriFactor(lib, *db), rhs), want) <= TOL_F64, ("diff", n)
+        pb = _random_pent(rng, n)
+        want = oracle.pent_solve(oracle.pent_prefactor(*pb), rhs.copy())
+        for ld in (m, m + 1):
+            got = _dev_solve(torch, bs.PentFactor(lib, *pb), rhs, ld)
+            assert per_system_max_rel(got, want) <= TOL_F64, ("pent", n, m, ld)
+        hb = bs.hyper_bands(1.0, n)
+        want = oracle.pent_solve(oracle.pent_prefactor(*hb), rhs.copy())
+        assert per_system_max_rel(_dev_solve(torch, bs.PentFactor(lib, *hb), rhs), want) <= TOL_F64, ("hyper", n)
+        u = bs.UniformPentFactor(lib, 1.0, -4.0, 7.0, -4.0, 1.0, n)
+        want = oracle.pent_solve(oracle.uniform_prefactor(1.0, -4.0, 7.0, -4.0, 1.0, n), rhs.copy())
+        assert per_system_max_rel(_dev_solve(torch, u, rhs), want) <= TOL_F64, ("uniform", n)
+
+
+def test_partition_long_systems_three_launches(lib, oracle, cuda_device):
+    """Few long systems (an ADI axis: 4096-row systems) take the partitioned
+    path: three launches (block forward sweeps, interface solve, block
+    backward sweeps)."""
+    torch = cuda_device
+    n, m = 4096, 1024
+    bands = bs.diffusion_bands(1.0, n)
+    f = bs.TriFactor(lib, *bands)
+    x = torch.empty((n, m), dtype=torch.float64, device="cuda")
+    lib.fill_rhs_dev(x.data_ptr(), n, m, m, seed=42)
+    rhs = x.clone()
+    f.solve_dev(x.data_ptr(), n, m)  # warm (plan + upload)
+    torch.cuda.synchronize()
+    x.copy_(rhs)
+    before = lib.kernel_launches()
+    f.solve_dev(x.data_ptr(), n, m)
+    torch.cuda.synchronize()
+    assert lib.kernel_launches() - before == 3
+    res = lib.tri_residual_dev(*bands, x.data_ptr(), rhs.data_ptr(), m, m)
+    assert 0.0 <= res <= TOL_F64, res
+    cols = np.arange(0, m, 17)
+    want = oracle.tri_solve(oracle.tri_prefactor(*bands), rhs.cpu().numpy()[:, cols].copy())
+    assert per_system_max_rel(x.cpu().numpy()[:, cols], want) <= TOL_F64
+
+
+def test_partition_disabled_matches_sequential(lib, oracle, cuda_device):
+    torch = cuda_device
+    rng = np.random.default_rng(5)
+    n, m = 512, 200
+    pb = _random_pent(rng, n)
+    rhs = rng.uniform(-1, 1, (n, m))
+    f = bs.PentFactor(lib, *pb)
+    os.environ["BANDSOLVE_PARTITION"] = "1"
+    part = _dev_solve(torch, f, rhs)
+    os.environ["BANDSOLVE_PARTITION"] = "0"
+    seq = _dev_solve(torch, f, rhs)
+    assert per_system_max_rel(part, seq) <= TOL_F64
