@@ -119,10 +119,17 @@ bandsolve_status solve_device(const Factor& f, void* x, bool f32,
                               void* stream);
 // Partitioned fast-mode solve (partition.cu) for the few-long-systems regime;
 // BANDSOLVE_OK and *done = false when it does not apply (caller falls back).
+// With `per`, the periodic (Woodbury) correction is fused into the last pass.
+struct PartPeriodic {
+  const double* z1;
+  const double* z2;
+  double c[4];  // tri: v_last, scale; pent: cap_inv
+};
 int partition_blocks(std::size_t n, std::size_t m, int sms, bool pent);  // 0 = not used
 bandsolve_status partition_solve_device(const Factor& f, double* x, std::size_t n,
                                         std::size_t m, std::size_t ld,
-                                        void* stream, int sms, bool* done);
+                                        void* stream, int sms, bool* done,
+                                        const PartPeriodic* per = nullptr);
 // Host batch: staged through the device, synchronous. With `per`, the
 // periodic correction follows the sweep on each staged chunk; with
 // `correct_only`, only the correction runs.

@@ -13,18 +13,21 @@
 //   A_k^-1 (coupling columns) (tri: 2, pent: 4 vectors of n).
 //   x_k = y_k - W_k x_(left interface) - V_k x_(right interface), so the 2K
 //   (tri) / 4K (pent) interface unknowns satisfy one dense R x R system whose
-//   matrix is shared: its LU (partial pivoting) is precomputed.
+//   matrix is shared: its inverse is precomputed (LU with partial pivoting).
 //
-// Device passes (4 HBM passes over the batch, like an off-chip sequential
+// Two launches, 4 HBM passes over the batch (like an off-chip sequential
 // sweep): (A) K*m independent block forward sweeps (thread per block-system,
 // deep register prefetch) that also emit the block's interface values of y =
 // A_k^-1 b_k -- the bottom ones are forward values, the top ones dot products
-// of the forward values with precomputed rows of the block's U^-1; (B) per
-// system, the R x R interface solve (LU in smem, banded loops); (C) K*m block
-// backward sweeps that start from the block's own solved bottom values and
-// fold the left-neighbour coupling in as g_i - F_i x_left (F = the forward
-// image of the coupling column). Arithmetic differs from the sequential sweep
-// by rounding only (fast mode, 1e-12).
+// of the forward values with precomputed rows of the block's U^-1; (B) K*m
+// block backward sweeps: each thread first forms the interface values it
+// needs (its own bottom rows and its left neighbour's) as rows of R^-1 times
+// the system's y interface vector (R independent FMAs, L2-resident), then
+// sweeps up from its own bottom values, folding the left coupling in as
+// g_i - F_i x_left (F = the forward image of the coupling column). A periodic
+// (Woodbury) correction fuses into (B): its coefficients need only x_0, x_1,
+// x_{n-2}, x_{n-1}, which are interface unknowns. Arithmetic differs from the
+// sequential sweep by rounding only (fast mode, 1e-12).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -46,8 +49,8 @@ struct PartPlan {
   std::vector<double> fwd, bwd;            // packed fast records, one per row (block-local factors)
   std::vector<double> fl;                  // forward images of the left coupling (tri: F, pent: F1 | F2)
   std::vector<double> pr;                  // rows of the block U^-1 (tri: P0, pent: P0 | P1)
-  std::vector<double> lu;                  // R x R, row-major, L unit-lower + U
-  std::vector<int> perm;                   // row permutation of the LU | row lo | row hi
+  std::vector<double> rinv;                // R x R inverse of the interface matrix, row-major
+  bool ok = false;                         // false: the plan broke down (sequential sweep instead)
   std::vector<std::pair<int, void*>> dev;  // device blobs
   ~PartPlan() {
     for (auto& d : dev) {
@@ -63,7 +66,7 @@ void PartPlanDeleter::operator()(PartPlan* p) const { delete p; }
 
 namespace {
 
-constexpr int kPartMaxR = 64;  // reduced-system order cap: the LU (32 KB) lives in smem
+constexpr int kPartMaxR = 64;  // interface-system order cap (R^-1 rows read per thread)
 
 // block factor forward / backward (any rounding: fast path), in place
 void tri_block_fwd(const Factor& f, double* v) {
@@ -147,7 +150,7 @@ std::unique_ptr<PartPlan, PartPlanDeleter> build_plan(const Factor& f, int K) {
       st = make_pent_factor(bb[0].data(), bb[1].data(), bb[2].data(), bb[3].data(), bb[4].data(), Lk, fb);
     }
     clear_error();
-    if (st != BANDSOLVE_OK) return nullptr;
+    if (st != BANDSOLVE_OK) return p;
     // packed fast records (same layout as solve.cu pack_*: fwd {a m, m} /
     // {e ia, b ia, ia, 0}; bwd chat / {gamma, delta})
     for (int i = 0; i < Lk; ++i) {
@@ -230,21 +233,30 @@ std::unique_ptr<PartPlan, PartPlanDeleter> build_plan(const Factor& f, int K) {
       }
     }
   }
-  if (!(worst < 1e100)) return nullptr;  // growth: leave it to the sequential sweep
-  if (!lu_factor(R, p->perm, p->R)) return nullptr;
-  // per-row extent of the (block-banded) factors: the solves skip exact zeros
+  if (!(worst < 1e100)) return p;  // growth: leave it to the sequential sweep
   const int r = p->R;
-  p->perm.resize(3 * r);
-  for (int i = 0; i < r; ++i) {
-    int lo = i, hi = i;
-    for (int c = 0; c < i; ++c)
-      if (R[static_cast<std::size_t>(i) * r + c] != 0.0) { lo = c; break; }
-    for (int c = r - 1; c > i; --c)
-      if (R[static_cast<std::size_t>(i) * r + c] != 0.0) { hi = c; break; }
-    p->perm[r + i] = lo;
-    p->perm[2 * r + i] = hi;
+  std::vector<int> perm;
+  if (!lu_factor(R, perm, r)) return p;
+  // R^-1 column by column: P A = L U  =>  A^-1 e_c = U^-1 L^-1 P e_c
+  p->rinv.assign(static_cast<std::size_t>(r) * r, 0.0);
+  std::vector<double> w(r);
+  for (int c = 0; c < r; ++c) {
+    for (int i = 0; i < r; ++i) {
+      double v = perm[i] == c ? 1.0 : 0.0;
+      for (int q = 0; q < i; ++q) v -= R[static_cast<std::size_t>(i) * r + q] * w[q];
+      w[i] = v;
+    }
+    for (int i = r - 1; i >= 0; --i) {
+      double v = w[i];
+      for (int q = i + 1; q < r; ++q) v -= R[static_cast<std::size_t>(i) * r + q] * w[q];
+      w[i] = v / R[static_cast<std::size_t>(i) * r + i];
+    }
+    for (int i = 0; i < r; ++i) {
+      p->rinv[static_cast<std::size_t>(i) * r + c] = w[i];
+      if (!(std::abs(w[i]) < 1e100)) return p;
+    }
   }
-  p->lu = std::move(R);
+  p->ok = true;
   return p;
 }
 
@@ -293,37 +305,6 @@ __global__ void __launch_bounds__(128) part_fwd_kernel(double* __restrict__ x, i
 }
 
 template <bool PENT>
-__global__ void part_reduce_kernel(int K, long long m, const double* __restrict__ lu_g,
-                                   const int* __restrict__ idx_g, double* __restrict__ z) {
-  extern __shared__ double sm[];
-  constexpr int NQ = PENT ? 4 : 2;
-  const int R = NQ * K;
-  double* lu = sm;
-  int* idx = reinterpret_cast<int*>(sm + R * R);  // perm | lo | hi
-  for (int t = threadIdx.x; t < R * R; t += blockDim.x) lu[t] = lu_g[t];
-  for (int t = threadIdx.x; t < 3 * R; t += blockDim.x) idx[t] = idx_g[t];
-  __syncthreads();
-  const long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (j >= m) return;
-  // interface values of y in pivot order, then P A = L U; z overwrites y in place
-  double w[kPartMaxR];
-  for (int i = 0; i < R; ++i) w[i] = z[static_cast<long long>(idx[i]) * m + j];
-  const int* lo = idx + R;
-  const int* hi = idx + 2 * R;
-  for (int i = 0; i < R; ++i) {
-    double v = w[i];
-    for (int c = lo[i]; c < i; ++c) v = fma(-lu[i * R + c], w[c], v);
-    w[i] = v;
-  }
-  for (int i = R - 1; i >= 0; --i) {
-    double v = w[i];
-    for (int c = i + 1; c <= hi[i]; ++c) v = fma(-lu[i * R + c], w[c], v);
-    w[i] = v / lu[i * R + i];
-  }
-  for (int i = 0; i < R; ++i) z[static_cast<long long>(i) * m + j] = w[i];
-}
-
-template <bool PENT>
 struct LeftHook {  // g_i - F_i x_left (the left-neighbour coupling's forward image)
   const double* f1;
   const double* f2;
@@ -335,37 +316,96 @@ struct LeftHook {  // g_i - F_i x_left (the left-neighbour coupling's forward im
 };
 
 template <bool PENT>
+struct CorrHook {  // stores x_i - (z1_i t1 + z2_i t2)
+  const double* z1;
+  const double* z2;
+  double t1, t2;
+  __device__ __forceinline__ double operator()(int i, double v) const {
+    if constexpr (PENT) return fma(-z1[i], t1, fma(-z2[i], t2, v));
+    else return fma(-z1[i], t1, v);
+  }
+};
+
+template <bool PENT, bool PER>
 __global__ void __launch_bounds__(128) part_bwd_kernel(double* __restrict__ x, int n, long long m, long long ld,
                                                        int K, int L, const double* __restrict__ fwd,
                                                        const double* __restrict__ bwd,
-                                                       const double* __restrict__ fl, const double* __restrict__ z) {
+                                                       const double* __restrict__ fl,
+                                                       const double* __restrict__ rinv,
+                                                       const double* __restrict__ yi, PartPeriodic per) {
   const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= static_cast<long long>(K) * m) return;
   const int k = static_cast<int>(t / m);
   const long long j = t - static_cast<long long>(k) * m;
   const int r0 = k * L;
   const int len = k + 1 < K ? L : n - r0;
+  constexpr int NQ = PENT ? 4 : 2;
+  constexpr int NH = NQ / 2;  // bottom interface rows per block
+  const int R = NQ * K;
+  // interface values: [own bottom NH | left bottom NH | (PER) global first NH | global last NH]
+  constexpr int NU = PER ? 4 * NH : 2 * NH;
+  int rowsel[NU];
+#pragma unroll
+  for (int h = 0; h < NH; ++h) {
+    rowsel[h] = NQ * k + NH + h;
+    rowsel[NH + h] = k > 0 ? NQ * k - NH + h : NQ * k + NH + h;  // (unused when k == 0)
+    if constexpr (PER) {
+      rowsel[2 * NH + h] = h;
+      rowsel[3 * NH + h] = R - NH + h;
+    }
+  }
+  double zu[NU];
+#pragma unroll
+  for (int u = 0; u < NU; ++u) zu[u] = 0.0;
+  for (int c = 0; c < R; ++c) {
+    const double y = yi[static_cast<long long>(c) * m + j];
+#pragma unroll
+    for (int u = 0; u < NU; ++u) zu[u] = fma(__ldg(rinv + rowsel[u] * R + c), y, zu[u]);
+  }
   const dev::Rows<double, PENT, true> rows{fwd + static_cast<long long>(r0) * (PENT ? 4 : 2),
                                            bwd + static_cast<long long>(r0) * (PENT ? 2 : 1)};
   double* col = x + static_cast<long long>(r0) * ld + j;
-  constexpr int NQ = PENT ? 4 : 2;
   LeftHook<PENT> hook{fl + r0, fl + n + r0, 0.0, 0.0};
+  if (k > 0) {
+    if constexpr (PENT) {
+      hook.xl2 = zu[2];  // x_{s-2}
+      hook.xl1 = zu[3];  // x_{s-1}
+    } else {
+      hook.xl1 = zu[1];  // x_{s-1}
+    }
+  }
+  CorrHook<PENT> corr{per.z1 + r0, per.z2 + r0, 0.0, 0.0};
+  if constexpr (PER) {
+    if constexpr (PENT) {  // periodic.cpp:189-194 (fast-mode rounding)
+      const double w1 = zu[4] - zu[7], w2 = zu[5] - zu[6];
+      corr.t1 = fma(per.c[0], w1, per.c[1] * w2);
+      corr.t2 = fma(per.c[2], w1, per.c[3] * w2);
+    } else {  // periodic.cpp:80
+      corr.t1 = fma(per.c[0], zu[3], zu[2]) * per.c[1];
+    }
+  }
   double s1, s2 = 0.0;
   if constexpr (PENT) {
-    if (k > 0) {
-      hook.xl2 = z[static_cast<long long>(NQ * k - 2) * m + j];  // x_{s-2}
-      hook.xl1 = z[static_cast<long long>(NQ * k - 1) * m + j];  // x_{s-1}
+    s1 = zu[0];  // own rows L-2, L-1
+    s2 = zu[1];
+    if constexpr (PER) {
+      col[static_cast<long long>(len - 2) * ld] = corr(len - 2, s1);
+      col[static_cast<long long>(len - 1) * ld] = corr(len - 1, s2);
+      dev::column_backward<double, PENT, true, kPartU>(col, len - 2, ld, rows, s1, s2, hook, corr);
+    } else {
+      col[static_cast<long long>(len - 2) * ld] = s1;
+      col[static_cast<long long>(len - 1) * ld] = s2;
+      dev::column_backward<double, PENT, true, kPartU>(col, len - 2, ld, rows, s1, s2, hook);
     }
-    s1 = z[static_cast<long long>(NQ * k + 2) * m + j];  // own rows L-2, L-1
-    s2 = z[static_cast<long long>(NQ * k + 3) * m + j];
-    col[static_cast<long long>(len - 2) * ld] = s1;
-    col[static_cast<long long>(len - 1) * ld] = s2;
-    dev::column_backward<double, PENT, true, kPartU>(col, len - 2, ld, rows, s1, s2, hook);
   } else {
-    if (k > 0) hook.xl1 = z[static_cast<long long>(NQ * k - 1) * m + j];
-    s1 = z[static_cast<long long>(NQ * k + 1) * m + j];  // own row L-1
-    col[static_cast<long long>(len - 1) * ld] = s1;
-    dev::column_backward<double, PENT, true, kPartU>(col, len - 1, ld, rows, s1, s2, hook);
+    s1 = zu[0];  // own row L-1
+    if constexpr (PER) {
+      col[static_cast<long long>(len - 1) * ld] = corr(len - 1, s1);
+      dev::column_backward<double, PENT, true, kPartU>(col, len - 1, ld, rows, s1, s2, hook, corr);
+    } else {
+      col[static_cast<long long>(len - 1) * ld] = s1;
+      dev::column_backward<double, PENT, true, kPartU>(col, len - 1, ld, rows, s1, s2, hook);
+    }
   }
 }
 
@@ -380,7 +420,9 @@ int partition_blocks(std::size_t n, std::size_t m, int sms, bool pent) {
   // few systems only: below ~one warp of systems per SM the sweep is latency-bound
   // (short systems: three launches cost more than the latency they hide)
   if (!forced && (m > static_cast<std::size_t>(sms) * 64 || n < 1024)) return 0;
-  const int kmax = kPartMaxR / (pent ? 4 : 2);
+  // pent: each backward thread forms 8 interface values from R^-1 rows, so a
+  // smaller interface system (K <= 8) wins over more blocks (measured)
+  const int kmax = pent ? 8 : kPartMaxR / 2;
   const char* ke = std::getenv("BANDSOLVE_PART_K");  // tuning override (power of two)
   if (ke && std::atoi(ke) >= 2 && std::atoi(ke) <= kmax && static_cast<int>(n) / std::atoi(ke) >= 16)
     return std::atoi(ke);
@@ -392,7 +434,7 @@ int partition_blocks(std::size_t n, std::size_t m, int sms, bool pent) {
 }
 
 bandsolve_status partition_solve_device(const Factor& f, double* x, std::size_t n, std::size_t m, std::size_t ld,
-                                        void* stream, int sms, bool* done) {
+                                        void* stream, int sms, bool* done, const PartPeriodic* per) {
   *done = false;
   const bool pent = f.kind != Kind::Tri;
   const int K = partition_blocks(n, m, sms, pent);
@@ -411,25 +453,29 @@ bandsolve_status partition_solve_device(const Factor& f, double* x, std::size_t 
       if (q && q->K == K) p = q.get();
     if (!p) {
       auto q = build_plan(f, K);
-      if (!q) return BANDSOLVE_OK;  // a block pivot broke down: the sequential sweep handles it
+      if (!q) return BANDSOLVE_OK;
       p = q.get();
       f.parts.push_back(std::move(q));
     }
+    if (!p->ok) return BANDSOLVE_OK;  // a block pivot broke down or grew: the sequential sweep handles it
     for (auto& d : p->dev)
       if (d.first == device) blob = d.second;
     if (!blob) {
-      const std::size_t bytes = (p->fwd.size() + p->bwd.size() + p->fl.size() + p->pr.size() + p->lu.size()) * sizeof(double) +
-                                p->perm.size() * sizeof(int);
+      const std::size_t bytes =
+          (p->fwd.size() + p->bwd.size() + p->fl.size() + p->pr.size() + p->rinv.size()) * sizeof(double);
       if (cudaMalloc(&blob, bytes) != cudaSuccess) {
         cudaGetLastError();
         return fail(BANDSOLVE_ERR_INTERNAL, "partition plan upload");
       }
       char* c = static_cast<char*>(blob);
-      for (const auto* v : {&p->fwd, &p->bwd, &p->fl, &p->pr, &p->lu}) {
-        cudaMemcpy(c, v->data(), v->size() * sizeof(double), cudaMemcpyHostToDevice);
+      for (const auto* v : {&p->fwd, &p->bwd, &p->fl, &p->pr, &p->rinv}) {
+        if (cudaMemcpy(c, v->data(), v->size() * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess) {
+          cudaGetLastError();
+          cudaFree(blob);
+          return fail(BANDSOLVE_ERR_INTERNAL, "partition plan upload");
+        }
         c += v->size() * sizeof(double);
       }
-      cudaMemcpy(c, p->perm.data(), p->perm.size() * sizeof(int), cudaMemcpyHostToDevice);
       p->dev.emplace_back(device, blob);
     }
   }
@@ -437,32 +483,30 @@ bandsolve_status partition_solve_device(const Factor& f, double* x, std::size_t 
   const double* bwd = fwd + p->fwd.size();
   const double* fl = bwd + p->bwd.size();
   const double* pr = fl + p->fl.size();
-  const double* lu = pr + p->pr.size();
-  const int* idx = reinterpret_cast<const int*>(lu + p->lu.size());
+  const double* rinv = pr + p->pr.size();
   auto s = static_cast<cudaStream_t>(stream);
   const int N = static_cast<int>(n);
   const long long M = static_cast<long long>(m), LD = static_cast<long long>(ld);
-  double* z = nullptr;
-  if (cudaMallocAsync(reinterpret_cast<void**>(&z), static_cast<std::size_t>(p->R) * m * sizeof(double), s) !=
+  double* yi = nullptr;  // interface values of y, [R][m]
+  if (cudaMallocAsync(reinterpret_cast<void**>(&yi), static_cast<std::size_t>(p->R) * m * sizeof(double), s) !=
       cudaSuccess) {
     cudaGetLastError();
     return fail(BANDSOLVE_ERR_INTERNAL, "partition scratch");
   }
   const long long tot = static_cast<long long>(K) * M;
   const unsigned g1 = static_cast<unsigned>((tot + 127) / 128);
-  const unsigned gj = static_cast<unsigned>((M + 127) / 128);
-  const std::size_t red_smem = static_cast<std::size_t>(p->R) * p->R * sizeof(double) + 3 * p->R * sizeof(int);
+  const PartPeriodic pa = per ? *per : PartPeriodic{};
   if (pent) {
-    part_fwd_kernel<true><<<g1, 128, 0, s>>>(x, N, M, LD, K, p->L, fwd, bwd, pr, z);
-    part_reduce_kernel<true><<<gj, 128, red_smem, s>>>(K, M, lu, idx, z);
-    part_bwd_kernel<true><<<g1, 128, 0, s>>>(x, N, M, LD, K, p->L, fwd, bwd, fl, z);
+    part_fwd_kernel<true><<<g1, 128, 0, s>>>(x, N, M, LD, K, p->L, fwd, bwd, pr, yi);
+    if (per) part_bwd_kernel<true, true><<<g1, 128, 0, s>>>(x, N, M, LD, K, p->L, fwd, bwd, fl, rinv, yi, pa);
+    else part_bwd_kernel<true, false><<<g1, 128, 0, s>>>(x, N, M, LD, K, p->L, fwd, bwd, fl, rinv, yi, pa);
   } else {
-    part_fwd_kernel<false><<<g1, 128, 0, s>>>(x, N, M, LD, K, p->L, fwd, bwd, pr, z);
-    part_reduce_kernel<false><<<gj, 128, red_smem, s>>>(K, M, lu, idx, z);
-    part_bwd_kernel<false><<<g1, 128, 0, s>>>(x, N, M, LD, K, p->L, fwd, bwd, fl, z);
+    part_fwd_kernel<false><<<g1, 128, 0, s>>>(x, N, M, LD, K, p->L, fwd, bwd, pr, yi);
+    if (per) part_bwd_kernel<false, true><<<g1, 128, 0, s>>>(x, N, M, LD, K, p->L, fwd, bwd, fl, rinv, yi, pa);
+    else part_bwd_kernel<false, false><<<g1, 128, 0, s>>>(x, N, M, LD, K, p->L, fwd, bwd, fl, rinv, yi, pa);
   }
-  note_launches(3);
-  cudaFreeAsync(z, s);
+  note_launches(2);
+  cudaFreeAsync(yi, s);
   if (cudaError_t e = cudaGetLastError(); e != cudaSuccess)
     return fail(BANDSOLVE_ERR_INTERNAL, std::string("partition launch: ") + cudaGetErrorString(e));
   *done = true;

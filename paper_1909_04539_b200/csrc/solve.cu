@@ -970,21 +970,41 @@ __global__ void cn_rhs_kernel(const double* __restrict__ u, double* __restrict__
   }
 }
 
-// ---- tiled transpose for the ADI x-sweeps -------------------------------------
-// out[c * ldo + r] = in[r * ldi + c], 32 x 32 tiles through padded smem so
-// both the reads and the writes are coalesced.
-__global__ void transpose_kernel(const double* __restrict__ in, double* __restrict__ out, int rows, int cols,
-                                 long long ldi, long long ldo) {
-  __shared__ double tile[32][33];
+// ---- fused stencil + transpose for the ADI half steps ---------------------------
+// out[c * ldo + r] = stencil_r(u)[r][c]: the periodic Crank-Nicolson explicit
+// half along rows (same operation order as cn_rhs_kernel) written transposed,
+// so the next implicit half sweeps the other axis with its systems
+// interleaved. One read of u (32 x 32 tile + 2-row halos through smem) and one
+// write of out per element instead of stencil and transpose as two passes.
+template <bool PENT>
+__global__ void cn_rhs_transpose_kernel(const double* __restrict__ u, double* __restrict__ out, int rows, int cols,
+                                        long long ldi, long long ldo, double s, double s4, double mid) {
+  using namespace dev;
+  constexpr int H = PENT ? 2 : 1;
+  __shared__ double tile[32 + 2 * H][33];
   const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
-  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
-    const int r = r0 + k, c = c0 + threadIdx.x;
-    if (r < rows && c < cols) tile[k][threadIdx.x] = in[static_cast<long long>(r) * ldi + c];
+  for (int k = threadIdx.y; k < 32 + 2 * H; k += blockDim.y) {
+    int r = r0 + k - H;
+    r = r < 0 ? r + rows : (r >= rows ? r - rows : r);  // periodic rows (|offset| <= 2 < rows)
+    const int c = c0 + threadIdx.x;
+    if (r0 + k - H < rows + H && c < cols) tile[k][threadIdx.x] = u[static_cast<long long>(r) * ldi + c];
   }
   __syncthreads();
+  const int x = threadIdx.x;  // tile row r0 + x
+  const int r = r0 + x;
+  if (r >= rows) return;
   for (int k = threadIdx.y; k < 32; k += blockDim.y) {
-    const int c = c0 + k, r = r0 + threadIdx.x;
-    if (r < rows && c < cols) out[static_cast<long long>(c) * ldo + r] = tile[threadIdx.x][k];
+    const int c = c0 + k;
+    if (c >= cols) break;
+    const double* t = &tile[x + H][k];
+    double o;
+    if constexpr (!PENT) {
+      o = add_rn(mul_rn(s, add_rn(t[-33], t[33])), mul_rn(mid, t[0]));
+    } else {
+      const double q = add_rn(mul_rn(-s, add_rn(t[-66], t[66])), mul_rn(s4, add_rn(t[-33], t[33])));
+      o = add_rn(q, mul_rn(mid, t[0]));
+    }
+    out[static_cast<long long>(c) * ldo + r] = o;
   }
 }
 
@@ -1083,7 +1103,7 @@ bandsolve_status describe_plan(Kind kind, std::size_t n, std::size_t m, std::siz
   char buf[256];
   const int K = f32 ? 0 : partition_blocks(n, m, sms, pent);
   if (K > 0)
-    std::snprintf(buf, sizeof buf, "partition K=%d blocks of %zu rows, interface system %d (dense LU), 3 launches", K,
+    std::snprintf(buf, sizeof buf, "partition K=%d blocks of %zu rows, interface system %d (dense LU), 2 launches", K,
                   n / K, (pent ? 4 : 2) * K);
   else if (p.kind == PlanKind::Regs)
     std::snprintf(buf, sizeof buf, "regs Wg=%d warps=%d+1 nb=%d head(L2)=%d tail(smem)=%d smem=%zu B spill=%.1f MB",
@@ -1305,8 +1325,25 @@ bandsolve_status periodic_device(const Periodic& p, double* x, std::size_t n, st
   BSB_CUDA(cudaGetDevice(&device));
   const int sms = num_sms(device);
   const bool pent = p.kind != Kind::Tri;
-  if (!correct_only && current_mode() == BANDSOLVE_MODE_FAST && std::getenv("BANDSOLVE_PERIODIC_UNFUSED") == nullptr &&
-      partition_blocks(n, m, sms, pent) == 0) {
+  const bool fuse = !correct_only && current_mode() == BANDSOLVE_MODE_FAST &&
+                    std::getenv("BANDSOLVE_PERIODIC_UNFUSED") == nullptr;
+  if (fuse && partition_blocks(n, m, sms, pent) > 0) {
+    // few long systems: partitioned sweep with the correction fused into its last pass
+    const double* blob = nullptr;
+    bandsolve_status st = periodic_device_z(p, device, &blob);
+    if (st != BANDSOLVE_OK) return st;
+    PartPeriodic pa{blob, blob + n, {0.0, 0.0, 0.0, 0.0}};
+    if (pent) {
+      for (int k = 0; k < 4; ++k) pa.c[k] = p.cap_inv[k];
+    } else {
+      pa.c[0] = p.v_last;
+      pa.c[1] = p.scale;
+    }
+    bool done = false;
+    st = partition_solve_device(*p.factor, x, n, m, ld, stream, sms, &done, &pa);
+    if (st != BANDSOLVE_OK || done) return st;
+  }
+  if (fuse && partition_blocks(n, m, sms, pent) == 0) {
     // fast mode: one fused pass (sweep_stream PER), when a streaming plan fits
     // (few long systems take the partitioned sweep + correction instead)
     const bool aligned = (reinterpret_cast<uintptr_t>(x) % 16 == 0) && ((ld * sizeof(double)) % 16 == 0);
@@ -1521,34 +1558,40 @@ bandsolve_status adi_step_device(const Periodic& px, const Periodic& py, double 
   auto s = static_cast<cudaStream_t>(stream);
   const bool pent = px.kind != Kind::Tri;
   const std::size_t ldt = (ny + 1) & ~std::size_t(1);  // transposed pitch (even: TMA plans)
-  double *t1 = nullptr, *t2 = nullptr;
+  double* t1 = nullptr;
   BSB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&t1), nx * ldt * sizeof(double), s));
-  cudaError_t err = cudaMallocAsync(reinterpret_cast<void**>(&t2), nx * ldt * sizeof(double), s);
-  if (err != cudaSuccess) {
-    cudaFreeAsync(t1, s);
-    return cuda_fail(err, "ADI scratch");
-  }
-  auto transpose = [&](const double* in, double* out, std::size_t rows, std::size_t cols, std::size_t ldi,
-                       std::size_t ldo) {
+  (void)work;  // scratch kept in the ABI; the fused stencil+transpose needs only t1
+  // pde.cpp:80-81 / :101-103: the coefficients are formed once on the host
+  const double cs = sigma, cs4 = pent ? 4.0 * sigma : 0.0, cmid = pent ? 1.0 - 6.0 * sigma : 1.0 - 2.0 * sigma;
+  auto rhs_t = [&](const double* in, double* out, std::size_t rows, std::size_t cols, std::size_t ldi,
+                   std::size_t ldo) {
     dim3 block(32, 8), grid(static_cast<unsigned>((cols + 31) / 32), static_cast<unsigned>((rows + 31) / 32));
-    transpose_kernel<<<grid, block, 0, s>>>(in, out, static_cast<int>(rows), static_cast<int>(cols),
-                                            static_cast<long long>(ldi), static_cast<long long>(ldo));
+    if (pent)
+      cn_rhs_transpose_kernel<true><<<grid, block, 0, s>>>(in, out, static_cast<int>(rows), static_cast<int>(cols),
+                                                           static_cast<long long>(ldi), static_cast<long long>(ldo),
+                                                           cs, cs4, cmid);
+    else
+      cn_rhs_transpose_kernel<false><<<grid, block, 0, s>>>(in, out, static_cast<int>(rows), static_cast<int>(cols),
+                                                            static_cast<long long>(ldi), static_cast<long long>(ldo),
+                                                            cs, cs4, cmid);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return cudaGetLastError();
   };
   bandsolve_status st = BANDSOLVE_OK;
+  cudaError_t err;
   do {
-    // half step 1: explicit along y, implicit along x
-    if ((st = cn_rhs_device(pent, sigma, field, work, ny, nx, ld, stream)) != BANDSOLVE_OK) break;
-    if ((err = transpose(work, t1, ny, nx, ld, ldt)) != cudaSuccess) { st = cuda_fail(err, "ADI transpose"); break; }
+    if (nx < (pent ? 6u : 3u) || ny < (pent ? 6u : 3u)) {
+      st = fail(BANDSOLVE_ERR_BAD_ARG, "periodic stencil needs n >= 3 (tri) / 6 (pent)");
+      break;
+    }
+    // half step 1: explicit along y, implicit along x (systems along x, interleaved after the transpose)
+    if ((err = rhs_t(field, t1, ny, nx, ld, ldt)) != cudaSuccess) { st = cuda_fail(err, "ADI stencil"); break; }
     if ((st = periodic_device(px, t1, nx, ny, ldt, stream, false)) != BANDSOLVE_OK) break;
     // half step 2: explicit along x, implicit along y
-    if ((st = cn_rhs_device(pent, sigma, t1, t2, nx, ny, ldt, stream)) != BANDSOLVE_OK) break;
-    if ((err = transpose(t2, field, nx, ny, ldt, ld)) != cudaSuccess) { st = cuda_fail(err, "ADI transpose"); break; }
+    if ((err = rhs_t(t1, field, nx, ny, ldt, ld)) != cudaSuccess) { st = cuda_fail(err, "ADI stencil"); break; }
     st = periodic_device(py, field, ny, nx, ld, stream, false);
   } while (false);
   cudaFreeAsync(t1, s);
-  cudaFreeAsync(t2, s);
   cudaGetLastError();
   return st;
 }

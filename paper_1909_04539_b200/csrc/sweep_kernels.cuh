@@ -252,7 +252,8 @@ __global__ void __launch_bounds__(W) sweep_smem(const __grid_constant__ CUtensor
 // those rows at rows.fwd/rows.bwd index 0..n-1. The forward and backward
 // halves are separate so the partitioned path (partition.cu) can hook them:
 // `post(i, v)` sees each forward value; `pre(i, g)` adjusts each backward
-// input; s1/s2 carry the recurrence state in and out.
+// input; `out(i, v)` maps each backward value to what is stored (the
+// recurrence carries v); s1/s2 carry the recurrence state in and out.
 struct NoHook {
   template <typename T>
   __device__ __forceinline__ T operator()(int, T v) const { return v; }
@@ -291,14 +292,14 @@ __device__ __forceinline__ void column_forward(T* col, int n, long long ld, cons
 }
 
 // backward over rows [0, n): the tail rows first (descending), then whole blocks
-template <typename T, bool PENT, bool FAST, int U, typename Pre = NoHook>
+template <typename T, bool PENT, bool FAST, int U, typename Pre = NoHook, typename Out = NoHook>
 __device__ __forceinline__ void column_backward(T* col, int n, long long ld, const Rows<T, PENT, FAST>& rows,
-                                                T& s1, T& s2, const Pre& pre = Pre{}) {
+                                                T& s1, T& s2, const Pre& pre = Pre{}, const Out& out = Out{}) {
   T cur[U], nxt[U];
   const int full = n / U;
   for (int i = n - 1; i >= full * U; --i) {
     T* p = col + static_cast<long long>(i) * ld;
-    *p = rows.backward(i, pre(i, *p), s1, s2);
+    *p = out(i, rows.backward(i, pre(i, *p), s1, s2));
   }
   if (full > 0) {
     const int top = (full - 1) * U;
@@ -314,7 +315,7 @@ __device__ __forceinline__ void column_backward(T* col, int n, long long ld, con
 #pragma unroll
     for (int u = U - 1; u >= 0; --u) {
       cur[u] = rows.backward(i0 + u, pre(i0 + u, cur[u]), s1, s2);
-      col[static_cast<long long>(i0 + u) * ld] = cur[u];
+      col[static_cast<long long>(i0 + u) * ld] = out(i0 + u, cur[u]);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) cur[u] = nxt[u];

@@ -89,9 +89,9 @@ def test_partition_within_tolerance(lib, oracle, cuda_device, forced):
         assert per_system_max_rel(_dev_solve(torch, u, rhs), want) <= TOL_F64, ("uniform", n)
 
 
-def test_partition_long_systems_three_launches(lib, oracle, cuda_device):
+def test_partition_long_systems_two_launches(lib, oracle, cuda_device):
     """Few long systems (an ADI axis: 4096-row systems) take the partitioned
-    path: three launches (block forward sweeps, interface solve, block
+    path: two launches (block forward sweeps; interface solve + block
     backward sweeps)."""
     torch = cuda_device
     n, m = 4096, 1024
@@ -106,7 +106,7 @@ def test_partition_long_systems_three_launches(lib, oracle, cuda_device):
     before = lib.kernel_launches()
     f.solve_dev(x.data_ptr(), n, m)
     torch.cuda.synchronize()
-    assert lib.kernel_launches() - before == 3
+    assert lib.kernel_launches() - before == 2
     res = lib.tri_residual_dev(*bands, x.data_ptr(), rhs.data_ptr(), m, m)
     assert 0.0 <= res <= TOL_F64, res
     cols = np.arange(0, m, 17)
@@ -126,3 +126,29 @@ def test_partition_disabled_matches_sequential(lib, oracle, cuda_device):
     os.environ["BANDSOLVE_PARTITION"] = "0"
     seq = _dev_solve(torch, f, rhs)
     assert per_system_max_rel(part, seq) <= TOL_F64
+
+
+@pytest.mark.parametrize("forced", ["1", None])
+def test_partition_periodic_fused_within_tolerance(lib, oracle, cuda_device, forced):
+    """The periodic (Woodbury) correction fused into the partitioned path's
+    backward pass: within 1e-12 of the reference's periodic solve."""
+    torch = cuda_device
+    if forced:
+        os.environ["BANDSOLVE_PARTITION"] = forced
+    rng = np.random.default_rng(31)
+    for n, m in [(130, 7), (1024, 130), (2050, 64), (4096, 33)]:
+        x = rng.uniform(-1, 1, (n, m))
+        for bands in [(-1.0, 3.0, -1.0), (-0.3, 1.9, -0.5), (1.0, -4.0, 7.0, -4.0, 1.0), (0.2, -0.8, 3.1, -0.7, 0.1)]:
+            if len(bands) == 3:
+                p = bs.PeriodicTri(lib, *bands, n)
+                want = oracle.periodic_tri_solve(oracle.periodic_tri_prepare(*bands, n), x.copy(), False)
+            else:
+                p = bs.PeriodicPent(lib, *bands, n)
+                want = oracle.periodic_pent_solve(oracle.periodic_pent_prepare(*bands, n), x.copy(), False)
+            for ld in (m, m + 2):
+                buf = torch.zeros((n, ld), dtype=torch.float64, device="cuda")
+                buf[:, :m] = torch.from_numpy(x).cuda()
+                p.solve_dev(buf.data_ptr(), n, m, ld=ld, stream=torch.cuda.current_stream().cuda_stream)
+                torch.cuda.synchronize()
+                got = buf[:, :m].cpu().numpy()
+                assert per_system_max_rel(got, want) <= TOL_F64, (n, m, ld, bands)
