@@ -540,13 +540,11 @@ Plan choose_plan(std::size_t n, std::size_t m, std::size_t ld, std::size_t elem,
   if (force && std::strcmp(force, "regs") == 0 &&
       plan_regs(n, m, elem, pent, sms, std::max(1, env_int("BANDSOLVE_SWG", 96) / 32), p))
     return p;
-  // few long systems (< ~1 warp per SM, n >= 1024): the group machinery cannot
-  // fill the SMs and the spill would not fit L2 -> thread per system in
-  // global memory with a deep register prefetch (measured on the ADI axes)
-  if (!force && m <= static_cast<std::size_t>(sms) * 32 && n >= 1024) {
-    p.why = "few long systems: deep-prefetch thread-per-system";
-    return p;
-  }
+  // Few long systems (< ~1 warp per SM) take the same order: with the TMEM
+  // tier a streaming plan that fits beats the thread-per-system global sweep
+  // (ADI axis 4096 x 4096 tri: 1.46x; 4096 x 1024: 1.39x; fp32 1024 x 4096:
+  // 3.4x, measured); shapes no on-chip plan fits fall through to global.
+  // (Fast mode first tries the partitioned path, partition.cu.)
   if (!force_smem && !force_persist && plan_stream(n, m, elem, pent, fast, sms, p)) return p;
   if (!force_smem && plan_persist(n, elem, pent, fast, sms, p)) return p;
   int best_sys = 0;
