@@ -72,6 +72,16 @@ size_t bandsolve_batch_systems(const bandsolve_batch* batch);
 double* bandsolve_batch_data(bandsolve_batch* batch);
 const double* bandsolve_batch_data_const(const bandsolve_batch* batch);
 
+/* ref bandsolve.h:57-62 (capi.cpp:130-141 -> batch.cpp:146-218). IBAT file:
+ * little-endian "IBAT" magic, u32 version = 1, u64 n, u64 m, then n*m
+ * binary64 values in interleaved order; byte-exact round trip. Open/seek/
+ * write failures -> BANDSOLVE_ERR_IO; truncated header, bad magic, version
+ * != 1, n or m of 0 or > 2^28, payload size mismatch -> BAD_FORMAT. */
+bandsolve_status bandsolve_batch_read_ibat(const char* path,
+                                           bandsolve_batch** out);
+bandsolve_status bandsolve_batch_write_ibat(const bandsolve_batch* batch,
+                                            const char* path);
+
 /* ---- Tridiagonal (ref bandsolve.h:67-78) ---------------------------------
  * sub/diag/sup of length n >= 2, finite, sub[0] = sup[n-1] = 0
  * (banded.cpp:40-57). The factor (banded.cpp:67-86) is computed on the host
@@ -92,6 +102,18 @@ void bandsolve_tri_factor_destroy(bandsolve_tri_factor* factor);
 bandsolve_status bandsolve_tri_solve_shared(const bandsolve_tri_factor* factor,
                                             bandsolve_batch* batch);
 
+/* ref bandsolve.h:80-85 (capi.cpp:165-172 -> tri_solver.cpp:51-112).
+ * Baseline with one band copy per system: a/b/c are consumed (b holds the
+ * pivot reciprocals, c the scaled super-diagonal on return, as in the
+ * reference), d holds the solutions. Shapes differ -> SHAPE_MISMATCH; n < 2
+ * -> BAD_ARG; a zero pivot -> FACTORIZATION_BREAKDOWN (outputs unspecified).
+ * Runs on the GPU (thread per system, the reference's operation order:
+ * bitwise equal), staged over column chunks, synchronous. */
+bandsolve_status bandsolve_tri_solve_per_system(bandsolve_batch* a,
+                                                bandsolve_batch* b,
+                                                bandsolve_batch* c,
+                                                bandsolve_batch* d);
+
 /* ---- Pentadiagonal (ref bandsolve.h:91-113) ------------------------------
  * Bands a..e of length n >= 5, main diagonal c, structural zeros
  * a[0] = a[1] = b[0] = d[n-1] = e[n-1] = e[n-2] = 0 (banded.cpp:88-116). */
@@ -106,6 +128,14 @@ void bandsolve_pent_factor_destroy(bandsolve_pent_factor* factor);
 /* ref bandsolve.h:99-100 (capi.cpp:191-195 -> pent_solver.cpp:67-81). */
 bandsolve_status bandsolve_pent_solve_shared(
     const bandsolve_pent_factor* factor, bandsolve_batch* batch);
+
+/* ref bandsolve.h:101-103 (capi.cpp:197-205 -> pent_solver.cpp:131-219).
+ * Per-system baseline: b..e are consumed (beta, alpha, gamma, delta as the
+ * reference leaves them), f holds the solutions; a is read only. n < 5 ->
+ * BAD_ARG; zero alpha -> FACTORIZATION_BREAKDOWN. GPU, bitwise, synchronous. */
+bandsolve_status bandsolve_pent_solve_per_system(
+    bandsolve_batch* a, bandsolve_batch* b, bandsolve_batch* c,
+    bandsolve_batch* d, bandsolve_batch* e, bandsolve_batch* f);
 
 /* ref bandsolve.h:107-113 (capi.cpp:207-227 -> pent_solver.cpp:83-111):
  * constant bands, epsilon kept as one scalar; bitwise equal to the shared
@@ -263,6 +293,16 @@ bandsolve_status bandsolve_pent_solve_shared_dev(
 bandsolve_status bandsolve_pent_solve_shared_dev_f32(
     const bandsolve_pent_factor* factor, float* x, size_t n, size_t m,
     size_t ld, void* stream);
+/* Device-resident per-system baselines (extension): the same arrays as the
+ * host calls, each n x m with row pitch ld, in device memory. Synchronises
+ * `stream` to report breakdown. */
+bandsolve_status bandsolve_tri_solve_per_system_dev(double* a, double* b,
+                                                    double* c, double* d,
+                                                    size_t n, size_t m,
+                                                    size_t ld, void* stream);
+bandsolve_status bandsolve_pent_solve_per_system_dev(
+    double* a, double* b, double* c, double* d, double* e, double* f,
+    size_t n, size_t m, size_t ld, void* stream);
 bandsolve_status bandsolve_pent_solve_uniform_dev(
     const bandsolve_uniform_pent_factor* factor, double* x, size_t n,
     size_t m, size_t ld, void* stream);

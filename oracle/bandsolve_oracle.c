@@ -560,3 +560,81 @@ void oracle_cn_rhs(int problem, double sigma_x, size_t n, size_t m,
     }
   }
 }
+
+/* ---- per-system baselines ------------------------------------------------ */
+/* tri_solver.cpp:51-112: reciprocals over b, chat over c, dhat over d, then
+ * the backward sweep in place over d. */
+int oracle_tri_per_system(const double* a, double* b, double* c, double* d, size_t n, size_t m) {
+  if (n < 2) return ST_BAD_ARG;
+  int broke = 0;
+  for (size_t j = 0; j < m; ++j) {
+    double denom = b[j];
+    if (!denom_ok(denom)) { broke = 1; continue; }
+    double r = 1.0 / denom;
+    b[j] = r;
+    double cg = c[j] * r;
+    c[j] = cg;
+    double dg = d[j] * r;
+    d[j] = dg;
+    int ok = 1;
+    for (size_t i = 1; i < n; ++i) {
+      const size_t k = i * m + j;
+      denom = b[k] - a[k] * cg;
+      if (!denom_ok(denom)) { broke = 1; ok = 0; break; }
+      r = 1.0 / denom;
+      b[k] = r;
+      cg = c[k] * r;
+      c[k] = cg;
+      dg = (d[k] - a[k] * dg) * r;
+      d[k] = dg;
+    }
+    if (!ok) continue;
+    double xnext = d[(n - 1) * m + j];
+    for (size_t i = n - 1; i-- > 0;) {
+      const size_t k = i * m + j;
+      const double xi = d[k] - c[k] * xnext;
+      d[k] = xi;
+      xnext = xi;
+    }
+  }
+  return broke ? ST_BREAKDOWN : ST_OK;
+}
+
+/* pent_solver.cpp:131-219: beta over b, alpha over c, gamma over d, delta
+ * over e (a doubles as epsilon), g then x over f. */
+int oracle_pent_per_system(const double* a, double* b, double* c, double* d, double* e, double* f,
+                           size_t n, size_t m) {
+  if (n < 5) return ST_BAD_ARG;
+  int broke = 0;
+#define AT(i) ((size_t)(i) * m + j)
+  for (size_t j = 0; j < m; ++j) {
+    double alpha = c[AT(0)];
+    if (!denom_ok(alpha)) { broke = 1; continue; }
+    d[AT(0)] /= alpha;
+    e[AT(0)] /= alpha;
+    alpha = c[AT(1)] - b[AT(1)] * d[AT(0)];
+    if (!denom_ok(alpha)) { broke = 1; continue; }
+    c[AT(1)] = alpha;
+    d[AT(1)] = (d[AT(1)] - b[AT(1)] * e[AT(0)]) / alpha;
+    e[AT(1)] /= alpha;
+    int ok = 1;
+    for (size_t i = 2; i < n; ++i) {
+      const double beta = b[AT(i)] - a[AT(i)] * d[AT(i - 2)];
+      b[AT(i)] = beta;
+      alpha = c[AT(i)] - a[AT(i)] * e[AT(i - 2)] - beta * d[AT(i - 1)];
+      if (!denom_ok(alpha)) { ok = 0; break; }
+      c[AT(i)] = alpha;
+      if (i + 1 < n) d[AT(i)] = (d[AT(i)] - beta * e[AT(i - 1)]) / alpha;
+      if (i + 2 < n) e[AT(i)] /= alpha;
+    }
+    if (!ok) { broke = 1; continue; }
+    f[AT(0)] /= c[AT(0)];
+    f[AT(1)] = (f[AT(1)] - b[AT(1)] * f[AT(0)]) / c[AT(1)];
+    for (size_t i = 2; i < n; ++i)
+      f[AT(i)] = (f[AT(i)] - a[AT(i)] * f[AT(i - 2)] - b[AT(i)] * f[AT(i - 1)]) / c[AT(i)];
+    f[AT(n - 2)] -= d[AT(n - 2)] * f[AT(n - 1)];
+    for (size_t i = n - 2; i-- > 0;) f[AT(i)] -= d[AT(i)] * f[AT(i + 1)] + e[AT(i)] * f[AT(i + 2)];
+  }
+#undef AT
+  return broke ? ST_BREAKDOWN : ST_OK;
+}

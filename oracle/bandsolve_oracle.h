@@ -114,6 +114,16 @@ double oracle_rhs_value(uint64_t seed, uint64_t i, uint64_t j);
 void oracle_fill_rhs(uint64_t seed, size_t n, size_t m, size_t j_offset,
                      size_t m_total, double* x);
 
+/* Per-system baselines, reference tri_solver.cpp:51-112 and
+ * pent_solver.cpp:131-219: one band copy per system, interleaved (n, m),
+ * destroyed in place exactly as the reference leaves them (tri: b, c, d;
+ * pent: b, c, d, e, f); d (tri) / f (pent) holds the solutions. Returns 0,
+ * 1 (n too small) or 3 (zero pivot in some column; the other columns are
+ * still solved, outputs unspecified, as in the reference). */
+int oracle_tri_per_system(const double* a, double* b, double* c, double* d, size_t n, size_t m);
+int oracle_pent_per_system(const double* a, double* b, double* c, double* d, double* e, double* f,
+                           size_t n, size_t m);
+
 #ifdef __cplusplus
 }
 #endif

@@ -62,6 +62,8 @@ class Oracle:
         self.lib = C.CDLL(path or build_port())
         L = self.lib
         L.oracle_tri_prefactor.argtypes = [_dp, _dp, _dp, _sz, _dp, _dp, _dp]
+        L.oracle_tri_per_system.argtypes = [_dp] * 4 + [_sz, _sz]
+        L.oracle_pent_per_system.argtypes = [_dp] * 6 + [_sz, _sz]
         L.oracle_tri_solve_shared.argtypes = [_dp, _dp, _dp, _sz, _sz, _sz, _dp]
         L.oracle_tri_solve_shared.restype = None
         L.oracle_pent_prefactor.argtypes = [_dp] * 5 + [_sz] + [_dp] * 5
@@ -132,6 +134,21 @@ class Oracle:
                                    _d(eps) if eps is not None else None, f.get("eps_scalar", 0.0),
                                    n, m, m, _d(x))
         return x
+
+    # -- per-system baselines (reference tri_solver.cpp:51-112, pent_solver.cpp:131-219)
+    def tri_per_system(self, a, b, c, d):
+        """Destroys copies of b, c, d as the reference does; returns (status, b, c, d)."""
+        arrs = [np.array(v, dtype=np.float64, order="C", copy=True) for v in (a, b, c, d)]
+        n, m = arrs[0].shape
+        st = self.lib.oracle_tri_per_system(*[_d(v) for v in arrs], n, m)
+        return (st, *arrs[1:])
+
+    def pent_per_system(self, a, b, c, d, e, f):
+        """Destroys copies of b..f as the reference does; returns (status, b, c, d, e, f)."""
+        arrs = [np.array(v, dtype=np.float64, order="C", copy=True) for v in (a, b, c, d, e, f)]
+        n, m = arrs[0].shape
+        st = self.lib.oracle_pent_per_system(*[_d(v) for v in arrs], n, m)
+        return (st, *arrs[1:])
 
     # -- periodic wrap correction (reference periodic.cpp) -----------------------
     def periodic_tri_prepare(self, a, b, c, n) -> dict:

@@ -71,6 +71,10 @@ _REFERENCE_SIGS = [
     ("bandsolve_batch_systems", _sz, [_vp]),
     ("bandsolve_batch_data", _dp, [_vp]),
     ("bandsolve_batch_data_const", _dp, [_vp]),
+    ("bandsolve_batch_read_ibat", _st, [C.c_char_p, C.POINTER(_vp)]),
+    ("bandsolve_batch_write_ibat", _st, [_vp, C.c_char_p]),
+    ("bandsolve_tri_solve_per_system", _st, [_vp] * 4),
+    ("bandsolve_pent_solve_per_system", _st, [_vp] * 6),
     ("bandsolve_tri_factor_create", _st, [_dp, _dp, _dp, _sz, C.POINTER(_vp)]),
     ("bandsolve_tri_factor_destroy", None, [_vp]),
     ("bandsolve_tri_solve_shared", _st, [_vp, _vp]),
@@ -106,6 +110,8 @@ _EXTENSION_SIGS = [
     ("bandsolve_pent_solve_shared_dev", _st, [_vp, _vp, _sz, _sz, _sz, _vp]),
     ("bandsolve_pent_solve_shared_dev_f32", _st, [_vp, _vp, _sz, _sz, _sz, _vp]),
     ("bandsolve_pent_solve_uniform_dev", _st, [_vp, _vp, _sz, _sz, _sz, _vp]),
+    ("bandsolve_tri_solve_per_system_dev", _st, [_vp] * 4 + [_sz, _sz, _sz, _vp]),
+    ("bandsolve_pent_solve_per_system_dev", _st, [_vp] * 6 + [_sz, _sz, _sz, _vp]),
     ("bandsolve_pent_solve_uniform_dev_f32", _st, [_vp, _vp, _sz, _sz, _sz, _vp]),
     ("bandsolve_tri_residual_dev", _st,
      [_dp, _dp, _dp, _sz, C.c_int, _vp, _vp, _sz, _sz, _vp, _dp]),
@@ -273,14 +279,27 @@ class Library:
 class Batch:
     """Owning bandsolve_batch handle with a numpy (n, m) view of its data."""
 
-    def __init__(self, lib: Library, n: int, m: int):
+    def __init__(self, lib: Library, n: int, m: int, _handle: Optional[_vp] = None):
         self.lib = lib
-        h = _vp()
-        lib.check(lib.lib.bandsolve_batch_create(n, m, C.byref(h)), "batch_create")
+        h = _handle
+        if h is None:
+            h = _vp()
+            lib.check(lib.lib.bandsolve_batch_create(n, m, C.byref(h)), "batch_create")
         self.handle = h
         self.n, self.m = n, m
         ptr = lib.lib.bandsolve_batch_data(h)
         self.array = np.ctypeslib.as_array(ptr, shape=(n, m))
+
+    @classmethod
+    def read_ibat(cls, lib: Library, path: str) -> "Batch":
+        """bandsolve_batch_read_ibat (ref batch.cpp:172-218)."""
+        h = _vp()
+        lib.check(lib.lib.bandsolve_batch_read_ibat(str(path).encode(), C.byref(h)), "batch_read_ibat")
+        return cls(lib, lib.lib.bandsolve_batch_rows(h), lib.lib.bandsolve_batch_systems(h), _handle=h)
+
+    def write_ibat(self, path: str) -> None:
+        """bandsolve_batch_write_ibat (ref batch.cpp:146-170)."""
+        self.lib.check(self.lib.lib.bandsolve_batch_write_ibat(self.handle, str(path).encode()), "batch_write_ibat")
 
     @classmethod
     def from_array(cls, lib: Library, arr) -> "Batch":
@@ -308,6 +327,18 @@ class Batch:
             self.close()
         except Exception:
             pass
+
+
+def tri_solve_per_system(lib: Library, a: Batch, b: Batch, c: Batch, d: Batch) -> None:
+    """bandsolve_tri_solve_per_system (ref tri_solver.cpp:51-112): a/b/c consumed, d -> x."""
+    lib.check(lib.lib.bandsolve_tri_solve_per_system(a.handle, b.handle, c.handle, d.handle),
+              "tri_solve_per_system")
+
+
+def pent_solve_per_system(lib: Library, a: Batch, b: Batch, c: Batch, d: Batch, e: Batch, f: Batch) -> None:
+    """bandsolve_pent_solve_per_system (ref pent_solver.cpp:131-219): b..e consumed, f -> x."""
+    lib.check(lib.lib.bandsolve_pent_solve_per_system(a.handle, b.handle, c.handle, d.handle, e.handle, f.handle),
+              "pent_solve_per_system")
 
 
 class _Factor:

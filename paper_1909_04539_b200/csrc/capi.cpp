@@ -144,6 +144,66 @@ BSB_API const double* bandsolve_batch_data_const(const bandsolve_batch* batch) {
   return batch ? batch->data : nullptr;
 }
 
+// ---- IBAT files (capi.cpp:130-141; batch.cpp:146-218) -------------------------
+BSB_API bandsolve_status bandsolve_batch_read_ibat(const char* path, bandsolve_batch** out) {
+  if (!path || !out) return null_arg();
+  *out = nullptr;
+  return guarded([&] {
+    auto b = std::make_unique<bandsolve_batch>();
+    bandsolve_status st = bsb::ibat_read(path, &b->n, &b->m, &b->data, &b->pinned);
+    if (st != BANDSOLVE_OK) return st;
+    *out = b.release();
+    return BANDSOLVE_OK;
+  });
+}
+
+BSB_API bandsolve_status bandsolve_batch_write_ibat(const bandsolve_batch* batch, const char* path) {
+  if (!batch || !path) return null_arg();
+  return guarded([&] { return bsb::ibat_write(path, batch->data, batch->n, batch->m); });
+}
+
+// ---- per-system baselines (capi.cpp:165-172, :197-205) --------------------------
+namespace {
+bandsolve_status per_system_batches(bool pent, bandsolve_batch* const* v) {
+  const int na = pent ? 6 : 4;
+  for (int q = 0; q < na; ++q)
+    if (!v[q]) return null_arg();
+  return guarded([&] {
+    for (int q = 1; q < na; ++q)
+      if (v[q]->n != v[0]->n || v[q]->m != v[0]->m)
+        return bsb::fail(BANDSOLVE_ERR_SHAPE_MISMATCH, "band/rhs buffers differ in shape");
+    double* arr[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    for (int q = 0; q < na; ++q) arr[q] = v[q]->data;
+    return bsb::per_system_host(pent, arr, v[0]->n, v[0]->m);
+  });
+}
+}  // namespace
+
+BSB_API bandsolve_status bandsolve_tri_solve_per_system(bandsolve_batch* a, bandsolve_batch* b, bandsolve_batch* c,
+                                                        bandsolve_batch* d) {
+  bandsolve_batch* v[4] = {a, b, c, d};
+  return per_system_batches(false, v);
+}
+
+BSB_API bandsolve_status bandsolve_pent_solve_per_system(bandsolve_batch* a, bandsolve_batch* b, bandsolve_batch* c,
+                                                         bandsolve_batch* d, bandsolve_batch* e, bandsolve_batch* f) {
+  bandsolve_batch* v[6] = {a, b, c, d, e, f};
+  return per_system_batches(true, v);
+}
+
+BSB_API bandsolve_status bandsolve_tri_solve_per_system_dev(double* a, double* b, double* c, double* d, size_t n,
+                                                            size_t m, size_t ld, void* stream) {
+  double* arr[4] = {a, b, c, d};
+  return guarded([&] { return bsb::per_system_device(false, arr, n, m, ld, stream); });
+}
+
+BSB_API bandsolve_status bandsolve_pent_solve_per_system_dev(double* a, double* b, double* c, double* d, double* e,
+                                                             double* f, size_t n, size_t m, size_t ld,
+                                                             void* stream) {
+  double* arr[6] = {a, b, c, d, e, f};
+  return guarded([&] { return bsb::per_system_device(true, arr, n, m, ld, stream); });
+}
+
 // ---- tridiagonal (capi.cpp:143-163) ----------------------------------------
 BSB_API bandsolve_status bandsolve_tri_factor_create(const double* sub, const double* diag, const double* sup,
                                                      size_t n, bandsolve_tri_factor** out) {

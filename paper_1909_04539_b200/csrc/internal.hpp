@@ -130,6 +130,16 @@ bandsolve_status partition_solve_device(const Factor& f, double* x, std::size_t 
                                         std::size_t m, std::size_t ld,
                                         void* stream, int sms, bool* done,
                                         const PartPeriodic* per = nullptr);
+// Per-system baselines (per_system.cu): arr = a, b, c, d (tri) / a..f (pent),
+// reference tri_solver.cpp:51-112, pent_solver.cpp:131-219. The device form
+// synchronises `stream` to report breakdown.
+bandsolve_status per_system_device(bool pent, double* const* arr, std::size_t n, std::size_t m, std::size_t ld,
+                                   void* stream);
+bandsolve_status per_system_host(bool pent, double* const* arr, std::size_t n, std::size_t m);
+// IBAT files (capi.cpp), reference batch.cpp:146-218
+bandsolve_status ibat_write(const char* path, const double* data, std::size_t n, std::size_t m);
+bandsolve_status ibat_read(const char* path, std::size_t* n, std::size_t* m, double** data, bool* pinned);
+
 // Host batch: staged through the device, synchronous. With `per`, the
 // periodic correction follows the sweep on each staged chunk; with
 // `correct_only`, only the correction runs.

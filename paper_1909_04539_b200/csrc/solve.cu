@@ -35,6 +35,8 @@ int mode_from_env() {
   return BANDSOLVE_MODE_EXACT;
 }
 
+}  // namespace
+
 bandsolve_status cuda_fail(cudaError_t err, const char* what) {
   return fail(BANDSOLVE_ERR_INTERNAL,
               std::string(what) + ": " + cudaGetErrorName(err) + " (" + cudaGetErrorString(err) + ")");
@@ -57,6 +59,8 @@ int device_count_cached() {
   }();
   return count;
 }
+
+namespace {
 
 // ---- packed factor records --------------------------------------------------
 // The signed zeros below make the generic row formulas of sweep_kernels.cuh
@@ -1596,37 +1600,6 @@ bandsolve_status adi_step_device(const Periodic& px, const Periodic& py, double 
 
 // ---- Crank-Nicolson driver: bandsolve_bench_run (reference capi.cpp:369-411,
 // pde.cpp run_benchmark :258-371) with the stepping loop on the GPU.
-namespace {
-void put_u32_le(unsigned char* p, uint32_t v) {
-  for (int k = 0; k < 4; ++k) p[k] = static_cast<unsigned char>(v >> (8 * k));
-}
-void put_u64_le(unsigned char* p, uint64_t v) {
-  for (int k = 0; k < 8; ++k) p[k] = static_cast<unsigned char>(v >> (8 * k));
-}
-// batch.cpp:146-171 (write_ibat): "IBAT", u32 version 1, u64 n, u64 m, then
-// the n x m payload as little-endian binary64.
-bandsolve_status write_ibat(const std::string& path, const double* data, std::size_t n, std::size_t m) {
-  FILE* f = std::fopen(path.c_str(), "wb");
-  if (!f) return fail(BANDSOLVE_ERR_IO, "cannot open for writing: " + path);
-  unsigned char header[24];
-  std::memcpy(header, "IBAT", 4);
-  put_u32_le(header + 4, 1);
-  put_u64_le(header + 8, n);
-  put_u64_le(header + 16, m);
-  bool ok = std::fwrite(header, 1, sizeof header, f) == sizeof header;
-  std::vector<unsigned char> payload(n * m * 8);
-  for (std::size_t k = 0; k < n * m; ++k) {
-    uint64_t bits;
-    std::memcpy(&bits, data + k, 8);
-    put_u64_le(payload.data() + 8 * k, bits);
-  }
-  ok = ok && std::fwrite(payload.data(), 1, payload.size(), f) == payload.size();
-  ok = (std::fflush(f) == 0) && ok;
-  std::fclose(f);
-  return ok ? BANDSOLVE_OK : fail(BANDSOLVE_ERR_IO, "short write: " + path);
-}
-}  // namespace
-
 bandsolve_status bench_run_device(const bandsolve_bench_params& prm, bandsolve_bench_result* res,
                                   int threads_report) {
   // capi.cpp:374-401 and pde.cpp:258-277: the reference's checks, in order
@@ -1726,7 +1699,7 @@ bandsolve_status bench_run_device(const bandsolve_bench_params& prm, bandsolve_b
         st = cuda_fail(err, "bench dump");
         break;
       }
-      st = write_ibat(prefix + "_step" + std::to_string(k + 1) + ".ibat", field.data(), n, m);
+      st = ibat_write((prefix + "_step" + std::to_string(k + 1) + ".ibat").c_str(), field.data(), n, m);
     }
   }
   cleanup();

@@ -19,12 +19,14 @@ for mode in exact fast; do
   done
 done
 timeout 300 python bench.py --config tri512 --f32 --no-cpu --steps 50 --warmup 5 >> gpurun_out/bench_sweep.jsonl 2>> gpurun_out/bench_err.log
-for extra in "--config pent512 --periodic" "--config pent512 --periodic --mode fast" "--config pent512 --cn" "--config pent512 --cn --mode fast" "--config tri512 --cn --mode fast" "--config c4tri" "--config c4pent --mode fast"; do
+for extra in "--config pent512 --periodic" "--config pent512 --periodic --mode fast" "--config pent512 --cn" "--config pent512 --cn --mode fast" "--config tri512 --cn --mode fast" "--config c4tri" "--config c4tri --mode fast" "--config c4pent" "--config c4pent --mode fast"; do
   timeout 300 python bench.py $extra --no-cpu --steps 20 --warmup 3 >> gpurun_out/bench_sweep.jsonl 2>> gpurun_out/bench_err.log
 done
 timeout 300 python bench.py --config pent512 --f32 --no-cpu --steps 50 --warmup 5 >> gpurun_out/bench_sweep.jsonl 2>> gpurun_out/bench_err.log
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
    --log-file gpurun_out/launches_c2.csv python bench.py --steps 5 --warmup 3 --no-cpu > gpurun_out/ncu_launch.log 2>&1
+timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 60 --csv \
+   --log-file gpurun_out/launches_c4tri_fast.csv python bench.py --config c4tri --mode fast --steps 2 --warmup 3 --no-cpu > /dev/null 2>&1
 for cfg in ${NCU_CFGS:-c2}; do
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:sweep_ -s 3 -c 1 \
     -o gpurun_out/prof_r1_${cfg} -f python bench.py --config $cfg --no-cpu --steps 3 --warmup 3 > gpurun_out/ncu_${cfg}.log 2>&1
