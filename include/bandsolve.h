@@ -203,7 +203,8 @@ bandsolve_status bandsolve_footprint(bandsolve_storage_variant variant,
  * IBAT dumps; the stepping loop (RHS assembly + cyclic solve per step) runs
  * on the GPU and each step is timed with CUDA events. The uniform variant
  * is the shared one (bitwise identical, pent_solver.cpp:83-97); the
- * per-system variant is outside this library (BANDSOLVE_ERR_BAD_ARG). */
+ * per-system variant rewrites replicated band copies every step and runs
+ * the per-system kernels, as the reference's engine (pde.cpp:168-221). */
 typedef enum bandsolve_problem {
   BANDSOLVE_PROBLEM_DIFFUSION = 0,
   BANDSOLVE_PROBLEM_HYPERDIFFUSION = 1

@@ -207,19 +207,59 @@ class Oracle:
         dtv = dt if dt > 0.0 else 1.0 * 2.0 * pow_dx
         return dtv / (2.0 * pow_dx)
 
-    def cn_trajectory(self, problem: int, n: int, m: int, steps: int, dt: float = 0.0) -> list:
-        """Fields after each step of run_benchmark (pde.cpp:279-343), shared variant."""
+    @staticmethod
+    def periodic_modified_bands(consts, n: int) -> list:
+        """The strictly banded A' of the periodic splitting (periodic.cpp:11-31 tri,
+        :97-129 pent), as the reference's per-system engine replicates it
+        (pde.cpp:168-185, :199-221)."""
+        if len(consts) == 3:
+            a, b, c = consts
+            sub, diag, sup = np.full(n, a), np.full(n, b), np.full(n, c)
+            sub[0] = 0.0
+            sup[n - 1] = 0.0
+            diag[0] = 2.0 * b
+            diag[n - 1] = b + a * c / b
+            return [sub, diag, sup]
+        a, b, c, d, e = consts
+        av, bv, cv, dv, ev = (np.full(n, v) for v in (a, b, c, d, e))
+        av[0] = av[1] = bv[0] = 0.0
+        dv[n - 1] = ev[n - 1] = ev[n - 2] = 0.0
+        cv[0] = c + b
+        dv[0] = d + a
+        bv[1] = b + a
+        dv[n - 2] = d + e
+        bv[n - 1] = b + e
+        cv[n - 1] = c + d
+        return [av, bv, cv, dv, ev]
+
+    def cn_trajectory(self, problem: int, n: int, m: int, steps: int, dt: float = 0.0, variant: int = 0) -> list:
+        """Fields after each step of run_benchmark (pde.cpp:279-343). Shared and
+        uniform variants sweep the shared factor (bitwise the same,
+        pent_solver.cpp:83-97); the per-system variant (1) rewrites replicated
+        band copies of A' every step, solves per system, then applies the
+        correction (pde.cpp:168-185, :199-221)."""
         s = self.cn_sigma(problem, n, dt)
         if problem == 0:
-            f = self.periodic_tri_prepare(-s, 1.0 + 2.0 * s, -s, n)
+            consts = (-s, 1.0 + 2.0 * s, -s)
+            f = self.periodic_tri_prepare(*consts, n)
             solve = self.periodic_tri_solve
         else:
-            f = self.periodic_pent_prepare(s, -4.0 * s, 1.0 + 6.0 * s, -4.0 * s, s, n)
+            consts = (s, -4.0 * s, 1.0 + 6.0 * s, -4.0 * s, s)
+            f = self.periodic_pent_prepare(*consts, n)
             solve = self.periodic_pent_solve
+        bands = self.periodic_modified_bands(consts, n)
         u = self.default_mode_initial(n, m)
         out = []
         for _ in range(steps):
-            u = solve(f, self.cn_rhs(problem, s, u))
+            rhs = self.cn_rhs(problem, s, u)
+            if variant == 1:
+                rep = [np.repeat(b[:, None], m, axis=1) for b in bands]
+                res = (self.tri_per_system if problem == 0 else self.pent_per_system)(*rep, rhs)
+                if res[0]:
+                    raise OracleError(res[0])
+                u = solve(f, res[-1], correct_only=True)
+            else:
+                u = solve(f, rhs)
             out.append(u.copy())
         return out
 

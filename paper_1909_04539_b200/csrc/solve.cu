@@ -972,6 +972,15 @@ __global__ void cn_rhs_kernel(const double* __restrict__ u, double* __restrict__
   }
 }
 
+// band -> n x m replicated copy (the per-system engine's fill_replicated,
+// pde.cpp:178-180)
+__global__ void replicate_band_kernel(const double* __restrict__ band, double* __restrict__ out, long long n,
+                                      long long m, long long ld) {
+  const long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  for (long long i = blockIdx.y; i < n; i += gridDim.y) out[i * ld + j] = band[i];
+}
+
 // ---- fused stencil + transpose for the ADI half steps ---------------------------
 // out[c * ldo + r] = stencil_r(u)[r][c]: the periodic Crank-Nicolson explicit
 // half along rows (same operation order as cn_rhs_kernel) written transposed,
@@ -1621,9 +1630,6 @@ bandsolve_status bench_run_device(const bandsolve_bench_params& prm, bandsolve_b
   } else if (n < 6) {
     return fail(BANDSOLVE_ERR_BAD_ARG, "hyperdiffusion benchmark needs n >= 6");
   }
-  if (prm.variant == BANDSOLVE_VARIANT_PER_SYSTEM)
-    return fail(BANDSOLVE_ERR_BAD_ARG,
-                "per-system variant is not provided by the B200 library (shared-LHS path only)");
   // pde.cpp:29-46: sigma_x = dt / (2 dx^p), default dt gives sigma_x = 1
   const double dx = 1.0 / static_cast<double>(n);
   const double pow_dx = diffusion ? dx * dx : dx * dx * dx * dx;
@@ -1651,6 +1657,7 @@ bandsolve_status bench_run_device(const bandsolve_bench_params& prm, bandsolve_b
   const std::size_t ld = (m + 1) & ~std::size_t(1);  // even pitch keeps the TMA plans
   const std::size_t bytes = n * ld * sizeof(double);
   double *du = nullptr, *ds = nullptr;
+  double* dbands = nullptr;  // per-system variant: A' bands (n each) | replicated copies (n x ld each)
   cudaStream_t s = nullptr;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   auto cleanup = [&]() {
@@ -1658,11 +1665,37 @@ bandsolve_status bench_run_device(const bandsolve_bench_params& prm, bandsolve_b
     if (e1) cudaEventDestroy(e1);
     if (du) cudaFree(du);
     if (ds) cudaFree(ds);
+    if (dbands) cudaFree(dbands);
     if (s) cudaStreamDestroy(s);
     cudaGetLastError();
   };
-  auto step = [&](const double* from, double* to) { return cn_step_device(*per, sigma, from, to, n, m, ld, s); };
+  // per-system variant (pde.cpp:168-185, :199-221): every step rewrites
+  // replicated band copies of A', solves per system, then corrects
+  const bool per_sys = prm.variant == BANDSOLVE_VARIANT_PER_SYSTEM;
+  const int nb = diffusion ? 3 : 5;
+  auto step = [&](const double* from, double* to) -> bandsolve_status {
+    if (!per_sys) return cn_step_device(*per, sigma, from, to, n, m, ld, s);
+    bandsolve_status q = cn_rhs_device(!diffusion, sigma, from, to, n, m, ld, s);
+    if (q != BANDSOLVE_OK) return q;
+    double* arr[6];
+    const dim3 grid(static_cast<unsigned>((m + 127) / 128), static_cast<unsigned>(std::min<std::size_t>(n, 4096)));
+    for (int b = 0; b < nb; ++b) {
+      arr[b] = dbands + nb * n + static_cast<std::size_t>(b) * n * ld;
+      replicate_band_kernel<<<grid, 128, 0, s>>>(dbands + b * n, arr[b], static_cast<long long>(n),
+                                                 static_cast<long long>(m), static_cast<long long>(ld));
+    }
+    g_launches.fetch_add(nb, std::memory_order_relaxed);
+    arr[nb] = to;
+    q = per_system_device(!diffusion, arr, n, m, ld, s);
+    if (q != BANDSOLVE_OK) return q;
+    return launch_periodic_correct(*per, to, n, m, ld, s);
+  };
   cudaError_t err = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  if (err == cudaSuccess && per_sys) {
+    err = cudaMalloc(&dbands, (nb * n + static_cast<std::size_t>(nb) * n * ld) * sizeof(double));
+    if (err == cudaSuccess)
+      err = cudaMemcpy(dbands, per->factor->bands.data(), nb * n * sizeof(double), cudaMemcpyHostToDevice);
+  }
   if (err == cudaSuccess) err = cudaMalloc(&du, bytes);
   if (err == cudaSuccess) err = cudaMalloc(&ds, bytes);
   if (err == cudaSuccess) err = cudaEventCreate(&e0);
@@ -1714,8 +1747,9 @@ bandsolve_status bench_run_device(const bandsolve_bench_params& prm, bandsolve_b
   res->per_step_mean_s = mean;
   res->per_step_std_s = per_step.size() > 1 ? std::sqrt(var / static_cast<double>(per_step.size() - 1)) : 0.0;
   const uint64_t un = n, um = m;
-  res->elements = diffusion ? 3 * un + un * um
-                            : (prm.variant == BANDSOLVE_VARIANT_UNIFORM ? 4 * un + un * um : 5 * un + un * um);
+  res->elements = per_sys ? (diffusion ? 4 : 6) * un * um
+                 : diffusion ? 3 * un + un * um
+                             : (prm.variant == BANDSOLVE_VARIANT_UNIFORM ? 4 * un + un * um : 5 * un + un * um);
   res->threads = threads_report;
   res->steps = prm.steps;
   return BANDSOLVE_OK;

@@ -29,6 +29,9 @@ CASES = [  # name, n, m, steps, dt, problem, variant
     ("hyper_n12_m4", 12, 4, 4, 0.0, 1, 0),
     ("hyper_n64_m9_uniform", 64, 9, 3, 0.0, 1, 2),
     ("hyper_n512_m24", 512, 24, 2, 0.0, 1, 0),
+    ("diff_n40_m6_per_system", 40, 6, 3, 0.0, 0, 1),
+    ("hyper_n48_m5_per_system", 48, 5, 3, 0.0, 1, 1),
+    ("hyper_n300_m9_per_system_dt", 300, 9, 2, 1e-9, 1, 1),
 ]
 
 

@@ -33,7 +33,7 @@ def cases():
 @pytest.mark.parametrize("name,params,fields", cases())
 def test_oracle_reproduces_reference_dumps(oracle, name, params, fields):
     n, m, steps, dt, prob, var = params
-    traj = oracle.cn_trajectory(prob, n, m, steps, dt)
+    traj = oracle.cn_trajectory(prob, n, m, steps, dt, var)
     for k in range(steps):
         assert bitwise_equal(traj[k], fields[k]), (name, k + 1)
 
@@ -72,7 +72,7 @@ def test_gpu_bench_run_dumps_bitwise(lib, cuda_device, tmp_path, name, params, f
     prefix = str(tmp_path / name)
     r = lib.bench_run(n, m, steps, prob, var, dt, dump_every=1, dump_prefix=prefix)
     assert r.steps == steps and r.per_step_mean_s > 0 and r.wall_s >= r.per_step_mean_s
-    assert r.elements == lib.footprint({(0, 0): 1, (1, 0): 3, (1, 2): 4}[(prob, var)], n, m)[0]
+    assert r.elements == lib.footprint({(0, 0): 1, (0, 1): 0, (1, 0): 3, (1, 1): 2, (1, 2): 4}[(prob, var)], n, m)[0]
     for k in range(steps):
         got = bs.read_ibat(f"{prefix}_step{k + 1}.ibat")
         assert bitwise_equal(got, fields[k]), (name, k + 1)
