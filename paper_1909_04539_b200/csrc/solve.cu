@@ -1340,6 +1340,7 @@ bandsolve_status periodic_device(const Periodic& p, double* x, std::size_t n, st
                     std::getenv("BANDSOLVE_PERIODIC_UNFUSED") == nullptr;
   if (fuse && partition_blocks(n, m, sms, pent) > 0) {
     // few long systems: partitioned sweep with the correction fused into its last pass
+    keep_pool_memory(device);
     const double* blob = nullptr;
     bandsolve_status st = periodic_device_z(p, device, &blob);
     if (st != BANDSOLVE_OK) return st;
@@ -1569,6 +1570,11 @@ bandsolve_status adi_step_device(const Periodic& px, const Periodic& py, double 
   auto s = static_cast<cudaStream_t>(stream);
   const bool pent = px.kind != Kind::Tri;
   const std::size_t ldt = (ny + 1) & ~std::size_t(1);  // transposed pitch (even: TMA plans)
+  {
+    int device = 0;
+    BSB_CUDA(cudaGetDevice(&device));
+    keep_pool_memory(device);  // the per-step scratch stays mapped in the stream-ordered pool
+  }
   double* t1 = nullptr;
   BSB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&t1), nx * ldt * sizeof(double), s));
   (void)work;  // scratch kept in the ABI; the fused stencil+transpose needs only t1
