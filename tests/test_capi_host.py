@@ -65,6 +65,10 @@ def test_in_scope_reference_entry_points_present(lib):
     if os.path.exists(REF_HEADER):
         ref = set(header_functions(REF_HEADER))
         assert set(IN_SCOPE) <= ref  # same names as the reference header
+        # the whole reference ABI is declared and exported (periodic, per-system,
+        # IBAT, footprint and bench included)
+        assert not sorted(ref - declared), sorted(ref - declared)
+        assert not sorted(ref - exported(lib.path))
 
 
 def test_status_strings_and_version(lib):
