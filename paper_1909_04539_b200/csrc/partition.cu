@@ -357,7 +357,22 @@ __global__ void __launch_bounds__(128) part_bwd_kernel(double* __restrict__ x, i
   double zu[NU];
 #pragma unroll
   for (int u = 0; u < NU; ++u) zu[u] = 0.0;
-  for (int c = 0; c < R; ++c) {
+  // batches of 16 independent L2 loads in flight (one L2 round trip per
+  // batch instead of per interface value)
+  constexpr int CB = 16;
+  int c0 = 0;
+  for (; c0 + CB <= R; c0 += CB) {
+    double y[CB];
+#pragma unroll
+    for (int c = 0; c < CB; ++c) y[c] = yi[static_cast<long long>(c0 + c) * m + j];
+#pragma unroll
+    for (int u = 0; u < NU; ++u) {
+      const double* row = rinv + rowsel[u] * R + c0;
+#pragma unroll
+      for (int c = 0; c < CB; ++c) zu[u] = fma(__ldg(row + c), y[c], zu[u]);
+    }
+  }
+  for (int c = c0; c < R; ++c) {
     const double y = yi[static_cast<long long>(c) * m + j];
 #pragma unroll
     for (int u = 0; u < NU; ++u) zu[u] = fma(__ldg(rinv + rowsel[u] * R + c), y, zu[u]);
@@ -420,9 +435,10 @@ int partition_blocks(std::size_t n, std::size_t m, int sms, bool pent) {
   // few systems only: below ~one warp of systems per SM the sweep is latency-bound
   // (short systems: three launches cost more than the latency they hide)
   if (!forced && (m > static_cast<std::size_t>(sms) * 64 || n < 1024)) return 0;
-  // pent: each backward thread forms 8 interface values from R^-1 rows, so a
-  // smaller interface system (K <= 8) wins over more blocks (measured)
-  const int kmax = pent ? 8 : kPartMaxR / 2;
+  // each backward thread forms 4 (tri) / 8 (pent) interface values from
+  // R^-1 rows, so a small interface system wins over more blocks (measured at
+  // 4096 x 4096: tri K=16 1.12e11 vs K=32 1.0e11 rows/s; pent K=8 = K=16)
+  const int kmax = pent ? 8 : 16;
   const char* ke = std::getenv("BANDSOLVE_PART_K");  // tuning override (power of two)
   if (ke && std::atoi(ke) >= 2 && std::atoi(ke) <= kmax && static_cast<int>(n) / std::atoi(ke) >= 16)
     return std::atoi(ke);
