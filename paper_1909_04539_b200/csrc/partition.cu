@@ -326,8 +326,10 @@ struct CorrHook {  // stores x_i - (z1_i t1 + z2_i t2)
   }
 };
 
+// (tri: <= 128 registers, 4 CTAs per SM keep 16 blocks x 4096 systems in one
+// wave; pent runs 8 blocks and keeps its registers)
 template <bool PENT, bool PER>
-__global__ void __launch_bounds__(128) part_bwd_kernel(double* __restrict__ x, int n, long long m, long long ld,
+__global__ void __launch_bounds__(128, PENT ? 1 : 4) part_bwd_kernel(double* __restrict__ x, int n, long long m, long long ld,
                                                        int K, int L, const double* __restrict__ fwd,
                                                        const double* __restrict__ bwd,
                                                        const double* __restrict__ fl,
