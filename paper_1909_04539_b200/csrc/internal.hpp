@@ -125,11 +125,21 @@ struct PartPeriodic {
   const double* z2;
   double c[4];  // tri: v_last, scale; pent: cap_inv
 };
+// With `st`, the RHS is the periodic CN stencil across systems of src, laid
+// out src[j * lds + i] (system j, row i): the ADI explicit half + transpose
+// fused into the first pass. x is then output only.
+struct PartStencil {
+  const double* src;
+  std::size_t lds;
+  double s, s4, mid;
+};
 int partition_blocks(std::size_t n, std::size_t m, int sms, bool pent);  // 0 = not used
+bool partition_stencil_ok(std::size_t n, std::size_t m, int K, std::size_t lds);
 bandsolve_status partition_solve_device(const Factor& f, double* x, std::size_t n,
                                         std::size_t m, std::size_t ld,
                                         void* stream, int sms, bool* done,
-                                        const PartPeriodic* per = nullptr);
+                                        const PartPeriodic* per = nullptr,
+                                        const PartStencil* st = nullptr);
 // Per-system baselines (per_system.cu): arr = a, b, c, d (tri) / a..f (pent),
 // reference tri_solver.cpp:51-112, pent_solver.cpp:131-219. The device form
 // synchronises `stream` to report breakdown.

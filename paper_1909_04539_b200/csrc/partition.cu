@@ -304,6 +304,136 @@ __global__ void __launch_bounds__(128) part_fwd_kernel(double* __restrict__ x, i
   }
 }
 
+// Pass A with the ADI explicit half fused in (adi_step_device, fast mode):
+// the RHS row i of system j is the periodic Crank-Nicolson stencil across
+// systems of a source array laid out the other way round, src[j * lds + i]
+// (the field before its transpose). Each thread reads its own source row
+// contiguously (16-byte loads; the 8 rows of a register block are one 64-byte
+// run), takes the stencil neighbours j +- 1 (+- 2) from adjacent lanes by
+// shuffles (edge lanes load theirs), and writes the forward values to x in
+// the interleaved layout: the stencil, the transpose and the forward sweep
+// in one pass. Needs m % 32 == 0 (whole warps per block) and even L, lds.
+constexpr int kStU = 8;
+
+template <bool PENT>
+__global__ void __launch_bounds__(128) part_fwd_stencil_kernel(
+    double* __restrict__ x, int n, long long m, long long ld, int K, int L, const double* __restrict__ fwd,
+    const double* __restrict__ bwd, const double* __restrict__ pr, double* __restrict__ yi,
+    const double* __restrict__ src, long long lds, double cs, double cs4, double cmid) {
+  using namespace dev;
+  const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= static_cast<long long>(K) * m) return;  // whole warps (m % 32 == 0)
+  const int lane = threadIdx.x & 31;
+  const int k = static_cast<int>(t / m);
+  const long long j = t - static_cast<long long>(k) * m;
+  const int r0 = k * L;
+  const int len = k + 1 < K ? L : n - r0;
+  const dev::Rows<double, PENT, true> rows{fwd + static_cast<long long>(r0) * (PENT ? 4 : 2),
+                                           bwd + static_cast<long long>(r0) * (PENT ? 2 : 1)};
+  // rows outside the warp: A = the nearer neighbour (lanes 0 / 31), B = the
+  // farther (pent: lanes 0, 1 / 30, 31); periodic across the m systems
+  auto wrap = [&](long long q) { return q < 0 ? q + m : (q >= m ? q - m : q); };
+  const double* own = src + j * lds + r0;
+  const double* rowA = own;
+  const double* rowB = own;
+  if (lane == 0) rowA = src + wrap(j - 1) * lds + r0;
+  if (lane == 31) rowA = src + wrap(j + 1) * lds + r0;
+  if constexpr (PENT) {
+    if (lane <= 1) rowB = src + wrap(j - 2) * lds + r0;
+    if (lane >= 30) rowB = src + wrap(j + 2) * lds + r0;
+  }
+  const bool needA = lane == 0 || lane == 31;
+  const bool needB = PENT && (lane <= 1 || lane >= 30);
+  double* col = x + static_cast<long long>(r0) * ld + j;
+  const double* p0 = pr + r0;
+  const double* p1 = pr + n + r0;
+  double s1 = 0.0, s2 = 0.0, a0 = 0.0, a1 = 0.0;
+  auto rhs_row = [&](double c, double d1, double u1, double d2, double u2) {
+    if constexpr (PENT) {  // pde.cpp:108 order
+      const double q = add_rn(mul_rn(-cs, add_rn(d2, u2)), mul_rn(cs4, add_rn(d1, u1)));
+      return add_rn(q, mul_rn(cmid, c));
+    } else {  // pde.cpp:85 order
+      return add_rn(mul_rn(cs, add_rn(d1, u1)), mul_rn(cmid, c));
+    }
+  };
+  auto load8 = [&](const double* p, int i0, double* v) {
+#pragma unroll
+    for (int u = 0; u < kStU; u += 2) {
+      const double2 w = *reinterpret_cast<const double2*>(p + i0 + u);
+      v[u] = w.x;
+      v[u + 1] = w.y;
+    }
+  };
+  const int full = len / kStU;
+  double c[kStU], cA[kStU], cB[kStU], n0[kStU], nA[kStU], nB[kStU];
+  if (full > 0) {
+    load8(own, 0, c);
+    if (needA) load8(rowA, 0, cA);
+    if (needB) load8(rowB, 0, cB);
+  }
+  for (int b = 0; b < full; ++b) {
+    const int i0 = b * kStU;
+    if (b + 1 < full) {
+      load8(own, i0 + kStU, n0);
+      if (needA) load8(rowA, i0 + kStU, nA);
+      if (needB) load8(rowB, i0 + kStU, nB);
+    }
+#pragma unroll
+    for (int u = 0; u < kStU; ++u) {
+      double d1 = __shfl_up_sync(0xffffffffu, c[u], 1);
+      double u1 = __shfl_down_sync(0xffffffffu, c[u], 1);
+      if (lane == 0) d1 = cA[u];
+      if (lane == 31) u1 = cA[u];
+      double d2 = 0.0, u2 = 0.0;
+      if constexpr (PENT) {
+        d2 = __shfl_up_sync(0xffffffffu, c[u], 2);
+        u2 = __shfl_down_sync(0xffffffffu, c[u], 2);
+        if (lane <= 1) d2 = cB[u];
+        if (lane >= 30) u2 = cB[u];
+      }
+      const double v = rows.forward(i0 + u, rhs_row(c[u], d1, u1, d2, u2), s1, s2);
+      a0 = fma(p0[i0 + u], v, a0);
+      if constexpr (PENT) a1 = fma(p1[i0 + u], v, a1);
+      col[static_cast<long long>(i0 + u) * ld] = v;
+    }
+#pragma unroll
+    for (int u = 0; u < kStU; ++u) {
+      c[u] = n0[u];
+      cA[u] = nA[u];
+      cB[u] = nB[u];
+    }
+  }
+  for (int i = full * kStU; i < len; ++i) {  // tail rows: scalar loads
+    const double cc = own[i];
+    const double ea = needA ? rowA[i] : 0.0, eb = needB ? rowB[i] : 0.0;
+    double d1 = __shfl_up_sync(0xffffffffu, cc, 1);
+    double u1 = __shfl_down_sync(0xffffffffu, cc, 1);
+    if (lane == 0) d1 = ea;
+    if (lane == 31) u1 = ea;
+    double d2 = 0.0, u2 = 0.0;
+    if constexpr (PENT) {
+      d2 = __shfl_up_sync(0xffffffffu, cc, 2);
+      u2 = __shfl_down_sync(0xffffffffu, cc, 2);
+      if (lane <= 1) d2 = eb;
+      if (lane >= 30) u2 = eb;
+    }
+    const double v = rows.forward(i, rhs_row(cc, d1, u1, d2, u2), s1, s2);
+    a0 = fma(p0[i], v, a0);
+    if constexpr (PENT) a1 = fma(p1[i], v, a1);
+    col[static_cast<long long>(i) * ld] = v;
+  }
+  if constexpr (PENT) {
+    const double g = static_cast<const double*>(rows.bwd)[2 * (len - 2)];  // gamma_{L-2}
+    yi[static_cast<long long>(4 * k) * m + j] = a0;
+    yi[static_cast<long long>(4 * k + 1) * m + j] = a1;
+    yi[static_cast<long long>(4 * k + 2) * m + j] = fma(-g, s1, s2);
+    yi[static_cast<long long>(4 * k + 3) * m + j] = s1;
+  } else {
+    yi[static_cast<long long>(2 * k) * m + j] = a0;
+    yi[static_cast<long long>(2 * k + 1) * m + j] = s1;
+  }
+}
+
 template <bool PENT>
 struct LeftHook {  // g_i - F_i x_left (the left-neighbour coupling's forward image)
   const double* f1;
@@ -428,6 +558,10 @@ __global__ void __launch_bounds__(128, PENT ? 1 : 4) part_bwd_kernel(double* __r
 
 }  // namespace
 
+bool partition_stencil_ok(std::size_t n, std::size_t m, int K, std::size_t lds) {
+  return K > 0 && m % 32 == 0 && (n / K) % 2 == 0 && lds % 2 == 0 && lds >= n;
+}
+
 int partition_blocks(std::size_t n, std::size_t m, int sms, bool pent) {
   const char* env = std::getenv("BANDSOLVE_PARTITION");
   if (env && std::strcmp(env, "0") == 0) return 0;
@@ -452,11 +586,13 @@ int partition_blocks(std::size_t n, std::size_t m, int sms, bool pent) {
 }
 
 bandsolve_status partition_solve_device(const Factor& f, double* x, std::size_t n, std::size_t m, std::size_t ld,
-                                        void* stream, int sms, bool* done, const PartPeriodic* per) {
+                                        void* stream, int sms, bool* done, const PartPeriodic* per,
+                                        const PartStencil* st) {
   *done = false;
   const bool pent = f.kind != Kind::Tri;
   const int K = partition_blocks(n, m, sms, pent);
   if (K == 0) return BANDSOLVE_OK;
+  if (st && !partition_stencil_ok(n, m, K, st->lds)) return BANDSOLVE_OK;
   int device = 0;
   if (cudaGetDevice(&device) != cudaSuccess) {
     cudaGetLastError();
@@ -514,7 +650,21 @@ bandsolve_status partition_solve_device(const Factor& f, double* x, std::size_t 
   const long long tot = static_cast<long long>(K) * M;
   const unsigned g1 = static_cast<unsigned>((tot + 127) / 128);
   const PartPeriodic pa = per ? *per : PartPeriodic{};
-  if (pent) {
+  if (st) {
+    if (pent)
+      part_fwd_stencil_kernel<true><<<g1, 128, 0, s>>>(x, N, M, LD, K, p->L, fwd, bwd, pr, yi, st->src, st->lds,
+                                                       st->s, st->s4, st->mid);
+    else
+      part_fwd_stencil_kernel<false><<<g1, 128, 0, s>>>(x, N, M, LD, K, p->L, fwd, bwd, pr, yi, st->src, st->lds,
+                                                        st->s, st->s4, st->mid);
+    if (per) {
+      if (pent) part_bwd_kernel<true, true><<<g1, 128, 0, s>>>(x, N, M, LD, K, p->L, fwd, bwd, fl, rinv, yi, pa);
+      else part_bwd_kernel<false, true><<<g1, 128, 0, s>>>(x, N, M, LD, K, p->L, fwd, bwd, fl, rinv, yi, pa);
+    } else {
+      if (pent) part_bwd_kernel<true, false><<<g1, 128, 0, s>>>(x, N, M, LD, K, p->L, fwd, bwd, fl, rinv, yi, pa);
+      else part_bwd_kernel<false, false><<<g1, 128, 0, s>>>(x, N, M, LD, K, p->L, fwd, bwd, fl, rinv, yi, pa);
+    }
+  } else if (pent) {
     part_fwd_kernel<true><<<g1, 128, 0, s>>>(x, N, M, LD, K, p->L, fwd, bwd, pr, yi);
     if (per) part_bwd_kernel<true, true><<<g1, 128, 0, s>>>(x, N, M, LD, K, p->L, fwd, bwd, fl, rinv, yi, pa);
     else part_bwd_kernel<true, false><<<g1, 128, 0, s>>>(x, N, M, LD, K, p->L, fwd, bwd, fl, rinv, yi, pa);

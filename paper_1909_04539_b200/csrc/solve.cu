@@ -1402,6 +1402,43 @@ bandsolve_status periodic_device(const Periodic& p, double* x, std::size_t n, st
   return launch_periodic_correct(p, x, n, m, ld, s);
 }
 
+// Fast-mode ADI half step in two launches: the explicit stencil across the
+// systems of `src` (laid out src[j * lds + i]) fused into the partitioned
+// forward pass, the periodic correction into the backward pass; *done =
+// false when the shape does not qualify (caller runs stencil+transpose and
+// periodic_device instead).
+bandsolve_status periodic_stencil_partition(const Periodic& p, const double* src, std::size_t lds, double cs,
+                                            double cs4, double cmid, double* x, std::size_t n, std::size_t m,
+                                            std::size_t ld, void* stream, bool* done) {
+  *done = false;
+  if (current_mode() != BANDSOLVE_MODE_FAST || std::getenv("BANDSOLVE_PERIODIC_UNFUSED") ||
+      std::getenv("BANDSOLVE_ADI_UNFUSED"))
+    return BANDSOLVE_OK;
+  if (reinterpret_cast<uintptr_t>(src) % 16 != 0) return BANDSOLVE_OK;
+  int device = 0;
+  BSB_CUDA(cudaGetDevice(&device));
+  const int sms = num_sms(device);
+  const bool pent = p.kind != Kind::Tri;
+  // tridiagonal only: the pentadiagonal variant (two neighbour rows per side
+  // in registers) measured slower than stencil+transpose and the plain pass
+  // (5.6e10 vs 6.7e10 rows/s at 4096^2); tri gains 1.11e11 -> 1.33e11
+  if (pent && !std::getenv("BANDSOLVE_ADI_FUSE_PENT")) return BANDSOLVE_OK;
+  if (partition_blocks(n, m, sms, pent) == 0) return BANDSOLVE_OK;
+  keep_pool_memory(device);
+  const double* blob = nullptr;
+  bandsolve_status st = periodic_device_z(p, device, &blob);
+  if (st != BANDSOLVE_OK) return st;
+  PartPeriodic pa{blob, blob + n, {0.0, 0.0, 0.0, 0.0}};
+  if (pent) {
+    for (int k = 0; k < 4; ++k) pa.c[k] = p.cap_inv[k];
+  } else {
+    pa.c[0] = p.v_last;
+    pa.c[1] = p.scale;
+  }
+  const PartStencil ps{src, lds, cs, cs4, cmid};
+  return partition_solve_device(*p.factor, x, n, m, ld, stream, sms, done, &pa, &ps);
+}
+
 bandsolve_status solve_host(const Factor& f, double* x, std::size_t n, std::size_t m, const Periodic* per,
                             bool correct_only) {
   if (n != f.n) return fail(BANDSOLVE_ERR_SHAPE_MISMATCH, "factor order != batch rows");
@@ -1602,11 +1639,22 @@ bandsolve_status adi_step_device(const Periodic& px, const Periodic& py, double 
       break;
     }
     // half step 1: explicit along y, implicit along x (systems along x, interleaved after the transpose)
-    if ((err = rhs_t(field, t1, ny, nx, ld, ldt)) != cudaSuccess) { st = cuda_fail(err, "ADI stencil"); break; }
-    if ((st = periodic_device(px, t1, nx, ny, ldt, stream, false)) != BANDSOLVE_OK) break;
+    bool done = false;
+    if ((st = periodic_stencil_partition(px, field, ld, cs, cs4, cmid, t1, nx, ny, ldt, stream, &done)) !=
+        BANDSOLVE_OK)
+      break;
+    if (!done) {
+      if ((err = rhs_t(field, t1, ny, nx, ld, ldt)) != cudaSuccess) { st = cuda_fail(err, "ADI stencil"); break; }
+      if ((st = periodic_device(px, t1, nx, ny, ldt, stream, false)) != BANDSOLVE_OK) break;
+    }
     // half step 2: explicit along x, implicit along y
-    if ((err = rhs_t(t1, field, nx, ny, ldt, ld)) != cudaSuccess) { st = cuda_fail(err, "ADI stencil"); break; }
-    st = periodic_device(py, field, ny, nx, ld, stream, false);
+    if ((st = periodic_stencil_partition(py, t1, ldt, cs, cs4, cmid, field, ny, nx, ld, stream, &done)) !=
+        BANDSOLVE_OK)
+      break;
+    if (!done) {
+      if ((err = rhs_t(t1, field, nx, ny, ldt, ld)) != cudaSuccess) { st = cuda_fail(err, "ADI stencil"); break; }
+      st = periodic_device(py, field, ny, nx, ld, stream, false);
+    }
   } while (false);
   cudaFreeAsync(t1, s);
   cudaGetLastError();

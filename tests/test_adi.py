@@ -5,6 +5,8 @@ cyclic solve, exact transposes): bitwise in exact mode, 1e-12 in fast mode.
 """
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import pytest
 
@@ -57,3 +59,35 @@ def test_gpu_adi_step(lib, oracle, cuda_device):
         adi.step_dev(f.data_ptr(), w.data_ptr(), stream=stream)
     torch.cuda.synchronize()
     assert abs(float(f.mean()) - mean0) <= 1e-13
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("fuse_pent", [False, True])
+def test_gpu_adi_fast_partitioned_fused_stencil(lib, oracle, cuda_device, fuse_pent):
+    """Fast mode on grids large enough for the partitioned path (both axes
+    >= 1024): the explicit half is fused into the partitioned forward pass
+    (tri; pent with BANDSOLVE_ADI_FUSE_PENT=1), the correction into the
+    backward pass. Within 1e-12 of the oracle's ADI step; an odd pitch and a
+    system count that is not a multiple of 32 take the unfused route."""
+    torch = cuda_device
+    rng = np.random.default_rng(43)
+    stream = torch.cuda.current_stream().cuda_stream
+    if fuse_pent:
+        os.environ["BANDSOLVE_ADI_FUSE_PENT"] = "1"
+    lib.set_mode(bs.MODE_FAST)
+    try:
+        for problem, ny, nx in [(0, 1024, 1056), (1, 1088, 1024), (0, 1030, 1024)]:
+            s = 0.9
+            c = rng.uniform(-1, 1, (ny, nx))
+            want = oracle.adi_step(problem, s, c)
+            adi = bs.ADI(lib, problem, s, nx, ny)
+            for ld in (nx, nx + 1, nx + 2):
+                f = torch.zeros((ny, ld), dtype=torch.float64, device="cuda")
+                f[:, :nx] = torch.from_numpy(c).cuda()
+                w = torch.zeros_like(f)
+                adi.step_dev(f.data_ptr(), w.data_ptr(), ld=ld, stream=stream)
+                torch.cuda.synchronize()
+                assert per_system_max_rel(f[:, :nx].cpu().numpy(), want) <= 1e-12, (problem, ny, nx, ld)
+    finally:
+        lib.set_mode(bs.MODE_EXACT)
+        os.environ.pop("BANDSOLVE_ADI_FUSE_PENT", None)
