@@ -544,6 +544,16 @@ Plan choose_plan(std::size_t n, std::size_t m, std::size_t ld, std::size_t elem,
   if (force && std::strcmp(force, "regs") == 0 &&
       plan_regs(n, m, elem, pent, sms, std::max(1, env_int("BANDSOLVE_SWG", 96) / 32), p))
     return p;
+  // Many long systems: once the forward intermediates mostly spill past L2,
+  // the on-chip plans fall below two plain streaming passes (thread per
+  // system in global memory: fwd read+write, bwd read+write at ~0.95 of HBM
+  // each = 0.48 of the 16 B/row roofline). Measured with 2^20 systems:
+  // tri/pent N=1536..4096 fp64 0.47-0.48 vs stream 0.24-0.41; fp32 N>=2048
+  // 0.40 vs 0.15-0.31; at 65536 systems of 2048, 0.42 vs 0.27.
+  if (!force && m >= static_cast<std::size_t>(sms) * 384 && n >= (elem == 8 ? 1536u : 2048u)) {
+    p.why = "many long systems: two streaming passes beat the spilling on-chip plans";
+    return p;
+  }
   // Few long systems (< ~1 warp per SM) take the same order: with the TMEM
   // tier a streaming plan that fits beats the thread-per-system global sweep
   // (ADI axis 4096 x 4096 tri: 1.46x; 4096 x 1024: 1.39x; fp32 1024 x 4096:

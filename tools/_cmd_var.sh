@@ -1,6 +1,12 @@
 cd $GRAFT_REPO_ROOT
-run() { python bench.py --no-cpu --steps 20 --warmup 3 "$@" | python -c "import json,sys,os; d=json.loads(sys.stdin.read()); c=d['config']; print(c['kind'], c['mode'], os.environ.get('BANDSOLVE_PART_K'), '%.3e'%d['value'], '%.3f ms'%d['ms_per_step'], d['gpu_launches'])" "$@"; }
-timeout 600 python -m pytest tests/test_adi.py -q -x 2>&1 | tail -1
-run --config c4tri --mode fast
-run --config c4tri --mode fast
-BANDSOLVE_PART_K=8 run --config c4tri --mode fast
+run() { python bench.py --no-cpu --steps 10 --warmup 3 "$@" | python -c "import json,sys,os; d=json.loads(sys.stdin.read()); c=d['config']; print(c['kind'], c['n'], c['batch_per_gpu'], d['dtype'], c['mode'], os.environ.get('BANDSOLVE_PLAN'), '%.3e'%d['value'], 'frac=%.3f'%d['roofline']['frac'], c['plan'][:30])" "$@"; }
+for m in 16384 65536 262144; do
+  run --config tri512 --n 2048 --m $m
+  BANDSOLVE_PLAN=global run --config tri512 --n 2048 --m $m
+done
+run --config tri512 --n 1536 --m 1048576
+BANDSOLVE_PLAN=global run --config tri512 --n 1536 --m 1048576
+BANDSOLVE_PLAN=global run --config tri512 --n 2048 --m 1048576 --f32
+BANDSOLVE_PLAN=global run --config tri512 --n 4096 --m 1048576 --f32
+BANDSOLVE_PLAN=global run --config tri512 --n 1024 --m 1048576 --f32
+BANDSOLVE_PLAN=global run --config tri512 --n 2048 --m 1048576 --mode fast
