@@ -152,3 +152,28 @@ def test_partition_periodic_fused_within_tolerance(lib, oracle, cuda_device, for
                 torch.cuda.synchronize()
                 got = buf[:, :m].cpu().numpy()
                 assert per_system_max_rel(got, want) <= TOL_F64, (n, m, ld, bands)
+
+
+def test_partition_through_host_api(lib, oracle, cuda_device):
+    """The reference-facing host call (pinned batch staged in column chunks)
+    takes the partitioned path per chunk in fast mode; within 1e-12."""
+    rng = np.random.default_rng(91)
+    n, m = 2048, 700
+    rhs = rng.uniform(-1, 1, (n, m))
+    tb = _random_tri(rng, n)
+    b = bs.Batch.from_array(lib, rhs)
+    bs.TriFactor(lib, *tb).solve(b)
+    want = oracle.tri_solve(oracle.tri_prefactor(*tb), rhs.copy())
+    assert per_system_max_rel(b.array, want) <= TOL_F64
+    pb = _random_pent(rng, n)
+    b = bs.Batch.from_array(lib, rhs)
+    bs.PentFactor(lib, *pb).solve(b)
+    want = oracle.pent_solve(oracle.pent_prefactor(*pb), rhs.copy())
+    assert per_system_max_rel(b.array, want) <= TOL_F64
+    os.environ["BANDSOLVE_HOST_CHUNK_MIB"] = "1"  # many small chunks: m per chunk = 64
+    try:
+        b = bs.Batch.from_array(lib, rhs)
+        bs.PentFactor(lib, *pb).solve(b)
+        assert per_system_max_rel(b.array, want) <= TOL_F64
+    finally:
+        os.environ.pop("BANDSOLVE_HOST_CHUNK_MIB", None)
