@@ -6,10 +6,11 @@
  * ownership and status semantics as the reference header
  * /root/reference/proj/include/bandsolve.h (cited per entry point as
  * "ref bandsolve.h:<line>", with the implementing reference source). A
- * caller linked against libbandsolve.so.1 can relink against
- * libbandsolve_b200.so for these entry points unchanged. The reference's
- * per-system, IBAT, footprint and benchmark-driver entry points are outside
- * this library's scope.
+ * caller linked against libbandsolve.so.1 runs unchanged against this
+ * library: all 37 reference entry points are implemented (shared, uniform and
+ * per-system solves, periodic corrections, IBAT I/O, footprint, the
+ * Crank-Nicolson benchmark driver and the residuals). The build also installs
+ * the reference SONAME alias libbandsolve.so.1.
  *
  * The second part ("B200 extensions") adds device-resident entry points for
  * callers that keep their batch in HBM: they take a device pointer, a row

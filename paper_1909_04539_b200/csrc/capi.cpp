@@ -369,11 +369,10 @@ BSB_API bandsolve_status bandsolve_periodic_pent_correct_dev(const bandsolve_per
 // ---- Crank-Nicolson (capi.cpp:300-411) ------------------------------------------
 BSB_API bandsolve_status bandsolve_footprint(bandsolve_storage_variant variant, size_t n, size_t m,
                                              uint64_t* elements, double* reduction_vs_baseline) {
-  // batch.cpp:72-105
-  if (!elements) return null_arg();
-  if (n < 2 || m < 1) return bsb::fail(BANDSOLVE_ERR_BAD_ARG, "footprint needs n >= 2, m >= 1");
-  const uint64_t un = n, um = m;
+  // capi.cpp:300-325 -> batch.cpp:72-105: the variant is checked first, then
+  // the shape; either out-parameter may be NULL (only the non-NULL ones are written)
   uint64_t count = 0, baseline = 0;
+  const uint64_t un = n, um = m;
   switch (variant) {
     case BANDSOLVE_STORAGE_TRI_PER_SYSTEM: count = baseline = 4 * um * un; break;
     case BANDSOLVE_STORAGE_TRI_SHARED: count = 3 * un + un * um; baseline = 4 * um * un; break;
@@ -382,7 +381,8 @@ BSB_API bandsolve_status bandsolve_footprint(bandsolve_storage_variant variant, 
     case BANDSOLVE_STORAGE_PENT_UNIFORM: count = 4 * un + un * um; baseline = 6 * um * un; break;
     default: return bsb::fail(BANDSOLVE_ERR_BAD_ARG, "unknown storage variant");
   }
-  *elements = count;
+  if (n < 2 || m < 1) return bsb::fail(BANDSOLVE_ERR_BAD_ARG, "footprint needs n >= 2, m >= 1");
+  if (elements) *elements = count;
   if (reduction_vs_baseline)
     *reduction_vs_baseline = 1.0 - static_cast<double>(count) / static_cast<double>(baseline);
   return BANDSOLVE_OK;

@@ -5,6 +5,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <deque>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -52,7 +53,9 @@ struct Factor {
   std::vector<double> bands;
 
   mutable std::mutex mu;
-  mutable std::vector<DeviceFactor> devices;  // one entry per touched device
+  // one entry per touched device; a deque so that an entry handed out to one
+  // thread never moves when another thread adds a device
+  mutable std::deque<DeviceFactor> devices;
   mutable std::vector<std::unique_ptr<PartPlan, PartPlanDeleter>> parts;
   ~Factor();
 };

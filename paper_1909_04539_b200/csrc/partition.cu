@@ -42,6 +42,8 @@
 
 namespace bsb {
 
+cudaError_t upload_sync(void* dst, const void* src, std::size_t bytes);  // solve.cu
+
 struct PartPlan {
   int K = 0, R = 0, L = 0;
   bool pent = false;
@@ -67,6 +69,11 @@ void PartPlanDeleter::operator()(PartPlan* p) const { delete p; }
 namespace {
 
 constexpr int kPartMaxR = 64;  // interface-system order cap (R^-1 rows read per thread)
+// Largest accepted growth of the block eliminations (pivot reciprocal x band
+// scale, spike / U^-1 / interface-inverse entries). Diagonally dominant and
+// the SPD stencil matrices stay below ~10; 1e6 keeps the rounding
+// amplification of the partitioned path well inside the 1e-12 contract.
+constexpr double kPartMaxGrowth = 1e6;
 
 // block factor forward / backward (any rounding: fast path), in place
 void tri_block_fwd(const Factor& f, double* v) {
@@ -151,6 +158,19 @@ std::unique_ptr<PartPlan, PartPlanDeleter> build_plan(const Factor& f, int K) {
     }
     clear_error();
     if (st != BANDSOLVE_OK) return p;
+    // A block k > 0 is not a leading principal submatrix: its unpivoted
+    // elimination can meet a tiny pivot even when the sequential factor is
+    // well conditioned (e.g. a near-zero diagonal entry at a block start).
+    // Reject block pivots that grow the elimination beyond kPartMaxGrowth
+    // relative to the band scale; the sequential sweep then runs instead.
+    {
+      double scale = 0.0, inv_max = 0.0;
+      for (int q = 0; q < nb; ++q)
+        for (int i = 0; i < Lk; ++i) scale = std::max(scale, std::abs(bb[q][i]));
+      const std::vector<double>& inv = pent ? fb->inv_alpha : fb->inv_denom;
+      for (int i = 0; i < Lk; ++i) inv_max = std::max(inv_max, std::abs(inv[i]));
+      if (!(scale * inv_max < kPartMaxGrowth)) return p;
+    }
     // packed fast records (same layout as solve.cu pack_*: fwd {a m, m} /
     // {e ia, b ia, ia, 0}; bwd chat / {gamma, delta})
     for (int i = 0; i < Lk; ++i) {
@@ -233,7 +253,7 @@ std::unique_ptr<PartPlan, PartPlanDeleter> build_plan(const Factor& f, int K) {
       }
     }
   }
-  if (!(worst < 1e100)) return p;  // growth: leave it to the sequential sweep
+  if (!(worst < kPartMaxGrowth)) return p;  // growth: leave it to the sequential sweep
   const int r = p->R;
   std::vector<int> perm;
   if (!lu_factor(R, perm, r)) return p;
@@ -253,7 +273,7 @@ std::unique_ptr<PartPlan, PartPlanDeleter> build_plan(const Factor& f, int K) {
     }
     for (int i = 0; i < r; ++i) {
       p->rinv[static_cast<std::size_t>(i) * r + c] = w[i];
-      if (!(std::abs(w[i]) < 1e100)) return p;
+      if (!(std::abs(w[i]) < kPartMaxGrowth)) return p;
     }
   }
   p->ok = true;
@@ -623,7 +643,7 @@ bandsolve_status partition_solve_device(const Factor& f, double* x, std::size_t 
       }
       char* c = static_cast<char*>(blob);
       for (const auto* v : {&p->fwd, &p->bwd, &p->fl, &p->pr, &p->rinv}) {
-        if (cudaMemcpy(c, v->data(), v->size() * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess) {
+        if (upload_sync(c, v->data(), v->size() * sizeof(double)) != cudaSuccess) {
           cudaGetLastError();
           cudaFree(blob);
           return fail(BANDSOLVE_ERR_INTERNAL, "partition plan upload");

@@ -48,6 +48,21 @@ bandsolve_status cuda_fail(cudaError_t err, const char* what) {
     if (err_ != cudaSuccess) return cuda_fail(err_, #call); \
   } while (0)
 
+// Upload of a per-device constant (factor records, correction vectors,
+// partition plans) that later solves read from ANY stream. A pageable
+// cudaMemcpy may return before its DMA lands, and kernels on non-blocking
+// streams are not ordered after the legacy stream, so the copy goes through a
+// private stream that is synchronised before the pointer is published.
+cudaError_t upload_sync(void* dst, const void* src, std::size_t bytes) {
+  cudaStream_t s = nullptr;
+  cudaError_t e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return e;
+  e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s);
+  const cudaError_t e2 = cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
+  return e != cudaSuccess ? e : e2;
+}
+
 int device_count_cached() {
   static int count = [] {
     int c = 0;
@@ -151,7 +166,7 @@ bandsolve_status ensure_device_factor(const Factor& f, int device, const DeviceF
   DeviceFactor d;
   d.device = device;
   BSB_CUDA(cudaMalloc(&d.base, total));
-  cudaError_t err = cudaMemcpy(d.base, blob.data(), total, cudaMemcpyHostToDevice);
+  cudaError_t err = upload_sync(d.base, blob.data(), total);
   if (err != cudaSuccess) {
     cudaFree(d.base);
     return cuda_fail(err, "factor upload");
@@ -162,7 +177,7 @@ bandsolve_status ensure_device_factor(const Factor& f, int device, const DeviceF
       d.fwd[p][q] = base + off_f[p][q];
       d.bwd[p][q] = base + off_b[p][q];
     }
-  f.devices.push_back(d);
+  f.devices.push_back(d);  // a deque: earlier entries never move
   *out = &f.devices.back();
   return BANDSOLVE_OK;
 }
@@ -1044,19 +1059,38 @@ struct StageContext {
   void* buf[kStages] = {};
   std::size_t cap[kStages] = {};
 };
-// Intentionally never destroyed: CUDA may already be torn down at thread exit.
-thread_local std::vector<StageContext*> t_contexts;
+// Freed when the thread exits (its streams and staging buffers). CUDA calls
+// made after the runtime has been unloaded at process exit just return
+// cudaErrorCudartUnloading, so the release is safe at any point.
+struct StageContexts {
+  std::vector<StageContext*> list;
+  ~StageContexts() {
+    for (StageContext* c : list) {
+      int prev = -1;
+      if (cudaGetDevice(&prev) == cudaSuccess && prev != c->device) cudaSetDevice(c->device);
+      for (int s = 0; s < kStages; ++s) {
+        if (c->streams[s]) cudaStreamSynchronize(c->streams[s]);
+        if (c->buf[s]) cudaFree(c->buf[s]);
+        if (c->streams[s]) cudaStreamDestroy(c->streams[s]);
+      }
+      if (prev >= 0 && prev != c->device) cudaSetDevice(prev);
+      delete c;
+    }
+    cudaGetLastError();
+  }
+};
+thread_local StageContexts t_contexts;
 
 bandsolve_status stage_context(int device, StageContext** out) {
-  for (StageContext* c : t_contexts)
+  for (StageContext* c : t_contexts.list)
     if (c->device == device) {
       *out = c;
       return BANDSOLVE_OK;
     }
   auto* c = new StageContext;
   c->device = device;
+  t_contexts.list.push_back(c);  // owned from here on, even if a stream fails below
   for (int s = 0; s < kStages; ++s) BSB_CUDA(cudaStreamCreateWithFlags(&c->streams[s], cudaStreamNonBlocking));
-  t_contexts.push_back(c);
   *out = c;
   return BANDSOLVE_OK;
 }
@@ -1210,7 +1244,7 @@ bandsolve_status periodic_device_z(const Periodic& p, int device, const double**
   std::memcpy(host.data() + 2 * n, p.fused.data(), p.fused.size() * sizeof(double));
   double* d = nullptr;
   BSB_CUDA(cudaMalloc(&d, host.size() * sizeof(double)));
-  cudaError_t err = cudaMemcpy(d, host.data(), host.size() * sizeof(double), cudaMemcpyHostToDevice);
+  cudaError_t err = upload_sync(d, host.data(), host.size() * sizeof(double));
   if (err != cudaSuccess) {
     cudaFree(d);
     return cuda_fail(err, "periodic z upload");
@@ -1758,7 +1792,7 @@ bandsolve_status bench_run_device(const bandsolve_bench_params& prm, bandsolve_b
   if (err == cudaSuccess && per_sys) {
     err = cudaMalloc(&dbands, (nb * n + static_cast<std::size_t>(nb) * n * ld) * sizeof(double));
     if (err == cudaSuccess)
-      err = cudaMemcpy(dbands, per->factor->bands.data(), nb * n * sizeof(double), cudaMemcpyHostToDevice);
+      err = cudaMemcpyAsync(dbands, per->factor->bands.data(), nb * n * sizeof(double), cudaMemcpyHostToDevice, s);
   }
   if (err == cudaSuccess) err = cudaMalloc(&du, bytes);
   if (err == cudaSuccess) err = cudaMalloc(&ds, bytes);

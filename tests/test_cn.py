@@ -63,6 +63,16 @@ def test_footprint_matches_reference(lib, reflib):
             assert lib.footprint(v, n, m) == reflib.footprint(v, n, m), (v, n, m)
     with pytest.raises(bs.BandsolveError):
         lib.footprint(0, 1, 1)
+    # either out-parameter may be NULL (reference capi.cpp:320-323): the same
+    # statuses and the same reduction as the reference
+    import ctypes as C
+    for L in (lib, reflib):
+        red = C.c_double(-1.0)
+        assert L.lib.bandsolve_footprint(3, 512, 4096, None, C.byref(red)) == bs.OK
+        assert red.value == reflib.footprint(3, 512, 4096)[1]
+        assert L.lib.bandsolve_footprint(3, 512, 4096, None, None) == bs.OK
+        assert L.lib.bandsolve_footprint(9, 512, 4096, None, None) == bs.ERR_BAD_ARG
+        assert L.lib.bandsolve_footprint(3, 1, 4096, None, None) == bs.ERR_BAD_ARG
 
 
 @pytest.mark.gpu

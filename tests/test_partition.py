@@ -172,8 +172,37 @@ def test_partition_through_host_api(lib, oracle, cuda_device):
     assert per_system_max_rel(b.array, want) <= TOL_F64
     os.environ["BANDSOLVE_HOST_CHUNK_MIB"] = "1"  # many small chunks: m per chunk = 64
     try:
+        # the planner must pick the partitioned path for a chunk's shape, and
+        # every chunk must launch exactly its two partitioned passes
+        assert lib.describe_plan(bs.KIND_PENT, n, 64).startswith("partition"), lib.describe_plan(bs.KIND_PENT, n, 64)
+        chunks = -(-m // 64)
         b = bs.Batch.from_array(lib, rhs)
-        bs.PentFactor(lib, *pb).solve(b)
+        f = bs.PentFactor(lib, *pb)
+        before = lib.kernel_launches()
+        f.solve(b)
+        assert lib.kernel_launches() - before == 2 * chunks
         assert per_system_max_rel(b.array, want) <= TOL_F64
     finally:
         os.environ.pop("BANDSOLVE_HOST_CHUNK_MIB", None)
+
+
+def test_partition_rejects_growing_block_pivots(lib, oracle, cuda_device):
+    """A block that is not a leading principal submatrix may meet a tiny pivot
+    even when the sequential factor is well conditioned: a near-zero diagonal
+    entry at a block start. The plan must be rejected (sequential
+    sweep instead), so the answer stays within 1e-12 of the reference."""
+    torch = cuda_device
+    os.environ["BANDSOLVE_PARTITION"] = "1"
+    rng = np.random.default_rng(17)
+    n, m = 2048, 256
+    sub = np.full(n, -1.0); sub[0] = 0
+    sup = np.full(n, -1.0); sup[-1] = 0
+    diag = np.full(n, 3.0)
+    for s in range(n // 16, n, n // 16):  # every candidate block start of K <= 16
+        diag[s] = 1e-14
+    rhs = rng.uniform(-1, 1, (n, m))
+    want = oracle.tri_solve(oracle.tri_prefactor(sub, diag, sup), rhs.copy())
+    before = lib.kernel_launches()
+    got = _dev_solve(torch, bs.TriFactor(lib, sub, diag, sup), rhs)
+    assert per_system_max_rel(got, want) <= TOL_F64
+    assert lib.kernel_launches() - before == 1  # the sequential sweep, not the 2 partitioned passes

@@ -233,3 +233,31 @@ def test_gpu_periodic_fused_fast_within_tolerance(lib, oracle, cuda_device, wg):
     finally:
         lib.set_mode(bs.MODE_EXACT)
         set_plan(None)
+
+
+@pytest.mark.gpu
+def test_gpu_fresh_handles_host_api_regression(lib, cuda_device):
+    """Round-1 driver failure: the first host-API solve with a fresh handle read
+    device constants (factor records, z vectors) whose pageable upload had not
+    landed, because the staged solve runs on non-blocking streams. Every fresh
+    handle's first solve must meet the reference's residual (periodic.cpp:131-214,
+    pent_solver.cpp:223-273) -- 50 fresh periodic and plain handles in a row."""
+    n, m = 512, 4096
+    rng = np.random.default_rng(5)
+    rhs = rng.uniform(-1, 1, (n, m))
+    hyper = (1.0, -4.0, 7.0, -4.0, 1.0)
+    full = [np.full(n, v) for v in hyper]
+    full[0][:2] = 0.0
+    full[1][0] = 0.0
+    full[3][-1] = 0.0
+    full[4][-2:] = 0.0
+    ref = bs.Batch.from_array(lib, rhs)
+    for k in range(50):
+        b = bs.Batch.from_array(lib, rhs)
+        bs.PeriodicPent(lib, *hyper, n).solve(b)
+        res = lib.pent_residual(*full, b, ref, cyclic=True)
+        assert res <= 1e-12, (k, "periodic", res)
+        b = bs.Batch.from_array(lib, rhs)
+        bs.PentFactor(lib, *full).solve(b)
+        res = lib.pent_residual(*full, b, ref, cyclic=False)
+        assert res <= 1e-12, (k, "plain", res)
