@@ -6,11 +6,16 @@
     python bench.py --impl reference                                            (CPU reference arm)
 
 A step is one in-place solve of one synthetic batch. Default workload is
-BASELINE.json configs[1]: pentadiagonal shared-LHS, fp64, N = 512 rows,
-65536 systems per GPU, hyperdiffusion LHS sigma_x = 1 (pde.cpp:67-71).
-Multi-GPU: every rank solves its own contiguous shard of the global batch
-(j0 = g*M), no data-path collective ("weak" scaling); NCCL carries only the
-barrier and the max-over-ranks of the device time.
+BASELINE.json configs[4], the configuration the metric is quoted on at
+1/2/4/8 B200: pentadiagonal shared-LHS, fp64, N = 1024 rows, a global batch
+of 2^24 systems (128 GiB) sharded across the GPUs ("strong" scaling: rank g
+of G solves columns [M g/G, M (g+1)/G) of the one global batch, the
+reference's split, parallel.cpp:53-54, via partition.shard_range),
+hyperdiffusion LHS sigma_x = 1 (pde.cpp:67-71). At one GPU the whole
+128 GiB batch is one device-resident in-place buffer (1000x the L2, so every
+step streams from HBM). Other configs (--config) are per-GPU ("weak")
+workloads. No data-path collective: NCCL carries only the start barrier and
+the max-over-ranks of the device time.
 
 Prints one JSON line on rank 0. Fields: value (device-resident, CUDA-event
 timed), e2e (through the reference-facing C ABI with a pinned host batch,
@@ -36,17 +41,23 @@ sys.path.insert(0, REPO)
 METRIC = "batch·N rows solved/s (fp64) and % of HBM roofline at 1/2/4/8 B200 vs CPU ref"
 
 CONFIGS = {
-    # name: (kind, n, systems per GPU, description)
+    # name: (kind, n, systems per GPU, description); STRONG configs give the
+    # GLOBAL batch instead, sharded across the ranks
     "c1": ("tri", 256, 4096, "configs[0]: tridiagonal shared-LHS, N=256, batch=4096, diffusion LHS sigma_x=1"),
     "c2": ("pent", 512, 65536, "configs[1]: pentadiagonal shared-LHS, N=512, batch=65536, hyperdiffusion LHS sigma_x=1"),
     "tri512": ("tri", 512, 1 << 20, "north-star target: tridiagonal N=512, batch=2^20, diffusion LHS sigma_x=1"),
     "pent512": ("pent", 512, 1 << 20, "north-star target: pentadiagonal N=512, batch=2^20, hyperdiffusion sigma_x=1"),
-    "c5": ("pent", 1024, 1 << 21, "configs[4] shard: pentadiagonal N=1024, 2^21 systems per GPU (2^24 at 8 GPUs)"),
+    "c5": ("pent", 1024, 1 << 24, "configs[4]: pentadiagonal shared-LHS, N=1024, batch=2^24 sharded across the "
+                                  "GPUs, hyperdiffusion LHS sigma_x=1"),
+    "c5s": ("pent", 1024, 1 << 21, "configs[4] shard: pentadiagonal N=1024, 2^21 systems per GPU (the 8-GPU shard)"),
     "c4tri": ("tri", 4096, 4096, "configs[3]: 2D ADI step (Peaceman-Rachford, periodic diffusion) on a 4096x4096 "
                                  "grid, tridiagonal solves along both axes"),
     "c4pent": ("pent", 4096, 4096, "configs[3]: 2D ADI step (periodic hyperdiffusion) on a 4096x4096 grid, "
                                    "pentadiagonal solves along both axes"),
 }
+STRONG = {"c5"}
+DEFAULT_CONFIG = "c5"
+E2E_MAX_SYSTEMS = 1 << 21  # pinned host batch per rank for e2e (16 GiB at N=1024): host RAM bound
 SEED = 42
 
 NVML_REASONS = {
@@ -201,7 +212,8 @@ def run_reference_arm(args, rank: int) -> None:
               f"{cores} threads on {os.cpu_count()} host cores")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong" if args.config in STRONG else "weak",
+            "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": desc, "kind": kind, "n": n, "batch": ms},
             "cpu_baseline": {"value": value, "unit": "rows/s", "cores": cores, "kind": lkind, "sample": sample},
             "e2e": {"value": value, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -246,7 +258,14 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
     torch.cuda.set_device(local_rank)
     lib = bs.load()
     lib.set_mode(bs.MODE_FAST if args.mode == "fast" else bs.MODE_EXACT)
-    kind, n, m, desc = CONFIGS[args.config]
+    from paper_1909_04539_b200.partition import shard_range, weak_shard
+
+    kind, n, m_cfg, desc = CONFIGS[args.config]
+    strong = args.config in STRONG
+    # this rank's shard [j0, j1) of the global batch
+    j0, j1 = shard_range(m_cfg, rank, world) if strong else weak_shard(m_cfg, rank)
+    m = j1 - j0
+    m_global = m_cfg if strong else m_cfg * world
     elem = 4 if args.f32 else 8
     dt = torch.float32 if args.f32 else torch.float64
     bands = lhs_for(kind, n)
@@ -261,15 +280,19 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
             raise SystemExit("--periodic is fp64 only")
     else:
         fac = bs.TriFactor(lib, *bands) if kind == "tri" else bs.PentFactor(lib, *bands)
-    j_off = rank * m  # this rank's shard of the global batch
 
-    # Rotating in-place buffers so every timed step streams from HBM: the
-    # working set is >= 4x the 126 MB L2.
+    # Every timed step must stream from HBM: one in-place buffer when it alone
+    # is >= 4x the 126 MB L2 (configs[4]: 128 GiB at one GPU), else rotating
+    # in-place buffers whose working set is >= 4x L2. ADI and CN steps
+    # ping-pong between two buffers.
+    l2 = 132644864
     bytes_per = n * m * elem
-    nbuf = max(2, min(8, -(-4 * 132644864 // bytes_per)))
+    nbuf = 1 if bytes_per >= 4 * l2 else min(8, -(-4 * l2 // bytes_per))
+    if adi or args.cn:
+        nbuf = max(2, nbuf)
     bufs = [torch.empty((n, m), dtype=dt, device="cuda") for _ in range(nbuf)]
     for b in bufs:
-        lib.fill_rhs_dev(b.data_ptr(), n, m, m, SEED, j_off, torch.cuda.current_stream().cuda_stream, f32=args.f32)
+        lib.fill_rhs_dev(b.data_ptr(), n, m, m, SEED, j0, torch.cuda.current_stream().cuda_stream, f32=args.f32)
     stream = torch.cuda.current_stream()
     sptr = stream.cuda_stream
     clocks = ClockSampler(local_rank)
@@ -308,7 +331,7 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
     axes = 2 if adi else 1  # an ADI step solves every grid point along both axes
-    rows_total = float(n) * m * world * args.steps * axes
+    rows_total = float(n) * m_global * args.steps * axes
     value = rows_total / (ms_max / 1e3)
     ms_per_step = ms_max / args.steps
 
@@ -324,10 +347,18 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
     # sweep, D2H inside bandsolve_*_solve_shared, synchronous)
     e2e = None
     if not args.f32 and not args.cn and not adi:
-        host = bs.Batch.from_array(lib, bufs[0].cpu().numpy())
-        e2e_steps = max(1, min(args.steps, 50))
-        for _ in range(min(args.warmup, 3)):
-            fac.solve(host)
+        # pinned host batch of this rank's columns (a leading column sample
+        # when the shard exceeds E2E_MAX_SYSTEMS: host RAM, not the device,
+        # bounds it), regenerated from the same generator indices
+        me = min(m, E2E_MAX_SYSTEMS)
+        host = bs.Batch(lib, n, me)
+        tmp = torch.empty((n, me), dtype=torch.float64, device="cuda")
+        lib.fill_rhs_dev(tmp.data_ptr(), n, me, me, SEED, j0, sptr)
+        torch.from_numpy(host.array).copy_(tmp)
+        del tmp
+        torch.cuda.empty_cache()
+        e2e_steps = max(1, min(args.steps, 50, (32 << 30) // (n * me * 8)))
+        fac.solve(host)  # warm-up
         if world > 1:
             dist.barrier()
         with clocks.window():
@@ -338,9 +369,15 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
         te = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": float(n) * m * world * e2e_steps / float(te.item()), "unit": "rows/s",
-               "h2d_bytes_per_step": n * m * elem, "d2h_bytes_per_step": n * m * elem,
-               "steps": e2e_steps, "api": f"bandsolve_{kind}_solve_shared (pinned host batch)"}
+        me_total = torch.tensor([me], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(me_total, op=dist.ReduceOp.SUM)
+        e2e = {"value": float(n) * float(me_total.item()) * e2e_steps / float(te.item()), "unit": "rows/s",
+               "h2d_bytes_per_step": n * me * elem, "d2h_bytes_per_step": n * me * elem,
+               "steps": e2e_steps, "api": f"bandsolve_{kind}_solve_shared (pinned host batch)",
+               "sample": (f"all {me} systems of the shard" if me == m else
+                          f"columns [{j0}, {j0 + me}) of each rank's shard ({me} of {m} systems: "
+                          f"a {n * me * 8 / 2**30:.0f} GiB pinned host batch per rank)")}
     clk = clocks.summary()
 
     cpu = None
@@ -350,14 +387,15 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong" if strong else "weak",
             "vs_baseline": None, "dtype": "f32" if args.f32 else "f64",
             "data": "synthetic: U(-1,1) RHS from SplitMix64(seed=42, i, global j), generated on device",
-            "config": {"workload": desc, "kind": kind, "n": n, "batch_per_gpu": m, "global_batch": m * world,
+            "config": {"workload": desc, "kind": kind, "n": n, "batch_per_gpu": m, "global_batch": m_global,
                        "mode": args.mode, "plan": plan, "periodic": bool(args.periodic), "cn_step": bool(args.cn),
                        "parallelism": f"dp{world} (systems sharded, no data-path collective)",
-                       "l2": f"{nbuf} rotating in-place buffers of {bytes_per / 2**20:.0f} MiB "
-                             f"(working set {nbuf * bytes_per / 132644864:.1f}x L2)"},
+                       "l2": (f"{nbuf} in-place buffer{'s' if nbuf > 1 else ''} of {bytes_per / 2**20:.0f} MiB "
+                              f"(working set {nbuf * bytes_per / l2:.1f}x L2, inputs larger than L2)")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_bytes_per_launch": algo_bytes, "peak_source": peak_src,
@@ -373,10 +411,10 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
 def main() -> int:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default=DEFAULT_CONFIG)
     ap.add_argument("--mode", choices=["exact", "fast"], default=os.environ.get("BANDSOLVE_BENCH_MODE", "exact"))
     ap.add_argument("--f32", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")

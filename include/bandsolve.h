@@ -410,6 +410,38 @@ bandsolve_status bandsolve_describe_plan(int kind, size_t n, size_t m,
                                          size_t ld, int f32, char* buf,
                                          size_t buflen);
 
+/* Devices the host-batch solves (bandsolve_*_solve_shared, periodic solves
+ * on a bandsolve_batch) spread over: the batch's m systems are split into
+ * contiguous column ranges j0 = m*g/G, one per listed device (the
+ * reference's worker split, parallel.cpp:53-54), each streamed through its
+ * own device's copy/sweep pipeline, all in flight at once. count = 0 (the
+ * default) uses the calling thread's current device. A device may be listed
+ * more than once (independent pipelines on it). Results are bitwise
+ * independent of the list. Ids are checked against the device count at
+ * solve time (BANDSOLVE_ERR_BAD_ARG). Process-wide setting. */
+bandsolve_status bandsolve_set_devices(const int* devices, int count);
+/* Writes up to `capacity` ids to `devices` (may be NULL); returns the count. */
+int bandsolve_get_devices(int* devices, int capacity);
+
+/* Tuning overrides (plans, ring depths, fused/unfused variants; for tests
+ * and tuning runs, never needed for correctness). The table is seeded once,
+ * at first use, from the environment variables BANDSOLVE_<key>; after that
+ * only these calls change it. Keys: PLAN (stream|global|persist|smem|smemW8|
+ * smemW16|smemW32), PWARPS, PTAIL (persist plan); SWG, STAIL, SKB, SKR, SPD,
+ * SV, SRC, SSEG, TM8, TMEM, SSTAG (stream plan: group width, smem tail rows,
+ * b / reload ring slots, L2 prefetch distance, systems per lane, recomputed
+ * rows, recompute segment chunks, TMEM with 5..8 warps, TMEM on/off, start
+ * stagger); PARTITION (0|1), PART_K; CN_UNFUSED, PERIODIC_UNFUSED,
+ * ADI_UNFUSED, ADI_FUSE_PENT (flags: set = on); HOST_CHUNK_MIB (host-batch
+ * staging chunk); L2_SETASIDE (1: grow the device's persisting-L2 limit to
+ * cover the spill scratch; process-wide state, off by default).
+ * value NULL unsets the key. Unknown key -> BANDSOLVE_ERR_BAD_ARG. */
+bandsolve_status bandsolve_tune_set(const char* key, const char* value);
+/* Current value (copied into buf) or BANDSOLVE_ERR_BAD_ARG when unset. */
+bandsolve_status bandsolve_tune_get(const char* key, char* buf, size_t buflen);
+/* Clear every override (the environment is not re-read). */
+void bandsolve_tune_reset(void);
+
 /* Number of this library's kernels launched since load (all threads). */
 uint64_t bandsolve_kernel_launches(void);
 

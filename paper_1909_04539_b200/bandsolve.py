@@ -135,6 +135,11 @@ _EXTENSION_SIGS = [
     ("bandsolve_adi_destroy", None, [_vp]),
     ("bandsolve_adi_step_dev", _st, [_vp, _vp, _vp, _sz, _vp]),
     ("bandsolve_describe_plan", _st, [C.c_int, _sz, _sz, _sz, C.c_int, C.c_char_p, _sz]),
+    ("bandsolve_set_devices", _st, [C.POINTER(C.c_int), C.c_int]),
+    ("bandsolve_get_devices", C.c_int, [C.POINTER(C.c_int), C.c_int]),
+    ("bandsolve_tune_set", _st, [C.c_char_p, C.c_char_p]),
+    ("bandsolve_tune_get", _st, [C.c_char_p, C.c_char_p, _sz]),
+    ("bandsolve_tune_reset", None, []),
     ("bandsolve_kernel_launches", C.c_uint64, []),
     ("bandsolve_last_error", C.c_char_p, []),
 ]
@@ -208,6 +213,31 @@ class Library:
 
     def get_mode(self) -> int:
         return self.lib.bandsolve_get_mode()
+
+    def set_devices(self, devices) -> None:
+        """Device list of the host-batch solves ([] = the current device)."""
+        ids = (C.c_int * max(1, len(devices)))(*devices)
+        self.check(self.lib.bandsolve_set_devices(ids if devices else None, len(devices)), "set_devices")
+
+    def get_devices(self) -> list[int]:
+        n = self.lib.bandsolve_get_devices(None, 0)
+        ids = (C.c_int * max(1, n))()
+        self.lib.bandsolve_get_devices(ids, n)
+        return list(ids[:n])
+
+    def tune(self, key: str, value=None) -> None:
+        """Set (value not None) or unset a tuning override (bandsolve_tune_set)."""
+        v = None if value is None else str(value).encode()
+        self.check(self.lib.bandsolve_tune_set(key.encode(), v), f"tune {key}")
+
+    def tune_get(self, key: str) -> Optional[str]:
+        buf = C.create_string_buffer(256)
+        if self.lib.bandsolve_tune_get(key.encode(), buf, 256) != 0:
+            return None
+        return buf.value.decode()
+
+    def tune_reset(self) -> None:
+        self.lib.bandsolve_tune_reset()
 
     def kernel_launches(self) -> int:
         return int(self.lib.bandsolve_kernel_launches())

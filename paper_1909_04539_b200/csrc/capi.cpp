@@ -616,6 +616,29 @@ BSB_API bandsolve_status bandsolve_describe_plan(int kind, size_t n, size_t m, s
   });
 }
 
+BSB_API bandsolve_status bandsolve_set_devices(const int* devices, int count) {
+  return guarded([&] { return bsb::set_devices(devices, count); });
+}
+
+BSB_API int bandsolve_get_devices(int* devices, int capacity) { return bsb::get_devices(devices, capacity); }
+
+BSB_API bandsolve_status bandsolve_tune_set(const char* key, const char* value) {
+  if (!key) return null_arg();
+  if (!bsb::tune_set(key, value)) return bsb::fail(BANDSOLVE_ERR_BAD_ARG, "unknown tuning key");
+  return BANDSOLVE_OK;
+}
+
+BSB_API bandsolve_status bandsolve_tune_get(const char* key, char* buf, size_t buflen) {
+  if (!key || !buf || buflen == 0) return null_arg();
+  const auto v = bsb::tune_str(key);
+  if (!v) return bsb::fail(BANDSOLVE_ERR_BAD_ARG, "tuning key not set");
+  std::strncpy(buf, v->c_str(), buflen - 1);
+  buf[buflen - 1] = '\0';
+  return BANDSOLVE_OK;
+}
+
+BSB_API void bandsolve_tune_reset(void) { bsb::tune_reset(); }
+
 BSB_API uint64_t bandsolve_kernel_launches(void) { return bsb::kernel_launches(); }
 
 BSB_API const char* bandsolve_last_error(void) { return bsb::last_error(); }

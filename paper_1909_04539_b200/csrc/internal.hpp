@@ -8,8 +8,11 @@
 #include <deque>
 #include <memory>
 #include <mutex>
+#include <optional>
 #include <string>
 #include <vector>
+
+#include <cuda_runtime_api.h>
 
 #include "../../include/bandsolve.h"
 
@@ -116,6 +119,23 @@ void periodic_pent_modified_bands(const Periodic& p, double* a, double* b,
 int current_mode();
 void set_mode(int mode);
 
+// Stream-ordered allocation from the library's own per-device pool (freed
+// blocks stay mapped; the application's default pool is untouched). Free
+// with cudaFreeAsync.
+cudaError_t pool_malloc_async_raw(void** p, std::size_t bytes, cudaStream_t s);
+template <typename T>
+cudaError_t pool_malloc_async(T** p, std::size_t bytes, cudaStream_t s) {
+  return pool_malloc_async_raw(reinterpret_cast<void**>(p), bytes, s);
+}
+
+// Tuning overrides (tuning.cpp): bandsolve_tune_set(), seeded once from the
+// BANDSOLVE_<KEY> environment. tune_flag: the key is set (any value).
+std::optional<std::string> tune_str(const char* key);
+long long tune_int(const char* key, long long dflt);
+bool tune_flag(const char* key);
+bool tune_set(const char* key, const char* value);
+void tune_reset();
+
 // Enqueue an in-place solve of the n x m (pitch ld) device array x.
 bandsolve_status solve_device(const Factor& f, void* x, bool f32,
                               std::size_t n, std::size_t m, std::size_t ld,
@@ -156,6 +176,9 @@ bandsolve_status ibat_read(const char* path, std::size_t* n, std::size_t* m, dou
 // Host batch: staged through the device, synchronous. With `per`, the
 // periodic correction follows the sweep on each staged chunk; with
 // `correct_only`, only the correction runs.
+// Device list of the host-batch solves (empty: the caller's current device).
+bandsolve_status set_devices(const int* ids, int count);
+int get_devices(int* ids, int capacity);
 bandsolve_status solve_host(const Factor& f, double* x, std::size_t n,
                             std::size_t m, const Periodic* per = nullptr,
                             bool correct_only = false);

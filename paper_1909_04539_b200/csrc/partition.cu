@@ -583,10 +583,10 @@ bool partition_stencil_ok(std::size_t n, std::size_t m, int K, std::size_t lds) 
 }
 
 int partition_blocks(std::size_t n, std::size_t m, int sms, bool pent) {
-  const char* env = std::getenv("BANDSOLVE_PARTITION");
-  if (env && std::strcmp(env, "0") == 0) return 0;
-  if (std::getenv("BANDSOLVE_PLAN")) return 0;  // a forced sweep plan (tests / tuning)
-  const bool forced = env && std::strcmp(env, "1") == 0;
+  const long long sel = tune_int("PARTITION", -1);  // 0: never, 1: whenever it applies
+  if (sel == 0) return 0;
+  if (tune_flag("PLAN")) return 0;  // a forced sweep plan (tests / tuning)
+  const bool forced = sel == 1;
   if (n > static_cast<std::size_t>(INT_MAX) || m == 0 || current_mode() != BANDSOLVE_MODE_FAST) return 0;
   // few systems only: below ~one warp of systems per SM the sweep is latency-bound
   // (short systems: three launches cost more than the latency they hide)
@@ -595,9 +595,8 @@ int partition_blocks(std::size_t n, std::size_t m, int sms, bool pent) {
   // R^-1 rows, so a small interface system wins over more blocks (measured at
   // 4096 x 4096: tri K=16 1.12e11 vs K=32 1.0e11 rows/s; pent K=8 = K=16)
   const int kmax = pent ? 8 : 16;
-  const char* ke = std::getenv("BANDSOLVE_PART_K");  // tuning override (power of two)
-  if (ke && std::atoi(ke) >= 2 && std::atoi(ke) <= kmax && static_cast<int>(n) / std::atoi(ke) >= 16)
-    return std::atoi(ke);
+  const int ke = static_cast<int>(tune_int("PART_K", 0));  // tuning override (power of two)
+  if (ke >= 2 && ke <= kmax && static_cast<int>(n) / ke >= 16) return ke;
   int K = 2;
   while (K < kmax && static_cast<std::size_t>(K) * m < static_cast<std::size_t>(sms) * 512 &&
          static_cast<int>(n) / (2 * K) >= 32)
@@ -662,7 +661,7 @@ bandsolve_status partition_solve_device(const Factor& f, double* x, std::size_t 
   const int N = static_cast<int>(n);
   const long long M = static_cast<long long>(m), LD = static_cast<long long>(ld);
   double* yi = nullptr;  // interface values of y, [R][m]
-  if (cudaMallocAsync(reinterpret_cast<void**>(&yi), static_cast<std::size_t>(p->R) * m * sizeof(double), s) !=
+  if (pool_malloc_async(reinterpret_cast<void**>(&yi), static_cast<std::size_t>(p->R) * m * sizeof(double), s) !=
       cudaSuccess) {
     cudaGetLastError();
     return fail(BANDSOLVE_ERR_INTERNAL, "partition scratch");

@@ -168,7 +168,7 @@ bandsolve_status per_system_device(bool pent, double* const* arr, std::size_t n,
   if (device_count_cached() == 0) return fail(BANDSOLVE_ERR_INTERNAL, "no CUDA device available (no CPU fallback)");
   auto s = static_cast<cudaStream_t>(stream);
   int* flag = nullptr;
-  BSB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&flag), sizeof(int), s));
+  BSB_CUDA(pool_malloc_async(reinterpret_cast<void**>(&flag), sizeof(int), s));
   cudaMemsetAsync(flag, 0, sizeof(int), s);
   const unsigned grid = static_cast<unsigned>((m + 127) / 128);
   if (pent)

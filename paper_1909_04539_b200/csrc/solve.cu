@@ -19,7 +19,6 @@
 #include "sweep_kernels.cuh"
 #include "sweep_persist.cuh"
 #include "sweep_stream.cuh"
-#include "sweep_regs.cuh"
 
 namespace bsb {
 
@@ -204,7 +203,7 @@ constexpr std::size_t kSmemPerBlockMax = 232448;  // 227 KB opt-in per CTA
 constexpr std::size_t kSmemReservedPerCta = 1024;
 constexpr double kSpillBudget = 64.0 * (1 << 20);  // bytes of spilled d-hat kept L2-resident (of 126 MB)
 
-enum class PlanKind { Global, Smem, Persist, Stream, Regs };
+enum class PlanKind { Global, Smem, Persist, Stream };
 
 struct Plan {
   PlanKind kind = PlanKind::Global;
@@ -216,6 +215,8 @@ struct Plan {
   int stagger_ns = 0;                  // stream: start delay of odd CTAs
   int V = 1;                           // stream: systems per lane
   int tmem_chunks = 0;                 // stream: head chunks kept in Tensor Memory
+  int rc_chunks = 0;                   // stream: head chunks recomputed from checkpoints (not stored)
+  int seg_chunks = 0;                  // stream: chunks per recomputed segment
   double model_us = 0;       // stream: modelled time
   std::size_t smem_bytes = 0;
   std::string why;
@@ -235,31 +236,51 @@ int num_sms(int device) {
   return v;
 }
 
-// Stream-ordered allocations (spill scratch, residual buffers) come from the
-// device's default pool; keep freed blocks cached so steady-state solves
-// never go back to the driver.
-void keep_pool_memory(int device) {
-  static std::atomic<uint64_t> done{0};
-  const uint64_t bit = device < 64 ? (1ull << device) : 0;
-  if (!bit || (done.load(std::memory_order_relaxed) & bit)) return;
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-    uint64_t threshold = UINT64_MAX;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
+// Stream-ordered allocations (spill scratch, residual buffers, ADI work)
+// come from a pool the library owns, one per device, that keeps freed blocks
+// mapped so steady-state solves never go back to the driver. The
+// application's default pool and its release threshold are left alone.
+cudaMemPool_t library_pool(int device) {
+  static std::mutex mu;
+  static cudaMemPool_t pools[64] = {};
+  if (device < 0 || device >= 64) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!pools[device]) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    cudaMemPool_t pool = nullptr;
+    if (cudaMemPoolCreate(&pool, &props) == cudaSuccess) {
+      uint64_t threshold = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
+      pools[device] = pool;
+    }
+    cudaGetLastError();
   }
-  cudaGetLastError();
-  done.fetch_or(bit, std::memory_order_relaxed);
+  return pools[device];
 }
+
+}  // namespace
+
+cudaError_t pool_malloc_async_raw(void** p, std::size_t bytes, cudaStream_t s) {
+  int device = 0;
+  if (cudaError_t e = cudaGetDevice(&device); e != cudaSuccess) return e;
+  cudaMemPool_t pool = library_pool(device);
+  if (!pool) return cudaMallocAsync(p, bytes, s);
+  return cudaMallocFromPoolAsync(p, bytes, pool, s);
+}
+
+namespace {
 
 // The spill scratch is written and re-read within one tile; its evict_last
 // lines are only protected from the evict-first b/x streams inside the L2
-// persisting set-aside, which is 0 by default. Grow the set-aside (never
-// shrink it) to cover the scratch, up to the device maximum.
-// BANDSOLVE_L2_SETASIDE=0 disables this (the solve stays correct, only the
-// spilled rows may then round-trip through HBM).
+// persisting set-aside, which is 0 by default. Opt-in (tuning key
+// L2_SETASIDE=1, since the limit is process-wide device state): grow the
+// set-aside (never shrink it) to cover the scratch, up to the device maximum.
+// Off, the solve is the same; only spilled rows may round-trip through HBM.
 void ensure_l2_setaside(int device, std::size_t bytes) {
-  const char* env = std::getenv("BANDSOLVE_L2_SETASIDE");
-  if (env && std::strcmp(env, "0") == 0) return;
+  if (tune_int("L2_SETASIDE", 0) == 0) return;
   static std::mutex mu;
   std::lock_guard<std::mutex> lock(mu);
   int max_persist = 0;
@@ -301,8 +322,9 @@ bool plan_persist(std::size_t n, std::size_t elem, bool pent, bool fast, int sms
   const int tail_full_chunks = static_cast<int>((n + dev::kRT - 1) / dev::kRT);
   const int need_sys = static_cast<int>(2.0 * 1.125 * chain_cycles(pent, fast, elem));
   int target = std::max(2, std::min(dev::kMaxWarps, (need_sys + dev::kPW - 1) / dev::kPW));
-  if (const char* e = std::getenv("BANDSOLVE_PWARPS")) target = std::max(1, std::min(dev::kMaxWarps, std::atoi(e)));
-  const int forced_tail = std::getenv("BANDSOLVE_PTAIL") ? std::atoi(std::getenv("BANDSOLVE_PTAIL")) : -1;
+  const bool forced_warps = tune_flag("PWARPS");
+  if (forced_warps) target = std::max(1, std::min(dev::kMaxWarps, static_cast<int>(tune_int("PWARPS", 1))));
+  const int forced_tail = static_cast<int>(tune_int("PTAIL", -1));
 
   auto fit = [&](int warps, int H, int TC) {
     return dev::PersistLayout::make(static_cast<int>(n), H, TC, warps, elem, fr, br).total <= kSmemPerBlockMax;
@@ -344,7 +366,7 @@ bool plan_persist(std::size_t n, std::size_t elem, bool pent, bool fast, int sms
     }
     if (best_tc < 0) continue;
     const double spill = static_cast<double>(warps) * dev::kPW * sms * p.H * elem;
-    if (spill <= kSpillBudget || warps == 1 || forced_tail >= 0 || std::getenv("BANDSOLVE_PWARPS")) {
+    if (spill <= kSpillBudget || warps == 1 || forced_tail >= 0 || forced_warps) {
       p.kind = PlanKind::Persist;
       p.warps = warps;
       p.TC = best_tc;
@@ -384,10 +406,7 @@ double stream_spill_factor(double spill_mb) {
   return pts[np - 1][1];
 }
 
-int env_int(const char* name, int dflt) {
-  const char* e = std::getenv(name);
-  return e ? std::atoi(e) : dflt;
-}
+int env_int(const char* key, int dflt) { return static_cast<int>(tune_int(key, dflt)); }
 
 // Streaming plan (sweep_stream.cuh): pick the systems per lane V, the group
 // width Wg (systems per SM in flight), the head/tail split and the ring
@@ -395,23 +414,27 @@ int env_int(const char* name, int dflt) {
 //   frac = compute(S) x spill_factor(spill) x (round utilisation),
 // preferring the smaller spill on ties.
 bool plan_stream(std::size_t n, std::size_t m, std::size_t elem, bool pent, bool fast, int sms, Plan& p,
-                 int per_arrays = 0, bool allow_tmem = true, int only_wg = 0) {
+                 int per_arrays = 0, bool allow_tmem = true, int only_wg = 0, bool allow_rc = false) {
   const std::size_t fr = fwd_rec_bytes(pent, elem), br = bwd_rec_bytes(pent, elem);
   const std::size_t fac = dev::align128(n * fr) + dev::align128(n * br);
   if (fac > kSmemPerBlockMax / 2 || n < 2) return false;
-  const int forced_wg = only_wg ? only_wg : env_int("BANDSOLVE_SWG", 0);
-  const int forced_tail = env_int("BANDSOLVE_STAIL", -1);
+  const int forced_wg = only_wg ? only_wg : env_int("SWG", 0);
+  const int forced_tail = env_int("STAIL", -1);
   // KR = 0: one FIFO ring of KB slots carries both the b chunks and the
   // spill reloads (every slot serves whichever head phase is running)
-  const int KB = std::max(1, env_int("BANDSOLVE_SKB", 4));
-  const int KR = std::max(0, env_int("BANDSOLVE_SKR", 4));
-  const int PD = std::max(0, env_int("BANDSOLVE_SPD", 4));
+  const int KB = std::max(1, env_int("SKB", 4));
+  const int KR = std::max(0, env_int("SKR", 4));
+  const int PD = std::max(0, env_int("SPD", 4));
+  // recompute tier (plain solves only): rows forced by BANDSOLVE_SRC (-1: none)
+  const int forced_rc = allow_rc ? env_int("SRC", -1) : -1;
+  const int forced_seg = env_int("SSEG", 0);
+  const bool tm8 = allow_rc && env_int("TM8", 0) != 0;  // TMEM tier with 5..8 compute warps
   const int N = static_cast<int>(n);
   bool found = false;
   double best_t = 1e300;
   double best_spill = 1e300;
   int tmem_pick = 0;
-  const int forced_v = env_int("BANDSOLVE_SV", 0);
+  const int forced_v = env_int("SV", 0);
   for (int cand = 0; cand < 16; ++cand) {
     const int V = cand < 8 ? 1 : 2;
     const int P = cand < 8 ? cand + 1 : cand - 7;
@@ -421,8 +444,18 @@ bool plan_stream(std::size_t n, std::size_t m, std::size_t elem, bool pent, bool
     if (forced_wg && Wg != forced_wg) continue;
     const long long groups = (static_cast<long long>(m) + Wg - 1) / Wg;
     const long long grid = std::min<long long>(sms, groups);
+    const bool tm_ok = allow_tmem && V == 1 && (P <= 4 || tm8) && env_int("TMEM", 1) != 0;
+    const int tcap = tm_ok ? dev::stream_tmem_cap_chunks(P, elem) : 0;
+    // recompute chunks / segment chunks for a head of h rows
+    auto rc_for = [&](int h) {
+      if (forced_rc < 0 || tcap == 0) return 0;
+      return std::max(0, std::min(forced_rc / dev::kSR, h / dev::kSR - std::min(h / dev::kSR, tcap)));
+    };
+    const int seg = std::max(1, std::min(tcap, forced_seg > 0 ? forced_seg : tcap));
+    auto ckpts_for = [&](int rc) { return rc > 0 ? (rc + seg - 1) / seg - 1 : 0; };
     auto fits = [&](int H, int TC) {
-      return dev::StreamLayout::make(N, H, TC, Wg, KB, KR, elem, fr, br, per_arrays).total <= kSmemPerBlockMax;
+      return dev::StreamLayout::make(N, H, TC, Wg, KB, KR, elem, fr, br, per_arrays, ckpts_for(rc_for(H))).total <=
+             kSmemPerBlockMax;
     };
     int H = -1;
     const int all_tc = (N + dev::kSR - 1) / dev::kSR;
@@ -448,21 +481,21 @@ bool plan_stream(std::size_t n, std::size_t m, std::size_t elem, bool pent, bool
     if (H < 0) continue;
     const int TC = (N - H + dev::kSR - 1) / dev::kSR;
     // TMEM tier (V = 1, one warp per TMEM lane quadrant): up to 2 KB per system
-    int rtc = 0;
-    if (allow_tmem && V == 1 && P <= 4 && env_int("BANDSOLVE_TMEM", 1) != 0)
-      rtc = std::min(H / dev::kSR, static_cast<int>(2048 / (dev::kSR * elem)));
-    const double spill = static_cast<double>(grid) * Wg * (H - rtc * dev::kSR) * elem;
+    const int rc = rc_for(H);
+    const int rtc = std::min(H / dev::kSR - rc, tcap);
+    const double spill = static_cast<double>(grid) * Wg * (H - (rtc + rc) * dev::kSR) * elem;
     const double rounds = static_cast<double>(m) / (static_cast<double>(Wg) * sms);
     const double util = rounds / std::ceil(rounds);
     const double frac = stream_compute_frac(Wg, pent, fast) * (V == 2 ? 0.95 : 1.0) *
-                        stream_spill_factor(spill / (1 << 20)) * util;
+                        stream_spill_factor(spill / (1 << 20)) * util *
+                        (16.0 / (16.0 + 8.0 * rc * dev::kSR / N));  // the recomputed rows read b twice
     const double t = static_cast<double>(n) * m * 2.0 * elem / (frac * 6.5e12);
     // TMEM-tier rule (measured at N = 384..512, tools/gpu_calib.sh): with the
     // forward intermediates split over TMEM + smem, the largest group whose
     // residual L2 spill stays <= 30 MB wins (capped at 96 systems in fast
     // mode); the calibrated model below decides everything else.
-    if (rtc > 0 && elem == 8 && N >= 384 && Wg >= 96 && spill <= 30.0 * (1 << 20) && Wg <= (fast ? 96 : 128) &&
-        !forced_wg) {
+    if (rtc > 0 && rc == 0 && elem == 8 && N >= 384 && Wg >= 96 && spill <= 30.0 * (1 << 20) &&
+        Wg <= (fast ? 96 : 128) && !forced_wg) {
       tmem_pick = Wg;
     }
     if (!found || t < best_t * 0.995 || (t <= best_t * 1.005 && spill < best_spill)) {
@@ -476,63 +509,31 @@ bool plan_stream(std::size_t n, std::size_t m, std::size_t elem, bool pent, bool
       p.KB = KB;
       p.KR = KR;
       p.PD = PD;
-      p.stagger_ns = env_int("BANDSOLVE_SSTAG", 0);
+      p.stagger_ns = env_int("SSTAG", 0);
       p.warps = P;
       p.model_us = t * 1e6;
-      p.smem_bytes = dev::StreamLayout::make(N, H, TC, Wg, KB, KR, elem, fr, br, per_arrays).total;
+      p.smem_bytes = dev::StreamLayout::make(N, H, TC, Wg, KB, KR, elem, fr, br, per_arrays, ckpts_for(rc)).total;
       p.V = V;
       p.tmem_chunks = rtc;
+      p.rc_chunks = rc;
+      p.seg_chunks = rc > 0 ? seg : 0;
     }
   }
-  if (found && tmem_pick && tmem_pick != p.Wg) {
+  if (found && tmem_pick && tmem_pick != p.Wg && forced_rc < 0) {
     // re-plan with the TMEM rule's group width (same layout rules)
     Plan q;
-    if (plan_stream(n, m, elem, pent, fast, sms, q, per_arrays, allow_tmem, tmem_pick)) p = q;
+    if (plan_stream(n, m, elem, pent, fast, sms, q, per_arrays, allow_tmem, tmem_pick, allow_rc)) p = q;
   }
   return found;
 }
 
 
-// Register-streamed plan (sweep_regs.cuh): Wg = 32 P systems per SM, the
-// longest smem tail that fits, the rest of the rows (a multiple of 16) in
-// the L2 scratch.
-bool plan_regs(std::size_t n, std::size_t m, std::size_t elem, bool pent, int sms, int P, Plan& p) {
-  const std::size_t fr = fwd_rec_bytes(pent, elem), br = bwd_rec_bytes(pent, elem);
-  const std::size_t fac = dev::align128(n * fr) + dev::align128(n * br);
-  if (fac > kSmemPerBlockMax / 2 || n < 2 || P < 1 || P > dev::kRMaxWarps) return false;
-  const int N = static_cast<int>(n);
-  const int Wg = 32 * P;
-  const int forced_tail = env_int("BANDSOLVE_STAIL", -1);
-  for (int tc = (N + dev::kSR - 1) / dev::kSR; tc >= 0; --tc) {
-    int h = std::max(0, N - tc * dev::kSR);
-    h = (h + dev::kSR - 1) / dev::kSR * dev::kSR;
-    if (forced_tail >= 0) h = (std::max(0, N - forced_tail) + dev::kSR - 1) / dev::kSR * dev::kSR;
-    if (h > N) h = N / dev::kSR * dev::kSR;
-    const int TC = (N - h + dev::kSR - 1) / dev::kSR;
-    const std::size_t bytes = dev::RegsLayout::make(N, TC, Wg, elem, fr, br).total;
-    if (bytes <= kSmemPerBlockMax) {
-      p.kind = PlanKind::Regs;
-      p.Wg = Wg;
-      p.warps = P;
-      p.H = h;
-      p.TC = TC;
-      p.V = 1;
-      p.KB = std::max(4, std::min(6, env_int("BANDSOLVE_SNB", pent ? 4 : 6)));  // register pipeline blocks
-      p.smem_bytes = bytes;
-      const long long groups = (static_cast<long long>(m) + Wg - 1) / Wg;
-      p.model_us = static_cast<double>(std::min<long long>(sms, groups)) * Wg * h * elem / 1e6;  // spill MB
-      return true;
-    }
-    if (forced_tail >= 0) return false;
-  }
-  return false;
-}
-
 Plan choose_plan(std::size_t n, std::size_t m, std::size_t ld, std::size_t elem, const void* x, bool pent,
                  bool fast, int sms) {
   Plan p;
   // BANDSOLVE_PLAN = stream | global | persist | smem | smemW8 | smemW16 | smemW32 (tuning / tests)
-  const char* force = std::getenv("BANDSOLVE_PLAN");
+  const std::optional<std::string> force_s = tune_str("PLAN");
+  const char* force = force_s ? force_s->c_str() : nullptr;
   int forced_w = 0;
   bool force_smem = false;
   bool force_persist = false;
@@ -556,9 +557,6 @@ Plan choose_plan(std::size_t n, std::size_t m, std::size_t ld, std::size_t elem,
     p.why = "shape beyond 32-bit TMA coordinates";
     return p;
   }
-  if (force && std::strcmp(force, "regs") == 0 &&
-      plan_regs(n, m, elem, pent, sms, std::max(1, env_int("BANDSOLVE_SWG", 96) / 32), p))
-    return p;
   // Many long systems: once the forward intermediates mostly spill past L2,
   // the on-chip plans fall below two plain streaming passes (thread per
   // system in global memory: fwd read+write, bwd read+write at ~0.95 of HBM
@@ -574,7 +572,7 @@ Plan choose_plan(std::size_t n, std::size_t m, std::size_t ld, std::size_t elem,
   // (ADI axis 4096 x 4096 tri: 1.46x; 4096 x 1024: 1.39x; fp32 1024 x 4096:
   // 3.4x, measured); shapes no on-chip plan fits fall through to global.
   // (Fast mode first tries the partitioned path, partition.cu.)
-  if (!force_smem && !force_persist && plan_stream(n, m, elem, pent, fast, sms, p)) return p;
+  if (!force_smem && !force_persist && plan_stream(n, m, elem, pent, fast, sms, p, 0, true, 0, true)) return p;
   if (!force_smem && plan_persist(n, elem, pent, fast, sms, p)) return p;
   int best_sys = 0;
   for (int W : {8, 16, 32}) {
@@ -673,7 +671,7 @@ cudaError_t launch_persist(const Plan& plan, T* x, int n, long long m, long long
     const std::size_t bytes = static_cast<std::size_t>(grid) * warps * plan.H * dev::kPW * sizeof(T);
     int device = 0;
     if (cudaGetDevice(&device) == cudaSuccess) ensure_l2_setaside(device, bytes);
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch), bytes, s);
+    cudaError_t e = pool_malloc_async(reinterpret_cast<void**>(&scratch), bytes, s);
     if (e != cudaSuccess) return e;
   }
   kern<<<static_cast<unsigned>(grid), warps * 32, smem, s>>>(map_ring, map_tail, x, n, m, ld, plan.H, plan.TC,
@@ -688,12 +686,15 @@ cudaError_t launch_persist(const Plan& plan, T* x, int n, long long m, long long
 }
 
 
-template <typename T, int V, bool PENT, bool FAST, int PER = 0, bool CN = false, bool TM = false>
+template <typename T, int V, bool PENT, bool FAST, int PER = 0, bool CN = false, int TM = 0>
 cudaError_t launch_stream_v(const Plan& plan, T* x, int n, long long m, long long ld, const void* fwd,
                             const void* bwd, cudaStream_t s, int sms, const dev::PerArgs& per_in = dev::PerArgs{}) {
   auto kern = dev::sweep_stream<T, V, PENT, FAST, PER, CN, TM>;
   dev::PerArgs per = per_in;
   per.tmem_chunks = TM ? plan.tmem_chunks : 0;
+  per.rc_chunks = (TM && !CN) ? plan.rc_chunks : 0;
+  per.seg_chunks = per.rc_chunks > 0 ? plan.seg_chunks : 0;
+  if (plan.warps > dev::stream_tm_warps(TM) && TM) return cudaErrorInvalidConfiguration;
   static std::atomic<uint64_t> configured{0};  // one bit per device: attributes are per context
   if (cudaError_t e = allow_big_smem_once(kern, configured); e != cudaSuccess) return e;
   CUtensorMap map;
@@ -702,12 +703,12 @@ cudaError_t launch_stream_v(const Plan& plan, T* x, int n, long long m, long lon
   const long long grid = std::min<long long>(sms, groups);
   const int P = plan.Wg / (32 * V);
   T* scratch = nullptr;
-  const int spilled_rows = plan.H - per.tmem_chunks * dev::kSR;
+  const int spilled_rows = plan.H - (per.tmem_chunks + per.rc_chunks) * dev::kSR;
   if (spilled_rows > 0) {
     const std::size_t bytes = static_cast<std::size_t>(grid) * plan.Wg * spilled_rows * sizeof(T);
     int device = 0;
     if (cudaGetDevice(&device) == cudaSuccess) ensure_l2_setaside(device, bytes);
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch), bytes, s);
+    cudaError_t e = pool_malloc_async(reinterpret_cast<void**>(&scratch), bytes, s);
     if (e != cudaSuccess) return e;
   }
   kern<<<static_cast<unsigned>(grid), (P + 2) * 32, plan.smem_bytes, s>>>(map, x, n, m, ld, plan.H, plan.TC, plan.KB,
@@ -725,52 +726,13 @@ cudaError_t launch_stream_v(const Plan& plan, T* x, int n, long long m, long lon
 template <typename T, bool PENT, bool FAST>
 cudaError_t launch_stream(const Plan& plan, T* x, int n, long long m, long long ld, const void* fwd,
                           const void* bwd, cudaStream_t s, int sms) {
-  if (plan.V == 1 && plan.tmem_chunks > 0)
-    return launch_stream_v<T, 1, PENT, FAST, 0, false, true>(plan, x, n, m, ld, fwd, bwd, s, sms);
+  if (plan.V == 1 && (plan.tmem_chunks > 0 || plan.rc_chunks > 0))
+    return plan.warps > 4 ? launch_stream_v<T, 1, PENT, FAST, 0, false, 2>(plan, x, n, m, ld, fwd, bwd, s, sms)
+                          : launch_stream_v<T, 1, PENT, FAST, 0, false, 1>(plan, x, n, m, ld, fwd, bwd, s, sms);
   if (plan.V == 2) return launch_stream_v<T, 2, PENT, FAST>(plan, x, n, m, ld, fwd, bwd, s, sms);
   return launch_stream_v<T, 1, PENT, FAST>(plan, x, n, m, ld, fwd, bwd, s, sms);
 }
 
-
-template <typename T, bool PENT, bool FAST, int NB>
-cudaError_t launch_regs_nb(const Plan& plan, T* x, int n, long long m, long long ld, const void* fwd,
-                           const void* bwd, cudaStream_t s, int sms);
-template <typename T, bool PENT, bool FAST>
-cudaError_t launch_regs(const Plan& plan, T* x, int n, long long m, long long ld, const void* fwd,
-                        const void* bwd, cudaStream_t s, int sms) {
-  if (plan.KB == 6) return launch_regs_nb<T, PENT, FAST, 6>(plan, x, n, m, ld, fwd, bwd, s, sms);
-  if (plan.KB == 5) return launch_regs_nb<T, PENT, FAST, 5>(plan, x, n, m, ld, fwd, bwd, s, sms);
-  return launch_regs_nb<T, PENT, FAST, 4>(plan, x, n, m, ld, fwd, bwd, s, sms);
-}
-
-template <typename T, bool PENT, bool FAST, int NB>
-cudaError_t launch_regs_nb(const Plan& plan, T* x, int n, long long m, long long ld, const void* fwd,
-                           const void* bwd, cudaStream_t s, int sms) {
-  auto kern = dev::sweep_regs<T, PENT, FAST, NB>;
-  static std::atomic<uint64_t> configured{0};  // one bit per device: attributes are per context
-  if (cudaError_t e = allow_big_smem_once(kern, configured); e != cudaSuccess) return e;
-  CUtensorMap map;
-  if (!encode_map(&map, x, sizeof(T), n, m, ld, 32, dev::kSR)) return cudaErrorInvalidValue;
-  const long long groups = (m + plan.Wg - 1) / plan.Wg;
-  const long long grid = std::min<long long>(sms, groups);
-  T* scratch = nullptr;
-  if (plan.H > 0) {
-    const std::size_t bytes = static_cast<std::size_t>(grid) * plan.Wg * plan.H * sizeof(T);
-    int device = 0;
-    if (cudaGetDevice(&device) == cudaSuccess) ensure_l2_setaside(device, bytes);
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch), bytes, s);
-    if (e != cudaSuccess) return e;
-  }
-  kern<<<static_cast<unsigned>(grid), (plan.warps + 1) * 32, plan.smem_bytes, s>>>(map, x, n, m, ld, plan.H, plan.TC,
-                                                                                  groups, fwd, bwd, scratch);
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  cudaError_t e = cudaGetLastError();
-  if (scratch) {
-    cudaError_t f = cudaFreeAsync(scratch, s);
-    if (e == cudaSuccess) e = f;
-  }
-  return e;
-}
 
 template <typename T, bool PENT, bool FAST>
 cudaError_t launch_global(T* x, int n, long long m, long long ld, const void* fwd, const void* bwd,
@@ -792,7 +754,6 @@ template <typename T, bool PENT, bool FAST>
 cudaError_t dispatch(const Plan& plan, T* x, int n, long long m, long long ld, const void* fwd,
                      const void* bwd, cudaStream_t s, int sms) {
   if (plan.kind == PlanKind::Stream) return launch_stream<T, PENT, FAST>(plan, x, n, m, ld, fwd, bwd, s, sms);
-  if (plan.kind == PlanKind::Regs) return launch_regs<T, PENT, FAST>(plan, x, n, m, ld, fwd, bwd, s, sms);
   if (plan.kind == PlanKind::Persist) return launch_persist<T, PENT, FAST>(plan, x, n, m, ld, fwd, bwd, s, sms);
   if (plan.kind == PlanKind::Smem) {
     switch (plan.W) {
@@ -1055,6 +1016,7 @@ uint64_t host_splitmix64(uint64_t z) {
 constexpr int kStages = 4;
 struct StageContext {
   int device = -1;
+  int slot = 0;  // position in the device list (a device may be listed more than once)
   cudaStream_t streams[kStages] = {};
   void* buf[kStages] = {};
   std::size_t cap[kStages] = {};
@@ -1081,14 +1043,15 @@ struct StageContexts {
 };
 thread_local StageContexts t_contexts;
 
-bandsolve_status stage_context(int device, StageContext** out) {
+bandsolve_status stage_context(int device, int slot, StageContext** out) {
   for (StageContext* c : t_contexts.list)
-    if (c->device == device) {
+    if (c->device == device && c->slot == slot) {
       *out = c;
       return BANDSOLVE_OK;
     }
   auto* c = new StageContext;
   c->device = device;
+  c->slot = slot;
   t_contexts.list.push_back(c);  // owned from here on, even if a stream fails below
   for (int s = 0; s < kStages; ++s) BSB_CUDA(cudaStreamCreateWithFlags(&c->streams[s], cudaStreamNonBlocking));
   *out = c;
@@ -1160,12 +1123,10 @@ bandsolve_status describe_plan(Kind kind, std::size_t n, std::size_t m, std::siz
   if (K > 0)
     std::snprintf(buf, sizeof buf, "partition K=%d blocks of %zu rows, interface system %d (dense LU), 2 launches", K,
                   n / K, (pent ? 4 : 2) * K);
-  else if (p.kind == PlanKind::Regs)
-    std::snprintf(buf, sizeof buf, "regs Wg=%d warps=%d+1 nb=%d head(L2)=%d tail(smem)=%d smem=%zu B spill=%.1f MB",
-                  p.Wg, p.warps, p.KB, p.H, static_cast<int>(n) - p.H, p.smem_bytes, p.model_us);
   else if (p.kind == PlanKind::Stream)
-    std::snprintf(buf, sizeof buf, "stream Wg=%d V=%d warps=%d+2 tmem=%d head(L2)=%d tail(smem)=%d rings=%d/%d pd=%d smem=%zu B model=%.1f us",
-                  p.Wg, p.V, p.warps, p.tmem_chunks * dev::kSR, p.H - p.tmem_chunks * dev::kSR, static_cast<int>(n) - p.H,
+    std::snprintf(buf, sizeof buf, "stream Wg=%d V=%d warps=%d+2 recompute=%d(seg %d) tmem=%d head(L2)=%d tail(smem)=%d rings=%d/%d pd=%d smem=%zu B model=%.1f us",
+                  p.Wg, p.V, p.warps, p.rc_chunks * dev::kSR, p.seg_chunks * dev::kSR, p.tmem_chunks * dev::kSR,
+                  p.H - (p.tmem_chunks + p.rc_chunks) * dev::kSR, static_cast<int>(n) - p.H,
                   p.KB, p.KR, p.PD, p.smem_bytes, p.model_us);
   else if (p.kind == PlanKind::Persist)
     std::snprintf(buf, sizeof buf, "persist warps=%d systems/sm=%d head(L2)=%d tail(smem)=%d smem=%zu B", p.warps,
@@ -1198,7 +1159,6 @@ bandsolve_status solve_device(const Factor& f, void* x, bool f32, std::size_t n,
   const int q = fast ? 1 : 0;
   auto s = static_cast<cudaStream_t>(stream);
   const int sms = num_sms(device);
-  keep_pool_memory(device);
   if (fast && !f32) {
     bool done = false;
     st = partition_solve_device(f, static_cast<double*>(x), n, m, ld, stream, sms, &done);
@@ -1263,7 +1223,7 @@ bandsolve_status launch_periodic_correct(const Periodic& p, double* x, std::size
   if (st != BANDSOLVE_OK) return st;
   const bool pent = p.kind != Kind::Tri;
   double* coef = nullptr;
-  BSB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&coef), (pent ? 2 : 1) * m * sizeof(double), s));
+  BSB_CUDA(pool_malloc_async(reinterpret_cast<void**>(&coef), (pent ? 2 : 1) * m * sizeof(double), s));
   const int threads = 128;
   const unsigned gx = static_cast<unsigned>((m + threads - 1) / threads);
   if (pent)
@@ -1309,7 +1269,7 @@ bandsolve_status cn_step_device(const Periodic& p, double sigma_x, const double*
   const bool aligned = (reinterpret_cast<uintptr_t>(u) % 16 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0) &&
                        ((ld * sizeof(double)) % 16 == 0);
   Plan plan;
-  if (std::getenv("BANDSOLVE_CN_UNFUSED") == nullptr && aligned && n <= static_cast<std::size_t>(INT_MAX) &&
+  if (!tune_flag("CN_UNFUSED") && aligned && n <= static_cast<std::size_t>(INT_MAX) &&
       m <= static_cast<std::size_t>(INT_MAX) / 2 &&
       plan_stream(n, m, sizeof(double), pent, fast, sms, plan, fast ? (pent ? 4 : 2) : 0)) {
     const DeviceFactor* df = nullptr;
@@ -1318,7 +1278,6 @@ bandsolve_status cn_step_device(const Periodic& p, double sigma_x, const double*
     const double* blob = nullptr;
     st = periodic_device_z(p, device, &blob);
     if (st != BANDSOLVE_OK) return st;
-    keep_pool_memory(device);
     dev::PerArgs per;
     per.arrays = blob + 2 * n;
     if (pent) {
@@ -1381,10 +1340,9 @@ bandsolve_status periodic_device(const Periodic& p, double* x, std::size_t n, st
   const int sms = num_sms(device);
   const bool pent = p.kind != Kind::Tri;
   const bool fuse = !correct_only && current_mode() == BANDSOLVE_MODE_FAST &&
-                    std::getenv("BANDSOLVE_PERIODIC_UNFUSED") == nullptr;
+                    !tune_flag("PERIODIC_UNFUSED");
   if (fuse && partition_blocks(n, m, sms, pent) > 0) {
     // few long systems: partitioned sweep with the correction fused into its last pass
-    keep_pool_memory(device);
     const double* blob = nullptr;
     bandsolve_status st = periodic_device_z(p, device, &blob);
     if (st != BANDSOLVE_OK) return st;
@@ -1412,7 +1370,6 @@ bandsolve_status periodic_device(const Periodic& p, double* x, std::size_t n, st
       const double* blob = nullptr;
       st = periodic_device_z(p, device, &blob);
       if (st != BANDSOLVE_OK) return st;
-      keep_pool_memory(device);
       dev::PerArgs per;
       per.arrays = blob + 2 * n;
       if (pent) {
@@ -1455,8 +1412,7 @@ bandsolve_status periodic_stencil_partition(const Periodic& p, const double* src
                                             double cs4, double cmid, double* x, std::size_t n, std::size_t m,
                                             std::size_t ld, void* stream, bool* done) {
   *done = false;
-  if (current_mode() != BANDSOLVE_MODE_FAST || std::getenv("BANDSOLVE_PERIODIC_UNFUSED") ||
-      std::getenv("BANDSOLVE_ADI_UNFUSED"))
+  if (current_mode() != BANDSOLVE_MODE_FAST || tune_flag("PERIODIC_UNFUSED") || tune_flag("ADI_UNFUSED"))
     return BANDSOLVE_OK;
   if (reinterpret_cast<uintptr_t>(src) % 16 != 0) return BANDSOLVE_OK;
   int device = 0;
@@ -1466,9 +1422,8 @@ bandsolve_status periodic_stencil_partition(const Periodic& p, const double* src
   // tridiagonal only: the pentadiagonal variant (two neighbour rows per side
   // in registers) measured slower than stencil+transpose and the plain pass
   // (5.6e10 vs 6.7e10 rows/s at 4096^2); tri gains 1.11e11 -> 1.33e11
-  if (pent && !std::getenv("BANDSOLVE_ADI_FUSE_PENT")) return BANDSOLVE_OK;
+  if (pent && !tune_flag("ADI_FUSE_PENT")) return BANDSOLVE_OK;
   if (partition_blocks(n, m, sms, pent) == 0) return BANDSOLVE_OK;
-  keep_pool_memory(device);
   const double* blob = nullptr;
   bandsolve_status st = periodic_device_z(p, device, &blob);
   if (st != BANDSOLVE_OK) return st;
@@ -1483,59 +1438,134 @@ bandsolve_status periodic_stencil_partition(const Periodic& p, const double* src
   return partition_solve_device(*p.factor, x, n, m, ld, stream, sms, done, &pa, &ps);
 }
 
+// ---- device list of the host-batch solves (bandsolve_set_devices) ------------------
+namespace {
+std::mutex g_dev_mu;
+std::vector<int> g_devices;  // empty: the calling thread's current device
+}  // namespace
+
+bandsolve_status set_devices(const int* ids, int count) {
+  if (count < 0 || (count > 0 && !ids)) return fail(BANDSOLVE_ERR_BAD_ARG, "bad device list");
+  for (int k = 0; k < count; ++k)
+    if (ids[k] < 0) return fail(BANDSOLVE_ERR_BAD_ARG, "negative device id");
+  std::lock_guard<std::mutex> lock(g_dev_mu);
+  g_devices.assign(ids, ids + count);
+  return BANDSOLVE_OK;
+}
+
+int get_devices(int* ids, int capacity) {
+  std::lock_guard<std::mutex> lock(g_dev_mu);
+  const int count = static_cast<int>(g_devices.size());
+  for (int k = 0; ids && k < std::min(count, capacity); ++k) ids[k] = g_devices[k];
+  return count;
+}
+
+// Host-batch solve: the m columns are split over the device list exactly as
+// the reference splits them over its workers (parallel.cpp:53-54, j0 =
+// m*g/G); each shard streams ~16 MiB column chunks through its own device's
+// staging pipeline (kStages streams: chunk k's H2D overlaps chunk k-1's sweep
+// and chunk k-2's D2H), so each GPU's copies use that GPU's own PCIe link.
+// One host thread issues everything asynchronously, round-robin over the
+// shards, then waits for all of them. Columns are independent, so the result
+// is bitwise the same for any device list.
 bandsolve_status solve_host(const Factor& f, double* x, std::size_t n, std::size_t m, const Periodic* per,
                             bool correct_only) {
   if (n != f.n) return fail(BANDSOLVE_ERR_SHAPE_MISMATCH, "factor order != batch rows");
   if (m == 0) return BANDSOLVE_OK;
-  if (device_count_cached() == 0) return fail(BANDSOLVE_ERR_INTERNAL, "no CUDA device available (no CPU fallback)");
-  int device = 0;
-  BSB_CUDA(cudaGetDevice(&device));
-  StageContext* ctx = nullptr;
-  bandsolve_status st = stage_context(device, &ctx);
-  if (st != BANDSOLVE_OK) return st;
+  const int ndev = device_count_cached();
+  if (ndev == 0) return fail(BANDSOLVE_ERR_INTERNAL, "no CUDA device available (no CPU fallback)");
+  int caller = 0;
+  BSB_CUDA(cudaGetDevice(&caller));
+  std::vector<int> devs;
+  {
+    std::lock_guard<std::mutex> lock(g_dev_mu);
+    devs = g_devices;
+  }
+  if (devs.empty()) devs.push_back(caller);
+  for (int d : devs)
+    if (d >= ndev) return fail(BANDSOLVE_ERR_BAD_ARG, "device list names a device that does not exist");
 
-  // Column chunks of ~16 MiB (multiple of 32 systems) pipelined over three
-  // streams: chunk k's H2D overlaps chunk k-1's sweep and chunk k-2's D2H.
+  struct Shard {
+    int device;
+    StageContext* ctx;
+    std::size_t j0, j1, w, chunks;
+    int stages;
+  };
+  const std::size_t G = devs.size();
   const std::size_t row_bytes = n * sizeof(double);
-  const std::size_t chunk_mib = static_cast<std::size_t>(std::max(1, env_int("BANDSOLVE_HOST_CHUNK_MIB", 16)));
-  std::size_t w = (chunk_mib << 20) / row_bytes;
-  w = std::max<std::size_t>(32, (w / 32) * 32);
-  if (w >= m) w = m;
-  const std::size_t chunks = (m + w - 1) / w;
-  const std::size_t need = n * ((w + 1) & ~std::size_t(1)) * sizeof(double);
-  const int stages = static_cast<int>(std::min<std::size_t>(kStages, chunks));
-  for (int s = 0; s < stages; ++s) {
-    if (ctx->cap[s] < need) {
-      if (ctx->buf[s]) {
-        BSB_CUDA(cudaStreamSynchronize(ctx->streams[s]));
-        BSB_CUDA(cudaFree(ctx->buf[s]));
-        ctx->buf[s] = nullptr;
-        ctx->cap[s] = 0;
+  const std::size_t chunk_mib = static_cast<std::size_t>(std::max(1, env_int("HOST_CHUNK_MIB", 16)));
+  std::vector<Shard> shards;
+  bandsolve_status st = BANDSOLVE_OK;
+  for (std::size_t g = 0; g < G && st == BANDSOLVE_OK; ++g) {
+    Shard sh{devs[g], nullptr, m * g / G, m * (g + 1) / G, 0, 0, 0};
+    if (sh.j1 == sh.j0) continue;
+    const std::size_t mg = sh.j1 - sh.j0;
+    std::size_t w = (chunk_mib << 20) / row_bytes;
+    w = std::max<std::size_t>(32, (w / 32) * 32);
+    sh.w = std::min(w, mg);
+    sh.chunks = (mg + sh.w - 1) / sh.w;
+    sh.stages = static_cast<int>(std::min<std::size_t>(kStages, sh.chunks));
+    if (cudaError_t e = cudaSetDevice(sh.device); e != cudaSuccess) {
+      st = cuda_fail(e, "cudaSetDevice");
+      break;
+    }
+    st = stage_context(sh.device, static_cast<int>(g), &sh.ctx);
+    const std::size_t need = n * ((sh.w + 1) & ~std::size_t(1)) * sizeof(double);
+    for (int q = 0; q < sh.stages && st == BANDSOLVE_OK; ++q) {
+      StageContext* c = sh.ctx;
+      if (c->cap[q] >= need) continue;
+      cudaError_t e = cudaSuccess;
+      if (c->buf[q]) {
+        e = cudaStreamSynchronize(c->streams[q]);
+        if (e == cudaSuccess) e = cudaFree(c->buf[q]);
+        c->buf[q] = nullptr;
+        c->cap[q] = 0;
       }
-      BSB_CUDA(cudaMalloc(&ctx->buf[s], need));
-      ctx->cap[s] = need;
+      if (e == cudaSuccess) e = cudaMalloc(&c->buf[q], need);
+      if (e != cudaSuccess) st = cuda_fail(e, "staging buffer");
+      else c->cap[q] = need;
+    }
+    shards.push_back(sh);
+  }
+  std::size_t max_chunks = 0;
+  for (const Shard& sh : shards) max_chunks = std::max(max_chunks, sh.chunks);
+  for (std::size_t k = 0; k < max_chunks && st == BANDSOLVE_OK; ++k) {
+    for (const Shard& sh : shards) {
+      if (k >= sh.chunks) continue;
+      cudaError_t e = cudaSetDevice(sh.device);
+      const int q = static_cast<int>(k % sh.stages);
+      cudaStream_t strm = sh.ctx->streams[q];
+      const std::size_t j0 = sh.j0 + k * sh.w;
+      const std::size_t wk = std::min(sh.w, sh.j1 - j0);
+      const std::size_t ldk = (wk + 1) & ~std::size_t(1);  // even pitch keeps the TMA path
+      double* d = static_cast<double*>(sh.ctx->buf[q]);
+      if (e == cudaSuccess)
+        e = cudaMemcpy2DAsync(d, ldk * sizeof(double), x + j0, m * sizeof(double), wk * sizeof(double), n,
+                              cudaMemcpyHostToDevice, strm);
+      if (e != cudaSuccess) {
+        st = cuda_fail(e, "host-to-device copy");
+        break;
+      }
+      st = per ? periodic_device(*per, d, n, wk, ldk, strm, correct_only) : solve_device(f, d, false, n, wk, ldk, strm);
+      if (st != BANDSOLVE_OK) break;
+      e = cudaMemcpy2DAsync(x + j0, m * sizeof(double), d, ldk * sizeof(double), wk * sizeof(double), n,
+                            cudaMemcpyDeviceToHost, strm);
+      if (e != cudaSuccess) {
+        st = cuda_fail(e, "device-to-host copy");
+        break;
+      }
     }
   }
-  for (std::size_t k = 0; k < chunks; ++k) {
-    const int s = static_cast<int>(k % stages);
-    cudaStream_t strm = ctx->streams[s];
-    const std::size_t j0 = k * w;
-    const std::size_t wk = std::min(w, m - j0);
-    const std::size_t ldk = (wk + 1) & ~std::size_t(1);  // even pitch keeps the TMA path
-    double* d = static_cast<double*>(ctx->buf[s]);
-    BSB_CUDA(cudaMemcpy2DAsync(d, ldk * sizeof(double), x + j0, m * sizeof(double), wk * sizeof(double), n,
-                               cudaMemcpyHostToDevice, strm));
-    if (per) st = periodic_device(*per, d, n, wk, ldk, strm, correct_only);
-    else st = solve_device(f, d, false, n, wk, ldk, strm);
-    if (st != BANDSOLVE_OK) {
-      for (int q = 0; q < stages; ++q) cudaStreamSynchronize(ctx->streams[q]);
-      return st;
+  // drain every shard (also on failure: no copy may still target x after we return)
+  for (const Shard& sh : shards) {
+    cudaSetDevice(sh.device);
+    for (int q = 0; q < sh.stages; ++q) {
+      cudaError_t e = cudaStreamSynchronize(sh.ctx->streams[q]);
+      if (e != cudaSuccess && st == BANDSOLVE_OK) st = cuda_fail(e, "staging stream");
     }
-    BSB_CUDA(cudaMemcpy2DAsync(x + j0, m * sizeof(double), d, ldk * sizeof(double), wk * sizeof(double), n,
-                               cudaMemcpyDeviceToHost, strm));
   }
-  for (int s = 0; s < stages; ++s) BSB_CUDA(cudaStreamSynchronize(ctx->streams[s]));
-  return BANDSOLVE_OK;
+  cudaSetDevice(caller);
+  return st;
 }
 
 bandsolve_status cn_rhs_device(bool pent, double sigma_x, const double* u, double* out, std::size_t n,
@@ -1605,8 +1635,8 @@ bandsolve_status residual_device(Kind kind, const double* const* bands, std::siz
   }
   double* dbands = nullptr;
   unsigned long long* dout = nullptr;
-  BSB_CUDA(cudaMallocAsync(&dbands, host.size() * sizeof(double), s));
-  BSB_CUDA(cudaMallocAsync(&dout, sizeof(unsigned long long), s));
+  BSB_CUDA(pool_malloc_async(&dbands, host.size() * sizeof(double), s));
+  BSB_CUDA(pool_malloc_async(&dout, sizeof(unsigned long long), s));
   BSB_CUDA(cudaMemcpyAsync(dbands, host.data(), host.size() * sizeof(double), cudaMemcpyHostToDevice, s));
   BSB_CUDA(cudaMemsetAsync(dout, 0, sizeof(unsigned long long), s));
   const int threads = 128;
@@ -1654,10 +1684,9 @@ bandsolve_status adi_step_device(const Periodic& px, const Periodic& py, double 
   {
     int device = 0;
     BSB_CUDA(cudaGetDevice(&device));
-    keep_pool_memory(device);  // the per-step scratch stays mapped in the stream-ordered pool
   }
   double* t1 = nullptr;
-  BSB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&t1), nx * ldt * sizeof(double), s));
+  BSB_CUDA(pool_malloc_async(reinterpret_cast<void**>(&t1), nx * ldt * sizeof(double), s));
   (void)work;  // scratch kept in the ABI; the fused stencil+transpose needs only t1
   // pde.cpp:80-81 / :101-103: the coefficients are formed once on the host
   const double cs = sigma, cs4 = pent ? 4.0 * sigma : 0.0, cmid = pent ? 1.0 - 6.0 * sigma : 1.0 - 2.0 * sigma;
@@ -1859,13 +1888,13 @@ bandsolve_status residual_host(Kind kind, const double* const* bands, std::size_
   int device = 0;
   BSB_CUDA(cudaGetDevice(&device));
   StageContext* ctx = nullptr;
-  bandsolve_status st = stage_context(device, &ctx);
+  bandsolve_status st = stage_context(device, 0, &ctx);
   if (st != BANDSOLVE_OK) return st;
   cudaStream_t s = ctx->streams[0];
   const std::size_t bytes = n * m * sizeof(double);
   double *dx = nullptr, *dr = nullptr;
-  BSB_CUDA(cudaMallocAsync(&dx, bytes, s));
-  BSB_CUDA(cudaMallocAsync(&dr, bytes, s));
+  BSB_CUDA(pool_malloc_async(&dx, bytes, s));
+  BSB_CUDA(pool_malloc_async(&dr, bytes, s));
   BSB_CUDA(cudaMemcpyAsync(dx, x, bytes, cudaMemcpyHostToDevice, s));
   BSB_CUDA(cudaMemcpyAsync(dr, rhs, bytes, cudaMemcpyHostToDevice, s));
   st = residual_device(kind, bands, n, cyclic, dx, dr, m, m, s, out);

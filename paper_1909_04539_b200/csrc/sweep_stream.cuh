@@ -97,16 +97,19 @@ __device__ __forceinline__ void st_stream_vec(Vec<T, V>* p, Vec<T, V> v) {
 }
 
 struct StreamLayout {
-  size_t fwd_off, bwd_off, per_off, bring_off, rring_off, tail_off, bar_off, total;
+  size_t fwd_off, bwd_off, per_off, ck_off, bring_off, rring_off, tail_off, bar_off, total;
   // chunk: elements of one chunk (all warps) = kSR x Wg; per_arrays: fp64
-  // arrays of n for the fused periodic correction (0, 2 tri, 4 pent)
+  // arrays of n for the fused periodic correction (0, 2 tri, 4 pent);
+  // ckpts: forward-state checkpoints per system (recompute tier: one per
+  // recomputed segment after the first, two values each)
   __host__ __device__ static StreamLayout make(int n, int H, int TC, int Wg, int KB, int KR, size_t elem,
-                                               size_t fwd_rec, size_t bwd_rec, int per_arrays = 0) {
+                                               size_t fwd_rec, size_t bwd_rec, int per_arrays = 0, int ckpts = 0) {
     StreamLayout L{};
     L.fwd_off = 0;
     L.bwd_off = align128(static_cast<size_t>(n) * fwd_rec);
     L.per_off = L.bwd_off + align128(static_cast<size_t>(n) * bwd_rec);
-    L.bring_off = L.per_off + align128(static_cast<size_t>(per_arrays) * n * sizeof(double));
+    L.ck_off = L.per_off + align128(static_cast<size_t>(per_arrays) * n * sizeof(double));
+    L.bring_off = L.ck_off + align128(static_cast<size_t>(ckpts) * Wg * 2 * elem);
     const size_t chunk = static_cast<size_t>(kSR) * Wg * elem;
     L.rring_off = L.bring_off + (H > 0 ? static_cast<size_t>(KB) * chunk : 0);
     L.tail_off = L.rring_off + (H > 0 ? static_cast<size_t>(KR) * chunk : 0);
@@ -142,33 +145,32 @@ __device__ __forceinline__ void tmem_dealloc_512(uint32_t taddr) {  // the alloc
 }
 __device__ __forceinline__ void tmem_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tmem_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-// 32 (fp64: 16 rows) / 16 (fp32: 16 rows) consecutive columns of this lane
-__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]) : "memory");
-  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-}
+// 16 consecutive 32-bit columns of this lane (8 fp64 / 16 fp32 rows). The
+// store is asynchronous: its source registers are free once it issues (the
+// hardware scoreboard covers them), but its data is only guaranteed visible
+// to later tcgen05.ld after tmem_wait_st(), which the readers issue once
+// before they start (not once per store: each wait would stall the warp for
+// the full TMEM write latency inside the dependent row loop).
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16};" ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]) : "memory");
-  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];" : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]) : "r"(taddr) : "memory");
-}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];" : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]) : "r"(taddr) : "memory");
 }
 // wait for this thread's TMEM loads; the registers are in/out operands so no
 // consumer can be scheduled above the wait
-__device__ __forceinline__ void tmem_wait_ld(uint32_t (&r)[32]) {
-  asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]), "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]), "+r"(r[29]), "+r"(r[30]), "+r"(r[31]) :: "memory");
-}
 __device__ __forceinline__ void tmem_wait_ld(uint32_t (&r)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15]) :: "memory");
 }
-// a 16-row chunk of one lane's values <-> raw 32-bit TMEM words
+// A piece of one lane's consecutive rows <-> 16 raw 32-bit TMEM words (one
+// .32x32b.x16 access): 8 fp64 / 16 fp32 rows. Row i of a TMEM region sits
+// at column i * kColsPerRow.
 template <typename T>
-struct TChunk {
-  static constexpr int kWords = kSR * static_cast<int>(sizeof(T)) / 4;
+struct TPiece {
+  static constexpr int kWords = 16;
+  static constexpr int kColsPerRow = static_cast<int>(sizeof(T)) / 4;
+  static constexpr int kRows = kWords / kColsPerRow;
   uint32_t w[kWords];
   __device__ __forceinline__ void put(int r, T v) {
     if constexpr (sizeof(T) == 8) {
@@ -182,16 +184,11 @@ struct TChunk {
     if constexpr (sizeof(T) == 8) return __hiloint2double(static_cast<int>(w[2 * r + 1]), static_cast<int>(w[2 * r]));
     else return __uint_as_float(w[r]);
   }
-  __device__ __forceinline__ void store(uint32_t taddr) const {
-    if constexpr (kWords == 32) tmem_st32(taddr, w);
-    else tmem_st16(taddr, w);
-  }
-  __device__ __forceinline__ void load(uint32_t taddr) {
-    if constexpr (kWords == 32) tmem_ld32(taddr, w);
-    else tmem_ld16(taddr, w);
-  }
+  __device__ __forceinline__ void store(uint32_t taddr) const { tmem_st16(taddr, w); }
+  __device__ __forceinline__ void load(uint32_t taddr) { tmem_ld16(taddr, w); }
   __device__ __forceinline__ void wait() { tmem_wait_ld(w); }
 };
+static_assert(kSR % TPiece<double>::kRows == 0 && kSR % TPiece<float>::kRows == 0, "pieces tile a chunk");
 
 // Forward sweep over C consecutive kSR-row chunks in ascending row order,
 // on this lane's pair of systems. base(c): the lane's row-0 pair of chunk c
@@ -326,14 +323,32 @@ struct PerArgs {
   // map), out receives u_new; stencil coefficients s, 4s, 1-2s / 1-6s
   void* out = nullptr;
   double cn[3] = {0.0, 0.0, 0.0};
-  // TMEM tier (kernel template TM): head chunks [0, tmem_chunks) of each
-  // system live in Tensor Memory instead of the L2 spill
+  // TMEM tier (kernel template TM): head chunks [rc_chunks, rc_chunks +
+  // tmem_chunks) of each system live in Tensor Memory instead of the L2 spill
   int tmem_chunks = 0;
+  // recompute tier (TM only): head chunks [0, rc_chunks) are not stored at
+  // all. The forward sweep checkpoints its state every seg_chunks chunks; the
+  // backward sweep re-streams b for one segment at a time (last first),
+  // re-runs the forward recurrence from the checkpoint into TMEM (the same
+  // operations on the same inputs: bitwise the same intermediates), and
+  // sweeps back over it. Costs one extra read of b for those rows.
+  int rc_chunks = 0;
+  int seg_chunks = 0;
 };
 
-__host__ __device__ constexpr int stream_threads(int V, bool TM) { return 32 * ((TM ? 4 : stream_max_warps(V)) + 2); }
+// TM: 0 = no TMEM tier; 1 = TMEM tier, up to 4 compute warps (one TMEM lane
+// quadrant each, 512 columns); 2 = up to 8 compute warps (warps w and w+4
+// share a lane quadrant, 256 columns each)
+__host__ __device__ constexpr int stream_tm_warps(int TM) { return TM == 1 ? 4 : 8; }
+__host__ __device__ constexpr int stream_threads(int V, int TM) {
+  return 32 * ((TM ? stream_tm_warps(TM) : stream_max_warps(V)) + 2);
+}
+// TMEM chunks (16 rows) a system can hold: 2 KB (1 KB with 8 warps) of lane storage
+__host__ __device__ constexpr int stream_tmem_cap_chunks(int P, size_t elem) {
+  return (P > 4 ? 256 : 512) * 4 / (kSR * static_cast<int>(elem));
+}
 
-template <typename T, int V, bool PENT, bool FAST, int PER = 0, bool CN = false, bool TM = false>
+template <typename T, int V, bool PENT, bool FAST, int PER = 0, bool CN = false, int TM = 0>
 __global__ void __launch_bounds__(stream_threads(V, TM), 1)
     sweep_stream(const __grid_constant__ CUtensorMap map_b, T* __restrict__ x, int n, long long m, long long ld,
                  int H, int TC, int KB, int KR, int PD, int stagger_ns, long long groups,
@@ -343,14 +358,19 @@ __global__ void __launch_bounds__(stream_threads(V, TM), 1)
   static_assert(!CN || sizeof(T) == 8, "fused Crank-Nicolson: fp64 only");
   static_assert(!TM || V == 1, "TMEM tier: one system per lane");
   constexpr int kPerArrays = PER == 0 ? 0 : (PER == 1 ? 2 : 4);
+  // recompute tier geometry (not with the fused CN stencil, whose look-ahead
+  // crosses segment ends)
+  const int RCc = (TM && !CN) ? per.rc_chunks : 0;
+  const int Lc = RCc > 0 ? per.seg_chunks : 1;
+  const int nseg = (RCc + Lc - 1) / Lc;
   using FwdR = typename Recs<T, PENT>::Fwd;
   using BwdR = typename Recs<T, PENT>::Bwd;
   extern __shared__ __align__(128) unsigned char smem[];
   const int P = static_cast<int>(blockDim.x >> 5) - 2;  // compute warps; warp P loads b, warp P+1 reloads
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const StreamLayout L =
-      StreamLayout::make(n, H, TC, P * 32 * V, KB, KR, sizeof(T), sizeof(FwdR), sizeof(BwdR), kPerArrays);
+  const StreamLayout L = StreamLayout::make(n, H, TC, P * 32 * V, KB, KR, sizeof(T), sizeof(FwdR), sizeof(BwdR),
+                                           kPerArrays, nseg > 0 ? nseg - 1 : 0);
   const double* const spc = reinterpret_cast<const double*>(smem + L.per_off);  // staged per arrays
   const FwdR* sf = reinterpret_cast<const FwdR*>(smem + L.fwd_off);
   const BwdR* sb = reinterpret_cast<const BwdR*>(smem + L.bwd_off);
@@ -365,15 +385,17 @@ __global__ void __launch_bounds__(stream_threads(V, TM), 1)
   uint64_t* t_empty = t_full + TC;
   uint64_t* spilled = t_empty + TC;  // completes once per group when all warps' spills are published
   const int HC = H / kSR;
-  const int RTc = TM ? per.tmem_chunks : 0;  // head chunks held in TMEM
-  const int HS = HC - RTc;                   // head chunks spilled to L2
+  const int RTc = TM ? per.tmem_chunks : 0;  // head chunks held in TMEM (after the recomputed ones)
+  const int HS = HC - RCc - RTc;             // head chunks spilled to L2
+  const int HT = RCc + RTc;                  // first spilled head chunk
   constexpr int kLW = 32 * V;      // systems per warp
   constexpr int kSBlk = kSR * kLW;  // elements of one warp's block of one chunk
   const int Wg = P * kLW;
   const int chunk = P * kSBlk;  // elements of one chunk (all warps)
-  // this CTA's spill scratch: head chunks [RTc, HC) x P warps x (kSR x 32V),
-  // reused by every group; spill chunk c lives at (c - RTc)
-  T* const spill_cta = scratch + static_cast<long long>(blockIdx.x) * HS * chunk - static_cast<long long>(RTc) * chunk;
+  // this CTA's spill scratch: head chunks [HT, HC) x P warps x (kSR x 32V),
+  // reused by every group; spill chunk c lives at (c - HT)
+  T* const spill_cta = scratch + static_cast<long long>(blockIdx.x) * HS * chunk - static_cast<long long>(HT) * chunk;
+  const bool use_tmem = TM && (RTc > 0 || RCc > 0);
   uint32_t& tmem_base_s = *reinterpret_cast<uint32_t*>(spilled + 1);  // written by tcgen05.alloc
 
   {  // factor records -> smem (16-byte words; device arrays padded to 256 B)
@@ -412,16 +434,25 @@ __global__ void __launch_bounds__(stream_threads(V, TM), 1)
   if ((blockIdx.x & 1) && stagger_ns > 0) {
     for (int t = 0; t < stagger_ns; t += 1000) __nanosleep(1000);
   }
-  if constexpr (TM) {
-    if (warp == 0 && RTc > 0) tmem_alloc_512(&tmem_base_s);
+  if constexpr (TM != 0) {
+    if (warp == 0 && use_tmem) tmem_alloc_512(&tmem_base_s);
     tmem_fence_before();
   }
   __syncthreads();
-  uint32_t tmem_lane_base = 0;  // this warp's TMEM lane quadrant, column 0
-  if constexpr (TM) {
+  uint32_t tmem_lane_base = 0;  // this warp's TMEM lane quadrant and first column
+  if constexpr (TM != 0) {
     tmem_fence_after();
-    tmem_lane_base = (RTc > 0 ? tmem_base_s : 0u) + (static_cast<uint32_t>(32 * (warp & 3)) << 16);
+    tmem_lane_base = (use_tmem ? tmem_base_s : 0u) + (static_cast<uint32_t>(32 * (warp & 3)) << 16) +
+                     static_cast<uint32_t>((warp >> 2) * 256);
   }
+  // the k-th recomputed chunk the backward sweep consumes: segments last to
+  // first, chunks ascending within a segment (segment j = chunks [j Lc, ..))
+  auto rc_chunk = [RCc, Lc, nseg](int k) {
+    const int last_len = RCc - (nseg - 1) * Lc;
+    if (k < last_len) return (nseg - 1) * Lc + k;
+    k -= last_len;
+    return (nseg - 2 - k / Lc) * Lc + k % Lc;
+  };
 
   // tail chunk k of the group with iteration parity `par` lives in slot
   // par ? TC-1-k : k
@@ -438,7 +469,8 @@ __global__ void __launch_bounds__(stream_threads(V, TM), 1)
     const uint64_t pol_b = policy_evict_first();  // every byte of b is read once
     const uint64_t pol_keep = policy_evict_last();
     const long long my_groups = (groups - blockIdx.x + gridDim.x - 1) / gridDim.x;
-    const long long b_total = my_groups * HC;  // b chunks this CTA streams through the ring
+    const int GB = HC + RCc;                    // b chunks per group: the head, then the recomputed segments
+    const long long b_total = my_groups * GB;  // b chunks this CTA streams through the ring
     long long b_next = 0;                      // next b chunk (CTA-local index) to enter the ring
     long long b_pf = 0;                        // b chunks prefetched into L2 so far
     Cursor cur;
@@ -449,8 +481,9 @@ __global__ void __launch_bounds__(stream_threads(V, TM), 1)
     };
     auto prefetch = [&]() {
       while (b_pf < b_total && b_pf < b_next + PD) {
-        const long long gi = b_pf / HC;
-        const int c = static_cast<int>(b_pf - gi * HC);
+        const long long gi = b_pf / GB;
+        const int k = static_cast<int>(b_pf - gi * GB);
+        const int c = k < HC ? k : rc_chunk(k - HC);
         const int c0 = static_cast<int>((blockIdx.x + gi * gridDim.x) * Wg);
         for (int w = 0; w < P; ++w) tma_prefetch_2d(&map_b, c0 + w * kLW, c * kSR);
         ++b_pf;
@@ -480,7 +513,7 @@ __global__ void __launch_bounds__(stream_threads(V, TM), 1)
       if (pre == HC) load_tail();
       if (KR == 0 && HS > 0) {  // unified ring: the spill comes back through the same FIFO
         mbar_wait(spilled, par);
-        for (int c = HC - 1; c >= RTc; --c) {
+        for (int c = HC - 1; c >= HT; --c) {
           if (issued >= static_cast<uint32_t>(KB)) mbar_wait(&b_empty[cur.slot], cur.phase ^ 1u);
           mbar_expect_tx(&b_full[cur.slot], c_bytes);
           bulk_load(bring + cur.slot * chunk, spill_cta + static_cast<long long>(c) * chunk, c_bytes,
@@ -488,6 +521,14 @@ __global__ void __launch_bounds__(stream_threads(V, TM), 1)
           cur.next(KB);
           ++issued;
         }
+      }
+      for (int k = 0; k < RCc; ++k) {  // b again for the recomputed segments
+        if (issued >= static_cast<uint32_t>(KB)) mbar_wait(&b_empty[cur.slot], cur.phase ^ 1u);
+        load_chunk(bring + cur.slot * chunk, c0, rc_chunk(k) * kSR, &b_full[cur.slot]);
+        cur.next(KB);
+        ++issued;
+        ++b_next;
+        prefetch();
       }
     }
     return;
@@ -502,7 +543,7 @@ __global__ void __launch_bounds__(stream_threads(V, TM), 1)
     uint32_t it = 0;
     for (long long g = blockIdx.x; g < groups; g += gridDim.x, ++it) {
       mbar_wait(spilled, it & 1u);  // every warp's head d-hat of this group is in the scratch
-      for (int c = HC - 1; c >= RTc; --c) {
+      for (int c = HC - 1; c >= HT; --c) {
         if (issued >= static_cast<uint32_t>(KR)) mbar_wait(&r_empty[cur.slot], cur.phase ^ 1u);
         mbar_expect_tx(&r_full[cur.slot], c_bytes);
         bulk_load(rring + cur.slot * chunk, spill_cta + static_cast<long long>(c) * chunk, c_bytes,
@@ -523,6 +564,9 @@ __global__ void __launch_bounds__(stream_threads(V, TM), 1)
   P2* const rring_l = reinterpret_cast<P2*>(rring) + wl;
   P2* const tail_l = reinterpret_cast<P2*>(tail) + wl;
   P2* const spill_l = reinterpret_cast<P2*>(spill_cta) + wl;
+  // recompute checkpoints: entry k of this lane at ck_l[k * ck_stride]
+  Vec<T, 2>* const ck_l = reinterpret_cast<Vec<T, 2>*>(smem + L.ck_off) + warp * 32 + lane;
+  const int ck_stride = Wg;
   const int tfull = (n - H) / kSR;  // full tail chunks (a partial one may follow)
   const int trem = (n - H) - tfull * kSR;
   Cursor bw, brl, rw, rrl;  // wait / release cursors of the two rings
@@ -566,7 +610,8 @@ __global__ void __launch_bounds__(stream_threads(V, TM), 1)
       out -= ld;
     };
     P2 s1{}, s2{};
-    TChunk<T> tbuf;  // TMEM tier staging (one 16-row chunk)
+    TPiece<T> tbuf;  // TMEM tier staging (one piece of rows)
+    using TP = TPiece<T>;
     // CN window: w1 = u_{i-1}, w2 = u_{i-2}; u0s/u1s = u_0, u_1 for the wrap
     P2 w1 = nw1, w2 = nw2, u0s{}, u1s{};
     auto stencil = [&](int row, P2 u, auto&& look) -> P2 {
@@ -641,10 +686,16 @@ __global__ void __launch_bounds__(stream_threads(V, TM), 1)
             brl.next(KB);
           },
           [&](int c, int r, P2*, P2 v) {
-            if (TM && c < RTc) {  // TMEM tier: gather the chunk, one tcgen05.st per 16 rows
-              if constexpr (TM) {
-                tbuf.put(r, v.v[0]);
-                if (r == kSR - 1) tbuf.store(tmem_lane_base + static_cast<uint32_t>(c * TChunk<T>::kWords));
+            if (TM && c < RCc) {  // recompute tier: keep only the segment-start states
+              if constexpr (TM != 0) {
+                if (r == kSR - 1 && (c + 1) % Lc == 0 && c + 1 < RCc) ck_l[((c + 1) / Lc - 1) * ck_stride] = Vec<T, 2>{{s1.v[0], s2.v[0]}};
+              }
+            } else if (TM && c < HT) {  // TMEM tier: gather the chunk, one tcgen05.st per 16 rows
+              if constexpr (TM != 0) {
+                tbuf.put(r % TP::kRows, v.v[0]);
+                if (r % TP::kRows == TP::kRows - 1)
+                  tbuf.store(tmem_lane_base +
+                             static_cast<uint32_t>(((c - RCc) * kSR + r - (TP::kRows - 1)) * TP::kColsPerRow));
               }
             } else {
               st_spill_vec<T, V>(spill_l + c * cpairs + r * kPR, v, pol_keep);
@@ -728,7 +779,7 @@ __global__ void __launch_bounds__(stream_threads(V, TM), 1)
       const int K = uni ? KB : KR;
       uint32_t cs = 0;
       bwd_chunks<T, V, PENT, FAST>(
-          HS, sb + RTc * kSR, s1, s2, [&](int) -> const P2* { return ring_l + cs * cpairs; },
+          HS, sb + HT * kSR, s1, s2, [&](int) -> const P2* { return ring_l + cs * cpairs; },
           [&](int) {
             cs = cw.slot;
             mbar_wait(&full[cw.slot], cw.phase);
@@ -739,29 +790,67 @@ __global__ void __launch_bounds__(stream_threads(V, TM), 1)
             if (lane == 0) mbar_arrive(&empty[cr.slot]);
             cr.next(K);
           },
-          [&](int c, int r, P2 v) { emit((RTc + c) * kSR + r, v); });
+          [&](int c, int r, P2 v) { emit((HT + c) * kSR + r, v); });
     }
-    // ---- backward, TMEM rows: one tcgen05.ld per 16 rows, a chunk ahead
-    if constexpr (TM) {
-      if (RTc > 0) {
-        TChunk<T> cur, nxt;
-        cur.load(tmem_lane_base + static_cast<uint32_t>((RTc - 1) * TChunk<T>::kWords));
+    // ---- backward, TMEM rows: one tcgen05.ld per 16 rows, a chunk ahead.
+    // nc chunks at TMEM columns [0, nc) hold rows [row0, row0 + 16 nc).
+    auto tmem_bwd = [&](int nc, int row0) {
+      if constexpr (TM != 0) {
+        const int np = nc * (kSR / TP::kRows);  // pieces, processed last to first, one loaded ahead
+        tmem_wait_st();  // this warp's stores of the region have landed
+        TP cur, nxt;
+        cur.load(tmem_lane_base + static_cast<uint32_t>((np - 1) * TP::kWords));
         cur.wait();
-        for (int c = RTc - 1; c >= 0; --c) {
-          if (c > 0) nxt.load(tmem_lane_base + static_cast<uint32_t>((c - 1) * TChunk<T>::kWords));
-          const BwdR* b = sb + c * kSR;
+        for (int pc = np - 1; pc >= 0; --pc) {
+          if (pc > 0) nxt.load(tmem_lane_base + static_cast<uint32_t>((pc - 1) * TP::kWords));
+          const BwdR* b = sb + row0 + pc * TP::kRows;
 #pragma unroll
-          for (int q = 0; q < kSR; ++q) {
-            const int r = kSR - 1 - q;
+          for (int q = 0; q < TP::kRows; ++q) {
+            const int r = TP::kRows - 1 - q;
             P2 y;
             y.v[0] = bwd_row<T, PENT, FAST>(b[r], cur.get(r), s1.v[0], s2.v[0]);
-            emit(c * kSR + r, y);
+            emit(row0 + pc * TP::kRows + r, y);
           }
-          if (c > 0) {
+          if (pc > 0) {
             nxt.wait();
             cur = nxt;
           }
         }
+      }
+    };
+    if (TM && RTc > 0) tmem_bwd(RTc, RCc * kSR);
+    // ---- backward, recomputed rows: per segment (last first) b comes back
+    // through the b ring, the forward recurrence re-runs from the segment's
+    // checkpoint into TMEM, and the backward sweep continues over it
+    if constexpr (TM != 0) {
+      for (int j = nseg - 1; j >= 0; --j) {
+        const int cb = j * Lc;
+        const int len = min(Lc, RCc - cb);
+        P2 f1{}, f2{};
+        if (j > 0) {
+          const Vec<T, 2> ck = ck_l[(j - 1) * ck_stride];
+          f1.v[0] = ck.v[0];
+          f2.v[0] = ck.v[1];
+        }
+        uint32_t cs = 0;
+        fwd_chunks<T, V, PENT, FAST>(
+            len, sf + cb * kSR, f1, f2, [&](int) { return bring_l + cs * cpairs; },
+            [&](int) {
+              cs = bw.slot;
+              mbar_wait(&b_full[bw.slot], bw.phase);
+              bw.next(KB);
+            },
+            [&](int) {
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&b_empty[brl.slot]);
+              brl.next(KB);
+            },
+            [&](int c, int r, P2*, P2 v) {
+              tbuf.put(r % TP::kRows, v.v[0]);
+              if (r % TP::kRows == TP::kRows - 1)
+                tbuf.store(tmem_lane_base + static_cast<uint32_t>((c * kSR + r - (TP::kRows - 1)) * TP::kColsPerRow));
+            });
+        tmem_bwd(len, cb * kSR);
       }
     }
   };
@@ -773,14 +862,14 @@ __global__ void __launch_bounds__(stream_threads(V, TM), 1)
   // the scratch is dead: drop this warp's L2 lines instead of writing them back
   if (HS > 0) {
     __syncwarp();
-    for (int c = RTc; c < HC; ++c) {
+    for (int c = HT; c < HC; ++c) {
       const char* base = reinterpret_cast<const char*>(spill_cta + static_cast<long long>(c) * chunk + warp * kSBlk);
       for (int off = lane * 128; off < kSBlk * static_cast<int>(sizeof(T)); off += 32 * 128)
         discard_l2_line(base + off);
     }
   }
-  if constexpr (TM) {  // every compute warp is done with TMEM: warp 0 frees it
-    if (RTc > 0) {
+  if constexpr (TM != 0) {  // every compute warp is done with TMEM: warp 0 frees it
+    if (use_tmem) {
       tmem_fence_before();
       asm volatile("bar.sync 1, %0;" ::"r"(P * 32) : "memory");
       tmem_fence_after();

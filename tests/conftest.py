@@ -43,10 +43,22 @@ def reflib():
 
 
 @pytest.fixture(scope="session")
-def lib():
+def _product_lib():
     _build_product()
     from paper_1909_04539_b200.bandsolve import Library
     return Library(PRODUCT_LIB)
+
+
+@pytest.fixture
+def lib(_product_lib):
+    """The product library with a clean tuning table (bandsolve_tune_reset)
+    and the default device list around every test: overrides never leak
+    between tests."""
+    _product_lib.tune_reset()
+    _product_lib.set_devices([])
+    yield _product_lib
+    _product_lib.tune_reset()
+    _product_lib.set_devices([])
 
 
 class Golden:

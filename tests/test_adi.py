@@ -5,7 +5,6 @@ cyclic solve, exact transposes): bitwise in exact mode, 1e-12 in fast mode.
 """
 from __future__ import annotations
 
-import os
 
 import numpy as np
 import pytest
@@ -66,14 +65,14 @@ def test_gpu_adi_step(lib, oracle, cuda_device):
 def test_gpu_adi_fast_partitioned_fused_stencil(lib, oracle, cuda_device, fuse_pent):
     """Fast mode on grids large enough for the partitioned path (both axes
     >= 1024): the explicit half is fused into the partitioned forward pass
-    (tri; pent with BANDSOLVE_ADI_FUSE_PENT=1), the correction into the
+    (tri; pent with tuning key ADI_FUSE_PENT), the correction into the
     backward pass. Within 1e-12 of the oracle's ADI step; an odd pitch and a
     system count that is not a multiple of 32 take the unfused route."""
     torch = cuda_device
     rng = np.random.default_rng(43)
     stream = torch.cuda.current_stream().cuda_stream
     if fuse_pent:
-        os.environ["BANDSOLVE_ADI_FUSE_PENT"] = "1"
+        lib.tune("ADI_FUSE_PENT", "1")
     lib.set_mode(bs.MODE_FAST)
     try:
         for problem, ny, nx in [(0, 1024, 1056), (1, 1088, 1024), (0, 1030, 1024)]:
@@ -90,4 +89,4 @@ def test_gpu_adi_fast_partitioned_fused_stencil(lib, oracle, cuda_device, fuse_p
                 assert per_system_max_rel(f[:, :nx].cpu().numpy(), want) <= 1e-12, (problem, ny, nx, ld)
     finally:
         lib.set_mode(bs.MODE_EXACT)
-        os.environ.pop("BANDSOLVE_ADI_FUSE_PENT", None)
+        lib.tune("ADI_FUSE_PENT", None)

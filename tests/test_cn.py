@@ -129,16 +129,12 @@ def test_gpu_cn_step_dev(lib, oracle, cuda_device):
         h.cn_step_dev(0.5, du.data_ptr(), du.data_ptr(), 8, 4)
 
 
-PLAN_ENV = ("BANDSOLVE_PLAN", "BANDSOLVE_SWG", "BANDSOLVE_STAIL", "BANDSOLVE_SKB", "BANDSOLVE_SV", "BANDSOLVE_SKR")
-
-
-def set_stream_plan(plan):
-    for k in PLAN_ENV:
-        os.environ.pop(k, None)
+def set_stream_plan(lib, plan):
+    lib.tune_reset()
     if plan:
-        os.environ["BANDSOLVE_PLAN"] = "stream"
-        for k, v in zip(PLAN_ENV[1:], plan):
-            os.environ[k] = v
+        lib.tune("PLAN", "stream")
+        for k, v in zip(("SWG", "STAIL", "SKB", "SV", "SKR"), plan):
+            lib.tune(k, v)
 
 
 @pytest.mark.gpu
@@ -149,7 +145,7 @@ def test_gpu_cn_fused_over_plans(lib, oracle, cuda_device, plan):
     tail chunks and the wrap rows: every split must give the reference's
     bits (exact) / stay within 1e-12 (fast, fused correction)."""
     torch = cuda_device
-    set_stream_plan(plan)
+    set_stream_plan(lib, plan)
     rng = np.random.default_rng(31)
     try:
         for prob, n, m in [(0, 3, 70), (0, 37, 130), (0, 512, 200), (1, 6, 65), (1, 50, 129), (1, 512, 300)]:
@@ -176,4 +172,4 @@ def test_gpu_cn_fused_over_plans(lib, oracle, cuda_device, plan):
                     assert per_system_max_rel(got, want) <= 1e-12, (plan, prob, n, m)
     finally:
         lib.set_mode(bs.MODE_EXACT)
-        set_stream_plan(None)
+        set_stream_plan(lib, None)

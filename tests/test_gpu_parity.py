@@ -8,7 +8,6 @@ All solves go through the C ABI of libbandsolve_b200.so.
 """
 from __future__ import annotations
 
-import os
 
 import numpy as np
 import pytest
@@ -27,7 +26,6 @@ def _exact_mode(lib):
     lib.set_mode(bs.MODE_EXACT)
     yield
     lib.set_mode(bs.MODE_EXACT)
-    set_plan(None)
 
 
 # ---- helpers -------------------------------------------------------------------
@@ -138,42 +136,42 @@ def test_cyclic_residual_matches_oracle(lib, oracle, cuda_device):
 SHAPES = [(2, 1), (3, 2), (5, 3), (31, 7), (32, 16), (33, 17), (64, 8), (65, 40), (100, 33), (257, 130),
           (512, 64), (1024, 48)]
 # plan overrides: (BANDSOLVE_PLAN, BANDSOLVE_PWARPS, BANDSOLVE_PTAIL) for the persist/smem/global
-# plans; "stream" takes (BANDSOLVE_SWG, BANDSOLVE_STAIL, BANDSOLVE_SKB): group width, smem tail
-# rows, ring slots.
+# plans; "stream" takes (BANDSOLVE_SWG, BANDSOLVE_STAIL, BANDSOLVE_SKB, BANDSOLVE_SV, BANDSOLVE_SKR,
+# BANDSOLVE_SRC, BANDSOLVE_SSEG, BANDSOLVE_TM8): group width, smem tail rows, ring slots, systems
+# per lane, reload-ring slots, recomputed rows, recompute segment chunks, TMEM with 5..8 warps.
 PLANS = [None, ("global",), ("smemW8",), ("smemW16",), ("smemW32",), ("persist", "1", "0"),
          ("persist", "2", "48"), ("persist", "3", "100000"),
          ("stream", "64", "0", "4", "2"), ("stream", "64", "16", "2", "1"), ("stream", "128", "40", "4", "2"),
          ("stream", "256", "100000", "4", "1"), ("stream", "192", "33", "2", "2"), ("stream", "96", "48", "3", "1"),
          ("stream", "32", "0", "4", "1"), ("stream", "96", "48", "4", "1", "4"),
          ("stream", "64", "8", "3", "2", "2"), ("stream", "96", "16", "4", "1", "4"), ("stream", "128", "40", "4", "1", "4"),
-         ("stream", "32", "0", "2", "1", "2"), ("regs", "96"), ("regs", "32", "16"), ("regs", "224", "40")]
-PLAN_ENV = ("BANDSOLVE_PLAN", "BANDSOLVE_PWARPS", "BANDSOLVE_PTAIL", "BANDSOLVE_SWG", "BANDSOLVE_STAIL",
-            "BANDSOLVE_SKB", "BANDSOLVE_SV", "BANDSOLVE_SKR")
+         ("stream", "32", "0", "2", "1", "2"),
+         # recompute tier: segments re-streamed and re-run from checkpoints (bitwise like every plan)
+         ("stream", "128", "32", "4", "1", "4", "64", "2"), ("stream", "64", "16", "2", "1", "2", "100000", "3"),
+         ("stream", "96", "0", "3", "1", "0", "100000", "1"), ("stream", "32", "48", "4", "1", "4", "100000", "16"),
+         ("stream", "256", "16", "4", "1", "4", "48", "4", "1"), ("stream", "192", "32", "3", "1", "2", "100000", "8", "1")]
+STREAM_KEYS = ("SWG", "STAIL", "SKB", "SV", "SKR", "SRC", "SSEG", "TM8")
 
 
-def set_plan(plan):
-    for k in PLAN_ENV:
-        os.environ.pop(k, None)
+def set_plan(lib, plan):
+    """Force a plan through the tuning table (bandsolve_tune_set)."""
+    lib.tune_reset()
     if not plan:
         return
-    if plan[0] == "regs":
-        os.environ["BANDSOLVE_PLAN"] = "regs"
-        for k, v in zip(("BANDSOLVE_SWG", "BANDSOLVE_STAIL"), plan[1:]):
-            os.environ[k] = v
-    elif plan[0] == "stream":
-        os.environ["BANDSOLVE_PLAN"] = "stream"
-        for k, v in zip(("BANDSOLVE_SWG", "BANDSOLVE_STAIL", "BANDSOLVE_SKB", "BANDSOLVE_SV", "BANDSOLVE_SKR"), plan[1:]):
-            os.environ[k] = v
+    if plan[0] == "stream":
+        lib.tune("PLAN", "stream")
+        for k, v in zip(STREAM_KEYS, plan[1:]):
+            lib.tune(k, v)
     else:
-        for k, v in zip(("BANDSOLVE_PLAN", "BANDSOLVE_PWARPS", "BANDSOLVE_PTAIL"), plan):
-            os.environ[k] = v
+        for k, v in zip(("PLAN", "PWARPS", "PTAIL"), plan):
+            lib.tune(k, v)
 
 
 @pytest.mark.parametrize("plan", PLANS)
 def test_tri_device_plans_bitwise(lib, oracle, cuda_device, plan):
     torch = cuda_device
     rng = np.random.default_rng(100)
-    set_plan(plan)
+    set_plan(lib, plan)
     for n, m in SHAPES:
         bands = random_tri(rng, n)
         f = bs.TriFactor(lib, *bands)
@@ -189,7 +187,7 @@ def test_tri_device_plans_bitwise(lib, oracle, cuda_device, plan):
 def test_pent_device_plans_bitwise(lib, oracle, cuda_device, plan):
     torch = cuda_device
     rng = np.random.default_rng(200)
-    set_plan(plan)
+    set_plan(lib, plan)
     for n, m in SHAPES:
         if n < 5:
             continue
@@ -205,11 +203,12 @@ def test_pent_device_plans_bitwise(lib, oracle, cuda_device, plan):
         assert bitwise_equal(dev_solve(torch, u, rhs), want_u), (plan, n, m)
 
 
-@pytest.mark.parametrize("plan", [None, ("global",), ("persist", "2", "0"), ("stream", "64", "48", "4", "2"), ("stream", "96", "48", "4", "1")])
+@pytest.mark.parametrize("plan", [None, ("global",), ("persist", "2", "0"), ("stream", "64", "48", "4", "2"),
+                                  ("stream", "96", "48", "4", "1"), ("stream", "128", "32", "4", "1", "4", "100000", "4")])
 def test_fast_mode_within_tolerance(lib, oracle, cuda_device, plan):
     torch = cuda_device
     rng = np.random.default_rng(300)
-    set_plan(plan)
+    set_plan(lib, plan)
     lib.set_mode(bs.MODE_FAST)
     for n, m in [(2, 3), (33, 17), (256, 64), (512, 96), (2048, 32)]:
         tb = random_tri(rng, n)
@@ -340,3 +339,40 @@ def test_config3_tri_batch_2p20(lib, oracle, cuda_device, n):
 
 def test_pent_n512_batch_2p20(lib, oracle, cuda_device):
     _check_config(lib, oracle, cuda_device, "pent", 512, 1 << 20, bs.hyper_bands(1.0, 512), sample_cols=64)
+
+
+def test_config5_pent_n1024_batch_2p24(lib, oracle, cuda_device):
+    """configs[4] at its full single-GPU size: pent N=1024, 2^24 systems
+    (128 GiB in place, the bench's default workload). Exact mode bitwise and
+    fast mode <= 1e-12 against the oracle on a column sample spread over the
+    whole batch (pent_solver.cpp:15-81), plus the sample's residual."""
+    torch = cuda_device
+    free, _ = torch.cuda.mem_get_info()
+    n, m = 1024, 1 << 24
+    if free < n * m * 8 + (4 << 30):
+        pytest.skip(f"needs {n * m * 8 / 2**30:.0f} GiB of device memory, {free / 2**30:.0f} GiB free")
+    bands = bs.hyper_bands(1.0, n)
+    f = bs.PentFactor(lib, *bands)
+    ref_f = oracle.pent_prefactor(*bands)
+    rng = np.random.default_rng(5)
+    cols = np.unique(np.concatenate([np.arange(64), np.arange(m - 64, m), rng.integers(0, m, 128)]))
+    rhs = np.concatenate([oracle.rhs(42, n, 1, j_offset=int(c)) for c in cols], axis=1)
+    want = oracle.pent_solve(ref_f, rhs.copy())
+    x = torch.empty((n, m), dtype=torch.float64, device="cuda")
+    idx = torch.from_numpy(cols).cuda()
+    try:
+        for mode in (bs.MODE_EXACT, bs.MODE_FAST):
+            lib.set_mode(mode)
+            lib.fill_rhs_dev(x.data_ptr(), n, m, m, seed=42)
+            f.solve_dev(x.data_ptr(), n, m)
+            torch.cuda.synchronize()
+            got = x[:, idx].cpu().numpy()
+            if mode == bs.MODE_EXACT:
+                assert bitwise_equal(got, want)
+            else:
+                assert per_system_max_rel(got, want) <= TOL_F64
+            sx, sr = bs.Batch.from_array(lib, got), bs.Batch.from_array(lib, rhs)
+            assert lib.pent_residual(*bands, sx, sr) <= TOL_F64
+    finally:
+        del x
+        torch.cuda.empty_cache()

@@ -1,10 +1,12 @@
-"""Multi-GPU host logic on CPU: world-size-2 gloo processes.
+"""Multi-GPU sharding across processes: world-size-2 gloo groups.
 
 Each rank takes its shard of one global synthetic batch (partition.py, the
-reference's j0 = M*g/G split), solves it with the CPU oracle standing in for
-its GPU, and the shards reassembled on rank 0 must equal the single-process
-solve bit for bit (ref parallel.hpp:20-23: columns are partition
-independent). Also checks the max-over-ranks reduction bench.py times with.
+reference's j0 = M*g/G split, which bench.py uses for its strong-scaling
+shards), solves it, and the shards reassembled on rank 0 must equal the
+single-process solve bit for bit (ref parallel.hpp:20-23: columns are
+partition independent). On CPU the oracle stands in for each rank's GPU (the
+host logic: split, gather, max-over-ranks reduction); the gpu-marked variant
+solves every shard through the product library.
 """
 from __future__ import annotations
 
@@ -88,3 +90,56 @@ def test_two_rank_shards_reassemble_bitwise():
     same, tmax = q.get(timeout=5)
     assert same
     assert tmax == 2.0
+
+
+def _gpu_worker(rank: int, world: int, port: int, q) -> None:
+    """bench.py's strong-scaling split through the product: each rank
+    generates and solves its shard [j0, j1) of the global batch on the GPU
+    (both ranks share cuda:0 on a one-GPU box), rank 0 reassembles."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1909_04539_b200 import bandsolve as bs
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        lib = bs.load()
+        n, m = 1024, 40000
+        f = bs.PentFactor(lib, *bs.hyper_bands(1.0, n))
+        j0, j1 = shard_range(m, rank, world)
+        x = torch.empty((n, j1 - j0), dtype=torch.float64, device="cuda")
+        lib.fill_rhs_dev(x.data_ptr(), n, j1 - j0, j1 - j0, 42, j0)
+        f.solve_dev(x.data_ptr(), n, j1 - j0)
+        torch.cuda.synchronize()
+        width = max(shard_range(m, g, world)[1] - shard_range(m, g, world)[0] for g in range(world))
+        buf = torch.zeros((n, width), dtype=torch.float64)
+        buf[:, : j1 - j0] = x.cpu()
+        parts = [torch.zeros_like(buf) for _ in range(world)]
+        dist.all_gather(parts, buf)
+        if rank == 0:
+            full = torch.empty((n, m), dtype=torch.float64, device="cuda")
+            lib.fill_rhs_dev(full.data_ptr(), n, m, m, 42, 0)
+            f.solve_dev(full.data_ptr(), n, m)
+            torch.cuda.synchronize()
+            got = np.concatenate([p.numpy()[:, : shard_range(m, g, world)[1] - shard_range(m, g, world)[0]]
+                                  for g, p in enumerate(parts)], axis=1)
+            q.put(got.tobytes() == full.cpu().numpy().tobytes())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_two_rank_product_split_bitwise_on_gpu():
+    mp = pytest.importorskip("torch.multiprocessing")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    assert q.get(timeout=5)

@@ -4,12 +4,11 @@ Fast mode promises the reference's answer within a per-system max-norm
 relative error of 1e-12; the partitioned path reorders the
 arithmetic (block sweeps + a dense interface solve + spike update), so it is
 held to that same bound against the oracle, over ragged block splits, padded
-pitches and every band structure. BANDSOLVE_PARTITION=1 forces the path even
+pitches and every band structure. The tuning key PARTITION=1 forces the path even
 where the planner would not pick it; =0 disables it.
 """
 from __future__ import annotations
 
-import os
 
 import numpy as np
 import pytest
@@ -41,10 +40,10 @@ def _random_pent(rng, n):
 @pytest.fixture(autouse=True)
 def _fast_mode(lib):
     lib.set_mode(bs.MODE_FAST)
-    os.environ.pop("BANDSOLVE_PLAN", None)
+    lib.tune("PLAN", None)
     yield
     lib.set_mode(bs.MODE_EXACT)
-    os.environ.pop("BANDSOLVE_PARTITION", None)
+    lib.tune("PARTITION", None)
 
 
 def _dev_solve(torch, factor, rhs, ld=None):
@@ -64,7 +63,7 @@ def _dev_solve(torch, factor, rhs, ld=None):
 def test_partition_within_tolerance(lib, oracle, cuda_device, forced):
     torch = cuda_device
     if forced:
-        os.environ["BANDSOLVE_PARTITION"] = forced
+        lib.tune("PARTITION", forced)
     rng = np.random.default_rng(77)
     for n, m in [(128, 5), (200, 33), (1000, 64), (1023, 257), (4096, 128), (4099, 96)]:
         rhs = rng.uniform(-1, 1, (n, m))
@@ -121,9 +120,9 @@ def test_partition_disabled_matches_sequential(lib, oracle, cuda_device):
     pb = _random_pent(rng, n)
     rhs = rng.uniform(-1, 1, (n, m))
     f = bs.PentFactor(lib, *pb)
-    os.environ["BANDSOLVE_PARTITION"] = "1"
+    lib.tune("PARTITION", "1")
     part = _dev_solve(torch, f, rhs)
-    os.environ["BANDSOLVE_PARTITION"] = "0"
+    lib.tune("PARTITION", "0")
     seq = _dev_solve(torch, f, rhs)
     assert per_system_max_rel(part, seq) <= TOL_F64
 
@@ -134,7 +133,7 @@ def test_partition_periodic_fused_within_tolerance(lib, oracle, cuda_device, for
     backward pass: within 1e-12 of the reference's periodic solve."""
     torch = cuda_device
     if forced:
-        os.environ["BANDSOLVE_PARTITION"] = forced
+        lib.tune("PARTITION", forced)
     rng = np.random.default_rng(31)
     for n, m in [(130, 7), (1024, 130), (2050, 64), (4096, 33)]:
         x = rng.uniform(-1, 1, (n, m))
@@ -170,7 +169,7 @@ def test_partition_through_host_api(lib, oracle, cuda_device):
     bs.PentFactor(lib, *pb).solve(b)
     want = oracle.pent_solve(oracle.pent_prefactor(*pb), rhs.copy())
     assert per_system_max_rel(b.array, want) <= TOL_F64
-    os.environ["BANDSOLVE_HOST_CHUNK_MIB"] = "1"  # many small chunks: m per chunk = 64
+    lib.tune("HOST_CHUNK_MIB", "1")  # many small chunks: m per chunk = 64
     try:
         # the planner must pick the partitioned path for a chunk's shape, and
         # every chunk must launch exactly its two partitioned passes
@@ -183,7 +182,7 @@ def test_partition_through_host_api(lib, oracle, cuda_device):
         assert lib.kernel_launches() - before == 2 * chunks
         assert per_system_max_rel(b.array, want) <= TOL_F64
     finally:
-        os.environ.pop("BANDSOLVE_HOST_CHUNK_MIB", None)
+        lib.tune("HOST_CHUNK_MIB", None)
 
 
 def test_partition_rejects_growing_block_pivots(lib, oracle, cuda_device):
@@ -192,7 +191,7 @@ def test_partition_rejects_growing_block_pivots(lib, oracle, cuda_device):
     entry at a block start. The plan must be rejected (sequential
     sweep instead), so the answer stays within 1e-12 of the reference."""
     torch = cuda_device
-    os.environ["BANDSOLVE_PARTITION"] = "1"
+    lib.tune("PARTITION", "1")
     rng = np.random.default_rng(17)
     n, m = 2048, 256
     sub = np.full(n, -1.0); sub[0] = 0

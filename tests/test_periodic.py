@@ -34,19 +34,15 @@ def oracle_solve(oracle, bands, x, correct_only=False):
     return oracle.periodic_pent_solve(f, x.copy(), correct_only)
 
 
-PLAN_ENV = ("BANDSOLVE_PLAN", "BANDSOLVE_PWARPS", "BANDSOLVE_PTAIL", "BANDSOLVE_SWG", "BANDSOLVE_STAIL")
-
-
-def set_plan(plan):
-    """(BANDSOLVE_PLAN, warps/group width, tail rows) override for the sweep under the correction."""
-    for k in PLAN_ENV:
-        os.environ.pop(k, None)
+def set_plan(lib, plan):
+    """(PLAN, warps/group width, tail rows) override for the sweep under the correction."""
+    lib.tune_reset()
     if not plan:
         return
-    os.environ["BANDSOLVE_PLAN"] = plan[0]
-    keys = ("BANDSOLVE_SWG", "BANDSOLVE_STAIL") if plan[0] == "stream" else ("BANDSOLVE_PWARPS", "BANDSOLVE_PTAIL")
+    lib.tune("PLAN", plan[0])
+    keys = ("SWG", "STAIL") if plan[0] == "stream" else ("PWARPS", "PTAIL")
     for k, v in zip(keys, plan[1:]):
-        os.environ[k] = v
+        lib.tune(k, v)
 
 
 def make(lib, bands, n):
@@ -140,7 +136,7 @@ def test_gpu_periodic_matches_golden(lib, cuda_device, name, case):
 @pytest.mark.parametrize("plan", [None, ("global",), ("stream", "64", "16"), ("persist", "1", "0")])
 def test_gpu_periodic_device_bitwise(lib, oracle, cuda_device, plan):
     torch = cuda_device
-    set_plan(plan)
+    set_plan(lib, plan)
     rng = np.random.default_rng(5)
     try:
         for n, m in [(3, 1), (6, 7), (64, 33), (257, 130), (512, 200)]:
@@ -160,7 +156,7 @@ def test_gpu_periodic_device_bitwise(lib, oracle, cuda_device, plan):
                         want = oracle_solve(oracle, bands, x, correct_only)
                         assert bitwise_equal(got, want), (plan, n, m, ld, bands, correct_only)
     finally:
-        set_plan(None)
+        set_plan(lib, None)
 
 
 @pytest.mark.gpu
@@ -213,7 +209,7 @@ def test_gpu_periodic_fused_fast_within_tolerance(lib, oracle, cuda_device, wg):
     """Fast mode fuses the correction into the sweep (y_0, y_1 from dot products
     of the forward outputs): within the 1e-12 fp64 tolerance of the reference."""
     torch = cuda_device
-    set_plan(("stream", wg) if wg else None)
+    set_plan(lib, ("stream", wg) if wg else None)
     lib.set_mode(bs.MODE_FAST)
     rng = np.random.default_rng(21)
     try:
@@ -232,7 +228,7 @@ def test_gpu_periodic_fused_fast_within_tolerance(lib, oracle, cuda_device, wg):
                     assert per_system_max_rel(got, want) <= 1e-12, (wg, n, m, ld, bands)
     finally:
         lib.set_mode(bs.MODE_EXACT)
-        set_plan(None)
+        set_plan(lib, None)
 
 
 @pytest.mark.gpu
