@@ -346,7 +346,7 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
     # e2e through the reference-facing host API (pinned host batch; H2D,
     # sweep, D2H inside bandsolve_*_solve_shared, synchronous)
     e2e = None
-    if not args.f32 and not args.cn and not adi:
+    if not args.f32 and not args.cn and not adi and not args.no_e2e:
         # pinned host batch of this rank's columns (a leading column sample
         # when the shard exceeds E2E_MAX_SYSTEMS: host RAM, not the device,
         # bounds it), regenerated from the same generator indices
@@ -418,6 +418,7 @@ def main() -> int:
     ap.add_argument("--mode", choices=["exact", "fast"], default=os.environ.get("BANDSOLVE_BENCH_MODE", "exact"))
     ap.add_argument("--f32", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-API end-to-end leg (tuning runs)")
     ap.add_argument("--periodic", action="store_true", help="cyclic (periodic) variant of the config's LHS")
     ap.add_argument("--cn", action="store_true",
                     help="Crank-Nicolson step (periodic stencil RHS + cyclic solve, sigma_x = 1) per step")

@@ -214,7 +214,11 @@ typedef enum bandsolve_problem {
 typedef enum bandsolve_variant {
   BANDSOLVE_VARIANT_SHARED = 0,
   BANDSOLVE_VARIANT_PER_SYSTEM = 1,
-  BANDSOLVE_VARIANT_UNIFORM = 2 /* hyperdiffusion only */
+  BANDSOLVE_VARIANT_UNIFORM = 2, /* hyperdiffusion only */
+  /* extension: the per-system step with cuSPARSE's gtsvInterleavedBatch
+   * (Thomas) / gpsvInterleavedBatch as the solver, the paper's cuThomasBatch
+   * comparator; ERR_INTERNAL when cuSPARSE is absent */
+  BANDSOLVE_VARIANT_CUSPARSE = 3
 } bandsolve_variant;
 
 typedef struct bandsolve_bench_params {
@@ -305,6 +309,25 @@ bandsolve_status bandsolve_tri_solve_per_system_dev(double* a, double* b,
 bandsolve_status bandsolve_pent_solve_per_system_dev(
     double* a, double* b, double* c, double* d, double* e, double* f,
     size_t n, size_t m, size_t ld, void* stream);
+/* cuSPARSE comparators (extension): the library
+ * per-system batch solvers the paper benchmarks against, on the same
+ * interleaved layout with pitch m (cuSPARSE takes none). Bands are per-system
+ * copies, n x m each, device memory: tri dl (sub, dl[0] = 0), d, du (sup,
+ * du[n-1] = 0); pent ds, dl, d, du, dw (the a..e bands). x (n x m) is
+ * overwritten with the solution; the bands may be overwritten. tri algo:
+ * 0 Thomas (cuThomasBatch), 1 LU with partial pivoting, 2 QR; pent: 0 (QR).
+ * cuSPARSE is loaded at first use (dlopen libcusparse.so.12); absent ->
+ * BANDSOLVE_ERR_INTERNAL. Stream-ordered, no synchronisation. */
+int bandsolve_cusparse_available(void);
+bandsolve_status bandsolve_tri_solve_cusparse_dev(double* dl, double* d,
+                                                  double* du, double* x,
+                                                  size_t n, size_t m, int algo,
+                                                  void* stream);
+bandsolve_status bandsolve_pent_solve_cusparse_dev(double* ds, double* dl,
+                                                   double* d, double* du,
+                                                   double* dw, double* x,
+                                                   size_t n, size_t m,
+                                                   void* stream);
 bandsolve_status bandsolve_pent_solve_uniform_dev(
     const bandsolve_uniform_pent_factor* factor, double* x, size_t n,
     size_t m, size_t ld, void* stream);

@@ -58,6 +58,7 @@ class BenchResult(C.Structure):
 
 PROBLEM_DIFFUSION, PROBLEM_HYPERDIFFUSION = 0, 1
 VARIANT_SHARED, VARIANT_PER_SYSTEM, VARIANT_UNIFORM = 0, 1, 2
+VARIANT_CUSPARSE = 3  # extension: the per-system step with cuSPARSE as the solver
 
 # (name, restype, argtypes) of the reference ABI subset (ref bandsolve.h)
 _REFERENCE_SIGS = [
@@ -113,6 +114,9 @@ _EXTENSION_SIGS = [
     ("bandsolve_tri_solve_per_system_dev", _st, [_vp] * 4 + [_sz, _sz, _sz, _vp]),
     ("bandsolve_pent_solve_per_system_dev", _st, [_vp] * 6 + [_sz, _sz, _sz, _vp]),
     ("bandsolve_pent_solve_uniform_dev_f32", _st, [_vp, _vp, _sz, _sz, _sz, _vp]),
+    ("bandsolve_cusparse_available", C.c_int, []),
+    ("bandsolve_tri_solve_cusparse_dev", _st, [_vp] * 4 + [_sz, _sz, C.c_int, _vp]),
+    ("bandsolve_pent_solve_cusparse_dev", _st, [_vp] * 6 + [_sz, _sz, _vp]),
     ("bandsolve_tri_residual_dev", _st,
      [_dp, _dp, _dp, _sz, C.c_int, _vp, _vp, _sz, _sz, _vp, _dp]),
     ("bandsolve_pent_residual_dev", _st,
@@ -252,6 +256,21 @@ class Library:
                      stream: int = 0, f32: bool = False) -> None:
         fn = self.lib.bandsolve_fill_rhs_dev_f32 if f32 else self.lib.bandsolve_fill_rhs_dev
         self.check(fn(ptr, n, m, ld, seed, j_offset, stream), "fill_rhs_dev")
+
+    def cusparse_available(self) -> bool:
+        return bool(self.lib.bandsolve_cusparse_available())
+
+    def cusparse_solve_dev(self, band_ptrs: Sequence[int], x_ptr: int, n: int, m: int, algo: int = 0,
+                           stream: int = 0) -> None:
+        """cuSPARSE gtsv/gpsvInterleavedBatch comparator on per-system device
+        bands (3 tri / 5 pent pointers, n x m each, pitch m)."""
+        if len(band_ptrs) == 3:
+            st = self.lib.bandsolve_tri_solve_cusparse_dev(*band_ptrs, x_ptr, n, m, algo, stream)
+        elif len(band_ptrs) == 5:
+            st = self.lib.bandsolve_pent_solve_cusparse_dev(*band_ptrs, x_ptr, n, m, stream)
+        else:
+            raise ValueError("3 (tri) or 5 (pent) band pointers")
+        self.check(st, "cusparse_solve_dev")
 
     # -- residuals ----------------------------------------------------------
     def footprint(self, variant: int, n: int, m: int) -> tuple[int, float]:

@@ -204,6 +204,26 @@ BSB_API bandsolve_status bandsolve_pent_solve_per_system_dev(double* a, double* 
   return guarded([&] { return bsb::per_system_device(true, arr, n, m, ld, stream); });
 }
 
+BSB_API int bandsolve_cusparse_available(void) {
+  try {
+    return bsb::cusparse_available() ? 1 : 0;
+  } catch (...) {
+    return 0;
+  }
+}
+
+BSB_API bandsolve_status bandsolve_tri_solve_cusparse_dev(double* dl, double* d, double* du, double* x, size_t n,
+                                                          size_t m, int algo, void* stream) {
+  double* arr[3] = {dl, d, du};
+  return guarded([&] { return bsb::cusparse_solve_device(false, arr, x, n, m, algo, stream); });
+}
+
+BSB_API bandsolve_status bandsolve_pent_solve_cusparse_dev(double* ds, double* dl, double* d, double* du, double* dw,
+                                                           double* x, size_t n, size_t m, void* stream) {
+  double* arr[5] = {ds, dl, d, du, dw};
+  return guarded([&] { return bsb::cusparse_solve_device(true, arr, x, n, m, 0, stream); });
+}
+
 // ---- tridiagonal (capi.cpp:143-163) ----------------------------------------
 BSB_API bandsolve_status bandsolve_tri_factor_create(const double* sub, const double* diag, const double* sup,
                                                      size_t n, bandsolve_tri_factor** out) {

@@ -169,6 +169,11 @@ bandsolve_status partition_solve_device(const Factor& f, double* x, std::size_t 
 bandsolve_status per_system_device(bool pent, double* const* arr, std::size_t n, std::size_t m, std::size_t ld,
                                    void* stream);
 bandsolve_status per_system_host(bool pent, double* const* arr, std::size_t n, std::size_t m);
+// cuSPARSE comparators (cusparse_cmp.cpp, dlopen'ed): gtsv/gpsvInterleavedBatch
+// on per-system bands, n x m with pitch m; x overwritten, stream-ordered.
+bool cusparse_available();
+bandsolve_status cusparse_solve_device(bool pent, double* const* bands, double* x, std::size_t n, std::size_t m,
+                                       int algo, void* stream);
 // IBAT files (capi.cpp), reference batch.cpp:146-218
 bandsolve_status ibat_write(const char* path, const double* data, std::size_t n, std::size_t m);
 bandsolve_status ibat_read(const char* path, std::size_t* n, std::size_t* m, double** data, bool* pinned);

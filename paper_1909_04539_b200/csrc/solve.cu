@@ -1743,7 +1743,7 @@ bandsolve_status bench_run_device(const bandsolve_bench_params& prm, bandsolve_b
   if (prm.problem != BANDSOLVE_PROBLEM_DIFFUSION && prm.problem != BANDSOLVE_PROBLEM_HYPERDIFFUSION)
     return fail(BANDSOLVE_ERR_BAD_ARG, "unknown problem");
   if (prm.variant != BANDSOLVE_VARIANT_SHARED && prm.variant != BANDSOLVE_VARIANT_PER_SYSTEM &&
-      prm.variant != BANDSOLVE_VARIANT_UNIFORM)
+      prm.variant != BANDSOLVE_VARIANT_UNIFORM && prm.variant != BANDSOLVE_VARIANT_CUSPARSE)
     return fail(BANDSOLVE_ERR_BAD_ARG, "unknown variant");
   const std::string prefix = prm.dump_prefix ? prm.dump_prefix : "";
   if (prm.dump_every > 0 && prefix.empty()) return fail(BANDSOLVE_ERR_BAD_ARG, "dump_every needs dump_prefix");
@@ -1781,7 +1781,10 @@ bandsolve_status bench_run_device(const bandsolve_bench_params& prm, bandsolve_b
       field[i * m + j] = std::sin(2.0 * 3.141592653589793238462643383279502884 * k * xv);  // std::numbers::pi
     }
   }
-  const std::size_t ld = (m + 1) & ~std::size_t(1);  // even pitch keeps the TMA plans
+  // even pitch keeps the TMA plans; cuSPARSE's interleaved solvers take no pitch
+  const bool cusp = prm.variant == BANDSOLVE_VARIANT_CUSPARSE;
+  if (cusp && !cusparse_available()) return fail(BANDSOLVE_ERR_INTERNAL, "cuSPARSE comparator unavailable");
+  const std::size_t ld = cusp ? m : (m + 1) & ~std::size_t(1);
   const std::size_t bytes = n * ld * sizeof(double);
   double *du = nullptr, *ds = nullptr;
   double* dbands = nullptr;  // per-system variant: A' bands (n each) | replicated copies (n x ld each)
@@ -1797,8 +1800,10 @@ bandsolve_status bench_run_device(const bandsolve_bench_params& prm, bandsolve_b
     cudaGetLastError();
   };
   // per-system variant (pde.cpp:168-185, :199-221): every step rewrites
-  // replicated band copies of A', solves per system, then corrects
-  const bool per_sys = prm.variant == BANDSOLVE_VARIANT_PER_SYSTEM;
+  // replicated band copies of A', solves per system, then corrects. The
+  // cuSPARSE variant (extension) is the same step with gtsv/gpsvInterleavedBatch
+  // as the per-system solver (the paper's cuThomasBatch protocol).
+  const bool per_sys = prm.variant == BANDSOLVE_VARIANT_PER_SYSTEM || cusp;
   const int nb = diffusion ? 3 : 5;
   auto step = [&](const double* from, double* to) -> bandsolve_status {
     if (!per_sys) return cn_step_device(*per, sigma, from, to, n, m, ld, s);
@@ -1813,7 +1818,7 @@ bandsolve_status bench_run_device(const bandsolve_bench_params& prm, bandsolve_b
     }
     g_launches.fetch_add(nb, std::memory_order_relaxed);
     arr[nb] = to;
-    q = per_system_device(!diffusion, arr, n, m, ld, s);
+    q = cusp ? cusparse_solve_device(!diffusion, arr, to, n, m, 0, s) : per_system_device(!diffusion, arr, n, m, ld, s);
     if (q != BANDSOLVE_OK) return q;
     return launch_periodic_correct(*per, to, n, m, ld, s);
   };

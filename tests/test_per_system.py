@@ -11,6 +11,8 @@
 """
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import pytest
 
@@ -183,3 +185,115 @@ def test_gpu_per_system_statuses(lib, cuda_device, pent):
     fn = lib.lib.bandsolve_pent_solve_per_system if pent else lib.lib.bandsolve_tri_solve_per_system
     assert fn(*[b.handle for b in mixed]) == bs.ERR_SHAPE_MISMATCH
     assert fn(*([None] * (6 if pent else 4))) == bs.ERR_BAD_ARG
+
+
+# ---- cuSPARSE comparators (gtsv/gpsvInterleavedBatch) ---------------------------------------------
+def max_rel_err(got, want):
+    """Per-system max-norm relative error, max over systems."""
+    return float(np.max(np.max(np.abs(got - want), axis=0) / np.max(np.abs(want), axis=0)))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("pent", [False, True])
+def test_gpu_cusparse_comparator_vs_oracle(lib, oracle, cuda_device, pent):
+    """The library comparator solves the reference's per-system problems to
+    1e-12 of the oracle (different algorithms: Thomas / QR, so not bitwise)."""
+    torch = cuda_device
+    assert lib.cusparse_available()
+    rng = np.random.default_rng(14)
+    for n, m in [(5, 1), (64, 17), (513, 300)]:
+        arrays = random_pent_columns(rng, n, m) if pent else random_tri_columns(rng, n, m)
+        want = (oracle.pent_per_system(*arrays) if pent else oracle.tri_per_system(*arrays))[-1]
+        dev = [torch.from_numpy(np.ascontiguousarray(v)).cuda() for v in arrays]
+        lib.cusparse_solve_dev([t.data_ptr() for t in dev[:-1]], dev[-1].data_ptr(), n, m,
+                               stream=torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        assert max_rel_err(dev[-1].cpu().numpy(), want) <= 1e-12, (n, m)
+
+
+@pytest.mark.gpu
+def test_gpu_cusparse_arguments(lib, cuda_device):
+    torch = cuda_device
+    t = torch.zeros((4, 3), dtype=torch.float64, device="cuda")
+    p = t.data_ptr()
+    with pytest.raises(bs.BandsolveError) as e:
+        lib.cusparse_solve_dev([p, p, p, p, p], p, 4, 3)  # pent needs n >= 5
+    assert e.value.status == bs.ERR_BAD_ARG
+    with pytest.raises(bs.BandsolveError) as e:
+        lib.cusparse_solve_dev([p, p, p], p, 4, 3, algo=7)
+    assert e.value.status == bs.ERR_BAD_ARG
+    assert lib.lib.bandsolve_tri_solve_cusparse_dev(None, None, None, None, 4, 3, 0, None) == bs.ERR_BAD_ARG
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("problem", [bs.PROBLEM_DIFFUSION, bs.PROBLEM_HYPERDIFFUSION])
+def test_gpu_bench_cusparse_variant_tracks_shared(lib, cuda_device, tmp_path, problem):
+    """The cuSPARSE step (same stencil, same correction) evolves the same
+    field as the shared step to rounding (pde.cpp run_benchmark protocol)."""
+    n, m, steps = 64, 48, 5
+    fields = {}
+    for v in (bs.VARIANT_SHARED, bs.VARIANT_CUSPARSE):
+        prefix = str(tmp_path / f"v{v}")
+        r = lib.bench_run(n, m, steps, problem=problem, variant=v, dump_every=steps, dump_prefix=prefix)
+        assert r.steps == steps and r.per_step_mean_s > 0
+        b = bs.Batch.read_ibat(lib, f"{prefix}_step{steps}.ibat")
+        fields[v] = b.array.copy()
+        b.close()
+    assert np.max(np.abs(fields[bs.VARIANT_SHARED] - fields[bs.VARIANT_CUSPARSE])) <= 1e-12
+
+
+@pytest.mark.gpu
+def test_gpu_acceptance_speedup_trend(lib, cuda_device):
+    """Reference acceptance criterion 8 (acceptance_main.cpp:482-510): at
+    n = 256, m = 4096, 1000 Crank-Nicolson steps, the shared-LHS step is no
+    slower than the per-system step, for both problems (mean of 3 runs)."""
+    for problem in (bs.PROBLEM_DIFFUSION, bs.PROBLEM_HYPERDIFFUSION):
+        mean = {}
+        for v in (bs.VARIANT_SHARED, bs.VARIANT_PER_SYSTEM):
+            mean[v] = sum(lib.bench_run(256, 4096, 1000, problem=problem, variant=v).per_step_mean_s
+                          for _ in range(3)) / 3
+        assert mean[bs.VARIANT_SHARED] <= mean[bs.VARIANT_PER_SYSTEM], (problem, mean)
+
+
+# ---- the bench command (reference tools/main.cpp run_bench) -----------------------------------------
+CLI = os.path.join(os.path.dirname(bs.DEFAULT_LIB), "bandsolve_b200")
+
+
+def run_cli(*args):
+    import subprocess
+    return subprocess.run([CLI, *args], capture_output=True, text=True, timeout=600)
+
+
+def test_cli_version_and_argument_errors(lib, tmp_path):
+    """Argument validation happens before any device work (exit 2, as the
+    reference's exit_args); --version prints the library version."""
+    assert os.path.exists(CLI), "bandsolve_b200 not built"
+    r = run_cli("--version")
+    assert r.returncode == 0 and r.stdout.strip() == "1.0.0"
+    out = str(tmp_path / "b.csv")
+    for bad in (["--problem", "heat"], ["--variants", "shared,fancy"], ["--n", "64,0"], ["--m", "x"],
+                ["--steps", "0"], ["--problem", "diffusion", "--variants", "uniform"], ["--bogus", "1"]):
+        r = run_cli("bench", "--out", out, *bad)
+        assert r.returncode == 2, (bad, r.stderr)
+        assert not os.path.exists(out)
+    assert run_cli("solve").returncode == 2
+
+
+@pytest.mark.gpu
+def test_gpu_cli_bench_csv_schema(lib, cuda_device, tmp_path):
+    out = tmp_path / "bench.csv"
+    r = run_cli("bench", "--problem", "both", "--variants", "shared,persystem,cusparse", "--n", "64,128",
+                "--m", "64,256", "--steps", "20", "--out", str(out))
+    assert r.returncode == 0, r.stderr
+    rows = out.read_text().splitlines()
+    assert rows[0] == "problem,variant,n,m,steps,threads,wall_s,per_step_mean_s,per_step_std_s,elements"
+    assert len(rows) == 1 + 2 * 3 * 2 * 2
+    for row in rows[1:]:
+        f = row.split(",")
+        assert f[0] in ("diffusion", "hyperdiffusion") and f[1] in ("shared", "persystem", "cusparse")
+        assert int(f[4]) == 20 and float(f[7]) > 0
+    sp = (tmp_path / "bench.speedup.csv").read_text().splitlines()
+    assert sp[0] == "problem,n,m,variant,speedup_vs_persystem"
+    assert len(sp) == 1 + 2 * 2 * 2 * 2
+    spc = (tmp_path / "bench.speedup_cusparse.csv").read_text().splitlines()
+    assert spc[0] == "problem,n,m,variant,speedup_vs_cusparse"
