@@ -692,7 +692,7 @@ cudaError_t launch_stream_v(const Plan& plan, T* x, int n, long long m, long lon
   auto kern = dev::sweep_stream<T, V, PENT, FAST, PER, CN, TM>;
   dev::PerArgs per = per_in;
   per.tmem_chunks = TM ? plan.tmem_chunks : 0;
-  per.rc_chunks = (TM && !CN) ? plan.rc_chunks : 0;
+  per.rc_chunks = (TM >= 2 && !CN) ? plan.rc_chunks : 0;
   per.seg_chunks = per.rc_chunks > 0 ? plan.seg_chunks : 0;
   if (plan.warps > dev::stream_tm_warps(TM) && TM) return cudaErrorInvalidConfiguration;
   static std::atomic<uint64_t> configured{0};  // one bit per device: attributes are per context
@@ -726,9 +726,12 @@ cudaError_t launch_stream_v(const Plan& plan, T* x, int n, long long m, long lon
 template <typename T, bool PENT, bool FAST>
 cudaError_t launch_stream(const Plan& plan, T* x, int n, long long m, long long ld, const void* fwd,
                           const void* bwd, cudaStream_t s, int sms) {
-  if (plan.V == 1 && (plan.tmem_chunks > 0 || plan.rc_chunks > 0))
-    return plan.warps > 4 ? launch_stream_v<T, 1, PENT, FAST, 0, false, 2>(plan, x, n, m, ld, fwd, bwd, s, sms)
-                          : launch_stream_v<T, 1, PENT, FAST, 0, false, 1>(plan, x, n, m, ld, fwd, bwd, s, sms);
+  if (plan.V == 1 && plan.warps > 4 && (plan.tmem_chunks > 0 || plan.rc_chunks > 0))
+    return launch_stream_v<T, 1, PENT, FAST, 0, false, 3>(plan, x, n, m, ld, fwd, bwd, s, sms);
+  if (plan.V == 1 && plan.rc_chunks > 0)
+    return launch_stream_v<T, 1, PENT, FAST, 0, false, 2>(plan, x, n, m, ld, fwd, bwd, s, sms);
+  if (plan.V == 1 && plan.tmem_chunks > 0)
+    return launch_stream_v<T, 1, PENT, FAST, 0, false, 1>(plan, x, n, m, ld, fwd, bwd, s, sms);
   if (plan.V == 2) return launch_stream_v<T, 2, PENT, FAST>(plan, x, n, m, ld, fwd, bwd, s, sms);
   return launch_stream_v<T, 1, PENT, FAST>(plan, x, n, m, ld, fwd, bwd, s, sms);
 }

@@ -145,12 +145,8 @@ __device__ __forceinline__ void tmem_dealloc_512(uint32_t taddr) {  // the alloc
 }
 __device__ __forceinline__ void tmem_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tmem_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-// 16 consecutive 32-bit columns of this lane (8 fp64 / 16 fp32 rows). The
-// store is asynchronous: its source registers are free once it issues (the
-// hardware scoreboard covers them), but its data is only guaranteed visible
-// to later tcgen05.ld after tmem_wait_st(), which the readers issue once
-// before they start (not once per store: each wait would stall the warp for
-// the full TMEM write latency inside the dependent row loop).
+// 16 / 32 consecutive 32-bit columns of this lane. tcgen05.st is
+// asynchronous; its data is visible to later tcgen05.ld after tmem_wait_st().
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16};" ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]) : "memory");
 }
@@ -158,17 +154,32 @@ __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];" : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]) : "r"(taddr) : "memory");
 }
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]) : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];" : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]) : "r"(taddr) : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld(uint32_t (&r)[32]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]), "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]), "+r"(r[29]), "+r"(r[30]), "+r"(r[31]) :: "memory");
+}
 // wait for this thread's TMEM loads; the registers are in/out operands so no
 // consumer can be scheduled above the wait
 __device__ __forceinline__ void tmem_wait_ld(uint32_t (&r)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15]) :: "memory");
 }
-// A piece of one lane's consecutive rows <-> 16 raw 32-bit TMEM words (one
-// .32x32b.x16 access): 8 fp64 / 16 fp32 rows. Row i of a TMEM region sits
-// at column i * kColsPerRow.
+// A piece of one lane's consecutive rows <-> raw 32-bit TMEM words: one
+// whole 16-row chunk per .32x32b access (x32 for fp64, x16 for fp32; the
+// 8-row x16 pieces for fp64 measured 10% slower at N = 512: twice the
+// tcgen05 instructions and waits in the row loops). Row i of a TMEM region
+// sits at column i * kColsPerRow.
+#ifndef BSB_TMEM_PIECE_ROWS
+#define BSB_TMEM_PIECE_ROWS 16
+#endif
 template <typename T>
 struct TPiece {
-  static constexpr int kWords = 16;
+  static constexpr int kWords = sizeof(T) == 8 ? 2 * BSB_TMEM_PIECE_ROWS : 16;
+  static_assert(kWords == 16 || kWords == 32, "x16 / x32 accesses");
   static constexpr int kColsPerRow = static_cast<int>(sizeof(T)) / 4;
   static constexpr int kRows = kWords / kColsPerRow;
   uint32_t w[kWords];
@@ -184,8 +195,19 @@ struct TPiece {
     if constexpr (sizeof(T) == 8) return __hiloint2double(static_cast<int>(w[2 * r + 1]), static_cast<int>(w[2 * r]));
     else return __uint_as_float(w[r]);
   }
-  __device__ __forceinline__ void store(uint32_t taddr) const { tmem_st16(taddr, w); }
-  __device__ __forceinline__ void load(uint32_t taddr) { tmem_ld16(taddr, w); }
+  // store, then wait for it: measured on B200 (N = 512, fp64) x32 + wait
+  // 0.71 of roofline, x16 without the wait 0.64, x32 without it 0.49 — an
+  // in-flight tcgen05.st pins its source registers, and the next piece's
+  // gather into them stalls longer than the wait itself
+  __device__ __forceinline__ void store(uint32_t taddr) const {
+    if constexpr (kWords == 32) tmem_st32(taddr, w);
+    else tmem_st16(taddr, w);
+    tmem_wait_st();
+  }
+  __device__ __forceinline__ void load(uint32_t taddr) {
+    if constexpr (kWords == 32) tmem_ld32(taddr, w);
+    else tmem_ld16(taddr, w);
+  }
   __device__ __forceinline__ void wait() { tmem_wait_ld(w); }
 };
 static_assert(kSR % TPiece<double>::kRows == 0 && kSR % TPiece<float>::kRows == 0, "pieces tile a chunk");
@@ -337,9 +359,13 @@ struct PerArgs {
 };
 
 // TM: 0 = no TMEM tier; 1 = TMEM tier, up to 4 compute warps (one TMEM lane
-// quadrant each, 512 columns); 2 = up to 8 compute warps (warps w and w+4
-// share a lane quadrant, 256 columns each)
-__host__ __device__ constexpr int stream_tm_warps(int TM) { return TM == 1 ? 4 : 8; }
+// quadrant each, 512 columns); 2 = TMEM tier + recompute tier, up to 4
+// compute warps; 3 = TMEM + recompute, up to 8 compute warps (warps w and
+// w+4 share a lane quadrant, 256 columns each). The recompute code lives only
+// in TM >= 2 instances: compiled into the plain TMEM kernel it pushes that
+// kernel to 255 registers with spills (measured 0.71 -> 0.49 of roofline at
+// N = 512).
+__host__ __device__ constexpr int stream_tm_warps(int TM) { return TM == 3 ? 8 : 4; }
 __host__ __device__ constexpr int stream_threads(int V, int TM) {
   return 32 * ((TM ? stream_tm_warps(TM) : stream_max_warps(V)) + 2);
 }
@@ -360,7 +386,8 @@ __global__ void __launch_bounds__(stream_threads(V, TM), 1)
   constexpr int kPerArrays = PER == 0 ? 0 : (PER == 1 ? 2 : 4);
   // recompute tier geometry (not with the fused CN stencil, whose look-ahead
   // crosses segment ends)
-  const int RCc = (TM && !CN) ? per.rc_chunks : 0;
+  constexpr bool kRC = TM >= 2 && !CN;
+  const int RCc = kRC ? per.rc_chunks : 0;
   const int Lc = RCc > 0 ? per.seg_chunks : 1;
   const int nseg = (RCc + Lc - 1) / Lc;
   using FwdR = typename Recs<T, PENT>::Fwd;
@@ -443,7 +470,7 @@ __global__ void __launch_bounds__(stream_threads(V, TM), 1)
   if constexpr (TM != 0) {
     tmem_fence_after();
     tmem_lane_base = (use_tmem ? tmem_base_s : 0u) + (static_cast<uint32_t>(32 * (warp & 3)) << 16) +
-                     static_cast<uint32_t>((warp >> 2) * 256);
+                     (TM == 3 ? static_cast<uint32_t>((warp >> 2) * 256) : 0u);
   }
   // the k-th recomputed chunk the backward sweep consumes: segments last to
   // first, chunks ascending within a segment (segment j = chunks [j Lc, ..))
@@ -686,8 +713,8 @@ __global__ void __launch_bounds__(stream_threads(V, TM), 1)
             brl.next(KB);
           },
           [&](int c, int r, P2*, P2 v) {
-            if (TM && c < RCc) {  // recompute tier: keep only the segment-start states
-              if constexpr (TM != 0) {
+            if (kRC && c < RCc) {  // recompute tier: keep only the segment-start states
+              if constexpr (kRC) {
                 if (r == kSR - 1 && (c + 1) % Lc == 0 && c + 1 < RCc) ck_l[((c + 1) / Lc - 1) * ck_stride] = Vec<T, 2>{{s1.v[0], s2.v[0]}};
               }
             } else if (TM && c < HT) {  // TMEM tier: gather the chunk, one tcgen05.st per 16 rows
@@ -822,7 +849,7 @@ __global__ void __launch_bounds__(stream_threads(V, TM), 1)
     // ---- backward, recomputed rows: per segment (last first) b comes back
     // through the b ring, the forward recurrence re-runs from the segment's
     // checkpoint into TMEM, and the backward sweep continues over it
-    if constexpr (TM != 0) {
+    if constexpr (kRC) {
       for (int j = nseg - 1; j >= 0; --j) {
         const int cb = j * Lc;
         const int len = min(Lc, RCc - cb);
