@@ -38,11 +38,15 @@
 #include <vector>
 
 #include "internal.hpp"
-#include "sweep_kernels.cuh"
+#include "sweep_spike.cuh"
 
 namespace bsb {
 
 cudaError_t upload_sync(void* dst, const void* src, std::size_t bytes);  // solve.cu
+bool encode_tile_map(CUtensorMap* map, void* x, std::size_t elem, long long n, long long m, long long ld,
+                     int box_w, int box_r);              // solve.cu
+cudaError_t allow_max_smem(const void* kern);            // solve.cu
+std::size_t max_smem_per_block();                        // solve.cu
 
 struct PartPlan {
   int K = 0, R = 0, L = 0;
@@ -54,12 +58,15 @@ struct PartPlan {
   std::vector<double> rinv;                // R x R inverse of the interface matrix, row-major
   bool ok = false;                         // false: the plan broke down (sequential sweep instead)
   std::vector<std::pair<int, void*>> dev;  // device blobs
+  std::vector<std::pair<int, void*>> spike_dev;  // device blobs of the one-pass kernel's records
   ~PartPlan() {
-    for (auto& d : dev) {
-      int prev = -1;
-      if (cudaGetDevice(&prev) == cudaSuccess && prev != d.first) cudaSetDevice(d.first);
-      cudaFree(d.second);
-      if (prev >= 0 && prev != d.first) cudaSetDevice(prev);
+    for (auto* list : {&dev, &spike_dev}) {
+      for (auto& d : *list) {
+        int prev = -1;
+        if (cudaGetDevice(&prev) == cudaSuccess && prev != d.first) cudaSetDevice(d.first);
+        cudaFree(d.second);
+        if (prev >= 0 && prev != d.first) cudaSetDevice(prev);
+      }
     }
     cudaGetLastError();
   }
@@ -696,6 +703,165 @@ bandsolve_status partition_solve_device(const Factor& f, double* x, std::size_t 
   cudaFreeAsync(yi, s);
   if (cudaError_t e = cudaGetLastError(); e != cudaSuccess)
     return fail(BANDSOLVE_ERR_INTERNAL, std::string("partition launch: ") + cudaGetErrorString(e));
+  *done = true;
+  return BANDSOLVE_OK;
+}
+
+// ---- one-pass partitioned sweep for many long systems (sweep_spike.cuh) ----------
+
+namespace {
+
+// Records of the one-pass kernel: [SpF x n][SpB x n] (the plan's block
+// factors, U^-1 rows and left-coupling images, interleaved per row).
+std::vector<double> spike_records(const PartPlan& p, int n) {
+  const bool pent = p.pent;
+  const int wf = pent ? 6 : 4, wb = pent ? 4 : 2;
+  std::vector<double> r(static_cast<std::size_t>(n) * (wf + wb), 0.0);
+  double* f = r.data();
+  double* b = r.data() + static_cast<std::size_t>(n) * wf;
+  for (int i = 0; i < n; ++i) {
+    const std::size_t u = static_cast<std::size_t>(i);
+    if (pent) {
+      f[6 * u + 0] = p.fwd[4 * u];      // eps/alpha
+      f[6 * u + 1] = p.fwd[4 * u + 1];  // beta/alpha
+      f[6 * u + 2] = p.fwd[4 * u + 2];  // 1/alpha
+      f[6 * u + 3] = p.pr[u];           // U^-1 row 0
+      f[6 * u + 4] = p.pr[n + u];       // U^-1 row 1
+      b[4 * u + 0] = p.bwd[2 * u];      // gamma
+      b[4 * u + 1] = p.bwd[2 * u + 1];  // delta
+      b[4 * u + 2] = p.fl[u];           // F (x_{s-2})
+      b[4 * u + 3] = p.fl[n + u];       // F (x_{s-1})
+    } else {
+      f[4 * u + 0] = p.fwd[2 * u];      // a/denom
+      f[4 * u + 1] = p.fwd[2 * u + 1];  // 1/denom
+      f[4 * u + 2] = p.pr[u];           // U^-1 row 0
+      b[2 * u + 0] = p.bwd[u];          // chat
+      b[2 * u + 1] = p.fl[u];           // F (x_{s-1})
+    }
+  }
+  return r;
+}
+
+// the plan for K blocks (cached on the factor), or nullptr when it broke down
+PartPlan* cached_plan(const Factor& f, int K) {
+  for (auto& q : f.parts)
+    if (q && q->K == K) return q->ok ? q.get() : nullptr;
+  auto q = build_plan(f, K);
+  if (!q) return nullptr;
+  PartPlan* p = q.get();
+  f.parts.push_back(std::move(q));
+  return p->ok ? p : nullptr;
+}
+
+int spike_ring_slots(int n, int R, bool pent) {
+  const std::size_t cap = max_smem_per_block();
+  for (int kb = 6; kb >= 2; --kb)
+    if (dev::SpikeLayout::make(n, R, kb, pent).total <= cap) return kb;
+  return 0;
+}
+
+}  // namespace
+
+int spike_blocks(std::size_t n, std::size_t m, std::size_t ld, const void* x, int sms, bool pent) {
+  const long long sel = tune_int("SPIKE", -1);  // 0: never, 1: whenever it applies
+  if (sel == 0 || tune_flag("PLAN")) return 0;
+  if (current_mode() != BANDSOLVE_MODE_FAST || n > static_cast<std::size_t>(dev::kSpMaxK) * dev::kSpMaxL || m == 0)
+    return 0;
+  if (reinterpret_cast<uintptr_t>(x) % 16 != 0 || ld % 2 != 0 || m > static_cast<std::size_t>(INT_MAX) / 2) return 0;
+  if (m % 2 != 0) return 0;  // TMA boxes: an odd batch would straddle a 16-byte granule at the edge
+  int K = 0;
+  for (int k = 2; k <= dev::kSpMaxK; k *= 2)
+    if (n % k == 0 && (n / k) % dev::kSpR == 0 && n / k <= static_cast<std::size_t>(dev::kSpMaxL) &&
+        n / k >= 2 * dev::kSpR) {
+      K = k;
+      break;
+    }
+  if (K == 0) return 0;
+  // many systems: at least one full wave of 32 (dev::kSpWarps / K)-system groups
+  const std::size_t wg = 32u * (dev::kSpWarps / K);
+  if (sel != 1 && m < static_cast<std::size_t>(sms) * wg) return 0;
+  if (spike_ring_slots(static_cast<int>(n), (pent ? 4 : 2) * K, pent) == 0) return 0;
+  return K;
+}
+
+bandsolve_status spike_solve_device(const Factor& f, double* x, std::size_t n, std::size_t m, std::size_t ld,
+                                    void* stream, int sms, bool* done) {
+  *done = false;
+  const bool pent = f.kind != Kind::Tri;
+  const int K = spike_blocks(n, m, ld, x, sms, pent);
+  if (K == 0) return BANDSOLVE_OK;
+  int device = 0;
+  if (cudaGetDevice(&device) != cudaSuccess) {
+    cudaGetLastError();
+    return BANDSOLVE_OK;
+  }
+  PartPlan* p = nullptr;
+  void* blob = nullptr;
+  {
+    std::lock_guard<std::mutex> lock(f.mu);
+    p = cached_plan(f, K);
+    if (!p) return BANDSOLVE_OK;  // a block pivot broke down or grew: the sequential sweep handles it
+    for (auto& d : p->spike_dev)
+      if (d.first == device) blob = d.second;
+    if (!blob) {
+      const std::vector<double> rec = spike_records(*p, static_cast<int>(n));
+      const std::size_t bytes = (rec.size() + p->rinv.size()) * sizeof(double);
+      if (cudaMalloc(&blob, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(BANDSOLVE_ERR_INTERNAL, "spike plan upload");
+      }
+      if (upload_sync(blob, rec.data(), rec.size() * sizeof(double)) != cudaSuccess ||
+          upload_sync(static_cast<double*>(blob) + rec.size(), p->rinv.data(), p->rinv.size() * sizeof(double)) !=
+              cudaSuccess) {
+        cudaGetLastError();
+        cudaFree(blob);
+        return fail(BANDSOLVE_ERR_INTERNAL, "spike plan upload");
+      }
+      p->spike_dev.emplace_back(device, blob);
+    }
+  }
+  const int N = static_cast<int>(n);
+  const int R = p->R;
+  const int KB = spike_ring_slots(N, R, pent);
+  const std::size_t rec_doubles = static_cast<std::size_t>(n) * (pent ? 10 : 6);
+  const double* rinv = static_cast<const double*>(blob) + rec_doubles;
+  CUtensorMap map;
+  if (!encode_tile_map(&map, x, sizeof(double), N, static_cast<long long>(m), static_cast<long long>(ld), 32,
+                       dev::kSpR))
+    return BANDSOLVE_OK;  // no tensor map: the sweep plans take it
+  const int Wg = 32 * (dev::kSpWarps / K);
+  const long long groups = (static_cast<long long>(m) + Wg - 1) / Wg;
+  const unsigned grid = static_cast<unsigned>(std::min<long long>(sms, groups));
+  const std::size_t smem = dev::SpikeLayout::make(N, R, KB, pent).total;
+  const int PD = static_cast<int>(tune_int("SPD", 4));
+  auto s = static_cast<cudaStream_t>(stream);
+  auto kern = pent ? dev::sweep_spike<true> : dev::sweep_spike<false>;
+  static std::atomic<uint64_t> configured[2];
+  const uint64_t bit = device < 64 ? (1ull << device) : 0;
+  std::atomic<uint64_t>& cfg = configured[pent ? 1 : 0];
+  if (!(bit && (cfg.load(std::memory_order_relaxed) & bit))) {
+    if (cudaError_t e = allow_max_smem(reinterpret_cast<const void*>(kern)); e != cudaSuccess)
+      return fail(BANDSOLVE_ERR_INTERNAL, std::string("spike attributes: ") + cudaGetErrorString(e));
+    if (bit) cfg.fetch_or(bit, std::memory_order_relaxed);
+  }
+  // lanes past the batch edge write their values here (branch-free stores)
+  static double* sinks[64] = {};
+  if (device >= 64) return BANDSOLVE_OK;
+  {
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lock(mu);
+    if (!sinks[device] && cudaMalloc(reinterpret_cast<void**>(&sinks[device]), 32 * sizeof(double)) != cudaSuccess) {
+      cudaGetLastError();
+      sinks[device] = nullptr;
+      return fail(BANDSOLVE_ERR_INTERNAL, "spike scratch");
+    }
+  }
+  kern<<<grid, 32 * (dev::kSpWarps + 1), smem, s>>>(map, x, N, static_cast<long long>(m),
+                                                     static_cast<long long>(ld), K, p->L, KB, PD, groups, blob, rinv,
+                                                     sinks[device]);
+  note_launches(1);
+  if (cudaError_t e = cudaGetLastError(); e != cudaSuccess)
+    return fail(BANDSOLVE_ERR_INTERNAL, std::string("spike launch: ") + cudaGetErrorString(e));
   *done = true;
   return BANDSOLVE_OK;
 }

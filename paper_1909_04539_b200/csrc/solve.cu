@@ -1111,6 +1111,13 @@ void host_free(double* p, bool pinned) {
   else std::free(p);
 }
 
+bool encode_tile_map(CUtensorMap* map, void* x, std::size_t elem, long long n, long long m, long long ld, int box_w,
+                     int box_r) {
+  return encode_map(map, x, elem, n, m, ld, box_w, box_r);
+}
+cudaError_t allow_max_smem(const void* kern) { return allow_big_smem(kern); }
+std::size_t max_smem_per_block() { return kSmemPerBlockMax; }
+
 bandsolve_status describe_plan(Kind kind, std::size_t n, std::size_t m, std::size_t ld, bool f32,
                                std::string& out) {
   alignas(16) static const double kProbe[2] = {0.0, 0.0};  // 16-byte aligned stand-in base
@@ -1122,8 +1129,12 @@ bandsolve_status describe_plan(Kind kind, std::size_t n, std::size_t m, std::siz
   const bool fast = current_mode() == BANDSOLVE_MODE_FAST;
   const Plan p = choose_plan(n, m, ld, f32 ? 4 : 8, kProbe, pent, fast, sms);
   char buf[256];
+  const int KS = f32 ? 0 : spike_blocks(n, m, ld, kProbe, sms, pent);
   const int K = f32 ? 0 : partition_blocks(n, m, sms, pent);
-  if (K > 0)
+  if (KS > 0)
+    std::snprintf(buf, sizeof buf, "spike K=%d blocks of %zu rows, interface system %d, 1 launch (TMEM-resident blocks)",
+                  KS, n / KS, (pent ? 4 : 2) * KS);
+  else if (K > 0)
     std::snprintf(buf, sizeof buf, "partition K=%d blocks of %zu rows, interface system %d (dense LU), 2 launches", K,
                   n / K, (pent ? 4 : 2) * K);
   else if (p.kind == PlanKind::Stream)
@@ -1164,6 +1175,8 @@ bandsolve_status solve_device(const Factor& f, void* x, bool f32, std::size_t n,
   const int sms = num_sms(device);
   if (fast && !f32) {
     bool done = false;
+    st = spike_solve_device(f, static_cast<double*>(x), n, m, ld, stream, sms, &done);
+    if (st != BANDSOLVE_OK || done) return st;
     st = partition_solve_device(f, static_cast<double*>(x), n, m, ld, stream, sms, &done);
     if (st != BANDSOLVE_OK || done) return st;
   }

@@ -1,0 +1,327 @@
+// One-pass partitioned ("spike") shared-LHS sweep for MANY long systems,
+// fast mode, fp64 (sm_100a).
+//
+// Why: a sequential sweep needs every forward intermediate of a system on
+// chip until its backward sweep, and an SM must keep ~100 dependency chains
+// in flight to pull HBM bandwidth. At N = 1024 that is ~800 KB per SM, more
+// than TMEM + shared memory + registers; the spill to L2 caps the
+// sequential plans near 0.5 of the HBM roofline (configs[4]).
+//
+// Because the LHS is shared, the partition method moves the per-system
+// storage to per-BLOCK storage at no extra HBM traffic: each system of
+// n = K L rows is split into K blocks (partition.cu build_plan: block
+// factors, the forward images F of the left coupling columns, rows 0/1 of
+// each block's U^-1, and the inverse of the R x R interface matrix, all per
+// matrix, computed once on the host). One compute warp owns block k of 32
+// systems, so a lane holds only L <= 128 forward values — half of its TMEM
+// lane (warps w and w + 4 share lane quadrant w % 4) — and an SM runs
+// 8 warps x 32 = 256 independent chains, two warps per scheduler:
+//
+//   forward   b streams in through a TMA ring (one {32 x 16} box per warp
+//             and chunk); the lane runs the block-local forward recurrence,
+//             gathers 16 rows and writes them to its TMEM lane with one
+//             tcgen05.st.32x32b.x32, and accumulates the two (one)
+//             interface dot products with the U^-1 rows;
+//   interface each warp publishes its block's interface values of y =
+//             A_k^-1 b_k in shared memory; after a named barrier every lane
+//             forms the x interface unknowns it needs (own bottom rows, the
+//             left neighbour's bottom rows) as rows of R^-1 times the
+//             system's y interface vector;
+//   backward  from its own bottom x values the lane sweeps up over the TMEM
+//             values (one tcgen05.ld per 16 rows, one chunk ahead), folding
+//             the left coupling in as g_i - F_i x_left, and streams x to HBM.
+//
+// Each 16-row chunk is computed in two stages so the dependency chain holds
+// ONE fp64 FMA per row: first everything that does not depend on the
+// recurrence (b * (1/alpha), the left-coupling update), for all 16 rows,
+// then the chain itself (measured: the interleaved single-stage loop ran at
+// ~85 cycles per backward row with one warp per scheduler).
+//
+// HBM traffic: read b once, write x once (16 B/row). Arithmetic differs
+// from the sequential sweep by rounding only (fast mode, 1e-12 contract),
+// exactly as the two-launch partitioned path of partition.cu.
+#pragma once
+
+#include "sweep_stream.cuh"
+
+namespace bsb {
+namespace dev {
+
+constexpr int kSpR = 16;       // rows per chunk: one TMA box {32 systems, 16 rows} per warp
+constexpr int kSpWarps = 8;    // compute warps: two per TMEM lane quadrant, 256 columns each
+constexpr int kSpMaxL = 128;   // rows per block: 1 KB of TMEM lane per fp64 value
+constexpr int kSpMaxK = 8;     // blocks per system
+constexpr int kSpMaxR = 32;    // interface unknowns (pent 4 K)
+
+// per-row records in shared memory, split by phase
+template <bool PENT>
+struct SpF;  // forward: fast records + U^-1 row entries
+template <>
+struct alignas(16) SpF<true> {
+  double e, b, ia, p0, p1, pad;  // e = eps/alpha, b = beta/alpha, ia = 1/alpha (block-local)
+};
+template <>
+struct alignas(16) SpF<false> {
+  double am, m, p0, pad;  // am = a/denom, m = 1/denom
+};
+template <bool PENT>
+struct SpB;  // backward: U entries + forward images of the left coupling
+template <>
+struct alignas(16) SpB<true> {
+  double g, d, f1, f2;  // gamma, delta, F (x_{s-2}), F (x_{s-1})
+};
+template <>
+struct alignas(16) SpB<false> {
+  double c, f1;  // chat, F (x_{s-1})
+};
+
+struct SpikeLayout {
+  size_t fwd_off, bwd_off, rinv_off, xch_off, ring_off, bar_off, total;
+  __host__ __device__ static SpikeLayout make(int n, int R, int KB, bool pent) {
+    SpikeLayout L{};
+    L.fwd_off = 0;
+    L.bwd_off = align128(static_cast<size_t>(n) * (pent ? sizeof(SpF<true>) : sizeof(SpF<false>)));
+    L.rinv_off = L.bwd_off + align128(static_cast<size_t>(n) * (pent ? sizeof(SpB<true>) : sizeof(SpB<false>)));
+    L.xch_off = L.rinv_off + align128(static_cast<size_t>(R) * R * sizeof(double));
+    // interface exchange, double-buffered: [2][warp][q][32 lanes]
+    L.ring_off = L.xch_off + align128(2ull * kSpWarps * (pent ? 4 : 2) * 32 * sizeof(double));
+    L.bar_off = L.ring_off + static_cast<size_t>(KB) * kSpWarps * kSpR * 32 * sizeof(double);
+    L.total = L.bar_off + static_cast<size_t>(2 * KB + 1) * sizeof(uint64_t);
+    return L;
+  }
+};
+
+template <bool PENT>
+__global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
+    sweep_spike(const __grid_constant__ CUtensorMap map_b, double* __restrict__ x, int n, long long m, long long ld,
+                int K, int L, int KB, int PD, long long groups, const void* __restrict__ recs,
+                const double* __restrict__ rinv_g, double* __restrict__ sink) {
+  using F = SpF<PENT>;
+  using B = SpB<PENT>;
+  constexpr int NQ = PENT ? 4 : 2;  // interface rows per block (top NH, bottom NH)
+  constexpr int NH = NQ / 2;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int R = NQ * K;
+  const int G = kSpWarps / K;  // 32-system groups per CTA iteration
+  const int Wg = 32 * G;
+  const SpikeLayout Ly = SpikeLayout::make(n, R, KB, PENT);
+  F* sf = reinterpret_cast<F*>(smem + Ly.fwd_off);
+  B* sb = reinterpret_cast<B*>(smem + Ly.bwd_off);
+  double* srinv = reinterpret_cast<double*>(smem + Ly.rinv_off);
+  double* xch = reinterpret_cast<double*>(smem + Ly.xch_off);
+  double* ring = reinterpret_cast<double*>(smem + Ly.ring_off);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Ly.bar_off);
+  uint64_t* empty = full + KB;
+  uint32_t& tmem_base_s = *reinterpret_cast<uint32_t*>(empty + KB);
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  constexpr int kBox = kSpR * 32;          // elements of one warp's box
+  constexpr int kChunk = kSpWarps * kBox;  // elements of one ring slot
+  const int CL = L / kSpR;                 // chunks per block
+
+  {  // records and R^-1 -> smem (16-byte words)
+    const size_t rec_words = static_cast<size_t>(n) * (sizeof(F) + sizeof(B)) / 16;
+    const uint4* src = static_cast<const uint4*>(recs);
+    uint4* dst = reinterpret_cast<uint4*>(smem + Ly.fwd_off);
+    const size_t fwd_words = static_cast<size_t>(n) * sizeof(F) / 16;
+    for (size_t i = threadIdx.x; i < rec_words; i += blockDim.x) {
+      const size_t o = i < fwd_words ? i : (Ly.bwd_off / 16 + (i - fwd_words));
+      dst[o] = src[i];
+    }
+    for (int i = threadIdx.x; i < R * R; i += blockDim.x) srinv[i] = rinv_g[i];
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < KB; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kSpWarps);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc_512(&tmem_base_s);
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+
+  if (warp == kSpWarps) {  // ---- producer: b chunks through the ring
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      const long long my_groups = (groups - blockIdx.x + gridDim.x - 1) / gridDim.x;
+      const long long total = my_groups * CL;
+      long long pf = 0;
+      auto chunk_at = [&](long long t, int& c0, int& c) {
+        const long long gi = t / CL;
+        c = static_cast<int>(t - gi * CL);
+        c0 = static_cast<int>((blockIdx.x + gi * gridDim.x) * Wg);
+      };
+      int slot = 0;
+      uint32_t phase = 0;
+      for (long long t = 0; t < total; ++t) {
+        for (; pf < total && pf < t + PD; ++pf) {  // keep PD chunks ahead in L2
+          int c0, c;
+          chunk_at(pf, c0, c);
+          for (int w = 0; w < kSpWarps; ++w) tma_prefetch_2d(&map_b, c0 + (w / K) * 32, (w % K) * L + c * kSpR);
+        }
+        if (t >= KB) mbar_wait(&empty[slot], phase ^ 1u);
+        int c0, c;
+        chunk_at(t, c0, c);
+        mbar_expect_tx(&full[slot], kChunk * sizeof(double));
+        for (int w = 0; w < kSpWarps; ++w)
+          tma_load_2d(ring + slot * kChunk + w * kBox, &map_b, c0 + (w / K) * 32, (w % K) * L + c * kSpR, &full[slot],
+                      pol);
+        if (++slot == KB) {
+          slot = 0;
+          phase ^= 1u;
+        }
+      }
+    }
+    return;
+  }
+
+  // ---- compute warps: block k of the 32 systems of group slot gs
+  const int k = warp % K;
+  const int gs = warp / K;
+  const int r0 = k * L;
+  const uint32_t tlane = tmem_base_s + (static_cast<uint32_t>(32 * (warp & 3)) << 16) +
+                         static_cast<uint32_t>((warp >> 2) * 256);
+  int slot = 0;
+  uint32_t phase = 0;
+  uint32_t par = 0;
+  const F* fk = sf + r0;
+  const B* bk = sb + r0;
+  for (long long g = blockIdx.x; g < groups; g += gridDim.x, par ^= 1u) {
+    // -- forward over the block, values to TMEM, interface dot products
+    double s1 = 0.0, s2 = 0.0, a0 = 0.0, a1 = 0.0;
+    for (int c = 0; c < CL; ++c) {
+      mbar_wait(&full[slot], phase);
+      const double* blk = ring + slot * kChunk + warp * kBox + lane;
+      const F* fc = fk + c * kSpR;
+      TPiece<double> buf;
+      double dv[kSpR];  // stage 1: b / pivot for the whole chunk (off the chain)
+#pragma unroll
+      for (int r = 0; r < kSpR; ++r) {
+        if constexpr (PENT) dv[r] = blk[r * 32] * fc[r].ia;
+        else dv[r] = blk[r * 32] * fc[r].m;
+      }
+#pragma unroll
+      for (int r = 0; r < kSpR; ++r) {  // stage 2: one FMA per row on the chain
+        const F f = fc[r];
+        double v;
+        if constexpr (PENT) {
+          v = fma(-f.b, s1, fma(-f.e, s2, dv[r]));
+          a1 = fma(f.p1, v, a1);
+        } else {
+          v = fma(-f.am, s1, dv[r]);
+        }
+        a0 = fma(f.p0, v, a0);
+        s2 = s1;
+        s1 = v;
+        buf.put(r, v);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+      if (++slot == KB) {
+        slot = 0;
+        phase ^= 1u;
+      }
+      buf.store(tlane + static_cast<uint32_t>(c * TPiece<double>::kWords));
+    }
+    // -- interface values of y for this block: top (dot products), bottom
+    double* xw = xch + (static_cast<size_t>(par) * kSpWarps + warp) * NQ * 32 + lane;
+    xw[0] = a0;
+    if constexpr (PENT) {
+      xw[32] = a1;
+      xw[64] = fma(-bk[L - 2].g, s1, s2);  // y_{L-2} = g_{L-2} - gamma_{L-2} g_{L-1}
+      xw[96] = s1;                          // y_{L-1} = g_{L-1}
+    } else {
+      xw[32] = s1;
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(kSpWarps * 32) : "memory");
+    // -- this system's interface unknowns: own bottom rows, left neighbour's
+    double y[kSpMaxR];
+#pragma unroll
+    for (int c = 0; c < kSpMaxR; ++c) {
+      if (c < R) {
+        const int kk = c / NQ, q = c - kk * NQ;
+        y[c] = xch[((static_cast<size_t>(par) * kSpWarps + gs * K + kk) * NQ + q) * 32 + lane];
+      } else {
+        y[c] = 0.0;
+      }
+    }
+    double zu[2 * NH];
+#pragma unroll
+    for (int h = 0; h < 2 * NH; ++h) {
+      const int row = h < NH ? NQ * k + NH + h : NQ * k - NH + (h - NH);
+      double acc = 0.0;
+      if (h < NH || k > 0) {
+#pragma unroll
+        for (int c = 0; c < kSpMaxR; ++c)
+          if (c < R) acc = fma(srinv[row * R + c], y[c], acc);
+      }
+      zu[h] = acc;
+    }
+    // -- backward from the own bottom unknowns, left coupling folded in, x
+    // streamed to HBM (lanes past m write a scratch word instead: no branch)
+    double xl1, xl2 = 0.0;
+    if constexpr (PENT) {
+      s1 = zu[0];   // x_{L-2}
+      s2 = zu[1];   // x_{L-1}
+      xl2 = zu[2];  // x_{s-2}
+      xl1 = zu[3];  // x_{s-1}
+    } else {
+      s1 = zu[0];   // x_{L-1}
+      xl1 = zu[1];  // x_{s-1}
+    }
+    const long long j = g * Wg + gs * 32 + lane;
+    const bool live = j < m;
+    const long long step = live ? ld : 0;
+    double* out = live ? x + static_cast<long long>(r0 + L - 1) * ld + j : sink + lane;
+    if constexpr (PENT) {
+      __stcs(out - step, s1);
+      __stcs(out, s2);
+    } else {
+      __stcs(out, s1);
+    }
+    out -= NH * step;
+    TPiece<double> cur, nxt;
+    cur.load(tlane + static_cast<uint32_t>((CL - 1) * TPiece<double>::kWords));
+    cur.wait();
+    auto chunk_bwd = [&](int c, auto first) {
+      constexpr int kTop = decltype(first)::value ? kSpR - 1 - NH : kSpR - 1;  // skip the interface rows
+      const B* bc = bk + c * kSpR;
+      double gv[kSpR];  // stage 1: left-coupling update (off the chain)
+#pragma unroll
+      for (int r = 0; r <= kTop; ++r) {
+        if constexpr (PENT) gv[r] = fma(-bc[r].f1, xl2, fma(-bc[r].f2, xl1, cur.get(r)));
+        else gv[r] = fma(-bc[r].f1, xl1, cur.get(r));
+      }
+#pragma unroll
+      for (int r = kTop; r >= 0; --r) {  // stage 2: one FMA per row on the chain
+        double v;
+        if constexpr (PENT) v = fma(-bc[r].g, s1, fma(-bc[r].d, s2, gv[r]));
+        else v = fma(-bc[r].c, s1, gv[r]);
+        s2 = s1;
+        s1 = v;
+        __stcs(out, v);
+        out -= step;
+      }
+    };
+    for (int c = CL - 1; c >= 0; --c) {
+      if (c > 0) nxt.load(tlane + static_cast<uint32_t>((c - 1) * TPiece<double>::kWords));
+      if (c == CL - 1) chunk_bwd(c, std::true_type{});
+      else chunk_bwd(c, std::false_type{});
+      if (c > 0) {
+        nxt.wait();
+        cur = nxt;
+      }
+    }
+  }
+  tmem_fence_before();
+  asm volatile("bar.sync 1, %0;" ::"r"(kSpWarps * 32) : "memory");
+  if (warp == 0) {
+    tmem_fence_after();
+    tmem_dealloc_512(tmem_base_s);
+  }
+}
+
+}  // namespace dev
+}  // namespace bsb

@@ -1,0 +1,139 @@
+"""One-pass partitioned sweep for many long systems (csrc/sweep_spike.cuh).
+
+Fast mode promises the reference's answer within a per-system max-norm
+relative error of 1e-12; the one-pass kernel reorders the
+arithmetic exactly like the two-launch partitioned path (block sweeps, a
+dense interface solve, the left-coupling update), so it is held to the same
+bound against the oracle: K = 4 and 8 blocks, ragged batch widths (TMA
+zero-fill + masked stores), padded pitches, every band structure, and a
+column sample at configs[4] scale (pent N = 1024). The tuning key SPIKE=1
+forces the kernel below its many-systems threshold; =0 disables it.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle.oracle import per_system_max_rel
+from paper_1909_04539_b200 import bandsolve as bs
+
+pytestmark = pytest.mark.gpu
+
+TOL_F64 = 1e-12
+
+
+def _random_tri(rng, n):
+    sub = rng.uniform(-1, 1, n); sub[0] = 0
+    sup = rng.uniform(-1, 1, n); sup[-1] = 0
+    diag = np.abs(sub) + np.abs(sup) + rng.uniform(0.5, 1.5, n)
+    return sub, diag, sup
+
+
+def _random_pent(rng, n):
+    a = rng.uniform(-1, 1, n); a[:2] = 0
+    b = rng.uniform(-1, 1, n); b[0] = 0
+    d = rng.uniform(-1, 1, n); d[-1] = 0
+    e = rng.uniform(-1, 1, n); e[-2:] = 0
+    c = np.abs(a) + np.abs(b) + np.abs(d) + np.abs(e) + rng.uniform(0.5, 1.5, n)
+    return a, b, c, d, e
+
+
+@pytest.fixture(autouse=True)
+def _fast_mode(lib):
+    lib.set_mode(bs.MODE_FAST)
+    yield
+    lib.set_mode(bs.MODE_EXACT)
+
+
+def _dev_solve(lib, torch, factor, rhs, ld=None):
+    n, m = rhs.shape
+    ld = m if ld is None else ld
+    buf = torch.full((n, ld), float("nan"), dtype=torch.float64, device="cuda")
+    buf[:, :m] = torch.from_numpy(rhs).cuda()
+    before = lib.kernel_launches()
+    factor.solve_dev(buf.data_ptr(), n, m, ld=ld, stream=torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    launches = lib.kernel_launches() - before
+    out = buf.cpu().numpy()
+    if ld > m:
+        assert np.all(np.isnan(out[:, m:]))
+    return out[:, :m], launches
+
+
+@pytest.mark.parametrize("n", [320, 512, 768, 1024])
+def test_spike_within_tolerance(lib, oracle, cuda_device, n):
+    torch = cuda_device
+    lib.tune("SPIKE", "1")
+    rng = np.random.default_rng(n)
+    K = {320: 4, 512: 4, 768: 8, 1024: 8}[n]
+    for m, ld in [(38, 40), (64, 64), (300, 302)]:
+        rhs = rng.uniform(-1, 1, (n, m))
+        cases = [("tri", bs.TriFactor, _random_tri(rng, n)), ("diff", bs.TriFactor, bs.diffusion_bands(1.0, n)),
+                 ("pent", bs.PentFactor, _random_pent(rng, n)), ("hyper", bs.PentFactor, bs.hyper_bands(1.0, n))]
+        for name, cls, bands in cases:
+            pent = cls is bs.PentFactor
+            assert lib.describe_plan(1 if pent else 0, n, m, ld).startswith(f"spike K={K}")
+            want = (oracle.pent_solve(oracle.pent_prefactor(*bands), rhs.copy()) if pent
+                    else oracle.tri_solve(oracle.tri_prefactor(*bands), rhs.copy()))
+            got, launches = _dev_solve(lib, torch, cls(lib, *bands), rhs, ld)
+            assert launches == 1, (name, n, m)
+            assert per_system_max_rel(got, want) <= TOL_F64, (name, n, m, ld)
+
+
+def test_spike_planner_threshold(lib, cuda_device):
+    """Without the override the kernel is taken for many systems only, in
+    fast mode only, and never for odd pitches (TMA 16-byte rule)."""
+    sms = cuda_device.cuda.get_device_properties(0).multi_processor_count
+    assert lib.describe_plan(1, 1024, 1 << 20).startswith("spike K=8")
+    assert lib.describe_plan(0, 512, 1 << 20).startswith("spike K=4")
+    assert not lib.describe_plan(1, 1024, sms * 32 - 2).startswith("spike")
+    assert not lib.describe_plan(1, 1024, (1 << 20) - 1, 1 << 20).startswith("spike")  # odd batch width
+    assert not lib.describe_plan(1, 1024, 1 << 20, (1 << 20) + 1).startswith("spike")
+    assert not lib.describe_plan(1, 1000, 1 << 20).startswith("spike")  # 1000 / 4 is not a chunk multiple
+    lib.tune("SPIKE", "0")
+    assert not lib.describe_plan(1, 1024, 1 << 20).startswith("spike")
+    lib.tune("SPIKE", None)
+    lib.set_mode(bs.MODE_EXACT)
+    assert not lib.describe_plan(1, 1024, 1 << 20).startswith("spike")
+
+
+def test_spike_breakdown_falls_back(lib, oracle, cuda_device):
+    """A block whose unpivoted elimination grows (tiny diagonal at a block
+    start) is rejected by the plan; the sequential sweep answers instead."""
+    torch = cuda_device
+    lib.tune("SPIKE", "1")
+    n, m = 512, 64
+    rng = np.random.default_rng(5)
+    sub, diag, sup = _random_tri(rng, n)
+    sub[256], sup[255] = 1.0, 1.0
+    diag[256] = 1e-14  # block 1 starts here: a near-zero pivot for the block factor
+    diag[255] = 4.0
+    rhs = rng.uniform(-1, 1, (n, m))
+    want = oracle.tri_solve(oracle.tri_prefactor(sub, diag, sup), rhs.copy())
+    got, _ = _dev_solve(lib, torch, bs.TriFactor(lib, sub, diag, sup), rhs)
+    assert per_system_max_rel(got, want) <= TOL_F64
+
+
+def test_spike_configs4_column_sample(lib, oracle, cuda_device):
+    """configs[4] shape (pent N = 1024, hyperdiffusion sigma_x = 1) through the
+    planner's own choice at 2^20 systems: residual over the whole batch and
+    a column sample against the oracle, both within the fast-mode bound."""
+    torch = cuda_device
+    n, m = 1024, 1 << 20
+    assert lib.describe_plan(1, n, m).startswith("spike K=8")
+    bands = bs.hyper_bands(1.0, n)
+    stream = torch.cuda.current_stream().cuda_stream
+    x = torch.empty((n, m), dtype=torch.float64, device="cuda")
+    lib.fill_rhs_dev(x.data_ptr(), n, m, m, 42, 0, stream)
+    rhs = x.clone()
+    fac = bs.PentFactor(lib, *bands)
+    fac.solve_dev(x.data_ptr(), n, m, ld=m, stream=stream)
+    res = lib.pent_residual_dev(*bands, x.data_ptr(), rhs.data_ptr(), m, m, stream=stream)
+    assert res <= 1e-12
+    cols = np.random.default_rng(3).choice(m, 512, replace=False)
+    cols.sort()
+    idx = torch.from_numpy(cols).cuda()
+    got = x.index_select(1, idx).cpu().numpy()
+    b = rhs.index_select(1, idx).cpu().numpy()
+    want = oracle.pent_solve(oracle.pent_prefactor(*bands), b.copy())
+    assert per_system_max_rel(got, want) <= TOL_F64
