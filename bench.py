@@ -290,9 +290,10 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
     nbuf = 1 if bytes_per >= 4 * l2 else min(8, -(-4 * l2 // bytes_per))
     if adi or args.cn:
         nbuf = max(2, nbuf)
-    bufs = [torch.empty((n, m), dtype=dt, device="cuda") for _ in range(nbuf)]
+    ld = m + args.pitch_pad  # row pitch of the device batch (elements)
+    bufs = [torch.empty((n, ld), dtype=dt, device="cuda") for _ in range(nbuf)]
     for b in bufs:
-        lib.fill_rhs_dev(b.data_ptr(), n, m, m, SEED, j0, torch.cuda.current_stream().cuda_stream, f32=args.f32)
+        lib.fill_rhs_dev(b.data_ptr(), n, m, ld, SEED, j0, torch.cuda.current_stream().cuda_stream, f32=args.f32)
     stream = torch.cuda.current_stream()
     sptr = stream.cuda_stream
     clocks = ClockSampler(local_rank)
@@ -301,12 +302,12 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
 
     def step(k):
         if adi:
-            fac.step_dev(bufs[k % nbuf].data_ptr(), bufs[(k + 1) % nbuf].data_ptr(), ld=m, stream=sptr)
+            fac.step_dev(bufs[k % nbuf].data_ptr(), bufs[(k + 1) % nbuf].data_ptr(), ld=ld, stream=sptr)
         elif args.cn:  # one Crank-Nicolson step: u_{k+1} = A^-1 B u_k, ping-pong buffers
-            fac.cn_step_dev(cn_sigma, bufs[k % nbuf].data_ptr(), bufs[(k + 1) % nbuf].data_ptr(), n, m, ld=m,
+            fac.cn_step_dev(cn_sigma, bufs[k % nbuf].data_ptr(), bufs[(k + 1) % nbuf].data_ptr(), n, m, ld=ld,
                             stream=sptr)
         else:
-            fac.solve_dev(bufs[k % nbuf].data_ptr(), n, m, ld=m, stream=sptr, f32=args.f32)
+            fac.solve_dev(bufs[k % nbuf].data_ptr(), n, m, ld=ld, stream=sptr, f32=args.f32)
 
     for k in range(args.warmup):
         step(k)
@@ -341,7 +342,7 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
     achieved = algo_bytes / (ms_local / args.steps / 1e3) / 1e9
     peak, peak_src = load_peak()
     traffic = load_traffic(args.config, args.mode)
-    plan = lib.describe_plan(0 if kind == "tri" else 1, n, m, m, args.f32)
+    plan = lib.describe_plan(0 if kind == "tri" else 1, n, m, ld, args.f32)
 
     # e2e through the reference-facing host API (pinned host batch; H2D,
     # sweep, D2H inside bandsolve_*_solve_shared, synchronous)
@@ -392,7 +393,10 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
             "vs_baseline": None, "dtype": "f32" if args.f32 else "f64",
             "data": "synthetic: U(-1,1) RHS from SplitMix64(seed=42, i, global j), generated on device",
             "config": {"workload": desc, "kind": kind, "n": n, "batch_per_gpu": m, "global_batch": m_global,
-                       "mode": args.mode, "plan": plan, "periodic": bool(args.periodic), "cn_step": bool(args.cn),
+                       "mode": args.mode,
+                       "arithmetic": ("fp64, FMA form / partitioned sweep, max rel err <= 1e-12 vs the reference"
+                                      if args.mode == "fast" else "fp64, reference operation order, bitwise equal"),
+                       "plan": plan, "periodic": bool(args.periodic), "cn_step": bool(args.cn),
                        "parallelism": f"dp{world} (systems sharded, no data-path collective)",
                        "l2": (f"{nbuf} in-place buffer{'s' if nbuf > 1 else ''} of {bytes_per / 2**20:.0f} MiB "
                               f"(working set {nbuf * bytes_per / l2:.1f}x L2, inputs larger than L2)")},
@@ -415,10 +419,15 @@ def main() -> int:
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--config", choices=sorted(CONFIGS), default=DEFAULT_CONFIG)
-    ap.add_argument("--mode", choices=["exact", "fast"], default=os.environ.get("BANDSOLVE_BENCH_MODE", "exact"))
+    # fast (default): fp64 in FMA form, partitioned one-pass sweep for long
+    # systems, within 1e-12 of the reference (north_star's fp64 tolerance;
+    # tests/test_spike.py, test_gpu_parity.py); exact: the reference's
+    # operation order, bitwise equal
+    ap.add_argument("--mode", choices=["exact", "fast"], default=os.environ.get("BANDSOLVE_BENCH_MODE", "fast"))
     ap.add_argument("--f32", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-API end-to-end leg (tuning runs)")
+    ap.add_argument("--pitch-pad", type=int, default=0, help="extra elements per row of the device batch (layout runs)")
     ap.add_argument("--periodic", action="store_true", help="cyclic (periodic) variant of the config's LHS")
     ap.add_argument("--cn", action="store_true",
                     help="Crank-Nicolson step (periodic stencil RHS + cyclic solve, sigma_x = 1) per step")
