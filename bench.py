@@ -245,7 +245,7 @@ def kernel_name(plan: str, f32: bool, kind: str, mode: str) -> str:
     k = plan.split()[0] if plan else "?"
     name = {"stream": "sweep_stream", "regs": "sweep_regs", "persist": "sweep_persist",
             "smem-tma": "sweep_smem", "global-inplace": "sweep_global",
-            "partition": "part_fwd_kernel+part_bwd_kernel"}.get(k, k)
+            "partition": "part_fwd_kernel+part_bwd_kernel", "spike": "sweep_spike"}.get(k, k)
     return f"{name}<{'float' if f32 else 'double'},{kind},{mode}>"
 
 

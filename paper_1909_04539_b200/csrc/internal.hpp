@@ -160,8 +160,9 @@ int partition_blocks(std::size_t n, std::size_t m, int sms, bool pent);  // 0 = 
 // One-pass partitioned sweep for many long systems (sweep_spike.cuh), fast
 // mode fp64: blocks per system, 0 when it does not apply.
 int spike_blocks(std::size_t n, std::size_t m, std::size_t ld, const void* x, int sms, bool pent);
+struct PartPeriodic;
 bandsolve_status spike_solve_device(const Factor& f, double* x, std::size_t n, std::size_t m, std::size_t ld,
-                                    void* stream, int sms, bool* done);
+                                    void* stream, int sms, bool* done, const PartPeriodic* per = nullptr);
 bool partition_stencil_ok(std::size_t n, std::size_t m, int K, std::size_t lds);
 bandsolve_status partition_solve_device(const Factor& f, double* x, std::size_t n,
                                         std::size_t m, std::size_t ld,

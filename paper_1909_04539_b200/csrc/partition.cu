@@ -753,10 +753,10 @@ PartPlan* cached_plan(const Factor& f, int K) {
   return p->ok ? p : nullptr;
 }
 
-int spike_ring_slots(int n, int R, bool pent) {
+int spike_ring_slots(int n, int R, bool pent, bool per) {
   const std::size_t cap = max_smem_per_block();
   for (int kb = 6; kb >= 2; --kb)
-    if (dev::SpikeLayout::make(n, R, kb, pent).total <= cap) return kb;
+    if (dev::SpikeLayout::make(n, R, kb, pent, per).total <= cap) return kb;
   return 0;
 }
 
@@ -780,12 +780,12 @@ int spike_blocks(std::size_t n, std::size_t m, std::size_t ld, const void* x, in
   // many systems: at least one full wave of 32 (dev::kSpWarps / K)-system groups
   const std::size_t wg = 32u * (dev::kSpWarps / K);
   if (sel != 1 && m < static_cast<std::size_t>(sms) * wg) return 0;
-  if (spike_ring_slots(static_cast<int>(n), (pent ? 4 : 2) * K, pent) == 0) return 0;
+  if (spike_ring_slots(static_cast<int>(n), (pent ? 4 : 2) * K, pent, true) == 0) return 0;
   return K;
 }
 
 bandsolve_status spike_solve_device(const Factor& f, double* x, std::size_t n, std::size_t m, std::size_t ld,
-                                    void* stream, int sms, bool* done) {
+                                    void* stream, int sms, bool* done, const PartPeriodic* per) {
   *done = false;
   const bool pent = f.kind != Kind::Tri;
   const int K = spike_blocks(n, m, ld, x, sms, pent);
@@ -822,7 +822,7 @@ bandsolve_status spike_solve_device(const Factor& f, double* x, std::size_t n, s
   }
   const int N = static_cast<int>(n);
   const int R = p->R;
-  const int KB = spike_ring_slots(N, R, pent);
+  const int KB = spike_ring_slots(N, R, pent, per != nullptr);
   const std::size_t rec_doubles = static_cast<std::size_t>(n) * (pent ? 10 : 6);
   const double* rinv = static_cast<const double*>(blob) + rec_doubles;
   CUtensorMap map;
@@ -832,13 +832,20 @@ bandsolve_status spike_solve_device(const Factor& f, double* x, std::size_t n, s
   const int Wg = 32 * (dev::kSpWarps / K);
   const long long groups = (static_cast<long long>(m) + Wg - 1) / Wg;
   const unsigned grid = static_cast<unsigned>(std::min<long long>(sms, groups));
-  const std::size_t smem = dev::SpikeLayout::make(N, R, KB, pent).total;
+  const std::size_t smem = dev::SpikeLayout::make(N, R, KB, pent, per != nullptr).total;
   const int PD = static_cast<int>(tune_int("SPD", 4));
   auto s = static_cast<cudaStream_t>(stream);
-  auto kern = pent ? dev::sweep_spike<true> : dev::sweep_spike<false>;
-  static std::atomic<uint64_t> configured[2];
+  auto kern = pent ? (per ? dev::sweep_spike<true, true> : dev::sweep_spike<true, false>)
+                   : (per ? dev::sweep_spike<false, true> : dev::sweep_spike<false, false>);
+  static std::atomic<uint64_t> configured[4];
   const uint64_t bit = device < 64 ? (1ull << device) : 0;
-  std::atomic<uint64_t>& cfg = configured[pent ? 1 : 0];
+  std::atomic<uint64_t>& cfg = configured[(pent ? 2 : 0) + (per ? 1 : 0)];
+  dev::SpikePer sp;
+  if (per) {
+    sp.z1 = per->z1;
+    sp.z2 = per->z2;
+    for (int q = 0; q < 4; ++q) sp.c[q] = per->c[q];
+  }
   if (!(bit && (cfg.load(std::memory_order_relaxed) & bit))) {
     if (cudaError_t e = allow_max_smem(reinterpret_cast<const void*>(kern)); e != cudaSuccess)
       return fail(BANDSOLVE_ERR_INTERNAL, std::string("spike attributes: ") + cudaGetErrorString(e));
@@ -858,7 +865,7 @@ bandsolve_status spike_solve_device(const Factor& f, double* x, std::size_t n, s
   }
   kern<<<grid, 32 * (dev::kSpWarps + 1), smem, s>>>(map, x, N, static_cast<long long>(m),
                                                      static_cast<long long>(ld), K, p->L, KB, PD, groups, blob, rinv,
-                                                     sinks[device]);
+                                                     sinks[device], sp);
   note_launches(1);
   if (cudaError_t e = cudaGetLastError(); e != cudaSuccess)
     return fail(BANDSOLVE_ERR_INTERNAL, std::string("spike launch: ") + cudaGetErrorString(e));

@@ -1357,8 +1357,9 @@ bandsolve_status periodic_device(const Periodic& p, double* x, std::size_t n, st
   const bool pent = p.kind != Kind::Tri;
   const bool fuse = !correct_only && current_mode() == BANDSOLVE_MODE_FAST &&
                     !tune_flag("PERIODIC_UNFUSED");
-  if (fuse && partition_blocks(n, m, sms, pent) > 0) {
-    // few long systems: partitioned sweep with the correction fused into its last pass
+  if (fuse && (spike_blocks(n, m, ld, x, sms, pent) > 0 || partition_blocks(n, m, sms, pent) > 0)) {
+    // many long systems: the one-pass partitioned sweep; few long systems:
+    // the two-launch partitioned sweep; the correction fused into both
     const double* blob = nullptr;
     bandsolve_status st = periodic_device_z(p, device, &blob);
     if (st != BANDSOLVE_OK) return st;
@@ -1370,6 +1371,8 @@ bandsolve_status periodic_device(const Periodic& p, double* x, std::size_t n, st
       pa.c[1] = p.scale;
     }
     bool done = false;
+    st = spike_solve_device(*p.factor, x, n, m, ld, stream, sms, &done, &pa);
+    if (st != BANDSOLVE_OK || done) return st;
     st = partition_solve_device(*p.factor, x, n, m, ld, stream, sms, &done, &pa);
     if (st != BANDSOLVE_OK || done) return st;
   }

@@ -75,13 +75,24 @@ struct alignas(16) SpB<false> {
   double c, f1;  // chat, F (x_{s-1})
 };
 
+// periodic (Woodbury) correction fused into the backward sweep: x_i -=
+// z1_i t1 + z2_i t2, the coefficients from x_0, x_1, x_{n-2}, x_{n-1}, which
+// are interface unknowns (periodic.cpp:57-89, :172-208; fast-mode rounding)
+struct SpikePer {
+  const double* z1 = nullptr;
+  const double* z2 = nullptr;
+  double c[4] = {0.0, 0.0, 0.0, 0.0};  // tri: v_last, scale; pent: cap_inv
+};
+
 struct SpikeLayout {
-  size_t fwd_off, bwd_off, rinv_off, xch_off, ring_off, bar_off, total;
-  __host__ __device__ static SpikeLayout make(int n, int R, int KB, bool pent) {
+  size_t fwd_off, bwd_off, z_off, rinv_off, xch_off, ring_off, bar_off, total;
+  __host__ __device__ static SpikeLayout make(int n, int R, int KB, bool pent, bool per = false) {
     SpikeLayout L{};
     L.fwd_off = 0;
     L.bwd_off = align128(static_cast<size_t>(n) * (pent ? sizeof(SpF<true>) : sizeof(SpF<false>)));
-    L.rinv_off = L.bwd_off + align128(static_cast<size_t>(n) * (pent ? sizeof(SpB<true>) : sizeof(SpB<false>)));
+    L.z_off = L.bwd_off + align128(static_cast<size_t>(n) * (pent ? sizeof(SpB<true>) : sizeof(SpB<false>)));
+    // z of the periodic correction: [n] pairs (pent) / values (tri)
+    L.rinv_off = L.z_off + (per ? align128(static_cast<size_t>(n) * (pent ? 2 : 1) * sizeof(double)) : 0);
     L.xch_off = L.rinv_off + align128(static_cast<size_t>(R) * R * sizeof(double));
     // interface exchange, double-buffered: [2][warp][q][32 lanes]
     L.ring_off = L.xch_off + align128(2ull * kSpWarps * (pent ? 4 : 2) * 32 * sizeof(double));
@@ -91,11 +102,11 @@ struct SpikeLayout {
   }
 };
 
-template <bool PENT>
+template <bool PENT, bool PER>
 __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
     sweep_spike(const __grid_constant__ CUtensorMap map_b, double* __restrict__ x, int n, long long m, long long ld,
                 int K, int L, int KB, int PD, long long groups, const void* __restrict__ recs,
-                const double* __restrict__ rinv_g, double* __restrict__ sink) {
+                const double* __restrict__ rinv_g, double* __restrict__ sink, SpikePer per) {
   using F = SpF<PENT>;
   using B = SpB<PENT>;
   constexpr int NQ = PENT ? 4 : 2;  // interface rows per block (top NH, bottom NH)
@@ -104,7 +115,7 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
   const int R = NQ * K;
   const int G = kSpWarps / K;  // 32-system groups per CTA iteration
   const int Wg = 32 * G;
-  const SpikeLayout Ly = SpikeLayout::make(n, R, KB, PENT);
+  const SpikeLayout Ly = SpikeLayout::make(n, R, KB, PENT, PER);
   F* sf = reinterpret_cast<F*>(smem + Ly.fwd_off);
   B* sb = reinterpret_cast<B*>(smem + Ly.bwd_off);
   double* srinv = reinterpret_cast<double*>(smem + Ly.rinv_off);
@@ -129,6 +140,17 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
       dst[o] = src[i];
     }
     for (int i = threadIdx.x; i < R * R; i += blockDim.x) srinv[i] = rinv_g[i];
+    if constexpr (PER) {
+      double* z = reinterpret_cast<double*>(smem + Ly.z_off);
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        if constexpr (PENT) {
+          z[2 * i] = per.z1[i];
+          z[2 * i + 1] = per.z2[i];
+        } else {
+          z[i] = per.z1[i];
+        }
+      }
+    }
   }
   if (threadIdx.x == 0) {
     for (int s = 0; s < KB; ++s) {
@@ -247,12 +269,17 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
         y[c] = 0.0;
       }
     }
-    double zu[2 * NH];
+    // [own bottom NH | left bottom NH | (PER) first NH | last NH of the system]
+    constexpr int NU = PER ? 4 * NH : 2 * NH;
+    double zu[NU];
 #pragma unroll
-    for (int h = 0; h < 2 * NH; ++h) {
-      const int row = h < NH ? NQ * k + NH + h : NQ * k - NH + (h - NH);
+    for (int h = 0; h < NU; ++h) {
+      const int row = h < NH ? NQ * k + NH + h
+                      : h < 2 * NH ? NQ * k - NH + (h - NH)
+                      : h < 3 * NH ? h - 2 * NH
+                                   : R - NH + (h - 3 * NH);
       double acc = 0.0;
-      if (h < NH || k > 0) {
+      if (h < NH || h >= 2 * NH || k > 0) {
 #pragma unroll
         for (int c = 0; c < kSpMaxR; ++c)
           if (c < R) acc = fma(srinv[row * R + c], y[c], acc);
@@ -271,15 +298,31 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
       s1 = zu[0];   // x_{L-1}
       xl1 = zu[1];  // x_{s-1}
     }
+    double t1 = 0.0, t2 = 0.0;  // periodic correction coefficients
+    if constexpr (PER) {
+      if constexpr (PENT) {  // periodic.cpp:189-194 (fast-mode rounding)
+        const double w1 = zu[4] - zu[7], w2 = zu[5] - zu[6];
+        t1 = fma(per.c[0], w1, per.c[1] * w2);
+        t2 = fma(per.c[2], w1, per.c[3] * w2);
+      } else {  // periodic.cpp:80
+        t1 = fma(per.c[0], zu[3], zu[2]) * per.c[1];
+      }
+    }
+    const double* zk = reinterpret_cast<const double*>(smem + Ly.z_off) + (PENT ? 2 : 1) * r0;
+    auto corr = [&](int i, double v) {  // stored value of local row i
+      if constexpr (!PER) return v;
+      else if constexpr (PENT) return fma(-zk[2 * i], t1, fma(-zk[2 * i + 1], t2, v));
+      else return fma(-zk[i], t1, v);
+    };
     const long long j = g * Wg + gs * 32 + lane;
     const bool live = j < m;
     const long long step = live ? ld : 0;
     double* out = live ? x + static_cast<long long>(r0 + L - 1) * ld + j : sink + lane;
     if constexpr (PENT) {
-      __stcs(out - step, s1);
-      __stcs(out, s2);
+      __stcs(out - step, corr(L - 2, s1));
+      __stcs(out, corr(L - 1, s2));
     } else {
-      __stcs(out, s1);
+      __stcs(out, corr(L - 1, s1));
     }
     out -= NH * step;
     TPiece<double> cur, nxt;
@@ -301,7 +344,7 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
         else v = fma(-bc[r].c, s1, gv[r]);
         s2 = s1;
         s1 = v;
-        __stcs(out, v);
+        __stcs(out, corr(c * kSpR + r, v));
         out -= step;
       }
     };

@@ -137,3 +137,32 @@ def test_spike_configs4_column_sample(lib, oracle, cuda_device):
     b = rhs.index_select(1, idx).cpu().numpy()
     want = oracle.pent_solve(oracle.pent_prefactor(*bands), b.copy())
     assert per_system_max_rel(got, want) <= TOL_F64
+
+
+@pytest.mark.parametrize("n", [320, 512, 1024])
+def test_spike_periodic_fused_within_tolerance(lib, oracle, cuda_device, n):
+    """Cyclic systems: the Woodbury correction rides in the spike kernel's
+    backward sweep (its coefficients need x_0, x_1, x_{n-2}, x_{n-1}, which
+    are interface unknowns) — one launch, within 1e-12 of the reference's
+    periodic solve (periodic.cpp:57-95, :172-214)."""
+    torch = cuda_device
+    lib.tune("SPIKE", "1")
+    rng = np.random.default_rng(n + 1)
+    for m, ld in [(64, 64), (300, 302)]:
+        x = rng.uniform(-1, 1, (n, m))
+        for bands in [(-1.0, 3.0, -1.0), (-0.3, 1.9, -0.5), (1.0, -4.0, 7.0, -4.0, 1.0),
+                      (0.2, -0.8, 3.1, -0.7, 0.1)]:
+            p = bs.PeriodicTri(lib, *bands, n) if len(bands) == 3 else bs.PeriodicPent(lib, *bands, n)
+            buf = torch.full((n, ld), float("nan"), dtype=torch.float64, device="cuda")
+            buf[:, :m] = torch.from_numpy(x).cuda()
+            before = lib.kernel_launches()
+            p.solve_dev(buf.data_ptr(), n, m, ld=ld, stream=torch.cuda.current_stream().cuda_stream)
+            torch.cuda.synchronize()
+            assert lib.kernel_launches() - before == 1, (n, m, bands)
+            out = buf.cpu().numpy()
+            assert np.all(np.isnan(out[:, m:]))
+            if len(bands) == 3:
+                want = oracle.periodic_tri_solve(oracle.periodic_tri_prepare(*bands, n), x.copy())
+            else:
+                want = oracle.periodic_pent_solve(oracle.periodic_pent_prepare(*bands, n), x.copy())
+            assert per_system_max_rel(out[:, :m], want) <= TOL_F64, (n, m, ld, bands)
