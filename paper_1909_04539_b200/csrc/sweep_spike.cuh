@@ -199,72 +199,96 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
     return;
   }
 
-  // ---- compute warps: block k of the 32 systems of group slot gs
+  // ---- compute warps: block k of the 32 systems of group slot gs.
+  // Software-pipelined across groups: after the interface solve of group g
+  // the warp interleaves, chunk by chunk, the backward sweep of g with the
+  // forward sweep of g + 1 (two independent dependency chains per warp, and
+  // b is read while x is written, so the SM's HBM traffic never comes in
+  // read-only / write-only bursts). The backward of g frees TMEM chunk
+  // CL-1-k in the same step as the forward of g + 1 needs one: forward chunk
+  // k of a group with parity p lives in TMEM slot p ? CL-1-k : k, so both use
+  // the same slot in step k (the backward reads it first).
   const int k = warp % K;
   const int gs = warp / K;
   const int r0 = k * L;
   const uint32_t tlane = tmem_base_s + (static_cast<uint32_t>(32 * (warp & 3)) << 16) +
                          static_cast<uint32_t>((warp >> 2) * 256);
+  auto tslot = [&](uint32_t p, int c) {
+    return tlane + static_cast<uint32_t>((p ? CL - 1 - c : c) * TPiece<double>::kWords);
+  };
   int slot = 0;
   uint32_t phase = 0;
-  uint32_t par = 0;
   const F* fk = sf + r0;
   const B* bk = sb + r0;
-  for (long long g = blockIdx.x; g < groups; g += gridDim.x, par ^= 1u) {
-    // -- forward over the block, values to TMEM, interface dot products
-    double s1 = 0.0, s2 = 0.0, a0 = 0.0, a1 = 0.0;
-    for (int c = 0; c < CL; ++c) {
-      mbar_wait(&full[slot], phase);
-      const double* blk = ring + slot * kChunk + warp * kBox + lane;
-      const F* fc = fk + c * kSpR;
-      TPiece<double> buf;
-      double dv[kSpR];  // stage 1: b / pivot for the whole chunk (off the chain)
+  const double* zk = reinterpret_cast<const double*>(smem + Ly.z_off) + (PENT ? 2 : 1) * r0;
+
+  // forward state of the group being read, backward state of the one being written
+  double fs1 = 0.0, fs2 = 0.0, a0 = 0.0, a1 = 0.0;
+  double bs1 = 0.0, bs2 = 0.0, xl1 = 0.0, xl2 = 0.0, t1 = 0.0, t2 = 0.0;
+  long long step = 0;
+  double* out = sink + lane;
+  TPiece<double> cur;
+
+  auto fwd_chunk = [&](int c, uint32_t p) {
+    mbar_wait(&full[slot], phase);
+    const double* blk = ring + slot * kChunk + warp * kBox + lane;
+    const F* fc = fk + c * kSpR;
+    TPiece<double> buf;
+    double dv[kSpR];  // stage 1: b / pivot for the whole chunk (off the chain)
 #pragma unroll
-      for (int r = 0; r < kSpR; ++r) {
-        if constexpr (PENT) dv[r] = blk[r * 32] * fc[r].ia;
-        else dv[r] = blk[r * 32] * fc[r].m;
-      }
-#pragma unroll
-      for (int r = 0; r < kSpR; ++r) {  // stage 2: one FMA per row on the chain
-        const F f = fc[r];
-        double v;
-        if constexpr (PENT) {
-          v = fma(-f.b, s1, fma(-f.e, s2, dv[r]));
-          a1 = fma(f.p1, v, a1);
-        } else {
-          v = fma(-f.am, s1, dv[r]);
-        }
-        a0 = fma(f.p0, v, a0);
-        s2 = s1;
-        s1 = v;
-        buf.put(r, v);
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[slot]);
-      if (++slot == KB) {
-        slot = 0;
-        phase ^= 1u;
-      }
-      buf.store(tlane + static_cast<uint32_t>(c * TPiece<double>::kWords));
+    for (int r = 0; r < kSpR; ++r) {
+      if constexpr (PENT) dv[r] = blk[r * 32] * fc[r].ia;
+      else dv[r] = blk[r * 32] * fc[r].m;
     }
-    // -- interface values of y for this block: top (dot products), bottom
-    double* xw = xch + (static_cast<size_t>(par) * kSpWarps + warp) * NQ * 32 + lane;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[slot]);
+    if (++slot == KB) {
+      slot = 0;
+      phase ^= 1u;
+    }
+#pragma unroll
+    for (int r = 0; r < kSpR; ++r) {  // stage 2: one FMA per row on the chain
+      const F f = fc[r];
+      double v;
+      if constexpr (PENT) {
+        v = fma(-f.b, fs1, fma(-f.e, fs2, dv[r]));
+        a1 = fma(f.p1, v, a1);
+      } else {
+        v = fma(-f.am, fs1, dv[r]);
+      }
+      a0 = fma(f.p0, v, a0);
+      fs2 = fs1;
+      fs1 = v;
+      buf.put(r, v);
+    }
+    buf.store(tslot(p, c));
+  };
+
+  auto corr = [&](int i, double v) {  // stored value of local row i (periodic correction)
+    if constexpr (!PER) return v;
+    else if constexpr (PENT) return fma(-zk[2 * i], t1, fma(-zk[2 * i + 1], t2, v));
+    else return fma(-zk[i], t1, v);
+  };
+
+  // interface of the group just read (xch parity p): its backward state
+  auto interface = [&](long long g, uint32_t p) {
+    double* xw = xch + (static_cast<size_t>(p) * kSpWarps + warp) * NQ * 32 + lane;
     xw[0] = a0;
     if constexpr (PENT) {
       xw[32] = a1;
-      xw[64] = fma(-bk[L - 2].g, s1, s2);  // y_{L-2} = g_{L-2} - gamma_{L-2} g_{L-1}
-      xw[96] = s1;                          // y_{L-1} = g_{L-1}
+      xw[64] = fma(-bk[L - 2].g, fs1, fs2);  // y_{L-2} = g_{L-2} - gamma_{L-2} g_{L-1}
+      xw[96] = fs1;                          // y_{L-1} = g_{L-1}
     } else {
-      xw[32] = s1;
+      xw[32] = fs1;
     }
+    fs1 = fs2 = a0 = a1 = 0.0;
     asm volatile("bar.sync 1, %0;" ::"r"(kSpWarps * 32) : "memory");
-    // -- this system's interface unknowns: own bottom rows, left neighbour's
     double y[kSpMaxR];
 #pragma unroll
     for (int c = 0; c < kSpMaxR; ++c) {
       if (c < R) {
         const int kk = c / NQ, q = c - kk * NQ;
-        y[c] = xch[((static_cast<size_t>(par) * kSpWarps + gs * K + kk) * NQ + q) * 32 + lane];
+        y[c] = xch[((static_cast<size_t>(p) * kSpWarps + gs * K + kk) * NQ + q) * 32 + lane];
       } else {
         y[c] = 0.0;
       }
@@ -286,19 +310,15 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
       }
       zu[h] = acc;
     }
-    // -- backward from the own bottom unknowns, left coupling folded in, x
-    // streamed to HBM (lanes past m write a scratch word instead: no branch)
-    double xl1, xl2 = 0.0;
     if constexpr (PENT) {
-      s1 = zu[0];   // x_{L-2}
-      s2 = zu[1];   // x_{L-1}
+      bs1 = zu[0];  // x_{L-2}
+      bs2 = zu[1];  // x_{L-1}
       xl2 = zu[2];  // x_{s-2}
       xl1 = zu[3];  // x_{s-1}
     } else {
-      s1 = zu[0];   // x_{L-1}
+      bs1 = zu[0];  // x_{L-1}
       xl1 = zu[1];  // x_{s-1}
     }
-    double t1 = 0.0, t2 = 0.0;  // periodic correction coefficients
     if constexpr (PER) {
       if constexpr (PENT) {  // periodic.cpp:189-194 (fast-mode rounding)
         const double w1 = zu[4] - zu[7], w2 = zu[5] - zu[6];
@@ -308,55 +328,60 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
         t1 = fma(per.c[0], zu[3], zu[2]) * per.c[1];
       }
     }
-    const double* zk = reinterpret_cast<const double*>(smem + Ly.z_off) + (PENT ? 2 : 1) * r0;
-    auto corr = [&](int i, double v) {  // stored value of local row i
-      if constexpr (!PER) return v;
-      else if constexpr (PENT) return fma(-zk[2 * i], t1, fma(-zk[2 * i + 1], t2, v));
-      else return fma(-zk[i], t1, v);
-    };
+    // x streamed to HBM (lanes past m write a scratch word: no branch)
     const long long j = g * Wg + gs * 32 + lane;
     const bool live = j < m;
-    const long long step = live ? ld : 0;
-    double* out = live ? x + static_cast<long long>(r0 + L - 1) * ld + j : sink + lane;
+    step = live ? ld : 0;
+    out = live ? x + static_cast<long long>(r0 + L - 1) * ld + j : sink + lane;
     if constexpr (PENT) {
-      __stcs(out - step, corr(L - 2, s1));
-      __stcs(out, corr(L - 1, s2));
+      __stcs(out - step, corr(L - 2, bs1));
+      __stcs(out, corr(L - 1, bs2));
     } else {
-      __stcs(out, corr(L - 1, s1));
+      __stcs(out, corr(L - 1, bs1));
     }
     out -= NH * step;
-    TPiece<double> cur, nxt;
-    cur.load(tlane + static_cast<uint32_t>((CL - 1) * TPiece<double>::kWords));
+    cur.load(tslot(p, CL - 1));  // the first backward chunk, loaded ahead
+  };
+
+  auto bwd_chunk = [&](int c, auto first) {
+    constexpr int kTop = decltype(first)::value ? kSpR - 1 - NH : kSpR - 1;  // skip the interface rows
     cur.wait();
-    auto chunk_bwd = [&](int c, auto first) {
-      constexpr int kTop = decltype(first)::value ? kSpR - 1 - NH : kSpR - 1;  // skip the interface rows
-      const B* bc = bk + c * kSpR;
-      double gv[kSpR];  // stage 1: left-coupling update (off the chain)
+    const B* bc = bk + c * kSpR;
+    double gv[kSpR];  // stage 1: left-coupling update (off the chain)
 #pragma unroll
-      for (int r = 0; r <= kTop; ++r) {
-        if constexpr (PENT) gv[r] = fma(-bc[r].f1, xl2, fma(-bc[r].f2, xl1, cur.get(r)));
-        else gv[r] = fma(-bc[r].f1, xl1, cur.get(r));
-      }
-#pragma unroll
-      for (int r = kTop; r >= 0; --r) {  // stage 2: one FMA per row on the chain
-        double v;
-        if constexpr (PENT) v = fma(-bc[r].g, s1, fma(-bc[r].d, s2, gv[r]));
-        else v = fma(-bc[r].c, s1, gv[r]);
-        s2 = s1;
-        s1 = v;
-        __stcs(out, corr(c * kSpR + r, v));
-        out -= step;
-      }
-    };
-    for (int c = CL - 1; c >= 0; --c) {
-      if (c > 0) nxt.load(tlane + static_cast<uint32_t>((c - 1) * TPiece<double>::kWords));
-      if (c == CL - 1) chunk_bwd(c, std::true_type{});
-      else chunk_bwd(c, std::false_type{});
-      if (c > 0) {
-        nxt.wait();
-        cur = nxt;
-      }
+    for (int r = 0; r <= kTop; ++r) {
+      if constexpr (PENT) gv[r] = fma(-bc[r].f1, xl2, fma(-bc[r].f2, xl1, cur.get(r)));
+      else gv[r] = fma(-bc[r].f1, xl1, cur.get(r));
     }
+#pragma unroll
+    for (int r = kTop; r >= 0; --r) {  // stage 2: one FMA per row on the chain
+      double v;
+      if constexpr (PENT) v = fma(-bc[r].g, bs1, fma(-bc[r].d, bs2, gv[r]));
+      else v = fma(-bc[r].c, bs1, gv[r]);
+      bs2 = bs1;
+      bs1 = v;
+      __stcs(out, corr(c * kSpR + r, v));
+      out -= step;
+    }
+  };
+
+  const long long my = (groups - blockIdx.x + gridDim.x - 1) / gridDim.x;
+  uint32_t p = 0;  // parity of the group being read
+  for (long long i = 0; i <= my; ++i, p ^= 1u) {
+    const long long g = blockIdx.x + i * gridDim.x;      // group read in this round (i < my)
+    const long long gp = g - gridDim.x;                   // group written in this round (i > 0)
+    // step kk: backward chunk CL-1-kk of gp, then forward chunk kk of g (same TMEM slot)
+    for (int kk = 0; kk < CL; ++kk) {
+      if (i > 0) {
+        const int c = CL - 1 - kk;
+        if (kk == 0) bwd_chunk(c, std::true_type{});
+        else bwd_chunk(c, std::false_type{});
+        if (c > 0) cur.load(tslot(p ^ 1u, c - 1));
+      }
+      if (i < my) fwd_chunk(kk, p);
+    }
+    if (i < my) interface(g, p);
+    (void)gp;
   }
   tmem_fence_before();
   asm volatile("bar.sync 1, %0;" ::"r"(kSpWarps * 32) : "memory");
