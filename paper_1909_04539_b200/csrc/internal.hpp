@@ -161,8 +161,15 @@ int partition_blocks(std::size_t n, std::size_t m, int sms, bool pent);  // 0 = 
 // mode fp64: blocks per system, 0 when it does not apply.
 int spike_blocks(std::size_t n, std::size_t m, std::size_t ld, const void* x, int sms, bool pent);
 struct PartPeriodic;
+// Crank-Nicolson step through the spike kernel: b = the periodic stencil of
+// u (read only), x receives u_new; c = s, 4s (pent), 1-2s / 1-6s
+struct SpikeCN {
+  const double* u;
+  double c[3];
+};
 bandsolve_status spike_solve_device(const Factor& f, double* x, std::size_t n, std::size_t m, std::size_t ld,
-                                    void* stream, int sms, bool* done, const PartPeriodic* per = nullptr);
+                                    void* stream, int sms, bool* done, const PartPeriodic* per = nullptr,
+                                    const SpikeCN* cn = nullptr);
 bool partition_stencil_ok(std::size_t n, std::size_t m, int K, std::size_t lds);
 bandsolve_status partition_solve_device(const Factor& f, double* x, std::size_t n,
                                         std::size_t m, std::size_t ld,

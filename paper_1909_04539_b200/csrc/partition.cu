@@ -769,10 +769,11 @@ int spike_blocks(std::size_t n, std::size_t m, std::size_t ld, const void* x, in
     return 0;
   if (reinterpret_cast<uintptr_t>(x) % 16 != 0 || ld % 2 != 0 || m > static_cast<std::size_t>(INT_MAX) / 2) return 0;
   if (m % 2 != 0) return 0;  // TMA boxes: an odd batch would straddle a 16-byte granule at the edge
+  const int kf = static_cast<int>(tune_int("SPIKE_K", 0));  // tuning override
   int K = 0;
   for (int k = 2; k <= dev::kSpMaxK; k *= 2)
     if (n % k == 0 && (n / k) % dev::kSpR == 0 && n / k <= static_cast<std::size_t>(dev::kSpMaxL) &&
-        n / k >= 2 * dev::kSpR) {
+        n / k >= 2 * dev::kSpR && (kf == 0 || k == kf)) {
       K = k;
       break;
     }
@@ -785,9 +786,10 @@ int spike_blocks(std::size_t n, std::size_t m, std::size_t ld, const void* x, in
 }
 
 bandsolve_status spike_solve_device(const Factor& f, double* x, std::size_t n, std::size_t m, std::size_t ld,
-                                    void* stream, int sms, bool* done, const PartPeriodic* per) {
+                                    void* stream, int sms, bool* done, const PartPeriodic* per, const SpikeCN* cn) {
   *done = false;
   const bool pent = f.kind != Kind::Tri;
+  if (cn && (!per || reinterpret_cast<uintptr_t>(cn->u) % 16 != 0)) return BANDSOLVE_OK;
   const int K = spike_blocks(n, m, ld, x, sms, pent);
   if (K == 0) return BANDSOLVE_OK;
   int device = 0;
@@ -826,8 +828,9 @@ bandsolve_status spike_solve_device(const Factor& f, double* x, std::size_t n, s
   const std::size_t rec_doubles = static_cast<std::size_t>(n) * (pent ? 10 : 6);
   const double* rinv = static_cast<const double*>(blob) + rec_doubles;
   CUtensorMap map;
-  if (!encode_tile_map(&map, x, sizeof(double), N, static_cast<long long>(m), static_cast<long long>(ld), 32,
-                       dev::kSpR))
+  // the tensor map reads b (in place: x; Crank-Nicolson: the old field u)
+  if (!encode_tile_map(&map, cn ? const_cast<double*>(cn->u) : x, sizeof(double), N, static_cast<long long>(m),
+                       static_cast<long long>(ld), 32, dev::kSpR))
     return BANDSOLVE_OK;  // no tensor map: the sweep plans take it
   const int Wg = 32 * (dev::kSpWarps / K);
   const long long groups = (static_cast<long long>(m) + Wg - 1) / Wg;
@@ -835,16 +838,21 @@ bandsolve_status spike_solve_device(const Factor& f, double* x, std::size_t n, s
   const std::size_t smem = dev::SpikeLayout::make(N, R, KB, pent, per != nullptr).total;
   const int PD = static_cast<int>(tune_int("SPD", 4));
   auto s = static_cast<cudaStream_t>(stream);
-  auto kern = pent ? (per ? dev::sweep_spike<true, true> : dev::sweep_spike<true, false>)
-                   : (per ? dev::sweep_spike<false, true> : dev::sweep_spike<false, false>);
-  static std::atomic<uint64_t> configured[4];
+  auto kern = cn ? (pent ? dev::sweep_spike<true, true, true> : dev::sweep_spike<false, true, true>)
+               : pent ? (per ? dev::sweep_spike<true, true> : dev::sweep_spike<true, false>)
+                      : (per ? dev::sweep_spike<false, true> : dev::sweep_spike<false, false>);
+  static std::atomic<uint64_t> configured[6];
   const uint64_t bit = device < 64 ? (1ull << device) : 0;
-  std::atomic<uint64_t>& cfg = configured[(pent ? 2 : 0) + (per ? 1 : 0)];
+  std::atomic<uint64_t>& cfg = configured[cn ? 4 + (pent ? 1 : 0) : (pent ? 2 : 0) + (per ? 1 : 0)];
   dev::SpikePer sp;
   if (per) {
     sp.z1 = per->z1;
     sp.z2 = per->z2;
     for (int q = 0; q < 4; ++q) sp.c[q] = per->c[q];
+  }
+  if (cn) {
+    sp.u = cn->u;
+    for (int q = 0; q < 3; ++q) sp.cn[q] = cn->c[q];
   }
   if (!(bit && (cfg.load(std::memory_order_relaxed) & bit))) {
     if (cudaError_t e = allow_max_smem(reinterpret_cast<const void*>(kern)); e != cudaSuccess)

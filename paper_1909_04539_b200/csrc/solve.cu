@@ -1284,6 +1284,25 @@ bandsolve_status cn_step_device(const Periodic& p, double sigma_x, const double*
   const int sms = num_sms(device);
   const bool aligned = (reinterpret_cast<uintptr_t>(u) % 16 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0) &&
                        ((ld * sizeof(double)) % 16 == 0);
+  if (fast && aligned && !tune_flag("CN_UNFUSED") && spike_blocks(n, m, ld, out, sms, pent) > 0) {
+    // many long systems: stencil + one-pass partitioned sweep + Woodbury
+    // correction in one launch (sweep_spike.cuh, template CN)
+    const double* blob = nullptr;
+    bandsolve_status st = periodic_device_z(p, device, &blob);
+    if (st != BANDSOLVE_OK) return st;
+    PartPeriodic pa{blob, blob + n, {0.0, 0.0, 0.0, 0.0}};
+    if (pent) {
+      for (int k = 0; k < 4; ++k) pa.c[k] = p.cap_inv[k];
+    } else {
+      pa.c[0] = p.v_last;
+      pa.c[1] = p.scale;
+    }
+    // pde.cpp:80-81 / :101-103
+    const SpikeCN cn{u, {sigma_x, pent ? 4.0 * sigma_x : 0.0, pent ? 1.0 - 6.0 * sigma_x : 1.0 - 2.0 * sigma_x}};
+    bool done = false;
+    st = spike_solve_device(*p.factor, out, n, m, ld, stream, sms, &done, &pa, &cn);
+    if (st != BANDSOLVE_OK || done) return st;
+  }
   Plan plan;
   if (!tune_flag("CN_UNFUSED") && aligned && n <= static_cast<std::size_t>(INT_MAX) &&
       m <= static_cast<std::size_t>(INT_MAX) / 2 &&

@@ -82,6 +82,11 @@ struct SpikePer {
   const double* z1 = nullptr;
   const double* z2 = nullptr;
   double c[4] = {0.0, 0.0, 0.0, 0.0};  // tri: v_last, scale; pent: cap_inv
+  // Crank-Nicolson step (template CN): the right-hand side is the explicit
+  // periodic stencil of the old field u (the tensor map's source, read
+  // only), pde.cpp:73-114; x receives u_new. cn = s, 4s (pent), 1-2s / 1-6s
+  const double* u = nullptr;
+  double cn[3] = {0.0, 0.0, 0.0};
 };
 
 struct SpikeLayout {
@@ -102,7 +107,7 @@ struct SpikeLayout {
   }
 };
 
-template <bool PENT, bool PER>
+template <bool PENT, bool PER, bool CN = false>
 __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
     sweep_spike(const __grid_constant__ CUtensorMap map_b, double* __restrict__ x, int n, long long m, long long ld,
                 int K, int L, int KB, int PD, long long groups, const void* __restrict__ recs,
@@ -229,16 +234,75 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
   double* out = sink + lane;
   TPiece<double> cur;
 
-  auto fwd_chunk = [&](int c, uint32_t p) {
+  // CN: the stencil's halo rows. h1/h2 = u at the two rows above the chunk
+  // (carried from the previous chunk; block starts load them), la0/la1 = the
+  // two rows below it (plain loads issued one chunk ahead; the next block's
+  // first rows at the block end), all with the periodic wrap.
+  double h1 = 0.0, h2 = 0.0, la0 = 0.0, la1 = 0.0, nh1 = 0.0, nh2 = 0.0, nla0 = 0.0, nla1 = 0.0;
+  auto u_at = [&](long long g, int row) -> double {  // u[row mod n] of this lane's system in group g
+    if constexpr (CN) {
+      row = row < 0 ? row + n : (row >= n ? row - n : row);
+      long long j = g * Wg + gs * 32 + lane;
+      j = j < m ? j : m - 1;
+      return __ldg(per.u + static_cast<long long>(row) * ld + j);
+    } else {
+      return 0.0;
+    }
+  };
+  auto halo_prefetch = [&](long long g) {  // chunk 0's halo of group g
+    if constexpr (CN) {
+      nh2 = u_at(g, r0 - 2);
+      nh1 = u_at(g, r0 - 1);
+      nla0 = u_at(g, r0 + kSpR);
+      nla1 = u_at(g, r0 + kSpR + 1);
+    }
+  };
+
+  auto fwd_chunk = [&](int c, uint32_t p, long long g) {
     mbar_wait(&full[slot], phase);
     const double* blk = ring + slot * kChunk + warp * kBox + lane;
     const F* fc = fk + c * kSpR;
     TPiece<double> buf;
     double dv[kSpR];  // stage 1: b / pivot for the whole chunk (off the chain)
+    if constexpr (CN) {
+      if (c == 0) {
+        h2 = nh2;
+        h1 = nh1;
+        la0 = nla0;
+        la1 = nla1;
+      }
+      // the next chunk's look-ahead rows (the next block's first rows at the end)
+      const int nb = (c + 2) * kSpR;
+      const double n0 = c + 1 < CL ? u_at(g, r0 + nb) : 0.0;
+      const double n1 = c + 1 < CL ? u_at(g, r0 + nb + 1) : 0.0;
+      double e[kSpR + 4];  // u rows -2 .. kSpR + 1 of the chunk
+      e[0] = h2;
+      e[1] = h1;
 #pragma unroll
-    for (int r = 0; r < kSpR; ++r) {
-      if constexpr (PENT) dv[r] = blk[r * 32] * fc[r].ia;
-      else dv[r] = blk[r * 32] * fc[r].m;
+      for (int r = 0; r < kSpR; ++r) e[r + 2] = blk[r * 32];
+      e[kSpR + 2] = la0;
+      e[kSpR + 3] = la1;
+      const double cs = per.cn[0], cs4 = per.cn[1], cmid = per.cn[2];
+#pragma unroll
+      for (int r = 0; r < kSpR; ++r) {
+        double f;
+        if constexpr (PENT)  // pde.cpp:108  o = -s*(u2 + d2) + s4*(u1 + d1) + mid*mi
+          f = (-cs * (e[r] + e[r + 4]) + cs4 * (e[r + 1] + e[r + 3])) + cmid * e[r + 2];
+        else  // pde.cpp:85  o = s*(up + dn) + mid*mi
+          f = cs * (e[r + 1] + e[r + 3]) + cmid * e[r + 2];
+        if constexpr (PENT) dv[r] = f * fc[r].ia;
+        else dv[r] = f * fc[r].m;
+      }
+      h2 = e[kSpR];
+      h1 = e[kSpR + 1];
+      la0 = n0;
+      la1 = n1;
+    } else {
+#pragma unroll
+      for (int r = 0; r < kSpR; ++r) {
+        if constexpr (PENT) dv[r] = blk[r * 32] * fc[r].ia;
+        else dv[r] = blk[r * 32] * fc[r].m;
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[slot]);
@@ -366,6 +430,7 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
   };
 
   const long long my = (groups - blockIdx.x + gridDim.x - 1) / gridDim.x;
+  if (my > 0) halo_prefetch(blockIdx.x);
   uint32_t p = 0;  // parity of the group being read
   for (long long i = 0; i <= my; ++i, p ^= 1u) {
     const long long g = blockIdx.x + i * gridDim.x;      // group read in this round (i < my)
@@ -378,7 +443,14 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
         else bwd_chunk(c, std::false_type{});
         if (c > 0) cur.load(tslot(p ^ 1u, c - 1));
       }
-      if (i < my) fwd_chunk(kk, p);
+      if (i < my) {
+        if (CN && kk == 0 && i + 1 < my) {  // consume this group's halo, then fetch the next group's
+          fwd_chunk(kk, p, g);
+          halo_prefetch(g + gridDim.x);
+        } else {
+          fwd_chunk(kk, p, g);
+        }
+      }
     }
     if (i < my) interface(g, p);
     (void)gp;

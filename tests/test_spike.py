@@ -166,3 +166,38 @@ def test_spike_periodic_fused_within_tolerance(lib, oracle, cuda_device, n):
             else:
                 want = oracle.periodic_pent_solve(oracle.periodic_pent_prepare(*bands, n), x.copy())
             assert per_system_max_rel(out[:, :m], want) <= TOL_F64, (n, m, ld, bands)
+
+
+@pytest.mark.parametrize("n", [320, 512, 1024])
+def test_spike_cn_step_within_tolerance(lib, oracle, cuda_device, n):
+    """Crank-Nicolson step u_new = A^-1 (B u) in one spike launch: the
+    explicit periodic stencil (pde.cpp:73-114) is formed from the ring boxes
+    plus halo rows across block edges and the wrap, then the partitioned
+    sweep and the Woodbury correction. Within 1e-12 of the reference's
+    assemble-then-solve; the old field is left untouched."""
+    torch = cuda_device
+    lib.tune("SPIKE", "1")
+    rng = np.random.default_rng(n + 2)
+    for prob in (0, 1):
+        for m, ld in [(64, 64), (300, 302)]:
+            s = 0.61
+            u = rng.uniform(-1, 1, (n, m))
+            if prob == 0:
+                h = bs.PeriodicTri(lib, -s, 1 + 2 * s, -s, n)
+                want = oracle.periodic_tri_solve(oracle.periodic_tri_prepare(-s, 1 + 2 * s, -s, n),
+                                                 oracle.cn_rhs(0, s, u))
+            else:
+                h = bs.PeriodicPent(lib, s, -4 * s, 1 + 6 * s, -4 * s, s, n)
+                want = oracle.periodic_pent_solve(oracle.periodic_pent_prepare(s, -4 * s, 1 + 6 * s, -4 * s, s, n),
+                                                  oracle.cn_rhs(1, s, u))
+            du = torch.full((n, ld), float("nan"), dtype=torch.float64, device="cuda")
+            du[:, :m] = torch.from_numpy(u).cuda()
+            do = torch.full_like(du, float("nan"))
+            before = lib.kernel_launches()
+            h.cn_step_dev(s, du.data_ptr(), do.data_ptr(), n, m, ld=ld, stream=torch.cuda.current_stream().cuda_stream)
+            torch.cuda.synchronize()
+            assert lib.kernel_launches() - before == 1, (prob, n, m)
+            out = do.cpu().numpy()
+            assert np.all(np.isnan(out[:, m:]))
+            assert per_system_max_rel(out[:, :m], want) <= TOL_F64, (prob, n, m, ld)
+            assert np.array_equal(du[:, :m].cpu().numpy(), u)
