@@ -35,6 +35,8 @@
 #include <climits>
 #include <cmath>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "internal.hpp"
@@ -753,11 +755,47 @@ PartPlan* cached_plan(const Factor& f, int K) {
   return p->ok ? p : nullptr;
 }
 
-int spike_ring_slots(int n, int R, bool pent, bool per) {
+// CTAs per cluster for K blocks (8 blocks per CTA beyond one CTA)
+int spike_cluster(int K) { return K > dev::kSpWarps ? K / dev::kSpWarps : 1; }
+
+int spike_ring_slots(int n, int K, bool pent, bool per) {
   const std::size_t cap = max_smem_per_block();
+  const int CS = spike_cluster(K);
+  const int Kc = CS > 1 ? dev::kSpWarps : K;
+  const int nl = n / K * Kc;
+  const int R = (pent ? 4 : 2) * K;
   for (int kb = 6; kb >= 2; --kb)
-    if (dev::SpikeLayout::make(n, R, kb, pent, per).total <= cap) return kb;
+    if (dev::SpikeLayout::make(nl, R, Kc, kb, pent, per).total <= cap) return kb;
   return 0;
+}
+
+// Clusters of CS CTAs that can be co-resident (GPC packing), 0 if none.
+int spike_active_clusters(const void* kern, int CS, std::size_t smem, int sms) {
+  if (CS == 1) return sms;
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto key = std::make_pair(kern, CS);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(CS * (sms / CS)), 1, 1);
+  cfg.blockDim = dim3(32 * (dev::kSpWarps + 1), 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = static_cast<unsigned>(CS);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  cache[key] = n;
+  return n;
 }
 
 }  // namespace
@@ -770,6 +808,7 @@ int spike_blocks(std::size_t n, std::size_t m, std::size_t ld, const void* x, in
   if (reinterpret_cast<uintptr_t>(x) % 16 != 0 || ld % 2 != 0 || m > static_cast<std::size_t>(INT_MAX) / 2) return 0;
   if (m % 2 != 0) return 0;  // TMA boxes: an odd batch would straddle a 16-byte granule at the edge
   const int kf = static_cast<int>(tune_int("SPIKE_K", 0));  // tuning override
+  // K <= 8: one CTA holds every block; K = 16 / 32: a cluster of K / 8 CTAs
   int K = 0;
   for (int k = 2; k <= dev::kSpMaxK; k *= 2)
     if (n % k == 0 && (n / k) % dev::kSpR == 0 && n / k <= static_cast<std::size_t>(dev::kSpMaxL) &&
@@ -778,10 +817,13 @@ int spike_blocks(std::size_t n, std::size_t m, std::size_t ld, const void* x, in
       break;
     }
   if (K == 0) return 0;
-  // many systems: at least one full wave of 32 (dev::kSpWarps / K)-system groups
-  const std::size_t wg = 32u * (dev::kSpWarps / K);
-  if (sel != 1 && m < static_cast<std::size_t>(sms) * wg) return 0;
-  if (spike_ring_slots(static_cast<int>(n), (pent ? 4 : 2) * K, pent, true) == 0) return 0;
+  // many systems: at least one full wave of groups (32 (8 / K) systems per
+  // CTA; a cluster of K / 8 CTAs per 32 systems)
+  const int CS = spike_cluster(K);
+  const std::size_t per_wave = CS > 1 ? 32u * static_cast<std::size_t>(sms / CS)
+                                      : 32u * static_cast<std::size_t>(dev::kSpWarps / K) * sms;
+  if (sel != 1 && m < per_wave) return 0;
+  if (spike_ring_slots(static_cast<int>(n), K, pent, true) == 0) return 0;
   return K;
 }
 
@@ -823,8 +865,10 @@ bandsolve_status spike_solve_device(const Factor& f, double* x, std::size_t n, s
     }
   }
   const int N = static_cast<int>(n);
+  const int CS = spike_cluster(K);
+  const int Kc = CS > 1 ? dev::kSpWarps : K;
   const int R = p->R;
-  const int KB = spike_ring_slots(N, R, pent, per != nullptr);
+  const int KB = spike_ring_slots(N, K, pent, per != nullptr);
   const std::size_t rec_doubles = static_cast<std::size_t>(n) * (pent ? 10 : 6);
   const double* rinv = static_cast<const double*>(blob) + rec_doubles;
   CUtensorMap map;
@@ -832,18 +876,26 @@ bandsolve_status spike_solve_device(const Factor& f, double* x, std::size_t n, s
   if (!encode_tile_map(&map, cn ? const_cast<double*>(cn->u) : x, sizeof(double), N, static_cast<long long>(m),
                        static_cast<long long>(ld), 32, dev::kSpR))
     return BANDSOLVE_OK;  // no tensor map: the sweep plans take it
-  const int Wg = 32 * (dev::kSpWarps / K);
+  const int Wg = CS > 1 ? 32 : 32 * (dev::kSpWarps / K);
   const long long groups = (static_cast<long long>(m) + Wg - 1) / Wg;
-  const unsigned grid = static_cast<unsigned>(std::min<long long>(sms, groups));
-  const std::size_t smem = dev::SpikeLayout::make(N, R, KB, pent, per != nullptr).total;
+  const std::size_t smem = dev::SpikeLayout::make(N / K * Kc, R, Kc, KB, pent, per != nullptr).total;
   const int PD = static_cast<int>(tune_int("SPD", 4));
   auto s = static_cast<cudaStream_t>(stream);
-  auto kern = cn ? (pent ? dev::sweep_spike<true, true, true> : dev::sweep_spike<false, true, true>)
-               : pent ? (per ? dev::sweep_spike<true, true> : dev::sweep_spike<true, false>)
-                      : (per ? dev::sweep_spike<false, true> : dev::sweep_spike<false, false>);
-  static std::atomic<uint64_t> configured[6];
+  using Kern = decltype(&dev::sweep_spike<true, true, true, 1>);
+  // [cluster size 1/2/4][cn][pent][per]
+#define BSB_SPIKE_SET(CSZ)                                                                                    \
+  {{{dev::sweep_spike<false, false, false, CSZ>, dev::sweep_spike<false, true, false, CSZ>},                 \
+    {dev::sweep_spike<true, false, false, CSZ>, dev::sweep_spike<true, true, false, CSZ>}},                  \
+   {{dev::sweep_spike<false, true, true, CSZ>, dev::sweep_spike<false, true, true, CSZ>},                    \
+    {dev::sweep_spike<true, true, true, CSZ>, dev::sweep_spike<true, true, true, CSZ>}}}
+  static const Kern kerns[3][2][2][2] = {BSB_SPIKE_SET(1), BSB_SPIKE_SET(2), BSB_SPIKE_SET(4)};
+#undef BSB_SPIKE_SET
+  const int csi = CS == 4 ? 2 : CS == 2 ? 1 : 0;
+  const int ki = csi * 8 + (cn ? 4 : 0) + (pent ? 2 : 0) + (per ? 1 : 0);
+  const Kern kern = kerns[csi][cn != nullptr][pent][per != nullptr];
+  static std::atomic<uint64_t> configured[24];
   const uint64_t bit = device < 64 ? (1ull << device) : 0;
-  std::atomic<uint64_t>& cfg = configured[cn ? 4 + (pent ? 1 : 0) : (pent ? 2 : 0) + (per ? 1 : 0)];
+  std::atomic<uint64_t>& attr_set = configured[ki];
   dev::SpikePer sp;
   if (per) {
     sp.z1 = per->z1;
@@ -854,10 +906,12 @@ bandsolve_status spike_solve_device(const Factor& f, double* x, std::size_t n, s
     sp.u = cn->u;
     for (int q = 0; q < 3; ++q) sp.cn[q] = cn->c[q];
   }
-  if (!(bit && (cfg.load(std::memory_order_relaxed) & bit))) {
+  if (!(bit && (attr_set.load(std::memory_order_relaxed) & bit))) {
     if (cudaError_t e = allow_max_smem(reinterpret_cast<const void*>(kern)); e != cudaSuccess)
       return fail(BANDSOLVE_ERR_INTERNAL, std::string("spike attributes: ") + cudaGetErrorString(e));
-    if (bit) cfg.fetch_or(bit, std::memory_order_relaxed);
+    if (CS > 1)  // clusters of up to 4: portable size, no opt-in needed
+      cudaFuncSetAttribute(reinterpret_cast<const void*>(kern), cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
+    if (bit) attr_set.fetch_or(bit, std::memory_order_relaxed);
   }
   // lanes past the batch edge write their values here (branch-free stores)
   static double* sinks[64] = {};
@@ -871,12 +925,26 @@ bandsolve_status spike_solve_device(const Factor& f, double* x, std::size_t n, s
       return fail(BANDSOLVE_ERR_INTERNAL, "spike scratch");
     }
   }
-  kern<<<grid, 32 * (dev::kSpWarps + 1), smem, s>>>(map, x, N, static_cast<long long>(m),
-                                                     static_cast<long long>(ld), K, p->L, KB, PD, groups, blob, rinv,
-                                                     sinks[device], sp);
+  const int active = spike_active_clusters(reinterpret_cast<const void*>(kern), CS, smem, sms);
+  if (active <= 0) return BANDSOLVE_OK;  // the cluster does not fit: the sweep plans take it
+  const unsigned grid = static_cast<unsigned>(CS * std::min<long long>(active, groups));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid, 1, 1);
+  cfg.blockDim = dim3(32 * (dev::kSpWarps + 1), 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = static_cast<unsigned>(CS);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = CS > 1 ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, map, x, N, static_cast<long long>(m), static_cast<long long>(ld), K,
+                                     p->L, KB, PD, groups, static_cast<const void*>(blob), rinv, sinks[device], sp);
   note_launches(1);
-  if (cudaError_t e = cudaGetLastError(); e != cudaSuccess)
-    return fail(BANDSOLVE_ERR_INTERNAL, std::string("spike launch: ") + cudaGetErrorString(e));
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(BANDSOLVE_ERR_INTERNAL, std::string("spike launch: ") + cudaGetErrorString(e));
   *done = true;
   return BANDSOLVE_OK;
 }

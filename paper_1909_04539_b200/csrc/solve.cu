@@ -486,7 +486,10 @@ bool plan_stream(std::size_t n, std::size_t m, std::size_t elem, bool pent, bool
     const double spill = static_cast<double>(grid) * Wg * (H - (rtc + rc) * dev::kSR) * elem;
     const double rounds = static_cast<double>(m) / (static_cast<double>(Wg) * sms);
     const double util = rounds / std::ceil(rounds);
-    const double frac = stream_compute_frac(Wg, pent, fast) * (V == 2 ? 0.95 : 1.0) *
+    // fp32 fast mode: the fp64 fast calibration underrates wider groups
+    // (measured tri N = 512, 2^20: Wg = 64 0.53, Wg = 96 0.78); the exact
+    // curve ranks fp32 groups correctly
+    const double frac = stream_compute_frac(Wg, pent, fast && elem == 8) * (V == 2 ? 0.95 : 1.0) *
                         stream_spill_factor(spill / (1 << 20)) * util *
                         (16.0 / (16.0 + 8.0 * rc * dev::kSR / N));  // the recomputed rows read b twice
     const double t = static_cast<double>(n) * m * 2.0 * elem / (frac * 6.5e12);
@@ -1132,8 +1135,8 @@ bandsolve_status describe_plan(Kind kind, std::size_t n, std::size_t m, std::siz
   const int KS = f32 ? 0 : spike_blocks(n, m, ld, kProbe, sms, pent);
   const int K = f32 ? 0 : partition_blocks(n, m, sms, pent);
   if (KS > 0)
-    std::snprintf(buf, sizeof buf, "spike K=%d blocks of %zu rows, interface system %d, 1 launch (TMEM-resident blocks)",
-                  KS, n / KS, (pent ? 4 : 2) * KS);
+    std::snprintf(buf, sizeof buf, "spike K=%d blocks of %zu rows, interface system %d, 1 launch (TMEM-resident blocks%s)",
+                  KS, n / KS, (pent ? 4 : 2) * KS, KS > 8 ? (KS == 16 ? ", clusters of 2 CTAs" : ", clusters of 4 CTAs") : "");
   else if (K > 0)
     std::snprintf(buf, sizeof buf, "partition K=%d blocks of %zu rows, interface system %d (dense LU), 2 launches", K,
                   n / K, (pent ? 4 : 2) * K);

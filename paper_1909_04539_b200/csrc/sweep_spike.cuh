@@ -23,19 +23,30 @@
 //             tcgen05.st.32x32b.x32, and accumulates the two (one)
 //             interface dot products with the U^-1 rows;
 //   interface each warp publishes its block's interface values of y =
-//             A_k^-1 b_k in shared memory; after a named barrier every lane
-//             forms the x interface unknowns it needs (own bottom rows, the
-//             left neighbour's bottom rows) as rows of R^-1 times the
-//             system's y interface vector;
+//             A_k^-1 b_k in shared memory; after a barrier every lane forms
+//             the x interface unknowns it needs (own bottom rows, the left
+//             neighbour's bottom rows) as rows of R^-1 times the system's y
+//             interface vector;
 //   backward  from its own bottom x values the lane sweeps up over the TMEM
 //             values (one tcgen05.ld per 16 rows, one chunk ahead), folding
 //             the left coupling in as g_i - F_i x_left, and streams x to HBM.
 //
+// Systems longer than 8 blocks (N = 2048, 4096: K = 16, 32) span a thread-
+// block CLUSTER of K / 8 CTAs, one per SM: each CTA holds 8 blocks of the
+// same 32 systems in its TMEM, the interface values travel through
+// distributed shared memory (ld.shared::cluster) after a cluster-scope
+// mbarrier, and each CTA keeps only the R^-1 rows its blocks need.
+//
+// Software pipeline across groups: after the interface solve of group g a
+// warp interleaves, chunk by chunk, the backward sweep of g with the forward
+// sweep of g + 1 (two independent dependency chains per warp; b is read
+// while x is written, so the SM's HBM traffic never comes in read-only /
+// write-only bursts). Forward chunk k of a group with parity p lives in TMEM
+// slot p ? CL-1-k : k, so in step k both use the slot the backward frees.
 // Each 16-row chunk is computed in two stages so the dependency chain holds
 // ONE fp64 FMA per row: first everything that does not depend on the
 // recurrence (b * (1/alpha), the left-coupling update), for all 16 rows,
-// then the chain itself (measured: the interleaved single-stage loop ran at
-// ~85 cycles per backward row with one warp per scheduler).
+// then the chain itself.
 //
 // HBM traffic: read b once, write x once (16 B/row). Arithmetic differs
 // from the sequential sweep by rounding only (fast mode, 1e-12 contract),
@@ -50,8 +61,8 @@ namespace dev {
 constexpr int kSpR = 16;       // rows per chunk: one TMA box {32 systems, 16 rows} per warp
 constexpr int kSpWarps = 8;    // compute warps: two per TMEM lane quadrant, 256 columns each
 constexpr int kSpMaxL = 128;   // rows per block: 1 KB of TMEM lane per fp64 value
-constexpr int kSpMaxK = 8;     // blocks per system
-constexpr int kSpMaxR = 32;    // interface unknowns (pent 4 K)
+constexpr int kSpMaxK = 32;    // blocks per system (a cluster of up to 4 CTAs)
+constexpr int kSpMaxCS = 4;    // CTAs per cluster
 
 // per-row records in shared memory, split by phase
 template <bool PENT>
@@ -89,25 +100,71 @@ struct SpikePer {
   double cn[3] = {0.0, 0.0, 0.0};
 };
 
+// Rows of R^-1 a CTA keeps (its blocks kb0 .. kb0+Kc-1): the bottom NH
+// unknowns of blocks kb0-1 .. kb0+Kc-1, then (periodic) the system's first
+// and last NH unknowns.
+__host__ __device__ constexpr int spike_rinv_rows(int Kc, int nh) { return (Kc + 3) * nh; }
+
 struct SpikeLayout {
   size_t fwd_off, bwd_off, z_off, rinv_off, xch_off, ring_off, bar_off, total;
-  __host__ __device__ static SpikeLayout make(int n, int R, int KB, bool pent, bool per = false) {
+  // nl: rows whose records this CTA holds; R: interface unknowns; Kc: blocks per CTA
+  __host__ __device__ static SpikeLayout make(int nl, int R, int Kc, int KB, bool pent, bool per = false) {
     SpikeLayout L{};
     L.fwd_off = 0;
-    L.bwd_off = align128(static_cast<size_t>(n) * (pent ? sizeof(SpF<true>) : sizeof(SpF<false>)));
-    L.z_off = L.bwd_off + align128(static_cast<size_t>(n) * (pent ? sizeof(SpB<true>) : sizeof(SpB<false>)));
-    // z of the periodic correction: [n] pairs (pent) / values (tri)
-    L.rinv_off = L.z_off + (per ? align128(static_cast<size_t>(n) * (pent ? 2 : 1) * sizeof(double)) : 0);
-    L.xch_off = L.rinv_off + align128(static_cast<size_t>(R) * R * sizeof(double));
+    L.bwd_off = align128(static_cast<size_t>(nl) * (pent ? sizeof(SpF<true>) : sizeof(SpF<false>)));
+    L.z_off = L.bwd_off + align128(static_cast<size_t>(nl) * (pent ? sizeof(SpB<true>) : sizeof(SpB<false>)));
+    // z of the periodic correction: [nl] pairs (pent) / values (tri)
+    L.rinv_off = L.z_off + (per ? align128(static_cast<size_t>(nl) * (pent ? 2 : 1) * sizeof(double)) : 0);
+    L.xch_off = L.rinv_off +
+                align128(static_cast<size_t>(spike_rinv_rows(Kc, pent ? 2 : 1)) * R * sizeof(double));
     // interface exchange, double-buffered: [2][warp][q][32 lanes]
     L.ring_off = L.xch_off + align128(2ull * kSpWarps * (pent ? 4 : 2) * 32 * sizeof(double));
     L.bar_off = L.ring_off + static_cast<size_t>(KB) * kSpWarps * kSpR * 32 * sizeof(double);
-    L.total = L.bar_off + static_cast<size_t>(2 * KB + 1) * sizeof(uint64_t);
+    // ring barriers, the two cluster interface barriers, the TMEM base word
+    L.total = L.bar_off + static_cast<size_t>(2 * KB + 3) * sizeof(uint64_t);
     return L;
   }
 };
 
-template <bool PENT, bool PER, bool CN = false>
+// ---- cluster primitives ----------------------------------------------------
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t map_rank(uint32_t saddr, uint32_t rank) {  // own smem -> CTA rank's
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ double ld_cluster_f64(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t remote_bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote_bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void fence_cluster() { asm volatile("fence.acq_rel.cluster;" ::: "memory"); }
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// CS: CTAs per cluster (1; 2 / 4 for K = 16 / 32), a compile-time constant:
+// with a runtime CS the single-CTA kernel measured 30% slower (tri N = 512:
+// 0.68 vs 0.96 of the HBM roofline)
+template <bool PENT, bool PER, bool CN = false, int CS = 1>
 __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
     sweep_spike(const __grid_constant__ CUtensorMap map_b, double* __restrict__ x, int n, long long m, long long ld,
                 int K, int L, int KB, int PD, long long groups, const void* __restrict__ recs,
@@ -118,9 +175,18 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
   constexpr int NH = NQ / 2;
   extern __shared__ __align__(128) unsigned char smem[];
   const int R = NQ * K;
-  const int G = kSpWarps / K;  // 32-system groups per CTA iteration
+  // CS == 1: the CTA holds all K blocks of G = 8/K groups of 32 systems;
+  // CS > 1: it holds blocks [kb0, kb0 + 8) of one group (G = 1)
+  const int rank = CS > 1 ? static_cast<int>(cluster_rank()) : 0;
+  const int Kc = CS > 1 ? kSpWarps : K;
+  const int kb0 = rank * Kc;
+  const int G = CS > 1 ? 1 : kSpWarps / K;
   const int Wg = 32 * G;
-  const SpikeLayout Ly = SpikeLayout::make(n, R, KB, PENT, PER);
+  const int nl = Kc * L;      // rows whose records this CTA holds
+  const int row0 = kb0 * L;   // first of them
+  const long long cid = blockIdx.x / CS;  // cluster (group walker) index
+  const long long ncl = gridDim.x / CS;
+  const SpikeLayout Ly = SpikeLayout::make(nl, R, Kc, KB, PENT, PER);
   F* sf = reinterpret_cast<F*>(smem + Ly.fwd_off);
   B* sb = reinterpret_cast<B*>(smem + Ly.bwd_off);
   double* srinv = reinterpret_cast<double*>(smem + Ly.rinv_off);
@@ -128,31 +194,46 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
   double* ring = reinterpret_cast<double*>(smem + Ly.ring_off);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + Ly.bar_off);
   uint64_t* empty = full + KB;
-  uint32_t& tmem_base_s = *reinterpret_cast<uint32_t*>(empty + KB);
+  // cluster interface barriers (CS > 1), one per group parity: a warp's
+  // arrival for group g + 1 can never land in the phase of group g
+  uint64_t* ibar = empty + KB;
+  uint32_t& tmem_base_s = *reinterpret_cast<uint32_t*>(ibar + 2);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   constexpr int kBox = kSpR * 32;          // elements of one warp's box
   constexpr int kChunk = kSpWarps * kBox;  // elements of one ring slot
   const int CL = L / kSpR;                 // chunks per block
 
-  {  // records and R^-1 -> smem (16-byte words)
-    const size_t rec_words = static_cast<size_t>(n) * (sizeof(F) + sizeof(B)) / 16;
-    const uint4* src = static_cast<const uint4*>(recs);
-    uint4* dst = reinterpret_cast<uint4*>(smem + Ly.fwd_off);
-    const size_t fwd_words = static_cast<size_t>(n) * sizeof(F) / 16;
-    for (size_t i = threadIdx.x; i < rec_words; i += blockDim.x) {
-      const size_t o = i < fwd_words ? i : (Ly.bwd_off / 16 + (i - fwd_words));
-      dst[o] = src[i];
+  {  // this CTA's records, its R^-1 rows and z -> smem
+    const uint4* srcf = static_cast<const uint4*>(recs);
+    const uint4* srcb = reinterpret_cast<const uint4*>(static_cast<const F*>(recs) + n);
+    uint4* dstf = reinterpret_cast<uint4*>(smem + Ly.fwd_off);
+    uint4* dstb = reinterpret_cast<uint4*>(smem + Ly.bwd_off);
+    constexpr int wf = sizeof(F) / 16, wb = sizeof(B) / 16;
+    for (int i = threadIdx.x; i < nl * wf; i += blockDim.x) dstf[i] = srcf[static_cast<size_t>(row0) * wf + i];
+    for (int i = threadIdx.x; i < nl * wb; i += blockDim.x) dstb[i] = srcb[static_cast<size_t>(row0) * wb + i];
+    const int nr = spike_rinv_rows(Kc, NH);
+    for (int i = threadIdx.x; i < nr * R; i += blockDim.x) {
+      const int t = i / R, c = i - t * R;
+      int row;  // global row of R^-1 kept at local row t
+      if (t < (Kc + 1) * NH) {
+        const int kk = kb0 - 1 + t / NH;  // block whose bottom unknowns these are
+        row = kk < 0 ? 0 : NQ * kk + NH + t % NH;
+      } else if (t < (Kc + 2) * NH) {
+        row = t - (Kc + 1) * NH;  // the system's first NH unknowns (block 0 top)
+      } else {
+        row = R - NH + (t - (Kc + 2) * NH);  // its last NH unknowns
+      }
+      srinv[i] = rinv_g[static_cast<size_t>(row) * R + c];
     }
-    for (int i = threadIdx.x; i < R * R; i += blockDim.x) srinv[i] = rinv_g[i];
     if constexpr (PER) {
       double* z = reinterpret_cast<double*>(smem + Ly.z_off);
-      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      for (int i = threadIdx.x; i < nl; i += blockDim.x) {
         if constexpr (PENT) {
-          z[2 * i] = per.z1[i];
-          z[2 * i + 1] = per.z2[i];
+          z[2 * i] = per.z1[row0 + i];
+          z[2 * i + 1] = per.z2[row0 + i];
         } else {
-          z[i] = per.z1[i];
+          z[i] = per.z1[row0 + i];
         }
       }
     }
@@ -162,23 +243,30 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kSpWarps);
     }
+    mbar_init(&ibar[0], CS * kSpWarps);
+    mbar_init(&ibar[1], CS * kSpWarps);
     fence_barrier_init();
   }
   if (warp == 0) tmem_alloc_512(&tmem_base_s);
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
+  if (CS > 1) cluster_sync_all();  // every CTA's barriers are initialised before remote arrivals
+
+  // block / group slot of warp w, and the global first row of its block
+  auto blk_of = [&](int w) { return CS > 1 ? kb0 + w : w % K; };
+  auto gs_of = [&](int w) { return CS > 1 ? 0 : w / K; };
 
   if (warp == kSpWarps) {  // ---- producer: b chunks through the ring
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
-      const long long my_groups = (groups - blockIdx.x + gridDim.x - 1) / gridDim.x;
+      const long long my_groups = (groups - cid + ncl - 1) / ncl;
       const long long total = my_groups * CL;
       long long pf = 0;
       auto chunk_at = [&](long long t, int& c0, int& c) {
         const long long gi = t / CL;
         c = static_cast<int>(t - gi * CL);
-        c0 = static_cast<int>((blockIdx.x + gi * gridDim.x) * Wg);
+        c0 = static_cast<int>((cid + gi * ncl) * Wg);
       };
       int slot = 0;
       uint32_t phase = 0;
@@ -186,281 +274,288 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
         for (; pf < total && pf < t + PD; ++pf) {  // keep PD chunks ahead in L2
           int c0, c;
           chunk_at(pf, c0, c);
-          for (int w = 0; w < kSpWarps; ++w) tma_prefetch_2d(&map_b, c0 + (w / K) * 32, (w % K) * L + c * kSpR);
+          for (int w = 0; w < kSpWarps; ++w) tma_prefetch_2d(&map_b, c0 + gs_of(w) * 32, blk_of(w) * L + c * kSpR);
         }
         if (t >= KB) mbar_wait(&empty[slot], phase ^ 1u);
         int c0, c;
         chunk_at(t, c0, c);
         mbar_expect_tx(&full[slot], kChunk * sizeof(double));
         for (int w = 0; w < kSpWarps; ++w)
-          tma_load_2d(ring + slot * kChunk + w * kBox, &map_b, c0 + (w / K) * 32, (w % K) * L + c * kSpR, &full[slot],
-                      pol);
+          tma_load_2d(ring + slot * kChunk + w * kBox, &map_b, c0 + gs_of(w) * 32, blk_of(w) * L + c * kSpR,
+                      &full[slot], pol);
         if (++slot == KB) {
           slot = 0;
           phase ^= 1u;
         }
       }
     }
-    return;
-  }
+  } else {
+    // ---- compute warps: block k of the 32 systems of group slot gs
+    const int k = blk_of(warp);
+    const int gs = gs_of(warp);
+    const int r0 = k * L;           // global first row of the block
+    const int rl = r0 - row0;       // its first row in this CTA's records
+    const uint32_t tlane = tmem_base_s + (static_cast<uint32_t>(32 * (warp & 3)) << 16) +
+                           static_cast<uint32_t>((warp >> 2) * 256);
+    auto tslot = [&](uint32_t p, int c) {
+      return tlane + static_cast<uint32_t>((p ? CL - 1 - c : c) * TPiece<double>::kWords);
+    };
+    int slot = 0;
+    uint32_t phase = 0;
+    uint32_t iphase = 0;  // bit p: phase parity of interface barrier p
+    const F* fk = sf + rl;
+    const B* bk = sb + rl;
+    const double* zk = reinterpret_cast<const double*>(smem + Ly.z_off) + (PENT ? 2 : 1) * rl;
 
-  // ---- compute warps: block k of the 32 systems of group slot gs.
-  // Software-pipelined across groups: after the interface solve of group g
-  // the warp interleaves, chunk by chunk, the backward sweep of g with the
-  // forward sweep of g + 1 (two independent dependency chains per warp, and
-  // b is read while x is written, so the SM's HBM traffic never comes in
-  // read-only / write-only bursts). The backward of g frees TMEM chunk
-  // CL-1-k in the same step as the forward of g + 1 needs one: forward chunk
-  // k of a group with parity p lives in TMEM slot p ? CL-1-k : k, so both use
-  // the same slot in step k (the backward reads it first).
-  const int k = warp % K;
-  const int gs = warp / K;
-  const int r0 = k * L;
-  const uint32_t tlane = tmem_base_s + (static_cast<uint32_t>(32 * (warp & 3)) << 16) +
-                         static_cast<uint32_t>((warp >> 2) * 256);
-  auto tslot = [&](uint32_t p, int c) {
-    return tlane + static_cast<uint32_t>((p ? CL - 1 - c : c) * TPiece<double>::kWords);
-  };
-  int slot = 0;
-  uint32_t phase = 0;
-  const F* fk = sf + r0;
-  const B* bk = sb + r0;
-  const double* zk = reinterpret_cast<const double*>(smem + Ly.z_off) + (PENT ? 2 : 1) * r0;
+    // forward state of the group being read, backward state of the one being written
+    double fs1 = 0.0, fs2 = 0.0, a0 = 0.0, a1 = 0.0;
+    double bs1 = 0.0, bs2 = 0.0, xl1 = 0.0, xl2 = 0.0, t1 = 0.0, t2 = 0.0;
+    long long step = 0;
+    double* out = sink + lane;
+    TPiece<double> cur;
 
-  // forward state of the group being read, backward state of the one being written
-  double fs1 = 0.0, fs2 = 0.0, a0 = 0.0, a1 = 0.0;
-  double bs1 = 0.0, bs2 = 0.0, xl1 = 0.0, xl2 = 0.0, t1 = 0.0, t2 = 0.0;
-  long long step = 0;
-  double* out = sink + lane;
-  TPiece<double> cur;
-
-  // CN: the stencil's halo rows. h1/h2 = u at the two rows above the chunk
-  // (carried from the previous chunk; block starts load them), la0/la1 = the
-  // two rows below it (plain loads issued one chunk ahead; the next block's
-  // first rows at the block end), all with the periodic wrap.
-  double h1 = 0.0, h2 = 0.0, la0 = 0.0, la1 = 0.0, nh1 = 0.0, nh2 = 0.0, nla0 = 0.0, nla1 = 0.0;
-  auto u_at = [&](long long g, int row) -> double {  // u[row mod n] of this lane's system in group g
-    if constexpr (CN) {
-      row = row < 0 ? row + n : (row >= n ? row - n : row);
-      long long j = g * Wg + gs * 32 + lane;
-      j = j < m ? j : m - 1;
-      return __ldg(per.u + static_cast<long long>(row) * ld + j);
-    } else {
-      return 0.0;
-    }
-  };
-  auto halo_prefetch = [&](long long g) {  // chunk 0's halo of group g
-    if constexpr (CN) {
-      nh2 = u_at(g, r0 - 2);
-      nh1 = u_at(g, r0 - 1);
-      nla0 = u_at(g, r0 + kSpR);
-      nla1 = u_at(g, r0 + kSpR + 1);
-    }
-  };
-
-  auto fwd_chunk = [&](int c, uint32_t p, long long g) {
-    mbar_wait(&full[slot], phase);
-    const double* blk = ring + slot * kChunk + warp * kBox + lane;
-    const F* fc = fk + c * kSpR;
-    TPiece<double> buf;
-    double dv[kSpR];  // stage 1: b / pivot for the whole chunk (off the chain)
-    if constexpr (CN) {
-      if (c == 0) {
-        h2 = nh2;
-        h1 = nh1;
-        la0 = nla0;
-        la1 = nla1;
-      }
-      // the next chunk's look-ahead rows (the next block's first rows at the end)
-      const int nb = (c + 2) * kSpR;
-      const double n0 = c + 1 < CL ? u_at(g, r0 + nb) : 0.0;
-      const double n1 = c + 1 < CL ? u_at(g, r0 + nb + 1) : 0.0;
-      double e[kSpR + 4];  // u rows -2 .. kSpR + 1 of the chunk
-      e[0] = h2;
-      e[1] = h1;
-#pragma unroll
-      for (int r = 0; r < kSpR; ++r) e[r + 2] = blk[r * 32];
-      e[kSpR + 2] = la0;
-      e[kSpR + 3] = la1;
-      const double cs = per.cn[0], cs4 = per.cn[1], cmid = per.cn[2];
-#pragma unroll
-      for (int r = 0; r < kSpR; ++r) {
-        double f;
-        if constexpr (PENT)  // pde.cpp:108  o = -s*(u2 + d2) + s4*(u1 + d1) + mid*mi
-          f = (-cs * (e[r] + e[r + 4]) + cs4 * (e[r + 1] + e[r + 3])) + cmid * e[r + 2];
-        else  // pde.cpp:85  o = s*(up + dn) + mid*mi
-          f = cs * (e[r + 1] + e[r + 3]) + cmid * e[r + 2];
-        if constexpr (PENT) dv[r] = f * fc[r].ia;
-        else dv[r] = f * fc[r].m;
-      }
-      h2 = e[kSpR];
-      h1 = e[kSpR + 1];
-      la0 = n0;
-      la1 = n1;
-    } else {
-#pragma unroll
-      for (int r = 0; r < kSpR; ++r) {
-        if constexpr (PENT) dv[r] = blk[r * 32] * fc[r].ia;
-        else dv[r] = blk[r * 32] * fc[r].m;
-      }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[slot]);
-    if (++slot == KB) {
-      slot = 0;
-      phase ^= 1u;
-    }
-#pragma unroll
-    for (int r = 0; r < kSpR; ++r) {  // stage 2: one FMA per row on the chain
-      const F f = fc[r];
-      double v;
-      if constexpr (PENT) {
-        v = fma(-f.b, fs1, fma(-f.e, fs2, dv[r]));
-        a1 = fma(f.p1, v, a1);
+    // CN: the stencil's halo rows. h1/h2 = u at the two rows above the chunk
+    // (carried from the previous chunk; block starts load them), la0/la1 = the
+    // two rows below it (plain loads issued one chunk ahead; the next block's
+    // first rows at the block end), all with the periodic wrap.
+    double h1 = 0.0, h2 = 0.0, la0 = 0.0, la1 = 0.0, nh1 = 0.0, nh2 = 0.0, nla0 = 0.0, nla1 = 0.0;
+    auto u_at = [&](long long g, int row) -> double {  // u[row mod n] of this lane's system in group g
+      if constexpr (CN) {
+        row = row < 0 ? row + n : (row >= n ? row - n : row);
+        long long j = g * Wg + gs * 32 + lane;
+        j = j < m ? j : m - 1;
+        return __ldg(per.u + static_cast<long long>(row) * ld + j);
       } else {
-        v = fma(-f.am, fs1, dv[r]);
+        return 0.0;
       }
-      a0 = fma(f.p0, v, a0);
-      fs2 = fs1;
-      fs1 = v;
-      buf.put(r, v);
-    }
-    buf.store(tslot(p, c));
-  };
+    };
+    auto halo_prefetch = [&](long long g) {  // chunk 0's halo of group g
+      if constexpr (CN) {
+        nh2 = u_at(g, r0 - 2);
+        nh1 = u_at(g, r0 - 1);
+        nla0 = u_at(g, r0 + kSpR);
+        nla1 = u_at(g, r0 + kSpR + 1);
+      }
+    };
 
-  auto corr = [&](int i, double v) {  // stored value of local row i (periodic correction)
-    if constexpr (!PER) return v;
-    else if constexpr (PENT) return fma(-zk[2 * i], t1, fma(-zk[2 * i + 1], t2, v));
-    else return fma(-zk[i], t1, v);
-  };
-
-  // interface of the group just read (xch parity p): its backward state
-  auto interface = [&](long long g, uint32_t p) {
-    double* xw = xch + (static_cast<size_t>(p) * kSpWarps + warp) * NQ * 32 + lane;
-    xw[0] = a0;
-    if constexpr (PENT) {
-      xw[32] = a1;
-      xw[64] = fma(-bk[L - 2].g, fs1, fs2);  // y_{L-2} = g_{L-2} - gamma_{L-2} g_{L-1}
-      xw[96] = fs1;                          // y_{L-1} = g_{L-1}
-    } else {
-      xw[32] = fs1;
-    }
-    fs1 = fs2 = a0 = a1 = 0.0;
-    asm volatile("bar.sync 1, %0;" ::"r"(kSpWarps * 32) : "memory");
-    double y[kSpMaxR];
+    auto fwd_chunk = [&](int c, uint32_t p, long long g) {
+      mbar_wait(&full[slot], phase);
+      const double* blk = ring + slot * kChunk + warp * kBox + lane;
+      const F* fc = fk + c * kSpR;
+      TPiece<double> buf;
+      double dv[kSpR];  // stage 1: b / pivot for the whole chunk (off the chain)
+      if constexpr (CN) {
+        if (c == 0) {
+          h2 = nh2;
+          h1 = nh1;
+          la0 = nla0;
+          la1 = nla1;
+        }
+        // the next chunk's look-ahead rows (the next block's first rows at the end)
+        const int nb = (c + 2) * kSpR;
+        const double n0 = c + 1 < CL ? u_at(g, r0 + nb) : 0.0;
+        const double n1 = c + 1 < CL ? u_at(g, r0 + nb + 1) : 0.0;
+        double e[kSpR + 4];  // u rows -2 .. kSpR + 1 of the chunk
+        e[0] = h2;
+        e[1] = h1;
 #pragma unroll
-    for (int c = 0; c < kSpMaxR; ++c) {
-      if (c < R) {
-        const int kk = c / NQ, q = c - kk * NQ;
-        y[c] = xch[((static_cast<size_t>(p) * kSpWarps + gs * K + kk) * NQ + q) * 32 + lane];
+        for (int r = 0; r < kSpR; ++r) e[r + 2] = blk[r * 32];
+        e[kSpR + 2] = la0;
+        e[kSpR + 3] = la1;
+        const double cs = per.cn[0], cs4 = per.cn[1], cmid = per.cn[2];
+#pragma unroll
+        for (int r = 0; r < kSpR; ++r) {
+          double f;
+          if constexpr (PENT)  // pde.cpp:108  o = -s*(u2 + d2) + s4*(u1 + d1) + mid*mi
+            f = (-cs * (e[r] + e[r + 4]) + cs4 * (e[r + 1] + e[r + 3])) + cmid * e[r + 2];
+          else  // pde.cpp:85  o = s*(up + dn) + mid*mi
+            f = cs * (e[r + 1] + e[r + 3]) + cmid * e[r + 2];
+          if constexpr (PENT) dv[r] = f * fc[r].ia;
+          else dv[r] = f * fc[r].m;
+        }
+        h2 = e[kSpR];
+        h1 = e[kSpR + 1];
+        la0 = n0;
+        la1 = n1;
       } else {
-        y[c] = 0.0;
-      }
-    }
-    // [own bottom NH | left bottom NH | (PER) first NH | last NH of the system]
-    constexpr int NU = PER ? 4 * NH : 2 * NH;
-    double zu[NU];
 #pragma unroll
-    for (int h = 0; h < NU; ++h) {
-      const int row = h < NH ? NQ * k + NH + h
-                      : h < 2 * NH ? NQ * k - NH + (h - NH)
-                      : h < 3 * NH ? h - 2 * NH
-                                   : R - NH + (h - 3 * NH);
-      double acc = 0.0;
-      if (h < NH || h >= 2 * NH || k > 0) {
-#pragma unroll
-        for (int c = 0; c < kSpMaxR; ++c)
-          if (c < R) acc = fma(srinv[row * R + c], y[c], acc);
-      }
-      zu[h] = acc;
-    }
-    if constexpr (PENT) {
-      bs1 = zu[0];  // x_{L-2}
-      bs2 = zu[1];  // x_{L-1}
-      xl2 = zu[2];  // x_{s-2}
-      xl1 = zu[3];  // x_{s-1}
-    } else {
-      bs1 = zu[0];  // x_{L-1}
-      xl1 = zu[1];  // x_{s-1}
-    }
-    if constexpr (PER) {
-      if constexpr (PENT) {  // periodic.cpp:189-194 (fast-mode rounding)
-        const double w1 = zu[4] - zu[7], w2 = zu[5] - zu[6];
-        t1 = fma(per.c[0], w1, per.c[1] * w2);
-        t2 = fma(per.c[2], w1, per.c[3] * w2);
-      } else {  // periodic.cpp:80
-        t1 = fma(per.c[0], zu[3], zu[2]) * per.c[1];
-      }
-    }
-    // x streamed to HBM (lanes past m write a scratch word: no branch)
-    const long long j = g * Wg + gs * 32 + lane;
-    const bool live = j < m;
-    step = live ? ld : 0;
-    out = live ? x + static_cast<long long>(r0 + L - 1) * ld + j : sink + lane;
-    if constexpr (PENT) {
-      __stcs(out - step, corr(L - 2, bs1));
-      __stcs(out, corr(L - 1, bs2));
-    } else {
-      __stcs(out, corr(L - 1, bs1));
-    }
-    out -= NH * step;
-    cur.load(tslot(p, CL - 1));  // the first backward chunk, loaded ahead
-  };
-
-  auto bwd_chunk = [&](int c, auto first) {
-    constexpr int kTop = decltype(first)::value ? kSpR - 1 - NH : kSpR - 1;  // skip the interface rows
-    cur.wait();
-    const B* bc = bk + c * kSpR;
-    double gv[kSpR];  // stage 1: left-coupling update (off the chain)
-#pragma unroll
-    for (int r = 0; r <= kTop; ++r) {
-      if constexpr (PENT) gv[r] = fma(-bc[r].f1, xl2, fma(-bc[r].f2, xl1, cur.get(r)));
-      else gv[r] = fma(-bc[r].f1, xl1, cur.get(r));
-    }
-#pragma unroll
-    for (int r = kTop; r >= 0; --r) {  // stage 2: one FMA per row on the chain
-      double v;
-      if constexpr (PENT) v = fma(-bc[r].g, bs1, fma(-bc[r].d, bs2, gv[r]));
-      else v = fma(-bc[r].c, bs1, gv[r]);
-      bs2 = bs1;
-      bs1 = v;
-      __stcs(out, corr(c * kSpR + r, v));
-      out -= step;
-    }
-  };
-
-  const long long my = (groups - blockIdx.x + gridDim.x - 1) / gridDim.x;
-  if (my > 0) halo_prefetch(blockIdx.x);
-  uint32_t p = 0;  // parity of the group being read
-  for (long long i = 0; i <= my; ++i, p ^= 1u) {
-    const long long g = blockIdx.x + i * gridDim.x;      // group read in this round (i < my)
-    const long long gp = g - gridDim.x;                   // group written in this round (i > 0)
-    // step kk: backward chunk CL-1-kk of gp, then forward chunk kk of g (same TMEM slot)
-    for (int kk = 0; kk < CL; ++kk) {
-      if (i > 0) {
-        const int c = CL - 1 - kk;
-        if (kk == 0) bwd_chunk(c, std::true_type{});
-        else bwd_chunk(c, std::false_type{});
-        if (c > 0) cur.load(tslot(p ^ 1u, c - 1));
-      }
-      if (i < my) {
-        if (CN && kk == 0 && i + 1 < my) {  // consume this group's halo, then fetch the next group's
-          fwd_chunk(kk, p, g);
-          halo_prefetch(g + gridDim.x);
-        } else {
-          fwd_chunk(kk, p, g);
+        for (int r = 0; r < kSpR; ++r) {
+          if constexpr (PENT) dv[r] = blk[r * 32] * fc[r].ia;
+          else dv[r] = blk[r * 32] * fc[r].m;
         }
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+      if (++slot == KB) {
+        slot = 0;
+        phase ^= 1u;
+      }
+#pragma unroll
+      for (int r = 0; r < kSpR; ++r) {  // stage 2: one FMA per row on the chain
+        const F f = fc[r];
+        double v;
+        if constexpr (PENT) {
+          v = fma(-f.b, fs1, fma(-f.e, fs2, dv[r]));
+          a1 = fma(f.p1, v, a1);
+        } else {
+          v = fma(-f.am, fs1, dv[r]);
+        }
+        a0 = fma(f.p0, v, a0);
+        fs2 = fs1;
+        fs1 = v;
+        buf.put(r, v);
+      }
+      buf.store(tslot(p, c));
+    };
+
+    auto corr = [&](int i, double v) {  // stored value of local row i (periodic correction)
+      if constexpr (!PER) return v;
+      else if constexpr (PENT) return fma(-zk[2 * i], t1, fma(-zk[2 * i + 1], t2, v));
+      else return fma(-zk[i], t1, v);
+    };
+
+    // interface of the group just read (xch parity p): its backward state
+    auto interface = [&](long long g, uint32_t p) {
+      double* xw = xch + (static_cast<size_t>(p) * kSpWarps + warp) * NQ * 32 + lane;
+      xw[0] = a0;
+      if constexpr (PENT) {
+        xw[32] = a1;
+        xw[64] = fma(-bk[L - 2].g, fs1, fs2);  // y_{L-2} = g_{L-2} - gamma_{L-2} g_{L-1}
+        xw[96] = fs1;                          // y_{L-1} = g_{L-1}
+      } else {
+        xw[32] = fs1;
+      }
+      fs1 = fs2 = a0 = a1 = 0.0;
+      if (CS == 1) {
+        asm volatile("bar.sync 1, %0;" ::"r"(kSpWarps * 32) : "memory");
+      } else {  // every warp of every CTA of the cluster has published its values
+        fence_cluster();
+        __syncwarp();
+        if (lane < CS) mbar_arrive_cluster(map_rank(smem_u32(&ibar[p]), static_cast<uint32_t>(lane)));
+        mbar_wait_cluster(&ibar[p], (iphase >> p) & 1u);
+        iphase ^= 1u << p;
+      }
+      // x interface unknowns needed here, streamed over the R y values:
+      // [own bottom NH | left bottom NH | (PER) first NH | last NH]
+      constexpr int NU = PER ? 4 * NH : 2 * NH;
+      int rows[NU];
+#pragma unroll
+      for (int h = 0; h < NU; ++h)
+        rows[h] = h < NH       ? (k - kb0 + 1) * NH + h
+                  : h < 2 * NH ? (k - kb0) * NH + (h - NH)
+                               : (Kc + 1) * NH + (h - 2 * NH);
+      double zu[NU];
+#pragma unroll
+      for (int h = 0; h < NU; ++h) zu[h] = 0.0;
+      const uint32_t xbase = smem_u32(xch + static_cast<size_t>(p) * kSpWarps * NQ * 32 + lane);
+      for (int kk = 0; kk < K; ++kk) {
+        double yv[NQ];
+        if (CS == 1) {
+          const double* src = xch + ((static_cast<size_t>(p) * kSpWarps + gs * K + kk) * NQ) * 32 + lane;
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) yv[q] = src[q * 32];
+        } else {
+          const uint32_t a = map_rank(xbase + static_cast<uint32_t>(((kk % kSpWarps) * NQ) * 32 * sizeof(double)),
+                                      static_cast<uint32_t>(kk / kSpWarps));
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) yv[q] = ld_cluster_f64(a + static_cast<uint32_t>(q * 32 * sizeof(double)));
+        }
+#pragma unroll
+        for (int h = 0; h < NU; ++h) {
+          const double* rr = srinv + static_cast<size_t>(rows[h]) * R + kk * NQ;
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) zu[h] = fma(rr[q], yv[q], zu[h]);
+        }
+      }
+      if (k == 0) {  // no left neighbour
+#pragma unroll
+        for (int h = NH; h < 2 * NH; ++h) zu[h] = 0.0;
+      }
+      if constexpr (PENT) {
+        bs1 = zu[0];  // x_{L-2}
+        bs2 = zu[1];  // x_{L-1}
+        xl2 = zu[2];  // x_{s-2}
+        xl1 = zu[3];  // x_{s-1}
+      } else {
+        bs1 = zu[0];  // x_{L-1}
+        xl1 = zu[1];  // x_{s-1}
+      }
+      if constexpr (PER) {
+        if constexpr (PENT) {  // periodic.cpp:189-194 (fast-mode rounding)
+          const double w1 = zu[4] - zu[7], w2 = zu[5] - zu[6];
+          t1 = fma(per.c[0], w1, per.c[1] * w2);
+          t2 = fma(per.c[2], w1, per.c[3] * w2);
+        } else {  // periodic.cpp:80
+          t1 = fma(per.c[0], zu[3], zu[2]) * per.c[1];
+        }
+      }
+      // x streamed to HBM (lanes past m write a scratch word: no branch)
+      const long long j = g * Wg + gs * 32 + lane;
+      const bool live = j < m;
+      step = live ? ld : 0;
+      out = live ? x + static_cast<long long>(r0 + L - 1) * ld + j : sink + lane;
+      if constexpr (PENT) {
+        __stcs(out - step, corr(L - 2, bs1));
+        __stcs(out, corr(L - 1, bs2));
+      } else {
+        __stcs(out, corr(L - 1, bs1));
+      }
+      out -= NH * step;
+      cur.load(tslot(p, CL - 1));  // the first backward chunk, loaded ahead
+    };
+
+    auto bwd_chunk = [&](int c, auto first) {
+      constexpr int kTop = decltype(first)::value ? kSpR - 1 - NH : kSpR - 1;  // skip the interface rows
+      cur.wait();
+      const B* bc = bk + c * kSpR;
+      double gv[kSpR];  // stage 1: left-coupling update (off the chain)
+#pragma unroll
+      for (int r = 0; r <= kTop; ++r) {
+        if constexpr (PENT) gv[r] = fma(-bc[r].f1, xl2, fma(-bc[r].f2, xl1, cur.get(r)));
+        else gv[r] = fma(-bc[r].f1, xl1, cur.get(r));
+      }
+#pragma unroll
+      for (int r = kTop; r >= 0; --r) {  // stage 2: one FMA per row on the chain
+        double v;
+        if constexpr (PENT) v = fma(-bc[r].g, bs1, fma(-bc[r].d, bs2, gv[r]));
+        else v = fma(-bc[r].c, bs1, gv[r]);
+        bs2 = bs1;
+        bs1 = v;
+        __stcs(out, corr(c * kSpR + r, v));
+        out -= step;
+      }
+    };
+
+    const long long my = (groups - cid + ncl - 1) / ncl;
+    if (my > 0) halo_prefetch(cid);
+    uint32_t p = 0;  // parity of the group being read
+    for (long long i = 0; i <= my; ++i, p ^= 1u) {
+      const long long g = cid + i * ncl;  // group read in this round (i < my)
+      // step kk: backward chunk CL-1-kk of the previous group, then forward
+      // chunk kk of g (same TMEM slot)
+      for (int kk = 0; kk < CL; ++kk) {
+        if (i > 0) {
+          const int c = CL - 1 - kk;
+          if (kk == 0) bwd_chunk(c, std::true_type{});
+          else bwd_chunk(c, std::false_type{});
+          if (c > 0) cur.load(tslot(p ^ 1u, c - 1));
+        }
+        if (i < my) {
+          fwd_chunk(kk, p, g);
+          if (CN && kk == 0 && i + 1 < my) halo_prefetch(g + ncl);  // this group's halo is consumed
+        }
+      }
+      if (i < my) interface(g, p);
     }
-    if (i < my) interface(g, p);
-    (void)gp;
+    tmem_fence_before();
+    asm volatile("bar.sync 1, %0;" ::"r"(kSpWarps * 32) : "memory");
+    if (warp == 0) {
+      tmem_fence_after();
+      tmem_dealloc_512(tmem_base_s);
+    }
   }
-  tmem_fence_before();
-  asm volatile("bar.sync 1, %0;" ::"r"(kSpWarps * 32) : "memory");
-  if (warp == 0) {
-    tmem_fence_after();
-    tmem_dealloc_512(tmem_base_s);
-  }
+  // a CTA's shared memory must outlive the cluster's remote reads of it
+  if (CS > 1) cluster_sync_all();
 }
 
 }  // namespace dev

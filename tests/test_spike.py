@@ -60,12 +60,14 @@ def _dev_solve(lib, torch, factor, rhs, ld=None):
     return out[:, :m], launches
 
 
-@pytest.mark.parametrize("n", [320, 512, 768, 1024])
+@pytest.mark.parametrize("n", [320, 512, 768, 1024, 1536, 2048, 4096])
 def test_spike_within_tolerance(lib, oracle, cuda_device, n):
+    """K <= 8 blocks in one CTA; K = 16 / 32 blocks across a cluster of
+    2 / 4 CTAs (interface values through distributed shared memory)."""
     torch = cuda_device
     lib.tune("SPIKE", "1")
     rng = np.random.default_rng(n)
-    K = {320: 4, 512: 4, 768: 8, 1024: 8}[n]
+    K = {320: 4, 512: 4, 768: 8, 1024: 8, 1536: 16, 2048: 16, 4096: 32}[n]
     for m, ld in [(38, 40), (64, 64), (300, 302)]:
         rhs = rng.uniform(-1, 1, (n, m))
         cases = [("tri", bs.TriFactor, _random_tri(rng, n)), ("diff", bs.TriFactor, bs.diffusion_bands(1.0, n)),
@@ -86,6 +88,8 @@ def test_spike_planner_threshold(lib, cuda_device):
     sms = cuda_device.cuda.get_device_properties(0).multi_processor_count
     assert lib.describe_plan(1, 1024, 1 << 20).startswith("spike K=8")
     assert lib.describe_plan(0, 512, 1 << 20).startswith("spike K=4")
+    assert lib.describe_plan(0, 2048, 1 << 20).startswith("spike K=16")
+    assert lib.describe_plan(1, 4096, 1 << 20).startswith("spike K=32")
     assert not lib.describe_plan(1, 1024, sms * 32 - 2).startswith("spike")
     assert not lib.describe_plan(1, 1024, (1 << 20) - 1, 1 << 20).startswith("spike")  # odd batch width
     assert not lib.describe_plan(1, 1024, 1 << 20, (1 << 20) + 1).startswith("spike")
@@ -139,7 +143,7 @@ def test_spike_configs4_column_sample(lib, oracle, cuda_device):
     assert per_system_max_rel(got, want) <= TOL_F64
 
 
-@pytest.mark.parametrize("n", [320, 512, 1024])
+@pytest.mark.parametrize("n", [320, 512, 1024, 2048, 4096])
 def test_spike_periodic_fused_within_tolerance(lib, oracle, cuda_device, n):
     """Cyclic systems: the Woodbury correction rides in the spike kernel's
     backward sweep (its coefficients need x_0, x_1, x_{n-2}, x_{n-1}, which
@@ -168,7 +172,7 @@ def test_spike_periodic_fused_within_tolerance(lib, oracle, cuda_device, n):
             assert per_system_max_rel(out[:, :m], want) <= TOL_F64, (n, m, ld, bands)
 
 
-@pytest.mark.parametrize("n", [320, 512, 1024])
+@pytest.mark.parametrize("n", [320, 512, 1024, 4096])
 def test_spike_cn_step_within_tolerance(lib, oracle, cuda_device, n):
     """Crank-Nicolson step u_new = A^-1 (B u) in one spike launch: the
     explicit periodic stencil (pde.cpp:73-114) is formed from the ring boxes
