@@ -454,7 +454,9 @@ int bandsolve_get_devices(int* devices, int capacity);
  * SV, SRC, SSEG, TM8, TMEM, SSTAG (stream plan: group width, smem tail rows,
  * b / reload ring slots, L2 prefetch distance, systems per lane, recomputed
  * rows, recompute segment chunks, TMEM with 5..8 warps, TMEM on/off, start
- * stagger); PARTITION (0|1), PART_K; CN_UNFUSED, PERIODIC_UNFUSED,
+ * stagger); SPIKE (0|1: the one-pass partitioned kernel, fast mode),
+ * SPIKE_K (its block count), NO_PDL (flag: no programmatic dependent
+ * launch); PARTITION (0|1), PART_K; CN_UNFUSED, PERIODIC_UNFUSED,
  * ADI_UNFUSED, ADI_FUSE_PENT (flags: set = on); HOST_CHUNK_MIB (host-batch
  * staging chunk); L2_SETASIDE (1: grow the device's persisting-L2 limit to
  * cover the spill scratch; process-wide state, off by default).

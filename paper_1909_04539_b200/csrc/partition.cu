@@ -933,13 +933,22 @@ bandsolve_status spike_solve_device(const Factor& f, double* x, std::size_t n, s
   cfg.blockDim = dim3(32 * (dev::kSpWarps + 1), 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = static_cast<unsigned>(CS);
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (!tune_flag("NO_PDL")) {  // the prologue may overlap the previous kernel (griddepcontrol.wait inside)
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (CS > 1) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = static_cast<unsigned>(CS);
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = CS > 1 ? 1 : 0;
+  cfg.numAttrs = na;
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, map, x, N, static_cast<long long>(m), static_cast<long long>(ld), K,
                                      p->L, KB, PD, groups, static_cast<const void*>(blob), rinv, sinks[device], sp);
   note_launches(1);

@@ -252,6 +252,12 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
   __syncthreads();
   tmem_fence_after();
   if (CS > 1) cluster_sync_all();  // every CTA's barriers are initialised before remote arrivals
+  // Programmatic dependent launch: the prologue above (records, barriers,
+  // TMEM) overlaps the previous kernel's tail; the batch itself is touched
+  // only after the previous grid has completed and flushed. The next launch
+  // may be scheduled as soon as SMs free up.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   // block / group slot of warp w, and the global first row of its block
   auto blk_of = [&](int w) { return CS > 1 ? kb0 + w : w % K; };

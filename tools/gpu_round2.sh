@@ -21,6 +21,10 @@ if [ -z "${SKIP_SWEEP:-}" ]; then
       st=30; [ $cfg = c5 ] && st=5
       timeout 300 python bench.py --config $cfg --mode $mode --no-cpu --no-e2e --steps $st --warmup 3 >> gpurun_out/bench_sweep.jsonl 2>> gpurun_out/bench_err.log
     done
+    for nn in 64 128 256 1024 2048 4096; do  # configs[2]: tri, 2^20 systems, N sweep
+      timeout 300 python bench.py --config tri512 --n $nn --m 1048576 --mode $mode --no-cpu --no-e2e --steps 10 --warmup 3 >> gpurun_out/bench_sweep.jsonl 2>> gpurun_out/bench_err.log
+      timeout 300 python bench.py --config tri512 --n $nn --m 1048576 --f32 --mode $mode --no-cpu --no-e2e --steps 10 --warmup 3 >> gpurun_out/bench_sweep.jsonl 2>> gpurun_out/bench_err.log
+    done
     timeout 300 python bench.py --config tri512 --f32 --mode $mode --no-cpu --steps 30 --warmup 3 >> gpurun_out/bench_sweep.jsonl 2>> gpurun_out/bench_err.log
     for extra in "--config pent512 --periodic" "--config tri512 --periodic" "--config pent512 --cn" "--config tri512 --cn" "--config c4tri" "--config c4pent"; do
       timeout 300 python bench.py $extra --mode $mode --no-cpu --no-e2e --steps 20 --warmup 3 >> gpurun_out/bench_sweep.jsonl 2>> gpurun_out/bench_err.log
@@ -30,7 +34,7 @@ fi
 if [ -z "${SKIP_NCU:-}" ]; then
   timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 40 --csv \
      --log-file gpurun_out/launches_default.csv python bench.py --steps 3 --warmup 3 --no-cpu --no-e2e > gpurun_out/ncu_launch.log 2>&1
-  for spec in "c5s fast sweep_spike" "pent512 fast sweep_spike" "tri512 fast sweep_spike" "pent512 exact sweep_stream" "c2 exact sweep_stream" "c2 fast sweep_spike"; do
+  for spec in "c5s fast sweep_spike" "pent512 fast sweep_spike" "tri512 fast sweep_spike" "pent512 exact sweep_stream" "c2 exact sweep_stream" "c2 fast sweep_spike" "c5s exact sweep_stream"; do
     set -- $spec
     tag=${1}_${2}
     timeout 900 ncu --set full --clock-control none --import-source on -k regex:$3 -s 3 -c 1 \
