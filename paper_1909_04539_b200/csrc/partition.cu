@@ -755,6 +755,24 @@ PartPlan* cached_plan(const Factor& f, int K) {
   return p->ok ? p : nullptr;
 }
 
+}  // namespace
+
+// A per-device scratch word per lane: lanes past the batch edge store there
+// (branch-free stores in the spike and pipe kernels). nullptr on failure.
+double* dead_lane_sink(int device) {
+  static double* sinks[64] = {};
+  static std::mutex mu;
+  if (device < 0 || device >= 64) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!sinks[device] && cudaMalloc(reinterpret_cast<void**>(&sinks[device]), 32 * sizeof(double)) != cudaSuccess) {
+    cudaGetLastError();
+    sinks[device] = nullptr;
+  }
+  return sinks[device];
+}
+
+namespace {
+
 // CTAs per cluster for K blocks (8 blocks per CTA beyond one CTA)
 int spike_cluster(int K) { return K > dev::kSpWarps ? K / dev::kSpWarps : 1; }
 
@@ -914,17 +932,8 @@ bandsolve_status spike_solve_device(const Factor& f, double* x, std::size_t n, s
     if (bit) attr_set.fetch_or(bit, std::memory_order_relaxed);
   }
   // lanes past the batch edge write their values here (branch-free stores)
-  static double* sinks[64] = {};
-  if (device >= 64) return BANDSOLVE_OK;
-  {
-    static std::mutex mu;
-    std::lock_guard<std::mutex> lock(mu);
-    if (!sinks[device] && cudaMalloc(reinterpret_cast<void**>(&sinks[device]), 32 * sizeof(double)) != cudaSuccess) {
-      cudaGetLastError();
-      sinks[device] = nullptr;
-      return fail(BANDSOLVE_ERR_INTERNAL, "spike scratch");
-    }
-  }
+  double* sink = dead_lane_sink(device);
+  if (!sink) return fail(BANDSOLVE_ERR_INTERNAL, "spike scratch");
   const int active = spike_active_clusters(reinterpret_cast<const void*>(kern), CS, smem, sms);
   if (active <= 0) return BANDSOLVE_OK;  // the cluster does not fit: the sweep plans take it
   const unsigned grid = static_cast<unsigned>(CS * std::min<long long>(active, groups));
@@ -950,7 +959,7 @@ bandsolve_status spike_solve_device(const Factor& f, double* x, std::size_t n, s
   cfg.attrs = attr;
   cfg.numAttrs = na;
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, map, x, N, static_cast<long long>(m), static_cast<long long>(ld), K,
-                                     p->L, KB, PD, groups, static_cast<const void*>(blob), rinv, sinks[device], sp);
+                                     p->L, KB, PD, groups, static_cast<const void*>(blob), rinv, sink, sp);
   note_launches(1);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return fail(BANDSOLVE_ERR_INTERNAL, std::string("spike launch: ") + cudaGetErrorString(e));

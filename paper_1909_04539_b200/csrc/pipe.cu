@@ -1,0 +1,104 @@
+// Host side of the pipelined on-chip sequential sweep (sweep_pipe.cuh):
+// plan (compute warps, ring depth) and launch.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <climits>
+#include <cstdint>
+
+#include "internal.hpp"
+#include "sweep_pipe.cuh"
+
+namespace bsb {
+
+bool encode_tile_map(CUtensorMap* map, void* x, std::size_t elem, long long n, long long m, long long ld,
+                     int box_w, int box_r);   // solve.cu
+cudaError_t allow_max_smem(const void* kern);  // solve.cu
+std::size_t max_smem_per_block();              // solve.cu
+double* dead_lane_sink(int device);            // partition.cu
+
+namespace {
+
+std::size_t fwd_rec(bool pent) { return pent ? sizeof(dev::PentFwd<double>) : sizeof(dev::TriFwd<double>); }
+std::size_t bwd_rec(bool pent) { return pent ? sizeof(dev::PentBwd<double>) : sizeof(double); }
+
+}  // namespace
+
+// Compute warps (2..4) of the pipelined plan for this shape, 0 when it does
+// not apply; *kb receives the ring depth.
+int pipe_warps(std::size_t n, std::size_t m, std::size_t ld, const void* x, bool pent, int sms, int* kb) {
+  const long long sel = tune_int("PIPE", -1);  // 0: never, 1: whenever it applies
+  if (sel == 0 || tune_flag("PLAN")) return 0;
+  if (n % dev::kPpR != 0 || n < 2 * dev::kPpR || n > 2u * dev::kPpTmemRows) return 0;
+  if (reinterpret_cast<uintptr_t>(x) % 16 != 0 || ld % 2 != 0 || m % 2 != 0 ||
+      m > static_cast<std::size_t>(INT_MAX) / 2)
+    return 0;
+  const std::size_t cap = max_smem_per_block();
+  for (int P = 4; P >= 2; --P) {
+    if (sel != 1 && m < static_cast<std::size_t>(sms) * 32 * P) continue;  // a full wave of groups
+    const int kmax = static_cast<int>(tune_int("PKB", 10));  // ring slots (tuning)
+    for (int k = kmax; k >= 3; --k)
+      if (dev::PipeLayout::make(static_cast<int>(n), P, k, fwd_rec(pent), bwd_rec(pent)).total <= cap) {
+        *kb = k;
+        return P;
+      }
+  }
+  return 0;
+}
+
+bandsolve_status pipe_solve_device(bool pent, bool fast, const void* fwd, const void* bwd, double* x, std::size_t n,
+                                   std::size_t m, std::size_t ld, void* stream, int sms, bool* done) {
+  *done = false;
+  int KB = 0;
+  const int P = pipe_warps(n, m, ld, x, pent, sms, &KB);
+  if (P == 0) return BANDSOLVE_OK;
+  int device = 0;
+  if (cudaGetDevice(&device) != cudaSuccess) {
+    cudaGetLastError();
+    return BANDSOLVE_OK;
+  }
+  double* sink = dead_lane_sink(device);
+  if (!sink) return fail(BANDSOLVE_ERR_INTERNAL, "pipe scratch");
+  CUtensorMap map;
+  if (!encode_tile_map(&map, x, sizeof(double), static_cast<long long>(n), static_cast<long long>(m),
+                       static_cast<long long>(ld), 32, dev::kPpR))
+    return BANDSOLVE_OK;
+  using Kern = decltype(&dev::sweep_pipe<true, false, 2>);
+#define BSB_PIPE_SET(PP)                                                                    \
+  {{dev::sweep_pipe<false, false, PP>, dev::sweep_pipe<false, true, PP>},                  \
+   {dev::sweep_pipe<true, false, PP>, dev::sweep_pipe<true, true, PP>}}
+  static const Kern kerns[3][2][2] = {BSB_PIPE_SET(2), BSB_PIPE_SET(3), BSB_PIPE_SET(4)};
+#undef BSB_PIPE_SET
+  const Kern kern = kerns[P - 2][pent][fast];
+  static std::atomic<uint64_t> configured[12];
+  std::atomic<uint64_t>& done_attr = configured[(P - 2) * 4 + (pent ? 2 : 0) + (fast ? 1 : 0)];
+  const uint64_t bit = device < 64 ? (1ull << device) : 0;
+  if (!(bit && (done_attr.load(std::memory_order_relaxed) & bit))) {
+    if (cudaError_t e = allow_max_smem(reinterpret_cast<const void*>(kern)); e != cudaSuccess)
+      return fail(BANDSOLVE_ERR_INTERNAL, std::string("pipe attributes: ") + cudaGetErrorString(e));
+    if (bit) done_attr.fetch_or(bit, std::memory_order_relaxed);
+  }
+  const int Wg = 32 * P;
+  const long long groups = (static_cast<long long>(m) + Wg - 1) / Wg;
+  const std::size_t smem = dev::PipeLayout::make(static_cast<int>(n), P, KB, fwd_rec(pent), bwd_rec(pent)).total;
+  const int PD = static_cast<int>(tune_int("SPD", 4));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(std::min<long long>(sms, groups)), 1, 1);
+  cfg.blockDim = dim3(32 * (P + 1), 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = static_cast<cudaStream_t>(stream);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = tune_flag("NO_PDL") ? 0 : 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, map, x, static_cast<int>(n), static_cast<long long>(m),
+                                     static_cast<long long>(ld), KB, PD, groups, fwd, bwd, sink);
+  note_launches(1);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(BANDSOLVE_ERR_INTERNAL, std::string("pipe launch: ") + cudaGetErrorString(e));
+  *done = true;
+  return BANDSOLVE_OK;
+}
+
+}  // namespace bsb

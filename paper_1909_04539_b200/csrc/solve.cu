@@ -1134,7 +1134,12 @@ bandsolve_status describe_plan(Kind kind, std::size_t n, std::size_t m, std::siz
   char buf[256];
   const int KS = f32 ? 0 : spike_blocks(n, m, ld, kProbe, sms, pent);
   const int K = f32 ? 0 : partition_blocks(n, m, sms, pent);
-  if (KS > 0)
+  int pkb = 0;
+  const int PP = (f32 || KS > 0 || K > 0) ? 0 : pipe_warps(n, m, ld, kProbe, pent, sms, &pkb);
+  if (PP > 0)
+    std::snprintf(buf, sizeof buf, "pipe Wg=%d warps=%d+1 tmem=%zu smem-rows=%zu ring=%d (all rows on chip, 1 launch)",
+                  32 * PP, PP, std::min<std::size_t>(n, 256), n > 256 ? n - 256 : 0, pkb);
+  else if (KS > 0)
     std::snprintf(buf, sizeof buf, "spike K=%d blocks of %zu rows, interface system %d, 1 launch (TMEM-resident blocks%s)",
                   KS, n / KS, (pent ? 4 : 2) * KS, KS > 8 ? (KS == 16 ? ", clusters of 2 CTAs" : ", clusters of 4 CTAs") : "");
   else if (K > 0)
@@ -1181,6 +1186,12 @@ bandsolve_status solve_device(const Factor& f, void* x, bool f32, std::size_t n,
     st = spike_solve_device(f, static_cast<double*>(x), n, m, ld, stream, sms, &done);
     if (st != BANDSOLVE_OK || done) return st;
     st = partition_solve_device(f, static_cast<double*>(x), n, m, ld, stream, sms, &done);
+    if (st != BANDSOLVE_OK || done) return st;
+  }
+  if (!f32) {  // every forward intermediate on chip, pipelined across groups
+    bool done = false;
+    st = pipe_solve_device(pent, fast, df->fwd[0][q], df->bwd[0][q], static_cast<double*>(x), n, m, ld, stream, sms,
+                           &done);
     if (st != BANDSOLVE_OK || done) return st;
   }
   const Plan plan = choose_plan(n, m, ld, f32 ? 4 : 8, x, pent, fast, sms);

@@ -1,0 +1,276 @@
+// Pipelined sequential shared-LHS sweep, every forward intermediate on chip
+// (sm_100a). The exact-mode kernel for systems of up to 512 rows.
+//
+// The exact mode must follow the reference's operation order
+// (tri_solver.cpp:25-47, pent_solver.cpp:19-62): one sequential recurrence
+// per system, so a system's n forward intermediates stay alive until its
+// backward sweep, and the streaming kernel (sweep_stream.cuh) spills the
+// rows that do not fit on chip to L2 (~20% throughput for any spill).
+//
+// Here each lane keeps ALL n rows of its system on chip — the first 256 in
+// its TMEM lane (one lane quadrant per compute warp), the rest in shared
+// memory — and the warp software-pipelines across groups exactly like
+// sweep_spike.cuh: in step k it runs backward row chunk CL-1-k of group g and
+// forward row chunk k of group g + 1 in ONE 16-row loop (two independent
+// dependency chains interleaved in the instruction stream), and the forward
+// chunk is stored into the storage slot the backward chunk has just been
+// read from (slot p ? CL-1-k : k for group parity p), so the storage per lane
+// stays n rows while both chains run. HBM traffic: read b once, write x once.
+//
+// P compute warps (32 P systems per group) + one TMA producer warp. The row
+// formulas are sweep_kernels.cuh's (exact: bitwise equal to the reference).
+#pragma once
+
+#include "sweep_spike.cuh"
+
+namespace bsb {
+namespace dev {
+
+constexpr int kPpR = 16;      // rows per chunk (one TMA box {32 x 16} per warp)
+constexpr int kPpTmemRows = 256;  // rows per lane in TMEM (512 columns of fp64)
+
+struct PipeLayout {
+  size_t fwd_off, bwd_off, stor_off, ring_off, bar_off, total;
+  // n rows (multiple of 16), P compute warps, KB ring slots
+  __host__ __device__ static PipeLayout make(int n, int P, int KB, size_t fwd_rec, size_t bwd_rec) {
+    PipeLayout L{};
+    const int CL = n / kPpR;
+    const int TT = CL < kPpTmemRows / kPpR ? CL : kPpTmemRows / kPpR;
+    L.fwd_off = 0;
+    L.bwd_off = align128(static_cast<size_t>(n) * fwd_rec);
+    L.stor_off = L.bwd_off + align128(static_cast<size_t>(n) * bwd_rec);
+    // shared-memory slots: [CL - TT][P warps][16 rows][32 lanes]
+    L.ring_off = L.stor_off + static_cast<size_t>(CL - TT) * P * kPpR * 32 * sizeof(double);
+    L.bar_off = L.ring_off + static_cast<size_t>(KB) * P * kPpR * 32 * sizeof(double);
+    L.total = L.bar_off + static_cast<size_t>(2 * KB + 1) * sizeof(uint64_t);
+    return L;
+  }
+};
+
+// One forward row (chain state fs1/fs2) and one backward row (bs1/bs2) of
+// two different groups, written as interleaved stages so that each stage
+// issues one operation of each chain: the chain-independent parts first
+// (b - eps g2, delta x2), then the three dependent operations of each
+// recurrence side by side. The operation order of each recurrence is the
+// reference's (exact) or the FMA form (fast).
+template <bool PENT, bool FAST, bool FW, bool BW>
+__device__ __forceinline__ void pipe_rows(const typename Recs<double, PENT>::Fwd& fr, double d, double& fs1,
+                                          double& fs2, double& fv, const typename Recs<double, PENT>::Bwd& br,
+                                          double g, double& bs1, double& bs2, double& bv) {
+  if constexpr (FAST) {
+    if constexpr (FW) {
+      if constexpr (PENT) fv = fma_rn(-fr.b, fs1, fma_rn(-fr.e, fs2, mul_rn(d, fr.ia)));
+      else fv = fma_rn(-fr.a, fs1, mul_rn(d, fr.m));
+    }
+    if constexpr (BW) {
+      if constexpr (PENT) bv = fma_rn(-br.g, bs1, fma_rn(-br.d, bs2, g));
+      else bv = fma_rn(-br, bs1, g);
+    }
+  } else if constexpr (PENT) {
+    double tf = 0.0, xb = 0.0, uf = 0.0, ub = 0.0;
+    if constexpr (FW) tf = sub_rn(d, mul_rn(fr.e, fs2));   // f - eps g2 (g2: one row old)
+    if constexpr (BW) xb = mul_rn(br.d, bs2);              // delta x2 (x2: one row old)
+    if constexpr (FW) uf = mul_rn(fr.b, fs1);              // chains: one op of each per stage
+    if constexpr (BW) ub = mul_rn(br.g, bs1);
+    if constexpr (FW) uf = sub_rn(tf, uf);
+    if constexpr (BW) ub = add_rn(ub, xb);
+    if constexpr (FW) fv = mul_rn(uf, fr.ia);              // ((f - eps g2) - beta g1) * ia
+    if constexpr (BW) bv = sub_rn(g, ub);                  // g - (gamma x1 + delta x2)
+  } else {
+    double uf = 0.0, ub = 0.0;
+    if constexpr (FW) uf = mul_rn(fr.a, fs1);
+    if constexpr (BW) ub = mul_rn(br, bs1);
+    if constexpr (FW) uf = sub_rn(d, uf);
+    if constexpr (BW) bv = sub_rn(g, ub);                  // dhat - chat next
+    if constexpr (FW) fv = mul_rn(uf, fr.m);               // (d - a prev) * m
+  }
+  if constexpr (FW) {
+    fs2 = fs1;
+    fs1 = fv;
+  }
+  if constexpr (BW) {
+    bs2 = bs1;
+    bs1 = bv;
+  }
+}
+
+template <bool PENT, bool FAST, int P>
+__global__ void __launch_bounds__(32 * (P + 1), 1)
+    sweep_pipe(const __grid_constant__ CUtensorMap map_b, double* __restrict__ x, int n, long long m, long long ld,
+               int KB, int PD, long long groups, const void* __restrict__ fwd_g, const void* __restrict__ bwd_g,
+               double* __restrict__ sink) {
+  using FwdR = typename Recs<double, PENT>::Fwd;
+  using BwdR = typename Recs<double, PENT>::Bwd;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const PipeLayout Ly = PipeLayout::make(n, P, KB, sizeof(FwdR), sizeof(BwdR));
+  const FwdR* sf = reinterpret_cast<const FwdR*>(smem + Ly.fwd_off);
+  const BwdR* sb = reinterpret_cast<const BwdR*>(smem + Ly.bwd_off);
+  double* stor = reinterpret_cast<double*>(smem + Ly.stor_off);
+  double* ring = reinterpret_cast<double*>(smem + Ly.ring_off);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Ly.bar_off);
+  uint64_t* empty = full + KB;
+  uint32_t& tmem_base_s = *reinterpret_cast<uint32_t*>(empty + KB);
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  constexpr int kBox = kPpR * 32;
+  constexpr int kChunk = P * kBox;
+  constexpr int Wg = 32 * P;
+  const int CL = n / kPpR;
+  const int TT = CL < kPpTmemRows / kPpR ? CL : kPpTmemRows / kPpR;  // chunks per lane in TMEM
+
+  {  // factor records -> smem (16-byte words)
+    const uint4* sfw = static_cast<const uint4*>(fwd_g);
+    const uint4* sbw = static_cast<const uint4*>(bwd_g);
+    uint4* df = reinterpret_cast<uint4*>(smem + Ly.fwd_off);
+    uint4* db = reinterpret_cast<uint4*>(smem + Ly.bwd_off);
+    const int wf = static_cast<int>((static_cast<size_t>(n) * sizeof(FwdR) + 15) / 16);
+    const int wb = static_cast<int>((static_cast<size_t>(n) * sizeof(BwdR) + 15) / 16);
+    for (int i = threadIdx.x; i < wf; i += blockDim.x) df[i] = sfw[i];
+    for (int i = threadIdx.x; i < wb; i += blockDim.x) db[i] = sbw[i];
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < KB; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], P);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc_512(&tmem_base_s);
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+
+  if (warp == P) {  // ---- producer: b chunks through the ring (one box per warp)
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      const long long my_groups = (groups - blockIdx.x + gridDim.x - 1) / gridDim.x;
+      const long long total = my_groups * CL;
+      long long pf = 0;
+      int slot = 0;
+      uint32_t phase = 0;
+      for (long long t = 0; t < total; ++t) {
+        for (; pf < total && pf < t + PD; ++pf) {
+          const long long gi = pf / CL;
+          const int c = static_cast<int>(pf - gi * CL);
+          const int c0 = static_cast<int>((blockIdx.x + gi * gridDim.x) * Wg);
+          for (int w = 0; w < P; ++w) tma_prefetch_2d(&map_b, c0 + w * 32, c * kPpR);
+        }
+        if (t >= KB) mbar_wait(&empty[slot], phase ^ 1u);
+        const long long gi = t / CL;
+        const int c = static_cast<int>(t - gi * CL);
+        const int c0 = static_cast<int>((blockIdx.x + gi * gridDim.x) * Wg);
+        mbar_expect_tx(&full[slot], kChunk * sizeof(double));
+        for (int w = 0; w < P; ++w)
+          tma_load_2d(ring + slot * kChunk + w * kBox, &map_b, c0 + w * 32, c * kPpR, &full[slot], pol);
+        if (++slot == KB) {
+          slot = 0;
+          phase ^= 1u;
+        }
+      }
+    }
+    return;
+  }
+
+  // ---- compute warps: lane = one system of the warp's 32
+  const uint32_t tlane = tmem_base_s + (static_cast<uint32_t>(32 * warp) << 16);
+  // storage slot of chunk c of a group with parity p
+  auto sidx = [&](uint32_t p, int c) { return p ? CL - 1 - c : c; };
+  auto slot_smem = [&](int s) { return stor + (static_cast<size_t>(s - TT) * P + warp) * kBox + lane; };
+  int slot = 0;
+  uint32_t phase = 0;
+  double fs1 = 0.0, fs2 = 0.0;  // forward state (group being read)
+  double bs1 = 0.0, bs2 = 0.0;  // backward state (group being written)
+  long long step = 0;
+  double* out = sink + lane;
+  TPiece<double> cur;  // the backward chunk's 16 forward values
+
+  // load the backward chunk's values from slot s (TMEM: asynchronous, waited in step())
+  auto bwd_load = [&](int s) {
+    if (s < TT) {
+      cur.load(tlane + static_cast<uint32_t>(s * TPiece<double>::kWords));
+    } else {
+      const double* q = slot_smem(s);
+#pragma unroll
+      for (int r = 0; r < kPpR; ++r) cur.put(r, q[r * 32]);
+    }
+  };
+
+  // One step: forward chunk kk of the group read (FW) and backward chunk c of
+  // the group written (BW), rows interleaved; both use storage slot s.
+  auto run_step = [&](int kk, int c, int s, auto fw, auto bw) {
+    constexpr bool FW = decltype(fw)::value, BW = decltype(bw)::value;
+    const double* blk = nullptr;
+    if constexpr (FW) {
+      mbar_wait(&full[slot], phase);
+      blk = ring + slot * kChunk + warp * kBox + lane;
+    }
+    if constexpr (BW) {
+      if (s < TT) cur.wait();
+    }
+    const FwdR* fc = sf + kk * kPpR;
+    const BwdR* bc = sb + c * kPpR;
+    TPiece<double> buf;
+#pragma unroll
+    for (int q = 0; q < kPpR; ++q) {
+      const int r = kPpR - 1 - q;
+      double fv = 0.0, bv = 0.0;
+      pipe_rows<PENT, FAST, FW, BW>(fc[q], FW ? blk[q * 32] : 0.0, fs1, fs2, fv, bc[r], BW ? cur.get(r) : 0.0, bs1,
+                                    bs2, bv);
+      if constexpr (FW) buf.put(q, fv);
+      if constexpr (BW) {
+        __stcs(out, bv);
+        out -= step;
+      }
+    }
+    if constexpr (FW) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+      if (++slot == KB) {
+        slot = 0;
+        phase ^= 1u;
+      }
+      if (s < TT) {
+        buf.store(tlane + static_cast<uint32_t>(s * TPiece<double>::kWords));
+      } else {
+        double* q = slot_smem(s);
+#pragma unroll
+        for (int r = 0; r < kPpR; ++r) q[r * 32] = buf.get(r);
+      }
+    }
+  };
+
+  const long long my = (groups - blockIdx.x + gridDim.x - 1) / gridDim.x;
+  uint32_t p = 0;  // parity of the group being read
+  for (long long i = 0; i <= my; ++i, p ^= 1u) {
+    const long long g = blockIdx.x + i * gridDim.x;  // group read in this round (i < my)
+    if (i > 0) {  // the group read last round is written this round: x from row n-1 down
+      const long long j = (g - gridDim.x) * Wg + warp * 32 + lane;
+      const bool live = j < m;
+      step = live ? ld : 0;
+      out = live ? x + static_cast<long long>(n - 1) * ld + j : sink + lane;
+      bs1 = bs2 = 0.0;
+      bwd_load(sidx(p ^ 1u, CL - 1));
+    }
+    fs1 = fs2 = 0.0;
+    for (int kk = 0; kk < CL; ++kk) {
+      const int c = CL - 1 - kk;
+      const int s = sidx(p, kk);  // == sidx(p ^ 1, c)
+      if (i > 0 && i < my) run_step(kk, c, s, std::true_type{}, std::true_type{});
+      else if (i < my) run_step(kk, c, s, std::true_type{}, std::false_type{});
+      else run_step(kk, c, s, std::false_type{}, std::true_type{});
+      if (i > 0 && c > 0) bwd_load(sidx(p ^ 1u, c - 1));  // next backward chunk (a different slot)
+    }
+    __syncwarp();  // this warp's smem slot stores are visible to its own next-round loads
+  }
+  tmem_fence_before();
+  asm volatile("bar.sync 1, %0;" ::"r"(P * 32) : "memory");
+  if (warp == 0) {
+    tmem_fence_after();
+    tmem_dealloc_512(tmem_base_s);
+  }
+}
+
+}  // namespace dev
+}  // namespace bsb

@@ -1,0 +1,90 @@
+"""Pipelined on-chip sequential sweep (csrc/sweep_pipe.cuh).
+
+Every forward intermediate stays on chip (TMEM + shared memory) and each warp
+interleaves the backward sweep of one group with the forward sweep of the
+next in the same storage slots. In exact mode it must reproduce the
+reference's bits (tri_solver.cpp:25-47, pent_solver.cpp:19-62) for every
+shape it takes — one and several TMEM-only / TMEM + smem chunk counts, ragged
+groups (masked stores), padded pitches, 2..4 compute warps — and stay within
+1e-12 in fast mode. The tuning key PIPE=1 forces it below its many-systems
+threshold; =0 disables it.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle.oracle import bitwise_equal, per_system_max_rel
+from paper_1909_04539_b200 import bandsolve as bs
+
+pytestmark = pytest.mark.gpu
+
+
+def _random_tri(rng, n):
+    sub = rng.uniform(-1, 1, n); sub[0] = 0
+    sup = rng.uniform(-1, 1, n); sup[-1] = 0
+    diag = np.abs(sub) + np.abs(sup) + rng.uniform(0.5, 1.5, n)
+    return sub, diag, sup
+
+
+def _random_pent(rng, n):
+    a = rng.uniform(-1, 1, n); a[:2] = 0
+    b = rng.uniform(-1, 1, n); b[0] = 0
+    d = rng.uniform(-1, 1, n); d[-1] = 0
+    e = rng.uniform(-1, 1, n); e[-2:] = 0
+    c = np.abs(a) + np.abs(b) + np.abs(d) + np.abs(e) + rng.uniform(0.5, 1.5, n)
+    return a, b, c, d, e
+
+
+def _dev_solve(lib, torch, factor, rhs, ld):
+    n, m = rhs.shape
+    buf = torch.full((n, ld), float("nan"), dtype=torch.float64, device="cuda")
+    buf[:, :m] = torch.from_numpy(rhs).cuda()
+    before = lib.kernel_launches()
+    factor.solve_dev(buf.data_ptr(), n, m, ld=ld, stream=torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    out = buf.cpu().numpy()
+    assert np.all(np.isnan(out[:, m:]))
+    return out[:, :m], lib.kernel_launches() - before
+
+
+@pytest.mark.parametrize("mode", [bs.MODE_EXACT, bs.MODE_FAST])
+@pytest.mark.parametrize("n", [32, 48, 256, 272, 320, 512])
+def test_pipe_matches_oracle(lib, oracle, cuda_device, mode, n):
+    torch = cuda_device
+    lib.tune("PIPE", "1")
+    lib.tune("SPIKE", "0")
+    lib.tune("PARTITION", "0")
+    lib.set_mode(mode)
+    rng = np.random.default_rng(n + mode)
+    try:
+        for m, ld in [(2, 2), (64, 66), (330, 330), (1000, 1002)]:
+            rhs = rng.uniform(-1, 1, (n, m))
+            for name, cls, bands in [("tri", bs.TriFactor, _random_tri(rng, n)),
+                                     ("diff", bs.TriFactor, bs.diffusion_bands(1.0, n)),
+                                     ("pent", bs.PentFactor, _random_pent(rng, n)),
+                                     ("hyper", bs.PentFactor, bs.hyper_bands(1.0, n))]:
+                pent = cls is bs.PentFactor
+                assert lib.describe_plan(1 if pent else 0, n, m, ld).startswith("pipe"), (n, m)
+                want = (oracle.pent_solve(oracle.pent_prefactor(*bands), rhs.copy()) if pent
+                        else oracle.tri_solve(oracle.tri_prefactor(*bands), rhs.copy()))
+                got, launches = _dev_solve(lib, torch, cls(lib, *bands), rhs, ld)
+                assert launches == 1
+                if mode == bs.MODE_EXACT:
+                    assert bitwise_equal(got, want), (name, n, m, ld)
+                else:
+                    assert per_system_max_rel(got, want) <= 1e-12, (name, n, m, ld)
+    finally:
+        lib.set_mode(bs.MODE_EXACT)
+
+
+def test_pipe_planner(lib, cuda_device):
+    """Taken in exact mode for many systems of n % 16 == 0, n <= 512 only."""
+    assert lib.describe_plan(1, 512, 1 << 20).startswith("pipe")
+    assert lib.describe_plan(0, 256, 1 << 20).startswith("pipe")
+    assert not lib.describe_plan(1, 520, 1 << 20).startswith("pipe")      # > 512 rows
+    assert not lib.describe_plan(1, 500, 1 << 20).startswith("pipe")      # not whole chunks
+    assert not lib.describe_plan(1, 512, (1 << 20) - 1, 1 << 20).startswith("pipe")  # odd batch
+    assert not lib.describe_plan(1, 512, 100).startswith("pipe")          # under one wave
+    lib.tune("PIPE", "0")
+    assert not lib.describe_plan(1, 512, 1 << 20).startswith("pipe")
