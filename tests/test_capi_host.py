@@ -212,8 +212,12 @@ def test_modes(lib):
 
 def test_plan_description(lib):
     s = lib.describe_plan(bs.KIND_PENT, 512, 65536)
-    assert s.startswith("stream"), s  # configs[1]: warp-specialised streaming kernel, head spilled to L2
+    assert s.startswith("pipe"), s  # configs[1]: every row on chip (TMEM + smem), pipelined across groups
+    lib.tune("PIPE", "0")
+    s = lib.describe_plan(bs.KIND_PENT, 512, 65536)
+    assert s.startswith("stream"), s  # the warp-specialised streaming kernel, head spilled to L2
     assert "head(L2)=0" not in s
+    lib.tune("PIPE", None)
     assert "head(L2)=0" in lib.describe_plan(bs.KIND_TRI, 256, 4096)  # config 1 fits smem entirely
     assert "global" in lib.describe_plan(bs.KIND_TRI, 64, 3)  # odd pitch: no TMA
     assert "global" in lib.describe_plan(bs.KIND_TRI, 100000, 1 << 20)  # tile > smem
