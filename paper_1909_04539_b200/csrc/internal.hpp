@@ -160,9 +160,9 @@ int partition_blocks(std::size_t n, std::size_t m, int sms, bool pent);  // 0 = 
 // One-pass partitioned sweep for many long systems (sweep_spike.cuh), fast
 // mode fp64: blocks per system, 0 when it does not apply.
 int spike_blocks(std::size_t n, std::size_t m, std::size_t ld, const void* x, int sms, bool pent);
-// Pipelined on-chip sequential sweep (sweep_pipe.cuh), fp64, n % 16 == 0,
-// n <= 512: compute warps (0 = not used) and the launch.
-int pipe_warps(std::size_t n, std::size_t m, std::size_t ld, const void* x, bool pent, int sms, int* kb);
+// Pipelined sequential sweep (sweep_pipe.cuh), fp64, n % 16 == 0: compute
+// warps (0 = not used), ring slots, shared-memory chunks, and the launch.
+int pipe_warps(std::size_t n, std::size_t m, std::size_t ld, const void* x, bool pent, int sms, int* kb, int* st);
 bandsolve_status pipe_solve_device(bool pent, bool fast, const void* fwd, const void* bwd, double* x, std::size_t n,
                                    std::size_t m, std::size_t ld, void* stream, int sms, bool* done);
 struct PartPeriodic;

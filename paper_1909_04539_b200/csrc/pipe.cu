@@ -16,6 +16,7 @@ bool encode_tile_map(CUtensorMap* map, void* x, std::size_t elem, long long n, l
 cudaError_t allow_max_smem(const void* kern);  // solve.cu
 std::size_t max_smem_per_block();              // solve.cu
 double* dead_lane_sink(int device);            // partition.cu
+bandsolve_status cuda_fail(cudaError_t err, const char* what);  // solve.cu
 
 namespace {
 
@@ -25,23 +26,37 @@ std::size_t bwd_rec(bool pent) { return pent ? sizeof(dev::PentBwd<double>) : si
 }  // namespace
 
 // Compute warps (2..4) of the pipelined plan for this shape, 0 when it does
-// not apply; *kb receives the ring depth.
-int pipe_warps(std::size_t n, std::size_t m, std::size_t ld, const void* x, bool pent, int sms, int* kb) {
+// not apply; *kb receives the ring depth, *st the shared-memory storage
+// chunks per lane (the rest beyond TMEM + smem goes to the L2 scratch).
+int pipe_warps(std::size_t n, std::size_t m, std::size_t ld, const void* x, bool pent, int sms, int* kb, int* st) {
   const long long sel = tune_int("PIPE", -1);  // 0: never, 1: whenever it applies
   if (sel == 0 || tune_flag("PLAN")) return 0;
-  if (n % dev::kPpR != 0 || n < 2 * dev::kPpR || n > 2u * dev::kPpTmemRows) return 0;
+  // beyond 512 rows the L2 tier takes the place of the streaming kernel's
+  // spill and measured level with it (pent N = 1024: 0.466 vs 0.473), so by
+  // default the pipelined plan stops where everything fits on chip
+  const std::size_t max_rows = static_cast<std::size_t>(tune_int("PIPE_MAX_N", 512));
+  if (n % dev::kPpR != 0 || n < 2 * dev::kPpR || n > max_rows) return 0;
   if (reinterpret_cast<uintptr_t>(x) % 16 != 0 || ld % 2 != 0 || m % 2 != 0 ||
       m > static_cast<std::size_t>(INT_MAX) / 2)
     return 0;
   const std::size_t cap = max_smem_per_block();
+  const int CL = static_cast<int>(n) / dev::kPpR;
+  const int TT = std::min(CL, dev::kPpTmemRows / dev::kPpR);
+  const int kmin = static_cast<int>(tune_int("PKB", 6));  // ring slots (tuning)
   for (int P = 4; P >= 2; --P) {
     if (sel != 1 && m < static_cast<std::size_t>(sms) * 32 * P) continue;  // a full wave of groups
-    const int kmax = static_cast<int>(tune_int("PKB", 10));  // ring slots (tuning)
-    for (int k = kmax; k >= 3; --k)
-      if (dev::PipeLayout::make(static_cast<int>(n), P, k, fwd_rec(pent), bwd_rec(pent)).total <= cap) {
-        *kb = k;
-        return P;
-      }
+    // as many shared-memory chunks as fit beside a ring of kmin slots; with
+    // an L2 tier, at most 2 warps (the spill is ~P x 148 x rows x 256 B)
+    for (int ST = CL - TT; ST >= 0; --ST) {
+      if (ST < CL - TT && P > 2) break;
+      if (dev::PipeLayout::make(static_cast<int>(n), P, kmin, fwd_rec(pent), bwd_rec(pent), ST).total > cap) continue;
+      int k = kmin;
+      while (k < 10 && dev::PipeLayout::make(static_cast<int>(n), P, k + 1, fwd_rec(pent), bwd_rec(pent), ST).total <= cap)
+        ++k;
+      *kb = k;
+      *st = ST;
+      return P;
+    }
   }
   return 0;
 }
@@ -49,8 +64,8 @@ int pipe_warps(std::size_t n, std::size_t m, std::size_t ld, const void* x, bool
 bandsolve_status pipe_solve_device(bool pent, bool fast, const void* fwd, const void* bwd, double* x, std::size_t n,
                                    std::size_t m, std::size_t ld, void* stream, int sms, bool* done) {
   *done = false;
-  int KB = 0;
-  const int P = pipe_warps(n, m, ld, x, pent, sms, &KB);
+  int KB = 0, ST = 0;
+  const int P = pipe_warps(n, m, ld, x, pent, sms, &KB, &ST);
   if (P == 0) return BANDSOLVE_OK;
   int device = 0;
   if (cudaGetDevice(&device) != cudaSuccess) {
@@ -80,22 +95,34 @@ bandsolve_status pipe_solve_device(bool pent, bool fast, const void* fwd, const 
   }
   const int Wg = 32 * P;
   const long long groups = (static_cast<long long>(m) + Wg - 1) / Wg;
-  const std::size_t smem = dev::PipeLayout::make(static_cast<int>(n), P, KB, fwd_rec(pent), bwd_rec(pent)).total;
+  const std::size_t smem =
+      dev::PipeLayout::make(static_cast<int>(n), P, KB, fwd_rec(pent), bwd_rec(pent), ST).total;
+  const int CL = static_cast<int>(n) / dev::kPpR;
+  const int GT = CL - std::min(CL, dev::kPpTmemRows / dev::kPpR) - ST;
+  const long long grid = std::min<long long>(sms, groups);
+  auto s = static_cast<cudaStream_t>(stream);
+  double* scratch = nullptr;  // the L2 tier: per CTA, GT chunks x P warps x 4 KiB
+  if (GT > 0) {
+    const std::size_t bytes = static_cast<std::size_t>(grid) * GT * P * dev::kPpR * 32 * sizeof(double);
+    if (cudaError_t e = pool_malloc_async(reinterpret_cast<void**>(&scratch), bytes, s); e != cudaSuccess)
+      return cuda_fail(e, "pipe scratch");
+  }
   const int PD = static_cast<int>(tune_int("SPD", 4));
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(static_cast<unsigned>(std::min<long long>(sms, groups)), 1, 1);
+  cfg.gridDim = dim3(static_cast<unsigned>(grid), 1, 1);
   cfg.blockDim = dim3(32 * (P + 1), 1, 1);
   cfg.dynamicSmemBytes = smem;
-  cfg.stream = static_cast<cudaStream_t>(stream);
+  cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = tune_flag("NO_PDL") ? 0 : 1;
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, map, x, static_cast<int>(n), static_cast<long long>(m),
-                                     static_cast<long long>(ld), KB, PD, groups, fwd, bwd, sink);
+                                     static_cast<long long>(ld), KB, PD, groups, fwd, bwd, sink, ST, scratch);
   note_launches(1);
   if (e == cudaSuccess) e = cudaGetLastError();
+  if (scratch) cudaFreeAsync(scratch, s);
   if (e != cudaSuccess) return fail(BANDSOLVE_ERR_INTERNAL, std::string("pipe launch: ") + cudaGetErrorString(e));
   *done = true;
   return BANDSOLVE_OK;

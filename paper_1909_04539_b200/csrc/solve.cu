@@ -1134,11 +1134,13 @@ bandsolve_status describe_plan(Kind kind, std::size_t n, std::size_t m, std::siz
   char buf[256];
   const int KS = f32 ? 0 : spike_blocks(n, m, ld, kProbe, sms, pent);
   const int K = f32 ? 0 : partition_blocks(n, m, sms, pent);
-  int pkb = 0;
-  const int PP = (f32 || KS > 0 || K > 0) ? 0 : pipe_warps(n, m, ld, kProbe, pent, sms, &pkb);
-  if (PP > 0)
-    std::snprintf(buf, sizeof buf, "pipe Wg=%d warps=%d+1 tmem=%zu smem-rows=%zu ring=%d (all rows on chip, 1 launch)",
-                  32 * PP, PP, std::min<std::size_t>(n, 256), n > 256 ? n - 256 : 0, pkb);
+  int pkb = 0, pst = 0;
+  const int PP = (f32 || KS > 0 || K > 0) ? 0 : pipe_warps(n, m, ld, kProbe, pent, sms, &pkb, &pst);
+  if (PP > 0) {
+    const std::size_t tm = std::min<std::size_t>(n, 256), sm = static_cast<std::size_t>(pst) * 16;
+    std::snprintf(buf, sizeof buf, "pipe Wg=%d warps=%d+1 tmem=%zu smem-rows=%zu l2-rows=%zu ring=%d (1 launch)",
+                  32 * PP, PP, tm, sm, n - tm - sm, pkb);
+  }
   else if (KS > 0)
     std::snprintf(buf, sizeof buf, "spike K=%d blocks of %zu rows, interface system %d, 1 launch (TMEM-resident blocks%s)",
                   KS, n / KS, (pent ? 4 : 2) * KS, KS > 8 ? (KS == 16 ? ", clusters of 2 CTAs" : ", clusters of 4 CTAs") : "");

@@ -1,5 +1,6 @@
-// Pipelined sequential shared-LHS sweep, every forward intermediate on chip
-// (sm_100a). The exact-mode kernel for systems of up to 512 rows.
+// Pipelined sequential shared-LHS sweep (sm_100a): the exact-mode kernel for
+// many systems. Up to 512 rows every forward intermediate stays on chip;
+// beyond, the last row chunks live in an L2 scratch tier.
 //
 // The exact mode must follow the reference's operation order
 // (tri_solver.cpp:25-47, pent_solver.cpp:19-62): one sequential recurrence
@@ -31,16 +32,16 @@ constexpr int kPpTmemRows = 256;  // rows per lane in TMEM (512 columns of fp64)
 
 struct PipeLayout {
   size_t fwd_off, bwd_off, stor_off, ring_off, bar_off, total;
-  // n rows (multiple of 16), P compute warps, KB ring slots
-  __host__ __device__ static PipeLayout make(int n, int P, int KB, size_t fwd_rec, size_t bwd_rec) {
+  // n rows (multiple of 16), P compute warps, KB ring slots, ST shared-memory
+  // storage chunks per lane (the first TT = min(n/16, 16) chunks live in
+  // TMEM, the last n/16 - TT - ST in the L2 scratch)
+  __host__ __device__ static PipeLayout make(int n, int P, int KB, size_t fwd_rec, size_t bwd_rec, int ST) {
     PipeLayout L{};
-    const int CL = n / kPpR;
-    const int TT = CL < kPpTmemRows / kPpR ? CL : kPpTmemRows / kPpR;
     L.fwd_off = 0;
     L.bwd_off = align128(static_cast<size_t>(n) * fwd_rec);
     L.stor_off = L.bwd_off + align128(static_cast<size_t>(n) * bwd_rec);
-    // shared-memory slots: [CL - TT][P warps][16 rows][32 lanes]
-    L.ring_off = L.stor_off + static_cast<size_t>(CL - TT) * P * kPpR * 32 * sizeof(double);
+    // shared-memory slots: [ST][P warps][16 rows][32 lanes]
+    L.ring_off = L.stor_off + static_cast<size_t>(ST) * P * kPpR * 32 * sizeof(double);
     L.bar_off = L.ring_off + static_cast<size_t>(KB) * P * kPpR * 32 * sizeof(double);
     L.total = L.bar_off + static_cast<size_t>(2 * KB + 1) * sizeof(uint64_t);
     return L;
@@ -98,11 +99,11 @@ template <bool PENT, bool FAST, int P>
 __global__ void __launch_bounds__(32 * (P + 1), 1)
     sweep_pipe(const __grid_constant__ CUtensorMap map_b, double* __restrict__ x, int n, long long m, long long ld,
                int KB, int PD, long long groups, const void* __restrict__ fwd_g, const void* __restrict__ bwd_g,
-               double* __restrict__ sink) {
+               double* __restrict__ sink, int ST, double* __restrict__ scratch) {
   using FwdR = typename Recs<double, PENT>::Fwd;
   using BwdR = typename Recs<double, PENT>::Bwd;
   extern __shared__ __align__(128) unsigned char smem[];
-  const PipeLayout Ly = PipeLayout::make(n, P, KB, sizeof(FwdR), sizeof(BwdR));
+  const PipeLayout Ly = PipeLayout::make(n, P, KB, sizeof(FwdR), sizeof(BwdR), ST);
   const FwdR* sf = reinterpret_cast<const FwdR*>(smem + Ly.fwd_off);
   const BwdR* sb = reinterpret_cast<const BwdR*>(smem + Ly.bwd_off);
   double* stor = reinterpret_cast<double*>(smem + Ly.stor_off);
@@ -178,6 +179,11 @@ __global__ void __launch_bounds__(32 * (P + 1), 1)
   // storage slot of chunk c of a group with parity p
   auto sidx = [&](uint32_t p, int c) { return p ? CL - 1 - c : c; };
   auto slot_smem = [&](int s) { return stor + (static_cast<size_t>(s - TT) * P + warp) * kBox + lane; };
+  // L2 tier: this CTA's scratch, [GT chunks][P warps][16 rows][32 lanes]
+  const int GT = CL - TT - ST;
+  double* const scr = scratch + static_cast<long long>(blockIdx.x) * GT * P * kBox;
+  auto slot_l2 = [&](int s) { return scr + (static_cast<long long>(s - TT - ST) * P + warp) * kBox + lane; };
+  const uint64_t pol_keep = policy_evict_last();
   int slot = 0;
   uint32_t phase = 0;
   double fs1 = 0.0, fs2 = 0.0;  // forward state (group being read)
@@ -190,10 +196,14 @@ __global__ void __launch_bounds__(32 * (P + 1), 1)
   auto bwd_load = [&](int s) {
     if (s < TT) {
       cur.load(tlane + static_cast<uint32_t>(s * TPiece<double>::kWords));
-    } else {
+    } else if (s < TT + ST) {
       const double* q = slot_smem(s);
 #pragma unroll
       for (int r = 0; r < kPpR; ++r) cur.put(r, q[r * 32]);
+    } else {  // this lane's own words, written by this lane one round earlier
+      const double* q = slot_l2(s);
+#pragma unroll
+      for (int r = 0; r < kPpR; ++r) cur.put(r, ld_spill(q + r * 32, pol_keep));
     }
   };
 
@@ -233,10 +243,14 @@ __global__ void __launch_bounds__(32 * (P + 1), 1)
       }
       if (s < TT) {
         buf.store(tlane + static_cast<uint32_t>(s * TPiece<double>::kWords));
-      } else {
+      } else if (s < TT + ST) {
         double* q = slot_smem(s);
 #pragma unroll
         for (int r = 0; r < kPpR; ++r) q[r * 32] = buf.get(r);
+      } else {
+        double* q = slot_l2(s);
+#pragma unroll
+        for (int r = 0; r < kPpR; ++r) st_spill(q + r * 32, buf.get(r), pol_keep);
       }
     }
   };
@@ -263,6 +277,11 @@ __global__ void __launch_bounds__(32 * (P + 1), 1)
       if (i > 0 && c > 0) bwd_load(sidx(p ^ 1u, c - 1));  // next backward chunk (a different slot)
     }
     __syncwarp();  // this warp's smem slot stores are visible to its own next-round loads
+  }
+  if (GT > 0) {  // the scratch is dead: drop this warp's lines instead of writing them back
+    for (int s = TT + ST; s < CL; ++s)
+      for (int r = lane; r < kPpR * 2; r += 32)  // 16 rows x 256 B = 32 lines of 128 B
+        discard_l2_line(reinterpret_cast<const char*>(slot_l2(s) - lane) + r * 128);
   }
   tmem_fence_before();
   asm volatile("bar.sync 1, %0;" ::"r"(P * 32) : "memory");

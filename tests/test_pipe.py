@@ -49,10 +49,11 @@ def _dev_solve(lib, torch, factor, rhs, ld):
 
 
 @pytest.mark.parametrize("mode", [bs.MODE_EXACT, bs.MODE_FAST])
-@pytest.mark.parametrize("n", [32, 48, 256, 272, 320, 512])
+@pytest.mark.parametrize("n", [32, 48, 256, 272, 320, 512, 784, 1024])
 def test_pipe_matches_oracle(lib, oracle, cuda_device, mode, n):
     torch = cuda_device
     lib.tune("PIPE", "1")
+    lib.tune("PIPE_MAX_N", "1024")
     lib.tune("SPIKE", "0")
     lib.tune("PARTITION", "0")
     lib.set_mode(mode)
@@ -82,7 +83,11 @@ def test_pipe_planner(lib, cuda_device):
     """Taken in exact mode for many systems of n % 16 == 0, n <= 512 only."""
     assert lib.describe_plan(1, 512, 1 << 20).startswith("pipe")
     assert lib.describe_plan(0, 256, 1 << 20).startswith("pipe")
-    assert not lib.describe_plan(1, 520, 1 << 20).startswith("pipe")      # > 512 rows
+    assert not lib.describe_plan(1, 528, 1 << 20).startswith("pipe")      # > 512 rows by default
+    lib.tune("PIPE_MAX_N", "1024")
+    assert "l2-rows=0" not in lib.describe_plan(1, 1024, 1 << 21)          # the L2 tier
+    assert not lib.describe_plan(1, 1040, 1 << 20).startswith("pipe")     # > 1024 rows
+    lib.tune("PIPE_MAX_N", None)
     assert not lib.describe_plan(1, 500, 1 << 20).startswith("pipe")      # not whole chunks
     assert not lib.describe_plan(1, 512, (1 << 20) - 1, 1 << 20).startswith("pipe")  # odd batch
     assert not lib.describe_plan(1, 512, 100).startswith("pipe")          # under one wave
