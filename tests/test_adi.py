@@ -90,3 +90,34 @@ def test_gpu_adi_fast_partitioned_fused_stencil(lib, oracle, cuda_device, fuse_p
     finally:
         lib.set_mode(bs.MODE_EXACT)
         lib.tune("ADI_FUSE_PENT", None)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("problem", [0, 1])
+def test_gpu_adi_configs3_full_size(lib, oracle, cuda_device, problem):
+    """configs[3] itself: one ADI step on the 4096 x 4096 field, every point
+    against the oracle's composition — bitwise in exact mode, within 1e-12
+    in fast mode (fused partitioned pass for tri, transpose + cluster spike
+    kernel for pent)."""
+    torch = cuda_device
+    rng = np.random.default_rng(44 + problem)
+    stream = torch.cuda.current_stream().cuda_stream
+    n = 4096
+    s = 1.0
+    c = rng.uniform(-1, 1, (n, n))
+    want = oracle.adi_step(problem, s, c)
+    adi = bs.ADI(lib, problem, s, n, n)
+    try:
+        for mode in (bs.MODE_EXACT, bs.MODE_FAST):
+            lib.set_mode(mode)
+            f = torch.from_numpy(c).cuda()
+            w = torch.zeros_like(f)
+            adi.step_dev(f.data_ptr(), w.data_ptr(), stream=stream)
+            torch.cuda.synchronize()
+            got = f.cpu().numpy()
+            if mode == bs.MODE_EXACT:
+                assert bitwise_equal(got, want), problem
+            else:
+                assert per_system_max_rel(got, want) <= 1e-12, problem
+    finally:
+        lib.set_mode(bs.MODE_EXACT)
