@@ -162,7 +162,8 @@ int partition_blocks(std::size_t n, std::size_t m, int sms, bool pent);  // 0 = 
 int spike_blocks(std::size_t n, std::size_t m, std::size_t ld, const void* x, int sms, bool pent);
 // Pipelined sequential sweep (sweep_pipe.cuh), fp64, n % 16 == 0: compute
 // warps (0 = not used), ring slots, shared-memory chunks, and the launch.
-int pipe_warps(std::size_t n, std::size_t m, std::size_t ld, const void* x, bool pent, int sms, int* kb, int* st);
+int pipe_warps(std::size_t n, std::size_t m, std::size_t ld, const void* x, bool pent, int sms, int* kb, int* rt,
+               int* st);
 bandsolve_status pipe_solve_device(bool pent, bool fast, const void* fwd, const void* bwd, double* x, std::size_t n,
                                    std::size_t m, std::size_t ld, void* stream, int sms, bool* done);
 struct PartPeriodic;

@@ -26,9 +26,11 @@ std::size_t bwd_rec(bool pent) { return pent ? sizeof(dev::PentBwd<double>) : si
 }  // namespace
 
 // Compute warps (2..4) of the pipelined plan for this shape, 0 when it does
-// not apply; *kb receives the ring depth, *st the shared-memory storage
-// chunks per lane (the rest beyond TMEM + smem goes to the L2 scratch).
-int pipe_warps(std::size_t n, std::size_t m, std::size_t ld, const void* x, bool pent, int sms, int* kb, int* st) {
+// not apply; *kb receives the ring depth, *rt the register chunks per lane
+// (0 or 4, with 3 warps), *st the shared-memory chunks per lane (the rest
+// beyond TMEM + registers + smem goes to the L2 scratch).
+int pipe_warps(std::size_t n, std::size_t m, std::size_t ld, const void* x, bool pent, int sms, int* kb, int* rt,
+               int* st) {
   const long long sel = tune_int("PIPE", -1);  // 0: never, 1: whenever it applies
   if (sel == 0 || tune_flag("PLAN")) return 0;
   // beyond 512 rows the L2 tier takes the place of the streaming kernel's
@@ -42,30 +44,43 @@ int pipe_warps(std::size_t n, std::size_t m, std::size_t ld, const void* x, bool
   const std::size_t cap = max_smem_per_block();
   const int CL = static_cast<int>(n) / dev::kPpR;
   const int TT = std::min(CL, dev::kPpTmemRows / dev::kPpR);
-  const int kmin = static_cast<int>(tune_int("PKB", 6));  // ring slots (tuning)
+  const int kmin = static_cast<int>(tune_int("PKB", 4));  // ring slots (tuning)
+  const int rt_force = static_cast<int>(tune_int("PRT", -1));
+  auto fits = [&](int P, int k, int ST) {
+    return dev::PipeLayout::make(static_cast<int>(n), P, k, fwd_rec(pent), bwd_rec(pent), ST).total <= cap;
+  };
+  auto take = [&](int P, int RT, int ST) {
+    int k = kmin;
+    while (k < 10 && fits(P, k + 1, ST)) ++k;
+    *kb = k;
+    *rt = RT;
+    *st = ST;
+    return P;
+  };
+  // 1) every row on chip: the most warps (chains) that fit, registers as a
+  // fourth tier for 3 warps
   for (int P = 4; P >= 2; --P) {
     if (sel != 1 && m < static_cast<std::size_t>(sms) * 32 * P) continue;  // a full wave of groups
-    // as many shared-memory chunks as fit beside a ring of kmin slots; with
-    // an L2 tier, at most 2 warps (the spill is ~P x 148 x rows x 256 B)
-    for (int ST = CL - TT; ST >= 0; --ST) {
-      if (ST < CL - TT && P > 2) break;
-      if (dev::PipeLayout::make(static_cast<int>(n), P, kmin, fwd_rec(pent), bwd_rec(pent), ST).total > cap) continue;
-      int k = kmin;
-      while (k < 10 && dev::PipeLayout::make(static_cast<int>(n), P, k + 1, fwd_rec(pent), bwd_rec(pent), ST).total <= cap)
-        ++k;
-      *kb = k;
-      *st = ST;
-      return P;
+    for (int RT : {0, 4}) {
+      if (RT > 0 && P != 3) continue;  // the only register-tier instance
+      if (rt_force >= 0 && RT != rt_force) continue;
+      const int ST = CL - TT - RT;
+      if (ST < 0) continue;
+      if (fits(P, kmin, ST)) return take(P, RT, ST);
     }
   }
+  // 2) the L2 tier (2 warps)
+  if (sel != 1 && m < static_cast<std::size_t>(sms) * 64) return 0;
+  for (int ST = CL - TT; ST >= 0; --ST)
+    if (fits(2, kmin, ST)) return take(2, 0, ST);
   return 0;
 }
 
 bandsolve_status pipe_solve_device(bool pent, bool fast, const void* fwd, const void* bwd, double* x, std::size_t n,
                                    std::size_t m, std::size_t ld, void* stream, int sms, bool* done) {
   *done = false;
-  int KB = 0, ST = 0;
-  const int P = pipe_warps(n, m, ld, x, pent, sms, &KB, &ST);
+  int KB = 0, RT = 0, ST = 0;
+  const int P = pipe_warps(n, m, ld, x, pent, sms, &KB, &RT, &ST);
   if (P == 0) return BANDSOLVE_OK;
   int device = 0;
   if (cudaGetDevice(&device) != cudaSuccess) {
@@ -78,15 +93,18 @@ bandsolve_status pipe_solve_device(bool pent, bool fast, const void* fwd, const 
   if (!encode_tile_map(&map, x, sizeof(double), static_cast<long long>(n), static_cast<long long>(m),
                        static_cast<long long>(ld), 32, dev::kPpR))
     return BANDSOLVE_OK;
-  using Kern = decltype(&dev::sweep_pipe<true, false, 2>);
-#define BSB_PIPE_SET(PP)                                                                    \
-  {{dev::sweep_pipe<false, false, PP>, dev::sweep_pipe<false, true, PP>},                  \
-   {dev::sweep_pipe<true, false, PP>, dev::sweep_pipe<true, true, PP>}}
-  static const Kern kerns[3][2][2] = {BSB_PIPE_SET(2), BSB_PIPE_SET(3), BSB_PIPE_SET(4)};
+  using Kern = decltype(&dev::sweep_pipe<true, false, 2, 0>);
+#define BSB_PIPE_SET(PP, RR)                                                                \
+  {{dev::sweep_pipe<false, false, PP, RR>, dev::sweep_pipe<false, true, PP, RR>},          \
+   {dev::sweep_pipe<true, false, PP, RR>, dev::sweep_pipe<true, true, PP, RR>}}
+  // [2 warps, 3 warps, 4 warps, 3 warps + register tier]
+  static const Kern kerns[4][2][2] = {BSB_PIPE_SET(2, 0), BSB_PIPE_SET(3, 0), BSB_PIPE_SET(4, 0),
+                                      BSB_PIPE_SET(3, 4)};
 #undef BSB_PIPE_SET
-  const Kern kern = kerns[P - 2][pent][fast];
-  static std::atomic<uint64_t> configured[12];
-  std::atomic<uint64_t>& done_attr = configured[(P - 2) * 4 + (pent ? 2 : 0) + (fast ? 1 : 0)];
+  const int ki = RT > 0 ? 3 : P - 2;
+  const Kern kern = kerns[ki][pent][fast];
+  static std::atomic<uint64_t> configured[16];
+  std::atomic<uint64_t>& done_attr = configured[ki * 4 + (pent ? 2 : 0) + (fast ? 1 : 0)];
   const uint64_t bit = device < 64 ? (1ull << device) : 0;
   if (!(bit && (done_attr.load(std::memory_order_relaxed) & bit))) {
     if (cudaError_t e = allow_max_smem(reinterpret_cast<const void*>(kern)); e != cudaSuccess)
@@ -98,7 +116,7 @@ bandsolve_status pipe_solve_device(bool pent, bool fast, const void* fwd, const 
   const std::size_t smem =
       dev::PipeLayout::make(static_cast<int>(n), P, KB, fwd_rec(pent), bwd_rec(pent), ST).total;
   const int CL = static_cast<int>(n) / dev::kPpR;
-  const int GT = CL - std::min(CL, dev::kPpTmemRows / dev::kPpR) - ST;
+  const int GT = CL - std::min(CL, dev::kPpTmemRows / dev::kPpR) - RT - ST;
   const long long grid = std::min<long long>(sms, groups);
   auto s = static_cast<cudaStream_t>(stream);
   double* scratch = nullptr;  // the L2 tier: per CTA, GT chunks x P warps x 4 KiB

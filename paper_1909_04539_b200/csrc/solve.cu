@@ -1134,12 +1134,14 @@ bandsolve_status describe_plan(Kind kind, std::size_t n, std::size_t m, std::siz
   char buf[256];
   const int KS = f32 ? 0 : spike_blocks(n, m, ld, kProbe, sms, pent);
   const int K = f32 ? 0 : partition_blocks(n, m, sms, pent);
-  int pkb = 0, pst = 0;
-  const int PP = (f32 || KS > 0 || K > 0) ? 0 : pipe_warps(n, m, ld, kProbe, pent, sms, &pkb, &pst);
+  int pkb = 0, prt = 0, pst = 0;
+  const int PP = (f32 || KS > 0 || K > 0) ? 0 : pipe_warps(n, m, ld, kProbe, pent, sms, &pkb, &prt, &pst);
   if (PP > 0) {
-    const std::size_t tm = std::min<std::size_t>(n, 256), sm = static_cast<std::size_t>(pst) * 16;
-    std::snprintf(buf, sizeof buf, "pipe Wg=%d warps=%d+1 tmem=%zu smem-rows=%zu l2-rows=%zu ring=%d (1 launch)",
-                  32 * PP, PP, tm, sm, n - tm - sm, pkb);
+    const std::size_t tm = std::min<std::size_t>(n, 256), rg = static_cast<std::size_t>(prt) * 16,
+                      sm = static_cast<std::size_t>(pst) * 16;
+    std::snprintf(buf, sizeof buf,
+                  "pipe Wg=%d warps=%d+1 tmem=%zu reg-rows=%zu smem-rows=%zu l2-rows=%zu ring=%d (1 launch)", 32 * PP,
+                  PP, tm, rg, sm, n - tm - rg - sm, pkb);
   }
   else if (KS > 0)
     std::snprintf(buf, sizeof buf, "spike K=%d blocks of %zu rows, interface system %d, 1 launch (TMEM-resident blocks%s)",

@@ -34,7 +34,7 @@ struct PipeLayout {
   size_t fwd_off, bwd_off, stor_off, ring_off, bar_off, total;
   // n rows (multiple of 16), P compute warps, KB ring slots, ST shared-memory
   // storage chunks per lane (the first TT = min(n/16, 16) chunks live in
-  // TMEM, the last n/16 - TT - ST in the L2 scratch)
+  // TMEM, then RT in registers, then ST in smem, the rest in the L2 scratch)
   __host__ __device__ static PipeLayout make(int n, int P, int KB, size_t fwd_rec, size_t bwd_rec, int ST) {
     PipeLayout L{};
     L.fwd_off = 0;
@@ -95,7 +95,11 @@ __device__ __forceinline__ void pipe_rows(const typename Recs<double, PENT>::Fwd
   }
 }
 
-template <bool PENT, bool FAST, int P>
+// RT: storage chunks per lane held in REGISTERS (after the TMEM chunks; a
+// lane's 16 x RT values in a statically indexed array, reached through a
+// switch on the slot). With RT = 4 and 3 compute warps, 96 systems of 512
+// rows fit on chip (TMEM 256 + registers 64 + shared memory 192 rows).
+template <bool PENT, bool FAST, int P, int RT = 0>
 __global__ void __launch_bounds__(32 * (P + 1), 1)
     sweep_pipe(const __grid_constant__ CUtensorMap map_b, double* __restrict__ x, int n, long long m, long long ld,
                int KB, int PD, long long groups, const void* __restrict__ fwd_g, const void* __restrict__ bwd_g,
@@ -178,11 +182,16 @@ __global__ void __launch_bounds__(32 * (P + 1), 1)
   const uint32_t tlane = tmem_base_s + (static_cast<uint32_t>(32 * warp) << 16);
   // storage slot of chunk c of a group with parity p
   auto sidx = [&](uint32_t p, int c) { return p ? CL - 1 - c : c; };
-  auto slot_smem = [&](int s) { return stor + (static_cast<size_t>(s - TT) * P + warp) * kBox + lane; };
+  // tiers by slot: TMEM [0, TT), registers [TT, TT + RT), shared memory
+  // [.., + ST), the L2 scratch [.., CL)
+  const int TR = TT + RT;
+  auto slot_smem = [&](int s) { return stor + (static_cast<size_t>(s - TR) * P + warp) * kBox + lane; };
   // L2 tier: this CTA's scratch, [GT chunks][P warps][16 rows][32 lanes]
-  const int GT = CL - TT - ST;
+  const int GT = CL - TR - ST;
   double* const scr = scratch + static_cast<long long>(blockIdx.x) * GT * P * kBox;
-  auto slot_l2 = [&](int s) { return scr + (static_cast<long long>(s - TT - ST) * P + warp) * kBox + lane; };
+  auto slot_l2 = [&](int s) { return scr + (static_cast<long long>(s - TR - ST) * P + warp) * kBox + lane; };
+  double rs[RT > 0 ? RT * kPpR : 1];  // register tier (static indices only)
+  (void)rs;
   const uint64_t pol_keep = policy_evict_last();
   int slot = 0;
   uint32_t phase = 0;
@@ -196,7 +205,20 @@ __global__ void __launch_bounds__(32 * (P + 1), 1)
   auto bwd_load = [&](int s) {
     if (s < TT) {
       cur.load(tlane + static_cast<uint32_t>(s * TPiece<double>::kWords));
-    } else if (s < TT + ST) {
+    } else if (s < TR) {
+      if constexpr (RT > 0) {
+        switch (s - TT) {
+#define BSB_RS_LOAD(K)                                                      \
+  case K:                                                                   \
+    if constexpr (K < RT) {                                                 \
+      _Pragma("unroll") for (int r = 0; r < kPpR; ++r) cur.put(r, rs[K * kPpR + r]); \
+    }                                                                       \
+    break;
+          BSB_RS_LOAD(0) BSB_RS_LOAD(1) BSB_RS_LOAD(2) BSB_RS_LOAD(3)
+#undef BSB_RS_LOAD
+        }
+      }
+    } else if (s < TR + ST) {
       const double* q = slot_smem(s);
 #pragma unroll
       for (int r = 0; r < kPpR; ++r) cur.put(r, q[r * 32]);
@@ -243,7 +265,20 @@ __global__ void __launch_bounds__(32 * (P + 1), 1)
       }
       if (s < TT) {
         buf.store(tlane + static_cast<uint32_t>(s * TPiece<double>::kWords));
-      } else if (s < TT + ST) {
+      } else if (s < TR) {
+        if constexpr (RT > 0) {
+          switch (s - TT) {
+#define BSB_RS_STORE(K)                                                     \
+  case K:                                                                   \
+    if constexpr (K < RT) {                                                 \
+      _Pragma("unroll") for (int r = 0; r < kPpR; ++r) rs[K * kPpR + r] = buf.get(r); \
+    }                                                                       \
+    break;
+            BSB_RS_STORE(0) BSB_RS_STORE(1) BSB_RS_STORE(2) BSB_RS_STORE(3)
+#undef BSB_RS_STORE
+          }
+        }
+      } else if (s < TR + ST) {
         double* q = slot_smem(s);
 #pragma unroll
         for (int r = 0; r < kPpR; ++r) q[r * 32] = buf.get(r);
@@ -279,7 +314,7 @@ __global__ void __launch_bounds__(32 * (P + 1), 1)
     __syncwarp();  // this warp's smem slot stores are visible to its own next-round loads
   }
   if (GT > 0) {  // the scratch is dead: drop this warp's lines instead of writing them back
-    for (int s = TT + ST; s < CL; ++s)
+    for (int s = TR + ST; s < CL; ++s)
       for (int r = lane; r < kPpR * 2; r += 32)  // 16 rows x 256 B = 32 lines of 128 B
         discard_l2_line(reinterpret_cast<const char*>(slot_l2(s) - lane) + r * 128);
   }
