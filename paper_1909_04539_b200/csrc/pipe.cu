@@ -30,7 +30,7 @@ std::size_t bwd_rec(bool pent) { return pent ? sizeof(dev::PentBwd<double>) : si
 // (0 or 4, with 3 warps), *st the shared-memory chunks per lane (the rest
 // beyond TMEM + registers + smem goes to the L2 scratch).
 int pipe_warps(std::size_t n, std::size_t m, std::size_t ld, const void* x, bool pent, int sms, int* kb, int* rt,
-               int* st) {
+               int* st, bool per) {
   const long long sel = tune_int("PIPE", -1);  // 0: never, 1: whenever it applies
   if (sel == 0 || tune_flag("PLAN")) return 0;
   // beyond 512 rows the L2 tier takes the place of the streaming kernel's
@@ -46,8 +46,9 @@ int pipe_warps(std::size_t n, std::size_t m, std::size_t ld, const void* x, bool
   const int TT = std::min(CL, dev::kPpTmemRows / dev::kPpR);
   const int kmin = static_cast<int>(tune_int("PKB", 4));  // ring slots (tuning)
   const int rt_force = static_cast<int>(tune_int("PRT", -1));
+  const int zw = per ? (pent ? 2 : 1) : 0;
   auto fits = [&](int P, int k, int ST) {
-    return dev::PipeLayout::make(static_cast<int>(n), P, k, fwd_rec(pent), bwd_rec(pent), ST).total <= cap;
+    return dev::PipeLayout::make(static_cast<int>(n), P, k, fwd_rec(pent), bwd_rec(pent), ST, zw).total <= cap;
   };
   auto take = [&](int P, int RT, int ST) {
     int k = kmin;
@@ -77,10 +78,11 @@ int pipe_warps(std::size_t n, std::size_t m, std::size_t ld, const void* x, bool
 }
 
 bandsolve_status pipe_solve_device(bool pent, bool fast, const void* fwd, const void* bwd, double* x, std::size_t n,
-                                   std::size_t m, std::size_t ld, void* stream, int sms, bool* done) {
+                                   std::size_t m, std::size_t ld, void* stream, int sms, bool* done,
+                                   const PartPeriodic* per) {
   *done = false;
   int KB = 0, RT = 0, ST = 0;
-  const int P = pipe_warps(n, m, ld, x, pent, sms, &KB, &RT, &ST);
+  const int P = pipe_warps(n, m, ld, x, pent, sms, &KB, &RT, &ST, per != nullptr);
   if (P == 0) return BANDSOLVE_OK;
   int device = 0;
   if (cudaGetDevice(&device) != cudaSuccess) {
@@ -93,18 +95,19 @@ bandsolve_status pipe_solve_device(bool pent, bool fast, const void* fwd, const 
   if (!encode_tile_map(&map, x, sizeof(double), static_cast<long long>(n), static_cast<long long>(m),
                        static_cast<long long>(ld), 32, dev::kPpR))
     return BANDSOLVE_OK;
-  using Kern = decltype(&dev::sweep_pipe<true, false, 2, 0>);
-#define BSB_PIPE_SET(PP, RR)                                                                \
-  {{dev::sweep_pipe<false, false, PP, RR>, dev::sweep_pipe<false, true, PP, RR>},          \
-   {dev::sweep_pipe<true, false, PP, RR>, dev::sweep_pipe<true, true, PP, RR>}}
-  // [2 warps, 3 warps, 4 warps, 3 warps + register tier]
-  static const Kern kerns[4][2][2] = {BSB_PIPE_SET(2, 0), BSB_PIPE_SET(3, 0), BSB_PIPE_SET(4, 0),
-                                      BSB_PIPE_SET(3, 4)};
+  using Kern = decltype(&dev::sweep_pipe<true, false, 2, 0, false>);
+#define BSB_PIPE_SET(PP, RR, PR)                                                                    \
+  {{dev::sweep_pipe<false, false, PP, RR, PR>, dev::sweep_pipe<false, true, PP, RR, PR>},          \
+   {dev::sweep_pipe<true, false, PP, RR, PR>, dev::sweep_pipe<true, true, PP, RR, PR>}}
+  // [periodic][2 warps, 3 warps, 4 warps, 3 warps + register tier]
+  static const Kern kerns[2][4][2][2] = {
+      {BSB_PIPE_SET(2, 0, false), BSB_PIPE_SET(3, 0, false), BSB_PIPE_SET(4, 0, false), BSB_PIPE_SET(3, 4, false)},
+      {BSB_PIPE_SET(2, 0, true), BSB_PIPE_SET(3, 0, true), BSB_PIPE_SET(4, 0, true), BSB_PIPE_SET(3, 4, true)}};
 #undef BSB_PIPE_SET
   const int ki = RT > 0 ? 3 : P - 2;
-  const Kern kern = kerns[ki][pent][fast];
-  static std::atomic<uint64_t> configured[16];
-  std::atomic<uint64_t>& done_attr = configured[ki * 4 + (pent ? 2 : 0) + (fast ? 1 : 0)];
+  const Kern kern = kerns[per != nullptr][ki][pent][fast];
+  static std::atomic<uint64_t> configured[32];
+  std::atomic<uint64_t>& done_attr = configured[(per ? 16 : 0) + ki * 4 + (pent ? 2 : 0) + (fast ? 1 : 0)];
   const uint64_t bit = device < 64 ? (1ull << device) : 0;
   if (!(bit && (done_attr.load(std::memory_order_relaxed) & bit))) {
     if (cudaError_t e = allow_max_smem(reinterpret_cast<const void*>(kern)); e != cudaSuccess)
@@ -114,7 +117,14 @@ bandsolve_status pipe_solve_device(bool pent, bool fast, const void* fwd, const 
   const int Wg = 32 * P;
   const long long groups = (static_cast<long long>(m) + Wg - 1) / Wg;
   const std::size_t smem =
-      dev::PipeLayout::make(static_cast<int>(n), P, KB, fwd_rec(pent), bwd_rec(pent), ST).total;
+      dev::PipeLayout::make(static_cast<int>(n), P, KB, fwd_rec(pent), bwd_rec(pent), ST, per ? (pent ? 2 : 1) : 0)
+          .total;
+  dev::PipePer pp;
+  if (per) {
+    pp.z1 = per->z1;
+    pp.z2 = per->z2;
+    for (int q = 0; q < 4; ++q) pp.c[q] = per->c[q];
+  }
   const int CL = static_cast<int>(n) / dev::kPpR;
   const int GT = CL - std::min(CL, dev::kPpTmemRows / dev::kPpR) - RT - ST;
   const long long grid = std::min<long long>(sms, groups);
@@ -137,7 +147,7 @@ bandsolve_status pipe_solve_device(bool pent, bool fast, const void* fwd, const 
   cfg.attrs = attr;
   cfg.numAttrs = tune_flag("NO_PDL") ? 0 : 1;
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, map, x, static_cast<int>(n), static_cast<long long>(m),
-                                     static_cast<long long>(ld), KB, PD, groups, fwd, bwd, sink, ST, scratch);
+                                     static_cast<long long>(ld), KB, PD, groups, fwd, bwd, sink, ST, scratch, pp);
   note_launches(1);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (scratch) cudaFreeAsync(scratch, s);

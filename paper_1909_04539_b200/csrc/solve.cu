@@ -1452,6 +1452,28 @@ bandsolve_status periodic_device(const Periodic& p, double* x, std::size_t n, st
       return BANDSOLVE_OK;
     }
   }
+  if (!correct_only && !tune_flag("PERIODIC_UNFUSED")) {
+    // exact mode (or fast without a fused plan): the pipelined on-chip sweep
+    // with the bitwise correction fused (a first backward pass finds y_0..)
+    const DeviceFactor* df = nullptr;
+    bandsolve_status st = ensure_device_factor(*p.factor, device, &df);
+    if (st != BANDSOLVE_OK) return st;
+    const double* blob = nullptr;
+    st = periodic_device_z(p, device, &blob);
+    if (st != BANDSOLVE_OK) return st;
+    PartPeriodic pa{blob, blob + n, {0.0, 0.0, 0.0, 0.0}};
+    if (pent) {
+      for (int k = 0; k < 4; ++k) pa.c[k] = p.cap_inv[k];
+    } else {
+      pa.c[0] = p.v_last;
+      pa.c[1] = p.scale;
+    }
+    const bool fast = current_mode() == BANDSOLVE_MODE_FAST;
+    bool done = false;
+    st = pipe_solve_device(pent, fast, df->fwd[0][fast ? 1 : 0], df->bwd[0][fast ? 1 : 0], x, n, m, ld, stream, sms,
+                           &done, &pa);
+    if (st != BANDSOLVE_OK || done) return st;
+  }
   if (!correct_only) {
     bandsolve_status st = solve_device(*p.factor, x, false, n, m, ld, stream);
     if (st != BANDSOLVE_OK) return st;

@@ -31,15 +31,18 @@ constexpr int kPpR = 16;      // rows per chunk (one TMA box {32 x 16} per warp)
 constexpr int kPpTmemRows = 256;  // rows per lane in TMEM (512 columns of fp64)
 
 struct PipeLayout {
-  size_t fwd_off, bwd_off, stor_off, ring_off, bar_off, total;
+  size_t fwd_off, bwd_off, z_off, stor_off, ring_off, bar_off, total;
   // n rows (multiple of 16), P compute warps, KB ring slots, ST shared-memory
   // storage chunks per lane (the first TT = min(n/16, 16) chunks live in
   // TMEM, then RT in registers, then ST in smem, the rest in the L2 scratch)
-  __host__ __device__ static PipeLayout make(int n, int P, int KB, size_t fwd_rec, size_t bwd_rec, int ST) {
+  // zw: doubles per row of the periodic correction's z (0, 1 tri, 2 pent)
+  __host__ __device__ static PipeLayout make(int n, int P, int KB, size_t fwd_rec, size_t bwd_rec, int ST,
+                                             int zw = 0) {
     PipeLayout L{};
     L.fwd_off = 0;
     L.bwd_off = align128(static_cast<size_t>(n) * fwd_rec);
-    L.stor_off = L.bwd_off + align128(static_cast<size_t>(n) * bwd_rec);
+    L.z_off = L.bwd_off + align128(static_cast<size_t>(n) * bwd_rec);
+    L.stor_off = L.z_off + align128(static_cast<size_t>(n) * zw * sizeof(double));
     // shared-memory slots: [ST][P warps][16 rows][32 lanes]
     L.ring_off = L.stor_off + static_cast<size_t>(ST) * P * kPpR * 32 * sizeof(double);
     L.bar_off = L.ring_off + static_cast<size_t>(KB) * P * kPpR * 32 * sizeof(double);
@@ -99,15 +102,30 @@ __device__ __forceinline__ void pipe_rows(const typename Recs<double, PENT>::Fwd
 // lane's 16 x RT values in a statically indexed array, reached through a
 // switch on the slot). With RT = 4 and 3 compute warps, 96 systems of 512
 // rows fit on chip (TMEM 256 + registers 64 + shared memory 192 rows).
-template <bool PENT, bool FAST, int P, int RT = 0>
+// PER: the periodic (Woodbury) correction fused, bitwise in exact mode. Its
+// coefficients need y_0 (y_1) — the last values the backward sweep produces
+// — so each group gets a first backward pass over its on-chip intermediates
+// that keeps only y_{n-1}, y_{n-2}, y_1, y_0 (no memory traffic), then the
+// interleaved second pass recomputes the same y (the same operations on the
+// same values: the same bits) and stores x_i = y_i - w z_i in the reference's
+// order (periodic.cpp:80-85, :189-203). z: z1 (and z2) of n doubles.
+struct PipePer {
+  const double* z1 = nullptr;
+  const double* z2 = nullptr;
+  double c[4] = {0.0, 0.0, 0.0, 0.0};  // tri: v_last, scale; pent: cap_inv
+};
+
+template <bool PENT, bool FAST, int P, int RT = 0, bool PER = false>
 __global__ void __launch_bounds__(32 * (P + 1), 1)
     sweep_pipe(const __grid_constant__ CUtensorMap map_b, double* __restrict__ x, int n, long long m, long long ld,
                int KB, int PD, long long groups, const void* __restrict__ fwd_g, const void* __restrict__ bwd_g,
-               double* __restrict__ sink, int ST, double* __restrict__ scratch) {
+               double* __restrict__ sink, int ST, double* __restrict__ scratch, PipePer per) {
   using FwdR = typename Recs<double, PENT>::Fwd;
   using BwdR = typename Recs<double, PENT>::Bwd;
   extern __shared__ __align__(128) unsigned char smem[];
-  const PipeLayout Ly = PipeLayout::make(n, P, KB, sizeof(FwdR), sizeof(BwdR), ST);
+  constexpr int ZW = PER ? (PENT ? 2 : 1) : 0;
+  const PipeLayout Ly = PipeLayout::make(n, P, KB, sizeof(FwdR), sizeof(BwdR), ST, ZW);
+  double* const sz = reinterpret_cast<double*>(smem + Ly.z_off);  // [n][ZW]
   const FwdR* sf = reinterpret_cast<const FwdR*>(smem + Ly.fwd_off);
   const BwdR* sb = reinterpret_cast<const BwdR*>(smem + Ly.bwd_off);
   double* stor = reinterpret_cast<double*>(smem + Ly.stor_off);
@@ -132,6 +150,12 @@ __global__ void __launch_bounds__(32 * (P + 1), 1)
     const int wb = static_cast<int>((static_cast<size_t>(n) * sizeof(BwdR) + 15) / 16);
     for (int i = threadIdx.x; i < wf; i += blockDim.x) df[i] = sfw[i];
     for (int i = threadIdx.x; i < wb; i += blockDim.x) db[i] = sbw[i];
+    if constexpr (PER) {
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        sz[ZW * i] = per.z1[i];
+        if constexpr (PENT) sz[ZW * i + 1] = per.z2[i];
+      }
+    }
   }
   if (threadIdx.x == 0) {
     for (int s = 0; s < KB; ++s) {
@@ -197,6 +221,7 @@ __global__ void __launch_bounds__(32 * (P + 1), 1)
   uint32_t phase = 0;
   double fs1 = 0.0, fs2 = 0.0;  // forward state (group being read)
   double bs1 = 0.0, bs2 = 0.0;  // backward state (group being written)
+  double wt1 = 0.0, wt2 = 0.0;  // periodic correction coefficients of the group being written
   long long step = 0;
   double* out = sink + lane;
   TPiece<double> cur;  // the backward chunk's 16 forward values
@@ -252,6 +277,13 @@ __global__ void __launch_bounds__(32 * (P + 1), 1)
                                     bs2, bv);
       if constexpr (FW) buf.put(q, fv);
       if constexpr (BW) {
+        if constexpr (PER) {  // x_i = y_i - w z_i (periodic.cpp:85 / :203)
+          const int row = c * kPpR + r;
+          if constexpr (PENT)
+            bv = sub_rn(bv, add_rn(mul_rn(sz[2 * row], wt1), mul_rn(sz[2 * row + 1], wt2)));
+          else
+            bv = sub_rn(bv, mul_rn(wt1, sz[row]));
+        }
         __stcs(out, bv);
         out -= step;
       }
@@ -300,6 +332,33 @@ __global__ void __launch_bounds__(32 * (P + 1), 1)
       step = live ? ld : 0;
       out = live ? x + static_cast<long long>(n - 1) * ld + j : sink + lane;
       bs1 = bs2 = 0.0;
+      if constexpr (PER) {  // first backward pass: y_{n-1}, y_{n-2}, y_1, y_0 only
+        double e0 = 0.0, e1 = 0.0, yl = 0.0, yl2 = 0.0;
+        for (int c = CL - 1; c >= 0; --c) {
+          const int s = sidx(p ^ 1u, c);
+          bwd_load(s);
+          if (s < TT) cur.wait();
+          const BwdR* bc = sb + c * kPpR;
+#pragma unroll
+          for (int q = 0; q < kPpR; ++q) {
+            const int r = kPpR - 1 - q;
+            double fv = 0.0, bv = 0.0, d0 = 0.0, d1 = 0.0;
+            pipe_rows<PENT, FAST, false, true>(sf[0], 0.0, d0, d1, fv, bc[r], cur.get(r), bs1, bs2, bv);
+            if (c == CL - 1 && q == 0) yl = bv;   // y_{n-1}
+            if (c == CL - 1 && q == 1) yl2 = bv;  // y_{n-2}
+            if (c == 0 && r == 1) e1 = bv;        // y_1
+            if (c == 0 && r == 0) e0 = bv;        // y_0
+          }
+        }
+        if constexpr (PENT) {  // periodic.cpp:189-194
+          const double w1 = sub_rn(e0, yl), w2 = sub_rn(e1, yl2);
+          wt1 = add_rn(mul_rn(per.c[0], w1), mul_rn(per.c[1], w2));
+          wt2 = add_rn(mul_rn(per.c[2], w1), mul_rn(per.c[3], w2));
+        } else {  // periodic.cpp:80
+          wt1 = mul_rn(add_rn(e0, mul_rn(per.c[0], yl)), per.c[1]);
+        }
+        bs1 = bs2 = 0.0;
+      }
       bwd_load(sidx(p ^ 1u, CL - 1));
     }
     fs1 = fs2 = 0.0;

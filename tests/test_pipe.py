@@ -93,3 +93,25 @@ def test_pipe_planner(lib, cuda_device):
     assert not lib.describe_plan(1, 512, 100).startswith("pipe")          # under one wave
     lib.tune("PIPE", "0")
     assert not lib.describe_plan(1, 512, 1 << 20).startswith("pipe")
+
+
+@pytest.mark.parametrize("n", [32, 256, 320, 512])
+def test_pipe_periodic_exact_bitwise(lib, oracle, cuda_device, n):
+    """Exact periodic solves with the correction fused: a first backward pass
+    over the on-chip intermediates finds y_0, y_1, y_{n-2}, y_{n-1}, the
+    second recomputes y and stores x = y - w z in the reference's order
+    (periodic.cpp:57-95, :172-214) — bitwise, one launch."""
+    torch = cuda_device
+    lib.tune("PIPE", "1")
+    rng = np.random.default_rng(n + 7)
+    for m, ld in [(64, 64), (330, 332)]:
+        x = rng.uniform(-1, 1, (n, m))
+        for bands in [(-1.0, 3.0, -1.0), (-0.3, 1.9, -0.5), (1.0, -4.0, 7.0, -4.0, 1.0), (0.2, -0.8, 3.1, -0.7, 0.1)]:
+            p = bs.PeriodicTri(lib, *bands, n) if len(bands) == 3 else bs.PeriodicPent(lib, *bands, n)
+            got, launches = _dev_solve(lib, torch, p, x, ld)
+            assert launches == 1, (n, m, bands)
+            if len(bands) == 3:
+                want = oracle.periodic_tri_solve(oracle.periodic_tri_prepare(*bands, n), x.copy())
+            else:
+                want = oracle.periodic_pent_solve(oracle.periodic_pent_prepare(*bands, n), x.copy())
+            assert bitwise_equal(got, want), (n, m, ld, bands)
