@@ -458,7 +458,8 @@ int bandsolve_get_devices(int* devices, int capacity);
  * SPIKE_K (its block count), NO_PDL (flag: no programmatic dependent
  * launch); PIPE (0|1: the pipelined on-chip sequential kernel), PKB (its
  * minimum ring slots), PIPE_MAX_N (its row limit, default 512; up to 1024
- * with an L2 tier); PARTITION (0|1), PART_K; CN_UNFUSED, PERIODIC_UNFUSED,
+ * with an L2 tier), PRT (its register chunks), PIPE_CN (flag: the CN step
+ * through it); PARTITION (0|1), PART_K; CN_UNFUSED, PERIODIC_UNFUSED,
  * ADI_UNFUSED, ADI_FUSE_PENT (flags: set = on); HOST_CHUNK_MIB (host-batch
  * staging chunk); L2_SETASIDE (1: grow the device's persisting-L2 limit to
  * cover the spill scratch; process-wide state, off by default).

@@ -163,11 +163,6 @@ int spike_blocks(std::size_t n, std::size_t m, std::size_t ld, const void* x, in
 // Pipelined sequential sweep (sweep_pipe.cuh), fp64, n % 16 == 0: compute
 // warps (0 = not used), ring slots, shared-memory chunks, and the launch.
 struct PartPeriodic;
-int pipe_warps(std::size_t n, std::size_t m, std::size_t ld, const void* x, bool pent, int sms, int* kb, int* rt,
-               int* st, bool per = false);
-bandsolve_status pipe_solve_device(bool pent, bool fast, const void* fwd, const void* bwd, double* x, std::size_t n,
-                                   std::size_t m, std::size_t ld, void* stream, int sms, bool* done,
-                                   const PartPeriodic* per = nullptr);
 // Crank-Nicolson step through the spike kernel: b = the periodic stencil of
 // u (read only), x receives u_new; c = s, 4s (pent), 1-2s / 1-6s
 struct SpikeCN {
@@ -177,6 +172,11 @@ struct SpikeCN {
 bandsolve_status spike_solve_device(const Factor& f, double* x, std::size_t n, std::size_t m, std::size_t ld,
                                     void* stream, int sms, bool* done, const PartPeriodic* per = nullptr,
                                     const SpikeCN* cn = nullptr);
+int pipe_warps(std::size_t n, std::size_t m, std::size_t ld, const void* x, bool pent, int sms, int* kb, int* rt,
+               int* st, bool per = false);
+bandsolve_status pipe_solve_device(bool pent, bool fast, const void* fwd, const void* bwd, double* x, std::size_t n,
+                                   std::size_t m, std::size_t ld, void* stream, int sms, bool* done,
+                                   const PartPeriodic* per = nullptr, const SpikeCN* cn = nullptr);
 bool partition_stencil_ok(std::size_t n, std::size_t m, int K, std::size_t lds);
 bandsolve_status partition_solve_device(const Factor& f, double* x, std::size_t n,
                                         std::size_t m, std::size_t ld,

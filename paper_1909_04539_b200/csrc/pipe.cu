@@ -79,8 +79,9 @@ int pipe_warps(std::size_t n, std::size_t m, std::size_t ld, const void* x, bool
 
 bandsolve_status pipe_solve_device(bool pent, bool fast, const void* fwd, const void* bwd, double* x, std::size_t n,
                                    std::size_t m, std::size_t ld, void* stream, int sms, bool* done,
-                                   const PartPeriodic* per) {
+                                   const PartPeriodic* per, const SpikeCN* cn) {
   *done = false;
+  if (cn && (!per || reinterpret_cast<uintptr_t>(cn->u) % 16 != 0)) return BANDSOLVE_OK;
   int KB = 0, RT = 0, ST = 0;
   const int P = pipe_warps(n, m, ld, x, pent, sms, &KB, &RT, &ST, per != nullptr);
   if (P == 0) return BANDSOLVE_OK;
@@ -92,22 +93,26 @@ bandsolve_status pipe_solve_device(bool pent, bool fast, const void* fwd, const 
   double* sink = dead_lane_sink(device);
   if (!sink) return fail(BANDSOLVE_ERR_INTERNAL, "pipe scratch");
   CUtensorMap map;
-  if (!encode_tile_map(&map, x, sizeof(double), static_cast<long long>(n), static_cast<long long>(m),
-                       static_cast<long long>(ld), 32, dev::kPpR))
+  // the tensor map reads b (in place: x; Crank-Nicolson: the old field u)
+  if (!encode_tile_map(&map, cn ? const_cast<double*>(cn->u) : x, sizeof(double), static_cast<long long>(n),
+                       static_cast<long long>(m), static_cast<long long>(ld), 32, dev::kPpR))
     return BANDSOLVE_OK;
-  using Kern = decltype(&dev::sweep_pipe<true, false, 2, 0, false>);
-#define BSB_PIPE_SET(PP, RR, PR)                                                                    \
-  {{dev::sweep_pipe<false, false, PP, RR, PR>, dev::sweep_pipe<false, true, PP, RR, PR>},          \
-   {dev::sweep_pipe<true, false, PP, RR, PR>, dev::sweep_pipe<true, true, PP, RR, PR>}}
-  // [periodic][2 warps, 3 warps, 4 warps, 3 warps + register tier]
-  static const Kern kerns[2][4][2][2] = {
-      {BSB_PIPE_SET(2, 0, false), BSB_PIPE_SET(3, 0, false), BSB_PIPE_SET(4, 0, false), BSB_PIPE_SET(3, 4, false)},
-      {BSB_PIPE_SET(2, 0, true), BSB_PIPE_SET(3, 0, true), BSB_PIPE_SET(4, 0, true), BSB_PIPE_SET(3, 4, true)}};
+  using Kern = decltype(&dev::sweep_pipe<true, false, 2, 0, false, false>);
+#define BSB_PIPE_SET(PP, RR, PR, CC)                                                                        \
+  {{dev::sweep_pipe<false, false, PP, RR, PR, CC>, dev::sweep_pipe<false, true, PP, RR, PR, CC>},          \
+   {dev::sweep_pipe<true, false, PP, RR, PR, CC>, dev::sweep_pipe<true, true, PP, RR, PR, CC>}}
+#define BSB_PIPE_WARPS(PR, CC) \
+  {BSB_PIPE_SET(2, 0, PR, CC), BSB_PIPE_SET(3, 0, PR, CC), BSB_PIPE_SET(4, 0, PR, CC), BSB_PIPE_SET(3, 4, PR, CC)}
+  // [plain, periodic, CN step][2 warps, 3 warps, 4 warps, 3 warps + register tier][pent][fast]
+  static const Kern kerns[3][4][2][2] = {BSB_PIPE_WARPS(false, false), BSB_PIPE_WARPS(true, false),
+                                         BSB_PIPE_WARPS(true, true)};
+#undef BSB_PIPE_WARPS
 #undef BSB_PIPE_SET
   const int ki = RT > 0 ? 3 : P - 2;
-  const Kern kern = kerns[per != nullptr][ki][pent][fast];
-  static std::atomic<uint64_t> configured[32];
-  std::atomic<uint64_t>& done_attr = configured[(per ? 16 : 0) + ki * 4 + (pent ? 2 : 0) + (fast ? 1 : 0)];
+  const int vi = cn ? 2 : per ? 1 : 0;
+  const Kern kern = kerns[vi][ki][pent][fast];
+  static std::atomic<uint64_t> configured[48];
+  std::atomic<uint64_t>& done_attr = configured[vi * 16 + ki * 4 + (pent ? 2 : 0) + (fast ? 1 : 0)];
   const uint64_t bit = device < 64 ? (1ull << device) : 0;
   if (!(bit && (done_attr.load(std::memory_order_relaxed) & bit))) {
     if (cudaError_t e = allow_max_smem(reinterpret_cast<const void*>(kern)); e != cudaSuccess)
@@ -124,6 +129,10 @@ bandsolve_status pipe_solve_device(bool pent, bool fast, const void* fwd, const 
     pp.z1 = per->z1;
     pp.z2 = per->z2;
     for (int q = 0; q < 4; ++q) pp.c[q] = per->c[q];
+  }
+  if (cn) {
+    pp.u = cn->u;
+    for (int q = 0; q < 3; ++q) pp.cn[q] = cn->c[q];
   }
   const int CL = static_cast<int>(n) / dev::kPpR;
   const int GT = CL - std::min(CL, dev::kPpTmemRows / dev::kPpR) - RT - ST;

@@ -1321,6 +1321,30 @@ bandsolve_status cn_step_device(const Periodic& p, double sigma_x, const double*
     st = spike_solve_device(*p.factor, out, n, m, ld, stream, sms, &done, &pa, &cn);
     if (st != BANDSOLVE_OK || done) return st;
   }
+  if (aligned && !tune_flag("CN_UNFUSED") && tune_flag("PIPE_CN")) {
+    // stencil + pipelined on-chip sweep + correction (bitwise in exact mode),
+    // one launch. Opt-in: the register pressure of the stencil + two backward
+    // passes measured below the streaming CN kernel (pent N = 512 exact:
+    // 0.24 with the register tier / 0.34 without, vs 0.37)
+    const DeviceFactor* df = nullptr;
+    bandsolve_status st = ensure_device_factor(*p.factor, device, &df);
+    if (st != BANDSOLVE_OK) return st;
+    const double* blob = nullptr;
+    st = periodic_device_z(p, device, &blob);
+    if (st != BANDSOLVE_OK) return st;
+    PartPeriodic pa{blob, blob + n, {0.0, 0.0, 0.0, 0.0}};
+    if (pent) {
+      for (int k = 0; k < 4; ++k) pa.c[k] = p.cap_inv[k];
+    } else {
+      pa.c[0] = p.v_last;
+      pa.c[1] = p.scale;
+    }
+    const SpikeCN cn{u, {sigma_x, pent ? 4.0 * sigma_x : 0.0, pent ? 1.0 - 6.0 * sigma_x : 1.0 - 2.0 * sigma_x}};
+    bool done = false;
+    st = pipe_solve_device(pent, fast, df->fwd[0][fast ? 1 : 0], df->bwd[0][fast ? 1 : 0], out, n, m, ld, stream, sms,
+                           &done, &pa, &cn);
+    if (st != BANDSOLVE_OK || done) return st;
+  }
   Plan plan;
   if (!tune_flag("CN_UNFUSED") && aligned && n <= static_cast<std::size_t>(INT_MAX) &&
       m <= static_cast<std::size_t>(INT_MAX) / 2 &&

@@ -113,9 +113,14 @@ struct PipePer {
   const double* z1 = nullptr;
   const double* z2 = nullptr;
   double c[4] = {0.0, 0.0, 0.0, 0.0};  // tri: v_last, scale; pent: cap_inv
+  // Crank-Nicolson step (template CN, with PER): b = the explicit periodic
+  // stencil of the old field u (the tensor map's source), in the reference's
+  // operation order (pde.cpp:85 / :108); x receives u_new. cn = s, 4s, mid
+  const double* u = nullptr;
+  double cn[3] = {0.0, 0.0, 0.0};
 };
 
-template <bool PENT, bool FAST, int P, int RT = 0, bool PER = false>
+template <bool PENT, bool FAST, int P, int RT = 0, bool PER = false, bool CN = false>
 __global__ void __launch_bounds__(32 * (P + 1), 1)
     sweep_pipe(const __grid_constant__ CUtensorMap map_b, double* __restrict__ x, int n, long long m, long long ld,
                int KB, int PD, long long groups, const void* __restrict__ fwd_g, const void* __restrict__ bwd_g,
@@ -256,12 +261,75 @@ __global__ void __launch_bounds__(32 * (P + 1), 1)
 
   // One step: forward chunk kk of the group read (FW) and backward chunk c of
   // the group written (BW), rows interleaved; both use storage slot s.
-  auto run_step = [&](int kk, int c, int s, auto fw, auto bw) {
+  // CN halo: h1/h2 = u at the two rows above the chunk (carried; the wrap
+  // rows n-2, n-1 for chunk 0, loaded a group ahead), la0/la1 = the two rows
+  // below it (the next chunk's ring slot; rows 0, 1 past the last chunk)
+  double h1 = 0.0, h2 = 0.0, la0 = 0.0, la1 = 0.0, nh1 = 0.0, nh2 = 0.0, nla0 = 0.0, nla1 = 0.0;
+  auto u_at = [&](long long g, int row) -> double {
+    if constexpr (CN) {
+      row = row < 0 ? row + n : (row >= n ? row - n : row);
+      long long j = g * Wg + warp * 32 + lane;
+      j = j < m ? j : m - 1;
+      return __ldg(per.u + static_cast<long long>(row) * ld + j);
+    } else {
+      return 0.0;
+    }
+  };
+  auto halo_prefetch = [&](long long g) {
+    if constexpr (CN) {
+      nh2 = u_at(g, n - 2);
+      nh1 = u_at(g, n - 1);
+    }
+  };
+
+  auto run_step = [&](int kk, int c, int s, auto fw, auto bw, long long gr) {
     constexpr bool FW = decltype(fw)::value, BW = decltype(bw)::value;
     const double* blk = nullptr;
+    double fin[CN ? kPpR : 1];  // CN: the stencil rows of this chunk
+    (void)fin;
+    (void)gr;
     if constexpr (FW) {
       mbar_wait(&full[slot], phase);
       blk = ring + slot * kChunk + warp * kBox + lane;
+      if constexpr (CN) {
+        if (kk == 0) {  // the wrap rows n-2, n-1 (loaded a group ahead)
+          h2 = nh2;
+          h1 = nh1;
+        }
+        if (kk + 1 < CL) {  // the next chunk's first two rows: the next ring slot (same warp box)
+          const int ns = slot + 1 == KB ? 0 : slot + 1;
+          mbar_wait(&full[ns], slot + 1 == KB ? phase ^ 1u : phase);
+          const double* nbx = ring + ns * kChunk + warp * kBox + lane;
+          la0 = nbx[0];
+          la1 = nbx[32];
+        } else {  // past the last row: rows 0, 1 of this group (kept from chunk 0)
+          la0 = nla0;
+          la1 = nla1;
+        }
+        double e[kPpR + 4];
+        e[0] = h2;
+        e[1] = h1;
+#pragma unroll
+        for (int r = 0; r < kPpR; ++r) e[r + 2] = blk[r * 32];
+        e[kPpR + 2] = la0;
+        e[kPpR + 3] = la1;
+        if (kk == 0) {
+          nla0 = e[2];
+          nla1 = e[3];
+        }
+        const double cs = per.cn[0], cs4 = per.cn[1], cmid = per.cn[2];
+#pragma unroll
+        for (int r = 0; r < kPpR; ++r) {
+          if constexpr (PENT) {  // pde.cpp:108
+            const double t = add_rn(mul_rn(-cs, add_rn(e[r], e[r + 4])), mul_rn(cs4, add_rn(e[r + 1], e[r + 3])));
+            fin[r] = add_rn(t, mul_rn(cmid, e[r + 2]));
+          } else {  // pde.cpp:85
+            fin[r] = add_rn(mul_rn(cs, add_rn(e[r + 1], e[r + 3])), mul_rn(cmid, e[r + 2]));
+          }
+        }
+        h2 = e[kPpR];
+        h1 = e[kPpR + 1];
+      }
     }
     if constexpr (BW) {
       if (s < TT) cur.wait();
@@ -273,8 +341,12 @@ __global__ void __launch_bounds__(32 * (P + 1), 1)
     for (int q = 0; q < kPpR; ++q) {
       const int r = kPpR - 1 - q;
       double fv = 0.0, bv = 0.0;
-      pipe_rows<PENT, FAST, FW, BW>(fc[q], FW ? blk[q * 32] : 0.0, fs1, fs2, fv, bc[r], BW ? cur.get(r) : 0.0, bs1,
-                                    bs2, bv);
+      double din = 0.0;
+      if constexpr (FW) {
+        if constexpr (CN) din = fin[q];
+        else din = blk[q * 32];
+      }
+      pipe_rows<PENT, FAST, FW, BW>(fc[q], din, fs1, fs2, fv, bc[r], BW ? cur.get(r) : 0.0, bs1, bs2, bv);
       if constexpr (FW) buf.put(q, fv);
       if constexpr (BW) {
         if constexpr (PER) {  // x_i = y_i - w z_i (periodic.cpp:85 / :203)
@@ -323,6 +395,7 @@ __global__ void __launch_bounds__(32 * (P + 1), 1)
   };
 
   const long long my = (groups - blockIdx.x + gridDim.x - 1) / gridDim.x;
+  if (my > 0) halo_prefetch(blockIdx.x);
   uint32_t p = 0;  // parity of the group being read
   for (long long i = 0; i <= my; ++i, p ^= 1u) {
     const long long g = blockIdx.x + i * gridDim.x;  // group read in this round (i < my)
@@ -365,9 +438,10 @@ __global__ void __launch_bounds__(32 * (P + 1), 1)
     for (int kk = 0; kk < CL; ++kk) {
       const int c = CL - 1 - kk;
       const int s = sidx(p, kk);  // == sidx(p ^ 1, c)
-      if (i > 0 && i < my) run_step(kk, c, s, std::true_type{}, std::true_type{});
-      else if (i < my) run_step(kk, c, s, std::true_type{}, std::false_type{});
-      else run_step(kk, c, s, std::false_type{}, std::true_type{});
+      if (i > 0 && i < my) run_step(kk, c, s, std::true_type{}, std::true_type{}, g);
+      else if (i < my) run_step(kk, c, s, std::true_type{}, std::false_type{}, g);
+      else run_step(kk, c, s, std::false_type{}, std::true_type{}, g);
+      if (CN && kk == 0 && i + 1 < my) halo_prefetch(g + gridDim.x);  // this group's halo is consumed
       if (i > 0 && c > 0) bwd_load(sidx(p ^ 1u, c - 1));  // next backward chunk (a different slot)
     }
     __syncwarp();  // this warp's smem slot stores are visible to its own next-round loads

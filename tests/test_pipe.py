@@ -115,3 +115,39 @@ def test_pipe_periodic_exact_bitwise(lib, oracle, cuda_device, n):
             else:
                 want = oracle.periodic_pent_solve(oracle.periodic_pent_prepare(*bands, n), x.copy())
             assert bitwise_equal(got, want), (n, m, ld, bands)
+
+
+@pytest.mark.parametrize("n", [32, 256, 512])
+def test_pipe_cn_step_exact_bitwise(lib, oracle, cuda_device, n):
+    """Crank-Nicolson step in one pipe launch: the explicit periodic stencil
+    in the reference's operation order (pde.cpp:85 / :108, halo rows carried
+    across chunks and the wrap), the sequential sweep and the fused exact
+    correction — bitwise equal to assemble-then-solve; the old field is left
+    untouched."""
+    torch = cuda_device
+    lib.tune("PIPE", "1")
+    lib.tune("PIPE_CN", "1")
+    rng = np.random.default_rng(n + 9)
+    for prob in (0, 1):
+        for m, ld in [(64, 64), (330, 332)]:
+            s = 0.61
+            u = rng.uniform(-1, 1, (n, m))
+            if prob == 0:
+                h = bs.PeriodicTri(lib, -s, 1 + 2 * s, -s, n)
+                want = oracle.periodic_tri_solve(oracle.periodic_tri_prepare(-s, 1 + 2 * s, -s, n),
+                                                 oracle.cn_rhs(0, s, u))
+            else:
+                h = bs.PeriodicPent(lib, s, -4 * s, 1 + 6 * s, -4 * s, s, n)
+                want = oracle.periodic_pent_solve(oracle.periodic_pent_prepare(s, -4 * s, 1 + 6 * s, -4 * s, s, n),
+                                                  oracle.cn_rhs(1, s, u))
+            du = torch.full((n, ld), float("nan"), dtype=torch.float64, device="cuda")
+            du[:, :m] = torch.from_numpy(u).cuda()
+            do = torch.full_like(du, float("nan"))
+            before = lib.kernel_launches()
+            h.cn_step_dev(s, du.data_ptr(), do.data_ptr(), n, m, ld=ld, stream=torch.cuda.current_stream().cuda_stream)
+            torch.cuda.synchronize()
+            assert lib.kernel_launches() - before == 1, (prob, n, m)
+            out = do.cpu().numpy()
+            assert np.all(np.isnan(out[:, m:]))
+            assert bitwise_equal(out[:, :m], want), (prob, n, m, ld)
+            assert np.array_equal(du[:, :m].cpu().numpy(), u)
