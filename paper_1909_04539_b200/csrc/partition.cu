@@ -840,7 +840,16 @@ int spike_blocks(std::size_t n, std::size_t m, std::size_t ld, const void* x, in
   const int CS = spike_cluster(K);
   const std::size_t per_wave = CS > 1 ? 32u * static_cast<std::size_t>(sms / CS)
                                       : 32u * static_cast<std::size_t>(dev::kSpWarps / K) * sms;
-  if (sel != 1 && m < per_wave) return 0;
+  if (sel != 1 && m < per_wave) {
+    // Few systems: shorter blocks put more CTAs to work (configs[0], tri
+    // N = 256 x 4096: K = 2 0.14, K = 8 0.33 of the HBM roofline, vs 0.21
+    // for the sequential sweep). Long ones (n >= 1024) take the two-launch
+    // partitioned path instead.
+    if (n >= 1024 || kf != 0) return 0;
+    while (K * 2 <= dev::kSpWarps && n % (2 * K) == 0 && (n / (2 * K)) % dev::kSpR == 0 &&
+           n / (2 * K) >= 2 * dev::kSpR)
+      K *= 2;
+  }
   if (spike_ring_slots(static_cast<int>(n), K, pent, true) == 0) return 0;
   return K;
 }

@@ -91,6 +91,7 @@ def test_spike_planner_threshold(lib, cuda_device):
     assert lib.describe_plan(0, 2048, 1 << 20).startswith("spike K=16")
     assert lib.describe_plan(1, 4096, 1 << 20).startswith("spike K=32")
     assert not lib.describe_plan(1, 1024, sms * 32 - 2).startswith("spike")
+    assert lib.describe_plan(0, 256, 4096).startswith("spike K=8")  # configs[0]: few systems, short blocks
     assert not lib.describe_plan(1, 1024, (1 << 20) - 1, 1 << 20).startswith("spike")  # odd batch width
     assert not lib.describe_plan(1, 1024, 1 << 20, (1 << 20) + 1).startswith("spike")
     assert not lib.describe_plan(1, 1000, 1 << 20).startswith("spike")  # 1000 / 4 is not a chunk multiple
