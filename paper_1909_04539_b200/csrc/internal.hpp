@@ -159,7 +159,8 @@ struct PartStencil {
 int partition_blocks(std::size_t n, std::size_t m, int sms, bool pent);  // 0 = not used
 // One-pass partitioned sweep for many long systems (sweep_spike.cuh), fast
 // mode fp64: blocks per system, 0 when it does not apply.
-int spike_blocks(std::size_t n, std::size_t m, std::size_t ld, const void* x, int sms, bool pent);
+int spike_blocks(std::size_t n, std::size_t m, std::size_t ld, const void* x, int sms, bool pent,
+                 std::size_t elem = 8);
 // Pipelined sequential sweep (sweep_pipe.cuh), fp64, n % 16 == 0: compute
 // warps (0 = not used), ring slots, shared-memory chunks, and the launch.
 struct PartPeriodic;
@@ -172,6 +173,8 @@ struct SpikeCN {
 bandsolve_status spike_solve_device(const Factor& f, double* x, std::size_t n, std::size_t m, std::size_t ld,
                                     void* stream, int sms, bool* done, const PartPeriodic* per = nullptr,
                                     const SpikeCN* cn = nullptr);
+bandsolve_status spike_solve_device_f32(const Factor& f, float* x, std::size_t n, std::size_t m, std::size_t ld,
+                                        void* stream, int sms, bool* done);
 int pipe_warps(std::size_t n, std::size_t m, std::size_t ld, const void* x, bool pent, int sms, int* kb, int* rt,
                int* st, bool per = false);
 bandsolve_status pipe_solve_device(bool pent, bool fast, const void* fwd, const void* bwd, double* x, std::size_t n,

@@ -60,16 +60,17 @@ struct PartPlan {
   std::vector<double> rinv;                // R x R inverse of the interface matrix, row-major
   bool ok = false;                         // false: the plan broke down (sequential sweep instead)
   std::vector<std::pair<int, void*>> dev;  // device blobs
-  std::vector<std::pair<int, void*>> spike_dev;  // device blobs of the one-pass kernel's records
+  // device blobs of the one-pass kernel's records, keyed 2 device + (fp32 ? 1 : 0)
+  std::vector<std::pair<int, void*>> spike_dev;
   ~PartPlan() {
-    for (auto* list : {&dev, &spike_dev}) {
-      for (auto& d : *list) {
-        int prev = -1;
-        if (cudaGetDevice(&prev) == cudaSuccess && prev != d.first) cudaSetDevice(d.first);
-        cudaFree(d.second);
-        if (prev >= 0 && prev != d.first) cudaSetDevice(prev);
-      }
-    }
+    auto release = [](int device, void* ptr) {
+      int prev = -1;
+      if (cudaGetDevice(&prev) == cudaSuccess && prev != device) cudaSetDevice(device);
+      cudaFree(ptr);
+      if (prev >= 0 && prev != device) cudaSetDevice(prev);
+    };
+    for (auto& d : dev) release(d.first, d.second);
+    for (auto& d : spike_dev) release(d.first / 2, d.second);
     cudaGetLastError();
   }
 };
@@ -713,35 +714,45 @@ bandsolve_status partition_solve_device(const Factor& f, double* x, std::size_t 
 
 namespace {
 
-// Records of the one-pass kernel: [SpF x n][SpB x n] (the plan's block
-// factors, U^-1 rows and left-coupling images, interleaved per row).
-std::vector<double> spike_records(const PartPlan& p, int n) {
-  const bool pent = p.pent;
-  const int wf = pent ? 6 : 4, wb = pent ? 4 : 2;
-  std::vector<double> r(static_cast<std::size_t>(n) * (wf + wb), 0.0);
-  double* f = r.data();
-  double* b = r.data() + static_cast<std::size_t>(n) * wf;
-  for (int i = 0; i < n; ++i) {
-    const std::size_t u = static_cast<std::size_t>(i);
-    if (pent) {
-      f[6 * u + 0] = p.fwd[4 * u];      // eps/alpha
-      f[6 * u + 1] = p.fwd[4 * u + 1];  // beta/alpha
-      f[6 * u + 2] = p.fwd[4 * u + 2];  // 1/alpha
-      f[6 * u + 3] = p.pr[u];           // U^-1 row 0
-      f[6 * u + 4] = p.pr[n + u];       // U^-1 row 1
-      b[4 * u + 0] = p.bwd[2 * u];      // gamma
-      b[4 * u + 1] = p.bwd[2 * u + 1];  // delta
-      b[4 * u + 2] = p.fl[u];           // F (x_{s-2})
-      b[4 * u + 3] = p.fl[n + u];       // F (x_{s-1})
+// Records of the one-pass kernel: [SpF<T> x n][SpB<T> x n] (the plan's block
+// factors, U^-1 rows and left-coupling images, interleaved per row), then
+// R^-1 (R x R, row-major), all in T.
+template <typename T>
+std::vector<unsigned char> spike_blob(const PartPlan& p, int n) {
+  const std::size_t nf = static_cast<std::size_t>(n);
+  const std::size_t sf = p.pent ? sizeof(dev::SpF<T, true>) : sizeof(dev::SpF<T, false>);
+  const std::size_t sb = p.pent ? sizeof(dev::SpB<T, true>) : sizeof(dev::SpB<T, false>);
+  std::vector<unsigned char> blob(nf * (sf + sb) + p.rinv.size() * sizeof(T), 0);
+  for (std::size_t u = 0; u < nf; ++u) {
+    if (p.pent) {
+      dev::SpF<T, true> f{};
+      f.e = static_cast<T>(p.fwd[4 * u]);       // eps/alpha
+      f.b = static_cast<T>(p.fwd[4 * u + 1]);   // beta/alpha
+      f.ia = static_cast<T>(p.fwd[4 * u + 2]);  // 1/alpha
+      f.p0 = static_cast<T>(p.pr[u]);           // U^-1 row 0
+      f.p1 = static_cast<T>(p.pr[nf + u]);      // U^-1 row 1
+      dev::SpB<T, true> b{};
+      b.g = static_cast<T>(p.bwd[2 * u]);       // gamma
+      b.d = static_cast<T>(p.bwd[2 * u + 1]);   // delta
+      b.f1 = static_cast<T>(p.fl[u]);           // F (x_{s-2})
+      b.f2 = static_cast<T>(p.fl[nf + u]);      // F (x_{s-1})
+      std::memcpy(blob.data() + u * sf, &f, sf);
+      std::memcpy(blob.data() + nf * sf + u * sb, &b, sb);
     } else {
-      f[4 * u + 0] = p.fwd[2 * u];      // a/denom
-      f[4 * u + 1] = p.fwd[2 * u + 1];  // 1/denom
-      f[4 * u + 2] = p.pr[u];           // U^-1 row 0
-      b[2 * u + 0] = p.bwd[u];          // chat
-      b[2 * u + 1] = p.fl[u];           // F (x_{s-1})
+      dev::SpF<T, false> f{};
+      f.am = static_cast<T>(p.fwd[2 * u]);      // a/denom
+      f.m = static_cast<T>(p.fwd[2 * u + 1]);   // 1/denom
+      f.p0 = static_cast<T>(p.pr[u]);           // U^-1 row 0
+      dev::SpB<T, false> b{};
+      b.c = static_cast<T>(p.bwd[u]);           // chat
+      b.f1 = static_cast<T>(p.fl[u]);           // F (x_{s-1})
+      std::memcpy(blob.data() + u * sf, &f, sf);
+      std::memcpy(blob.data() + nf * sf + u * sb, &b, sb);
     }
   }
-  return r;
+  T* r = reinterpret_cast<T*>(blob.data() + nf * (sf + sb));
+  for (std::size_t i = 0; i < p.rinv.size(); ++i) r[i] = static_cast<T>(p.rinv[i]);
+  return blob;
 }
 
 // the plan for K blocks (cached on the factor), or nullptr when it broke down
@@ -776,14 +787,14 @@ namespace {
 // CTAs per cluster for K blocks (8 blocks per CTA beyond one CTA)
 int spike_cluster(int K) { return K > dev::kSpWarps ? K / dev::kSpWarps : 1; }
 
-int spike_ring_slots(int n, int K, bool pent, bool per) {
+int spike_ring_slots(int n, int K, bool pent, bool per, std::size_t elem) {
   const std::size_t cap = max_smem_per_block();
   const int CS = spike_cluster(K);
   const int Kc = CS > 1 ? dev::kSpWarps : K;
   const int nl = n / K * Kc;
   const int R = (pent ? 4 : 2) * K;
   for (int kb = 6; kb >= 2; --kb)
-    if (dev::SpikeLayout::make(nl, R, Kc, kb, pent, per).total <= cap) return kb;
+    if (dev::SpikeLayout::make(nl, R, Kc, kb, pent, per, elem).total <= cap) return kb;
   return 0;
 }
 
@@ -818,18 +829,26 @@ int spike_active_clusters(const void* kern, int CS, std::size_t smem, int sms) {
 
 }  // namespace
 
-int spike_blocks(std::size_t n, std::size_t m, std::size_t ld, const void* x, int sms, bool pent) {
+int spike_blocks(std::size_t n, std::size_t m, std::size_t ld, const void* x, int sms, bool pent, std::size_t elem) {
   const long long sel = tune_int("SPIKE", -1);  // 0: never, 1: whenever it applies
   if (sel == 0 || tune_flag("PLAN")) return 0;
-  if (current_mode() != BANDSOLVE_MODE_FAST || n > static_cast<std::size_t>(dev::kSpMaxK) * dev::kSpMaxL || m == 0)
-    return 0;
-  if (reinterpret_cast<uintptr_t>(x) % 16 != 0 || ld % 2 != 0 || m > static_cast<std::size_t>(INT_MAX) / 2) return 0;
-  if (m % 2 != 0) return 0;  // TMA boxes: an odd batch would straddle a 16-byte granule at the edge
+  const std::size_t maxl = elem == 8 ? dev::spike_max_rows<double>() : dev::spike_max_rows<float>();
+  if (current_mode() != BANDSOLVE_MODE_FAST || n > static_cast<std::size_t>(dev::kSpMaxK) * maxl || m == 0) return 0;
+  // TMA: 16-byte aligned base and pitch; the batch edge inside a 16-byte
+  // granule (odd fp64 / non-multiple-of-4 fp32 batches would straddle one)
+  const std::size_t gran = 16 / elem;
+  if (reinterpret_cast<uintptr_t>(x) % 16 != 0 || ld % gran != 0 || m > static_cast<std::size_t>(INT_MAX) / 2) return 0;
+  if (m % gran != 0) return 0;
+  // fp32 moves half the bytes per row through the same per-row work: the
+  // kernel runs at ~0.5 of the fp32 roofline, above the sequential plans only
+  // for long systems (tri 2^20 systems: N = 1024 / 4096 0.51 / 0.58 vs 0.43 /
+  // 0.40; N = 512: 0.50 vs 0.78)
+  if (elem == 4 && n < 1024 && sel != 1) return 0;
   const int kf = static_cast<int>(tune_int("SPIKE_K", 0));  // tuning override
   // K <= 8: one CTA holds every block; K = 16 / 32: a cluster of K / 8 CTAs
   int K = 0;
   for (int k = 2; k <= dev::kSpMaxK; k *= 2)
-    if (n % k == 0 && (n / k) % dev::kSpR == 0 && n / k <= static_cast<std::size_t>(dev::kSpMaxL) &&
+    if (n % k == 0 && (n / k) % dev::kSpR == 0 && n / k <= maxl &&
         n / k >= 2 * dev::kSpR && (kf == 0 || k == kf)) {
       K = k;
       break;
@@ -850,16 +869,20 @@ int spike_blocks(std::size_t n, std::size_t m, std::size_t ld, const void* x, in
            n / (2 * K) >= 2 * dev::kSpR)
       K *= 2;
   }
-  if (spike_ring_slots(static_cast<int>(n), K, pent, true) == 0) return 0;
+  if (spike_ring_slots(static_cast<int>(n), K, pent, elem == 8, elem) == 0) return 0;
   return K;
 }
 
-bandsolve_status spike_solve_device(const Factor& f, double* x, std::size_t n, std::size_t m, std::size_t ld,
-                                    void* stream, int sms, bool* done, const PartPeriodic* per, const SpikeCN* cn) {
+namespace {
+
+template <typename T>
+bandsolve_status spike_solve_t(const Factor& f, T* x, std::size_t n, std::size_t m, std::size_t ld, void* stream,
+                               int sms, bool* done, const PartPeriodic* per, const SpikeCN* cn) {
   *done = false;
   const bool pent = f.kind != Kind::Tri;
   if (cn && (!per || reinterpret_cast<uintptr_t>(cn->u) % 16 != 0)) return BANDSOLVE_OK;
-  const int K = spike_blocks(n, m, ld, x, sms, pent);
+  if (sizeof(T) != 8 && (per || cn)) return BANDSOLVE_OK;  // fp32: plain solves
+  const int K = spike_blocks(n, m, ld, x, sms, pent, sizeof(T));
   if (K == 0) return BANDSOLVE_OK;
   int device = 0;
   if (cudaGetDevice(&device) != cudaSuccess) {
@@ -872,55 +895,64 @@ bandsolve_status spike_solve_device(const Factor& f, double* x, std::size_t n, s
     std::lock_guard<std::mutex> lock(f.mu);
     p = cached_plan(f, K);
     if (!p) return BANDSOLVE_OK;  // a block pivot broke down or grew: the sequential sweep handles it
+    const int key = device * 2 + (sizeof(T) == 8 ? 0 : 1);  // one blob per device and precision
     for (auto& d : p->spike_dev)
-      if (d.first == device) blob = d.second;
+      if (d.first == key) blob = d.second;
     if (!blob) {
-      const std::vector<double> rec = spike_records(*p, static_cast<int>(n));
-      const std::size_t bytes = (rec.size() + p->rinv.size()) * sizeof(double);
-      if (cudaMalloc(&blob, bytes) != cudaSuccess) {
+      const std::vector<unsigned char> hb = spike_blob<T>(*p, static_cast<int>(n));
+      if (cudaMalloc(&blob, hb.size()) != cudaSuccess) {
         cudaGetLastError();
         return fail(BANDSOLVE_ERR_INTERNAL, "spike plan upload");
       }
-      if (upload_sync(blob, rec.data(), rec.size() * sizeof(double)) != cudaSuccess ||
-          upload_sync(static_cast<double*>(blob) + rec.size(), p->rinv.data(), p->rinv.size() * sizeof(double)) !=
-              cudaSuccess) {
+      if (upload_sync(blob, hb.data(), hb.size()) != cudaSuccess) {
         cudaGetLastError();
         cudaFree(blob);
         return fail(BANDSOLVE_ERR_INTERNAL, "spike plan upload");
       }
-      p->spike_dev.emplace_back(device, blob);
+      p->spike_dev.emplace_back(key, blob);
     }
   }
   const int N = static_cast<int>(n);
   const int CS = spike_cluster(K);
   const int Kc = CS > 1 ? dev::kSpWarps : K;
   const int R = p->R;
-  const int KB = spike_ring_slots(N, K, pent, per != nullptr);
-  const std::size_t rec_doubles = static_cast<std::size_t>(n) * (pent ? 10 : 6);
-  const double* rinv = static_cast<const double*>(blob) + rec_doubles;
+  const int KB = spike_ring_slots(N, K, pent, per != nullptr, sizeof(T));
+  const std::size_t rec_bytes =
+      static_cast<std::size_t>(n) * (pent ? sizeof(dev::SpF<T, true>) + sizeof(dev::SpB<T, true>)
+                                          : sizeof(dev::SpF<T, false>) + sizeof(dev::SpB<T, false>));
+  const T* rinv = reinterpret_cast<const T*>(static_cast<const unsigned char*>(blob) + rec_bytes);
   CUtensorMap map;
   // the tensor map reads b (in place: x; Crank-Nicolson: the old field u)
-  if (!encode_tile_map(&map, cn ? const_cast<double*>(cn->u) : x, sizeof(double), N, static_cast<long long>(m),
-                       static_cast<long long>(ld), 32, dev::kSpR))
+  void* src = cn ? const_cast<double*>(cn->u) : static_cast<void*>(x);
+  if (!encode_tile_map(&map, src, sizeof(T), N, static_cast<long long>(m), static_cast<long long>(ld), 32,
+                       dev::kSpR))
     return BANDSOLVE_OK;  // no tensor map: the sweep plans take it
   const int Wg = CS > 1 ? 32 : 32 * (dev::kSpWarps / K);
   const long long groups = (static_cast<long long>(m) + Wg - 1) / Wg;
-  const std::size_t smem = dev::SpikeLayout::make(N / K * Kc, R, Kc, KB, pent, per != nullptr).total;
+  const std::size_t smem = dev::SpikeLayout::make(N / K * Kc, R, Kc, KB, pent, per != nullptr, sizeof(T)).total;
   const int PD = static_cast<int>(tune_int("SPD", 4));
   auto s = static_cast<cudaStream_t>(stream);
-  using Kern = decltype(&dev::sweep_spike<true, true, true, 1>);
-  // [cluster size 1/2/4][cn][pent][per]
-#define BSB_SPIKE_SET(CSZ)                                                                                    \
-  {{{dev::sweep_spike<false, false, false, CSZ>, dev::sweep_spike<false, true, false, CSZ>},                 \
-    {dev::sweep_spike<true, false, false, CSZ>, dev::sweep_spike<true, true, false, CSZ>}},                  \
-   {{dev::sweep_spike<false, true, true, CSZ>, dev::sweep_spike<false, true, true, CSZ>},                    \
-    {dev::sweep_spike<true, true, true, CSZ>, dev::sweep_spike<true, true, true, CSZ>}}}
-  static const Kern kerns[3][2][2][2] = {BSB_SPIKE_SET(1), BSB_SPIKE_SET(2), BSB_SPIKE_SET(4)};
-#undef BSB_SPIKE_SET
+  using Kern = decltype(&dev::sweep_spike<T, true, false, false, 1>);
   const int csi = CS == 4 ? 2 : CS == 2 ? 1 : 0;
-  const int ki = csi * 8 + (cn ? 4 : 0) + (pent ? 2 : 0) + (per ? 1 : 0);
-  const Kern kern = kerns[csi][cn != nullptr][pent][per != nullptr];
-  static std::atomic<uint64_t> configured[24];
+  Kern kern;
+  if constexpr (sizeof(T) == 8) {
+    // [cluster size 1/2/4][cn][pent][per]
+#define BSB_SPIKE_SET(CSZ)                                                                                        \
+  {{{dev::sweep_spike<T, false, false, false, CSZ>, dev::sweep_spike<T, false, true, false, CSZ>},               \
+    {dev::sweep_spike<T, true, false, false, CSZ>, dev::sweep_spike<T, true, true, false, CSZ>}},                \
+   {{dev::sweep_spike<T, false, true, true, CSZ>, dev::sweep_spike<T, false, true, true, CSZ>},                  \
+    {dev::sweep_spike<T, true, true, true, CSZ>, dev::sweep_spike<T, true, true, true, CSZ>}}}
+    static const Kern kerns[3][2][2][2] = {BSB_SPIKE_SET(1), BSB_SPIKE_SET(2), BSB_SPIKE_SET(4)};
+#undef BSB_SPIKE_SET
+    kern = kerns[csi][cn != nullptr][pent][per != nullptr];
+  } else {  // fp32: plain solves
+    static const Kern kerns[3][2] = {{dev::sweep_spike<T, false, false, false, 1>, dev::sweep_spike<T, true, false, false, 1>},
+                                     {dev::sweep_spike<T, false, false, false, 2>, dev::sweep_spike<T, true, false, false, 2>},
+                                     {dev::sweep_spike<T, false, false, false, 4>, dev::sweep_spike<T, true, false, false, 4>}};
+    kern = kerns[csi][pent];
+  }
+  const int ki = (sizeof(T) == 8 ? 0 : 24) + csi * 8 + (cn ? 4 : 0) + (pent ? 2 : 0) + (per ? 1 : 0);
+  static std::atomic<uint64_t> configured[48];
   const uint64_t bit = device < 64 ? (1ull << device) : 0;
   std::atomic<uint64_t>& attr_set = configured[ki];
   dev::SpikePer sp;
@@ -941,7 +973,7 @@ bandsolve_status spike_solve_device(const Factor& f, double* x, std::size_t n, s
     if (bit) attr_set.fetch_or(bit, std::memory_order_relaxed);
   }
   // lanes past the batch edge write their values here (branch-free stores)
-  double* sink = dead_lane_sink(device);
+  T* sink = reinterpret_cast<T*>(dead_lane_sink(device));
   if (!sink) return fail(BANDSOLVE_ERR_INTERNAL, "spike scratch");
   const int active = spike_active_clusters(reinterpret_cast<const void*>(kern), CS, smem, sms);
   if (active <= 0) return BANDSOLVE_OK;  // the cluster does not fit: the sweep plans take it
@@ -974,6 +1006,18 @@ bandsolve_status spike_solve_device(const Factor& f, double* x, std::size_t n, s
   if (e != cudaSuccess) return fail(BANDSOLVE_ERR_INTERNAL, std::string("spike launch: ") + cudaGetErrorString(e));
   *done = true;
   return BANDSOLVE_OK;
+}
+
+}  // namespace
+
+bandsolve_status spike_solve_device(const Factor& f, double* x, std::size_t n, std::size_t m, std::size_t ld,
+                                    void* stream, int sms, bool* done, const PartPeriodic* per, const SpikeCN* cn) {
+  return spike_solve_t<double>(f, x, n, m, ld, stream, sms, done, per, cn);
+}
+
+bandsolve_status spike_solve_device_f32(const Factor& f, float* x, std::size_t n, std::size_t m, std::size_t ld,
+                                        void* stream, int sms, bool* done) {
+  return spike_solve_t<float>(f, x, n, m, ld, stream, sms, done, nullptr, nullptr);
 }
 
 }  // namespace bsb

@@ -1132,7 +1132,7 @@ bandsolve_status describe_plan(Kind kind, std::size_t n, std::size_t m, std::siz
   const bool fast = current_mode() == BANDSOLVE_MODE_FAST;
   const Plan p = choose_plan(n, m, ld, f32 ? 4 : 8, kProbe, pent, fast, sms);
   char buf[256];
-  const int KS = f32 ? 0 : spike_blocks(n, m, ld, kProbe, sms, pent);
+  const int KS = spike_blocks(n, m, ld, kProbe, sms, pent, f32 ? 4 : 8);
   const int K = f32 ? 0 : partition_blocks(n, m, sms, pent);
   int pkb = 0, prt = 0, pst = 0;
   const int PP = (f32 || KS > 0 || K > 0) ? 0 : pipe_warps(n, m, ld, kProbe, pent, sms, &pkb, &prt, &pst);
@@ -1185,6 +1185,11 @@ bandsolve_status solve_device(const Factor& f, void* x, bool f32, std::size_t n,
   const int q = fast ? 1 : 0;
   auto s = static_cast<cudaStream_t>(stream);
   const int sms = num_sms(device);
+  if (fast && f32) {  // fp32: the one-pass partitioned kernel in float (1e-5 contract)
+    bool done = false;
+    st = spike_solve_device_f32(f, static_cast<float*>(x), n, m, ld, stream, sms, &done);
+    if (st != BANDSOLVE_OK || done) return st;
+  }
   if (fast && !f32) {
     bool done = false;
     st = spike_solve_device(f, static_cast<double*>(x), n, m, ld, stream, sms, &done);

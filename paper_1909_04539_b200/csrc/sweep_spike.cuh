@@ -64,27 +64,31 @@ constexpr int kSpMaxL = 128;   // rows per block: 1 KB of TMEM lane per fp64 val
 constexpr int kSpMaxK = 32;    // blocks per system (a cluster of up to 4 CTAs)
 constexpr int kSpMaxCS = 4;    // CTAs per cluster
 
-// per-row records in shared memory, split by phase
-template <bool PENT>
+// per-row records in shared memory, split by phase (fp64 or fp32: the
+// fp32 kernel runs the same plan rounded to float)
+template <typename T, bool PENT>
 struct SpF;  // forward: fast records + U^-1 row entries
-template <>
-struct alignas(16) SpF<true> {
-  double e, b, ia, p0, p1, pad;  // e = eps/alpha, b = beta/alpha, ia = 1/alpha (block-local)
+template <typename T>
+struct alignas(16) SpF<T, true> {
+  T e, b, ia, p0, p1, pad;  // e = eps/alpha, b = beta/alpha, ia = 1/alpha (block-local)
 };
-template <>
-struct alignas(16) SpF<false> {
-  double am, m, p0, pad;  // am = a/denom, m = 1/denom
+template <typename T>
+struct alignas(16) SpF<T, false> {
+  T am, m, p0, pad;  // am = a/denom, m = 1/denom
 };
-template <bool PENT>
+template <typename T, bool PENT>
 struct SpB;  // backward: U entries + forward images of the left coupling
-template <>
-struct alignas(16) SpB<true> {
-  double g, d, f1, f2;  // gamma, delta, F (x_{s-2}), F (x_{s-1})
+template <typename T>
+struct alignas(16) SpB<T, true> {
+  T g, d, f1, f2;  // gamma, delta, F (x_{s-2}), F (x_{s-1})
 };
-template <>
-struct alignas(16) SpB<false> {
-  double c, f1;  // chat, F (x_{s-1})
+template <typename T>
+struct alignas(16) SpB<T, false> {
+  T c, f1;  // chat, F (x_{s-1})
 };
+// rows per block: one lane's TMEM share (256 columns) holds 128 fp64 / 256 fp32 values
+template <typename T>
+__host__ __device__ constexpr int spike_max_rows() { return 256 * 4 / static_cast<int>(sizeof(T)); }
 
 // periodic (Woodbury) correction fused into the backward sweep: x_i -=
 // z1_i t1 + z2_i t2, the coefficients from x_0, x_1, x_{n-2}, x_{n-1}, which
@@ -107,19 +111,24 @@ __host__ __device__ constexpr int spike_rinv_rows(int Kc, int nh) { return (Kc +
 
 struct SpikeLayout {
   size_t fwd_off, bwd_off, z_off, rinv_off, xch_off, ring_off, bar_off, total;
-  // nl: rows whose records this CTA holds; R: interface unknowns; Kc: blocks per CTA
-  __host__ __device__ static SpikeLayout make(int nl, int R, int Kc, int KB, bool pent, bool per = false) {
+  // nl: rows whose records this CTA holds; R: interface unknowns; Kc: blocks
+  // per CTA; elem: 8 (fp64) / 4 (fp32)
+  __host__ __device__ static SpikeLayout make(int nl, int R, int Kc, int KB, bool pent, bool per = false,
+                                              size_t elem = 8) {
     SpikeLayout L{};
+    const size_t sf = elem == 8 ? (pent ? sizeof(SpF<double, true>) : sizeof(SpF<double, false>))
+                                : (pent ? sizeof(SpF<float, true>) : sizeof(SpF<float, false>));
+    const size_t sb = elem == 8 ? (pent ? sizeof(SpB<double, true>) : sizeof(SpB<double, false>))
+                                : (pent ? sizeof(SpB<float, true>) : sizeof(SpB<float, false>));
     L.fwd_off = 0;
-    L.bwd_off = align128(static_cast<size_t>(nl) * (pent ? sizeof(SpF<true>) : sizeof(SpF<false>)));
-    L.z_off = L.bwd_off + align128(static_cast<size_t>(nl) * (pent ? sizeof(SpB<true>) : sizeof(SpB<false>)));
+    L.bwd_off = align128(static_cast<size_t>(nl) * sf);
+    L.z_off = L.bwd_off + align128(static_cast<size_t>(nl) * sb);
     // z of the periodic correction: [nl] pairs (pent) / values (tri)
     L.rinv_off = L.z_off + (per ? align128(static_cast<size_t>(nl) * (pent ? 2 : 1) * sizeof(double)) : 0);
-    L.xch_off = L.rinv_off +
-                align128(static_cast<size_t>(spike_rinv_rows(Kc, pent ? 2 : 1)) * R * sizeof(double));
+    L.xch_off = L.rinv_off + align128(static_cast<size_t>(spike_rinv_rows(Kc, pent ? 2 : 1)) * R * elem);
     // interface exchange, double-buffered: [2][warp][q][32 lanes]
-    L.ring_off = L.xch_off + align128(2ull * kSpWarps * (pent ? 4 : 2) * 32 * sizeof(double));
-    L.bar_off = L.ring_off + static_cast<size_t>(KB) * kSpWarps * kSpR * 32 * sizeof(double);
+    L.ring_off = L.xch_off + align128(2ull * kSpWarps * (pent ? 4 : 2) * 32 * elem);
+    L.bar_off = L.ring_off + static_cast<size_t>(KB) * kSpWarps * kSpR * 32 * elem;
     // ring barriers, the two cluster interface barriers, the TMEM base word
     L.total = L.bar_off + static_cast<size_t>(2 * KB + 3) * sizeof(uint64_t);
     return L;
@@ -141,6 +150,16 @@ __device__ __forceinline__ double ld_cluster_f64(uint32_t addr) {
   double v;
   asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
   return v;
+}
+__device__ __forceinline__ float ld_cluster_f32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+  return v;
+}
+template <typename T>
+__device__ __forceinline__ T ld_cluster(uint32_t addr) {
+  if constexpr (sizeof(T) == 8) return ld_cluster_f64(addr);
+  else return ld_cluster_f32(addr);
 }
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t remote_bar) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote_bar) : "memory");
@@ -164,13 +183,14 @@ __device__ __forceinline__ void cluster_sync_all() {
 // CS: CTAs per cluster (1; 2 / 4 for K = 16 / 32), a compile-time constant:
 // with a runtime CS the single-CTA kernel measured 30% slower (tri N = 512:
 // 0.68 vs 0.96 of the HBM roofline)
-template <bool PENT, bool PER, bool CN = false, int CS = 1>
+template <typename T, bool PENT, bool PER, bool CN = false, int CS = 1>
 __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
-    sweep_spike(const __grid_constant__ CUtensorMap map_b, double* __restrict__ x, int n, long long m, long long ld,
+    sweep_spike(const __grid_constant__ CUtensorMap map_b, T* __restrict__ x, int n, long long m, long long ld,
                 int K, int L, int KB, int PD, long long groups, const void* __restrict__ recs,
-                const double* __restrict__ rinv_g, double* __restrict__ sink, SpikePer per) {
-  using F = SpF<PENT>;
-  using B = SpB<PENT>;
+                const T* __restrict__ rinv_g, T* __restrict__ sink, SpikePer per) {
+  static_assert(sizeof(T) == 8 || (!PER && !CN), "fp32: plain solves only");
+  using F = SpF<T, PENT>;
+  using B = SpB<T, PENT>;
   constexpr int NQ = PENT ? 4 : 2;  // interface rows per block (top NH, bottom NH)
   constexpr int NH = NQ / 2;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -186,12 +206,12 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
   const int row0 = kb0 * L;   // first of them
   const long long cid = blockIdx.x / CS;  // cluster (group walker) index
   const long long ncl = gridDim.x / CS;
-  const SpikeLayout Ly = SpikeLayout::make(nl, R, Kc, KB, PENT, PER);
+  const SpikeLayout Ly = SpikeLayout::make(nl, R, Kc, KB, PENT, PER, sizeof(T));
   F* sf = reinterpret_cast<F*>(smem + Ly.fwd_off);
   B* sb = reinterpret_cast<B*>(smem + Ly.bwd_off);
-  double* srinv = reinterpret_cast<double*>(smem + Ly.rinv_off);
-  double* xch = reinterpret_cast<double*>(smem + Ly.xch_off);
-  double* ring = reinterpret_cast<double*>(smem + Ly.ring_off);
+  T* srinv = reinterpret_cast<T*>(smem + Ly.rinv_off);
+  T* xch = reinterpret_cast<T*>(smem + Ly.xch_off);
+  T* ring = reinterpret_cast<T*>(smem + Ly.ring_off);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + Ly.bar_off);
   uint64_t* empty = full + KB;
   // cluster interface barriers (CS > 1), one per group parity: a warp's
@@ -285,7 +305,7 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
         if (t >= KB) mbar_wait(&empty[slot], phase ^ 1u);
         int c0, c;
         chunk_at(t, c0, c);
-        mbar_expect_tx(&full[slot], kChunk * sizeof(double));
+        mbar_expect_tx(&full[slot], kChunk * sizeof(T));
         for (int w = 0; w < kSpWarps; ++w)
           tma_load_2d(ring + slot * kChunk + w * kBox, &map_b, c0 + gs_of(w) * 32, blk_of(w) * L + c * kSpR,
                       &full[slot], pol);
@@ -304,7 +324,7 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
     const uint32_t tlane = tmem_base_s + (static_cast<uint32_t>(32 * (warp & 3)) << 16) +
                            static_cast<uint32_t>((warp >> 2) * 256);
     auto tslot = [&](uint32_t p, int c) {
-      return tlane + static_cast<uint32_t>((p ? CL - 1 - c : c) * TPiece<double>::kWords);
+      return tlane + static_cast<uint32_t>((p ? CL - 1 - c : c) * TPiece<T>::kWords);
     };
     int slot = 0;
     uint32_t phase = 0;
@@ -314,11 +334,11 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
     const double* zk = reinterpret_cast<const double*>(smem + Ly.z_off) + (PENT ? 2 : 1) * rl;
 
     // forward state of the group being read, backward state of the one being written
-    double fs1 = 0.0, fs2 = 0.0, a0 = 0.0, a1 = 0.0;
-    double bs1 = 0.0, bs2 = 0.0, xl1 = 0.0, xl2 = 0.0, t1 = 0.0, t2 = 0.0;
+    T fs1 = T(0), fs2 = T(0), a0 = T(0), a1 = T(0);
+    T bs1 = T(0), bs2 = T(0), xl1 = T(0), xl2 = T(0), t1 = T(0), t2 = T(0);
     long long step = 0;
-    double* out = sink + lane;
-    TPiece<double> cur;
+    T* out = sink + lane;
+    TPiece<T> cur;
 
     // CN: the stencil's halo rows. h1/h2 = u at the two rows above the chunk
     // (carried from the previous chunk; block starts load them), la0/la1 = the
@@ -346,10 +366,10 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
 
     auto fwd_chunk = [&](int c, uint32_t p, long long g) {
       mbar_wait(&full[slot], phase);
-      const double* blk = ring + slot * kChunk + warp * kBox + lane;
+      const T* blk = ring + slot * kChunk + warp * kBox + lane;
       const F* fc = fk + c * kSpR;
-      TPiece<double> buf;
-      double dv[kSpR];  // stage 1: b / pivot for the whole chunk (off the chain)
+      TPiece<T> buf;
+      T dv[kSpR];  // stage 1: b / pivot for the whole chunk (off the chain)
       if constexpr (CN) {
         if (c == 0) {
           h2 = nh2;
@@ -399,7 +419,7 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
 #pragma unroll
       for (int r = 0; r < kSpR; ++r) {  // stage 2: one FMA per row on the chain
         const F f = fc[r];
-        double v;
+        T v;
         if constexpr (PENT) {
           v = fma(-f.b, fs1, fma(-f.e, fs2, dv[r]));
           a1 = fma(f.p1, v, a1);
@@ -414,7 +434,7 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
       buf.store(tslot(p, c));
     };
 
-    auto corr = [&](int i, double v) {  // stored value of local row i (periodic correction)
+    auto corr = [&](int i, T v) {  // stored value of local row i (periodic correction)
       if constexpr (!PER) return v;
       else if constexpr (PENT) return fma(-zk[2 * i], t1, fma(-zk[2 * i + 1], t2, v));
       else return fma(-zk[i], t1, v);
@@ -422,7 +442,7 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
 
     // interface of the group just read (xch parity p): its backward state
     auto interface = [&](long long g, uint32_t p) {
-      double* xw = xch + (static_cast<size_t>(p) * kSpWarps + warp) * NQ * 32 + lane;
+      T* xw = xch + (static_cast<size_t>(p) * kSpWarps + warp) * NQ * 32 + lane;
       xw[0] = a0;
       if constexpr (PENT) {
         xw[32] = a1;
@@ -431,7 +451,7 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
       } else {
         xw[32] = fs1;
       }
-      fs1 = fs2 = a0 = a1 = 0.0;
+      fs1 = fs2 = a0 = a1 = T(0);
       if (CS == 1) {
         asm volatile("bar.sync 1, %0;" ::"r"(kSpWarps * 32) : "memory");
       } else {  // every warp of every CTA of the cluster has published its values
@@ -450,32 +470,32 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
         rows[h] = h < NH       ? (k - kb0 + 1) * NH + h
                   : h < 2 * NH ? (k - kb0) * NH + (h - NH)
                                : (Kc + 1) * NH + (h - 2 * NH);
-      double zu[NU];
+      T zu[NU];
 #pragma unroll
-      for (int h = 0; h < NU; ++h) zu[h] = 0.0;
+      for (int h = 0; h < NU; ++h) zu[h] = T(0);
       const uint32_t xbase = smem_u32(xch + static_cast<size_t>(p) * kSpWarps * NQ * 32 + lane);
       for (int kk = 0; kk < K; ++kk) {
-        double yv[NQ];
+        T yv[NQ];
         if (CS == 1) {
-          const double* src = xch + ((static_cast<size_t>(p) * kSpWarps + gs * K + kk) * NQ) * 32 + lane;
+          const T* src = xch + ((static_cast<size_t>(p) * kSpWarps + gs * K + kk) * NQ) * 32 + lane;
 #pragma unroll
           for (int q = 0; q < NQ; ++q) yv[q] = src[q * 32];
         } else {
-          const uint32_t a = map_rank(xbase + static_cast<uint32_t>(((kk % kSpWarps) * NQ) * 32 * sizeof(double)),
+          const uint32_t a = map_rank(xbase + static_cast<uint32_t>(((kk % kSpWarps) * NQ) * 32 * sizeof(T)),
                                       static_cast<uint32_t>(kk / kSpWarps));
 #pragma unroll
-          for (int q = 0; q < NQ; ++q) yv[q] = ld_cluster_f64(a + static_cast<uint32_t>(q * 32 * sizeof(double)));
+          for (int q = 0; q < NQ; ++q) yv[q] = ld_cluster<T>(a + static_cast<uint32_t>(q * 32 * sizeof(T)));
         }
 #pragma unroll
         for (int h = 0; h < NU; ++h) {
-          const double* rr = srinv + static_cast<size_t>(rows[h]) * R + kk * NQ;
+          const T* rr = srinv + static_cast<size_t>(rows[h]) * R + kk * NQ;
 #pragma unroll
           for (int q = 0; q < NQ; ++q) zu[h] = fma(rr[q], yv[q], zu[h]);
         }
       }
       if (k == 0) {  // no left neighbour
 #pragma unroll
-        for (int h = NH; h < 2 * NH; ++h) zu[h] = 0.0;
+        for (int h = NH; h < 2 * NH; ++h) zu[h] = T(0);
       }
       if constexpr (PENT) {
         bs1 = zu[0];  // x_{L-2}
@@ -514,7 +534,7 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
       constexpr int kTop = decltype(first)::value ? kSpR - 1 - NH : kSpR - 1;  // skip the interface rows
       cur.wait();
       const B* bc = bk + c * kSpR;
-      double gv[kSpR];  // stage 1: left-coupling update (off the chain)
+      T gv[kSpR];  // stage 1: left-coupling update (off the chain)
 #pragma unroll
       for (int r = 0; r <= kTop; ++r) {
         if constexpr (PENT) gv[r] = fma(-bc[r].f1, xl2, fma(-bc[r].f2, xl1, cur.get(r)));
@@ -522,7 +542,7 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
       }
 #pragma unroll
       for (int r = kTop; r >= 0; --r) {  // stage 2: one FMA per row on the chain
-        double v;
+        T v;
         if constexpr (PENT) v = fma(-bc[r].g, bs1, fma(-bc[r].d, bs2, gv[r]));
         else v = fma(-bc[r].c, bs1, gv[r]);
         bs2 = bs1;

@@ -206,3 +206,31 @@ def test_spike_cn_step_within_tolerance(lib, oracle, cuda_device, n):
             assert np.all(np.isnan(out[:, m:]))
             assert per_system_max_rel(out[:, :m], want) <= TOL_F64, (prob, n, m, ld)
             assert np.array_equal(du[:, :m].cpu().numpy(), u)
+
+
+@pytest.mark.parametrize("n", [256, 512, 1024, 2048, 4096])
+def test_spike_fp32_within_tolerance(lib, oracle, cuda_device, n):
+    """fp32 batches: the same plan rounded to float (records, R^-1, TMEM
+    storage of up to 256 fp32 rows per lane), within the 1e-5 fp32 contract
+    of the fp64 reference solution."""
+    torch = cuda_device
+    lib.tune("SPIKE", "1")
+    rng = np.random.default_rng(n + 3)
+    for m, ld in [(64, 64), (300, 304)]:
+        rhs = rng.uniform(-1, 1, (n, m))
+        for cls, bands in [(bs.TriFactor, bs.diffusion_bands(1.0, n)), (bs.TriFactor, _random_tri(rng, n)),
+                           (bs.PentFactor, bs.hyper_bands(1.0, n)), (bs.PentFactor, _random_pent(rng, n))]:
+            pent = cls is bs.PentFactor
+            assert lib.describe_plan(1 if pent else 0, n, m, ld, True).startswith("spike"), (n, m)
+            want = (oracle.pent_solve(oracle.pent_prefactor(*bands), rhs.copy()) if pent
+                    else oracle.tri_solve(oracle.tri_prefactor(*bands), rhs.copy()))
+            buf = torch.full((n, ld), float("nan"), dtype=torch.float32, device="cuda")
+            buf[:, :m] = torch.from_numpy(rhs.astype(np.float32)).cuda()
+            before = lib.kernel_launches()
+            cls(lib, *bands).solve_dev(buf.data_ptr(), n, m, ld=ld, stream=torch.cuda.current_stream().cuda_stream,
+                                       f32=True)
+            torch.cuda.synchronize()
+            assert lib.kernel_launches() - before == 1
+            out = buf.cpu().numpy()
+            assert np.all(np.isnan(out[:, m:]))
+            assert per_system_max_rel(out[:, :m].astype(np.float64), want) <= 1e-5, (n, m, pent)
