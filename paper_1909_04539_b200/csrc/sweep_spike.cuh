@@ -34,8 +34,8 @@
 // Systems longer than 8 blocks (N = 2048, 4096: K = 16, 32) span a thread-
 // block CLUSTER of K / 8 CTAs, one per SM: each CTA holds 8 blocks of the
 // same 32 systems in its TMEM, the interface values travel through
-// distributed shared memory (ld.shared::cluster) after a cluster-scope
-// mbarrier, and each CTA keeps only the R^-1 rows its blocks need.
+// distributed shared memory (ld.shared::cluster) after the hardware cluster
+// barrier, and each CTA keeps only the R^-1 rows its blocks need.
 //
 // Software pipeline across groups: after the interface solve of group g a
 // warp interleaves, chunk by chunk, the backward sweep of g with the forward
@@ -129,8 +129,8 @@ struct SpikeLayout {
     // interface exchange, double-buffered: [2][warp][q][32 lanes]
     L.ring_off = L.xch_off + align128(2ull * kSpWarps * (pent ? 4 : 2) * 32 * elem);
     L.bar_off = L.ring_off + static_cast<size_t>(KB) * kSpWarps * kSpR * 32 * elem;
-    // ring barriers, the two cluster interface barriers, the TMEM base word
-    L.total = L.bar_off + static_cast<size_t>(2 * KB + 3) * sizeof(uint64_t);
+    // ring barriers, the TMEM base word
+    L.total = L.bar_off + static_cast<size_t>(2 * KB + 1) * sizeof(uint64_t);
     return L;
   }
 };
@@ -161,21 +161,6 @@ __device__ __forceinline__ T ld_cluster(uint32_t addr) {
   if constexpr (sizeof(T) == 8) return ld_cluster_f64(addr);
   else return ld_cluster_f32(addr);
 }
-__device__ __forceinline__ void mbar_arrive_cluster(uint32_t remote_bar) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote_bar) : "memory");
-}
-__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
-  uint32_t ok = 0;
-  while (!ok)
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void fence_cluster() { asm volatile("fence.acq_rel.cluster;" ::: "memory"); }
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -214,10 +199,7 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
   T* ring = reinterpret_cast<T*>(smem + Ly.ring_off);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + Ly.bar_off);
   uint64_t* empty = full + KB;
-  // cluster interface barriers (CS > 1), one per group parity: a warp's
-  // arrival for group g + 1 can never land in the phase of group g
-  uint64_t* ibar = empty + KB;
-  uint32_t& tmem_base_s = *reinterpret_cast<uint32_t*>(ibar + 2);
+  uint32_t& tmem_base_s = *reinterpret_cast<uint32_t*>(empty + KB);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   constexpr int kBox = kSpR * 32;          // elements of one warp's box
@@ -263,8 +245,6 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kSpWarps);
     }
-    mbar_init(&ibar[0], CS * kSpWarps);
-    mbar_init(&ibar[1], CS * kSpWarps);
     fence_barrier_init();
   }
   if (warp == 0) tmem_alloc_512(&tmem_base_s);
@@ -284,6 +264,9 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
   auto gs_of = [&](int w) { return CS > 1 ? 0 : w / K; };
 
   if (warp == kSpWarps) {  // ---- producer: b chunks through the ring
+    // (clusters: the other lanes exit, which takes them out of the cluster
+    // barrier; lane 0 arrives once per group, see below)
+    if (CS > 1 && lane != 0) return;
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
       const long long my_groups = (groups - cid + ncl - 1) / ncl;
@@ -313,6 +296,21 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
           slot = 0;
           phase ^= 1u;
         }
+        if constexpr (CS > 1) {
+          // one arrival per group's interface barrier (split phase: the wait
+          // for the previous group's comes just before the next arrival, so
+          // the ring keeps filling across the barrier)
+          if (c == CL - 1) {
+            if (t >= CL) asm volatile("barrier.cluster.wait.acquire;" ::: "memory");
+            asm volatile("barrier.cluster.arrive.release;" ::: "memory");
+          }
+        }
+      }
+      if constexpr (CS > 1) {
+        if (total > 0) asm volatile("barrier.cluster.wait.acquire;" ::: "memory");
+        // the final cluster barrier (below) for this lane
+        asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
+        return;
       }
     }
   } else {
@@ -328,7 +326,6 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
     };
     int slot = 0;
     uint32_t phase = 0;
-    uint32_t iphase = 0;  // bit p: phase parity of interface barrier p
     const F* fk = sf + rl;
     const B* bk = sb + rl;
     const double* zk = reinterpret_cast<const double*>(smem + Ly.z_off) + (PENT ? 2 : 1) * rl;
@@ -455,11 +452,10 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
       if (CS == 1) {
         asm volatile("bar.sync 1, %0;" ::"r"(kSpWarps * 32) : "memory");
       } else {  // every warp of every CTA of the cluster has published its values
-        fence_cluster();
-        __syncwarp();
-        if (lane < CS) mbar_arrive_cluster(map_rank(smem_u32(&ibar[p]), static_cast<uint32_t>(lane)));
-        mbar_wait_cluster(&ibar[p], (iphase >> p) & 1u);
-        iphase ^= 1u << p;
+        // the hardware cluster barrier (every compute thread of every CTA,
+        // plus each producer's one arrival per group)
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" :::
+                         "memory");
       }
       // x interface unknowns needed here, streamed over the R y values:
       // [own bottom NH | left bottom NH | (PER) first NH | last NH]
@@ -581,7 +577,7 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
     }
   }
   // a CTA's shared memory must outlive the cluster's remote reads of it
-  if (CS > 1) cluster_sync_all();
+  if constexpr (CS > 1) cluster_sync_all();
 }
 
 }  // namespace dev

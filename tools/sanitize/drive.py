@@ -67,8 +67,47 @@ def fam_other_plans():
         sweep({"PLAN": p}, bs.MODE_EXACT, [(300, 100, 100)], 0.0)
 
 
-def fam_spike():
-    sweep({"SPIKE": "1"}, bs.MODE_FAST, [(512, 300, 302), (1024, 64, 64)], 1e-12)
+def fam_spike():  # single CTA (K = 4, 8) and clusters of 2 / 4 CTAs (K = 16, 32)
+    sweep({"SPIKE": "1"}, bs.MODE_FAST, [(512, 300, 302), (1024, 64, 64), (2048, 64, 64), (4096, 32, 32)], 1e-12)
+
+
+def fam_spike_variants():  # periodic and CN fused, fp32
+    rng = np.random.default_rng(5)
+    lib.tune_reset()
+    lib.tune("SPIKE", "1")
+    lib.set_mode(bs.MODE_FAST)
+    n, m = 512, 64
+    x = rng.uniform(-1, 1, (n, m))
+    p = bs.PeriodicPent(lib, 1.0, -4.0, 7.0, -4.0, 1.0, n)
+    check(dev_solve(p, x, m), orc.periodic_pent_solve(orc.periodic_pent_prepare(1.0, -4.0, 7.0, -4.0, 1.0, n),
+                                                      x.copy()), 1e-12, "spike periodic pent")
+    u = torch.from_numpy(x).cuda()
+    out = torch.empty_like(u)
+    p.cn_step_dev(0.61, u.data_ptr(), out.data_ptr(), n, m, stream=stream)
+    torch.cuda.synchronize()
+    b32 = torch.from_numpy(x.astype(np.float32)).cuda()
+    bs.TriFactor(lib, *bs.diffusion_bands(1.0, 1024)).solve_dev(
+        torch.from_numpy(rng.uniform(-1, 1, (1024, 64)).astype(np.float32)).cuda().data_ptr(), 1024, 64, ld=64,
+        stream=stream, f32=True)
+    torch.cuda.synchronize()
+    del b32
+    print("spike variants ok", flush=True)
+    lib.tune_reset()
+    lib.set_mode(bs.MODE_EXACT)
+
+
+def fam_pipe():  # TMEM only, TMEM + registers + smem, L2 tier, periodic fused (exact)
+    sweep({"PIPE": "1"}, bs.MODE_EXACT, [(256, 128, 128), (512, 200, 202)], 0.0)
+    sweep({"PIPE": "1", "PIPE_MAX_N": "1024"}, bs.MODE_EXACT, [(1024, 64, 64)], 0.0)
+    rng = np.random.default_rng(6)
+    lib.tune_reset()
+    lib.tune("PIPE", "1")
+    n, m = 512, 64
+    x = rng.uniform(-1, 1, (n, m))
+    p = bs.PeriodicTri(lib, -1.0, 3.0, -1.0, n)
+    check(dev_solve(p, x, m), orc.periodic_tri_solve(orc.periodic_tri_prepare(-1.0, 3.0, -1.0, n), x.copy()), 0.0,
+          "pipe periodic tri (exact)")
+    lib.tune_reset()
 
 
 def fam_partition():
