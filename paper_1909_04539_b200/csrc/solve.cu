@@ -714,9 +714,18 @@ cudaError_t launch_stream_v(const Plan& plan, T* x, int n, long long m, long lon
     cudaError_t e = pool_malloc_async(reinterpret_cast<void**>(&scratch), bytes, s);
     if (e != cudaSuccess) return e;
   }
+  // the scratch as rows of 32 V elements for the reload TMA (box: one chunk of all warps)
+  CUtensorMap map_s = map;
+  if (scratch) {
+    const long long rows = grid * static_cast<long long>(P) * (spilled_rows / dev::kSR) * dev::kSR;
+    if (!encode_map(&map_s, scratch, sizeof(T), rows, 32 * V, 32 * V, 32 * V, dev::kSR * P)) {
+      cudaFreeAsync(scratch, s);
+      return cudaErrorInvalidValue;
+    }
+  }
   kern<<<static_cast<unsigned>(grid), (P + 2) * 32, plan.smem_bytes, s>>>(map, x, n, m, ld, plan.H, plan.TC, plan.KB,
                                                                          plan.KR, plan.PD, plan.stagger_ns, groups, fwd, bwd,
-                                                                         scratch, per);
+                                                                         scratch, per, map_s);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();
   if (scratch) {

@@ -379,7 +379,7 @@ __global__ void __launch_bounds__(stream_threads(V, TM), 1)
     sweep_stream(const __grid_constant__ CUtensorMap map_b, T* __restrict__ x, int n, long long m, long long ld,
                  int H, int TC, int KB, int KR, int PD, int stagger_ns, long long groups,
                  const void* __restrict__ fwd_g, const void* __restrict__ bwd_g, T* __restrict__ scratch,
-                 const PerArgs per) {
+                 const PerArgs per, const __grid_constant__ CUtensorMap map_s) {
   static_assert(PER == 0 || (FAST && sizeof(T) == 8 && (PER == 2) == PENT), "fused periodic: fast fp64 only");
   static_assert(!CN || sizeof(T) == 8, "fused Crank-Nicolson: fp64 only");
   static_assert(!TM || V == 1, "TMEM tier: one system per lane");
@@ -423,6 +423,12 @@ __global__ void __launch_bounds__(stream_threads(V, TM), 1)
   // reused by every group; spill chunk c lives at (c - HT)
   T* const spill_cta = scratch + static_cast<long long>(blockIdx.x) * HS * chunk - static_cast<long long>(HT) * chunk;
   const bool use_tmem = TM && (RTc > 0 || RCc > 0);
+  // the spill comes back through 2D TMA loads over the scratch viewed as
+  // rows of 32 V elements (map_s, box {32 V, 16 P}): chunk c of this CTA
+  // starts at this row
+  auto spill_row = [&](int c) {
+    return static_cast<int>((static_cast<long long>(blockIdx.x) * HS + (c - HT)) * P * kSR);
+  };
   uint32_t& tmem_base_s = *reinterpret_cast<uint32_t*>(spilled + 1);  // written by tcgen05.alloc
 
   {  // factor records -> smem (16-byte words; device arrays padded to 256 B)
@@ -543,8 +549,7 @@ __global__ void __launch_bounds__(stream_threads(V, TM), 1)
         for (int c = HC - 1; c >= HT; --c) {
           if (issued >= static_cast<uint32_t>(KB)) mbar_wait(&b_empty[cur.slot], cur.phase ^ 1u);
           mbar_expect_tx(&b_full[cur.slot], c_bytes);
-          bulk_load(bring + cur.slot * chunk, spill_cta + static_cast<long long>(c) * chunk, c_bytes,
-                    &b_full[cur.slot], pol_keep);
+          tma_load_2d(bring + cur.slot * chunk, &map_s, 0, spill_row(c), &b_full[cur.slot], pol_keep);
           cur.next(KB);
           ++issued;
         }
@@ -573,8 +578,7 @@ __global__ void __launch_bounds__(stream_threads(V, TM), 1)
       for (int c = HC - 1; c >= HT; --c) {
         if (issued >= static_cast<uint32_t>(KR)) mbar_wait(&r_empty[cur.slot], cur.phase ^ 1u);
         mbar_expect_tx(&r_full[cur.slot], c_bytes);
-        bulk_load(rring + cur.slot * chunk, spill_cta + static_cast<long long>(c) * chunk, c_bytes,
-                  &r_full[cur.slot], pol_keep);
+        tma_load_2d(rring + cur.slot * chunk, &map_s, 0, spill_row(c), &r_full[cur.slot], pol_keep);
         cur.next(KR);
         ++issued;
       }
