@@ -787,14 +787,14 @@ namespace {
 // CTAs per cluster for K blocks (8 blocks per CTA beyond one CTA)
 int spike_cluster(int K) { return K > dev::kSpWarps ? K / dev::kSpWarps : 1; }
 
-int spike_ring_slots(int n, int K, bool pent, bool per, std::size_t elem) {
+int spike_ring_slots(int n, int K, bool pent, bool per, std::size_t elem, std::size_t rec = 0) {
   const std::size_t cap = max_smem_per_block();
   const int CS = spike_cluster(K);
   const int Kc = CS > 1 ? dev::kSpWarps : K;
   const int nl = n / K * Kc;
   const int R = (pent ? 4 : 2) * K;
   for (int kb = 6; kb >= 2; --kb)
-    if (dev::SpikeLayout::make(nl, R, Kc, kb, pent, per, elem).total <= cap) return kb;
+    if (dev::SpikeLayout::make(nl, R, Kc, kb, pent, per, elem, rec).total <= cap) return kb;
   return 0;
 }
 
@@ -832,18 +832,21 @@ int spike_active_clusters(const void* kern, int CS, std::size_t smem, int sms) {
 int spike_blocks(std::size_t n, std::size_t m, std::size_t ld, const void* x, int sms, bool pent, std::size_t elem) {
   const long long sel = tune_int("SPIKE", -1);  // 0: never, 1: whenever it applies
   if (sel == 0 || tune_flag("PLAN")) return 0;
-  const std::size_t maxl = elem == 8 ? dev::spike_max_rows<double>() : dev::spike_max_rows<float>();
+  // fp32 runs as pairs of adjacent systems per lane (8 bytes, like fp64)
+  const bool fp32 = elem == 4;
+  const std::size_t maxl = dev::spike_max_rows<double>();
   if (current_mode() != BANDSOLVE_MODE_FAST || n > static_cast<std::size_t>(dev::kSpMaxK) * maxl || m == 0) return 0;
   // TMA: 16-byte aligned base and pitch; the batch edge inside a 16-byte
   // granule (odd fp64 / non-multiple-of-4 fp32 batches would straddle one)
   const std::size_t gran = 16 / elem;
   if (reinterpret_cast<uintptr_t>(x) % 16 != 0 || ld % gran != 0 || m > static_cast<std::size_t>(INT_MAX) / 2) return 0;
   if (m % gran != 0) return 0;
+  if (fp32) m /= 2;
   // fp32 moves half the bytes per row through the same per-row work: the
   // kernel runs at ~0.5 of the fp32 roofline, above the sequential plans only
   // for long systems (tri 2^20 systems: N = 1024 / 4096 0.51 / 0.58 vs 0.43 /
   // 0.40; N = 512: 0.50 vs 0.78)
-  if (elem == 4 && n < 1024 && sel != 1) return 0;
+  if (fp32 && n < static_cast<std::size_t>(tune_int("SPIKE_F32_MIN_N", 0)) && sel != 1) return 0;
   const int kf = static_cast<int>(tune_int("SPIKE_K", 0));  // tuning override
   // K <= 8: one CTA holds every block; K = 16 / 32: a cluster of K / 8 CTAs
   int K = 0;
@@ -869,7 +872,7 @@ int spike_blocks(std::size_t n, std::size_t m, std::size_t ld, const void* x, in
            n / (2 * K) >= 2 * dev::kSpR)
       K *= 2;
   }
-  if (spike_ring_slots(static_cast<int>(n), K, pent, elem == 8, elem) == 0) return 0;
+  if (spike_ring_slots(static_cast<int>(n), K, pent, !fp32, 8, fp32 ? 4 : 8) == 0) return 0;
   return K;
 }
 
@@ -881,8 +884,15 @@ bandsolve_status spike_solve_t(const Factor& f, T* x, std::size_t n, std::size_t
   *done = false;
   const bool pent = f.kind != Kind::Tri;
   if (cn && (!per || reinterpret_cast<uintptr_t>(cn->u) % 16 != 0)) return BANDSOLVE_OK;
-  if (sizeof(T) != 8 && (per || cn)) return BANDSOLVE_OK;  // fp32: plain solves
-  const int K = spike_blocks(n, m, ld, x, sms, pent, sizeof(T));
+  // fp32: two adjacent systems per lane (T = float2), plain solves only
+  constexpr bool kPair = std::is_same<T, float2>::value;
+  using S = dev::Scalar<T>;
+  if (kPair && (per || cn)) return BANDSOLVE_OK;
+  const int K = spike_blocks(n, m, ld, x, sms, pent, kPair ? 4 : sizeof(T));
+  if (kPair) {  // the kernel sees pairs
+    m /= 2;
+    ld /= 2;
+  }
   if (K == 0) return BANDSOLVE_OK;
   int device = 0;
   if (cudaGetDevice(&device) != cudaSuccess) {
@@ -895,11 +905,11 @@ bandsolve_status spike_solve_t(const Factor& f, T* x, std::size_t n, std::size_t
     std::lock_guard<std::mutex> lock(f.mu);
     p = cached_plan(f, K);
     if (!p) return BANDSOLVE_OK;  // a block pivot broke down or grew: the sequential sweep handles it
-    const int key = device * 2 + (sizeof(T) == 8 ? 0 : 1);  // one blob per device and precision
+    const int key = device * 2 + (sizeof(S) == 8 ? 0 : 1);  // one blob per device and precision
     for (auto& d : p->spike_dev)
       if (d.first == key) blob = d.second;
     if (!blob) {
-      const std::vector<unsigned char> hb = spike_blob<T>(*p, static_cast<int>(n));
+      const std::vector<unsigned char> hb = spike_blob<S>(*p, static_cast<int>(n));
       if (cudaMalloc(&blob, hb.size()) != cudaSuccess) {
         cudaGetLastError();
         return fail(BANDSOLVE_ERR_INTERNAL, "spike plan upload");
@@ -916,11 +926,11 @@ bandsolve_status spike_solve_t(const Factor& f, T* x, std::size_t n, std::size_t
   const int CS = spike_cluster(K);
   const int Kc = CS > 1 ? dev::kSpWarps : K;
   const int R = p->R;
-  const int KB = spike_ring_slots(N, K, pent, per != nullptr, sizeof(T));
+  const int KB = spike_ring_slots(N, K, pent, per != nullptr, sizeof(T), sizeof(S));
   const std::size_t rec_bytes =
-      static_cast<std::size_t>(n) * (pent ? sizeof(dev::SpF<T, true>) + sizeof(dev::SpB<T, true>)
-                                          : sizeof(dev::SpF<T, false>) + sizeof(dev::SpB<T, false>));
-  const T* rinv = reinterpret_cast<const T*>(static_cast<const unsigned char*>(blob) + rec_bytes);
+      static_cast<std::size_t>(n) * (pent ? sizeof(dev::SpF<S, true>) + sizeof(dev::SpB<S, true>)
+                                          : sizeof(dev::SpF<S, false>) + sizeof(dev::SpB<S, false>));
+  const S* rinv = reinterpret_cast<const S*>(static_cast<const unsigned char*>(blob) + rec_bytes);
   CUtensorMap map;
   // the tensor map reads b (in place: x; Crank-Nicolson: the old field u)
   void* src = cn ? const_cast<double*>(cn->u) : static_cast<void*>(x);
@@ -929,13 +939,15 @@ bandsolve_status spike_solve_t(const Factor& f, T* x, std::size_t n, std::size_t
     return BANDSOLVE_OK;  // no tensor map: the sweep plans take it
   const int Wg = CS > 1 ? 32 : 32 * (dev::kSpWarps / K);
   const long long groups = (static_cast<long long>(m) + Wg - 1) / Wg;
-  const std::size_t smem = dev::SpikeLayout::make(N / K * Kc, R, Kc, KB, pent, per != nullptr, sizeof(T)).total;
+  const std::size_t smem =
+      dev::SpikeLayout::make(N / K * Kc, R, Kc, KB, pent, per != nullptr, sizeof(T), sizeof(S)).total;
   const int PD = static_cast<int>(tune_int("SPD", 4));
   auto s = static_cast<cudaStream_t>(stream);
   using Kern = decltype(&dev::sweep_spike<T, true, false, false, 1>);
+  static_assert(sizeof(T) == 8, "8-byte lane values (fp64, or fp32 pairs)");
   const int csi = CS == 4 ? 2 : CS == 2 ? 1 : 0;
   Kern kern;
-  if constexpr (sizeof(T) == 8) {
+  if constexpr (!kPair) {
     // [cluster size 1/2/4][cn][pent][per]
 #define BSB_SPIKE_SET(CSZ)                                                                                        \
   {{{dev::sweep_spike<T, false, false, false, CSZ>, dev::sweep_spike<T, false, true, false, CSZ>},               \
@@ -951,7 +963,7 @@ bandsolve_status spike_solve_t(const Factor& f, T* x, std::size_t n, std::size_t
                                      {dev::sweep_spike<T, false, false, false, 4>, dev::sweep_spike<T, true, false, false, 4>}};
     kern = kerns[csi][pent];
   }
-  const int ki = (sizeof(T) == 8 ? 0 : 24) + csi * 8 + (cn ? 4 : 0) + (pent ? 2 : 0) + (per ? 1 : 0);
+  const int ki = (kPair ? 24 : 0) + csi * 8 + (cn ? 4 : 0) + (pent ? 2 : 0) + (per ? 1 : 0);
   static std::atomic<uint64_t> configured[48];
   const uint64_t bit = device < 64 ? (1ull << device) : 0;
   std::atomic<uint64_t>& attr_set = configured[ki];
@@ -1017,7 +1029,7 @@ bandsolve_status spike_solve_device(const Factor& f, double* x, std::size_t n, s
 
 bandsolve_status spike_solve_device_f32(const Factor& f, float* x, std::size_t n, std::size_t m, std::size_t ld,
                                         void* stream, int sms, bool* done) {
-  return spike_solve_t<float>(f, x, n, m, ld, stream, sms, done, nullptr, nullptr);
+  return spike_solve_t<float2>(f, reinterpret_cast<float2*>(x), n, m, ld, stream, sms, done, nullptr, nullptr);
 }
 
 }  // namespace bsb

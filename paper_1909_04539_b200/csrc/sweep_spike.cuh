@@ -113,19 +113,21 @@ struct SpikeLayout {
   size_t fwd_off, bwd_off, z_off, rinv_off, xch_off, ring_off, bar_off, total;
   // nl: rows whose records this CTA holds; R: interface unknowns; Kc: blocks
   // per CTA; elem: 8 (fp64) / 4 (fp32)
+  // rec: record / R^-1 element size (0: elem; 4 for the paired fp32 kernel)
   __host__ __device__ static SpikeLayout make(int nl, int R, int Kc, int KB, bool pent, bool per = false,
-                                              size_t elem = 8) {
+                                              size_t elem = 8, size_t rec = 0) {
     SpikeLayout L{};
-    const size_t sf = elem == 8 ? (pent ? sizeof(SpF<double, true>) : sizeof(SpF<double, false>))
-                                : (pent ? sizeof(SpF<float, true>) : sizeof(SpF<float, false>));
-    const size_t sb = elem == 8 ? (pent ? sizeof(SpB<double, true>) : sizeof(SpB<double, false>))
-                                : (pent ? sizeof(SpB<float, true>) : sizeof(SpB<float, false>));
+    if (rec == 0) rec = elem;
+    const size_t sf = rec == 8 ? (pent ? sizeof(SpF<double, true>) : sizeof(SpF<double, false>))
+                               : (pent ? sizeof(SpF<float, true>) : sizeof(SpF<float, false>));
+    const size_t sb = rec == 8 ? (pent ? sizeof(SpB<double, true>) : sizeof(SpB<double, false>))
+                               : (pent ? sizeof(SpB<float, true>) : sizeof(SpB<float, false>));
     L.fwd_off = 0;
     L.bwd_off = align128(static_cast<size_t>(nl) * sf);
     L.z_off = L.bwd_off + align128(static_cast<size_t>(nl) * sb);
     // z of the periodic correction: [nl] pairs (pent) / values (tri)
     L.rinv_off = L.z_off + (per ? align128(static_cast<size_t>(nl) * (pent ? 2 : 1) * sizeof(double)) : 0);
-    L.xch_off = L.rinv_off + align128(static_cast<size_t>(spike_rinv_rows(Kc, pent ? 2 : 1)) * R * elem);
+    L.xch_off = L.rinv_off + align128(static_cast<size_t>(spike_rinv_rows(Kc, pent ? 2 : 1)) * R * rec);
     // interface exchange, double-buffered: [2][warp][q][32 lanes]
     L.ring_off = L.xch_off + align128(2ull * kSpWarps * (pent ? 4 : 2) * 32 * elem);
     L.bar_off = L.ring_off + static_cast<size_t>(KB) * kSpWarps * kSpR * 32 * elem;
@@ -156,10 +158,55 @@ __device__ __forceinline__ float ld_cluster_f32(uint32_t addr) {
   asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
   return v;
 }
+__device__ __forceinline__ float2 ld_cluster_f32x2(uint32_t addr) {
+  float2 v;
+  asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr) : "memory");
+  return v;
+}
 template <typename T>
 __device__ __forceinline__ T ld_cluster(uint32_t addr) {
-  if constexpr (sizeof(T) == 8) return ld_cluster_f64(addr);
+  if constexpr (std::is_same<T, float2>::value) return ld_cluster_f32x2(addr);
+  else if constexpr (sizeof(T) == 8) return ld_cluster_f64(addr);
   else return ld_cluster_f32(addr);
+}
+
+// A lane's value type T: double (fp64), float (fp32), or float2 — two fp32
+// systems per lane, packed FFMA2 arithmetic, moved and stored exactly like
+// one fp64 value (8 bytes per lane and row). Records stay scalar (Scalar<T>).
+template <typename T>
+struct ScalarOf {
+  using type = T;
+};
+template <>
+struct ScalarOf<float2> {
+  using type = float;
+};
+template <typename T>
+using Scalar = typename ScalarOf<T>::type;
+__device__ __forceinline__ double vfma(double a, double b, double c) { return fma(a, b, c); }
+__device__ __forceinline__ float vfma(float a, float b, float c) { return fmaf(a, b, c); }
+__device__ __forceinline__ float2 vfma(float a, float2 b, float2 c) { return __ffma2_rn(make_float2(a, a), b, c); }
+__device__ __forceinline__ double vmul(double b, double a) { return b * a; }
+__device__ __forceinline__ float vmul(float b, float a) { return b * a; }
+__device__ __forceinline__ float2 vmul(float2 b, float a) { return __fmul2_rn(b, make_float2(a, a)); }
+// TMEM words: a float2 rides in the 64-bit slot of a double
+template <typename T>
+using TPieceOf = TPiece<std::conditional_t<sizeof(T) == 4, float, double>>;
+template <typename T>
+__device__ __forceinline__ auto to_word(T v) {
+  if constexpr (std::is_same<T, float2>::value)
+    return __longlong_as_double(static_cast<long long>((static_cast<unsigned long long>(__float_as_uint(v.y)) << 32) |
+                                                       __float_as_uint(v.x)));
+  else return v;
+}
+template <typename T, typename W>
+__device__ __forceinline__ T from_word(W w) {
+  if constexpr (std::is_same<T, float2>::value) {
+    const unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(w));
+    return make_float2(__uint_as_float(static_cast<unsigned>(u)), __uint_as_float(static_cast<unsigned>(u >> 32)));
+  } else {
+    return w;
+  }
 }
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -172,10 +219,12 @@ template <typename T, bool PENT, bool PER, bool CN = false, int CS = 1>
 __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
     sweep_spike(const __grid_constant__ CUtensorMap map_b, T* __restrict__ x, int n, long long m, long long ld,
                 int K, int L, int KB, int PD, long long groups, const void* __restrict__ recs,
-                const T* __restrict__ rinv_g, T* __restrict__ sink, SpikePer per) {
-  static_assert(sizeof(T) == 8 || (!PER && !CN), "fp32: plain solves only");
-  using F = SpF<T, PENT>;
-  using B = SpB<T, PENT>;
+                const Scalar<T>* __restrict__ rinv_g, T* __restrict__ sink, SpikePer per) {
+  static_assert(std::is_same<T, double>::value || (!PER && !CN), "fp32: plain solves only");
+  using S = Scalar<T>;  // record / R^-1 type
+  using F = SpF<S, PENT>;
+  using B = SpB<S, PENT>;
+  using TP = TPieceOf<T>;
   constexpr int NQ = PENT ? 4 : 2;  // interface rows per block (top NH, bottom NH)
   constexpr int NH = NQ / 2;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -191,10 +240,10 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
   const int row0 = kb0 * L;   // first of them
   const long long cid = blockIdx.x / CS;  // cluster (group walker) index
   const long long ncl = gridDim.x / CS;
-  const SpikeLayout Ly = SpikeLayout::make(nl, R, Kc, KB, PENT, PER, sizeof(T));
+  const SpikeLayout Ly = SpikeLayout::make(nl, R, Kc, KB, PENT, PER, sizeof(T), sizeof(S));
   F* sf = reinterpret_cast<F*>(smem + Ly.fwd_off);
   B* sb = reinterpret_cast<B*>(smem + Ly.bwd_off);
-  T* srinv = reinterpret_cast<T*>(smem + Ly.rinv_off);
+  S* srinv = reinterpret_cast<S*>(smem + Ly.rinv_off);
   T* xch = reinterpret_cast<T*>(smem + Ly.xch_off);
   T* ring = reinterpret_cast<T*>(smem + Ly.ring_off);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + Ly.bar_off);
@@ -322,7 +371,7 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
     const uint32_t tlane = tmem_base_s + (static_cast<uint32_t>(32 * (warp & 3)) << 16) +
                            static_cast<uint32_t>((warp >> 2) * 256);
     auto tslot = [&](uint32_t p, int c) {
-      return tlane + static_cast<uint32_t>((p ? CL - 1 - c : c) * TPiece<T>::kWords);
+      return tlane + static_cast<uint32_t>((p ? CL - 1 - c : c) * TP::kWords);
     };
     int slot = 0;
     uint32_t phase = 0;
@@ -331,11 +380,11 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
     const double* zk = reinterpret_cast<const double*>(smem + Ly.z_off) + (PENT ? 2 : 1) * rl;
 
     // forward state of the group being read, backward state of the one being written
-    T fs1 = T(0), fs2 = T(0), a0 = T(0), a1 = T(0);
-    T bs1 = T(0), bs2 = T(0), xl1 = T(0), xl2 = T(0), t1 = T(0), t2 = T(0);
+    T fs1{}, fs2{}, a0{}, a1{};
+    T bs1{}, bs2{}, xl1{}, xl2{}, t1{}, t2{};
     long long step = 0;
     T* out = sink + lane;
-    TPiece<T> cur;
+    TP cur;
 
     // CN: the stencil's halo rows. h1/h2 = u at the two rows above the chunk
     // (carried from the previous chunk; block starts load them), la0/la1 = the
@@ -365,7 +414,7 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
       mbar_wait(&full[slot], phase);
       const T* blk = ring + slot * kChunk + warp * kBox + lane;
       const F* fc = fk + c * kSpR;
-      TPiece<T> buf;
+      TP buf;
       T dv[kSpR];  // stage 1: b / pivot for the whole chunk (off the chain)
       if constexpr (CN) {
         if (c == 0) {
@@ -403,8 +452,8 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
       } else {
 #pragma unroll
         for (int r = 0; r < kSpR; ++r) {
-          if constexpr (PENT) dv[r] = blk[r * 32] * fc[r].ia;
-          else dv[r] = blk[r * 32] * fc[r].m;
+          if constexpr (PENT) dv[r] = vmul(blk[r * 32], fc[r].ia);
+          else dv[r] = vmul(blk[r * 32], fc[r].m);
         }
       }
       __syncwarp();
@@ -418,15 +467,15 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
         const F f = fc[r];
         T v;
         if constexpr (PENT) {
-          v = fma(-f.b, fs1, fma(-f.e, fs2, dv[r]));
-          a1 = fma(f.p1, v, a1);
+          v = vfma(-f.b, fs1, vfma(-f.e, fs2, dv[r]));
+          a1 = vfma(f.p1, v, a1);
         } else {
-          v = fma(-f.am, fs1, dv[r]);
+          v = vfma(-f.am, fs1, dv[r]);
         }
-        a0 = fma(f.p0, v, a0);
+        a0 = vfma(f.p0, v, a0);
         fs2 = fs1;
         fs1 = v;
-        buf.put(r, v);
+        buf.put(r, to_word(v));
       }
       buf.store(tslot(p, c));
     };
@@ -443,12 +492,12 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
       xw[0] = a0;
       if constexpr (PENT) {
         xw[32] = a1;
-        xw[64] = fma(-bk[L - 2].g, fs1, fs2);  // y_{L-2} = g_{L-2} - gamma_{L-2} g_{L-1}
+        xw[64] = vfma(-bk[L - 2].g, fs1, fs2);  // y_{L-2} = g_{L-2} - gamma_{L-2} g_{L-1}
         xw[96] = fs1;                          // y_{L-1} = g_{L-1}
       } else {
         xw[32] = fs1;
       }
-      fs1 = fs2 = a0 = a1 = T(0);
+      fs1 = fs2 = a0 = a1 = T{};
       if (CS == 1) {
         asm volatile("bar.sync 1, %0;" ::"r"(kSpWarps * 32) : "memory");
       } else {  // every warp of every CTA of the cluster has published its values
@@ -468,7 +517,7 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
                                : (Kc + 1) * NH + (h - 2 * NH);
       T zu[NU];
 #pragma unroll
-      for (int h = 0; h < NU; ++h) zu[h] = T(0);
+      for (int h = 0; h < NU; ++h) zu[h] = T{};
       const uint32_t xbase = smem_u32(xch + static_cast<size_t>(p) * kSpWarps * NQ * 32 + lane);
       for (int kk = 0; kk < K; ++kk) {
         T yv[NQ];
@@ -484,14 +533,14 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
         }
 #pragma unroll
         for (int h = 0; h < NU; ++h) {
-          const T* rr = srinv + static_cast<size_t>(rows[h]) * R + kk * NQ;
+          const S* rr = srinv + static_cast<size_t>(rows[h]) * R + kk * NQ;
 #pragma unroll
-          for (int q = 0; q < NQ; ++q) zu[h] = fma(rr[q], yv[q], zu[h]);
+          for (int q = 0; q < NQ; ++q) zu[h] = vfma(rr[q], yv[q], zu[h]);
         }
       }
       if (k == 0) {  // no left neighbour
 #pragma unroll
-        for (int h = NH; h < 2 * NH; ++h) zu[h] = T(0);
+        for (int h = NH; h < 2 * NH; ++h) zu[h] = T{};
       }
       if constexpr (PENT) {
         bs1 = zu[0];  // x_{L-2}
@@ -533,14 +582,15 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
       T gv[kSpR];  // stage 1: left-coupling update (off the chain)
 #pragma unroll
       for (int r = 0; r <= kTop; ++r) {
-        if constexpr (PENT) gv[r] = fma(-bc[r].f1, xl2, fma(-bc[r].f2, xl1, cur.get(r)));
-        else gv[r] = fma(-bc[r].f1, xl1, cur.get(r));
+        const T g = from_word<T>(cur.get(r));
+        if constexpr (PENT) gv[r] = vfma(-bc[r].f1, xl2, vfma(-bc[r].f2, xl1, g));
+        else gv[r] = vfma(-bc[r].f1, xl1, g);
       }
 #pragma unroll
       for (int r = kTop; r >= 0; --r) {  // stage 2: one FMA per row on the chain
         T v;
-        if constexpr (PENT) v = fma(-bc[r].g, bs1, fma(-bc[r].d, bs2, gv[r]));
-        else v = fma(-bc[r].c, bs1, gv[r]);
+        if constexpr (PENT) v = vfma(-bc[r].g, bs1, vfma(-bc[r].d, bs2, gv[r]));
+        else v = vfma(-bc[r].c, bs1, gv[r]);
         bs2 = bs1;
         bs1 = v;
         __stcs(out, corr(c * kSpR + r, v));
