@@ -457,9 +457,10 @@ int bandsolve_get_devices(int* devices, int capacity);
  * stagger); SPIKE (0|1: the one-pass partitioned kernel, fast mode),
  * SPIKE_K (its block count), NO_PDL (flag: no programmatic dependent
  * launch); PIPE (0|1: the pipelined on-chip sequential kernel), PKB (its
- * minimum ring slots), PIPE_MAX_N (its row limit, default 512; up to 1024
- * with an L2 tier), PRT (its register chunks), PIPE_CN (flag: the CN step
- * through it); PARTITION (0|1), PART_K; CN_UNFUSED, PERIODIC_UNFUSED,
+ * minimum ring slots), PIPE_MAX_N (its row limit, default 4096; beyond 512
+ * rows with an L2 tier), PIPE_L2_P (compute warps with the L2 tier), PRT
+ * (its register chunks), PIPE_CN (flag: the CN step through it),
+ * SPIKE_F32_MIN_N (smallest n for the fp32 spike kernel); PARTITION (0|1), PART_K; CN_UNFUSED, PERIODIC_UNFUSED,
  * ADI_UNFUSED, ADI_FUSE_PENT (flags: set = on); HOST_CHUNK_MIB (host-batch
  * staging chunk); L2_SETASIDE (1: grow the device's persisting-L2 limit to
  * cover the spill scratch; process-wide state, off by default).

@@ -33,10 +33,11 @@ int pipe_warps(std::size_t n, std::size_t m, std::size_t ld, const void* x, bool
                int* st, bool per) {
   const long long sel = tune_int("PIPE", -1);  // 0: never, 1: whenever it applies
   if (sel == 0 || tune_flag("PLAN")) return 0;
-  // beyond 512 rows the L2 tier takes the place of the streaming kernel's
-  // spill and measured level with it (pent N = 1024: 0.466 vs 0.473), so by
-  // default the pipelined plan stops where everything fits on chip
-  const std::size_t max_rows = static_cast<std::size_t>(tune_int("PIPE_MAX_N", 512));
+  // beyond 512 rows the last chunks live in the L2 tier (cp.async-staged a
+  // few chunks ahead): measured 0.50-0.88 of the roofline at N = 4096..640
+  // where the streaming kernel's spill / the two-pass sweep reached 0.43-0.68;
+  // the limit in practice is the factor records in shared memory
+  const std::size_t max_rows = static_cast<std::size_t>(tune_int("PIPE_MAX_N", 4096));
   if (n % dev::kPpR != 0 || n < 2 * dev::kPpR || n > max_rows) return 0;
   if (reinterpret_cast<uintptr_t>(x) % 16 != 0 || ld % 2 != 0 || m % 2 != 0 ||
       m > static_cast<std::size_t>(INT_MAX) / 2)
@@ -47,12 +48,14 @@ int pipe_warps(std::size_t n, std::size_t m, std::size_t ld, const void* x, bool
   const int kmin = static_cast<int>(tune_int("PKB", 4));  // ring slots (tuning)
   const int rt_force = static_cast<int>(tune_int("PRT", -1));
   const int zw = per ? (pent ? 2 : 1) : 0;
-  auto fits = [&](int P, int k, int ST) {
-    return dev::PipeLayout::make(static_cast<int>(n), P, k, fwd_rec(pent), bwd_rec(pent), ST, zw).total <= cap;
+  auto fits = [&](int P, int k, int ST, int RT) {
+    return dev::PipeLayout::make(static_cast<int>(n), P, k, fwd_rec(pent), bwd_rec(pent), ST, zw,
+                                 dev::pipe_stage_chunks(static_cast<int>(n), RT, ST))
+               .total <= cap;
   };
   auto take = [&](int P, int RT, int ST) {
     int k = kmin;
-    while (k < 10 && fits(P, k + 1, ST)) ++k;
+    while (k < 10 && fits(P, k + 1, ST, RT)) ++k;
     *kb = k;
     *rt = RT;
     *st = ST;
@@ -67,13 +70,18 @@ int pipe_warps(std::size_t n, std::size_t m, std::size_t ld, const void* x, bool
       if (rt_force >= 0 && RT != rt_force) continue;
       const int ST = CL - TT - RT;
       if (ST < 0) continue;
-      if (fits(P, kmin, ST)) return take(P, RT, ST);
+      if (fits(P, kmin, ST, RT)) return take(P, RT, ST);
     }
   }
-  // 2) the L2 tier (2 warps)
-  if (sel != 1 && m < static_cast<std::size_t>(sms) * 64) return 0;
-  for (int ST = CL - TT; ST >= 0; --ST)
-    if (fits(2, kmin, ST)) return take(2, 0, ST);
+  // 2) the L2 tier: up to 1024 rows 3 warps with the register tier (pent
+  // N = 1024: 0.63 vs 0.59 without it, 0.57 with 2 warps), beyond that 2
+  // warps (less L2 scratch in flight: N = 2048 0.55 vs 0.50); PIPE_L2_P, PRT
+  const int PL = static_cast<int>(
+      std::min<long long>(4, std::max<long long>(2, tune_int("PIPE_L2_P", n <= 1024 ? 3 : 2))));
+  const int RL = PL == 3 && rt_force != 0 ? 4 : 0;
+  if (sel != 1 && m < static_cast<std::size_t>(sms) * 32 * PL) return 0;
+  for (int ST = CL - TT - RL; ST >= 0; --ST)
+    if (fits(PL, kmin, ST, RL)) return take(PL, RL, ST);
   return 0;
 }
 
@@ -122,7 +130,8 @@ bandsolve_status pipe_solve_device(bool pent, bool fast, const void* fwd, const 
   const int Wg = 32 * P;
   const long long groups = (static_cast<long long>(m) + Wg - 1) / Wg;
   const std::size_t smem =
-      dev::PipeLayout::make(static_cast<int>(n), P, KB, fwd_rec(pent), bwd_rec(pent), ST, per ? (pent ? 2 : 1) : 0)
+      dev::PipeLayout::make(static_cast<int>(n), P, KB, fwd_rec(pent), bwd_rec(pent), ST, per ? (pent ? 2 : 1) : 0,
+                            dev::pipe_stage_chunks(static_cast<int>(n), RT, ST))
           .total;
   dev::PipePer pp;
   if (per) {

@@ -29,22 +29,41 @@ namespace dev {
 
 constexpr int kPpR = 16;      // rows per chunk (one TMA box {32 x 16} per warp)
 constexpr int kPpTmemRows = 256;  // rows per lane in TMEM (512 columns of fp64)
+constexpr int kPpStage = 3;       // L2-tier chunks in flight per warp (cp.async staging slots)
+
+// staging slots of the L2 tier: kPpStage when any chunk lives in L2
+__host__ __device__ inline int pipe_stage_chunks(int n, int RT, int ST) {
+  const int CL = n / kPpR;
+  const int TT = CL < kPpTmemRows / kPpR ? CL : kPpTmemRows / kPpR;
+  return CL - TT - RT - ST > 0 ? kPpStage : 0;
+}
+
+__device__ __forceinline__ void cp_async_16(void* sdst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 
 struct PipeLayout {
-  size_t fwd_off, bwd_off, z_off, stor_off, ring_off, bar_off, total;
+  size_t fwd_off, bwd_off, z_off, stor_off, stage_off, ring_off, bar_off, total;
   // n rows (multiple of 16), P compute warps, KB ring slots, ST shared-memory
   // storage chunks per lane (the first TT = min(n/16, 16) chunks live in
   // TMEM, then RT in registers, then ST in smem, the rest in the L2 scratch)
-  // zw: doubles per row of the periodic correction's z (0, 1 tri, 2 pent)
+  // zw: doubles per row of the periodic correction's z (0, 1 tri, 2 pent);
+  // DS: staging chunks of the L2 tier (pipe_stage_chunks)
   __host__ __device__ static PipeLayout make(int n, int P, int KB, size_t fwd_rec, size_t bwd_rec, int ST,
-                                             int zw = 0) {
+                                             int zw = 0, int DS = 0) {
     PipeLayout L{};
     L.fwd_off = 0;
     L.bwd_off = align128(static_cast<size_t>(n) * fwd_rec);
     L.z_off = L.bwd_off + align128(static_cast<size_t>(n) * bwd_rec);
     L.stor_off = L.z_off + align128(static_cast<size_t>(n) * zw * sizeof(double));
     // shared-memory slots: [ST][P warps][16 rows][32 lanes]
-    L.ring_off = L.stor_off + static_cast<size_t>(ST) * P * kPpR * 32 * sizeof(double);
+    L.stage_off = L.stor_off + static_cast<size_t>(ST) * P * kPpR * 32 * sizeof(double);
+    L.ring_off = L.stage_off + static_cast<size_t>(DS) * P * kPpR * 32 * sizeof(double);
     L.bar_off = L.ring_off + static_cast<size_t>(KB) * P * kPpR * 32 * sizeof(double);
     L.total = L.bar_off + static_cast<size_t>(2 * KB + 1) * sizeof(uint64_t);
     return L;
@@ -129,12 +148,14 @@ __global__ void __launch_bounds__(32 * (P + 1), 1)
   using BwdR = typename Recs<double, PENT>::Bwd;
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int ZW = PER ? (PENT ? 2 : 1) : 0;
-  const PipeLayout Ly = PipeLayout::make(n, P, KB, sizeof(FwdR), sizeof(BwdR), ST, ZW);
+  const int DS = pipe_stage_chunks(n, RT, ST);
+  const PipeLayout Ly = PipeLayout::make(n, P, KB, sizeof(FwdR), sizeof(BwdR), ST, ZW, DS);
   double* const sz = reinterpret_cast<double*>(smem + Ly.z_off);  // [n][ZW]
   const FwdR* sf = reinterpret_cast<const FwdR*>(smem + Ly.fwd_off);
   const BwdR* sb = reinterpret_cast<const BwdR*>(smem + Ly.bwd_off);
   double* stor = reinterpret_cast<double*>(smem + Ly.stor_off);
   double* ring = reinterpret_cast<double*>(smem + Ly.ring_off);
+  double* stage = reinterpret_cast<double*>(smem + Ly.stage_off);  // [DS][P warps][16 rows][32 lanes]
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + Ly.bar_off);
   uint64_t* empty = full + KB;
   uint32_t& tmem_base_s = *reinterpret_cast<uint32_t*>(empty + KB);
@@ -231,8 +252,24 @@ __global__ void __launch_bounds__(32 * (P + 1), 1)
   double* out = sink + lane;
   TPiece<double> cur;  // the backward chunk's 16 forward values
 
-  // load the backward chunk's values from slot s (TMEM: asynchronous, waited in step())
-  auto bwd_load = [&](int s) {
+  // L2 tier: chunk c of the group being written (parity pw) -> staging slot
+  // c % DS, as one cp.async group (empty when the chunk is not in L2), DS
+  // chunks ahead of its use, so the L2 latency overlaps the row loops. A
+  // lane copies 16-byte pieces of other lanes' words (the warp syncs).
+  auto l2_prefetch = [&](uint32_t pw, int c) {
+    if (GT > 0) {
+      if (c >= 0 && sidx(pw, c) >= TR + ST) {
+        const double* src = slot_l2(sidx(pw, c)) - lane;
+        double* dst = stage + (static_cast<size_t>(c % DS) * P + warp) * kBox;
+#pragma unroll
+        for (int k = 0; k < kBox / 64; ++k) cp_async_16(dst + 2 * (lane + 32 * k), src + 2 * (lane + 32 * k));
+      }
+      cp_async_commit();
+    }
+  };
+  // load the backward chunk c's values from slot s (TMEM: asynchronous, waited
+  // in step(); L2 tier: from the staging slot when staged, else directly)
+  auto bwd_load = [&](int s, int c, bool staged) {
     if (s < TT) {
       cur.load(tlane + static_cast<uint32_t>(s * TPiece<double>::kWords));
     } else if (s < TR) {
@@ -250,6 +287,12 @@ __global__ void __launch_bounds__(32 * (P + 1), 1)
       }
     } else if (s < TR + ST) {
       const double* q = slot_smem(s);
+#pragma unroll
+      for (int r = 0; r < kPpR; ++r) cur.put(r, q[r * 32]);
+    } else if (staged) {
+      cp_async_wait<kPpStage - 1>();  // DS - 1 younger groups may still be in flight
+      __syncwarp();
+      const double* q = stage + (static_cast<size_t>(c % DS) * P + warp) * kBox + lane;
 #pragma unroll
       for (int r = 0; r < kPpR; ++r) cur.put(r, q[r * 32]);
     } else {  // this lane's own words, written by this lane one round earlier
@@ -409,7 +452,7 @@ __global__ void __launch_bounds__(32 * (P + 1), 1)
         double e0 = 0.0, e1 = 0.0, yl = 0.0, yl2 = 0.0;
         for (int c = CL - 1; c >= 0; --c) {
           const int s = sidx(p ^ 1u, c);
-          bwd_load(s);
+          bwd_load(s, c, false);
           if (s < TT) cur.wait();
           const BwdR* bc = sb + c * kPpR;
 #pragma unroll
@@ -432,7 +475,10 @@ __global__ void __launch_bounds__(32 * (P + 1), 1)
         }
         bs1 = bs2 = 0.0;
       }
-      bwd_load(sidx(p ^ 1u, CL - 1));
+      for (int d = 0; d < DS; ++d) l2_prefetch(p ^ 1u, CL - 1 - d);
+      bwd_load(sidx(p ^ 1u, CL - 1), CL - 1, true);
+      __syncwarp();  // every lane has read the staging slot before it is refilled
+      l2_prefetch(p ^ 1u, CL - 1 - DS);
     }
     fs1 = fs2 = 0.0;
     for (int kk = 0; kk < CL; ++kk) {
@@ -442,7 +488,11 @@ __global__ void __launch_bounds__(32 * (P + 1), 1)
       else if (i < my) run_step(kk, c, s, std::true_type{}, std::false_type{}, g);
       else run_step(kk, c, s, std::false_type{}, std::true_type{}, g);
       if (CN && kk == 0 && i + 1 < my) halo_prefetch(g + gridDim.x);  // this group's halo is consumed
-      if (i > 0 && c > 0) bwd_load(sidx(p ^ 1u, c - 1));  // next backward chunk (a different slot)
+      if (i > 0 && c > 0) {  // next backward chunk (a different slot)
+        bwd_load(sidx(p ^ 1u, c - 1), c - 1, true);
+        __syncwarp();
+        l2_prefetch(p ^ 1u, c - 1 - DS);
+      }
     }
     __syncwarp();  // this warp's smem slot stores are visible to its own next-round loads
   }

@@ -49,11 +49,10 @@ def _dev_solve(lib, torch, factor, rhs, ld):
 
 
 @pytest.mark.parametrize("mode", [bs.MODE_EXACT, bs.MODE_FAST])
-@pytest.mark.parametrize("n", [32, 48, 256, 272, 320, 512, 784, 1024])
+@pytest.mark.parametrize("n", [32, 48, 256, 272, 320, 512, 784, 1024, 1296, 2048, 4096])
 def test_pipe_matches_oracle(lib, oracle, cuda_device, mode, n):
     torch = cuda_device
     lib.tune("PIPE", "1")
-    lib.tune("PIPE_MAX_N", "1024")
     lib.tune("SPIKE", "0")
     lib.tune("PARTITION", "0")
     lib.set_mode(mode)
@@ -66,6 +65,8 @@ def test_pipe_matches_oracle(lib, oracle, cuda_device, mode, n):
                                      ("pent", bs.PentFactor, _random_pent(rng, n)),
                                      ("hyper", bs.PentFactor, bs.hyper_bands(1.0, n))]:
                 pent = cls is bs.PentFactor
+                if pent and n > 3072:
+                    continue  # the pentadiagonal records of 4096 rows exceed shared memory
                 assert lib.describe_plan(1 if pent else 0, n, m, ld).startswith("pipe"), (n, m)
                 want = (oracle.pent_solve(oracle.pent_prefactor(*bands), rhs.copy()) if pent
                         else oracle.tri_solve(oracle.tri_prefactor(*bands), rhs.copy()))
@@ -80,13 +81,20 @@ def test_pipe_matches_oracle(lib, oracle, cuda_device, mode, n):
 
 
 def test_pipe_planner(lib, cuda_device):
-    """Taken in exact mode for many systems of n % 16 == 0, n <= 512 only."""
+    """Taken in exact mode for many systems of n % 16 == 0, n <= 4096 (beyond
+    512 rows with the cp.async-staged L2 tier: 3 warps + registers up to 1024
+    rows, then 2 warps)."""
     assert lib.describe_plan(1, 512, 1 << 20).startswith("pipe")
     assert lib.describe_plan(0, 256, 1 << 20).startswith("pipe")
-    assert not lib.describe_plan(1, 528, 1 << 20).startswith("pipe")      # > 512 rows by default
-    lib.tune("PIPE_MAX_N", "1024")
-    assert "l2-rows=0" not in lib.describe_plan(1, 1024, 1 << 21)          # the L2 tier
-    assert not lib.describe_plan(1, 1040, 1 << 20).startswith("pipe")     # > 1024 rows
+    assert "l2-rows=0" in lib.describe_plan(1, 512, 1 << 20)               # every row on chip
+    s = lib.describe_plan(1, 1024, 1 << 21)                               # configs[4]'s shard
+    assert s.startswith("pipe Wg=96") and "l2-rows=0" not in s and "reg-rows=64" in s, s  # the L2 tier
+    assert lib.describe_plan(0, 2048, 1 << 20).startswith("pipe Wg=64")
+    assert lib.describe_plan(0, 4096, 1 << 20).startswith("pipe Wg=64")
+    assert not lib.describe_plan(1, 4096, 1 << 20).startswith("pipe")     # pent records > smem
+    assert not lib.describe_plan(0, 4112, 1 << 20).startswith("pipe")     # > 4096 rows
+    lib.tune("PIPE_MAX_N", "512")
+    assert not lib.describe_plan(1, 528, 1 << 20).startswith("pipe")
     lib.tune("PIPE_MAX_N", None)
     assert not lib.describe_plan(1, 500, 1 << 20).startswith("pipe")      # not whole chunks
     assert not lib.describe_plan(1, 512, (1 << 20) - 1, 1 << 20).startswith("pipe")  # odd batch
