@@ -34,15 +34,10 @@ fi
 if [ -z "${SKIP_NCU:-}" ]; then
   timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 40 --csv \
      --log-file gpurun_out/launches_default.csv python bench.py --steps 3 --warmup 3 --no-cpu --no-e2e > gpurun_out/ncu_launch.log 2>&1
-  for spec in "c5s fast sweep_spike" "pent512 fast sweep_spike" "tri512 fast sweep_spike" "pent512 exact sweep_stream" "c2 exact sweep_stream" "c2 fast sweep_spike" "c5s exact sweep_stream"; do
+  for spec in "c5s fast sweep_spike" "pent512 fast sweep_spike" "tri512 fast sweep_spike" "pent512 exact sweep_pipe" \
+              "c2 exact sweep_pipe" "c2 fast sweep_spike" "c5s exact sweep_pipe" "tri512 fast sweep_spike tri512f32_fast --f32"; do
     set -- $spec
-    tag=${1}_${2}
-    timeout 900 ncu --set full --clock-control none --import-source on -k regex:$3 -s 3 -c 1 \
-      -o /tmp/ncurep/$tag -f python bench.py --config $1 --mode $2 --no-cpu --no-e2e --steps 2 --warmup 3 > gpurun_out/ncu/$tag.log 2>&1
-    ncu -i /tmp/ncurep/$tag.ncu-rep --page raw --csv > gpurun_out/ncu/$tag.raw.csv 2>>gpurun_out/ncu/$tag.log
-    ncu -i /tmp/ncurep/$tag.ncu-rep --page details --csv > gpurun_out/ncu/$tag.details.csv 2>>gpurun_out/ncu/$tag.log
-    ncu -i /tmp/ncurep/$tag.ncu-rep --page source --csv --print-source sass > gpurun_out/ncu/$tag.sass.csv 2>>gpurun_out/ncu/$tag.log
-    gzip -f gpurun_out/ncu/$tag.sass.csv
+    bash tools/gpu_ncu1.sh "$@"
   done
 fi
 tail -3 gpurun_out/pytest_gpu.log 2>/dev/null; cat gpurun_out/smoke.log 2>/dev/null; cat gpurun_out/bench_default.json gpurun_out/bench_ref.json
