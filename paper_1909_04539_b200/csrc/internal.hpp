@@ -179,7 +179,8 @@ int pipe_warps(std::size_t n, std::size_t m, std::size_t ld, const void* x, bool
                int* st, bool per = false);
 bandsolve_status pipe_solve_device(bool pent, bool fast, const void* fwd, const void* bwd, double* x, std::size_t n,
                                    std::size_t m, std::size_t ld, void* stream, int sms, bool* done,
-                                   const PartPeriodic* per = nullptr, const SpikeCN* cn = nullptr);
+                                   const PartPeriodic* per = nullptr, const SpikeCN* cn = nullptr,
+                                   bool f32 = false);
 bool partition_stencil_ok(std::size_t n, std::size_t m, int K, std::size_t lds);
 bandsolve_status partition_solve_device(const Factor& f, double* x, std::size_t n,
                                         std::size_t m, std::size_t ld,

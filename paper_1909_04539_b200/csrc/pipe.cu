@@ -87,9 +87,14 @@ int pipe_warps(std::size_t n, std::size_t m, std::size_t ld, const void* x, bool
 
 bandsolve_status pipe_solve_device(bool pent, bool fast, const void* fwd, const void* bwd, double* x, std::size_t n,
                                    std::size_t m, std::size_t ld, void* stream, int sms, bool* done,
-                                   const PartPeriodic* per, const SpikeCN* cn) {
+                                   const PartPeriodic* per, const SpikeCN* cn, bool f32) {
   *done = false;
   if (cn && (!per || reinterpret_cast<uintptr_t>(cn->u) % 16 != 0)) return BANDSOLVE_OK;
+  if (f32) {  // pairs of adjacent fp32 systems per lane (8-byte words), plain solves
+    if (per || cn || m % 4 != 0 || ld % 4 != 0) return BANDSOLVE_OK;
+    m /= 2;
+    ld /= 2;
+  }
   int KB = 0, RT = 0, ST = 0;
   const int P = pipe_warps(n, m, ld, x, pent, sms, &KB, &RT, &ST, per != nullptr);
   if (P == 0) return BANDSOLVE_OK;
@@ -116,10 +121,17 @@ bandsolve_status pipe_solve_device(bool pent, bool fast, const void* fwd, const 
                                          BSB_PIPE_WARPS(true, true)};
 #undef BSB_PIPE_WARPS
 #undef BSB_PIPE_SET
+  // fp32 pairs: [2 warps, 3 warps, 4 warps, 3 warps + register tier][pent][fast]
+#define BSB_PIPE_F2(PP, RR)                                                                                 \
+  {{dev::sweep_pipe<false, false, PP, RR, false, false, float2>,                                           \
+    dev::sweep_pipe<false, true, PP, RR, false, false, float2>},                                           \
+   {dev::sweep_pipe<true, false, PP, RR, false, false, float2>, dev::sweep_pipe<true, true, PP, RR, false, false, float2>}}
+  static const Kern kf2[4][2][2] = {BSB_PIPE_F2(2, 0), BSB_PIPE_F2(3, 0), BSB_PIPE_F2(4, 0), BSB_PIPE_F2(3, 4)};
+#undef BSB_PIPE_F2
   const int ki = RT > 0 ? 3 : P - 2;
-  const int vi = cn ? 2 : per ? 1 : 0;
-  const Kern kern = kerns[vi][ki][pent][fast];
-  static std::atomic<uint64_t> configured[48];
+  const int vi = f32 ? 3 : cn ? 2 : per ? 1 : 0;
+  const Kern kern = f32 ? kf2[ki][pent][fast] : kerns[vi][ki][pent][fast];
+  static std::atomic<uint64_t> configured[64];
   std::atomic<uint64_t>& done_attr = configured[vi * 16 + ki * 4 + (pent ? 2 : 0) + (fast ? 1 : 0)];
   const uint64_t bit = device < 64 ? (1ull << device) : 0;
   if (!(bit && (done_attr.load(std::memory_order_relaxed) & bit))) {

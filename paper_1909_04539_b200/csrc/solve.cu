@@ -1144,13 +1144,15 @@ bandsolve_status describe_plan(Kind kind, std::size_t n, std::size_t m, std::siz
   const int KS = spike_blocks(n, m, ld, kProbe, sms, pent, f32 ? 4 : 8);
   const int K = f32 ? 0 : partition_blocks(n, m, sms, pent);
   int pkb = 0, prt = 0, pst = 0;
-  const int PP = (f32 || KS > 0 || K > 0) ? 0 : pipe_warps(n, m, ld, kProbe, pent, sms, &pkb, &prt, &pst);
+  const int PP = (KS > 0 || K > 0 || (f32 && (m % 4 != 0 || ld % 4 != 0)))
+                     ? 0
+                     : pipe_warps(n, f32 ? m / 2 : m, f32 ? ld / 2 : ld, kProbe, pent, sms, &pkb, &prt, &pst);
   if (PP > 0) {
     const std::size_t tm = std::min<std::size_t>(n, 256), rg = static_cast<std::size_t>(prt) * 16,
                       sm = static_cast<std::size_t>(pst) * 16;
     std::snprintf(buf, sizeof buf,
-                  "pipe Wg=%d warps=%d+1 tmem=%zu reg-rows=%zu smem-rows=%zu l2-rows=%zu ring=%d (1 launch)", 32 * PP,
-                  PP, tm, rg, sm, n - tm - rg - sm, pkb);
+                  "pipe Wg=%d warps=%d+1 tmem=%zu reg-rows=%zu smem-rows=%zu l2-rows=%zu ring=%d%s (1 launch)",
+                  (f32 ? 64 : 32) * PP, PP, tm, rg, sm, n - tm - rg - sm, pkb, f32 ? " fp32 pairs" : "");
   }
   else if (KS > 0)
     std::snprintf(buf, sizeof buf, "spike K=%d blocks of %zu rows, interface system %d, 1 launch (TMEM-resident blocks%s)",
@@ -1206,10 +1208,10 @@ bandsolve_status solve_device(const Factor& f, void* x, bool f32, std::size_t n,
     st = partition_solve_device(f, static_cast<double*>(x), n, m, ld, stream, sms, &done);
     if (st != BANDSOLVE_OK || done) return st;
   }
-  if (!f32) {  // every forward intermediate on chip, pipelined across groups
+  {  // every forward intermediate on chip, pipelined across groups (fp32: system pairs per lane)
     bool done = false;
-    st = pipe_solve_device(pent, fast, df->fwd[0][q], df->bwd[0][q], static_cast<double*>(x), n, m, ld, stream, sms,
-                           &done);
+    st = pipe_solve_device(pent, fast, df->fwd[p][q], df->bwd[p][q], static_cast<double*>(x), n, m, ld, stream, sms,
+                           &done, nullptr, nullptr, f32);
     if (st != BANDSOLVE_OK || done) return st;
   }
   const Plan plan = choose_plan(n, m, ld, f32 ? 4 : 8, x, pent, fast, sms);

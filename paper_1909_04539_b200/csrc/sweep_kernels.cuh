@@ -47,6 +47,16 @@ __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(
 __device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
 __device__ __forceinline__ double fma_rn(double a, double b, double c) { return __fma_rn(a, b, c); }
 __device__ __forceinline__ float fma_rn(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+// two fp32 systems at once. mul/add/sub as two scalar .rn operations: ptxas
+// (12.9) contracts packed mul.rn.f32x2 + sub.rn.f32x2 into FFMA2 even with
+// the explicit rounding (and __fmul2_rn/__fadd2_rn likewise), which would
+// break the exact mode's separate roundings; scalar .rn is never contracted
+__device__ __forceinline__ float2 mul_rn(float a, float2 b) { return make_float2(__fmul_rn(a, b.x), __fmul_rn(a, b.y)); }
+__device__ __forceinline__ float2 mul_rn(float2 a, float b) { return make_float2(__fmul_rn(a.x, b), __fmul_rn(a.y, b)); }
+__device__ __forceinline__ float2 add_rn(float2 a, float2 b) { return make_float2(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y)); }
+__device__ __forceinline__ float2 sub_rn(float2 a, float2 b) { return make_float2(__fsub_rn(a.x, b.x), __fsub_rn(a.y, b.y)); }
+// the fast mode's fused form (packed FFMA2)
+__device__ __forceinline__ float2 fma_rn(float a, float2 b, float2 c) { return __ffma2_rn(make_float2(a, a), b, c); }
 
 // ---- packed factor records (filled by solve.cu pack_*) ---------------------
 // tri forward:  exact {a_i, m_i}          fast {a_i*m_i, m_i}

@@ -76,10 +76,10 @@ struct PipeLayout {
 // (b - eps g2, delta x2), then the three dependent operations of each
 // recurrence side by side. The operation order of each recurrence is the
 // reference's (exact) or the FMA form (fast).
-template <bool PENT, bool FAST, bool FW, bool BW>
-__device__ __forceinline__ void pipe_rows(const typename Recs<double, PENT>::Fwd& fr, double d, double& fs1,
-                                          double& fs2, double& fv, const typename Recs<double, PENT>::Bwd& br,
-                                          double g, double& bs1, double& bs2, double& bv) {
+template <bool PENT, bool FAST, bool FW, bool BW, typename T = double>
+__device__ __forceinline__ void pipe_rows(const typename Recs<Scalar<T>, PENT>::Fwd& fr, T d, T& fs1, T& fs2, T& fv,
+                                          const typename Recs<Scalar<T>, PENT>::Bwd& br, T g, T& bs1, T& bs2,
+                                          T& bv) {
   if constexpr (FAST) {
     if constexpr (FW) {
       if constexpr (PENT) fv = fma_rn(-fr.b, fs1, fma_rn(-fr.e, fs2, mul_rn(d, fr.ia)));
@@ -90,7 +90,7 @@ __device__ __forceinline__ void pipe_rows(const typename Recs<double, PENT>::Fwd
       else bv = fma_rn(-br, bs1, g);
     }
   } else if constexpr (PENT) {
-    double tf = 0.0, xb = 0.0, uf = 0.0, ub = 0.0;
+    T tf{}, xb{}, uf{}, ub{};
     if constexpr (FW) tf = sub_rn(d, mul_rn(fr.e, fs2));   // f - eps g2 (g2: one row old)
     if constexpr (BW) xb = mul_rn(br.d, bs2);              // delta x2 (x2: one row old)
     if constexpr (FW) uf = mul_rn(fr.b, fs1);              // chains: one op of each per stage
@@ -100,7 +100,7 @@ __device__ __forceinline__ void pipe_rows(const typename Recs<double, PENT>::Fwd
     if constexpr (FW) fv = mul_rn(uf, fr.ia);              // ((f - eps g2) - beta g1) * ia
     if constexpr (BW) bv = sub_rn(g, ub);                  // g - (gamma x1 + delta x2)
   } else {
-    double uf = 0.0, ub = 0.0;
+    T uf{}, ub{};
     if constexpr (FW) uf = mul_rn(fr.a, fs1);
     if constexpr (BW) ub = mul_rn(br, bs1);
     if constexpr (FW) uf = sub_rn(d, uf);
@@ -139,13 +139,17 @@ struct PipePer {
   double cn[3] = {0.0, 0.0, 0.0};
 };
 
-template <bool PENT, bool FAST, int P, int RT = 0, bool PER = false, bool CN = false>
+// T: double, or float2 = two fp32 systems per lane (packed FMUL2/FADD2 in
+// the same operation order: the bits of the scalar fp32 sweep), stored and
+// moved as 8-byte words exactly like fp64; x, m, ld then count pairs.
+template <bool PENT, bool FAST, int P, int RT = 0, bool PER = false, bool CN = false, typename T = double>
 __global__ void __launch_bounds__(32 * (P + 1), 1)
     sweep_pipe(const __grid_constant__ CUtensorMap map_b, double* __restrict__ x, int n, long long m, long long ld,
                int KB, int PD, long long groups, const void* __restrict__ fwd_g, const void* __restrict__ bwd_g,
                double* __restrict__ sink, int ST, double* __restrict__ scratch, PipePer per) {
-  using FwdR = typename Recs<double, PENT>::Fwd;
-  using BwdR = typename Recs<double, PENT>::Bwd;
+  static_assert(std::is_same<T, double>::value || (!PER && !CN), "fp32 pairs: plain solves only");
+  using FwdR = typename Recs<Scalar<T>, PENT>::Fwd;
+  using BwdR = typename Recs<Scalar<T>, PENT>::Bwd;
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int ZW = PER ? (PENT ? 2 : 1) : 0;
   const int DS = pipe_stage_chunks(n, RT, ST);
@@ -245,8 +249,8 @@ __global__ void __launch_bounds__(32 * (P + 1), 1)
   const uint64_t pol_keep = policy_evict_last();
   int slot = 0;
   uint32_t phase = 0;
-  double fs1 = 0.0, fs2 = 0.0;  // forward state (group being read)
-  double bs1 = 0.0, bs2 = 0.0;  // backward state (group being written)
+  T fs1{}, fs2{};  // forward state (group being read)
+  T bs1{}, bs2{};  // backward state (group being written)
   double wt1 = 0.0, wt2 = 0.0;  // periodic correction coefficients of the group being written
   long long step = 0;
   double* out = sink + lane;
@@ -383,14 +387,15 @@ __global__ void __launch_bounds__(32 * (P + 1), 1)
 #pragma unroll
     for (int q = 0; q < kPpR; ++q) {
       const int r = kPpR - 1 - q;
-      double fv = 0.0, bv = 0.0;
-      double din = 0.0;
+      T fv{}, bv{};
+      T din{};
       if constexpr (FW) {
         if constexpr (CN) din = fin[q];
-        else din = blk[q * 32];
+        else din = from_word<T>(blk[q * 32]);
       }
-      pipe_rows<PENT, FAST, FW, BW>(fc[q], din, fs1, fs2, fv, bc[r], BW ? cur.get(r) : 0.0, bs1, bs2, bv);
-      if constexpr (FW) buf.put(q, fv);
+      pipe_rows<PENT, FAST, FW, BW, T>(fc[q], din, fs1, fs2, fv, bc[r], BW ? from_word<T>(cur.get(r)) : T{}, bs1, bs2,
+                                       bv);
+      if constexpr (FW) buf.put(q, to_word(fv));
       if constexpr (BW) {
         if constexpr (PER) {  // x_i = y_i - w z_i (periodic.cpp:85 / :203)
           const int row = c * kPpR + r;
@@ -399,7 +404,7 @@ __global__ void __launch_bounds__(32 * (P + 1), 1)
           else
             bv = sub_rn(bv, mul_rn(wt1, sz[row]));
         }
-        __stcs(out, bv);
+        __stcs(out, to_word(bv));
         out -= step;
       }
     }
@@ -447,7 +452,7 @@ __global__ void __launch_bounds__(32 * (P + 1), 1)
       const bool live = j < m;
       step = live ? ld : 0;
       out = live ? x + static_cast<long long>(n - 1) * ld + j : sink + lane;
-      bs1 = bs2 = 0.0;
+      bs1 = bs2 = T{};
       if constexpr (PER) {  // first backward pass: y_{n-1}, y_{n-2}, y_1, y_0 only
         double e0 = 0.0, e1 = 0.0, yl = 0.0, yl2 = 0.0;
         for (int c = CL - 1; c >= 0; --c) {
@@ -473,14 +478,14 @@ __global__ void __launch_bounds__(32 * (P + 1), 1)
         } else {  // periodic.cpp:80
           wt1 = mul_rn(add_rn(e0, mul_rn(per.c[0], yl)), per.c[1]);
         }
-        bs1 = bs2 = 0.0;
+        bs1 = bs2 = T{};
       }
       for (int d = 0; d < DS; ++d) l2_prefetch(p ^ 1u, CL - 1 - d);
       bwd_load(sidx(p ^ 1u, CL - 1), CL - 1, true);
       __syncwarp();  // every lane has read the staging slot before it is refilled
       l2_prefetch(p ^ 1u, CL - 1 - DS);
     }
-    fs1 = fs2 = 0.0;
+    fs1 = fs2 = T{};
     for (int kk = 0; kk < CL; ++kk) {
       const int c = CL - 1 - kk;
       const int s = sidx(p, kk);  // == sidx(p ^ 1, c)

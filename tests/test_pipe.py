@@ -103,7 +103,7 @@ def test_pipe_planner(lib, cuda_device):
     assert not lib.describe_plan(1, 512, 1 << 20).startswith("pipe")
 
 
-@pytest.mark.parametrize("n", [32, 256, 320, 512])
+@pytest.mark.parametrize("n", [32, 256, 320, 512, 1024, 2048])
 def test_pipe_periodic_exact_bitwise(lib, oracle, cuda_device, n):
     """Exact periodic solves with the correction fused: a first backward pass
     over the on-chip intermediates finds y_0, y_1, y_{n-2}, y_{n-1}, the
@@ -159,3 +159,48 @@ def test_pipe_cn_step_exact_bitwise(lib, oracle, cuda_device, n):
             assert np.all(np.isnan(out[:, m:]))
             assert bitwise_equal(out[:, :m], want), (prob, n, m, ld)
             assert np.array_equal(du[:, :m].cpu().numpy(), u)
+
+
+@pytest.mark.parametrize("mode", [bs.MODE_EXACT, bs.MODE_FAST])
+@pytest.mark.parametrize("n", [32, 256, 512, 1024, 2048])
+def test_pipe_fp32_pairs(lib, oracle, cuda_device, mode, n):
+    """fp32 batches through the pipelined kernel, two systems per lane
+    (float2, packed FMUL2/FADD2/FFMA2): in exact mode the same bits as the
+    scalar fp32 sequential sweep (the streaming kernel, PIPE=0), and within
+    the 1e-5 fp32 contract of the fp64 reference solution in both modes."""
+    torch = cuda_device
+    lib.tune("SPIKE", "0")
+    lib.set_mode(mode)
+    rng = np.random.default_rng(n + 11 + mode)
+    try:
+        for m, ld in [(64, 64), (328, 332), (1000, 1000)]:
+            rhs = rng.uniform(-1, 1, (n, m)).astype(np.float32)
+            for cls, bands in [(bs.TriFactor, _random_tri(rng, n)), (bs.TriFactor, bs.diffusion_bands(1.0, n)),
+                               (bs.PentFactor, _random_pent(rng, n)), (bs.PentFactor, bs.hyper_bands(1.0, n))]:
+                pent = cls is bs.PentFactor
+                fac = cls(lib, *bands)
+                outs = []
+                for force in ("1", "0"):
+                    lib.tune("PIPE", force)
+                    plan = lib.describe_plan(1 if pent else 0, n, m, ld, True)
+                    assert plan.startswith("pipe") == (force == "1"), plan
+                    if force == "1":
+                        assert "fp32 pairs" in plan, plan
+                    buf = torch.full((n, ld), float("nan"), dtype=torch.float32, device="cuda")
+                    buf[:, :m] = torch.from_numpy(rhs).cuda()
+                    before = lib.kernel_launches()
+                    fac.solve_dev(buf.data_ptr(), n, m, ld=ld, stream=torch.cuda.current_stream().cuda_stream,
+                                  f32=True)
+                    torch.cuda.synchronize()
+                    if force == "1":
+                        assert lib.kernel_launches() - before == 1
+                    out = buf.cpu().numpy()
+                    assert np.all(np.isnan(out[:, m:]))
+                    outs.append(out[:, :m])
+                if mode == bs.MODE_EXACT:
+                    assert np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32)), (n, m, ld, pent)
+                want = (oracle.pent_solve(oracle.pent_prefactor(*bands), rhs.astype(np.float64))
+                        if pent else oracle.tri_solve(oracle.tri_prefactor(*bands), rhs.astype(np.float64)))
+                assert per_system_max_rel(outs[0].astype(np.float64), want) <= 1e-5, (n, m, pent)
+    finally:
+        lib.set_mode(bs.MODE_EXACT)
