@@ -57,6 +57,7 @@ CONFIGS = {
 }
 STRONG = {"c5"}
 DEFAULT_CONFIG = "c5"
+DEFAULT_MODE = "fast"
 E2E_MAX_SYSTEMS = 1 << 21  # pinned host batch per rank for e2e (16 GiB at N=1024): host RAM bound
 SEED = 42
 
@@ -423,7 +424,7 @@ def main() -> int:
     # systems, within 1e-12 of the reference (north_star's fp64 tolerance;
     # tests/test_spike.py, test_gpu_parity.py); exact: the reference's
     # operation order, bitwise equal
-    ap.add_argument("--mode", choices=["exact", "fast"], default=os.environ.get("BANDSOLVE_BENCH_MODE", "fast"))
+    ap.add_argument("--mode", choices=["exact", "fast"], default=os.environ.get("BANDSOLVE_BENCH_MODE", DEFAULT_MODE))
     ap.add_argument("--f32", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-API end-to-end leg (tuning runs)")

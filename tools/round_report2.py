@@ -77,6 +77,15 @@ def launches():
     allt = sum(tot.values()) or 1.0
     out += ["", "Share of GPU time by kernel: " + ", ".join(f"`{k}` {100 * v / allt:.1f}%" for k, v in tot.most_common())]
     open(os.path.join(DST, f"{TAG}_launches_default.md"), "w").write("\n".join(out) + "\n")
+    # DRAM bytes per sweep launch of the default workload (single-pass
+    # counters: the --set full replay of a 128 GiB in-place launch is not run)
+    sw = [(m.get("dram__bytes_read.sum", 0.0) + m.get("dram__bytes_write.sum", 0.0), k) for (i, k), m in per.items()
+          if "sweep_" in k]
+    if not sw:
+        return None
+    return {"dram_bytes_per_launch": sum(b for b, _ in sw) / len(sw), "kernel": sw[0][1][:90],
+            "source": f"profiles/{TAG}_launches_default.md (dram__bytes_read.sum + dram__bytes_write.sum, mean over "
+                      f"{len(sw)} sweep launches of the default bench)"}
 
 
 KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
@@ -172,9 +181,13 @@ def main():
         p = os.path.join(SRC, src)
         if os.path.exists(p):
             shutil.copy(p, os.path.join(DST, f"{TAG}_{dst}"))
-    launches()
+    dflt = launches()
     tp = os.path.join(DST, "ncu_traffic.json")
     traffic = json.load(open(tp)) if os.path.exists(tp) else {}
+    if dflt:
+        sys.path.insert(0, os.getcwd())
+        import bench  # noqa: E402  (the default config / mode keys bench.py looks up)
+        traffic[f"{bench.DEFAULT_CONFIG}/{bench.DEFAULT_MODE}"] = dflt
     ncu_reports(traffic)
     json.dump(traffic, open(tp, "w"), indent=1)
     print("written:", sorted(f for f in os.listdir(DST) if f.startswith(TAG)))
