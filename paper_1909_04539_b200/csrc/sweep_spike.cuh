@@ -519,23 +519,44 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
 #pragma unroll
       for (int h = 0; h < NU; ++h) zu[h] = T{};
       const uint32_t xbase = smem_u32(xch + static_cast<size_t>(p) * kSpWarps * NQ * 32 + lane);
-      for (int kk = 0; kk < K; ++kk) {
-        T yv[NQ];
-        if (CS == 1) {
+      if constexpr (CS == 1) {
+        for (int kk = 0; kk < K; ++kk) {
+          T yv[NQ];
           const T* src = xch + ((static_cast<size_t>(p) * kSpWarps + gs * K + kk) * NQ) * 32 + lane;
 #pragma unroll
           for (int q = 0; q < NQ; ++q) yv[q] = src[q * 32];
-        } else {
-          const uint32_t a = map_rank(xbase + static_cast<uint32_t>(((kk % kSpWarps) * NQ) * 32 * sizeof(T)),
-                                      static_cast<uint32_t>(kk / kSpWarps));
 #pragma unroll
-          for (int q = 0; q < NQ; ++q) yv[q] = ld_cluster<T>(a + static_cast<uint32_t>(q * 32 * sizeof(T)));
+          for (int h = 0; h < NU; ++h) {
+            const S* rr = srinv + static_cast<size_t>(rows[h]) * R + kk * NQ;
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) zu[h] = vfma(rr[q], yv[q], zu[h]);
+          }
         }
+      } else {
+        // K = 8 CS blocks, their y values in the CTAs of the cluster: the
+        // remote (DSMEM) loads of KU blocks are issued back to back before
+        // their FMAs, so the ~cluster-latency is paid K / KU times, not K
+        constexpr int KU = PENT ? 4 : 8;
+#pragma unroll 1
+        for (int k0 = 0; k0 < 8 * CS; k0 += KU) {
+          T yv[KU][NQ];
 #pragma unroll
-        for (int h = 0; h < NU; ++h) {
-          const S* rr = srinv + static_cast<size_t>(rows[h]) * R + kk * NQ;
+          for (int u = 0; u < KU; ++u) {
+            const int kk = k0 + u;
+            const uint32_t a = map_rank(xbase + static_cast<uint32_t>(((kk % kSpWarps) * NQ) * 32 * sizeof(T)),
+                                        static_cast<uint32_t>(kk / kSpWarps));
 #pragma unroll
-          for (int q = 0; q < NQ; ++q) zu[h] = vfma(rr[q], yv[q], zu[h]);
+            for (int q = 0; q < NQ; ++q) yv[u][q] = ld_cluster<T>(a + static_cast<uint32_t>(q * 32 * sizeof(T)));
+          }
+#pragma unroll
+          for (int u = 0; u < KU; ++u) {
+#pragma unroll
+            for (int h = 0; h < NU; ++h) {
+              const S* rr = srinv + static_cast<size_t>(rows[h]) * R + (k0 + u) * NQ;
+#pragma unroll
+              for (int q = 0; q < NQ; ++q) zu[h] = vfma(rr[q], yv[u][q], zu[h]);
+            }
+          }
         }
       }
       if (k == 0) {  // no left neighbour
