@@ -241,6 +241,39 @@ def load_traffic(config: str, mode: str) -> float | None:
         return None
 
 
+def sustained_copy_gbs(torch, ms_timed: float) -> float | None:
+    """Device copy rate (read + write bytes) back to back for as long as the
+    timed region lasted (0.2-1.5 s), right after it: what the board sustains
+    under its power cap for a long step, next to the burst copy figure of
+    MEASURED_PEAKS.json that `frac` is quoted against. Context only."""
+    if ms_timed < 100.0:
+        return None
+    try:
+        nbytes = 2 << 30
+        a = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+        b = torch.empty_like(a)
+        a.fill_(1)
+        b.copy_(a)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        b.copy_(a)
+        e1.record()
+        torch.cuda.synchronize()
+        reps = max(4, int(min(max(ms_timed, 200.0), 1500.0) / max(e0.elapsed_time(e1), 1e-3)))
+        e0.record()
+        for _ in range(reps):
+            b.copy_(a)
+        e1.record()
+        torch.cuda.synchronize()
+        gbs = 2.0 * nbytes * reps / (e0.elapsed_time(e1) / 1e3) / 1e9
+        del a, b
+        torch.cuda.empty_cache()
+        return gbs
+    except Exception:  # no room next to the batch: leave it out
+        return None
+
+
 def kernel_name(plan: str, f32: bool, kind: str, mode: str) -> str:
     """Name of the sweep kernel the plan launches (what ncu lists)."""
     k = plan.split()[0] if plan else "?"
@@ -343,6 +376,7 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
     achieved = algo_bytes / (ms_local / args.steps / 1e3) / 1e9
     peak, peak_src = load_peak()
     traffic = load_traffic(args.config, args.mode)
+    sustained = sustained_copy_gbs(torch, ms_local) if not args.no_sustained else None
     plan = lib.describe_plan(0 if kind == "tri" else 1, n, m, ld, args.f32)
 
     # e2e through the reference-facing host API (pinned host batch; H2D,
@@ -403,6 +437,8 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
                               f"(working set {nbuf * bytes_per / l2:.1f}x L2, inputs larger than L2)")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
+                         "sustained_copy_gbs": sustained,
+                         "frac_of_sustained_copy": achieved / sustained if sustained else None,
                          "algorithmic_bytes_per_launch": algo_bytes, "peak_source": peak_src,
                          "kernel": kernel_name(plan, args.f32, kind, args.mode)},
             "cpu_baseline": cpu,
@@ -428,6 +464,7 @@ def main() -> int:
     ap.add_argument("--f32", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-API end-to-end leg (tuning runs)")
+    ap.add_argument("--no-sustained", action="store_true", help="skip the sustained device-copy reference rate")
     ap.add_argument("--pitch-pad", type=int, default=0, help="extra elements per row of the device batch (layout runs)")
     ap.add_argument("--periodic", action="store_true", help="cyclic (periodic) variant of the config's LHS")
     ap.add_argument("--cn", action="store_true",

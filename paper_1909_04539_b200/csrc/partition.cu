@@ -320,8 +320,8 @@ __global__ void __launch_bounds__(128) part_fwd_kernel(double* __restrict__ x, i
                                            bwd + static_cast<long long>(r0) * (PENT ? 2 : 1)};
   double s1 = 0.0, s2 = 0.0, a0 = 0.0, a1 = 0.0;
   const DotHook<PENT> hook{pr + r0, pr + n + r0, &a0, &a1};
-  dev::column_forward<double, PENT, true, kPartU>(x + static_cast<long long>(r0) * ld + j, len, ld, rows, s1, s2,
-                                                  hook);
+  dev::column_forward<double, PENT, true, kPartU, DotHook<PENT>, 2>(x + static_cast<long long>(r0) * ld + j, len, ld,
+                                                                    rows, s1, s2, hook);
   if constexpr (PENT) {
     const double g = static_cast<const double*>(rows.bwd)[2 * (len - 2)];  // gamma_{L-2}
     yi[static_cast<long long>(4 * k) * m + j] = a0;
@@ -403,6 +403,11 @@ __global__ void __launch_bounds__(128) part_fwd_stencil_kernel(
   }
   for (int b = 0; b < full; ++b) {
     const int i0 = b * kStU;
+    if (b + 3 < full) {  // L2 prefetch two runs beyond the register double buffer
+      prefetch_l2(own + i0 + 3 * kStU);
+      if (needA) prefetch_l2(rowA + i0 + 3 * kStU);
+      if (needB) prefetch_l2(rowB + i0 + 3 * kStU);
+    }
     if (b + 1 < full) {
       load8(own, i0 + kStU, n0);
       if (needA) load8(rowA, i0 + kStU, nA);
@@ -568,20 +573,20 @@ __global__ void __launch_bounds__(128, PENT ? 1 : 4) part_bwd_kernel(double* __r
     if constexpr (PER) {
       col[static_cast<long long>(len - 2) * ld] = corr(len - 2, s1);
       col[static_cast<long long>(len - 1) * ld] = corr(len - 1, s2);
-      dev::column_backward<double, PENT, true, kPartU>(col, len - 2, ld, rows, s1, s2, hook, corr);
+      dev::column_backward<double, PENT, true, kPartU, LeftHook<PENT>, CorrHook<PENT>, 2>(col, len - 2, ld, rows, s1, s2, hook, corr);
     } else {
       col[static_cast<long long>(len - 2) * ld] = s1;
       col[static_cast<long long>(len - 1) * ld] = s2;
-      dev::column_backward<double, PENT, true, kPartU>(col, len - 2, ld, rows, s1, s2, hook);
+      dev::column_backward<double, PENT, true, kPartU, LeftHook<PENT>, dev::NoHook, 2>(col, len - 2, ld, rows, s1, s2, hook);
     }
   } else {
     s1 = zu[0];  // own row L-1
     if constexpr (PER) {
       col[static_cast<long long>(len - 1) * ld] = corr(len - 1, s1);
-      dev::column_backward<double, PENT, true, kPartU>(col, len - 1, ld, rows, s1, s2, hook, corr);
+      dev::column_backward<double, PENT, true, kPartU, LeftHook<PENT>, CorrHook<PENT>, 2>(col, len - 1, ld, rows, s1, s2, hook, corr);
     } else {
       col[static_cast<long long>(len - 1) * ld] = s1;
-      dev::column_backward<double, PENT, true, kPartU>(col, len - 1, ld, rows, s1, s2, hook);
+      dev::column_backward<double, PENT, true, kPartU, LeftHook<PENT>, dev::NoHook, 2>(col, len - 1, ld, rows, s1, s2, hook);
     }
   }
 }

@@ -1580,7 +1580,7 @@ int get_devices(int* ids, int capacity) {
 
 // Host-batch solve: the m columns are split over the device list exactly as
 // the reference splits them over its workers (parallel.cpp:53-54, j0 =
-// m*g/G); each shard streams ~16 MiB column chunks through its own device's
+// m*g/G); each shard streams ~64 MiB column chunks through its own device's
 // staging pipeline (kStages streams: chunk k's H2D overlaps chunk k-1's sweep
 // and chunk k-2's D2H), so each GPU's copies use that GPU's own PCIe link.
 // One host thread issues everything asynchronously, round-robin over the
@@ -1611,7 +1611,7 @@ bandsolve_status solve_host(const Factor& f, double* x, std::size_t n, std::size
   };
   const std::size_t G = devs.size();
   const std::size_t row_bytes = n * sizeof(double);
-  const std::size_t chunk_mib = static_cast<std::size_t>(std::max(1, env_int("HOST_CHUNK_MIB", 16)));
+  const std::size_t chunk_mib = static_cast<std::size_t>(std::max(1, env_int("HOST_CHUNK_MIB", 64)));
   std::vector<Shard> shards;
   bandsolve_status st = BANDSOLVE_OK;
   for (std::size_t g = 0; g < G && st == BANDSOLVE_OK; ++g) {

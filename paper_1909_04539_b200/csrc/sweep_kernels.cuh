@@ -269,7 +269,11 @@ struct NoHook {
   __device__ __forceinline__ T operator()(int, T v) const { return v; }
 };
 
-template <typename T, bool PENT, bool FAST, int U, typename Post = NoHook>
+// L2 prefetch (no register cost): PF > 0 pulls the rows PF blocks beyond the
+// register double buffer into L2 so its loads pay L2, not HBM, latency
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
+template <typename T, bool PENT, bool FAST, int U, typename Post = NoHook, int PF = 0>
 __device__ __forceinline__ void column_forward(T* col, int n, long long ld, const Rows<T, PENT, FAST>& rows,
                                                T& s1, T& s2, const Post& post = Post{}) {
   T cur[U], nxt[U];
@@ -280,6 +284,12 @@ __device__ __forceinline__ void column_forward(T* col, int n, long long ld, cons
   }
   for (int b = 0; b < full; ++b) {
     const int i0 = b * U;
+    if constexpr (PF > 0) {
+      if (b + 1 + PF < full) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) prefetch_l2(col + static_cast<long long>(i0 + (1 + PF) * U + u) * ld);
+      }
+    }
     if (b + 1 < full) {
 #pragma unroll
       for (int u = 0; u < U; ++u) nxt[u] = col[static_cast<long long>(i0 + U + u) * ld];
@@ -302,7 +312,7 @@ __device__ __forceinline__ void column_forward(T* col, int n, long long ld, cons
 }
 
 // backward over rows [0, n): the tail rows first (descending), then whole blocks
-template <typename T, bool PENT, bool FAST, int U, typename Pre = NoHook, typename Out = NoHook>
+template <typename T, bool PENT, bool FAST, int U, typename Pre = NoHook, typename Out = NoHook, int PF = 0>
 __device__ __forceinline__ void column_backward(T* col, int n, long long ld, const Rows<T, PENT, FAST>& rows,
                                                 T& s1, T& s2, const Pre& pre = Pre{}, const Out& out = Out{}) {
   T cur[U], nxt[U];
@@ -318,6 +328,12 @@ __device__ __forceinline__ void column_backward(T* col, int n, long long ld, con
   }
   for (int b = full - 1; b >= 0; --b) {
     const int i0 = b * U;
+    if constexpr (PF > 0) {
+      if (b - 1 - PF >= 0) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) prefetch_l2(col + static_cast<long long>(i0 - (1 + PF) * U + u) * ld);
+      }
+    }
     if (b > 0) {
 #pragma unroll
       for (int u = 0; u < U; ++u) nxt[u] = col[static_cast<long long>(i0 - U + u) * ld];
@@ -332,22 +348,22 @@ __device__ __forceinline__ void column_backward(T* col, int n, long long ld, con
   }
 }
 
-template <typename T, bool PENT, bool FAST, int U>
+template <typename T, bool PENT, bool FAST, int U, int PF = 0>
 __device__ __forceinline__ void column_sweep(T* col, int n, long long ld, const Rows<T, PENT, FAST>& rows) {
   T s1 = T(0), s2 = T(0);
-  column_forward<T, PENT, FAST, U>(col, n, ld, rows, s1, s2);
+  column_forward<T, PENT, FAST, U, NoHook, PF>(col, n, ld, rows, s1, s2);
   s1 = T(0);
   s2 = T(0);
-  column_backward<T, PENT, FAST, U>(col, n, ld, rows, s1, s2);
+  column_backward<T, PENT, FAST, U, NoHook, NoHook, PF>(col, n, ld, rows, s1, s2);
 }
 
-template <typename T, bool PENT, bool FAST, int U = 8>
+template <typename T, bool PENT, bool FAST, int U = 8, int PF = 0>
 __global__ void __launch_bounds__(128) sweep_global(T* __restrict__ x, int n, long long m,
                                                     long long ld, const void* __restrict__ fwd,
                                                     const void* __restrict__ bwd) {
   const long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= m) return;
-  column_sweep<T, PENT, FAST, U>(x + j, n, ld, Rows<T, PENT, FAST>{fwd, bwd});
+  column_sweep<T, PENT, FAST, U, PF>(x + j, n, ld, Rows<T, PENT, FAST>{fwd, bwd});
 }
 
 }  // namespace dev
