@@ -727,7 +727,9 @@ std::vector<unsigned char> spike_blob(const PartPlan& p, int n) {
   const std::size_t nf = static_cast<std::size_t>(n);
   const std::size_t sf = p.pent ? sizeof(dev::SpF<T, true>) : sizeof(dev::SpF<T, false>);
   const std::size_t sb = p.pent ? sizeof(dev::SpB<T, true>) : sizeof(dev::SpB<T, false>);
-  std::vector<unsigned char> blob(nf * (sf + sb) + p.rinv.size() * sizeof(T), 0);
+  // [F x n][B x n][pent: U^-1 row 1 x n][R^-1]
+  const std::size_t sp = p.pent ? sizeof(T) : 0;
+  std::vector<unsigned char> blob(nf * (sf + sb + sp) + p.rinv.size() * sizeof(T), 0);
   for (std::size_t u = 0; u < nf; ++u) {
     if (p.pent) {
       dev::SpF<T, true> f{};
@@ -735,7 +737,8 @@ std::vector<unsigned char> spike_blob(const PartPlan& p, int n) {
       f.b = static_cast<T>(p.fwd[4 * u + 1]);   // beta/alpha
       f.ia = static_cast<T>(p.fwd[4 * u + 2]);  // 1/alpha
       f.p0 = static_cast<T>(p.pr[u]);           // U^-1 row 0
-      f.p1 = static_cast<T>(p.pr[nf + u]);      // U^-1 row 1
+      const T p1 = static_cast<T>(p.pr[nf + u]);  // U^-1 row 1
+      std::memcpy(blob.data() + nf * (sf + sb) + u * sp, &p1, sp);
       dev::SpB<T, true> b{};
       b.g = static_cast<T>(p.bwd[2 * u]);       // gamma
       b.d = static_cast<T>(p.bwd[2 * u + 1]);   // delta
@@ -755,7 +758,7 @@ std::vector<unsigned char> spike_blob(const PartPlan& p, int n) {
       std::memcpy(blob.data() + nf * sf + u * sb, &b, sb);
     }
   }
-  T* r = reinterpret_cast<T*>(blob.data() + nf * (sf + sb));
+  T* r = reinterpret_cast<T*>(blob.data() + nf * (sf + sb + sp));
   for (std::size_t i = 0; i < p.rinv.size(); ++i) r[i] = static_cast<T>(p.rinv[i]);
   return blob;
 }
@@ -933,7 +936,7 @@ bandsolve_status spike_solve_t(const Factor& f, T* x, std::size_t n, std::size_t
   const int R = p->R;
   const int KB = spike_ring_slots(N, K, pent, per != nullptr, sizeof(T), sizeof(S));
   const std::size_t rec_bytes =
-      static_cast<std::size_t>(n) * (pent ? sizeof(dev::SpF<S, true>) + sizeof(dev::SpB<S, true>)
+      static_cast<std::size_t>(n) * (pent ? sizeof(dev::SpF<S, true>) + sizeof(dev::SpB<S, true>) + sizeof(S)
                                           : sizeof(dev::SpF<S, false>) + sizeof(dev::SpB<S, false>));
   const S* rinv = reinterpret_cast<const S*>(static_cast<const unsigned char*>(blob) + rec_bytes);
   CUtensorMap map;

@@ -70,7 +70,7 @@ template <typename T, bool PENT>
 struct SpF;  // forward: fast records + U^-1 row entries
 template <typename T>
 struct alignas(16) SpF<T, true> {
-  T e, b, ia, p0, p1, pad;  // e = eps/alpha, b = beta/alpha, ia = 1/alpha (block-local)
+  T e, b, ia, p0;  // e = eps/alpha, b = beta/alpha, ia = 1/alpha (block-local); U^-1 row 1 in its own array
 };
 template <typename T>
 struct alignas(16) SpF<T, false> {
@@ -110,7 +110,7 @@ struct SpikePer {
 __host__ __device__ constexpr int spike_rinv_rows(int Kc, int nh) { return (Kc + 3) * nh; }
 
 struct SpikeLayout {
-  size_t fwd_off, bwd_off, z_off, rinv_off, xch_off, ring_off, bar_off, total;
+  size_t fwd_off, p1_off, bwd_off, z_off, rinv_off, xch_off, ring_off, bar_off, total;
   // nl: rows whose records this CTA holds; R: interface unknowns; Kc: blocks
   // per CTA; elem: 8 (fp64) / 4 (fp32)
   // rec: record / R^-1 element size (0: elem; 4 for the paired fp32 kernel)
@@ -123,7 +123,10 @@ struct SpikeLayout {
     const size_t sb = rec == 8 ? (pent ? sizeof(SpB<double, true>) : sizeof(SpB<double, false>))
                                : (pent ? sizeof(SpB<float, true>) : sizeof(SpB<float, false>));
     L.fwd_off = 0;
-    L.bwd_off = align128(static_cast<size_t>(nl) * sf);
+    // pent: U^-1 row 1 as a plain array (a 16-byte aligned 5-value record
+    // would carry a pad word: 8 KB at N = 1024, the room of a fourth ring slot)
+    L.p1_off = align128(static_cast<size_t>(nl) * sf);
+    L.bwd_off = L.p1_off + (pent ? align128(static_cast<size_t>(nl) * rec) : 0);
     L.z_off = L.bwd_off + align128(static_cast<size_t>(nl) * sb);
     // z of the periodic correction: [nl] pairs (pent) / values (tri)
     L.rinv_off = L.z_off + (per ? align128(static_cast<size_t>(nl) * (pent ? 2 : 1) * sizeof(double)) : 0);
@@ -242,6 +245,7 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
   const long long ncl = gridDim.x / CS;
   const SpikeLayout Ly = SpikeLayout::make(nl, R, Kc, KB, PENT, PER, sizeof(T), sizeof(S));
   F* sf = reinterpret_cast<F*>(smem + Ly.fwd_off);
+  S* sp1 = reinterpret_cast<S*>(smem + Ly.p1_off);
   B* sb = reinterpret_cast<B*>(smem + Ly.bwd_off);
   S* srinv = reinterpret_cast<S*>(smem + Ly.rinv_off);
   T* xch = reinterpret_cast<T*>(smem + Ly.xch_off);
@@ -263,6 +267,10 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
     constexpr int wf = sizeof(F) / 16, wb = sizeof(B) / 16;
     for (int i = threadIdx.x; i < nl * wf; i += blockDim.x) dstf[i] = srcf[static_cast<size_t>(row0) * wf + i];
     for (int i = threadIdx.x; i < nl * wb; i += blockDim.x) dstb[i] = srcb[static_cast<size_t>(row0) * wb + i];
+    if constexpr (PENT) {  // blob: [F x n][B x n][p1 x n][R^-1]
+      const S* srcp = reinterpret_cast<const S*>(static_cast<const B*>(static_cast<const void*>(srcb)) + n);
+      for (int i = threadIdx.x; i < nl; i += blockDim.x) sp1[i] = srcp[row0 + i];
+    }
     const int nr = spike_rinv_rows(Kc, NH);
     for (int i = threadIdx.x; i < nr * R; i += blockDim.x) {
       const int t = i / R, c = i - t * R;
@@ -376,6 +384,7 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
     int slot = 0;
     uint32_t phase = 0;
     const F* fk = sf + rl;
+    const S* p1k = sp1 + rl;
     const B* bk = sb + rl;
     const double* zk = reinterpret_cast<const double*>(smem + Ly.z_off) + (PENT ? 2 : 1) * rl;
 
@@ -414,6 +423,7 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
       mbar_wait(&full[slot], phase);
       const T* blk = ring + slot * kChunk + warp * kBox + lane;
       const F* fc = fk + c * kSpR;
+      const S* p1c = p1k + c * kSpR;
       TP buf;
       T dv[kSpR];  // stage 1: b / pivot for the whole chunk (off the chain)
       if constexpr (CN) {
@@ -468,7 +478,7 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
         T v;
         if constexpr (PENT) {
           v = vfma(-f.b, fs1, vfma(-f.e, fs2, dv[r]));
-          a1 = vfma(f.p1, v, a1);
+          a1 = vfma(p1c[r], v, a1);
         } else {
           v = vfma(-f.am, fs1, dv[r]);
         }
