@@ -376,3 +376,37 @@ def test_config5_pent_n1024_batch_2p24(lib, oracle, cuda_device):
     finally:
         del x
         torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("mode", [bs.MODE_EXACT, bs.MODE_FAST])
+@pytest.mark.parametrize("n", [64, 512, 1024, 4096])
+def test_config3_tri_f32_batch_2p20(lib, oracle, cuda_device, mode, n):
+    """configs[2] in fp32 at its full batch (2^20 systems; N = 4096 at 2^18):
+    the fp32 plans (system pairs per lane) within north_star's fp32
+    tolerance of the reference solving the same fp32-rounded right-hand
+    sides, on a column sample spread over the batch, plus its residual."""
+    torch = cuda_device
+    lib.set_mode(mode)
+    m = 1 << 20 if n <= 1024 else 1 << 18
+    bands = bs.diffusion_bands(1.0, n)
+    f = bs.TriFactor(lib, *bands)
+    x64 = torch.empty((n, m), dtype=torch.float64, device="cuda")
+    lib.fill_rhs_dev(x64.data_ptr(), n, m, m, seed=42)
+    x = x64.float()
+    del x64
+    rng = np.random.default_rng(n)
+    cols = np.unique(np.concatenate([np.arange(64), np.arange(m - 64, m), rng.integers(0, m, 128)]))
+    idx = torch.from_numpy(cols).cuda()
+    rhs = x[:, idx].double().cpu().numpy()
+    try:
+        f.solve_dev(x.data_ptr(), n, m, f32=True)
+        torch.cuda.synchronize()
+        got = x[:, idx].double().cpu().numpy()
+        want = oracle.tri_solve(oracle.tri_prefactor(*bands), rhs.copy())
+        assert per_system_max_rel(got, want) <= TOL_F32, (n, m)
+        sx, sr = bs.Batch.from_array(lib, got), bs.Batch.from_array(lib, rhs)
+        assert lib.tri_residual(*bands, sx, sr) <= TOL_F32
+    finally:
+        lib.set_mode(bs.MODE_EXACT)
+        del x
+        torch.cuda.empty_cache()
