@@ -321,7 +321,7 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
     # ping-pong between two buffers.
     l2 = 132644864
     bytes_per = n * m * elem
-    nbuf = 1 if bytes_per >= 4 * l2 else min(8, -(-4 * l2 // bytes_per))
+    nbuf = 1 if bytes_per >= 4 * l2 else -(-4 * l2 // bytes_per)  # configs[0] (8 MiB): 64 buffers
     if adi or args.cn:
         nbuf = max(2, nbuf)
     ld = m + args.pitch_pad  # row pitch of the device batch (elements)
