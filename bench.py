@@ -386,7 +386,7 @@ def run_gpu_arm(args, rank: int, world: int, local_rank: int) -> None:
         # pinned host batch of this rank's columns (a leading column sample
         # when the shard exceeds E2E_MAX_SYSTEMS: host RAM, not the device,
         # bounds it), regenerated from the same generator indices
-        me = min(m, E2E_MAX_SYSTEMS)
+        me = min(m, max(32, E2E_MAX_SYSTEMS // world // 32 * 32))  # 16 GiB of pinned host memory in all
         host = bs.Batch(lib, n, me)
         tmp = torch.empty((n, me), dtype=torch.float64, device="cuda")
         lib.fill_rhs_dev(tmp.data_ptr(), n, me, me, SEED, j0, sptr)
