@@ -58,7 +58,7 @@ CONFIGS = {
 STRONG = {"c5"}
 DEFAULT_CONFIG = "c5"
 DEFAULT_MODE = "fast"
-E2E_MAX_SYSTEMS = 1 << 21  # pinned host batch per rank for e2e (16 GiB at N=1024): host RAM bound
+E2E_MAX_SYSTEMS = 1 << 21  # pinned host batch for e2e, split over the ranks (16 GiB at N=1024): host RAM bound
 SEED = 42
 
 NVML_REASONS = {
