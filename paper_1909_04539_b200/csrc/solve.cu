@@ -757,7 +757,15 @@ cudaError_t launch_global(T* x, int n, long long m, long long ld, const void* fw
   while (threads > 32 && (m + threads - 1) / threads < sms) threads >>= 1;
   const long long grid = (m + threads - 1) / threads;
   const bool deep = m <= static_cast<long long>(sms) * 64 && n >= 256;  // few long systems
-  if (deep)
+  // records in shared memory (16-byte rounded; the packed arrays are 256-byte padded)
+  const int rec_f = (n * static_cast<int>(PENT ? sizeof(dev::PentFwd<T>) : sizeof(dev::TriFwd<T>)) + 15) / 16 * 16;
+  const int rec_b = (n * static_cast<int>(PENT ? sizeof(dev::PentBwd<T>) : sizeof(T)) + 15) / 16 * 16;
+  if (deep && static_cast<std::size_t>(rec_f + rec_b) <= kSmemPerBlockMax && !tune_flag("GLOBAL_NOREC")) {
+    auto kern = dev::sweep_global_rec<T, PENT, FAST, 32>;  // 16-row blocks / L2 prefetch measured slower
+    static std::atomic<uint64_t> configured{0};
+    if (cudaError_t e = allow_big_smem_once(kern, configured); e != cudaSuccess) return e;
+    kern<<<static_cast<unsigned>(grid), threads, rec_f + rec_b, s>>>(x, n, m, ld, fwd, bwd, rec_f, rec_b);
+  } else if (deep)
     dev::sweep_global<T, PENT, FAST, 32><<<static_cast<unsigned>(grid), threads, 0, s>>>(x, n, m, ld, fwd, bwd);
   else
     dev::sweep_global<T, PENT, FAST><<<static_cast<unsigned>(grid), threads, 0, s>>>(x, n, m, ld, fwd, bwd);

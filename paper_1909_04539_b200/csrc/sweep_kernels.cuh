@@ -366,5 +366,28 @@ __global__ void __launch_bounds__(128) sweep_global(T* __restrict__ x, int n, lo
   column_sweep<T, PENT, FAST, U, PF>(x + j, n, ld, Rows<T, PENT, FAST>{fwd, bwd});
 }
 
+// Few long systems (one warp per SM, e.g. the ADI axes): the same sweep with
+// the factor records staged once into shared memory (fwd then bwd arrays,
+// rec_f / rec_b bytes), so every row reads its record with a shared load
+// instead of an L2 round trip; the RHS still streams through the register
+// double buffer.
+template <typename T, bool PENT, bool FAST, int U, int PF = 0>
+__global__ void __launch_bounds__(128) sweep_global_rec(T* __restrict__ x, int n, long long m, long long ld,
+                                                        const void* __restrict__ fwd, const void* __restrict__ bwd,
+                                                        int rec_f, int rec_b) {
+  extern __shared__ __align__(16) unsigned char srec[];
+  {
+    const uint4* sf = static_cast<const uint4*>(fwd);
+    const uint4* sb = static_cast<const uint4*>(bwd);
+    uint4* d = reinterpret_cast<uint4*>(srec);
+    for (int i = threadIdx.x; i < rec_f / 16; i += blockDim.x) d[i] = sf[i];
+    for (int i = threadIdx.x; i < rec_b / 16; i += blockDim.x) d[rec_f / 16 + i] = sb[i];
+  }
+  __syncthreads();
+  const long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  column_sweep<T, PENT, FAST, U, PF>(x + j, n, ld, Rows<T, PENT, FAST>{srec, srec + rec_f});
+}
+
 }  // namespace dev
 }  // namespace bsb
