@@ -293,6 +293,21 @@ std::unique_ptr<PartPlan, PartPlanDeleter> build_plan(const Factor& f, int K) {
 // ---- kernels ------------------------------------------------------------------
 constexpr int kPartU = 16;  // rows per register block (two in flight per thread)
 
+// Per-row arrays of the block a CTA solves, staged once into shared memory
+// when every thread of the CTA works on the same block (the ADI axes: m a
+// multiple of 128): the rows' factor records, U^-1 rows, coupling images and
+// periodic z are then shared loads instead of an L2 round trip per row on
+// the dependency chain. Returns that block, or -1 (the global arrays are used).
+__device__ __forceinline__ int cta_block(long long m, int K, int stage) {
+  if (!stage) return -1;
+  const long long t0 = static_cast<long long>(blockIdx.x) * blockDim.x, t1 = t0 + blockDim.x - 1;
+  if (t1 >= static_cast<long long>(K) * m) return -1;
+  return t0 / m == t1 / m ? static_cast<int>(t0 / m) : -1;
+}
+__device__ __forceinline__ void cta_copy(double* dst, const double* src, int count) {
+  for (int i = threadIdx.x; i < count; i += blockDim.x) dst[i] = src[i];
+}
+
 template <bool PENT>
 struct DotHook {  // accumulates the top interface values of y during the forward sweep
   const double* p0;
@@ -309,17 +324,29 @@ template <bool PENT>
 __global__ void __launch_bounds__(128) part_fwd_kernel(double* __restrict__ x, int n, long long m, long long ld,
                                                        int K, int L, const double* __restrict__ fwd,
                                                        const double* __restrict__ bwd,
-                                                       const double* __restrict__ pr, double* __restrict__ yi) {
+                                                       const double* __restrict__ pr, double* __restrict__ yi,
+                                                       int stage) {
+  extern __shared__ __align__(128) double pst[];
+  constexpr int FW = PENT ? 4 : 2;
+  const int kc = cta_block(m, K, stage);
+  if (kc >= 0) {  // [records FW x len | P0 | P1]
+    const int r0c = kc * L, lenc = kc + 1 < K ? L : n - r0c;
+    cta_copy(pst, fwd + static_cast<long long>(r0c) * FW, lenc * FW);
+    cta_copy(pst + lenc * FW, pr + r0c, lenc);
+    if constexpr (PENT) cta_copy(pst + lenc * (FW + 1), pr + n + r0c, lenc);
+  }
+  __syncthreads();
   const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= static_cast<long long>(K) * m) return;
   const int k = static_cast<int>(t / m);
   const long long j = t - static_cast<long long>(k) * m;
   const int r0 = k * L;
   const int len = k + 1 < K ? L : n - r0;
-  const dev::Rows<double, PENT, true> rows{fwd + static_cast<long long>(r0) * (PENT ? 4 : 2),
+  const bool sh = kc >= 0;
+  const dev::Rows<double, PENT, true> rows{sh ? pst : fwd + static_cast<long long>(r0) * FW,
                                            bwd + static_cast<long long>(r0) * (PENT ? 2 : 1)};
   double s1 = 0.0, s2 = 0.0, a0 = 0.0, a1 = 0.0;
-  const DotHook<PENT> hook{pr + r0, pr + n + r0, &a0, &a1};
+  const DotHook<PENT> hook{sh ? pst + len * FW : pr + r0, sh ? pst + len * (FW + 1) : pr + n + r0, &a0, &a1};
   dev::column_forward<double, PENT, true, kPartU, DotHook<PENT>, 2>(x + static_cast<long long>(r0) * ld + j, len, ld,
                                                                     rows, s1, s2, hook);
   if constexpr (PENT) {
@@ -349,8 +376,18 @@ template <bool PENT>
 __global__ void __launch_bounds__(128) part_fwd_stencil_kernel(
     double* __restrict__ x, int n, long long m, long long ld, int K, int L, const double* __restrict__ fwd,
     const double* __restrict__ bwd, const double* __restrict__ pr, double* __restrict__ yi,
-    const double* __restrict__ src, long long lds, double cs, double cs4, double cmid) {
+    const double* __restrict__ src, long long lds, double cs, double cs4, double cmid, int stage) {
   using namespace dev;
+  extern __shared__ __align__(128) double pst[];
+  constexpr int FW = PENT ? 4 : 2;
+  const int kc = cta_block(m, K, stage);
+  if (kc >= 0) {  // [records FW x len | P0 | P1]
+    const int r0c = kc * L, lenc = kc + 1 < K ? L : n - r0c;
+    cta_copy(pst, fwd + static_cast<long long>(r0c) * FW, lenc * FW);
+    cta_copy(pst + lenc * FW, pr + r0c, lenc);
+    if constexpr (PENT) cta_copy(pst + lenc * (FW + 1), pr + n + r0c, lenc);
+  }
+  __syncthreads();
   const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= static_cast<long long>(K) * m) return;  // whole warps (m % 32 == 0)
   const int lane = threadIdx.x & 31;
@@ -358,7 +395,8 @@ __global__ void __launch_bounds__(128) part_fwd_stencil_kernel(
   const long long j = t - static_cast<long long>(k) * m;
   const int r0 = k * L;
   const int len = k + 1 < K ? L : n - r0;
-  const dev::Rows<double, PENT, true> rows{fwd + static_cast<long long>(r0) * (PENT ? 4 : 2),
+  const bool sh = kc >= 0;
+  const dev::Rows<double, PENT, true> rows{sh ? pst : fwd + static_cast<long long>(r0) * FW,
                                            bwd + static_cast<long long>(r0) * (PENT ? 2 : 1)};
   // rows outside the warp: A = the nearer neighbour (lanes 0 / 31), B = the
   // farther (pent: lanes 0, 1 / 30, 31); periodic across the m systems
@@ -375,8 +413,8 @@ __global__ void __launch_bounds__(128) part_fwd_stencil_kernel(
   const bool needA = lane == 0 || lane == 31;
   const bool needB = PENT && (lane <= 1 || lane >= 30);
   double* col = x + static_cast<long long>(r0) * ld + j;
-  const double* p0 = pr + r0;
-  const double* p1 = pr + n + r0;
+  const double* p0 = sh ? pst + len * FW : pr + r0;
+  const double* p1 = sh ? pst + len * (FW + 1) : pr + n + r0;
   double s1 = 0.0, s2 = 0.0, a0 = 0.0, a1 = 0.0;
   auto rhs_row = [&](double c, double d1, double u1, double d2, double u2) {
     if constexpr (PENT) {  // pde.cpp:108 order
@@ -499,7 +537,22 @@ __global__ void __launch_bounds__(128, PENT ? 1 : 4) part_bwd_kernel(double* __r
                                                        const double* __restrict__ bwd,
                                                        const double* __restrict__ fl,
                                                        const double* __restrict__ rinv,
-                                                       const double* __restrict__ yi, PartPeriodic per) {
+                                                       const double* __restrict__ yi, PartPeriodic per,
+                                                       int stage) {
+  extern __shared__ __align__(128) double pst[];
+  constexpr int BWN = PENT ? 2 : 1;  // doubles per bwd record; also F / z arrays per row
+  const int kc = cta_block(m, K, stage);
+  if (kc >= 0) {  // [bwd records | F1 (| F2) | (PER) z1 (| z2)]
+    const int r0c = kc * L, lenc = kc + 1 < K ? L : n - r0c;
+    cta_copy(pst, bwd + static_cast<long long>(r0c) * BWN, lenc * BWN);
+    cta_copy(pst + lenc * BWN, fl + r0c, lenc);
+    if constexpr (PENT) cta_copy(pst + lenc * (BWN + 1), fl + n + r0c, lenc);
+    if constexpr (PER) {
+      cta_copy(pst + lenc * 2 * BWN, per.z1 + r0c, lenc);
+      if constexpr (PENT) cta_copy(pst + lenc * (2 * BWN + 1), per.z2 + r0c, lenc);
+    }
+  }
+  __syncthreads();
   const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= static_cast<long long>(K) * m) return;
   const int k = static_cast<int>(t / m);
@@ -544,10 +597,11 @@ __global__ void __launch_bounds__(128, PENT ? 1 : 4) part_bwd_kernel(double* __r
 #pragma unroll
     for (int u = 0; u < NU; ++u) zu[u] = fma(__ldg(rinv + rowsel[u] * R + c), y, zu[u]);
   }
+  const bool sh = kc >= 0;
   const dev::Rows<double, PENT, true> rows{fwd + static_cast<long long>(r0) * (PENT ? 4 : 2),
-                                           bwd + static_cast<long long>(r0) * (PENT ? 2 : 1)};
+                                           sh ? pst : bwd + static_cast<long long>(r0) * BWN};
   double* col = x + static_cast<long long>(r0) * ld + j;
-  LeftHook<PENT> hook{fl + r0, fl + n + r0, 0.0, 0.0};
+  LeftHook<PENT> hook{sh ? pst + len * BWN : fl + r0, sh ? pst + len * (BWN + 1) : fl + n + r0, 0.0, 0.0};
   if (k > 0) {
     if constexpr (PENT) {
       hook.xl2 = zu[2];  // x_{s-2}
@@ -556,7 +610,8 @@ __global__ void __launch_bounds__(128, PENT ? 1 : 4) part_bwd_kernel(double* __r
       hook.xl1 = zu[1];  // x_{s-1}
     }
   }
-  CorrHook<PENT> corr{per.z1 + r0, per.z2 + r0, 0.0, 0.0};
+  CorrHook<PENT> corr{sh ? pst + len * 2 * BWN : per.z1 + r0, sh ? pst + len * (2 * BWN + 1) : per.z2 + r0, 0.0,
+                      0.0};
   if constexpr (PER) {
     if constexpr (PENT) {  // periodic.cpp:189-194 (fast-mode rounding)
       const double w1 = zu[4] - zu[7], w2 = zu[5] - zu[6];
@@ -684,28 +739,36 @@ bandsolve_status partition_solve_device(const Factor& f, double* x, std::size_t 
   const long long tot = static_cast<long long>(K) * M;
   const unsigned g1 = static_cast<unsigned>((tot + 127) / 128);
   const PartPeriodic pa = per ? *per : PartPeriodic{};
+  // shared-memory staging of the CTA's block rows (cta_block): the longest
+  // block (the last absorbs n % K), within the default 48 KB
+  const int lmax = N - (K - 1) * p->L;
+  const std::size_t fb = static_cast<std::size_t>(lmax) * (pent ? 6 : 3) * sizeof(double);
+  const std::size_t bb = static_cast<std::size_t>(lmax) * (pent ? 4 : 2) * (per ? 2 : 1) * sizeof(double);
+  const bool stage_ok = fb <= 48 * 1024 && bb <= 48 * 1024 && !tune_flag("PART_NOSTAGE");
+  const int sg = stage_ok ? 1 : 0;
+  const std::size_t sf = stage_ok ? fb : 0, sb = stage_ok ? bb : 0;
   if (st) {
     if (pent)
-      part_fwd_stencil_kernel<true><<<g1, 128, 0, s>>>(x, N, M, LD, K, p->L, fwd, bwd, pr, yi, st->src, st->lds,
-                                                       st->s, st->s4, st->mid);
+      part_fwd_stencil_kernel<true><<<g1, 128, sf, s>>>(x, N, M, LD, K, p->L, fwd, bwd, pr, yi, st->src, st->lds,
+                                                        st->s, st->s4, st->mid, sg);
     else
-      part_fwd_stencil_kernel<false><<<g1, 128, 0, s>>>(x, N, M, LD, K, p->L, fwd, bwd, pr, yi, st->src, st->lds,
-                                                        st->s, st->s4, st->mid);
+      part_fwd_stencil_kernel<false><<<g1, 128, sf, s>>>(x, N, M, LD, K, p->L, fwd, bwd, pr, yi, st->src, st->lds,
+                                                         st->s, st->s4, st->mid, sg);
     if (per) {
-      if (pent) part_bwd_kernel<true, true><<<g1, 128, 0, s>>>(x, N, M, LD, K, p->L, fwd, bwd, fl, rinv, yi, pa);
-      else part_bwd_kernel<false, true><<<g1, 128, 0, s>>>(x, N, M, LD, K, p->L, fwd, bwd, fl, rinv, yi, pa);
+      if (pent) part_bwd_kernel<true, true><<<g1, 128, sb, s>>>(x, N, M, LD, K, p->L, fwd, bwd, fl, rinv, yi, pa, sg);
+      else part_bwd_kernel<false, true><<<g1, 128, sb, s>>>(x, N, M, LD, K, p->L, fwd, bwd, fl, rinv, yi, pa, sg);
     } else {
-      if (pent) part_bwd_kernel<true, false><<<g1, 128, 0, s>>>(x, N, M, LD, K, p->L, fwd, bwd, fl, rinv, yi, pa);
-      else part_bwd_kernel<false, false><<<g1, 128, 0, s>>>(x, N, M, LD, K, p->L, fwd, bwd, fl, rinv, yi, pa);
+      if (pent) part_bwd_kernel<true, false><<<g1, 128, sb, s>>>(x, N, M, LD, K, p->L, fwd, bwd, fl, rinv, yi, pa, sg);
+      else part_bwd_kernel<false, false><<<g1, 128, sb, s>>>(x, N, M, LD, K, p->L, fwd, bwd, fl, rinv, yi, pa, sg);
     }
   } else if (pent) {
-    part_fwd_kernel<true><<<g1, 128, 0, s>>>(x, N, M, LD, K, p->L, fwd, bwd, pr, yi);
-    if (per) part_bwd_kernel<true, true><<<g1, 128, 0, s>>>(x, N, M, LD, K, p->L, fwd, bwd, fl, rinv, yi, pa);
-    else part_bwd_kernel<true, false><<<g1, 128, 0, s>>>(x, N, M, LD, K, p->L, fwd, bwd, fl, rinv, yi, pa);
+    part_fwd_kernel<true><<<g1, 128, sf, s>>>(x, N, M, LD, K, p->L, fwd, bwd, pr, yi, sg);
+    if (per) part_bwd_kernel<true, true><<<g1, 128, sb, s>>>(x, N, M, LD, K, p->L, fwd, bwd, fl, rinv, yi, pa, sg);
+    else part_bwd_kernel<true, false><<<g1, 128, sb, s>>>(x, N, M, LD, K, p->L, fwd, bwd, fl, rinv, yi, pa, sg);
   } else {
-    part_fwd_kernel<false><<<g1, 128, 0, s>>>(x, N, M, LD, K, p->L, fwd, bwd, pr, yi);
-    if (per) part_bwd_kernel<false, true><<<g1, 128, 0, s>>>(x, N, M, LD, K, p->L, fwd, bwd, fl, rinv, yi, pa);
-    else part_bwd_kernel<false, false><<<g1, 128, 0, s>>>(x, N, M, LD, K, p->L, fwd, bwd, fl, rinv, yi, pa);
+    part_fwd_kernel<false><<<g1, 128, sf, s>>>(x, N, M, LD, K, p->L, fwd, bwd, pr, yi, sg);
+    if (per) part_bwd_kernel<false, true><<<g1, 128, sb, s>>>(x, N, M, LD, K, p->L, fwd, bwd, fl, rinv, yi, pa, sg);
+    else part_bwd_kernel<false, false><<<g1, 128, sb, s>>>(x, N, M, LD, K, p->L, fwd, bwd, fl, rinv, yi, pa, sg);
   }
   note_launches(2);
   cudaFreeAsync(yi, s);
