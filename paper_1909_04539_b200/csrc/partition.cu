@@ -666,7 +666,7 @@ int partition_blocks(std::size_t n, std::size_t m, int sms, bool pent) {
   // 4096 x 4096: tri K=16 1.12e11 vs K=32 1.0e11 rows/s; pent K=8 = K=16)
   const int kmax = pent ? 8 : 16;
   const int ke = static_cast<int>(tune_int("PART_K", 0));  // tuning override (power of two)
-  if (ke >= 2 && ke <= kmax && static_cast<int>(n) / ke >= 16) return ke;
+  if (ke >= 2 && ke <= kPartMaxR / (pent ? 4 : 2) && static_cast<int>(n) / ke >= 16) return ke;
   int K = 2;
   while (K < kmax && static_cast<std::size_t>(K) * m < static_cast<std::size_t>(sms) * 512 &&
          static_cast<int>(n) / (2 * K) >= 32)
