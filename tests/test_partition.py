@@ -135,7 +135,8 @@ def test_partition_periodic_fused_within_tolerance(lib, oracle, cuda_device, for
     if forced:
         lib.tune("PARTITION", forced)
     rng = np.random.default_rng(31)
-    for n, m in [(130, 7), (1024, 130), (2050, 64), (4096, 33)]:
+    # m a multiple of 128: every CTA solves one block (rows staged in shared memory)
+    for n, m in [(130, 7), (1024, 130), (2050, 64), (4096, 33), (1024, 256), (4096, 128)]:
         x = rng.uniform(-1, 1, (n, m))
         for bands in [(-1.0, 3.0, -1.0), (-0.3, 1.9, -0.5), (1.0, -4.0, 7.0, -4.0, 1.0), (0.2, -0.8, 3.1, -0.7, 0.1)]:
             if len(bands) == 3:
