@@ -369,8 +369,10 @@ bandsolve_status bandsolve_periodic_pent_cn_step_dev(
  *   (I - s Lx) u* = (I + s Ly) u,   (I - s Ly) u' = (I + s Lx) u*
  * with the Crank-Nicolson bands and stencils of the 1D driver along each
  * axis. y-solves run on the interleaved layout directly (systems = x), x-solves
- * on a transposed copy (systems = y). work: an ny x ld scratch array; the
- * call is stream-ordered. */
+ * on a transposed copy (systems = y). work: an ny x ld scratch array, used
+ * as the transposed field (pitch ny rounded up to even) when it is 16-byte
+ * aligned and large enough, else the library takes a block from its pool for
+ * the step; must not alias field. The call is stream-ordered. */
 typedef struct bandsolve_adi bandsolve_adi;
 bandsolve_status bandsolve_adi_create(int problem, double sigma_x, size_t nx,
                                       size_t ny, bandsolve_adi** out);

@@ -1811,9 +1811,12 @@ bandsolve_status adi_step_device(const Periodic& px, const Periodic& py, double 
     int device = 0;
     BSB_CUDA(cudaGetDevice(&device));
   }
-  double* t1 = nullptr;
-  BSB_CUDA(pool_malloc_async(reinterpret_cast<void**>(&t1), nx * ldt * sizeof(double), s));
-  (void)work;  // scratch kept in the ABI; the fused stencil+transpose needs only t1
+  // the transposed field lives in the caller's work array when it is large
+  // enough (ny x ld doubles >= nx x ldt, 16-byte aligned: TMA), else in a
+  // pool block for this step
+  const bool own_t1 = !(reinterpret_cast<uintptr_t>(work) % 16 == 0 && ny * ld >= nx * ldt);
+  double* t1 = own_t1 ? nullptr : work;
+  if (own_t1) BSB_CUDA(pool_malloc_async(reinterpret_cast<void**>(&t1), nx * ldt * sizeof(double), s));
   // pde.cpp:80-81 / :101-103: the coefficients are formed once on the host
   const double cs = sigma, cs4 = pent ? 4.0 * sigma : 0.0, cmid = pent ? 1.0 - 6.0 * sigma : 1.0 - 2.0 * sigma;
   auto rhs_t = [&](const double* in, double* out, std::size_t rows, std::size_t cols, std::size_t ldi,
@@ -1855,7 +1858,7 @@ bandsolve_status adi_step_device(const Periodic& px, const Periodic& py, double 
       st = periodic_device(py, field, ny, nx, ld, stream, false);
     }
   } while (false);
-  cudaFreeAsync(t1, s);
+  if (own_t1) cudaFreeAsync(t1, s);
   cudaGetLastError();
   return st;
 }
