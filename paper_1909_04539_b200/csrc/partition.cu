@@ -62,6 +62,7 @@ struct PartPlan {
   std::vector<std::pair<int, void*>> dev;  // device blobs
   // device blobs of the one-pass kernel's records, keyed 2 device + (fp32 ? 1 : 0)
   std::vector<std::pair<int, void*>> spike_dev;
+  int sp_dp = -1, sp_df = -1;  // spike decay cut-offs in chunks (spike_cutoffs), -1: not computed
   ~PartPlan() {
     auto release = [](int device, void* ptr) {
       int prev = -1;
@@ -949,6 +950,31 @@ int spike_blocks(std::size_t n, std::size_t m, std::size_t ld, const void* x, in
 
 namespace {
 
+// First block-local chunk (of kSpR rows) past which every entry of the
+// per-row vectors (arrays of n values, block length L) is below 1e-18 of the
+// vector's largest magnitude, over all blocks: from there on their FMAs
+// contribute nothing above fp64 rounding (fast mode).
+int spike_cutoff(const std::vector<double>& v, std::size_t off, int n, int L) {
+  double mx = 0.0;
+  for (int u = 0; u < n; ++u) mx = std::max(mx, std::abs(v[off + u]));
+  const double thr = 1e-18 * mx;
+  int last = -1;  // last block-local row with a non-negligible entry
+  for (int u = 0; u < n; ++u)
+    if (!(std::abs(v[off + u]) < thr)) last = std::max(last, u % L);
+  return last / dev::kSpR + 1;
+}
+void spike_cutoffs(PartPlan& p, int n) {
+  if (p.sp_dp >= 0) return;
+  const int L = n / p.K;
+  const bool off = tune_int("SPIKE_CUT", 1) == 0;  // 0: never skip (A/B)
+  p.sp_dp = off ? (1 << 30) : spike_cutoff(p.pr, 0, n, L);
+  p.sp_df = off ? (1 << 30) : spike_cutoff(p.fl, 0, n, L);
+  if (p.pent && !off) {
+    p.sp_dp = std::max(p.sp_dp, spike_cutoff(p.pr, static_cast<std::size_t>(n), n, L));
+    p.sp_df = std::max(p.sp_df, spike_cutoff(p.fl, static_cast<std::size_t>(n), n, L));
+  }
+}
+
 template <typename T>
 bandsolve_status spike_solve_t(const Factor& f, T* x, std::size_t n, std::size_t m, std::size_t ld, void* stream,
                                int sms, bool* done, const PartPeriodic* per, const SpikeCN* cn) {
@@ -976,6 +1002,7 @@ bandsolve_status spike_solve_t(const Factor& f, T* x, std::size_t n, std::size_t
     std::lock_guard<std::mutex> lock(f.mu);
     p = cached_plan(f, K);
     if (!p) return BANDSOLVE_OK;  // a block pivot broke down or grew: the sequential sweep handles it
+    spike_cutoffs(*p, static_cast<int>(n));
     const int key = device * 2 + (sizeof(S) == 8 ? 0 : 1);  // one blob per device and precision
     for (auto& d : p->spike_dev)
       if (d.first == key) blob = d.second;
@@ -1039,6 +1066,8 @@ bandsolve_status spike_solve_t(const Factor& f, T* x, std::size_t n, std::size_t
   const uint64_t bit = device < 64 ? (1ull << device) : 0;
   std::atomic<uint64_t>& attr_set = configured[ki];
   dev::SpikePer sp;
+  sp.dp = p->sp_dp;
+  sp.df = p->sp_df;
   if (per) {
     sp.z1 = per->z1;
     sp.z2 = per->z2;

@@ -102,6 +102,13 @@ struct SpikePer {
   // only), pde.cpp:73-114; x receives u_new. cn = s, 4s (pent), 1-2s / 1-6s
   const double* u = nullptr;
   double cn[3] = {0.0, 0.0, 0.0};
+  // Decay cut-offs (block-local chunks): the U^-1 rows feeding the interface
+  // dot products and the forward images of the left coupling decay away from
+  // the block top; past chunk dp / df every entry is below 1e-18 of the
+  // vector's largest, so those FMAs are skipped (fast mode only; far below
+  // its rounding; plain pentadiagonal kernels). Defaults: never skip.
+  int dp = 1 << 30;
+  int df = 1 << 30;
 };
 
 // Rows of R^-1 a CTA keeps (its blocks kb0 .. kb0+Kc-1): the bottom NH
@@ -229,6 +236,10 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
   using B = SpB<S, PENT>;
   using TP = TPieceOf<T>;
   constexpr int NQ = PENT ? 4 : 2;  // interface rows per block (top NH, bottom NH)
+  // decay cut-offs (SpikePer::dp / df): compiled into the plain pentadiagonal
+  // kernels only, where they measured faster (configs[4] 0.78 -> 0.81; the
+  // tri and Crank-Nicolson instances measured slower with the extra branch)
+  constexpr bool kCut = PENT && !CN;
   constexpr int NH = NQ / 2;
   extern __shared__ __align__(128) unsigned char smem[];
   const int R = NQ * K;
@@ -472,20 +483,33 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
         slot = 0;
         phase ^= 1u;
       }
+      if (!kCut || c < per.dp) {
 #pragma unroll
-      for (int r = 0; r < kSpR; ++r) {  // stage 2: one FMA per row on the chain
-        const F f = fc[r];
-        T v;
-        if constexpr (PENT) {
-          v = vfma(-f.b, fs1, vfma(-f.e, fs2, dv[r]));
-          a1 = vfma(p1c[r], v, a1);
-        } else {
-          v = vfma(-f.am, fs1, dv[r]);
+        for (int r = 0; r < kSpR; ++r) {  // stage 2: one FMA per row on the chain
+          const F f = fc[r];
+          T v;
+          if constexpr (PENT) {
+            v = vfma(-f.b, fs1, vfma(-f.e, fs2, dv[r]));
+            a1 = vfma(p1c[r], v, a1);
+          } else {
+            v = vfma(-f.am, fs1, dv[r]);
+          }
+          a0 = vfma(f.p0, v, a0);
+          fs2 = fs1;
+          fs1 = v;
+          buf.put(r, to_word(v));
         }
-        a0 = vfma(f.p0, v, a0);
-        fs2 = fs1;
-        fs1 = v;
-        buf.put(r, to_word(v));
+      } else {  // U^-1 rows 0/1 have decayed: no interface accumulation
+#pragma unroll
+        for (int r = 0; r < kSpR; ++r) {
+          const F f = fc[r];
+          T v;
+          if constexpr (PENT) v = vfma(-f.b, fs1, vfma(-f.e, fs2, dv[r]));
+          else v = vfma(-f.am, fs1, dv[r]);
+          fs2 = fs1;
+          fs1 = v;
+          buf.put(r, to_word(v));
+        }
       }
       buf.store(tslot(p, c));
     };
@@ -611,11 +635,16 @@ __global__ void __launch_bounds__(32 * (kSpWarps + 1), 1)
       cur.wait();
       const B* bc = bk + c * kSpR;
       T gv[kSpR];  // stage 1: left-coupling update (off the chain)
+      if (!kCut || c < per.df) {
 #pragma unroll
-      for (int r = 0; r <= kTop; ++r) {
-        const T g = from_word<T>(cur.get(r));
-        if constexpr (PENT) gv[r] = vfma(-bc[r].f1, xl2, vfma(-bc[r].f2, xl1, g));
-        else gv[r] = vfma(-bc[r].f1, xl1, g);
+        for (int r = 0; r <= kTop; ++r) {
+          const T g = from_word<T>(cur.get(r));
+          if constexpr (PENT) gv[r] = vfma(-bc[r].f1, xl2, vfma(-bc[r].f2, xl1, g));
+          else gv[r] = vfma(-bc[r].f1, xl1, g);
+        }
+      } else {  // the coupling's forward images have decayed
+#pragma unroll
+        for (int r = 0; r <= kTop; ++r) gv[r] = from_word<T>(cur.get(r));
       }
 #pragma unroll
       for (int r = kTop; r >= 0; --r) {  // stage 2: one FMA per row on the chain

@@ -20,7 +20,7 @@ const char* const kKeys[] = {
     "PLAN",       "PWARPS",         "PTAIL",       "SWG",         "STAIL",           "SKB",
     "SKR",        "SPD",            "SV",          "SRC",         "SSEG",            "TM8",
     "TMEM",       "SSTAG",          "PARTITION",   "PART_K",      "CN_UNFUSED",      "PERIODIC_UNFUSED",
-    "ADI_UNFUSED", "ADI_FUSE_PENT", "HOST_CHUNK_MIB", "L2_SETASIDE", "SPIKE", "SPIKE_K", "SPIKE_F32_MIN_N", "NO_PDL", "GLOBAL_NOREC", "PART_NOSTAGE", "PIPE", "PKB", "PIPE_MAX_N", "PIPE_L2_P", "PRT", "PIPE_CN",
+    "ADI_UNFUSED", "ADI_FUSE_PENT", "HOST_CHUNK_MIB", "L2_SETASIDE", "SPIKE", "SPIKE_K", "SPIKE_F32_MIN_N", "NO_PDL", "GLOBAL_NOREC", "PART_NOSTAGE", "SPIKE_CUT", "PIPE", "PKB", "PIPE_MAX_N", "PIPE_L2_P", "PRT", "PIPE_CN",
 };
 
 bool known(const char* key) {
