@@ -234,3 +234,34 @@ def test_spike_fp32_within_tolerance(lib, oracle, cuda_device, n):
             out = buf.cpu().numpy()
             assert np.all(np.isnan(out[:, m:]))
             assert per_system_max_rel(out[:, :m].astype(np.float64), want) <= 1e-5, (n, m, pent)
+
+
+@pytest.mark.parametrize("n", [512, 1024, 2048])
+def test_spike_decay_cutoffs(lib, oracle, cuda_device, n):
+    """Pentadiagonal decay cut-offs (sweep_spike.cuh SpikePer::dp / df):
+    strongly dominant bands (fast decay: most chunks skip the interface and
+    coupling FMAs) and weakly dominant ones (slow decay: few or none skip)
+    stay within 1e-12 of the reference, and the strongly dominant result is
+    within 1e-15 of the same kernel with the cut-offs disabled (SPIKE_CUT=0)."""
+    torch = cuda_device
+    lib.tune("SPIKE", "1")
+    rng = np.random.default_rng(7 * n)
+    m = 96
+    rhs = rng.uniform(-1, 1, (n, m))
+    strong = (np.full(n, 0.1), np.full(n, -0.2), np.full(n, 4.0), np.full(n, -0.2), np.full(n, 0.1))
+    weak = (np.full(n, 1.0), np.full(n, -4.0), np.full(n, 6.2), np.full(n, -4.0), np.full(n, 1.0))
+    for name, bands in [("strong", strong), ("weak", weak), ("hyper", bs.hyper_bands(1.0, n))]:
+        a, b, c, d, e = (np.array(v, dtype=np.float64) for v in bands)
+        a[:2] = 0; b[0] = 0; d[-1] = 0; e[-2:] = 0
+        bands = (a, b, c, d, e)
+        want = oracle.pent_solve(oracle.pent_prefactor(*bands), rhs.copy())
+        got, _ = _dev_solve(lib, torch, bs.PentFactor(lib, *bands), rhs)
+        assert per_system_max_rel(got, want) <= TOL_F64, (name, n)
+        lib.tune("SPIKE_CUT", "0")
+        try:
+            full, _ = _dev_solve(lib, torch, bs.PentFactor(lib, *bands), rhs)
+        finally:
+            lib.tune("SPIKE_CUT", None)
+        assert per_system_max_rel(full, want) <= TOL_F64, (name, n)
+        if name == "strong":
+            assert per_system_max_rel(got, full) <= 1e-15, n
